@@ -1,0 +1,149 @@
+"""Pins for oracle/fe.py: P1 FE black box (CPU only)."""
+import json
+import os
+
+import numpy as np
+import pytest
+import scipy.special
+
+from oracle import fe
+from usfft_inputs import config
+
+GOLD = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "spec_examples.json")))
+
+
+def _model(n, a_func, f_func):
+    return dict(n=n, d=0, amp=[], theta="sin", form="affine", f=f_func, a_func=a_func)
+
+
+def test_constant_coefficient_is_five_point_laplacian():
+    """a = 1 on the "/" triangulation: P1 stiffness = textbook 5-point Laplacian (no h scaling in
+    2-D), hypotenuse couplings vanish; centroid load of f = x2 is h^2 x2 at each node."""
+    n = 6
+    G = (n - 1) ** 2
+    cx, cy = fe.centroids(n)
+    ab, b = fe.assemble(n, np.ones_like(cx), cy.copy())
+    A = fe.banded_to_dense(ab)
+    ref = np.zeros((G, G))
+    for j in range(1, n):
+        for i in range(1, n):
+            p = (j - 1) * (n - 1) + (i - 1)
+            ref[p, p] = 4.0
+            for di, dj in ((1, 0), (-1, 0), (0, 1), (0, -1)):
+                ii, jj = i + di, j + dj
+                if 1 <= ii <= n - 1 and 1 <= jj <= n - 1:
+                    ref[p, (jj - 1) * (n - 1) + (ii - 1)] = -1.0
+    assert np.abs(A - ref).max() < 1e-13
+    x1, x2 = fe.node_coords(n)
+    assert np.allclose(b, x2 / n ** 2, rtol=1e-13, atol=0)
+
+
+def _order(errs, ns):
+    return [np.log(errs[k] / errs[k + 1]) / np.log(ns[k + 1] / ns[k]) for k in range(len(ns) - 1)]
+
+
+def test_manufactured_constant_coefficient_order2():
+    """a = 1, f = 2 pi^2 sin(pi x1) sin(pi x2) -> u = sin sin; order >= 1.9."""
+    ns = [8, 16, 32]
+    errs = []
+    for n in ns:
+        m = _model(n, lambda x1, x2: np.ones_like(x1),
+                   lambda x1, x2: 2 * np.pi ** 2 * np.sin(np.pi * x1) * np.sin(np.pi * x2))
+        u = fe.solve(m, np.zeros(0))
+        x1, x2 = fe.node_coords(n)
+        errs.append(np.abs(u - np.sin(np.pi * x1) * np.sin(np.pi * x2)).max())
+    assert min(_order(errs, ns)) >= 1.9
+
+
+def test_manufactured_variable_coefficient_order2():
+    """a = 1 + x1 x2 / 2, u = sin sin, f = -div(a grad u) in closed form."""
+    def a(x1, x2):
+        return 1.0 + 0.5 * x1 * x2
+
+    def f(x1, x2):
+        s1, s2 = np.sin(np.pi * x1), np.sin(np.pi * x2)
+        c1, c2 = np.cos(np.pi * x1), np.cos(np.pi * x2)
+        return a(x1, x2) * 2 * np.pi ** 2 * s1 * s2 - (0.5 * x2 * np.pi * c1 * s2 + 0.5 * x1 * np.pi * s1 * c2)
+
+    ns = [8, 16, 32]
+    errs = []
+    for n in ns:
+        u = fe.solve(_model(n, a, f), np.zeros(0))
+        x1, x2 = fe.node_coords(n)
+        errs.append(np.abs(u - np.sin(np.pi * x1) * np.sin(np.pi * x2)).max())
+    assert min(_order(errs, ns)) >= 1.9
+
+
+@pytest.mark.parametrize("cfg", [1, 2, 4])
+def test_spd_m_matrix_and_residual(cfg):
+    """Cholesky succeeds (SPD); f = x2 >= 0 gives u >= 0 (M-matrix); residual at round-off."""
+    m = config(cfg)
+    rng = np.random.default_rng(cfg)
+    for _ in range(3):
+        u, rr = fe.solve(m, rng.random(m["d"]), return_residual=True)
+        assert np.all(u >= 0.0) and rr < 1e-11
+
+
+def test_coefficient_maps():
+    m = config(1)
+    x1, x2 = np.random.default_rng(0).random((2, 50))
+    assert np.allclose(fe.coefficient(m, np.zeros(4), x1, x2), 1.0, atol=0)
+    ml = config(4)
+    y = np.full(20, 0.5)                                                        # Phi^-1(1/2) = 0
+    assert np.allclose(fe.coefficient(ml, y, x1, x2), 1.0, atol=0)
+    assert fe.theta_map("probit", np.array([0.0]))[0] == -6.0                   # clip (Z15)
+    assert abs(fe.theta_map("probit", np.array([0.975]))[0] - 1.959963984540054) < 1e-12
+    # tent: phi(0) = alpha = -1, phi(1/2) = beta = 1 (A2); symmetric (A3)
+    assert fe.theta_map("tent", np.array([0.0, 0.5, 0.25]))[0:3].tolist() == [-1.0, 1.0, 0.0]
+    t = np.linspace(0, 0.5, 11)
+    assert np.allclose(fe.theta_map("tent", 0.5 - t), fe.theta_map("tent", 0.5 + t))
+
+
+@pytest.mark.parametrize("ex", GOLD["ellipticity"])
+def test_paper_ellipticity_bounds(ex):
+    """Periodic model of Sec. 4.2: a_min/max = 1 -/+ (c/sqrt6) zeta(mu); the
+    oracle's coefficient stays inside the d-term bounds for random (x, y)."""
+    z = scipy.special.zeta(ex["mu"])
+    assert abs(1 - ex["c"] / np.sqrt(6) * z - ex["a_min"]) <= ex["tol"]
+    assert abs(1 + ex["c"] / np.sqrt(6) * z - ex["a_max"]) <= ex["tol"]
+    d = 10
+    amp = [ex["c"] / np.sqrt(6) * j ** -ex["mu"] for j in range(1, d + 1)]
+    m = dict(n=8, d=d, amp=amp, theta="sin", form="affine", f="x2")
+    rng = np.random.default_rng(1)
+    for _ in range(50):
+        a = fe.coefficient(m, rng.random(d), *rng.random((2, 200)))
+        assert a.min() >= 1 - sum(amp) - 1e-15 and a.max() <= 1 + sum(amp) + 1e-15
+
+
+def test_stencil_derivation_matches_element_assembly():
+    """Z11: the element-assembled matrix for arbitrary centroid values equals the 5-point stencil
+    w_h(i,j) = (a(T_lo(i,j)) + a(T_up(i,j-1)))/2, w_v(i,j) = (a(T_up(i,j)) + a(T_lo(i-1,j)))/2.
+    This checks the derivation the GPU path uses against textbook assembly."""
+    n = 7
+    G = (n - 1) ** 2
+    rng = np.random.default_rng(3)
+    a_T = rng.uniform(0.5, 2.0, size=2 * n * n)
+    A = fe.banded_to_dense(fe.assemble(n, a_T, np.zeros_like(a_T))[0])
+
+    def lo(ci, cj):
+        return a_T[2 * (cj * n + ci)]
+
+    def up(ci, cj):
+        return a_T[2 * (cj * n + ci) + 1]
+
+    def idx(i, j):
+        return (j - 1) * (n - 1) + (i - 1) if 1 <= i <= n - 1 and 1 <= j <= n - 1 else -1
+
+    R = np.zeros((G, G))
+    for j in range(1, n):
+        for i in range(1, n):
+            p = idx(i, j)
+            wE = (lo(i, j) + up(i, j - 1)) / 2
+            wW = (lo(i - 1, j) + up(i - 1, j - 1)) / 2
+            wN = (up(i, j) + lo(i - 1, j)) / 2
+            wS = (up(i, j - 1) + lo(i - 1, j - 1)) / 2
+            R[p, p] = wE + wW + wN + wS
+            for q, w in ((idx(i + 1, j), wE), (idx(i - 1, j), wW), (idx(i, j + 1), wN), (idx(i, j - 1), wS)):
+                if q >= 0:
+                    R[p, q] = -w
+    assert np.abs(A - R).max() < 1e-13
