@@ -1,0 +1,232 @@
+/*
+ * usfft.h — C-ABI of the B200-native usFFT detection step (arXiv 2109.04131).
+ *
+ * The operations are the steps of one dimension-incremental detection round of Alg. 1
+ * "The usFFT on a set T_G".  Citations: P:n = PAPER.md line n (LaTeX
+ * source) with its section/equation/algorithm; S:n = SPEC.md line n; Zn = a reading of a place
+ * where the paper is silent, listed in DESIGN.md §3.
+ *
+ * Conventions (all calls)
+ *  - Every function returns usfft_status.  USFFT_OK = 0.  On USFFT_EINVAL nothing was launched or
+ *    written.  CUDA errors are sticky (the ctx must be finalized); USFFT_ENOCONV and
+ *    USFFT_ENOTRECON are not sticky and the outputs are written.  usfft_last_error() returns a
+ *    message owned by the ctx (valid until the next call on it).
+ *  - "dev" pointers are device memory owned by the caller (e.g. torch tensors); the library
+ *    borrows them for stream-ordered use on the ctx stream, so the caller keeps them alive until
+ *    that stream has passed the call.  "host" pointers are read during the call only (they are
+ *    staged into ctx-owned device memory before the call returns).  Workspace (tables, per-CTA
+ *    scratch) is owned by the ctx and grows on demand.
+ *  - Calls are asynchronous on the ctx stream unless marked "syncs" (a host output needs it).
+ *  - One ctx per (GPU, stream); not thread-safe.  Multi-GPU: every rank has its own ctx and the
+ *    caller performs the exchange steps between calls; the calls take the
+ *    node/sample ranges that rank owns.
+ *  - Layouts: sample index fastest.  Samples of a round are b = l*M + i (lattice l, node i).
+ *    Candidates of a round are j = a*n1 + c for rows a of I_prev and entries c of kt (Z10).
+ */
+#ifndef USFFT_H
+#define USFFT_H
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef int32_t usfft_status;
+enum {
+    USFFT_OK = 0,
+    USFFT_EINVAL = 1,     /* bad argument; nothing launched                                  */
+    USFFT_ENOMEM = 2,     /* workspace allocation failed                                      */
+    USFFT_ECUDA = 3,      /* CUDA error (sticky)                                              */
+    USFFT_ENCCL = 4,      /* reserved for an in-library collective                            */
+    USFFT_ENOCONV = 5,    /* some PCG sample missed tol at maxit (outputs still written)      */
+    USFFT_ENOTRECON = 6,  /* injectivity test failed (mode-R caller decides what to do)       */
+    USFFT_EUNIMPL = 7     /* option not implemented                                           */
+};
+
+typedef struct usfft_ctx usfft_ctx;
+
+/* Rank-1 lattice sampling set of one round (R1L P:230-233; eq. lattice_nodes P:837-839;
+ * Alg. 1 Step 2b P:309-311; Step 1 line nodes P:288-293).
+ *   d          parameter dimension d_y
+ *   t          components of z (Step 2: the round's dimension t; Step 1: 1)
+ *   line_axis  -1 for Step 2 (components 0..t-1 from the lattice, t..d-1 = shift);
+ *              a >= 0 for Step 1 (component a = ((i*z) mod M)/M with t = 1, all others = shift)
+ *   L, M       number of lattices and lattice size (M >= 2; prime for Step 2, Z2)
+ *   z          host int64 [L][t], entries in [0, M)
+ *   shift      host fp64 [d], the random components x' of the round, in [0,1)
+ */
+typedef struct {
+    int32_t d;
+    int32_t t;
+    int32_t line_axis;
+    int32_t L;
+    int64_t M;
+    const int64_t *z;
+    const double *shift;
+} usfft_lattice_desc;
+
+/* PDE black box (eq. pde, weak form P:155-158; coefficient families P:84-98; BASELINE
+ * configs; P1 FE on the uniform "/" triangulation with centroid quadrature, Z11/Z12).
+ *   n          cells per side, G = (n-1)^2 interior nodes (x1 fastest), 2 <= n <= 128
+ *   d          number of coefficient terms (<= 64)
+ *   theta      0: sin(2 pi y) (periodic)  1: tent 1-|2(1-2y)| (eq. tent)
+ *              2: clip(Phi^-1(y), -6, 6) (Z15)
+ *   form       0: a = 1 + sum_j amp_j theta_j sin(j pi x1) sin(j pi x2)   1: a = exp(sum ...)
+ *   f_kind     0: f(x) = x2 (all BASELINE configs)
+ *   amp        host fp64 [d]
+ *   tol        relative residual target ||r_k||_2 <= tol ||b||_2 (Z13; BASELINE 1e-12)
+ *   maxit      PCG iteration cap
+ */
+typedef struct {
+    int32_t n;
+    int32_t d;
+    int32_t theta;
+    int32_t form;
+    int32_t f_kind;
+    int32_t maxit;
+    const double *amp;
+    double tol;
+} usfft_pde_desc;
+
+/* Round plan input/output (usfft_plan_round). */
+typedef struct {
+    int64_t seed;
+    int32_t step;     /* 1: Step 1 & 2a line round; 2: Step 2 round   */
+    int32_t t;        /* dimension-increment index t, 1-based                                */
+    int32_t i;        /* detection round i, 1-based                                           */
+    int32_t d;        /* parameter dimension d_y                                              */
+    int32_t N;        /* search box Gamma = [-N, N]^d, K_t = 2N+1                     */
+    int32_t s_tilde;  /* sparsity of the round                                        */
+    int32_t mode;     /* Algorithm A: 0 = L random R1Ls (Z1), 1 = single reconstructing */
+    int32_t pad_;
+    int64_t nJ;       /* |J_t| (Step 2) or K_t (Step 1)                                        */
+} usfft_plan_in;
+
+typedef struct {
+    int64_t M;           /* lattice size                                                      */
+    int32_t L;           /* number of lattices                                                */
+    int32_t t_z;         /* components of each z (desc.t)                                     */
+    int32_t line_axis;   /* desc.line_axis                                                    */
+    int32_t pad_;
+    int64_t z[2048];     /* [L][t_z]                                                          */
+    double shift[64];    /* x'_1..x'_d                                                        */
+} usfft_plan_out;
+
+/* ---- context ------------------------------------------------------------------------------ */
+
+/* Create a ctx on `device` launching on `stream` (a cudaStream_t; NULL = legacy default). */
+usfft_status usfft_init(usfft_ctx **out, int device, void *stream);
+usfft_status usfft_set_stream(usfft_ctx *ctx, void *stream);
+usfft_status usfft_finalize(usfft_ctx *ctx);
+const char *usfft_last_error(const usfft_ctx *ctx);
+/* Number of kernels this ctx has launched since init (evidence counter for benchmarks). */
+int64_t usfft_launch_count(const usfft_ctx *ctx);
+
+/* ---- a1: round plan (usfft_plan_round) ----------------------------------------------------
+ * The random choices of round (t, i) of Alg. 1: the shift x' (P:287 / P:307, one per round and
+ * shared by every lattice and node chi_g) and the sampling set (Step 1: the line
+ * lattice z = 1, M = K_t; Step 2 mode A: M, L and z_l by readings Z2-Z4; mode R: the first
+ * reconstructing z found by the search of Z2 on the device-resident J_t = I_prev x kt, syncs).
+ * I_prev / kt are only read in mode R (dev int16, layouts as in usfft_lattice). */
+usfft_status usfft_plan_round(usfft_ctx *ctx, const usfft_plan_in *in, const int16_t *I_prev,
+                              int64_t n_prev, const int16_t *kt, int32_t n1, usfft_plan_out *out);
+
+/* ---- a2 + a3: lattice nodes and candidate index maps (usfft_lattice) -----------------------
+ * nodes    dev fp64 [d][nb] (may be NULL): component j of sample b0+bl, bl < nb, per the desc.
+ *          Bit-exact: ((i*z) mod M) is an exact int64 and is divided by M once (IEEE).
+ * I_prev   dev int16 [n_prev][t-1] rows of I^(1..t-1) (ignored when t == 1; pass n_prev = 1)
+ * kt       dev int16 [n1], the candidate t-th components (I^(t) in Step 2; -N..N in Step 1)
+ * bins     dev int32 [L][n_prev*n1] (may be NULL): b_l(k) = (k . z_l) mod M in [0, M)
+ *          (S:119-127).  Requires |k_c| * z * t < 2^62.
+ * injective host int32 [L] (may be NULL; syncs): 1 if k -> b_l(k) is one-to-one on J_t
+ *          (reconstructing single R1L, Table 1 row 1 P:242), else 0.  When any
+ *          entry is 0 the call returns USFFT_ENOTRECON. */
+usfft_status usfft_lattice(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_t b0, int64_t nb,
+                           double *nodes, const int16_t *I_prev, int64_t n_prev,
+                           const int16_t *kt, int32_t n1, int32_t *bins, int32_t *injective);
+
+/* ---- a4 + a5: sample the black box (usfft_sample_pde) -------------------------------------
+ * One FE solve per node y_b, b = b0 .. b0+nb-1 (Alg. 1 Step 2c "Sample p ... for every chi_g",
+ * P:313; one solve serves all G nodes).  The nodes are generated in-kernel from `lat`
+ * (bit-identical to usfft_lattice) unless `nodes` (dev fp64 [d][nb]) is given.
+ * Jacobi PCG from x0 = 0, stop on the recursive ||r||_2 <= tol ||b||_2 (Z13).
+ * u        dev fp64 [G][ldu]: u[g*ldu + bl] = u(x_g, y_{b0+bl}), ldu >= nb
+ * iters    dev int32 [nb] (may be NULL): PCG iterations per sample
+ * relres   dev fp64 [nb] (may be NULL): final recursive ||r||/||b||
+ * n_noconv host int32 (may be NULL; syncs): samples that missed tol; > 0 -> USFFT_ENOCONV */
+usfft_status usfft_sample_pde(usfft_ctx *ctx, const usfft_pde_desc *pde,
+                              const usfft_lattice_desc *lat, int64_t b0, int64_t nb,
+                              const double *nodes, double *u, int64_t ldu, int32_t *iters,
+                              double *relres, int32_t *n_noconv);
+
+/* ---- a7 + a8: lattice FFT and detection key (usfft_lattice_fft) ----------------------------
+ * For each owned node g < G_loc and lattice l: the length-M DFT of the samples of lattice l
+ * (Alg. 1 P:296 "via FFT"), then for each candidate j the per-lattice value
+ *   v_l(j,g) = (1/M) F[g][l][b] (conj(F[g][l][M-b]) for b > M/2, real input, Z17/Z18)
+ * and the key kappa_min(j,g) = min_l fl(fl(re*re) + fl(im*im)) (Z1, Z5).
+ * u        dev fp64 sample slabs after the exchange: nslab slabs back to back, slab p holds
+ *          [G_loc][slab_b0[p+1]-slab_b0[p]] and starts at u + G_loc*slab_b0[p]
+ *          (nslab = 1, slab_b0 = {0, L*M}: plain [G_loc][L*M])
+ * slab_b0  host int64 [nslab+1], 0 = slab_b0[0] < ... < slab_b0[nslab] = L*M
+ * spectra  dev fp64x2 [G_loc][L][M/2+1] (unscaled DFT bins 0..M/2)
+ * kappa_min dev fp64 [G_loc][nJ];  kappa_max dev fp64 [1]: max over owned g and all j */
+usfft_status usfft_lattice_fft(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_t G_loc,
+                               const double *u, int32_t nslab, const int64_t *slab_b0,
+                               const int32_t *bins, int64_t nJ, double *spectra,
+                               double *kappa_min, double *kappa_max);
+
+/* ---- a9 + a10: threshold and per-node selection (usfft_detect_select) ----------------------
+ * theta^2 = fl(theta_abs^2) if theta_abs > 0, else fl(fl(theta_rel^2) * kappa_max[0]) (Z5;
+ * kappa_max must be the max over ALL nodes, i.e. all-reduced when nranks > 1).
+ * For each owned g: D_g = the first s_tilde candidates in the order (kappa desc, j asc) (Z6)
+ * that satisfy kappa >= theta^2 and kappa > 0 (Alg. 1, Step 2d P:316).
+ * votes    dev int32 [nJ]: zeroed, then votes[j] = #{owned g : j in D_g} (Z24)
+ * det_g    dev int32 [G_loc][s_tilde]: D_g ascending, -1 padded;  n_det_g dev int32 [G_loc]
+ * theta2   dev fp64 [1] (may be NULL): the theta^2 used */
+usfft_status usfft_detect_select(usfft_ctx *ctx, int64_t G_loc, int64_t nJ,
+                                 const double *kappa_min, const double *kappa_max,
+                                 int32_t s_tilde, double theta_rel, double theta_abs,
+                                 int32_t *votes, int32_t *det_g, int32_t *n_det_g,
+                                 double *theta2);
+
+/* ---- a11: union (usfft_detect_union) ------------------------------------------------------
+ * votes must be summed over all ranks (Step 2e P:318: union over g).  flags |= (votes > 0)
+ * (running union over the rounds i of one t).  Outputs, identical on every rank:
+ * det_idx  dev int32 [nJ]: this round's detected j ascending; n_det host int64 (syncs)
+ * union_idx dev int32 [nJ] (may be NULL): all j with flags set, ascending; n_union host int64 */
+usfft_status usfft_detect_union(usfft_ctx *ctx, int64_t nJ, const int32_t *votes,
+                                uint8_t *flags, int32_t *det_idx, int64_t *n_det,
+                                int32_t *union_idx, int64_t *n_union);
+
+/* ---- a12: coefficient resolve (usfft_resolve) ---------------------------------------------
+ * For each owned g and each k = det_idx[q], q < n_det (Step 2d "computes the Fourier
+ * coefficients" P:277/P:316, reading Z1):
+ *   l*(k,g) = min{ l : no k' in D_g \ {k} has b_l(k') = b_l(k) };  coef = v_{l*}(k,g);
+ *   no such l: componentwise lower median over l of v_l(k,g), lstar = -1.
+ * coef dev fp64x2 [G_loc][n_det];  lstar dev int32 [G_loc][n_det] (may be NULL) */
+usfft_status usfft_resolve(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_t G_loc,
+                           const double *spectra, const int32_t *bins, int64_t nJ,
+                           const int32_t *det_g, const int32_t *n_det_g, int32_t s_tilde,
+                           const int32_t *det_idx, int64_t n_det, double *coef,
+                           int32_t *lstar);
+
+/* ---- candidate rows (usfft_gather_rows) ----------------------------------------------------
+ * rows[q] = (I_prev[a], kt[c]) for j = idx[q] = a*n1 + c, q < n: the frequency vectors of
+ * I^(1..t) handed to the next dimension.  rows dev int16 [n][t]. */
+usfft_status usfft_gather_rows(usfft_ctx *ctx, const int32_t *idx, int64_t n,
+                               const int16_t *I_prev, int32_t t, const int16_t *kt, int32_t n1,
+                               int16_t *rows);
+
+/* ---- evaluation (usfft_eval) --------------------------------------------------------------
+ * U[g][q] = Re sum_{k in I} C[g][k] e^{2 pi i k . y_q} (eq. eval_formula, identity
+ * periodization of the periodic model P:945-949).
+ * I dev int16 [nI][d]; C dev fp64x2 [G][nI]; Y dev fp64 [d][n]; U dev fp64 [G][n] */
+usfft_status usfft_eval(usfft_ctx *ctx, int32_t d, const int16_t *I, int64_t nI,
+                        const double *C, int64_t G, const double *Y, int64_t n, double *U);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* USFFT_H */

@@ -1,0 +1,205 @@
+"""Thin Python binding of the C-ABI (include/usfft.h): same names, argument marshalling only.
+
+Device arrays are torch CUDA tensors (contiguous, the dtype the header names); host arrays are
+numpy.  Every compute step runs in libusfft.so; nothing here touches the method's arithmetic.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from dataclasses import dataclass
+
+import numpy as np
+import torch
+
+from . import _native as N
+
+
+class UsfftError(RuntimeError):
+    def __init__(self, status: int, where: str, msg: str):
+        super().__init__(f"{where}: {N.STATUS_NAMES.get(status, status)}: {msg}")
+        self.status = status
+
+
+def _check(ctx: "Context", status: int, where: str, allow=()):
+    if status != N.OK and status not in allow:
+        raise UsfftError(status, where, ctx.last_error())
+    return status
+
+
+def _p(t, dtype=None):
+    """data_ptr of a contiguous CUDA tensor (or None)."""
+    if t is None:
+        return None
+    if not isinstance(t, torch.Tensor) or not t.is_cuda:
+        raise TypeError("device arguments must be CUDA tensors")
+    if not t.is_contiguous():
+        raise ValueError("device arguments must be contiguous")
+    if dtype is not None and t.dtype != dtype:
+        raise TypeError(f"expected {dtype}, got {t.dtype}")
+    return t.data_ptr()
+
+
+class Context:
+    """usfft_ctx on one device, launching on a torch stream (default: the current stream)."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+        self.lib = N.load()
+        if not torch.cuda.is_available():
+            raise RuntimeError("usFFT needs a CUDA device; there is no CPU path")
+        self.device = device
+        self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        h = C.c_void_p()
+        st = self.lib.usfft_init(C.byref(h), device, C.c_void_p(self.stream.cuda_stream))
+        if st != N.OK:
+            raise UsfftError(st, "usfft_init", "device/context creation failed")
+        self.h = h
+
+    def last_error(self) -> str:
+        m = self.lib.usfft_last_error(self.h)
+        return m.decode() if m else ""
+
+    def launches(self) -> int:
+        return int(self.lib.usfft_launch_count(self.h))
+
+    def set_stream(self, stream: torch.cuda.Stream):
+        self.stream = stream
+        _check(self, self.lib.usfft_set_stream(self.h, C.c_void_p(stream.cuda_stream)), "usfft_set_stream")
+
+    def close(self):
+        if getattr(self, "h", None):
+            self.lib.usfft_finalize(self.h)
+            self.h = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class Plan:
+    """A round plan (usfft_plan_out) plus the parameter dimension."""
+    d: int
+    M: int
+    L: int
+    t_z: int
+    line_axis: int
+    z: np.ndarray        # int64 [L][t_z]
+    shift: np.ndarray    # float64 [d]
+
+    def desc(self):
+        z = np.ascontiguousarray(self.z, dtype=np.int64)
+        s = np.ascontiguousarray(self.shift, dtype=np.float64)
+        dsc = N.LatticeDesc(self.d, self.t_z, self.line_axis, self.L, self.M,
+                            z.ctypes.data_as(C.POINTER(C.c_int64)),
+                            s.ctypes.data_as(C.POINTER(C.c_double)))
+        return dsc, (z, s)                              # keep the arrays alive
+
+
+def usfft_plan_round(ctx: Context, seed: int, step: int, t: int, i: int, d: int, N_: int,
+                     s_tilde: int, mode: str, nJ: int, I_prev=None, n_prev: int = 1,
+                     kt=None) -> Plan:
+    pin = N.PlanIn(seed, step, t, i, d, N_, s_tilde, 1 if mode == "R" else 0, 0, nJ)
+    out = N.PlanOut()
+    n1 = 0 if kt is None else int(kt.numel())
+    _check(ctx, ctx.lib.usfft_plan_round(ctx.h, C.byref(pin), _p(I_prev, torch.int16), n_prev,
+                                         _p(kt, torch.int16), n1, C.byref(out)), "usfft_plan_round")
+    z = np.ctypeslib.as_array(out.z)[: out.L * out.t_z].reshape(out.L, out.t_z).copy()
+    shift = np.ctypeslib.as_array(out.shift)[:d].copy()
+    return Plan(d, int(out.M), int(out.L), int(out.t_z), int(out.line_axis), z, shift)
+
+
+def usfft_lattice(ctx: Context, plan: Plan, b0: int, nb: int, nodes=None, I_prev=None,
+                  n_prev: int = 1, kt=None, bins=None, injective: bool = False):
+    """a2 + a3.  Returns the per-lattice injectivity list when injective=True (syncs)."""
+    dsc, keep = plan.desc()
+    n1 = 0 if kt is None else int(kt.numel())
+    inj = (C.c_int32 * plan.L)() if injective else None
+    st = ctx.lib.usfft_lattice(ctx.h, C.byref(dsc), b0, nb, _p(nodes, torch.float64),
+                               _p(I_prev, torch.int16), n_prev, _p(kt, torch.int16), n1,
+                               _p(bins, torch.int32), inj)
+    _check(ctx, st, "usfft_lattice", allow=(N.ENOTRECON,))
+    return [int(v) for v in inj] if injective else None
+
+
+def pde_desc(cfg: dict, maxit: int = 20000, tol: float = 1e-12):
+    amp = np.ascontiguousarray(cfg["amp"][: cfg["d"]], dtype=np.float64)
+    theta = {"sin": 0, "tent": 1, "probit": 2}[cfg["theta"]]
+    form = {"affine": 0, "exp": 1}[cfg["form"]]
+    f_kind = {"x2": 0}[cfg.get("f", "x2")]
+    dsc = N.PdeDesc(cfg["n"], cfg["d"], theta, form, f_kind, maxit,
+                    amp.ctypes.data_as(C.POINTER(C.c_double)), tol)
+    return dsc, amp
+
+
+def usfft_sample_pde(ctx: Context, pde, plan: Plan, b0: int, nb: int, u, ldu: int | None = None,
+                     nodes=None, iters=None, relres=None, check_conv: bool = False) -> int:
+    """a4 + a5.  Returns the number of non-converged samples if check_conv (syncs), else -1."""
+    dsc, keep = plan.desc()
+    pdsc, amp = pde
+    ldu = nb if ldu is None else ldu
+    nc = C.c_int32(0)
+    st = ctx.lib.usfft_sample_pde(ctx.h, C.byref(pdsc), C.byref(dsc), b0, nb,
+                                  _p(nodes, torch.float64), _p(u, torch.float64), ldu,
+                                  _p(iters, torch.int32), _p(relres, torch.float64),
+                                  C.byref(nc) if check_conv else None)
+    _check(ctx, st, "usfft_sample_pde", allow=(N.ENOCONV,))
+    return int(nc.value) if check_conv else -1
+
+
+def usfft_lattice_fft(ctx: Context, plan: Plan, G_loc: int, u, slab_b0, bins, nJ: int, spectra,
+                      kappa_min, kappa_max):
+    """a7 + a8 on the exchanged sample slabs (slab_b0: host int sample offsets)."""
+    dsc, keep = plan.desc()
+    sb = np.ascontiguousarray(slab_b0, dtype=np.int64)
+    st = ctx.lib.usfft_lattice_fft(ctx.h, C.byref(dsc), G_loc, _p(u, torch.float64),
+                                   len(sb) - 1, sb.ctypes.data_as(C.POINTER(C.c_int64)),
+                                   _p(bins, torch.int32), nJ, _p(spectra, torch.float64),
+                                   _p(kappa_min, torch.float64), _p(kappa_max, torch.float64))
+    _check(ctx, st, "usfft_lattice_fft")
+
+
+def usfft_detect_select(ctx: Context, G_loc: int, nJ: int, kappa_min, kappa_max, s_tilde: int,
+                        theta_rel: float, theta_abs: float, votes, det_g, n_det_g, theta2=None):
+    st = ctx.lib.usfft_detect_select(ctx.h, G_loc, nJ, _p(kappa_min, torch.float64),
+                                     _p(kappa_max, torch.float64), s_tilde, theta_rel, theta_abs,
+                                     _p(votes, torch.int32), _p(det_g, torch.int32),
+                                     _p(n_det_g, torch.int32), _p(theta2, torch.float64))
+    _check(ctx, st, "usfft_detect_select")
+
+
+def usfft_detect_union(ctx: Context, nJ: int, votes, flags, det_idx, union_idx=None):
+    """a11; returns (n_det, n_union) (syncs)."""
+    nd, nu = C.c_int64(0), C.c_int64(0)
+    st = ctx.lib.usfft_detect_union(ctx.h, nJ, _p(votes, torch.int32), _p(flags, torch.uint8),
+                                    _p(det_idx, torch.int32), C.byref(nd),
+                                    _p(union_idx, torch.int32), C.byref(nu))
+    _check(ctx, st, "usfft_detect_union")
+    return int(nd.value), int(nu.value)
+
+
+def usfft_resolve(ctx: Context, plan: Plan, G_loc: int, spectra, bins, nJ: int, det_g, n_det_g,
+                  s_tilde: int, det_idx, n_det: int, coef, lstar=None):
+    dsc, keep = plan.desc()
+    st = ctx.lib.usfft_resolve(ctx.h, C.byref(dsc), G_loc, _p(spectra, torch.float64),
+                               _p(bins, torch.int32), nJ, _p(det_g, torch.int32),
+                               _p(n_det_g, torch.int32), s_tilde, _p(det_idx, torch.int32), n_det,
+                               _p(coef, torch.float64), _p(lstar, torch.int32))
+    _check(ctx, st, "usfft_resolve")
+
+
+def usfft_gather_rows(ctx: Context, idx, n: int, I_prev, t: int, kt, rows):
+    st = ctx.lib.usfft_gather_rows(ctx.h, _p(idx, torch.int32), n, _p(I_prev, torch.int16), t,
+                                   _p(kt, torch.int16), int(kt.numel()), _p(rows, torch.int16))
+    _check(ctx, st, "usfft_gather_rows")
+
+
+def usfft_eval(ctx: Context, I, C_, Y, U):
+    """U[g][q] = Re sum_k C[g][k] e^{2 pi i k.y_q}; I int16 [nI][d], C fp64 [G][nI][2], Y [d][n]."""
+    nI, d = I.shape
+    G = C_.shape[0]
+    n = Y.shape[1]
+    st = ctx.lib.usfft_eval(ctx.h, d, _p(I, torch.int16), nI, _p(C_, torch.float64), G,
+                            _p(Y, torch.float64), n, _p(U, torch.float64))
+    _check(ctx, st, "usfft_eval")

@@ -1,0 +1,181 @@
+// common.cuh — ctx, error plumbing and deterministic block reductions shared by the usFFT
+// kernels (sm_100a).  Nothing here is shared with oracle/ (see DESIGN.md §1).
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdarg>
+#include <cstdio>
+#include <map>
+#include <string>
+#include <utility>
+
+#include "../../include/usfft.h"
+
+struct usfft_ctx {
+    int device = 0;
+    cudaStream_t stream = nullptr;
+    int sm_count = 148;
+    size_t smem_optin = 0;
+    bool sticky = false;
+    std::string err;
+    int64_t launches = 0;
+    // general device workspace — grows on demand
+    void *ws = nullptr;
+    size_t ws_size = 0;
+    // small device scalar area (counters, maxima): 4 KB allocated at init
+    void *dscal = nullptr;
+    // cached tables
+    std::map<int64_t, double2 *> twiddles;                  // M -> e^{-2 pi i m/M}, m < M
+    std::map<std::pair<int, int>, double *> sintab;          // (n, d) -> sin(j pi m/(3n))
+};
+
+namespace usfft {
+
+// Small host arrays travel as kernel parameters (<= 32 KB parameter space on sm_70+, CUDA 12.1+),
+// so no call needs a host sync to stage them.
+constexpr int kMaxZ = 2048;      // L * t entries of z
+constexpr int kMaxD = 64;        // parameter dimension d
+constexpr int kMaxSlab = 64;     // exchange slabs (ranks)
+
+struct LatParams {
+    int32_t d, t, line_axis, L;
+    int64_t M;
+    int64_t z[kMaxZ];
+    double shift[kMaxD];
+};
+
+
+inline usfft_status fail(usfft_ctx *c, usfft_status s, const char *fmt, ...) {
+    char buf[512];
+    va_list ap;
+    va_start(ap, fmt);
+    vsnprintf(buf, sizeof buf, fmt, ap);
+    va_end(ap);
+    c->err = buf;
+    if (s == USFFT_ECUDA) c->sticky = true;
+    return s;
+}
+
+#define USFFT_CUDA(c, expr)                                                                   \
+    do {                                                                                      \
+        cudaError_t e_ = (expr);                                                              \
+        if (e_ != cudaSuccess)                                                                \
+            return usfft::fail((c), USFFT_ECUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,   \
+                               cudaGetErrorString(e_));                                       \
+    } while (0)
+
+#define USFFT_CHECK_LAUNCH(c)                                                                 \
+    do {                                                                                      \
+        (c)->launches++;                                                                      \
+        cudaError_t e_ = cudaGetLastError();                                                  \
+        if (e_ != cudaSuccess)                                                                \
+            return usfft::fail((c), USFFT_ECUDA, "%s:%d launch: %s", __FILE__, __LINE__,      \
+                               cudaGetErrorString(e_));                                       \
+    } while (0)
+
+#define USFFT_REQUIRE(c, cond, ...)                                                           \
+    do {                                                                                      \
+        if (!(cond)) return usfft::fail((c), USFFT_EINVAL, __VA_ARGS__);                      \
+    } while (0)
+
+#define USFFT_ENTER(c)                                                                        \
+    do {                                                                                      \
+        if (!(c)) return USFFT_EINVAL;                                                        \
+        if ((c)->sticky) return USFFT_ECUDA;                                                  \
+        (c)->err.clear();                                                                     \
+    } while (0)
+
+// Grow-only device buffers.  Growth synchronises the stream first (buffers may be in use).
+inline usfft_status ensure(usfft_ctx *c, void **buf, size_t *size, size_t need) {
+    if (need <= *size) return USFFT_OK;
+    size_t want = need + need / 4 + 4096;
+    if (*buf) {
+        USFFT_CUDA(c, cudaStreamSynchronize(c->stream));
+        USFFT_CUDA(c, cudaFree(*buf));
+        *buf = nullptr;
+        *size = 0;
+    }
+    if (cudaMalloc(buf, want) != cudaSuccess) {
+        cudaGetLastError();
+        return fail(c, USFFT_ENOMEM, "cudaMalloc(%zu) failed", want);
+    }
+    *size = want;
+    return USFFT_OK;
+}
+
+inline unsigned grid1d(int64_t n, int block) {
+    int64_t g = (n + block - 1) / block;
+    if (g < 1) g = 1;
+    if (g > 0x7fffffff) g = 0x7fffffff;
+    return static_cast<unsigned>(g);
+}
+
+}  // namespace usfft
+
+// ---------------------------------------------------------------------------------------------
+// Deterministic block reductions: each thread contributes one partial; the tree is fixed
+// (xor-butterfly inside each warp, then warp partials summed in warp order), so the result
+// depends only on blockDim and the partials, never on scheduling.
+// ---------------------------------------------------------------------------------------------
+template <int NV>
+__device__ __forceinline__ void block_sum(double (&v)[NV], double *scratch /* [32*NV] */) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) v[k] += __shfl_xor_sync(0xffffffffu, v[k], o);
+    }
+    if (lane == 0) {
+#pragma unroll
+        for (int k = 0; k < NV; ++k) scratch[k * 32 + warp] = v[k];
+    }
+    __syncthreads();
+#pragma unroll
+    for (int k = 0; k < NV; ++k) {
+        double s = 0.0;
+        for (int w = 0; w < nwarp; ++w) s += scratch[k * 32 + w];
+        v[k] = s;
+    }
+    __syncthreads();
+}
+
+// v_l = F[b]/M of a real-input spectrum stored for bins 0..M/2 (mirror bins conjugated, Z17/Z18)
+__device__ __forceinline__ double2 spec_value(const double2 *__restrict__ row, int64_t M, int64_t b) {
+    const int64_t Mh = M / 2 + 1;
+    const double Md = (double)M;
+    if (b < Mh) {
+        const double2 v = row[b];
+        return make_double2(v.x / Md, v.y / Md);
+    }
+    const double2 v = row[M - b];
+    return make_double2(v.x / Md, -v.y / Md);
+}
+
+// Exclusive block scan of one int per thread (fixed order); *total receives the block sum.
+__device__ __forceinline__ int block_exscan(int v, int *sh /* [33] */, int *total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5, nwarp = blockDim.x >> 5;
+    int x = v;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        int y = __shfl_up_sync(0xffffffffu, x, o);
+        if (lane >= o) x += y;
+    }
+    if (lane == 31) sh[warp] = x;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        int run = 0;
+        for (int w = 0; w < nwarp; ++w) {
+            int t = sh[w];
+            sh[w] = run;
+            run += t;
+        }
+        sh[32] = run;
+    }
+    __syncthreads();
+    const int ex = sh[warp] + x - v;
+    *total = sh[32];
+    __syncthreads();
+    return ex;
+}

@@ -1,0 +1,264 @@
+// detect.cu — K8 threshold + per-node top-s~ selection + votes, K10 union/compaction, K7b resolve.
+// usfft_detect_select / usfft_detect_union / usfft_resolve (include/usfft.h; a9-a12 of SURVEY §8(a)).
+//
+// Selection is a radix select on the 64-bit patterns of the keys (non-negative doubles order like
+// uint64): 8 passes of 8 bits find the s~-th largest key T; then one ordered pass keeps every key
+// > T and the first (by candidate index) keys == T up to s~ (Z6), and of those the ones with
+// kappa >= theta^2 and kappa > 0 (Z5).  All decisions are integer/ordered comparisons of the same
+// doubles, hence exact and independent of thread scheduling; votes are integer atomics.
+#include "common.cuh"
+
+namespace usfft {
+
+__device__ __forceinline__ double theta2_of(double theta_rel, double theta_abs, const double *kmax) {
+    if (theta_abs > 0.0) return __dmul_rn(theta_abs, theta_abs);
+    return __dmul_rn(__dmul_rn(theta_rel, theta_rel), kmax[0]);
+}
+
+// one CTA per owned node g
+__global__ void __launch_bounds__(512)
+k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__ kmax,
+         int32_t s_tilde, double theta_rel, double theta_abs, int32_t *__restrict__ votes,
+         int32_t *__restrict__ det_g, int32_t *__restrict__ n_det_g, double *__restrict__ th2_out) {
+    __shared__ unsigned int hist[256];
+    __shared__ unsigned long long s_prefix;
+    __shared__ long long s_need;
+    __shared__ int scan_sh[33];
+    const int64_t g = blockIdx.x;
+    const unsigned long long *keys =
+        reinterpret_cast<const unsigned long long *>(kmin + g * nJ);
+    const double th2 = theta2_of(theta_rel, theta_abs, kmax);
+    if (g == 0 && threadIdx.x == 0 && th2_out) th2_out[0] = th2;
+
+    unsigned long long T = 0ull;
+    long long need_eq;
+    if ((int64_t)s_tilde >= nJ) {
+        // every candidate is within the top s~
+        T = 0ull;
+        need_eq = nJ;
+    } else {
+        unsigned long long prefix = 0ull, pmask = 0ull;
+        long long k = s_tilde;                       // rank (1-based, from the top) still to find
+        for (int pass = 0; pass < 8; ++pass) {
+            const int shift = 56 - 8 * pass;
+            for (int q = threadIdx.x; q < 256; q += blockDim.x) hist[q] = 0u;
+            __syncthreads();
+            for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) {
+                const unsigned long long key = keys[j];
+                if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255ull], 1u);
+            }
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                long long cum = 0;
+                int digit = 0;
+                for (int dg = 255; dg >= 0; --dg) {
+                    if (cum + (long long)hist[dg] >= k) {
+                        digit = dg;
+                        break;
+                    }
+                    cum += hist[dg];
+                }
+                k -= cum;
+                s_prefix = prefix | ((unsigned long long)digit << shift);
+                s_need = k;
+            }
+            __syncthreads();
+            prefix = s_prefix;
+            k = s_need;
+            pmask |= 255ull << shift;
+        }
+        T = prefix;
+        need_eq = k;                                 // how many keys == T are taken (by index)
+    }
+    // ordered pass: membership, threshold, output in ascending j, votes
+    int eq_run = 0, out_run = 0;
+    int32_t *out = det_g + g * (int64_t)s_tilde;
+    for (int64_t base = 0; base < nJ; base += blockDim.x) {
+        const int64_t j = base + threadIdx.x;
+        unsigned long long key = 0ull;
+        bool valid = j < nJ;
+        if (valid) key = keys[j];
+        const int is_eq = (valid && key == T) ? 1 : 0;
+        int eq_tot;
+        const int eq_before = eq_run + block_exscan(is_eq, scan_sh, &eq_tot);
+        bool member = valid && (key > T || (is_eq && eq_before < need_eq));
+        const double kv = __longlong_as_double((long long)key);
+        const int take = (member && kv >= th2 && kv > 0.0) ? 1 : 0;
+        int tot;
+        const int pos = out_run + block_exscan(take, scan_sh, &tot);
+        if (take) {
+            out[pos] = (int32_t)j;
+            atomicAdd(votes + j, 1);
+        }
+        eq_run += eq_tot;
+        out_run += tot;
+    }
+    for (int q = out_run + threadIdx.x; q < s_tilde; q += blockDim.x) out[q] = -1;
+    if (threadIdx.x == 0) n_det_g[g] = out_run;
+}
+
+// single CTA: flags |= votes > 0; ordered compaction of this round's detections and of the union
+__global__ void __launch_bounds__(1024)
+k_union(const int32_t *__restrict__ votes, int64_t nJ, uint8_t *__restrict__ flags,
+        int32_t *__restrict__ det_idx, int32_t *__restrict__ union_idx,
+        long long *__restrict__ counts) {
+    __shared__ int scan_sh[33];
+    long long nd = 0, nu = 0;
+    for (int64_t base = 0; base < nJ; base += blockDim.x) {
+        const int64_t j = base + threadIdx.x;
+        int v = 0, f = 0;
+        if (j < nJ) {
+            v = votes[j] > 0 ? 1 : 0;
+            f = (flags[j] | v) ? 1 : 0;
+            flags[j] = (uint8_t)f;
+        }
+        int tv, tf;
+        const int pv = block_exscan(v, scan_sh, &tv);
+        const int pf = block_exscan(f, scan_sh, &tf);
+        if (v) det_idx[nd + pv] = (int32_t)j;
+        if (f && union_idx) union_idx[nu + pf] = (int32_t)j;
+        nd += tv;
+        nu += tf;
+    }
+    if (threadIdx.x == 0) {
+        counts[0] = nd;
+        counts[1] = nu;
+    }
+}
+
+__device__ __forceinline__ int member_sorted(const int32_t *__restrict__ a, int n, int32_t k) {
+    int lo = 0, hi = n;
+    while (lo < hi) {
+        int mid = (lo + hi) >> 1;
+        if (a[mid] < k) lo = mid + 1;
+        else hi = mid;
+    }
+    return (lo < n && a[lo] == k) ? 1 : 0;
+}
+
+// one CTA per owned node g: l* = first lattice where k is alias-free w.r.t. D_g (Z1, a12)
+__global__ void __launch_bounds__(256)
+k_resolve(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t nJ, int64_t M,
+          int32_t L, const int32_t *__restrict__ det_g, const int32_t *__restrict__ n_det_g,
+          int32_t s_tilde, const int32_t *__restrict__ det_idx, int64_t n_det,
+          double2 *__restrict__ coef, int32_t *__restrict__ lstar) {
+    extern __shared__ int cnt[];                       // [M]
+    const int64_t g = blockIdx.x;
+    const int32_t *Dg = det_g + g * (int64_t)s_tilde;
+    const int nD = n_det_g[g];
+    const int64_t Mh = M / 2 + 1;
+    int32_t *ls = lstar + g * n_det;
+    for (int64_t q = threadIdx.x; q < n_det; q += blockDim.x) ls[q] = -1;
+    for (int l = 0; l < L; ++l) {
+        for (int64_t m = threadIdx.x; m < M; m += blockDim.x) cnt[m] = 0;
+        __syncthreads();
+        for (int q = threadIdx.x; q < nD; q += blockDim.x) atomicAdd(&cnt[bins[(int64_t)l * nJ + Dg[q]]], 1);
+        __syncthreads();
+        for (int64_t q = threadIdx.x; q < n_det; q += blockDim.x) {
+            if (ls[q] >= 0) continue;
+            const int32_t k = det_idx[q];
+            const int64_t b = bins[(int64_t)l * nJ + k];
+            if (cnt[b] - member_sorted(Dg, nD, k) == 0) {
+                ls[q] = l;
+                coef[g * n_det + q] = spec_value(F + (g * L + l) * Mh, M, b);
+            }
+        }
+        __syncthreads();
+    }
+    // median fallback (componentwise, lower median for even L)
+    for (int64_t q = threadIdx.x; q < n_det; q += blockDim.x) {
+        if (ls[q] >= 0) continue;
+        const int32_t k = det_idx[q];
+        double re[64], im[64];
+        for (int l = 0; l < L; ++l) {
+            const double2 v = spec_value(F + (g * L + l) * Mh, M, bins[(int64_t)l * nJ + k]);
+            re[l] = v.x;
+            im[l] = v.y;
+        }
+        for (int a = 1; a < L; ++a) {              // insertion sort, L <= 64
+            double x = re[a], y = im[a];
+            int p = a - 1;
+            while (p >= 0 && re[p] > x) { re[p + 1] = re[p]; --p; }
+            re[p + 1] = x;
+            p = a - 1;
+            while (p >= 0 && im[p] > y) { im[p + 1] = im[p]; --p; }
+            im[p + 1] = y;
+        }
+        coef[g * n_det + q] = make_double2(re[(L - 1) / 2], im[(L - 1) / 2]);
+    }
+}
+
+}  // namespace usfft
+
+using namespace usfft;
+
+extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t nJ,
+                                            const double *kappa_min, const double *kappa_max,
+                                            int32_t s_tilde, double theta_rel, double theta_abs,
+                                            int32_t *votes, int32_t *det_g, int32_t *n_det_g,
+                                            double *theta2) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, G_loc >= 0 && nJ >= 0 && s_tilde >= 1, "bad sizes");
+    USFFT_REQUIRE(c, nJ <= 0x7fffffff, "|J| too large");
+    USFFT_REQUIRE(c, theta_rel >= 0.0 && theta_abs >= 0.0, "negative theta");
+    USFFT_REQUIRE(c, nJ == 0 || votes != nullptr, "votes NULL");
+    USFFT_REQUIRE(c, G_loc == 0 || nJ == 0 || (kappa_min && kappa_max && det_g && n_det_g), "NULL pointer");
+    if (nJ > 0) USFFT_CUDA(c, cudaMemsetAsync(votes, 0, sizeof(int32_t) * nJ, c->stream));
+    if (G_loc == 0 || nJ == 0) {
+        if (G_loc > 0 && n_det_g) USFFT_CUDA(c, cudaMemsetAsync(n_det_g, 0, sizeof(int32_t) * G_loc, c->stream));
+        return USFFT_OK;
+    }
+    k_select<<<(unsigned)G_loc, 512, 0, c->stream>>>(kappa_min, nJ, kappa_max, s_tilde, theta_rel,
+                                                      theta_abs, votes, det_g, n_det_g, theta2);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
+extern "C" usfft_status usfft_detect_union(usfft_ctx *c, int64_t nJ, const int32_t *votes,
+                                           uint8_t *flags, int32_t *det_idx, int64_t *n_det,
+                                           int32_t *union_idx, int64_t *n_union) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, nJ >= 0 && nJ <= 0x7fffffff, "bad |J|");
+    USFFT_REQUIRE(c, nJ == 0 || (votes && flags && det_idx), "NULL pointer");
+    USFFT_REQUIRE(c, n_det != nullptr, "n_det NULL");
+    long long *counts = reinterpret_cast<long long *>(static_cast<char *>(c->dscal) + 64);
+    if (nJ == 0) {
+        *n_det = 0;
+        if (n_union) *n_union = 0;
+        return USFFT_OK;
+    }
+    k_union<<<1, 1024, 0, c->stream>>>(votes, nJ, flags, det_idx, union_idx, counts);
+    USFFT_CHECK_LAUNCH(c);
+    long long h[2];
+    USFFT_CUDA(c, cudaMemcpyAsync(h, counts, sizeof h, cudaMemcpyDeviceToHost, c->stream));
+    USFFT_CUDA(c, cudaStreamSynchronize(c->stream));
+    *n_det = h[0];
+    if (n_union) *n_union = h[1];
+    return USFFT_OK;
+}
+
+extern "C" usfft_status usfft_resolve(usfft_ctx *c, const usfft_lattice_desc *lat, int64_t G_loc,
+                                      const double *spectra, const int32_t *bins, int64_t nJ,
+                                      const int32_t *det_g, const int32_t *n_det_g, int32_t s_tilde,
+                                      const int32_t *det_idx, int64_t n_det, double *coef,
+                                      int32_t *lstar) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, lat != nullptr && lat->M >= 2 && lat->L >= 1 && lat->L <= 64, "bad lattice desc (L <= 64)");
+    USFFT_REQUIRE(c, G_loc >= 0 && n_det >= 0 && s_tilde >= 1, "bad sizes");
+    if (G_loc == 0 || n_det == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, spectra && bins && det_g && n_det_g && det_idx && coef, "NULL pointer");
+    const size_t smem = sizeof(int) * (size_t)lat->M;
+    USFFT_REQUIRE(c, smem <= c->smem_optin, "M too large for the resolve occupancy table");
+    int32_t *ls = lstar;
+    if (!ls) {
+        usfft_status s = ensure(c, &c->ws, &c->ws_size, sizeof(int32_t) * (size_t)G_loc * n_det);
+        if (s) return s;
+        ls = static_cast<int32_t *>(c->ws);
+    }
+    USFFT_CUDA(c, cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_resolve<<<(unsigned)G_loc, 256, smem, c->stream>>>(
+        reinterpret_cast<const double2 *>(spectra), bins, nJ, lat->M, lat->L, det_g, n_det_g,
+        s_tilde, det_idx, n_det, reinterpret_cast<double2 *>(coef), ls);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}

@@ -1,0 +1,89 @@
+// eval.cu — K11 evaluation of the approximant at test points (usfft_eval, include/usfft.h).
+//
+// U[g][q] = Re sum_k C[g][k] e^{2 pi i k.y_q} = sum_k Cre[g][k] cos(2 pi k.y_q) - Cim[g][k] sin(2 pi k.y_q)
+// (eq. eval_formula P:468-470 with the identity periodization of the periodic model P:945-949).
+// This is a real GEMM [G x 2|I|] . [2|I| x n] whose right operand is generated on the fly from the
+// sparse integer frequencies: each 64x64 output tile loops over k in chunks of 16, stages the
+// C chunk and the phase chunk (k.y reduced mod 1, then sincospi) in shared memory, and every
+// thread accumulates a 4x4 register tile in fp64.
+#include "common.cuh"
+
+namespace usfft {
+
+constexpr int EV_TG = 64, EV_TQ = 64, EV_TK = 16;
+
+__global__ void __launch_bounds__(256)
+k_eval(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
+       int64_t G, const double *__restrict__ Y, int64_t n, double *__restrict__ U) {
+    __shared__ double cre[EV_TK][EV_TG + 1], cim[EV_TK][EV_TG + 1];
+    __shared__ double cs[EV_TK][EV_TQ + 1], sn[EV_TK][EV_TQ + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t g0 = (int64_t)blockIdx.y * EV_TG, q0 = (int64_t)blockIdx.x * EV_TQ;
+    double acc[4][4] = {};
+    for (int64_t k0 = 0; k0 < nI; k0 += EV_TK) {
+        for (int e = threadIdx.x; e < EV_TK * EV_TG; e += blockDim.x) {
+            const int kk = e / EV_TG, gg = e % EV_TG;
+            double2 v = make_double2(0.0, 0.0);
+            if (k0 + kk < nI && g0 + gg < G) v = C[(g0 + gg) * nI + k0 + kk];
+            cre[kk][gg] = v.x;
+            cim[kk][gg] = v.y;
+        }
+        for (int e = threadIdx.x; e < EV_TK * EV_TQ; e += blockDim.x) {
+            const int kk = e / EV_TQ, qq = e % EV_TQ;
+            double c = 0.0, s = 0.0;
+            if (k0 + kk < nI && q0 + qq < n) {
+                double ph = 0.0;
+                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
+                sincospi(2.0 * (ph - rint(ph)), &s, &c);
+            }
+            cs[kk][qq] = c;
+            sn[kk][qq] = s;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < EV_TK; ++kk) {
+            double a_re[4], a_im[4], b_c[4], b_s[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                a_re[r] = cre[kk][ty * 4 + r];
+                a_im[r] = cim[kk][ty * 4 + r];
+                b_c[r] = cs[kk][tx * 4 + r];
+                b_s[r] = sn[kk][tx * 4 + r];
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int s2 = 0; s2 < 4; ++s2) acc[r][s2] += a_re[r] * b_c[s2] - a_im[r] * b_s[s2];
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t g = g0 + ty * 4 + r;
+        if (g >= G) continue;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+            const int64_t q = q0 + tx * 4 + s2;
+            if (q < n) U[g * n + q] = acc[r][s2];
+        }
+    }
+}
+
+}  // namespace usfft
+
+using namespace usfft;
+
+extern "C" usfft_status usfft_eval(usfft_ctx *c, int32_t d, const int16_t *I, int64_t nI,
+                                   const double *C, int64_t G, const double *Y, int64_t n,
+                                   double *U) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, d >= 1 && d <= kMaxD && nI >= 0 && G >= 0 && n >= 0, "bad sizes");
+    if (G == 0 || n == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, U != nullptr && Y != nullptr, "U / Y NULL");
+    USFFT_REQUIRE(c, nI == 0 || (I && C), "I / C NULL");
+    USFFT_REQUIRE(c, (n + EV_TQ - 1) / EV_TQ <= 0x7fffffff && (G + EV_TG - 1) / EV_TG <= 65535, "grid too large");
+    dim3 grid((unsigned)((n + EV_TQ - 1) / EV_TQ), (unsigned)((G + EV_TG - 1) / EV_TG));
+    k_eval<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}

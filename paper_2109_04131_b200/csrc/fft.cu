@@ -1,0 +1,158 @@
+// fft.cu — K6 lattice DFT along the sample axis + K7 candidate gather / detection key.
+// usfft_lattice_fft (include/usfft.h; a7 + a8 of SURVEY §8(a)).
+//
+// K6 (this version): direct DFT per (node, lattice) row staged in shared memory, the phase index
+// (i*m) mod M carried as an exact integer, twiddles e^{-2 pi i m/M} from a per-M table built with
+// sincospi.  Real input, bins 0..M/2 (Z17).
+// K7: v_l(j,g) = F[g][l][b]/M with b = bins[l][j] (conjugated mirror bin for b > M/2, Z17/Z18),
+// kappa_l = fl(fl(re*re) + fl(im*im)) (no FMA contraction, Z5), kappa_min = min over l (Z1);
+// the max over (g, j) of kappa_min is accumulated with an integer atomicMax on the bit pattern
+// (non-negative doubles order like uint64), so it is exact and order-independent.
+#include "common.cuh"
+
+namespace usfft {
+
+struct SlabParams {
+    int32_t nslab;
+    int64_t b0[kMaxSlab + 1];
+};
+
+__global__ void k_twiddles(int64_t M, double2 *__restrict__ tw) {
+    for (int64_t m = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; m < M;
+         m += (int64_t)gridDim.x * blockDim.x) {
+        double s, c;
+        sincospi((double)(2 * m) / (double)M, &s, &c);
+        tw[m] = make_double2(c, -s);                              // e^{-2 pi i m / M}
+    }
+}
+
+__device__ __forceinline__ double sample_at(const double *__restrict__ u, const SlabParams &S,
+                                            int64_t G_loc, int64_t g, int64_t b) {
+    int p = 0;
+    while (p + 1 < S.nslab && b >= S.b0[p + 1]) ++p;
+    const int64_t w = S.b0[p + 1] - S.b0[p];
+    return u[G_loc * S.b0[p] + g * w + (b - S.b0[p])];
+}
+
+// one CTA per row (g, l): F[g][l][m] = sum_i u[g][l*M+i] e^{-2 pi i (i m mod M)/M}, m <= M/2
+__global__ void k_dft_direct(const double *__restrict__ u, const SlabParams S, int64_t G_loc,
+                             int64_t M, int32_t L, const double2 *__restrict__ tw,
+                             double2 *__restrict__ F) {
+    extern __shared__ double sm[];
+    double *xs = sm;                                             // [M]
+    double2 *ts = reinterpret_cast<double2 *>(sm + ((M + 1) & ~int64_t(1)));   // [M]
+    const int64_t row = blockIdx.x;
+    const int64_t g = row / L, l = row - g * L;
+    const int64_t Mh = M / 2 + 1;
+    for (int64_t i = threadIdx.x; i < M; i += blockDim.x) {
+        xs[i] = sample_at(u, S, G_loc, g, l * M + i);
+        ts[i] = tw[i];
+    }
+    __syncthreads();
+    for (int64_t m = threadIdx.x; m < Mh; m += blockDim.x) {
+        double re = 0.0, im = 0.0;
+        int64_t idx = 0;
+        for (int64_t i = 0; i < M; ++i) {
+            const double2 w = ts[idx];
+            re += xs[i] * w.x;
+            im += xs[i] * w.y;
+            idx += m;
+            if (idx >= M) idx -= M;
+        }
+        F[row * Mh + m] = make_double2(re, im);
+    }
+}
+
+// one CTA per owned node g
+__global__ void k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins,
+                        int64_t nJ, int64_t M, int32_t L, double *__restrict__ kmin,
+                        unsigned long long *__restrict__ kmax) {
+    __shared__ unsigned long long wmax[32];
+    const int64_t g = blockIdx.x;
+    const int64_t Mh = M / 2 + 1;
+    unsigned long long best = 0ull;
+    for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) {
+        double km = 0.0;
+        for (int l = 0; l < L; ++l) {
+            const int64_t b = bins[(int64_t)l * nJ + j];
+            const double2 v = spec_value(F + (g * L + l) * Mh, M, b);
+            const double re = v.x, im = v.y;
+            const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+            km = (l == 0) ? k : fmin(km, k);
+        }
+        kmin[g * nJ + j] = km;
+        const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
+        best = bits > best ? bits : best;
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other > best ? other : best;
+    }
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = wmax[w] > best ? wmax[w] : best;
+        atomicMax(kmax, best);
+    }
+}
+
+}  // namespace usfft
+
+using namespace usfft;
+
+static usfft_status get_twiddles(usfft_ctx *c, int64_t M, double2 **out) {
+    auto it = c->twiddles.find(M);
+    if (it != c->twiddles.end()) {
+        *out = it->second;
+        return USFFT_OK;
+    }
+    double2 *tw = nullptr;
+    USFFT_CUDA(c, cudaMalloc(&tw, sizeof(double2) * M));
+    k_twiddles<<<grid1d(M, 256), 256, 0, c->stream>>>(M, tw);
+    USFFT_CHECK_LAUNCH(c);
+    c->twiddles[M] = tw;
+    *out = tw;
+    return USFFT_OK;
+}
+
+extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc *lat,
+                                          int64_t G_loc, const double *u, int32_t nslab,
+                                          const int64_t *slab_b0, const int32_t *bins, int64_t nJ,
+                                          double *spectra, double *kappa_min, double *kappa_max) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, lat != nullptr, "lattice desc is NULL");
+    const int64_t M = lat->M;
+    const int32_t L = lat->L;
+    USFFT_REQUIRE(c, M >= 2 && M <= (int64_t(1) << 26) && L >= 1, "bad M / L");
+    USFFT_REQUIRE(c, G_loc >= 0 && nJ >= 0, "negative sizes");
+    USFFT_REQUIRE(c, nslab >= 1 && nslab <= kMaxSlab && slab_b0 != nullptr, "nslab out of [1, %d]", kMaxSlab);
+    USFFT_REQUIRE(c, slab_b0[0] == 0 && slab_b0[nslab] == (int64_t)L * M, "slab_b0 must span [0, L*M]");
+    for (int p = 0; p < nslab; ++p)
+        USFFT_REQUIRE(c, slab_b0[p + 1] >= slab_b0[p], "slab_b0 not monotone");
+    USFFT_REQUIRE(c, G_loc == 0 || (u && spectra), "u / spectra NULL");
+    USFFT_REQUIRE(c, nJ == 0 || G_loc == 0 || (bins && kappa_min), "bins / kappa_min NULL");
+    const size_t smem = sizeof(double) * (size_t)((M + 1) & ~int64_t(1)) + sizeof(double2) * (size_t)M;
+    USFFT_REQUIRE(c, smem <= c->smem_optin, "M = %lld too large for the direct DFT", (long long)M);
+    SlabParams S;
+    S.nslab = nslab;
+    for (int p = 0; p <= nslab; ++p) S.b0[p] = slab_b0[p];
+
+    if (kappa_max) USFFT_CUDA(c, cudaMemsetAsync(kappa_max, 0, sizeof(double), c->stream));
+    if (G_loc == 0) return USFFT_OK;
+    double2 *tw = nullptr;
+    usfft_status s = get_twiddles(c, M, &tw);
+    if (s) return s;
+    USFFT_CUDA(c, cudaFuncSetAttribute(k_dft_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t rows = G_loc * L;
+    k_dft_direct<<<(unsigned)rows, 256, smem, c->stream>>>(u, S, G_loc, M, L, tw,
+                                                            reinterpret_cast<double2 *>(spectra));
+    USFFT_CHECK_LAUNCH(c);
+    if (nJ > 0) {
+        unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
+        if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
+        k_kappa<<<(unsigned)G_loc, 256, 0, c->stream>>>(reinterpret_cast<const double2 *>(spectra),
+                                                        bins, nJ, M, L, kappa_min, km);
+        USFFT_CHECK_LAUNCH(c);
+    }
+    return USFFT_OK;
+}

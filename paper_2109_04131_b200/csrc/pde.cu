@@ -1,0 +1,282 @@
+// pde.cu — K3 coefficient field + K4 batched Jacobi-PCG: one P1 FE solve per lattice node.
+// usfft_sample_pde (include/usfft.h; a4 + a5 of SURVEY §8(a)).
+//
+// Discretisation (DESIGN.md §3 Z11/Z12): on the uniform "/" triangulation the P1 stiffness of
+// -div(a grad u) with centroid-quadrature a is the 5-point operator
+//     (A u)_p = sum_{edges e=(p,q)} w_e (u_p - u_q),
+//     w_h(i,j) = (a(T_lo(i,j)) + a(T_up(i,j-1)))/2,  w_v(i,j) = (a(T_up(i,j)) + a(T_lo(i-1,j)))/2,
+// T_lo(ci,cj) centroid ((ci+2/3)h, (cj+1/3)h), T_up(ci,cj) centroid ((ci+1/3)h, (cj+2/3)h);
+// the centroid load of f = x2 is b_p = h^2 x2_p.  (The oracle assembles element by element; a
+// CPU test checks this stencil against that assembly.)
+//
+// One CTA solves one sample at a time (persistent loop over samples).  The padded node grid
+// (n+1)^2 holds p with a zero Dirichlet ring, so the stencil needs no bounds checks.  Per-sample
+// state lives in shared memory when it fits (n <= 64) and in a per-CTA global scratch slab
+// otherwise; the per-thread q values stay in registers.  Block reductions are fixed trees, so a
+// sample's result does not depend on which CTA or rank solved it.
+#include "lattice.cuh"
+
+namespace usfft {
+
+struct PdeParams {
+    int32_t n, d, theta, form, f_kind, maxit;
+    double tol2;              // tol^2
+    double amp[kMaxD];
+};
+
+__device__ __forceinline__ double theta_of(int kind, double y) {
+    if (kind == 0) return sinpi(2.0 * y);                         // sin(2 pi y)
+    if (kind == 1) return 1.0 - fabs(2.0 * (1.0 - 2.0 * y));      // tent, eq. tent
+    double v = normcdfinv(y);                                      // Phi^-1 (Z15)
+    return fmin(fmax(v, -6.0), 6.0);                               // clip, NaN-free: -inf -> -6
+}
+
+// sin(j pi m / (3n)) for j = 1..d, m = 0..3n: the centroid abscissae are (3c+1)h/3, (3c+2)h/3.
+__global__ void k_sintab(int n, int d, double *__restrict__ S) {
+    const int W = 3 * n + 1;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d * W; e += gridDim.x * blockDim.x) {
+        const int j = e / W + 1, m = e % W;
+        S[e] = sinpi((double)(j * m) / (double)(3 * n));
+    }
+}
+
+// a at a triangle centroid with sin-table columns m1 (x1) and m2 (x2)
+__device__ __forceinline__ double coef_at(const PdeParams &Q, const double *__restrict__ th_amp,
+                                          const double *__restrict__ S, int W, int m1, int m2) {
+    double s = 0.0;
+    for (int j = 0; j < Q.d; ++j) s += th_amp[j] * S[j * W + m1] * S[j * W + m2];
+    return Q.form == 0 ? 1.0 + s : exp(s);
+}
+
+template <int NPT, int THREADS>
+__global__ void __launch_bounds__(THREADS)
+k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
+      int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
+      double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
+      double *__restrict__ gscratch, int64_t region) {
+    extern __shared__ double smem[];
+    __shared__ double red[64];
+    __shared__ double th_amp[kMaxD];
+
+    const int n = Q.n, nx = n - 1, G = nx * nx, np = n + 1, W = 3 * n + 1;
+    double *base = gscratch ? gscratch + (int64_t)blockIdx.x * region : smem;
+    double *p = base;                    // [(n+1)^2] padded
+    double *wh = p + np * np;            // wh[j*np+i]: edge (i,j)-(i+1,j)
+    double *wv = wh + np * np;           // wv[j*np+i]: edge (i,j)-(i,j+1)
+    double *x = wv + np * np;            // [G]
+    double *r = x + G;                   // [G]
+    double *dinv = r + G;                // [G]
+    constexpr int T = THREADS;
+    const int tid = threadIdx.x;
+    const double h2b = 1.0 / ((double)n * n * n);   // b_p = h^2 * x2_p = j / n^3
+
+    for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
+        const int64_t b = b0 + bl;
+        // ---- K3: theta_j(y_b) and the edge weights ----------------------------------------
+        if (tid < Q.d) {
+            const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
+            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
+        }
+        __syncthreads();
+        for (int e = tid; e < np * np; e += T) {
+            const int i = e % np, j = e / np;
+            p[e] = 0.0;
+            double h = 0.0, v = 0.0;
+            if (i < n && j >= 1 && j <= nx)                        // horizontal edge (i,j)-(i+1,j)
+                h = 0.5 * (coef_at(Q, th_amp, S, W, 3 * i + 2, 3 * j + 1) +        // T_lo(i,j)
+                           coef_at(Q, th_amp, S, W, 3 * i + 1, 3 * (j - 1) + 2));  // T_up(i,j-1)
+            if (j < n && i >= 1 && i <= nx)                        // vertical edge (i,j)-(i,j+1)
+                v = 0.5 * (coef_at(Q, th_amp, S, W, 3 * i + 1, 3 * j + 2) +        // T_up(i,j)
+                           coef_at(Q, th_amp, S, W, 3 * (i - 1) + 2, 3 * j + 1));  // T_lo(i-1,j)
+            wh[e] = h;
+            wv[e] = v;
+        }
+        __syncthreads();
+        // ---- PCG init: x = 0, r = b, p = z = D^-1 r ---------------------------------------
+        double acc[2] = {0.0, 0.0};      // rz, bb
+        for (int k = 0; k < NPT; ++k) {
+            const int g = tid + k * T;
+            if (g < G) {
+                const int i = g % nx + 1, j = g / nx + 1, e = j * np + i;
+                const double dg = wh[e] + wh[e - 1] + wv[e] + wv[e - np];
+                const double di = 1.0 / dg;
+                const double bv = (double)j * h2b;
+                dinv[g] = di;
+                x[g] = 0.0;
+                r[g] = bv;
+                const double z = di * bv;
+                p[e] = z;
+                acc[0] += bv * z;
+                acc[1] += bv * bv;
+            }
+        }
+        block_sum<2>(acc, red);
+        double rz = acc[0];
+        const double bb = acc[1];
+        double rr = bb;
+        int it = 0;
+        while (rr > Q.tol2 * bb && it < Q.maxit) {
+            // q = A p, pq = p.q
+            double q[NPT];
+            double pq[1] = {0.0};
+#pragma unroll
+            for (int k = 0; k < NPT; ++k) {
+                const int g = tid + k * T;
+                q[k] = 0.0;
+                if (g < G) {
+                    const int i = g % nx + 1, j = g / nx + 1, e = j * np + i;
+                    const double we = wh[e], ww = wh[e - 1], wn = wv[e], ws = wv[e - np];
+                    const double pc = p[e];
+                    const double qq = (we + ww + wn + ws) * pc - we * p[e + 1] - ww * p[e - 1] -
+                                      wn * p[e + np] - ws * p[e - np];
+                    q[k] = qq;
+                    pq[0] += pc * qq;
+                }
+            }
+            block_sum<1>(pq, red);
+            const double alpha = rz / pq[0];
+            double acc2[2] = {0.0, 0.0};   // rz_new, rr
+#pragma unroll
+            for (int k = 0; k < NPT; ++k) {
+                const int g = tid + k * T;
+                if (g < G) {
+                    const int i = g % nx + 1, j = g / nx + 1, e = j * np + i;
+                    x[g] += alpha * p[e];
+                    const double rn = r[g] - alpha * q[k];
+                    r[g] = rn;
+                    acc2[0] += rn * (dinv[g] * rn);
+                    acc2[1] += rn * rn;
+                }
+            }
+            block_sum<2>(acc2, red);
+            const double beta = acc2[0] / rz;
+            rz = acc2[0];
+            rr = acc2[1];
+#pragma unroll
+            for (int k = 0; k < NPT; ++k) {
+                const int g = tid + k * T;
+                if (g < G) {
+                    const int i = g % nx + 1, j = g / nx + 1, e = j * np + i;
+                    p[e] = dinv[g] * r[g] + beta * p[e];
+                }
+            }
+            __syncthreads();
+            ++it;
+        }
+        // ---- output u[g][bl] ----------------------------------------------------------------
+        for (int g = tid; g < G; g += T) u[(int64_t)g * ldu + bl] = x[g];
+        if (tid == 0) {
+            if (iters) iters[bl] = it;
+            if (relres) relres[bl] = sqrt(rr / bb);
+            if (rr > Q.tol2 * bb) atomicAdd(noconv, 1);
+        }
+        __syncthreads();
+    }
+}
+
+}  // namespace usfft
+
+using namespace usfft;
+
+namespace {
+template <int NPT, int THREADS>
+usfft_status launch_pcg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
+                        int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters,
+                        double *relres, int32_t *noconv, const double *S) {
+    const int threads = THREADS;
+    const int n = Q.n, G = (n - 1) * (n - 1), np = n + 1;
+    const int64_t region = 3LL * np * np + 3LL * G;           // doubles per sample state
+    const size_t bytes = (size_t)region * sizeof(double);
+    double *gscratch = nullptr;
+    int grid = 0;
+    size_t dyn = 0;
+    if (bytes + 1024 <= c->smem_optin) {
+        dyn = bytes;
+        USFFT_CUDA(c, cudaFuncSetAttribute(k_pcg<NPT, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        int per_sm = 0;
+        USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg<NPT, THREADS>, threads, dyn));
+        if (per_sm < 1) per_sm = 1;
+        grid = per_sm * c->sm_count;
+    } else {
+        int per_sm = 0;
+        USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg<NPT, THREADS>, threads, 0));
+        if (per_sm < 1) per_sm = 1;
+        grid = per_sm * c->sm_count;
+        if ((int64_t)grid > nb) grid = (int)nb;
+        usfft_status s = ensure(c, &c->ws, &c->ws_size, (size_t)grid * bytes);
+        if (s) return s;
+        gscratch = static_cast<double *>(c->ws);
+    }
+    if ((int64_t)grid > nb) grid = (int)nb;
+    k_pcg<NPT, THREADS><<<grid, threads, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
+                                                   noconv, S, gscratch, region);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+}  // namespace
+
+extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde,
+                                         const usfft_lattice_desc *lat, int64_t b0, int64_t nb,
+                                         const double *nodes, double *u, int64_t ldu,
+                                         int32_t *iters, double *relres, int32_t *n_noconv) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, pde != nullptr, "pde desc is NULL");
+    static thread_local LatParams P;
+    static thread_local PdeParams Q;
+    usfft_status s = make_lat_params(c, lat, &P);
+    if (s) return s;
+    USFFT_REQUIRE(c, pde->n >= 2 && pde->n <= 128, "n = %d out of [2, 128]", pde->n);
+    USFFT_REQUIRE(c, pde->d >= 1 && pde->d <= P.d, "pde d = %d must be in [1, lattice d]", pde->d);
+    USFFT_REQUIRE(c, pde->theta >= 0 && pde->theta <= 2, "theta kind %d", pde->theta);
+    USFFT_REQUIRE(c, pde->form == 0 || pde->form == 1, "form %d", pde->form);
+    USFFT_REQUIRE(c, pde->f_kind == 0, "f_kind %d not implemented", pde->f_kind);
+    USFFT_REQUIRE(c, pde->amp != nullptr, "amp is NULL");
+    USFFT_REQUIRE(c, pde->tol > 0.0 && pde->maxit >= 1, "tol/maxit");
+    USFFT_REQUIRE(c, b0 >= 0 && nb >= 0 && b0 + nb <= (int64_t)P.L * P.M, "sample range");
+    USFFT_REQUIRE(c, ldu >= nb && u != nullptr, "u is NULL or ldu < nb");
+    if (nb == 0) {
+        if (n_noconv) *n_noconv = 0;
+        return USFFT_OK;
+    }
+    Q.n = pde->n;
+    Q.d = pde->d;
+    Q.theta = pde->theta;
+    Q.form = pde->form;
+    Q.f_kind = pde->f_kind;
+    Q.maxit = pde->maxit;
+    Q.tol2 = pde->tol * pde->tol;
+    for (int j = 0; j < pde->d; ++j) Q.amp[j] = pde->amp[j];
+
+    // sin table for (n, d): cached per ctx
+    auto key = std::make_pair(pde->n, pde->d);
+    double *S = nullptr;
+    auto it = c->sintab.find(key);
+    if (it == c->sintab.end()) {
+        const size_t cnt = (size_t)pde->d * (3 * pde->n + 1);
+        USFFT_CUDA(c, cudaMalloc(&S, cnt * sizeof(double)));
+        k_sintab<<<grid1d(cnt, 256), 256, 0, c->stream>>>(pde->n, pde->d, S);
+        USFFT_CHECK_LAUNCH(c);
+        c->sintab[key] = S;
+    } else {
+        S = it->second;
+    }
+    int32_t *noconv = reinterpret_cast<int32_t *>(c->dscal);      // device counter slot 0
+    USFFT_CUDA(c, cudaMemsetAsync(noconv, 0, sizeof(int32_t), c->stream));
+
+    const int n = pde->n, G = (n - 1) * (n - 1);
+    // threads x nodes-per-thread: 128x2 (G <= 256), 256x4 (G <= 1024), 512x8, 1024x16
+    if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else if (G <= 4096) s = launch_pcg<8, 512>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else s = launch_pcg<16, 1024>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    if (s) return s;
+    int32_t host_nc = 0;
+    if (n_noconv) {
+        USFFT_CUDA(c, cudaMemcpyAsync(&host_nc, noconv, sizeof(int32_t), cudaMemcpyDeviceToHost, c->stream));
+        USFFT_CUDA(c, cudaStreamSynchronize(c->stream));
+        *n_noconv = host_nc;
+    }
+    if (n_noconv && host_nc > 0)
+        return fail(c, USFFT_ENOCONV, "%d of %lld samples missed tol at maxit", host_nc, (long long)nb);
+    return USFFT_OK;
+}

@@ -1,0 +1,194 @@
+"""Alg. 1 "The usFFT on a set T_G" driven through the C-ABI on one or more GPUs.
+
+The host loop only sequences the C-ABI calls, sizes buffers and runs the collectives of
+dist.Exchange; every step of a round (plan, nodes, bins, PDE solves, FFT, keys, selection,
+union, resolve, row gather) runs in libusfft.so.
+
+Round r = (step, t, i):
+  a1 plan (usfft_plan_round) -> a2/a3 bins (usfft_lattice) -> a4/a5 samples of this rank
+  (usfft_sample_pde, nodes generated in-kernel) -> a6 transpose (Exchange.transpose) ->
+  a7/a8 FFT + keys (usfft_lattice_fft) -> a9 kappa_max MAX -> a10 select + votes
+  (usfft_detect_select) -> votes SUM -> a11 union (usfft_detect_union) -> a12 resolve
+  (usfft_resolve, final round only).
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+import torch
+
+from . import binding as B
+from .dist import Exchange, partition
+
+
+@dataclass
+class RoundResult:
+    plan: B.Plan
+    nJ: int
+    n_det: int
+    n_union: int
+    det_idx: torch.Tensor          # int32 [n_det] (device)
+    union_idx: torch.Tensor        # int32 [n_union]
+    theta2: float | None = None
+    coef: torch.Tensor | None = None       # fp64 [G_loc][n_det][2]
+    lstar: torch.Tensor | None = None
+    iters: torch.Tensor | None = None
+    times: dict = field(default_factory=dict)
+
+
+class Detector:
+    """One usFFT detection run (Steps 1-2 of Alg. 1) for a workload preset (usfft_inputs)."""
+
+    def __init__(self, cfg: dict, device: int = 0, group=None, maxit: int = 20000,
+                 timing: bool = False, blackbox=None):
+        """blackbox: optional callable (detector, plan, b0, nb) -> fp64 CUDA tensor [G][nb]
+        replacing the PDE sampler (Alg. 1 takes any black box); cfg["G"] then gives G."""
+        self.cfg = cfg
+        self.blackbox = blackbox
+        self.dev = torch.device("cuda", device)
+        self.ctx = B.Context(device)
+        self.pde = B.pde_desc(cfg, maxit=maxit, tol=cfg.get("cg_tol", 1e-12)) if blackbox is None else None
+        self.ex = Exchange(group)
+        self.P, self.rank = self.ex.P, self.ex.rank
+        self.G = cfg["G"] if blackbox is not None else (cfg["n"] - 1) ** 2
+        self.g0, self.g1 = partition(self.G, self.P, self.rank)
+        self.G_loc = self.g1 - self.g0
+        self.timing = timing
+        self.n_samples = 0
+
+    # ------------------------------------------------------------------------------------------
+    def round(self, step: int, t: int, i: int, I_prev: torch.Tensor, n_prev: int,
+              kt: torch.Tensor, s_tilde: int, flags: torch.Tensor, want_coef: bool = False,
+              keep_iters: bool = False) -> RoundResult:
+        cfg, ctx, dev = self.cfg, self.ctx, self.dev
+        n1 = int(kt.numel())
+        nJ = n_prev * n1
+        ev = {}
+
+        def mark(name):
+            if self.timing:
+                e = torch.cuda.Event(enable_timing=True)
+                e.record(ctx.stream)
+                ev[name] = e
+
+        mark("start")
+        plan = B.usfft_plan_round(ctx, cfg["seed"], step, t, i, cfg["d"], cfg["N"], s_tilde,
+                                  cfg.get("mode", "A") if step == 2 else "A", nJ,
+                                  I_prev if t > 1 else None, n_prev, kt)
+        L, M = plan.L, plan.M
+        Btot = L * M
+        bins = torch.empty((L, nJ), dtype=torch.int32, device=dev)
+        B.usfft_lattice(ctx, plan, 0, 0, None, I_prev if plan.t_z > 1 else None, n_prev, kt, bins)
+        # this rank's samples
+        b0, b1 = partition(Btot, self.P, self.rank)
+        nb = b1 - b0
+        u = torch.empty((self.G, nb), dtype=torch.float64, device=dev)
+        iters = torch.empty(nb, dtype=torch.int32, device=dev) if keep_iters else None
+        mark("plan")
+        if nb and self.blackbox is not None:
+            u = self.blackbox(self, plan, b0, nb)
+        elif nb:
+            B.usfft_sample_pde(ctx, self.pde, plan, b0, nb, u, nb, None, iters)
+        self.n_samples += Btot
+        mark("pde")
+        slabs, sb = self.ex.transpose(u, self.G, Btot)
+        mark("exchange")
+        Mh = M // 2 + 1
+        spectra = torch.empty((self.G_loc, L, Mh, 2), dtype=torch.float64, device=dev)
+        kmin = torch.empty((self.G_loc, nJ), dtype=torch.float64, device=dev)
+        kmax = torch.zeros(1, dtype=torch.float64, device=dev)
+        B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, nJ, spectra, kmin, kmax)
+        mark("fft")
+        self.ex.max_(kmax)
+        votes = torch.empty(nJ, dtype=torch.int32, device=dev)
+        det_g = torch.empty((self.G_loc, s_tilde), dtype=torch.int32, device=dev)
+        n_det_g = torch.empty(self.G_loc, dtype=torch.int32, device=dev)
+        th2 = torch.empty(1, dtype=torch.float64, device=dev)
+        B.usfft_detect_select(ctx, self.G_loc, nJ, kmin, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
+                              cfg.get("theta_abs", 0.0), votes, det_g, n_det_g, th2)
+        self.ex.sum_(votes)
+        det_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
+        union_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
+        n_det, n_union = B.usfft_detect_union(ctx, nJ, votes, flags, det_idx, union_idx)
+        mark("detect")
+        res = RoundResult(plan, nJ, n_det, n_union, det_idx[:n_det], union_idx[:n_union])
+        res.iters = iters
+        if want_coef and n_det > 0:
+            coef = torch.empty((self.G_loc, n_det, 2), dtype=torch.float64, device=dev)
+            lstar = torch.empty((self.G_loc, n_det), dtype=torch.int32, device=dev)
+            B.usfft_resolve(ctx, plan, self.G_loc, spectra, bins, nJ, det_g, n_det_g, s_tilde,
+                            det_idx, n_det, coef, lstar)
+            res.coef, res.lstar = coef, lstar
+        mark("resolve")
+        res.theta2 = th2
+        if self.timing:
+            torch.cuda.synchronize(dev)
+            names = list(ev)
+            res.times = {names[k]: ev[names[k - 1]].elapsed_time(ev[names[k]]) for k in range(1, len(names))}
+        # debugging/parity handles
+        res.bins, res.kappa_min, res.spectra, res.votes, res.det_g, res.n_det_g = bins, kmin, spectra, votes, det_g, n_det_g
+        res.kappa_max, res.u, res.slab_b0 = kmax, u, sb
+        return res
+
+    # ------------------------------------------------------------------------------------------
+    def step1(self, log: list | None = None) -> list[torch.Tensor]:
+        """Step 1 & 2a: I^(t) for t = 1..d as device int16 vectors."""
+        cfg, dev = self.cfg, self.dev
+        N, d, r = cfg["N"], cfg["d"], cfg["r"]
+        kt = torch.arange(-N, N + 1, dtype=torch.int16, device=dev)
+        empty = torch.zeros(1, dtype=torch.int16, device=dev)
+        out = []
+        for t in range(1, d + 1):
+            flags = torch.zeros(kt.numel(), dtype=torch.uint8, device=dev)
+            res = None
+            for i in range(1, r + 1):
+                res = self.round(1, t, i, empty, 1, kt, cfg["s_local"], flags)
+                if log is not None:
+                    log.append(dict(step=1, t=t, i=i, M=res.plan.M, B=res.plan.M, nJ=res.nJ, n_det=res.n_det))
+            n_u = res.n_union
+            if n_u == 0:
+                out.append(torch.zeros(1, dtype=torch.int16, device=dev))             # Z9
+                continue
+            rows = torch.empty((n_u, 1), dtype=torch.int16, device=dev)
+            B.usfft_gather_rows(self.ctx, res.union_idx, n_u, None, 1, kt, rows)
+            out.append(rows.reshape(-1))
+        return out
+
+    def step2(self, I1d: list[torch.Tensor], log: list | None = None, t_stop: int | None = None):
+        """Step 2: returns (I^(1..d) int16 [nI][d] device, coef [G_loc][nI][2])."""
+        cfg, dev, ctx = self.cfg, self.dev, self.ctx
+        d, r = cfg["d"], cfg["r"]
+        I_prev = I1d[0].reshape(-1, 1).contiguous()
+        coef = None
+        t_end = d if t_stop is None else t_stop
+        for t in range(2, t_end + 1):
+            r_t, s_t = (r, cfg["s_local"]) if t < d else (1, cfg["s"])
+            kt = I1d[t - 1]
+            n_prev = I_prev.shape[0]
+            nJ = n_prev * int(kt.numel())
+            flags = torch.zeros(nJ, dtype=torch.uint8, device=dev)
+            res = None
+            for i in range(1, r_t + 1):
+                res = self.round(2, t, i, I_prev, n_prev, kt, s_t, flags, want_coef=(t == d))
+                if log is not None:
+                    log.append(dict(step=2, t=t, i=i, M=res.plan.M, L=res.plan.L,
+                                    B=res.plan.M * res.plan.L, nJ=nJ, n_det=res.n_det))
+            n_u = res.n_union
+            rows = torch.empty((max(n_u, 1), t), dtype=torch.int16, device=dev)
+            if n_u:
+                B.usfft_gather_rows(ctx, res.union_idx, n_u, I_prev if t > 1 else None, t, kt, rows)
+            I_prev = rows[:n_u].contiguous()
+            if t == d:
+                coef = res.coef
+            if n_u == 0:
+                return I_prev, None
+        return I_prev, coef
+
+    def run(self, log: list | None = None):
+        I1d = self.step1(log)
+        return self.step2(I1d, log)
+
+
+def to_numpy_rows(I: torch.Tensor) -> np.ndarray:
+    return I.to("cpu").numpy().astype(np.int64)
