@@ -325,7 +325,7 @@ def test_full_run_trig_poly_matches_oracle(B, mode):
 def test_full_run_pde_config1(B):
     """Config 1 (mode A for runtime): GPU Alg. 1 vs oracle Alg. 1 on the PDE black box."""
     from paper_2109_04131_b200.driver import Detector
-    from tests.parity import compare_round
+    from parity import compare_round
     cfg = config(1, mode="A")
     det = Detector(cfg)
     log_g = []

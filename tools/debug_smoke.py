@@ -41,3 +41,16 @@ c = res.coef.cpu().numpy(); cg = c[..., 0] + 1j * c[..., 1]
 d = np.abs(cg - ref["coef"]); g, q = np.unravel_index(d.argmax(), d.shape)
 print("coef max diff", d.max(), "at", g, q, "rel", d.max() / np.abs(ref["coef"]).max(), "lstar", ls[g, q], ref["lstar"][g, q], cg[g, q], ref["coef"][g, q])
 Vg = np.abs(V).max(); print("max|V|", Vg)
+
+km_ref = ref["kappa_min"]
+dd = np.abs(np.sqrt(km) - np.sqrt(km_ref)); g, k = np.unravel_index(dd.argmax(), dd.shape)
+print("worst kappa at g,k", g, k, "gpu", km[g, k], "oracle", km_ref[g, k])
+Vg = odft.round_values(U, p.M, p.L, bins)          # oracle DFT of the GPU samples (diagnostic only)
+kg = odet.kappa_min(Vg)
+print("oracle-DFT-of-GPU-u vs GPU kappa:", np.abs(np.sqrt(kg) - np.sqrt(km)).max() / np.sqrt(km_ref.max()))
+print("oracle-DFT-of-GPU-u vs oracle kappa:", np.abs(np.sqrt(kg) - np.sqrt(km_ref)).max() / np.sqrt(km_ref.max()))
+sp = res.spectra.cpu().numpy(); Mh = p.M // 2 + 1
+full = np.stack([odft.lattice_dft(U[:, l * p.M:(l + 1) * p.M], p.M, np.arange(Mh)) for l in range(p.L)], 1)
+print("spectra err", np.abs((sp[..., 0] + 1j * sp[..., 1]) / p.M - full).max() / np.abs(full).max())
+kk = odet.kappa(V)
+print("per-lattice kappa at worst:", kk[:, g, k], "bins", bins[:, k])
