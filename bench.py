@@ -135,7 +135,7 @@ def run_ours(args):
     clocks = ClockSampler(local)
     clocks.start()
     launches0 = det.ctx.launches()
-    step_ms, phase, iters_sum, samples, rounds = [], {}, 0, 0, []
+    step_ms, phase, iters_sum, samples = [], {}, 0, 0
     for k in range(args.steps):
         flush.fill_(float(k))                         # evict L2 between timed iterations
         torch.cuda.synchronize()
@@ -147,11 +147,13 @@ def run_ours(args):
         e1.record(stream)
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
+        if args.verbose:
+            print(f"step {k}: {step_ms[-1]:.3f} ms " + " ".join(f"{a}={b:.3f}" for a, b in res.times.items()),
+                  file=sys.stderr, flush=True)
         for name, ms in res.times.items():
             phase[name] = phase.get(name, 0.0) + ms
         iters_sum += int(res.iters.sum().item()) if res.iters is not None and res.iters.numel() else 0
         samples += res.plan.L * res.plan.M
-        rounds.append(res)
     launches = det.ctx.launches() - launches0
     clk = clocks.stop()
     total_ms = float(np.sum(step_ms))
@@ -312,6 +314,7 @@ def main():
     ap.add_argument("--t", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
+    ap.add_argument("--verbose", action="store_true")
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

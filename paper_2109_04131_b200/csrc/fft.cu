@@ -8,6 +8,10 @@
 // kappa_l = fl(fl(re*re) + fl(im*im)) (no FMA contraction, Z5), kappa_min = min over l (Z1);
 // the max over (g, j) of kappa_min is accumulated with an integer atomicMax on the bit pattern
 // (non-negative doubles order like uint64), so it is exact and order-independent.
+#include <cmath>
+#include <cstdlib>
+#include <vector>
+
 #include "common.cuh"
 
 namespace usfft {
@@ -98,7 +102,117 @@ __global__ void k_kappa(const double2 *__restrict__ F, const int32_t *__restrict
 
 }  // namespace usfft
 
+#include "rader.cuh"
+
 using namespace usfft;
+
+namespace {
+
+bool is_prime64(int64_t n) {
+    if (n < 2) return false;
+    if (n % 2 == 0) return n == 2;
+    for (int64_t f = 3; f * f <= n; f += 2)
+        if (n % f == 0) return false;
+    return true;
+}
+
+int64_t powmod(int64_t b, int64_t e, int64_t m) {
+    int64_t r = 1 % m;
+    b %= m;
+    while (e > 0) {
+        if (e & 1) r = (r * b) % m;
+        b = (b * b) % m;
+        e >>= 1;
+    }
+    return r;
+}
+
+// Rader plan for prime M with 7-smooth M-1 (nullptr-equivalent plan.M == 0 otherwise)
+usfft_status get_rader(usfft_ctx *c, int64_t M, RaderPlan *out) {
+    static thread_local std::map<std::pair<usfft_ctx *, int64_t>, RaderPlan> cache;
+    auto key = std::make_pair(c, M);
+    auto it = cache.find(key);
+    if (it != cache.end()) {
+        *out = it->second;
+        return USFFT_OK;
+    }
+    RaderPlan P;
+    const int64_t N = M - 1;
+    int64_t rem = N;
+    int ns = 0;
+    if (M >= 5 && is_prime64(M)) {
+        for (int r : {4, 2, 3, 5, 7})
+            while (rem % r == 0 && ns < 32) {
+                P.radix[ns++] = r;
+                rem /= r;
+            }
+    }
+    if (rem != 1 || M < 5 || !is_prime64(M)) {          // not Rader-able: caller falls back
+        cache[key] = P;
+        *out = P;
+        return USFFT_OK;
+    }
+    P.M = M;
+    P.N = N;
+    P.nstage = ns;
+    // primitive root: g^(N/f) != 1 for every prime factor f of N
+    int64_t gp = 2;
+    for (;; ++gp) {
+        bool ok = true;
+        for (int64_t f : {2, 3, 5, 7})
+            if (N % f == 0 && powmod(gp, N / f, M) == 1) ok = false;
+        if (ok) break;
+    }
+    const int64_t ginv = powmod(gp, N - 1, M);
+    std::vector<int32_t> perm(N), outidx(N);
+    int64_t a = 1, bq = 1;
+    for (int64_t k = 0; k < N; ++k) {
+        perm[k] = (int32_t)a;
+        outidx[k] = (int32_t)bq;
+        a = (a * gp) % M;
+        bq = (bq * ginv) % M;
+    }
+    const long double PI = 3.141592653589793238462643383279502884L;
+    std::vector<long double> cN(N), sN(N);
+    for (int64_t k = 0; k < N; ++k) {
+        cN[k] = cosl(2.0L * PI * (long double)k / (long double)N);
+        sN[k] = sinl(2.0L * PI * (long double)k / (long double)N);
+    }
+    std::vector<double2> tw(N), bf(N);
+    for (int64_t k = 0; k < N; ++k) tw[k] = make_double2((double)cN[k], (double)-sN[k]);
+    // b_n = e^{-2 pi i g^{-n}/M};  Bf[k] = (1/N) sum_n b_n e^{-2 pi i n k / N}  (long double)
+    std::vector<long double> br(N), bi(N);
+    for (int64_t n = 0; n < N; ++n) {
+        const long double ang = 2.0L * PI * (long double)outidx[n] / (long double)M;
+        br[n] = cosl(ang);
+        bi[n] = -sinl(ang);
+    }
+    for (int64_t k = 0; k < N; ++k) {
+        long double re = 0.0L, im = 0.0L;
+        int64_t idx = 0;
+        for (int64_t n = 0; n < N; ++n) {
+            // (br + i bi) (cN[idx] - i sN[idx])
+            re += br[n] * cN[idx] + bi[n] * sN[idx];
+            im += bi[n] * cN[idx] - br[n] * sN[idx];
+            idx += k;
+            if (idx >= N) idx -= N;
+        }
+        bf[k] = make_double2((double)(re / (long double)N), (double)(im / (long double)N));
+    }
+    USFFT_CUDA(c, cudaMalloc(&P.tw, sizeof(double2) * N));
+    USFFT_CUDA(c, cudaMalloc(&P.bf, sizeof(double2) * N));
+    USFFT_CUDA(c, cudaMalloc(&P.perm, sizeof(int32_t) * N));
+    USFFT_CUDA(c, cudaMalloc(&P.outidx, sizeof(int32_t) * N));
+    USFFT_CUDA(c, cudaMemcpy(P.tw, tw.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
+    USFFT_CUDA(c, cudaMemcpy(P.bf, bf.data(), sizeof(double2) * N, cudaMemcpyHostToDevice));
+    USFFT_CUDA(c, cudaMemcpy(P.perm, perm.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    USFFT_CUDA(c, cudaMemcpy(P.outidx, outidx.data(), sizeof(int32_t) * N, cudaMemcpyHostToDevice));
+    cache[key] = P;
+    *out = P;
+    return USFFT_OK;
+}
+
+}  // namespace
 
 static usfft_status get_twiddles(usfft_ctx *c, int64_t M, double2 **out) {
     auto it = c->twiddles.find(M);
@@ -132,7 +246,6 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
     USFFT_REQUIRE(c, G_loc == 0 || (u && spectra), "u / spectra NULL");
     USFFT_REQUIRE(c, nJ == 0 || G_loc == 0 || (bins && kappa_min), "bins / kappa_min NULL");
     const size_t smem = sizeof(double) * (size_t)((M + 1) & ~int64_t(1)) + sizeof(double2) * (size_t)M;
-    USFFT_REQUIRE(c, smem <= c->smem_optin, "M = %lld too large for the direct DFT", (long long)M);
     SlabParams S;
     S.nslab = nslab;
     for (int p = 0; p <= nslab; ++p) S.b0[p] = slab_b0[p];
@@ -142,11 +255,34 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
     double2 *tw = nullptr;
     usfft_status s = get_twiddles(c, M, &tw);
     if (s) return s;
-    USFFT_CUDA(c, cudaFuncSetAttribute(k_dft_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const int64_t rows = G_loc * L;
-    k_dft_direct<<<(unsigned)rows, 256, smem, c->stream>>>(u, S, G_loc, M, L, tw,
-                                                            reinterpret_cast<double2 *>(spectra));
-    USFFT_CHECK_LAUNCH(c);
+    RaderPlan R;
+    s = get_rader(c, M, &R);
+    if (s) return s;
+    const char *force = getenv("USFFT_DFT");
+    const size_t smem_r = sizeof(double) * (size_t)((M + 1) & ~int64_t(1)) + 2 * sizeof(double2) * (size_t)(M - 1);
+    if (R.M == M && smem_r <= c->smem_optin && !(force && force[0] == 'd')) {
+        RaderArgs A;
+        A.M = R.M;
+        A.N = R.N;
+        A.nstage = R.nstage;
+        for (int k = 0; k < 32; ++k) A.radix[k] = R.radix[k];
+        A.tw = R.tw;
+        A.perm = R.perm;
+        A.outidx = R.outidx;
+        A.bf = R.bf;
+        USFFT_CUDA(c, cudaFuncSetAttribute(k_fft_rader, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+        const int threads = M <= 512 ? 128 : 256;
+        k_fft_rader<<<(unsigned)rows, threads, smem_r, c->stream>>>(u, S, G_loc, L, A,
+                                                                     reinterpret_cast<double2 *>(spectra));
+        USFFT_CHECK_LAUNCH(c);
+    } else {
+        USFFT_REQUIRE(c, smem <= c->smem_optin, "M = %lld too large for the direct DFT", (long long)M);
+        USFFT_CUDA(c, cudaFuncSetAttribute(k_dft_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        k_dft_direct<<<(unsigned)rows, 256, smem, c->stream>>>(u, S, G_loc, M, L, tw,
+                                                                reinterpret_cast<double2 *>(spectra));
+        USFFT_CHECK_LAUNCH(c);
+    }
     if (nJ > 0) {
         unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
         if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);

@@ -355,3 +355,42 @@ def test_eval_parity(B, ctx):
     B.usfft_eval(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), U)
     ref = oeval.evaluate(I, Cc, Y).real
     assert np.abs(U.cpu().numpy() - ref).max() <= 1e-11 * np.abs(Cc).sum(1).max()
+
+
+# ------------------------------------------------------------------------------ kernel variants
+def test_fft_variants_agree(B, ctx, monkeypatch):
+    """Rader/Stockham FFT (default for prime M with 7-smooth M-1) vs the direct DFT kernel."""
+    from paper_2109_04131_b200.binding import Plan
+    for G, M, L in ((5, 401, 3), (2, 4001, 2), (4, 97, 5)):
+        U, z, J, bins = _round_inputs(M, G, M, L, 64)
+        p = Plan(3, M, L, 3, -1, z, np.zeros(3))
+        Mh = M // 2 + 1
+        out = []
+        for mode in ("rader", "direct"):
+            monkeypatch.setenv("USFFT_DFT", mode)
+            sp = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
+            km = torch.empty((G, 64), dtype=torch.float64, device="cuda")
+            kx = torch.empty(1, dtype=torch.float64, device="cuda")
+            B.usfft_lattice_fft(ctx, p, G, dev(U, torch.float64), [0, L * M], dev(bins, torch.int32), 64, sp, km, kx)
+            out.append(sp.cpu().numpy())
+        monkeypatch.delenv("USFFT_DFT")
+        ref = np.stack([odft.lattice_dft(U[:, l * M:(l + 1) * M], M, np.arange(Mh)) for l in range(L)], 1) * M
+        for o in out:
+            assert np.abs(o[..., 0] + 1j * o[..., 1] - ref).max() <= 1e-12 * np.abs(ref).max()
+
+
+def test_pcg_variants_agree(B, ctx, monkeypatch):
+    """Register-resident PCG (default for n-1 <= 31) and the shared-memory PCG both meet the
+    oracle tolerance on the same samples."""
+    for cfgid in (1, 2):
+        cfg = config(cfgid)
+        p = B.usfft_plan_round(ctx, cfg["seed"], 2, 4, 2, cfg["d"], cfg["N"], cfg["s"], "A", 300)
+        nb, G = 24, (cfg["n"] - 1) ** 2
+        Y = olat.nodes(p.M, p.z, p.shift, 4)[:, 5:5 + nb]
+        ref = ofe.sample_pde(cfg, Y)
+        for mode in ("reg", "smem"):
+            monkeypatch.setenv("USFFT_PCG", mode)
+            u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
+            assert B.usfft_sample_pde(ctx, B.pde_desc(cfg), p, 5, nb, u, nb, check_conv=True) == 0
+            assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
+        monkeypatch.delenv("USFFT_PCG")
