@@ -134,6 +134,7 @@ def run_ours(args):
         dist.barrier()
     clocks = ClockSampler(local)
     clocks.start()
+    torch.cuda.cudart().cudaProfilerStart()          # ncu --profile-from-start off: timed steps only
     launches0 = det.ctx.launches()
     step_ms, phase, iters_sum, samples = [], {}, 0, 0
     for k in range(args.steps):
@@ -155,6 +156,7 @@ def run_ours(args):
         iters_sum += int(res.iters.sum().item()) if res.iters is not None and res.iters.numel() else 0
         samples += res.plan.L * res.plan.M
     launches = det.ctx.launches() - launches0
+    torch.cuda.cudart().cudaProfilerStop()
     clk = clocks.stop()
     total_ms = float(np.sum(step_ms))
     t_tensor = torch.tensor([total_ms, phase.get("pde", 0.0)], dtype=torch.float64, device="cuda")

@@ -142,7 +142,7 @@ usfft_status get_rader(usfft_ctx *c, int64_t M, RaderPlan *out) {
     int ns = 0;
     if (M >= 5 && is_prime64(M)) {
         for (int r : {4, 2, 3, 5, 7})
-            while (rem % r == 0 && ns < 32) {
+            while (rem % r == 0 && ns < 16) {
                 P.radix[ns++] = r;
                 rem /= r;
             }
@@ -266,7 +266,8 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         A.M = R.M;
         A.N = R.N;
         A.nstage = R.nstage;
-        for (int k = 0; k < 32; ++k) A.radix[k] = R.radix[k];
+        A.radix_code = 0;
+        for (int k = 0; k < R.nstage && k < 16; ++k) A.radix_code |= (uint64_t)R.radix[k] << (4 * k);
         A.tw = R.tw;
         A.perm = R.perm;
         A.outidx = R.outidx;

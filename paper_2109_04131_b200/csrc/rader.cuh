@@ -24,7 +24,7 @@ struct RaderPlan {
 struct RaderArgs {
     int64_t M, N;
     int nstage;
-    int radix[32];
+    uint64_t radix_code;        // radix of stage st in bits [4st, 4st+4)
     const double2 *tw;
     const int32_t *perm;
     const int32_t *outidx;
@@ -51,44 +51,42 @@ __device__ __forceinline__ void stockham_stage(const double2 *__restrict__ in, d
             const double2 a = in[j + r * nbf];
             v[r] = r == 0 ? a : cmul(a, __ldg(tw + (r * jm * tstep) % N));
         }
-        double2 y[R];
+        const int base = (j / Ns) * Ns * R + jm;
         if (R == 2) {
-            y[0] = cadd(v[0], v[1]);
-            y[1] = csub(v[0], v[1]);
+            out[base] = cadd(v[0], v[1]);
+            out[base + Ns] = csub(v[0], v[1]);
         } else if (R == 4) {
             const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
             const double2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
-            y[0] = cadd(s02, s13);
-            y[2] = csub(s02, s13);
-            y[1] = make_double2(d02.x + d13.y, d02.y - d13.x);     // d02 - i d13
-            y[3] = make_double2(d02.x - d13.y, d02.y + d13.x);     // d02 + i d13
+            out[base] = cadd(s02, s13);
+            out[base + 2 * Ns] = csub(s02, s13);
+            out[base + Ns] = make_double2(d02.x + d13.y, d02.y - d13.x);        // d02 - i d13
+            out[base + 3 * Ns] = make_double2(d02.x - d13.y, d02.y + d13.x);    // d02 + i d13
         } else {
             const int wR = N / R;
 #pragma unroll
-            for (int s = 0; s < R; ++s) {
+            for (int s2 = 0; s2 < R; ++s2) {
                 double2 acc = v[0];
 #pragma unroll
-                for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], __ldg(tw + ((r * s) % R) * wR)));
-                y[s] = acc;
+                for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], __ldg(tw + ((r * s2) % R) * wR)));
+                out[base + s2 * Ns] = acc;
             }
         }
-        const int base = (j / Ns) * Ns * R + jm;
-#pragma unroll
-        for (int s = 0; s < R; ++s) out[base + s * Ns] = y[s];
     }
 }
 
-// forward FFT_N of buf[0] in place over the stage list; returns the buffer holding the result
-__device__ __forceinline__ double2 *fft_stockham(double2 *b0, double2 *b1, const RaderArgs &A) {
+// forward FFT_N of b0 over the stage list (ping-pong with b1); returns the buffer with the result
+__device__ __forceinline__ double2 *fft_stockham(double2 *b0, double2 *b1, int N, int nstage,
+                                                 uint64_t code, const double2 *__restrict__ tw) {
     int Ns = 1;
     double2 *in = b0, *out = b1;
-    for (int st = 0; st < A.nstage; ++st) {
-        const int R = A.radix[st];
-        if (R == 4) stockham_stage<4>(in, out, (int)A.N, Ns, A.tw);
-        else if (R == 2) stockham_stage<2>(in, out, (int)A.N, Ns, A.tw);
-        else if (R == 3) stockham_stage<3>(in, out, (int)A.N, Ns, A.tw);
-        else if (R == 5) stockham_stage<5>(in, out, (int)A.N, Ns, A.tw);
-        else stockham_stage<7>(in, out, (int)A.N, Ns, A.tw);
+    for (int st = 0; st < nstage; ++st) {
+        const int R = (int)((code >> (4 * st)) & 15u);
+        if (R == 4) stockham_stage<4>(in, out, N, Ns, tw);
+        else if (R == 2) stockham_stage<2>(in, out, N, Ns, tw);
+        else if (R == 3) stockham_stage<3>(in, out, N, Ns, tw);
+        else if (R == 5) stockham_stage<5>(in, out, N, Ns, tw);
+        else stockham_stage<7>(in, out, N, Ns, tw);
         __syncthreads();
         Ns *= R;
         double2 *t = in;
@@ -120,7 +118,7 @@ k_fft_rader(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int
     const double x0 = xs[0];
     for (int64_t p = threadIdx.x; p < N; p += blockDim.x) b0[p] = make_double2(xs[__ldg(A.perm + p)], 0.0);
     __syncthreads();
-    double2 *Ahat = fft_stockham(b0, b1, A);
+    double2 *Ahat = fft_stockham(b0, b1, (int)N, A.nstage, A.radix_code, A.tw);
     double2 *other = Ahat == b0 ? b1 : b0;
     // pointwise product with FFT(b)/N, conjugated for the inverse transform
     for (int64_t k = threadIdx.x; k < N; k += blockDim.x) {
@@ -128,7 +126,7 @@ k_fft_rader(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int
         Ahat[k] = make_double2(c.x, -c.y);
     }
     __syncthreads();
-    double2 *conv = fft_stockham(Ahat, other, A);     // conj of the cyclic convolution
+    double2 *conv = fft_stockham(Ahat, other, (int)N, A.nstage, A.radix_code, A.tw);     // conj of the cyclic convolution
     double2 *stage_out = conv == b0 ? b1 : b0;
     // X[g^{-q}] = x0 + conv[q]; stage bins <= M/2 in natural order, then store coalesced
     for (int64_t q = threadIdx.x; q < N; q += blockDim.x) {
