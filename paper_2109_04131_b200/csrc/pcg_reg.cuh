@@ -9,7 +9,7 @@
 //     beta = gamma/gamma_old, alpha = gamma/(delta - beta*gamma/alpha_old)
 //     p = r^ + beta p;  s = w + beta s;  x^ += alpha p;  r^ -= alpha s
 // stopping on the true-residual recurrence ||r||_2 <= tol ||b||_2 (Z13).  Per iteration: one CTA
-// barrier for the vertical halo, one fixed-tree reduction.  Mapping: a thread owns a BC x BR block
+// barrier (shared by the reduction and the vertical halo, see the loop comment).  Mapping: a thread owns a BC x BR block
 // of nodes (BC columns, BR rows); LX threads of a warp segment cover a row of blocks and exchange
 // left/right neighbours by width-LX shuffles; row groups exchange their edge rows via shared
 // memory.  All edge weights, the diagonal and the four CG vectors live in registers.
@@ -17,7 +17,7 @@
 
 namespace usfft {
 
-template <int BC, int BR, int LX, int NWARP>
+template <int NC, int BC, int BR, int LX, int NWARP>
 __global__ void __launch_bounds__(NWARP * 32, 3)
 k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
           int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
@@ -26,12 +26,11 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
     constexpr int NRG = NWARP * RGW;             // row groups per CTA
     constexpr int NCOL = LX * BC;                // covered columns
     extern __shared__ double sm[];
-    __shared__ double red[3][NWARP];
+    __shared__ double red[2][4][NWARP];          // [parity][gamma, delta, rho, pad][warp]
     __shared__ double th_amp[kMaxD];
-    __shared__ double topv[NRG][NCOL];           // each row group's top row of r^
-    __shared__ double botv[NRG][NCOL];           // each row group's bottom row of r^
+    __shared__ double4 halo[2][2][NRG][NCOL];    // [parity][top, bottom row][row group][col]
 
-    const int n = Q.n, nx = n - 1, np = n + 1, W = 3 * n + 1;
+    constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1;   // NC = cells per side (== Q.n)
     double *aT = sm;                             // [2 n^2] coefficient at triangle centroids
     double *dg = sm + 2 * n * n;                 // [(n+1)^2] diagonal of A (padded)
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -66,7 +65,8 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         }
         __syncthreads();
         // ---- per-thread state --------------------------------------------------------------
-        double d[BR][BC], x[BR][BC], r[BR][BC], p[BR][BC], s[BR][BC];
+        double x[BR][BC], r[BR][BC], p[BR][BC], s[BR][BC];
+        const double *dgb = dg + (row0 + 1) * np + col0 + 1;   // diagonal of node (q, c): dgb[q*np + c]
         double wE[BR][BC + 1];                   // -w^ of the edge right of column c-1 (c=0: left edge)
         double wN[BR + 1][BC];                   // -w^ of the edge above row k-1 (k=0: bottom edge)
 #pragma unroll
@@ -75,11 +75,10 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             for (int c = 0; c < BC; ++c) {
                 const int i = col0 + c + 1, j = row0 + k + 1;
                 const bool ok = i <= nx && j <= nx;
-                d[k][c] = ok ? dg[j * np + i] : 1.0;
                 x[k][c] = 0.0;
                 p[k][c] = 0.0;
                 s[k][c] = 0.0;
-                r[k][c] = ok ? ((double)j * inv_n3) / sqrt(d[k][c]) : 0.0;      // b^ = D^-1/2 b
+                r[k][c] = ok ? ((double)j * inv_n3) / sqrt(dg[j * np + i]) : 0.0;      // b^ = D^-1/2 b
             }
 #pragma unroll
         for (int k = 0; k < BR; ++k)
@@ -103,91 +102,115 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             }
 #undef WH
 #undef WV
-        double bb = 0.0;                          // ||b||^2 = sum d r^^2 at start (reduced below)
-        double gamma_old = 1.0, alpha_old = 1.0, rho = 0.0;
-        int it = 0;
-        bool first = true;
-        while (true) {
-            // ---- halo: own edge rows to shared memory, horizontal neighbours by shuffle -----
+        // Iteration k (k = 0, 1, ...):  w_k = A^ r_k; one reduction -> gamma_k, delta_k, rho_k;
+        // beta_k = gamma_k / gamma_{k-1}, alpha_k = gamma_k / (delta_k - gamma_k^2 / (gamma_{k-1}
+        // alpha_{k-1})); then s_k = w_k + beta_k s_{k-1}, p_k = r_k + beta_k p_{k-1},
+        // x += alpha_k p_k, r_{k+1} = r_k - alpha_k s_k.  The vertical halo needs r_{k+1} of the
+        // neighbouring row groups: each thread publishes (r_k, w_k, s_{k-1}) of its edge rows
+        // before the reduction barrier and every reader recomputes the neighbour's s_k and
+        // r_{k+1} with the same fma sequence, so one barrier per iteration suffices (the halo
+        // and partial-sum buffers alternate by iteration parity).
+        double rho = 0.0, bb = 0.0;
+        double g_inv = 0.0, ga_inv = 0.0;        // 1/gamma_{k-1}, 1/(gamma_{k-1} alpha_{k-1})
+        double below[BC], above[BC];             // neighbour r_k on the rows below/above
 #pragma unroll
-            for (int c = 0; c < BC; ++c) {
-                topv[rg][col0 + c] = r[BR - 1][c];
-                botv[rg][col0 + c] = r[0][c];
-            }
+        for (int c = 0; c < BC; ++c) {           // r_0 of the neighbouring rows: b^ there
+            const int i = col0 + c + 1;
+            const int jb = row0, ja = row0 + BR + 1;
+            below[c] = (jb >= 1 && i <= nx && rg > 0) ? ((double)jb * inv_n3) / sqrt(dg[jb * np + i]) : 0.0;
+            above[c] = (ja <= nx && i <= nx && rg + 1 < NRG) ? ((double)ja * inv_n3) / sqrt(dg[ja * np + i]) : 0.0;
+        }
+        int it = 0;
+        for (int k = 0;; ++k) {
+            const int buf = k & 1;
+            // ---- horizontal halo by shuffle, w = A^ r^ and the three partial dots ------------
             double left[BR], right[BR];
 #pragma unroll
-            for (int k = 0; k < BR; ++k) {
-                left[k] = __shfl_up_sync(0xffffffffu, r[k][BC - 1], 1, LX);
-                right[k] = __shfl_down_sync(0xffffffffu, r[k][0], 1, LX);
+            for (int q = 0; q < BR; ++q) {
+                left[q] = __shfl_up_sync(0xffffffffu, r[q][BC - 1], 1, LX);
+                right[q] = __shfl_down_sync(0xffffffffu, r[q][0], 1, LX);
             }
-            __syncthreads();
-            double below[BC], above[BC];
-#pragma unroll
-            for (int c = 0; c < BC; ++c) {
-                below[c] = rg > 0 ? topv[rg - 1][col0 + c] : 0.0;
-                above[c] = rg + 1 < NRG ? botv[rg + 1][col0 + c] : 0.0;
-            }
-            // ---- w = A^ r^ and the three partial dots ---------------------------------------
-            double acc[3] = {0.0, 0.0, 0.0};     // gamma, delta, rho
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};    // gamma, delta, rho, (pad)
             double w[BR][BC];
 #pragma unroll
-            for (int k = 0; k < BR; ++k)
+            for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    const double rl = c > 0 ? r[k][c - 1] : left[k];
-                    const double rr = c + 1 < BC ? r[k][c + 1] : right[k];
-                    const double rd = k > 0 ? r[k - 1][c] : below[c];
-                    const double ru = k + 1 < BR ? r[k + 1][c] : above[c];
-                    double v = fma(wE[k][c + 1], rr, r[k][c]);
-                    v = fma(wE[k][c], rl, v);
-                    v = fma(wN[k + 1][c], ru, v);
-                    v = fma(wN[k][c], rd, v);
-                    w[k][c] = v;
-                    acc[0] = fma(r[k][c], r[k][c], acc[0]);
-                    acc[1] = fma(v, r[k][c], acc[1]);
-                    acc[2] = fma(d[k][c] * r[k][c], r[k][c], acc[2]);
+                    const double rl = c > 0 ? r[q][c - 1] : left[q];
+                    const double rr = c + 1 < BC ? r[q][c + 1] : right[q];
+                    const double rd = q > 0 ? r[q - 1][c] : below[c];
+                    const double ru = q + 1 < BR ? r[q + 1][c] : above[c];
+                    double v = fma(wE[q][c + 1], rr, r[q][c]);
+                    v = fma(wE[q][c], rl, v);
+                    v = fma(wN[q + 1][c], ru, v);
+                    v = fma(wN[q][c], rd, v);
+                    w[q][c] = v;
+                    acc[0] = fma(r[q][c], r[q][c], acc[0]);
+                    acc[1] = fma(v, r[q][c], acc[1]);
+                    acc[2] = fma(dgb[q * np + c] * r[q][c], r[q][c], acc[2]);   // padded: r = 0
                 }
-            // ---- one fixed-tree block reduction ----------------------------------------------
+            // ---- publish the edge rows (r_k, w_k, s_{k-1}) for the neighbours ----------------
 #pragma unroll
-            for (int o = 16; o > 0; o >>= 1) {
-#pragma unroll
-                for (int q = 0; q < 3; ++q) acc[q] += __shfl_xor_sync(0xffffffffu, acc[q], o);
+            for (int c = 0; c < BC; ++c) {
+                halo[buf][0][rg][col0 + c] = make_double4(r[BR - 1][c], w[BR - 1][c], s[BR - 1][c], 0.0);
+                halo[buf][1][rg][col0 + c] = make_double4(r[0][c], w[0][c], s[0][c], 0.0);
             }
-            if (lane == 0) {
-#pragma unroll
-                for (int q = 0; q < 3; ++q) red[q][warp] = acc[q];
+            // ---- warp reduction with value exchange: 6 double shuffles for 4 values ---------
+            {
+                const bool hi16 = lane & 16, hi8 = lane & 8;
+                const double s0 = hi16 ? acc[0] : acc[2], s1 = hi16 ? acc[1] : acc[3];
+                const double k0 = hi16 ? acc[2] : acc[0], k1 = hi16 ? acc[3] : acc[1];
+                const double a0 = k0 + __shfl_xor_sync(0xffffffffu, s0, 16);
+                const double a1 = k1 + __shfl_xor_sync(0xffffffffu, s1, 16);
+                double v = (hi8 ? a1 : a0) + __shfl_xor_sync(0xffffffffu, hi8 ? a0 : a1, 8);
+                v += __shfl_xor_sync(0xffffffffu, v, 4);
+                v += __shfl_xor_sync(0xffffffffu, v, 2);
+                v += __shfl_xor_sync(0xffffffffu, v, 1);
+                // lane 0: gamma, lane 8: delta, lane 16: rho, lane 24: pad
+                if ((lane & 7) == 0) red[buf][lane >> 3][warp] = v;
             }
             __syncthreads();
-            double gamma = 0.0, delta = 0.0;
-            rho = 0.0;
+            double gsum[3];
 #pragma unroll
-            for (int q = 0; q < NWARP; ++q) {
-                gamma += red[0][q];
-                delta += red[1][q];
-                rho += red[2][q];
+            for (int q = 0; q < 3; ++q) {            // fixed pairwise tree over the warps
+                double t[NWARP];
+#pragma unroll
+                for (int ww = 0; ww < NWARP; ++ww) t[ww] = red[buf][q][ww];
+#pragma unroll
+                for (int h = 1; h < NWARP; h <<= 1)
+#pragma unroll
+                    for (int ww = 0; ww + h < NWARP; ww += 2 * h) t[ww] += t[ww + h];
+                gsum[q] = t[0];
             }
-            if (first) bb = rho;
+            const double gamma = gsum[0], delta = gsum[1];
+            rho = gsum[2];
+            if (k == 0) bb = rho;
             if (rho <= Q.tol2 * bb || it >= Q.maxit) break;
-            double alpha, beta;
-            if (first) {
-                beta = 0.0;
-                alpha = gamma / delta;
-            } else {
-                beta = gamma / gamma_old;
-                alpha = gamma / (delta - beta * gamma / alpha_old);
-            }
-            first = false;
-            gamma_old = gamma;
-            alpha_old = alpha;
+            const double beta = k == 0 ? 0.0 : gamma * g_inv;
+            const double alpha = k == 0 ? gamma / delta : gamma / (delta - gamma * gamma * ga_inv);
+            g_inv = 1.0 / gamma;                     // off the critical path of the next iteration
+            ga_inv = 1.0 / (gamma * alpha);
 #pragma unroll
-            for (int k = 0; k < BR; ++k)
+            for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    p[k][c] = fma(beta, p[k][c], r[k][c]);
-                    s[k][c] = fma(beta, s[k][c], w[k][c]);
-                    x[k][c] = fma(alpha, p[k][c], x[k][c]);
-                    r[k][c] = fma(-alpha, s[k][c], r[k][c]);
+                    p[q][c] = fma(beta, p[q][c], r[q][c]);
+                    s[q][c] = fma(beta, s[q][c], w[q][c]);
+                    x[q][c] = fma(alpha, p[q][c], x[q][c]);
+                    r[q][c] = fma(-alpha, s[q][c], r[q][c]);
                 }
+            // neighbours' r_{k+1} on the rows below / above, recomputed with the same fma chain
+#pragma unroll
+            for (int c = 0; c < BC; ++c) {
+                if (rg > 0) {
+                    const double4 hb = halo[buf][0][rg - 1][col0 + c];
+                    below[c] = fma(-alpha, fma(beta, hb.z, hb.y), hb.x);
+                }
+                if (rg + 1 < NRG) {
+                    const double4 ha = halo[buf][1][rg + 1][col0 + c];
+                    above[c] = fma(-alpha, fma(beta, ha.z, ha.y), ha.x);
+                }
+            }
             ++it;
         }
         // ---- output: x = D^{-1/2} x^ ----------------------------------------------------------
@@ -196,7 +219,7 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
                 const int i = col0 + c + 1, j = row0 + k + 1;
-                if (i <= nx && j <= nx) u[(int64_t)((j - 1) * nx + (i - 1)) * ldu + bl] = x[k][c] / sqrt(d[k][c]);
+                if (i <= nx && j <= nx) u[(int64_t)((j - 1) * nx + (i - 1)) * ldu + bl] = x[k][c] / sqrt(dg[j * np + i]);
             }
         if (tid == 0) {
             if (iters) iters[bl] = it;

@@ -183,13 +183,13 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
 using namespace usfft;
 
 namespace {
-template <int BC, int BR, int LX, int NWARP>
+template <int NC, int BC, int BR, int LX, int NWARP>
 usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                             const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
                             int32_t *iters, double *relres, int32_t *noconv, const double *S) {
     const int n = Q.n;
     const size_t dyn = sizeof(double) * (size_t)(2 * n * n + (n + 1) * (n + 1));
-    auto kern = k_pcg_reg<BC, BR, LX, NWARP>;
+    auto kern = k_pcg_reg<NC, BC, BR, LX, NWARP>;
     USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int per_sm = 0;
     USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWARP * 32, dyn));
@@ -287,14 +287,14 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     USFFT_CUDA(c, cudaMemsetAsync(noconv, 0, sizeof(int32_t), c->stream));
 
     const int n = pde->n, G = (n - 1) * (n - 1);
-    // register-resident CTA-per-sample PCG where the whole sample fits the register file
-    // (n-1 <= 31); otherwise shared/global-memory PCG.  USFFT_PCG=smem forces the latter.
+    // register-resident CTA-per-sample PCG (mesh size a template parameter: n = 16, 32, the
+    // meshes of configs 1-2); otherwise the shared/global-memory PCG.  USFFT_PCG=smem forces the latter.
     const char *force = getenv("USFFT_PCG");
     const bool reg_ok = !(force && force[0] == 's');
-    if (reg_ok && n - 1 <= 15)
-        s = launch_pcg_reg<2, 4, 8, 1>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
-    else if (reg_ok && n - 1 <= 31)
-        s = launch_pcg_reg<2, 4, 16, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    if (reg_ok && n == 16)
+        s = launch_pcg_reg<16, 2, 4, 8, 1>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else if (reg_ok && n == 32)
+        s = launch_pcg_reg<32, 2, 4, 16, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     // threads x nodes-per-thread: 128x2 (G <= 256), 256x4 (G <= 1024), 512x8, 1024x16
     else if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
