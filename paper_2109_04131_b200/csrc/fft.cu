@@ -103,10 +103,23 @@ __global__ void k_kappa(const double2 *__restrict__ F, const int32_t *__restrict
 }  // namespace usfft
 
 #include "rader.cuh"
+#include "rader_t.cuh"
 
 using namespace usfft;
 
 namespace {
+
+template <int N, int WPR, int RPC>
+usfft_status launch_rader_t(usfft_ctx *c, const double *u, const SlabParams &S, int64_t G_loc,
+                            int32_t L, const RaderArgs &A, double2 *F) {
+    const int64_t rows = G_loc * L;
+    const size_t smem = sizeof(double2) * 2 * (size_t)N * RPC;
+    auto kern = k_fft_rader_t<N, WPR, RPC>;
+    USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<(unsigned)((rows + RPC - 1) / RPC), WPR * 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
 
 bool is_prime64(int64_t n) {
     if (n < 2) return false;
@@ -272,11 +285,19 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         A.perm = R.perm;
         A.outidx = R.outidx;
         A.bf = R.bf;
-        USFFT_CUDA(c, cudaFuncSetAttribute(k_fft_rader, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
-        const int threads = M <= 512 ? 128 : 256;
-        k_fft_rader<<<(unsigned)rows, threads, smem_r, c->stream>>>(u, S, G_loc, L, A,
-                                                                     reinterpret_cast<double2 *>(spectra));
-        USFFT_CHECK_LAUNCH(c);
+        double2 *Fo = reinterpret_cast<double2 *>(spectra);
+        const bool generic = force && force[0] == 'g';     // USFFT_DFT=generic: runtime-plan kernel
+        if (!generic && R.N == 96) s = launch_rader_t<96, 1, 4>(c, u, S, G_loc, L, A, Fo);
+        else if (!generic && R.N == 400) s = launch_rader_t<400, 1, 4>(c, u, S, G_loc, L, A, Fo);
+        else if (!generic && R.N == 2016) s = launch_rader_t<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
+        else if (!generic && R.N == 4000) s = launch_rader_t<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
+        else {
+            USFFT_CUDA(c, cudaFuncSetAttribute(k_fft_rader, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+            const int threads = M <= 512 ? 128 : 256;
+            k_fft_rader<<<(unsigned)rows, threads, smem_r, c->stream>>>(u, S, G_loc, L, A, Fo);
+            USFFT_CHECK_LAUNCH(c);
+        }
+        if (s) return s;
     } else {
         USFFT_REQUIRE(c, smem <= c->smem_optin, "M = %lld too large for the direct DFT", (long long)M);
         USFFT_CUDA(c, cudaFuncSetAttribute(k_dft_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));

@@ -59,9 +59,10 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         // w_h(i,j) = (a_lo(i,j) + a_up(i,j-1))/2 ; w_v(i,j) = (a_up(i,j) + a_lo(i-1,j))/2
 #define WH(i, j) (0.5 * (aT[2 * ((j) * n + (i))] + aT[2 * (((j) - 1) * n + (i)) + 1]))
 #define WV(i, j) (0.5 * (aT[2 * ((j) * n + (i)) + 1] + aT[2 * ((j) * n + (i) - 1)]))
-        for (int e = tid; e < nx * nx; e += NWARP * 32) {
-            const int i = e % nx + 1, j = e / nx + 1;
-            dg[j * np + i] = WH(i, j) + WH(i - 1, j) + WV(i, j) + WV(i, j - 1);
+        for (int e = tid; e < np * np; e += NWARP * 32) {   // ring entries = 1 (padded nodes, r = 0)
+            const int i = e % np, j = e / np;
+            dg[e] = (i >= 1 && i <= nx && j >= 1 && j <= nx)
+                        ? WH(i, j) + WH(i - 1, j) + WV(i, j) + WV(i, j - 1) : 1.0;
         }
         __syncthreads();
         // ---- per-thread state --------------------------------------------------------------

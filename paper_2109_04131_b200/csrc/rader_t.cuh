@@ -1,0 +1,151 @@
+// rader_t.cuh — compile-time specialisations of the Rader lattice FFT (rader.cuh) for the lattice
+// sizes the size rule Z2 produces (M = 97, 401, 2017, 4001: N = M-1 = 96, 400, 2016, 4000).
+// With N a template parameter every Stockham index (j / Ns, j % Ns, twiddle index) is a constant
+// division and the stage list is unrolled.  A group of WPR warps transforms one row (WPR = 1:
+// warp-synchronous, no CTA barrier); a CTA holds RPC rows.  Shared memory per row: two N-point
+// complex ping-pong buffers; the real input row is staged in the second buffer.
+#pragma once
+
+namespace usfft {
+
+template <int N>
+struct RadixList {
+    __host__ __device__ static constexpr int count() {
+        int n = N, c = 0;
+        for (int r : {4, 2, 3, 5, 7})
+            while (n % r == 0) {
+                n /= r;
+                ++c;
+            }
+        return c;
+    }
+    __host__ __device__ static constexpr int radix(int st) {
+        int n = N, c = 0;
+        for (int r : {4, 2, 3, 5, 7})
+            while (n % r == 0) {
+                if (c == st) return r;
+                n /= r;
+                ++c;
+            }
+        return 1;
+    }
+    __host__ __device__ static constexpr int ns(int st) {            // product of the radices before stage st
+        int p = 1;
+        for (int k = 0; k < st; ++k) p *= radix(k);
+        return p;
+    }
+};
+
+template <int GROUP>
+__device__ __forceinline__ void group_sync(int gid) {
+    if (GROUP == 32) __syncwarp();
+    else asm volatile("bar.sync %0, %1;" ::"r"(gid + 1), "r"(GROUP) : "memory");
+}
+
+template <int N, int R, int NS, int GROUP>
+__device__ __forceinline__ void stage_t(const double2 *__restrict__ in, double2 *__restrict__ out,
+                                        const double2 *__restrict__ tw, int t) {
+    constexpr int NBF = N / R, TSTEP = N / (NS * R), WR = N / R;
+    for (int j = t; j < NBF; j += GROUP) {
+        const int jm = j % NS;
+        double2 v[R];
+#pragma unroll
+        for (int r = 0; r < R; ++r) {
+            const double2 a = in[j + r * NBF];
+            v[r] = (r == 0 || NS == 1) ? a : cmul(a, __ldg(tw + r * jm * TSTEP));
+        }
+        const int base = (j / NS) * NS * R + jm;
+        if (R == 2) {
+            out[base] = cadd(v[0], v[1]);
+            out[base + NS] = csub(v[0], v[1]);
+        } else if (R == 4) {
+            const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+            const double2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
+            out[base] = cadd(s02, s13);
+            out[base + 2 * NS] = csub(s02, s13);
+            out[base + NS] = make_double2(d02.x + d13.y, d02.y - d13.x);
+            out[base + 3 * NS] = make_double2(d02.x - d13.y, d02.y + d13.x);
+        } else {
+#pragma unroll
+            for (int s2 = 0; s2 < R; ++s2) {
+                double2 acc = v[0];
+#pragma unroll
+                for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], __ldg(tw + ((r * s2) % R) * WR)));
+                out[base + s2 * NS] = acc;
+            }
+        }
+    }
+}
+
+template <int N, int ST, int GROUP>
+__device__ __forceinline__ double2 *fft_t(double2 *in, double2 *out, const double2 *__restrict__ tw,
+                                          int t, int gid) {
+    if constexpr (ST == RadixList<N>::count()) {
+        return in;
+    } else {
+        constexpr int R = RadixList<N>::radix(ST);
+        stage_t<N, R, RadixList<N>::ns(ST), GROUP>(in, out, tw, t);
+        group_sync<GROUP>(gid);
+        return fft_t<N, ST + 1, GROUP>(out, in, tw, t, gid);
+    }
+}
+
+template <int N, int WPR, int RPC>
+__global__ void __launch_bounds__(WPR * 32 * RPC)
+k_fft_rader_t(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_t L,
+              const RaderArgs A, double2 *__restrict__ F, int64_t rows) {
+    constexpr int GROUP = WPR * 32;
+    constexpr int M = N + 1, MH = M / 2 + 1;
+    extern __shared__ double2 smt[];
+    const int gid = threadIdx.x / GROUP, t = threadIdx.x % GROUP;
+    const int64_t row = (int64_t)blockIdx.x * RPC + gid;
+    if (row >= rows) return;                               // whole group exits together
+    double2 *b0 = smt + (size_t)gid * 2 * N;
+    double2 *b1 = b0 + N;
+    double *xs = reinterpret_cast<double *>(b1);           // real row staged in b1 (M <= 2N)
+    const int64_t g = row / L, l = row - g * L;
+    double part = 0.0;
+    for (int i = t; i < M; i += GROUP) {
+        const double v = sample_at(u, S, G_loc, g, l * M + i);
+        xs[i] = v;
+        part += v;
+    }
+    // X[0] = sum_i x_i: fixed tree over the group (shuffles, then warp partials in order)
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+    __shared__ double wsum[32];
+    if (WPR > 1) {
+        if ((t & 31) == 0) wsum[gid * WPR + (t >> 5)] = part;
+    }
+    group_sync<GROUP>(gid);
+    if (WPR > 1) {
+        double tot = 0.0;
+#pragma unroll
+        for (int w = 0; w < WPR; ++w) tot += wsum[gid * WPR + w];
+        part = tot;
+    }
+    const double x0 = xs[0];
+    for (int p = t; p < N; p += GROUP) b0[p] = make_double2(xs[__ldg(A.perm + p)], 0.0);
+    group_sync<GROUP>(gid);
+    double2 *Ahat = fft_t<N, 0, GROUP>(b0, b1, A.tw, t, gid);
+    double2 *other = Ahat == b0 ? b1 : b0;
+    for (int k = t; k < N; k += GROUP) {
+        const double2 c = cmul(Ahat[k], __ldg(A.bf + k));
+        Ahat[k] = make_double2(c.x, -c.y);
+    }
+    group_sync<GROUP>(gid);
+    double2 *conv = fft_t<N, 0, GROUP>(Ahat, other, A.tw, t, gid);
+    double2 *stage_out = conv == b0 ? b1 : b0;
+    for (int q = t; q < N; q += GROUP) {
+        const int32_t m = __ldg(A.outidx + q);
+        if (m < MH) {
+            const double2 c = conv[q];
+            stage_out[m] = make_double2(x0 + c.x, -c.y);
+        }
+    }
+    group_sync<GROUP>(gid);
+    double2 *dst = F + row * MH;
+    for (int m = t; m < MH; m += GROUP) dst[m] = m == 0 ? make_double2(part, 0.0) : stage_out[m];
+}
+
+}  // namespace usfft
