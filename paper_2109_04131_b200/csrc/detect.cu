@@ -23,6 +23,7 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     __shared__ unsigned int hist[256];
     __shared__ unsigned long long s_prefix;
     __shared__ long long s_need;
+    __shared__ bool s_exact;
     __shared__ int scan_sh[33];
     const int64_t g = blockIdx.x;
     const unsigned long long *keys =
@@ -30,15 +31,18 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     const double th2 = theta2_of(theta_rel, theta_abs, kmax);
     if (g == 0 && threadIdx.x == 0 && th2_out) th2_out[0] = th2;
 
-    unsigned long long T = 0ull;
-    long long need_eq;
+    // Radix select of the s~-th largest key.  After a pass the bucket holding rank k is known;
+    // if that bucket holds exactly k keys, every key >= its lower bound is a member and no tie
+    // remains (early exit, typical for distinct doubles); otherwise keep refining.
+    unsigned long long T = 0ull, Tmin = 0ull;
+    long long need_eq = 0;
+    bool by_min = false;                         // members = {key >= Tmin}
     if ((int64_t)s_tilde >= nJ) {
-        // every candidate is within the top s~
-        T = 0ull;
-        need_eq = nJ;
+        by_min = true;                           // every candidate is within the top s~
+        Tmin = 0ull;
     } else {
         unsigned long long prefix = 0ull, pmask = 0ull;
-        long long k = s_tilde;                       // rank (1-based, from the top) still to find
+        long long k = s_tilde;                   // rank (1-based, from the top) still to find
         for (int pass = 0; pass < 8; ++pass) {
             const int shift = 56 - 8 * pass;
             for (int q = threadIdx.x; q < 256; q += blockDim.x) hist[q] = 0u;
@@ -48,27 +52,52 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
                 if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255ull], 1u);
             }
             __syncthreads();
-            if (threadIdx.x == 0) {
-                long long cum = 0;
-                int digit = 0;
-                for (int dg = 255; dg >= 0; --dg) {
-                    if (cum + (long long)hist[dg] >= k) {
-                        digit = dg;
-                        break;
-                    }
-                    cum += hist[dg];
+            if (threadIdx.x < 32) {              // warp-parallel search from the top bucket
+                const int lane = threadIdx.x;
+                unsigned int c8[8];
+                unsigned int cl = 0;
+#pragma unroll
+                for (int b = 0; b < 8; ++b) {
+                    c8[b] = hist[8 * lane + b];
+                    cl += c8[b];
                 }
-                k -= cum;
-                s_prefix = prefix | ((unsigned long long)digit << shift);
-                s_need = k;
+                long long suf = cl;              // sum over lanes >= lane
+#pragma unroll
+                for (int o = 1; o < 32; o <<= 1) {
+                    const long long y = __shfl_down_sync(0xffffffffu, suf, o);
+                    if (lane + o < 32) suf += y;
+                }
+                const unsigned int ball = __ballot_sync(0xffffffffu, suf >= k);
+                const int Ls = __popc(ball) - 1;       // top-most lane whose suffix reaches k
+                if (lane == Ls) {
+                    long long cum = suf - cl;          // keys in buckets above this lane's
+                    int digit = 8 * lane;
+                    unsigned int cnt = 0;
+                    for (int b = 7; b >= 0; --b) {
+                        if (cum + (long long)c8[b] >= k) {
+                            digit = 8 * lane + b;
+                            cnt = c8[b];
+                            break;
+                        }
+                        cum += c8[b];
+                    }
+                    s_prefix = prefix | ((unsigned long long)digit << shift);
+                    s_need = k - cum;
+                    s_exact = (long long)cnt == k - cum;
+                }
             }
             __syncthreads();
             prefix = s_prefix;
             k = s_need;
             pmask |= 255ull << shift;
+            if (s_exact) {                      // whole bucket selected: members are key >= prefix
+                by_min = true;
+                Tmin = prefix;
+                break;
+            }
         }
         T = prefix;
-        need_eq = k;                                 // how many keys == T are taken (by index)
+        need_eq = k;                             // how many keys == T are taken (by index)
     }
     // ordered pass: membership, threshold, output in ascending j, votes
     int eq_run = 0, out_run = 0;
@@ -78,10 +107,10 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
         unsigned long long key = 0ull;
         bool valid = j < nJ;
         if (valid) key = keys[j];
-        const int is_eq = (valid && key == T) ? 1 : 0;
+        const int is_eq = (!by_min && valid && key == T) ? 1 : 0;
         int eq_tot;
         const int eq_before = eq_run + block_exscan(is_eq, scan_sh, &eq_tot);
-        bool member = valid && (key > T || (is_eq && eq_before < need_eq));
+        const bool member = valid && (by_min ? key >= Tmin : (key > T || (is_eq && eq_before < need_eq)));
         const double kv = __longlong_as_double((long long)key);
         const int take = (member && kv >= th2 && kv > 0.0) ? 1 : 0;
         int tot;

@@ -67,21 +67,27 @@ __global__ void k_dft_direct(const double *__restrict__ u, const SlabParams S, i
     }
 }
 
-// one CTA per owned node g
-__global__ void k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins,
-                        int64_t nJ, int64_t M, int32_t L, double *__restrict__ kmin,
-                        unsigned long long *__restrict__ kmax) {
+// one CTA per owned node g; the node's L spectra rows are staged in shared memory when they fit
+__global__ void __launch_bounds__(256)
+k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t nJ, int64_t M,
+        int32_t L, double *__restrict__ kmin, unsigned long long *__restrict__ kmax, int staged) {
+    extern __shared__ double2 fs[];
     __shared__ unsigned long long wmax[32];
     const int64_t g = blockIdx.x;
     const int64_t Mh = M / 2 + 1;
+    const double2 *src = F + g * L * Mh;
+    if (staged) {
+        for (int64_t e = threadIdx.x; e < (int64_t)L * Mh; e += blockDim.x) fs[e] = src[e];
+        __syncthreads();
+        src = fs;
+    }
     unsigned long long best = 0ull;
     for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) {
         double km = 0.0;
         for (int l = 0; l < L; ++l) {
             const int64_t b = bins[(int64_t)l * nJ + j];
-            const double2 v = spec_value(F + (g * L + l) * Mh, M, b);
-            const double re = v.x, im = v.y;
-            const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+            const double2 v = spec_value(src + l * Mh, M, b);
+            const double k = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
             km = (l == 0) ? k : fmin(km, k);
         }
         kmin[g * nJ + j] = km;
@@ -308,8 +314,12 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
     if (nJ > 0) {
         unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
         if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
-        k_kappa<<<(unsigned)G_loc, 256, 0, c->stream>>>(reinterpret_cast<const double2 *>(spectra),
-                                                        bins, nJ, M, L, kappa_min, km);
+        const size_t st_bytes = sizeof(double2) * (size_t)L * (size_t)(M / 2 + 1);
+        const int staged = st_bytes <= 96 * 1024 ? 1 : 0;
+        if (staged)
+            USFFT_CUDA(c, cudaFuncSetAttribute(k_kappa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st_bytes));
+        k_kappa<<<(unsigned)G_loc, 256, staged ? st_bytes : 0, c->stream>>>(
+            reinterpret_cast<const double2 *>(spectra), bins, nJ, M, L, kappa_min, km, staged);
         USFFT_CHECK_LAUNCH(c);
     }
     return USFFT_OK;

@@ -28,7 +28,9 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
     extern __shared__ double sm[];
     __shared__ double red[2][4][NWARP];          // [parity][gamma, delta, rho, pad][warp]
     __shared__ double th_amp[kMaxD];
-    __shared__ double4 halo[2][2][NRG][NCOL];    // [parity][top, bottom row][row group][col]
+    __shared__ double hr[2][2][NRG][NCOL];       // [parity][top, bottom row][row group][col]: r_k
+    __shared__ double hw[2][2][NRG][NCOL];       // w_k
+    __shared__ double hs[2][2][NRG][NCOL];       // s_{k-1}
 
     constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1;   // NC = cells per side (== Q.n)
     double *aT = sm;                             // [2 n^2] coefficient at triangle centroids
@@ -153,8 +155,12 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             // ---- publish the edge rows (r_k, w_k, s_{k-1}) for the neighbours ----------------
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
-                halo[buf][0][rg][col0 + c] = make_double4(r[BR - 1][c], w[BR - 1][c], s[BR - 1][c], 0.0);
-                halo[buf][1][rg][col0 + c] = make_double4(r[0][c], w[0][c], s[0][c], 0.0);
+                hr[buf][0][rg][col0 + c] = r[BR - 1][c];
+                hw[buf][0][rg][col0 + c] = w[BR - 1][c];
+                hs[buf][0][rg][col0 + c] = s[BR - 1][c];
+                hr[buf][1][rg][col0 + c] = r[0][c];
+                hw[buf][1][rg][col0 + c] = w[0][c];
+                hs[buf][1][rg][col0 + c] = s[0][c];
             }
             // ---- warp reduction with value exchange: 6 double shuffles for 4 values ---------
             {
@@ -171,6 +177,19 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
                 if ((lane & 7) == 0) red[buf][lane >> 3][warp] = v;
             }
             __syncthreads();
+            // prefetch the neighbours' edge rows (unconditional loads, clamped row groups) so the
+            // shared-memory latency overlaps the scalar recurrences below
+            const int rgb = rg > 0 ? rg - 1 : rg, rga = rg + 1 < NRG ? rg + 1 : rg;
+            double nb_r[BC], nb_w[BC], nb_s[BC], na_r[BC], na_w[BC], na_s[BC];
+#pragma unroll
+            for (int c = 0; c < BC; ++c) {
+                nb_r[c] = hr[buf][0][rgb][col0 + c];
+                nb_w[c] = hw[buf][0][rgb][col0 + c];
+                nb_s[c] = hs[buf][0][rgb][col0 + c];
+                na_r[c] = hr[buf][1][rga][col0 + c];
+                na_w[c] = hw[buf][1][rga][col0 + c];
+                na_s[c] = hs[buf][1][rga][col0 + c];
+            }
             double gsum[3];
 #pragma unroll
             for (int q = 0; q < 3; ++q) {            // fixed pairwise tree over the warps
@@ -203,14 +222,10 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             // neighbours' r_{k+1} on the rows below / above, recomputed with the same fma chain
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
-                if (rg > 0) {
-                    const double4 hb = halo[buf][0][rg - 1][col0 + c];
-                    below[c] = fma(-alpha, fma(beta, hb.z, hb.y), hb.x);
-                }
-                if (rg + 1 < NRG) {
-                    const double4 ha = halo[buf][1][rg + 1][col0 + c];
-                    above[c] = fma(-alpha, fma(beta, ha.z, ha.y), ha.x);
-                }
+                const double vb = fma(-alpha, fma(beta, nb_s[c], nb_w[c]), nb_r[c]);
+                const double va = fma(-alpha, fma(beta, na_s[c], na_w[c]), na_r[c]);
+                below[c] = rg > 0 ? vb : 0.0;
+                above[c] = rg + 1 < NRG ? va : 0.0;
             }
             ++it;
         }
