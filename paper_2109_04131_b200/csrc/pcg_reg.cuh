@@ -17,8 +17,8 @@
 
 namespace usfft {
 
-template <int NC, int BC, int BR, int LX, int NWARP>
-__global__ void __launch_bounds__(NWARP * 32, 3)
+template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
+__global__ void __launch_bounds__(NWARP * 32, MINB)
 k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
           int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
           double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S) {
@@ -177,19 +177,6 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
                 if ((lane & 7) == 0) red[buf][lane >> 3][warp] = v;
             }
             __syncthreads();
-            // prefetch the neighbours' edge rows (unconditional loads, clamped row groups) so the
-            // shared-memory latency overlaps the scalar recurrences below
-            const int rgb = rg > 0 ? rg - 1 : rg, rga = rg + 1 < NRG ? rg + 1 : rg;
-            double nb_r[BC], nb_w[BC], nb_s[BC], na_r[BC], na_w[BC], na_s[BC];
-#pragma unroll
-            for (int c = 0; c < BC; ++c) {
-                nb_r[c] = hr[buf][0][rgb][col0 + c];
-                nb_w[c] = hw[buf][0][rgb][col0 + c];
-                nb_s[c] = hs[buf][0][rgb][col0 + c];
-                na_r[c] = hr[buf][1][rga][col0 + c];
-                na_w[c] = hw[buf][1][rga][col0 + c];
-                na_s[c] = hs[buf][1][rga][col0 + c];
-            }
             double gsum[3];
 #pragma unroll
             for (int q = 0; q < 3; ++q) {            // fixed pairwise tree over the warps
@@ -210,6 +197,19 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             const double alpha = k == 0 ? gamma / delta : gamma / (delta - gamma * gamma * ga_inv);
             g_inv = 1.0 / gamma;                     // off the critical path of the next iteration
             ga_inv = 1.0 / (gamma * alpha);
+            // the neighbours' edge rows (unconditional loads, clamped row groups); their latency overlaps
+            // the vector updates below
+            const int rgb = rg > 0 ? rg - 1 : rg, rga = rg + 1 < NRG ? rg + 1 : rg;
+            double nb_r[BC], nb_w[BC], nb_s[BC], na_r[BC], na_w[BC], na_s[BC];
+#pragma unroll
+            for (int c = 0; c < BC; ++c) {
+                nb_r[c] = hr[buf][0][rgb][col0 + c];
+                nb_w[c] = hw[buf][0][rgb][col0 + c];
+                nb_s[c] = hs[buf][0][rgb][col0 + c];
+                na_r[c] = hr[buf][1][rga][col0 + c];
+                na_w[c] = hw[buf][1][rga][col0 + c];
+                na_s[c] = hs[buf][1][rga][col0 + c];
+            }
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll

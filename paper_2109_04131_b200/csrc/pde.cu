@@ -183,13 +183,13 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
 using namespace usfft;
 
 namespace {
-template <int NC, int BC, int BR, int LX, int NWARP>
+template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                             const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
                             int32_t *iters, double *relres, int32_t *noconv, const double *S) {
     const int n = Q.n;
     const size_t dyn = sizeof(double) * (size_t)(2 * n * n + (n + 1) * (n + 1));
-    auto kern = k_pcg_reg<NC, BC, BR, LX, NWARP>;
+    auto kern = k_pcg_reg<NC, BC, BR, LX, NWARP, MINB>;
     USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int per_sm = 0;
     USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWARP * 32, dyn));
@@ -292,9 +292,10 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     const char *force = getenv("USFFT_PCG");
     const bool reg_ok = !(force && force[0] == 's');
     if (reg_ok && n == 16)
-        s = launch_pcg_reg<16, 2, 4, 8, 1>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        s = launch_pcg_reg<16, 2, 4, 8, 1, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (reg_ok && n == 32)
-        s = launch_pcg_reg<32, 2, 4, 16, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        s = getenv("USFFT_PCG4") ? launch_pcg_reg<32, 2, 4, 16, 4, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S)
+                                 : launch_pcg_reg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     // threads x nodes-per-thread: 128x2 (G <= 256), 256x4 (G <= 1024), 512x8, 1024x16
     else if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);

@@ -394,3 +394,16 @@ def test_pcg_variants_agree(B, ctx, monkeypatch):
             assert B.usfft_sample_pde(ctx, B.pde_desc(cfg), p, 5, nb, u, nb, check_conv=True) == 0
             assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
         monkeypatch.delenv("USFFT_PCG")
+
+
+def test_pcg_all_samples_of_a_round_converge(B, ctx):
+    """Every sample of a full config-2 round converges (guards against NaN/stagnation paths)."""
+    cfg = config(2)
+    p = B.usfft_plan_round(ctx, cfg["seed"], 2, 5, 3, cfg["d"], cfg["N"], cfg["s"], "A", 1000)
+    nb, G = p.L * p.M, 961
+    u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
+    iters = torch.empty(nb, dtype=torch.int32, device="cuda")
+    rel = torch.empty(nb, dtype=torch.float64, device="cuda")
+    assert B.usfft_sample_pde(ctx, B.pde_desc(cfg), p, 0, nb, u, nb, None, iters, rel, check_conv=True) == 0
+    assert torch.isfinite(u).all() and rel.max().item() <= 1e-12
+    assert iters.max().item() < 300
