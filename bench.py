@@ -32,6 +32,23 @@ FLOPS_PER_NODE_ITER = 22      # Jacobi PCG, 5-point stencil: DESIGN.md §5 (algo
 FP64_FMA_PER_CLK_PER_SM = 64  # B200 fp64 datapath: 37 TF at 1.965 GHz x 148 SMs
 
 
+def ncu_traffic(kernel_prefix: str):
+    """dram read+write bytes per launch of a kernel from the newest committed ncu --set full
+    summary (profiles/*_ncu.json), or None."""
+    import glob
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json")))
+    scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
+    for path in reversed(files):
+        for d in json.load(open(path)).get("full", []):
+            if kernel_prefix in d.get("kernel", ""):
+                tot = 0.0
+                for m in ("dram__bytes_read.sum", "dram__bytes_write.sum"):
+                    val, unit = d[m].split()
+                    tot += float(val) * scale.get(unit, 1.0)
+                return {"bytes": tot, "source": os.path.relpath(path, ROOT)}
+    return None
+
+
 def peaks():
     p = {"hbm_gbs": 6650.0, "sm_max_mhz": 1965.0, "source": "fallback (B200_PROFILING.md)"}
     path = os.path.join(ROOT, "MEASURED_PEAKS.json")
@@ -216,7 +233,9 @@ def run_ours(args):
                        "parallelism": f"samples sharded over {world} GPU(s)"},
             "roofline": {"kernel": "k_pcg (batched Jacobi PCG, on-chip)", "bound": "alu",
                          "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
-                         "frac": ach / fp64_peak if fp64_peak else None, "traffic": None,
+                         "frac": ach / fp64_peak if fp64_peak else None,
+                         "traffic": (ncu_traffic("k_pcg_reg") or {}).get("bytes"),
+                         "traffic_source": (ncu_traffic("k_pcg_reg") or {}).get("source"),
                          "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz",
                          "flops_per_node_iter": FLOPS_PER_NODE_ITER},
             "fft": {"kernel": "k_dft_direct + k_kappa", "ms_per_step": fft_ms,
