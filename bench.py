@@ -295,7 +295,7 @@ def run_reference(args):
     cfg = config(args.config)
     t_b = args.t if args.t else min(5, cfg["d"])
     s_t = cfg["s_local"] if t_b < cfg["d"] else cfg["s"]
-    nJ = 1500                                        # |J_t| scale of config 2 at t ~ 5
+    nJ = 1000                                        # |J_t| of the config-2 t = 5 round the GPU arm times
     M = oplan.lattice_size(s_t, cfg["N"])
     L = oplan.num_lattices(nJ)
 

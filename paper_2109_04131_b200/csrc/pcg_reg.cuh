@@ -17,6 +17,20 @@
 
 namespace usfft {
 
+// 1/a for positive normal a: hardware seed (MUFU.RCP64H) refined by three Newton steps, no
+// special-case branches (the CG scalars are positive and far from the fp64 range limits while
+// the iteration runs; breakdown values stop the loop through the residual test first).
+__device__ __forceinline__ double rcp_pos(double a) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    double e = fma(-a, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-a, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-a, y, 1.0);
+    return fma(y, e, y);
+}
+
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 __global__ void __launch_bounds__(NWARP * 32, MINB)
 k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
@@ -133,12 +147,15 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
                 left[q] = __shfl_up_sync(0xffffffffu, r[q][BC - 1], 1, LX);
                 right[q] = __shfl_down_sync(0xffffffffu, r[q][0], 1, LX);
             }
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};    // gamma, delta, rho, (pad)
+            // partial dots in two interleaved chains per value (even / odd node) to halve the
+            // dependent-FMA latency; combined in a fixed order below
+            double acc2[2][3] = {{0.0, 0.0, 0.0}, {0.0, 0.0, 0.0}};   // [chain][gamma, delta, rho]
             double w[BR][BC];
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
+                    const int ch = (q * BC + c) & 1;
                     const double rl = c > 0 ? r[q][c - 1] : left[q];
                     const double rr = c + 1 < BC ? r[q][c + 1] : right[q];
                     const double rd = q > 0 ? r[q - 1][c] : below[c];
@@ -148,10 +165,11 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
                     v = fma(wN[q + 1][c], ru, v);
                     v = fma(wN[q][c], rd, v);
                     w[q][c] = v;
-                    acc[0] = fma(r[q][c], r[q][c], acc[0]);
-                    acc[1] = fma(v, r[q][c], acc[1]);
-                    acc[2] = fma(dgb[q * np + c] * r[q][c], r[q][c], acc[2]);   // padded: r = 0
+                    acc2[ch][0] = fma(r[q][c], r[q][c], acc2[ch][0]);
+                    acc2[ch][1] = fma(v, r[q][c], acc2[ch][1]);
+                    acc2[ch][2] = fma(dgb[q * np + c] * r[q][c], r[q][c], acc2[ch][2]);   // padded: r = 0
                 }
+            double acc[4] = {acc2[0][0] + acc2[1][0], acc2[0][1] + acc2[1][1], acc2[0][2] + acc2[1][2], 0.0};
             // ---- publish the edge rows (r_k, w_k, s_{k-1}) for the neighbours ----------------
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
@@ -194,9 +212,9 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             if (k == 0) bb = rho;
             if (rho <= Q.tol2 * bb || it >= Q.maxit) break;
             const double beta = k == 0 ? 0.0 : gamma * g_inv;
-            const double alpha = k == 0 ? gamma / delta : gamma / (delta - gamma * gamma * ga_inv);
-            g_inv = 1.0 / gamma;                     // off the critical path of the next iteration
-            ga_inv = 1.0 / (gamma * alpha);
+            const double alpha = gamma * rcp_pos(k == 0 ? delta : delta - gamma * gamma * ga_inv);
+            g_inv = rcp_pos(gamma);                  // off the critical path of the next iteration
+            ga_inv = rcp_pos(gamma * alpha);
             // the neighbours' edge rows (unconditional loads, clamped row groups); their latency overlaps
             // the vector updates below
             const int rgb = rg > 0 ? rg - 1 : rg, rga = rg + 1 < NRG ? rg + 1 : rg;

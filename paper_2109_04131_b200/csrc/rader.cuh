@@ -37,6 +37,55 @@ __device__ __forceinline__ double2 cmul(double2 a, double2 b) {
 __device__ __forceinline__ double2 cadd(double2 a, double2 b) { return make_double2(a.x + b.x, a.y + b.y); }
 __device__ __forceinline__ double2 csub(double2 a, double2 b) { return make_double2(a.x - b.x, a.y - b.y); }
 
+
+// y_s = sum_r v_r e^{-2 pi i r s / R}, written to out[base + s*stride].  Radix 2 and 4 by the
+// textbook butterflies; 3 and 5 by the symmetric (real-coefficient) forms; 7 generic via twiddles.
+template <int R>
+__device__ __forceinline__ void dft_small(const double2 (&v)[R], double2 *__restrict__ out, int base,
+                                          int stride, const double2 *__restrict__ tw, int wR) {
+    if (R == 2) {
+        out[base] = cadd(v[0], v[1]);
+        out[base + stride] = csub(v[0], v[1]);
+    } else if (R == 4) {
+        const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
+        const double2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
+        out[base] = cadd(s02, s13);
+        out[base + 2 * stride] = csub(s02, s13);
+        out[base + stride] = make_double2(d02.x + d13.y, d02.y - d13.x);        // d02 - i d13
+        out[base + 3 * stride] = make_double2(d02.x - d13.y, d02.y + d13.x);    // d02 + i d13
+    } else if (R == 3) {
+        const double S3 = 0.86602540378443864676;                              // sin(2 pi/3)
+        const double2 t1 = cadd(v[1], v[2]), t2 = csub(v[1], v[2]);
+        const double2 a = make_double2(fma(-0.5, t1.x, v[0].x), fma(-0.5, t1.y, v[0].y));
+        const double2 b = make_double2(S3 * t2.x, S3 * t2.y);
+        out[base] = cadd(v[0], t1);
+        out[base + stride] = make_double2(a.x + b.y, a.y - b.x);                // a - i b
+        out[base + 2 * stride] = make_double2(a.x - b.y, a.y + b.x);            // a + i b
+    } else if (R == 5) {
+        const double C1 = 0.30901699437494742410, C2 = -0.80901699437494742410;  // cos(2pi/5), cos(4pi/5)
+        const double S1 = 0.95105651629515357212, S2 = 0.58778525229247312917;   // sin(2pi/5), sin(4pi/5)
+        const double2 t1 = cadd(v[1], v[4]), t2 = cadd(v[2], v[3]);
+        const double2 t3 = csub(v[1], v[4]), t4 = csub(v[2], v[3]);
+        const double2 a1 = make_double2(fma(C2, t2.x, fma(C1, t1.x, v[0].x)), fma(C2, t2.y, fma(C1, t1.y, v[0].y)));
+        const double2 a2 = make_double2(fma(C1, t2.x, fma(C2, t1.x, v[0].x)), fma(C1, t2.y, fma(C2, t1.y, v[0].y)));
+        const double2 b1 = make_double2(fma(S2, t4.x, S1 * t3.x), fma(S2, t4.y, S1 * t3.y));
+        const double2 b2 = make_double2(fma(-S1, t4.x, S2 * t3.x), fma(-S1, t4.y, S2 * t3.y));
+        out[base] = cadd(v[0], cadd(t1, t2));
+        out[base + stride] = make_double2(a1.x + b1.y, a1.y - b1.x);            // a1 - i b1
+        out[base + 4 * stride] = make_double2(a1.x - b1.y, a1.y + b1.x);        // a1 + i b1
+        out[base + 2 * stride] = make_double2(a2.x + b2.y, a2.y - b2.x);        // a2 - i b2
+        out[base + 3 * stride] = make_double2(a2.x - b2.y, a2.y + b2.x);        // a2 + i b2
+    } else {
+#pragma unroll
+        for (int s2 = 0; s2 < R; ++s2) {
+            double2 acc = v[0];
+#pragma unroll
+            for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], __ldg(tw + ((r * s2) % R) * wR)));
+            out[base + s2 * stride] = acc;
+        }
+    }
+}
+
 // one Stockham stage of radix R: in -> out, Ns = product of earlier radices
 template <int R>
 __device__ __forceinline__ void stockham_stage(const double2 *__restrict__ in, double2 *__restrict__ out,
@@ -52,26 +101,7 @@ __device__ __forceinline__ void stockham_stage(const double2 *__restrict__ in, d
             v[r] = r == 0 ? a : cmul(a, __ldg(tw + (r * jm * tstep) % N));
         }
         const int base = (j / Ns) * Ns * R + jm;
-        if (R == 2) {
-            out[base] = cadd(v[0], v[1]);
-            out[base + Ns] = csub(v[0], v[1]);
-        } else if (R == 4) {
-            const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
-            const double2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
-            out[base] = cadd(s02, s13);
-            out[base + 2 * Ns] = csub(s02, s13);
-            out[base + Ns] = make_double2(d02.x + d13.y, d02.y - d13.x);        // d02 - i d13
-            out[base + 3 * Ns] = make_double2(d02.x - d13.y, d02.y + d13.x);    // d02 + i d13
-        } else {
-            const int wR = N / R;
-#pragma unroll
-            for (int s2 = 0; s2 < R; ++s2) {
-                double2 acc = v[0];
-#pragma unroll
-                for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], __ldg(tw + ((r * s2) % R) * wR)));
-                out[base + s2 * Ns] = acc;
-            }
-        }
+        dft_small<R>(v, out, base, Ns, tw, N / R);
     }
 }
 

@@ -55,25 +55,7 @@ __device__ __forceinline__ void stage_t(const double2 *__restrict__ in, double2 
             v[r] = (r == 0 || NS == 1) ? a : cmul(a, __ldg(tw + r * jm * TSTEP));
         }
         const int base = (j / NS) * NS * R + jm;
-        if (R == 2) {
-            out[base] = cadd(v[0], v[1]);
-            out[base + NS] = csub(v[0], v[1]);
-        } else if (R == 4) {
-            const double2 s02 = cadd(v[0], v[2]), d02 = csub(v[0], v[2]);
-            const double2 s13 = cadd(v[1], v[3]), d13 = csub(v[1], v[3]);
-            out[base] = cadd(s02, s13);
-            out[base + 2 * NS] = csub(s02, s13);
-            out[base + NS] = make_double2(d02.x + d13.y, d02.y - d13.x);
-            out[base + 3 * NS] = make_double2(d02.x - d13.y, d02.y + d13.x);
-        } else {
-#pragma unroll
-            for (int s2 = 0; s2 < R; ++s2) {
-                double2 acc = v[0];
-#pragma unroll
-                for (int r = 1; r < R; ++r) acc = cadd(acc, cmul(v[r], __ldg(tw + ((r * s2) % R) * WR)));
-                out[base + s2 * NS] = acc;
-            }
-        }
+        dft_small<R>(v, out, base, NS, tw, WR);
     }
 }
 
