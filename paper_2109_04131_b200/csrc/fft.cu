@@ -77,15 +77,17 @@ k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t
     const int64_t Mh = M / 2 + 1;
     const double2 *src = F + g * L * Mh;
     if (staged) {
-        for (int64_t e = threadIdx.x; e < (int64_t)L * Mh; e += blockDim.x) fs[e] = src[e];
+#pragma unroll 8
+        for (int64_t e = threadIdx.x; e < (int64_t)L * Mh; e += blockDim.x) fs[e] = __ldg(src + e);
         __syncthreads();
         src = fs;
     }
     unsigned long long best = 0ull;
     for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) {
         double km = 0.0;
+#pragma unroll 4
         for (int l = 0; l < L; ++l) {
-            const int64_t b = bins[(int64_t)l * nJ + j];
+            const int64_t b = __ldg(bins + (int64_t)l * nJ + j);
             const double2 v = spec_value(src + l * Mh, M, b);
             const double k = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
             km = (l == 0) ? k : fmin(km, k);
@@ -122,7 +124,12 @@ usfft_status launch_rader_t(usfft_ctx *c, const double *u, const SlabParams &S, 
     const size_t smem = sizeof(double2) * 2 * (size_t)N * RPC;
     auto kern = k_fft_rader_t<N, WPR, RPC>;
     USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<(unsigned)((rows + RPC - 1) / RPC), WPR * 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
+    int per_sm = 0;
+    USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPR * 32 * RPC, smem));
+    int64_t grid = (rows + RPC - 1) / RPC;
+    const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
+    if (grid > resident) grid = resident;                 // persistent: each group loops over rows
+    kern<<<(unsigned)grid, WPR * 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }

@@ -78,56 +78,82 @@ k_fft_rader_t(const double *__restrict__ u, const SlabParams S, int64_t G_loc, i
               const RaderArgs A, double2 *__restrict__ F, int64_t rows) {
     constexpr int GROUP = WPR * 32;
     constexpr int M = N + 1, MH = M / 2 + 1;
+    constexpr int PER = (M + GROUP - 1) / GROUP;          // samples per thread per row
     extern __shared__ double2 smt[];
+    __shared__ double wsum[32];
     const int gid = threadIdx.x / GROUP, t = threadIdx.x % GROUP;
-    const int64_t row = (int64_t)blockIdx.x * RPC + gid;
-    if (row >= rows) return;                               // whole group exits together
     double2 *b0 = smt + (size_t)gid * 2 * N;
     double2 *b1 = b0 + N;
     double *xs = reinterpret_cast<double *>(b1);           // real row staged in b1 (M <= 2N)
-    const int64_t g = row / L, l = row - g * L;
-    double part = 0.0;
-    for (int i = t; i < M; i += GROUP) {
-        const double v = sample_at(u, S, G_loc, g, l * M + i);
-        xs[i] = v;
-        part += v;
-    }
-    // X[0] = sum_i x_i: fixed tree over the group (shuffles, then warp partials in order)
+    const bool one_slab = S.nslab == 1;
+    const int64_t stride = (int64_t)gridDim.x * RPC;
+    int64_t row = (int64_t)blockIdx.x * RPC + gid;
+    // register prefetch of the group's next row (one slab: the row is contiguous)
+    double xv[PER];
+    auto fetch = [&](int64_t rw) {
+        const int64_t g = rw / L, l = rw - g * L;
+        if (one_slab) {
+            const double *src = u + g * (int64_t)L * M + l * M;
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
-    __shared__ double wsum[32];
-    if (WPR > 1) {
-        if ((t & 31) == 0) wsum[gid * WPR + (t >> 5)] = part;
-    }
-    group_sync<GROUP>(gid);
-    if (WPR > 1) {
-        double tot = 0.0;
+            for (int k = 0; k < PER; ++k) {
+                const int i = t + k * GROUP;
+                xv[k] = i < M ? __ldg(src + i) : 0.0;
+            }
+        } else {
 #pragma unroll
-        for (int w = 0; w < WPR; ++w) tot += wsum[gid * WPR + w];
-        part = tot;
-    }
-    const double x0 = xs[0];
-    for (int p = t; p < N; p += GROUP) b0[p] = make_double2(xs[__ldg(A.perm + p)], 0.0);
-    group_sync<GROUP>(gid);
-    double2 *Ahat = fft_t<N, 0, GROUP>(b0, b1, A.tw, t, gid);
-    double2 *other = Ahat == b0 ? b1 : b0;
-    for (int k = t; k < N; k += GROUP) {
-        const double2 c = cmul(Ahat[k], __ldg(A.bf + k));
-        Ahat[k] = make_double2(c.x, -c.y);
-    }
-    group_sync<GROUP>(gid);
-    double2 *conv = fft_t<N, 0, GROUP>(Ahat, other, A.tw, t, gid);
-    double2 *stage_out = conv == b0 ? b1 : b0;
-    for (int q = t; q < N; q += GROUP) {
-        const int32_t m = __ldg(A.outidx + q);
-        if (m < MH) {
-            const double2 c = conv[q];
-            stage_out[m] = make_double2(x0 + c.x, -c.y);
+            for (int k = 0; k < PER; ++k) {
+                const int i = t + k * GROUP;
+                xv[k] = i < M ? sample_at(u, S, G_loc, g, l * M + i) : 0.0;
+            }
         }
+    };
+    if (row < rows) fetch(row);
+    for (; row < rows; row += stride) {
+        double part = 0.0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = t + k * GROUP;
+            if (i < M) xs[i] = xv[k];
+            part += xv[k];
+        }
+        if (row + stride < rows) fetch(row + stride);       // overlaps the transforms below
+        // X[0] = sum_i x_i: fixed tree over the group (shuffles, then warp partials in order)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) part += __shfl_xor_sync(0xffffffffu, part, o);
+        if (WPR > 1) {
+            if ((t & 31) == 0) wsum[gid * WPR + (t >> 5)] = part;
+        }
+        group_sync<GROUP>(gid);
+        if (WPR > 1) {
+            double tot = 0.0;
+#pragma unroll
+            for (int w = 0; w < WPR; ++w) tot += wsum[gid * WPR + w];
+            part = tot;
+        }
+        const double x0 = xs[0];
+        for (int p = t; p < N; p += GROUP) b0[p] = make_double2(xs[__ldg(A.perm + p)], 0.0);
+        group_sync<GROUP>(gid);
+        double2 *Ahat = fft_t<N, 0, GROUP>(b0, b1, A.tw, t, gid);
+        double2 *other = Ahat == b0 ? b1 : b0;
+        for (int k = t; k < N; k += GROUP) {
+            const double2 c = cmul(Ahat[k], __ldg(A.bf + k));
+            Ahat[k] = make_double2(c.x, -c.y);
+        }
+        group_sync<GROUP>(gid);
+        double2 *conv = fft_t<N, 0, GROUP>(Ahat, other, A.tw, t, gid);
+        double2 *stage_out = conv == b0 ? b1 : b0;
+        for (int q = t; q < N; q += GROUP) {
+            const int32_t m = __ldg(A.outidx + q);
+            if (m < MH) {
+                const double2 c = conv[q];
+                stage_out[m] = make_double2(x0 + c.x, -c.y);
+            }
+        }
+        group_sync<GROUP>(gid);
+        double2 *dst = F + row * MH;
+        for (int m = t; m < MH; m += GROUP) dst[m] = m == 0 ? make_double2(part, 0.0) : stage_out[m];
+        group_sync<GROUP>(gid);                               // buffers are reused by the next row
     }
-    group_sync<GROUP>(gid);
-    double2 *dst = F + row * MH;
-    for (int m = t; m < MH; m += GROUP) dst[m] = m == 0 ? make_double2(part, 0.0) : stage_out[m];
 }
 
 }  // namespace usfft
