@@ -407,3 +407,66 @@ def test_pcg_all_samples_of_a_round_converge(B, ctx):
     assert B.usfft_sample_pde(ctx, B.pde_desc(cfg), p, 0, nb, u, nb, None, iters, rel, check_conv=True) == 0
     assert torch.isfinite(u).all() and rel.max().item() <= 1e-12
     assert iters.max().item() < 300
+
+
+def test_emulated_multirank_round_bitexact(B, ctx):
+    """A whole Step-2 round computed as P = 3 virtual ranks (sample shards, exchanged slabs, node
+    shards, kappa_max MAX, votes SUM) is bit-identical to the P = 1 round.  The
+    exchange is emulated by slicing on one GPU; the NCCL calls themselves are plumbing."""
+    from paper_2109_04131_b200.dist import bounds
+    cfg = config(2)
+    t, s = 3, cfg["s_local"]
+    rng = np.random.default_rng(12)
+    I_prev = np.unique(rng.integers(-8, 9, size=(40, t - 1)), axis=0)
+    kt = np.arange(-3, 4)
+    Id, ktd = dev(I_prev, torch.int16), dev(kt, torch.int16)
+    nJ = I_prev.shape[0] * kt.shape[0]
+    p = B.usfft_plan_round(ctx, cfg["seed"], 2, t, 2, cfg["d"], cfg["N"], s, "A", nJ)
+    Bt, G, Mh = p.L * p.M, 961, p.M // 2 + 1
+    bins = torch.empty((p.L, nJ), dtype=torch.int32, device="cuda")
+    B.usfft_lattice(ctx, p, 0, 0, None, Id, I_prev.shape[0], ktd, bins)
+    pde = B.pde_desc(cfg)
+
+    def one_round(P):
+        sb, gb = bounds(Bt, P), bounds(G, P)
+        u_r = []
+        for r in range(P):                                   # sample shards
+            nb = sb[r + 1] - sb[r]
+            u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
+            B.usfft_sample_pde(ctx, pde, p, sb[r], nb, u, nb)
+            u_r.append(u)
+        kmaxes, kmins, specs = [], [], []
+        for r in range(P):                                   # exchanged slabs -> node shards
+            gl = gb[r + 1] - gb[r]
+            slab = torch.cat([u_r[q][gb[r]:gb[r + 1]].reshape(-1) for q in range(P)]).contiguous()
+            sp = torch.empty((gl, p.L, Mh, 2), dtype=torch.float64, device="cuda")
+            km = torch.empty((gl, nJ), dtype=torch.float64, device="cuda")
+            kx = torch.empty(1, dtype=torch.float64, device="cuda")
+            B.usfft_lattice_fft(ctx, p, gl, slab, sb, bins, nJ, sp, km, kx)
+            kmaxes.append(kx), kmins.append(km), specs.append(sp)
+        kmax = torch.stack(kmaxes).max().reshape(1)          # all-reduce MAX
+        votes_all = torch.zeros(nJ, dtype=torch.int32, device="cuda")
+        outs = []
+        for r in range(P):
+            gl = gb[r + 1] - gb[r]
+            v = torch.empty(nJ, dtype=torch.int32, device="cuda")
+            dg_ = torch.empty((gl, s), dtype=torch.int32, device="cuda")
+            nd_ = torch.empty(gl, dtype=torch.int32, device="cuda")
+            B.usfft_detect_select(ctx, gl, nJ, kmins[r], kmax, s, 1e-6, 0.0, v, dg_, nd_)
+            votes_all += v                                   # all-reduce SUM
+            outs.append((dg_, nd_))
+        flags = torch.zeros(nJ, dtype=torch.uint8, device="cuda")
+        det = torch.empty(nJ, dtype=torch.int32, device="cuda")
+        n_det, _ = B.usfft_detect_union(ctx, nJ, votes_all, flags, det)
+        coefs = []
+        for r in range(P):
+            gl = gb[r + 1] - gb[r]
+            cf = torch.empty((gl, n_det, 2), dtype=torch.float64, device="cuda")
+            B.usfft_resolve(ctx, p, gl, specs[r], bins, nJ, outs[r][0], outs[r][1], s, det, n_det, cf)
+            coefs.append(cf)
+        return (torch.cat(u_r, 1), torch.cat(kmins), kmax, votes_all, det[:n_det].clone(),
+                torch.cat(coefs))
+
+    a, b = one_round(1), one_round(3)
+    for x, y in zip(a, b):
+        assert torch.equal(x, y)
