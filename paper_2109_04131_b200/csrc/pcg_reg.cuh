@@ -5,7 +5,7 @@
 // in the symmetrically scaled form: with D = diag(A), x^ = D^{1/2} x, r^ = D^{-1/2} r and
 // A^ = D^{-1/2} A D^{-1/2} (unit diagonal), CG on A^ x^ = b^ produces the Jacobi-PCG iterates
 // (z = D^-1 r <-> r^).  The loop is the Chronopoulos-Gear single-reduction variant:
-//     w = A^ r^;  gamma = (r^,r^), delta = (w,r^), rho = sum d r^^2 (= ||r||_2^2)   [one reduction]
+//     w = A^ r^;  gamma = (r^,r^), delta = (w,r^) [+ rho = sum d r^^2 = ||r||_2^2]   [one reduction]
 //     beta = gamma/gamma_old, alpha = gamma/(delta - beta*gamma/alpha_old)
 //     p = r^ + beta p;  s = w + beta s;  x^ += alpha p;  r^ -= alpha s
 // stopping on the true-residual recurrence ||r||_2 <= tol ||b||_2 (Z13).  Per iteration: one CTA
@@ -41,6 +41,7 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
     constexpr int NCOL = LX * BC;                // covered columns
     extern __shared__ double sm[];
     __shared__ double red[2][4][NWARP];          // [parity][gamma, delta, rho, pad][warp]
+    __shared__ unsigned long long dminmax[2];    // bit patterns of min / max diagonal (d > 0)
     __shared__ double th_amp[kMaxD];
     __shared__ double hr[2][2][NRG][NCOL];       // [parity][top, bottom row][row group][col]: r_k
     __shared__ double hw[2][2][NRG][NCOL];       // w_k
@@ -75,12 +76,24 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         // w_h(i,j) = (a_lo(i,j) + a_up(i,j-1))/2 ; w_v(i,j) = (a_up(i,j) + a_lo(i-1,j))/2
 #define WH(i, j) (0.5 * (aT[2 * ((j) * n + (i))] + aT[2 * (((j) - 1) * n + (i)) + 1]))
 #define WV(i, j) (0.5 * (aT[2 * ((j) * n + (i)) + 1] + aT[2 * ((j) * n + (i) - 1)]))
-        for (int e = tid; e < np * np; e += NWARP * 32) {   // ring entries = 1 (padded nodes, r = 0)
-            const int i = e % np, j = e / np;
-            dg[e] = (i >= 1 && i <= nx && j >= 1 && j <= nx)
-                        ? WH(i, j) + WH(i - 1, j) + WV(i, j) + WV(i, j - 1) : 1.0;
+        if (tid == 0) {
+            dminmax[0] = ~0ull;
+            dminmax[1] = 0ull;
         }
         __syncthreads();
+        for (int e = tid; e < np * np; e += NWARP * 32) {   // ring entries = 1 (padded nodes, r = 0)
+            const int i = e % np, j = e / np;
+            const bool in = i >= 1 && i <= nx && j >= 1 && j <= nx;
+            const double v = in ? WH(i, j) + WH(i - 1, j) + WV(i, j) + WV(i, j - 1) : 1.0;
+            dg[e] = v;
+            if (in) {                                     // order-free min / max (positive doubles)
+                atomicMin(&dminmax[0], (unsigned long long)__double_as_longlong(v));
+                atomicMax(&dminmax[1], (unsigned long long)__double_as_longlong(v));
+            }
+        }
+        __syncthreads();
+        const double d_min = __longlong_as_double((long long)dminmax[0]);
+        const double d_max = __longlong_as_double((long long)dminmax[1]);
         // ---- per-thread state --------------------------------------------------------------
         double x[BR][BC], r[BR][BC], p[BR][BC], s[BR][BC];
         const double *dgb = dg + (row0 + 1) * np + col0 + 1;   // diagonal of node (q, c): dgb[q*np + c]
@@ -127,7 +140,13 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         // before the reduction barrier and every reader recomputes the neighbour's s_k and
         // r_{k+1} with the same fma sequence, so one barrier per iteration suffices (the halo
         // and partial-sum buffers alternate by iteration parity).
+        // Stopping rule (Z13): ||r||_2^2 = rho = sum d r^^2 and d_min gamma <= rho <= d_max gamma
+        // with gamma = (r^, r^).  rho is reduced only when gamma says the test may be close
+        // (need_rho); otherwise d_max gamma <= tol^2 ||b||^2 (a sufficient condition) decides.  An
+        // ambiguous iteration without rho continues, and the next one computes rho, so the loop
+        // stops at most one iteration after the exact rule would.
         double rho = 0.0, bb = 0.0;
+        bool need_rho = true, conv = false;
         double g_inv = 0.0, ga_inv = 0.0;        // 1/gamma_{k-1}, 1/(gamma_{k-1} alpha_{k-1})
         double below[BC], above[BC];             // neighbour r_k on the rows below/above
 #pragma unroll
@@ -167,8 +186,16 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
                     w[q][c] = v;
                     acc2[ch][0] = fma(r[q][c], r[q][c], acc2[ch][0]);
                     acc2[ch][1] = fma(v, r[q][c], acc2[ch][1]);
-                    acc2[ch][2] = fma(dgb[q * np + c] * r[q][c], r[q][c], acc2[ch][2]);   // padded: r = 0
                 }
+            if (need_rho) {                              // uniform branch (see the stopping rule)
+#pragma unroll
+                for (int q = 0; q < BR; ++q)
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) {
+                        const int ch = (q * BC + c) & 1;
+                        acc2[ch][2] = fma(dgb[q * np + c] * r[q][c], r[q][c], acc2[ch][2]);   // padded: r = 0
+                    }
+            }
             double acc[4] = {acc2[0][0] + acc2[1][0], acc2[0][1] + acc2[1][1], acc2[0][2] + acc2[1][2], 0.0};
             // ---- publish the edge rows (r_k, w_k, s_{k-1}) for the neighbours ----------------
 #pragma unroll
@@ -208,9 +235,11 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
                 gsum[q] = t[0];
             }
             const double gamma = gsum[0], delta = gsum[1];
-            rho = gsum[2];
+            rho = need_rho ? gsum[2] : d_max * gamma;    // exact, or an upper bound of ||r||^2
             if (k == 0) bb = rho;
-            if (rho <= Q.tol2 * bb || it >= Q.maxit) break;
+            conv = rho <= Q.tol2 * bb;
+            if (conv || it >= Q.maxit) break;
+            need_rho = d_min * gamma <= 4.0 * Q.tol2 * bb;
             const double beta = k == 0 ? 0.0 : gamma * g_inv;
             const double alpha = gamma * rcp_pos(k == 0 ? delta : delta - gamma * gamma * ga_inv);
             g_inv = rcp_pos(gamma);                  // off the critical path of the next iteration
@@ -257,8 +286,8 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             }
         if (tid == 0) {
             if (iters) iters[bl] = it;
-            if (relres) relres[bl] = sqrt(rho / bb);
-            if (rho > Q.tol2 * bb) atomicAdd(noconv, 1);
+            if (relres) relres[bl] = sqrt(rho / bb);       // exact or an upper bound
+            if (!conv) atomicAdd(noconv, 1);
         }
         __syncthreads();
     }
