@@ -294,8 +294,15 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     if (reg_ok && n == 16)
         s = launch_pcg_reg<16, 2, 4, 8, 1, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (reg_ok && n == 32)
-        s = getenv("USFFT_PCG4") ? launch_pcg_reg<32, 2, 4, 16, 4, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S)
-                                 : launch_pcg_reg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    {
+        const char *lay = getenv("USFFT_PCG_LAYOUT");       // experiments: thread block of nodes
+        if (lay && lay[0] == '1')
+            s = launch_pcg_reg<32, 1, 4, 32, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        else if (getenv("USFFT_PCG4"))
+            s = launch_pcg_reg<32, 2, 4, 16, 4, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        else
+            s = launch_pcg_reg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    }
     // threads x nodes-per-thread: 128x2 (G <= 256), 256x4 (G <= 1024), 512x8, 1024x16
     else if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
