@@ -78,6 +78,10 @@ typedef struct {
  *   amp        host fp64 [d]
  *   tol        relative residual target ||r_k||_2 <= tol ||b||_2 (Z13; BASELINE 1e-12)
  *   maxit      PCG iteration cap
+ *   precond    0: Jacobi (diagonal) PCG;  1: geometric-multigrid V(1,1) preconditioned CG
+ *              (damped-Jacobi smoothing, bilinear P, R = P^T, rediscretised coarse meshes;
+ *              implemented for n = 16, 32 -> USFFT_EUNIMPL otherwise).  Any solver is admissible
+ *              for the black box; both are CG with an SPD preconditioner (Z13).
  */
 typedef struct {
     int32_t n;
@@ -88,6 +92,8 @@ typedef struct {
     int32_t maxit;
     const double *amp;
     double tol;
+    int32_t precond;
+    int32_t pad_;
 } usfft_pde_desc;
 
 /* Round plan input/output (usfft_plan_round). */
@@ -154,7 +160,7 @@ usfft_status usfft_lattice(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_
  * Jacobi PCG from x0 = 0, stop on the recursive ||r||_2 <= tol ||b||_2 (Z13).
  * u        dev fp64 [G][ldu]: u[g*ldu + bl] = u(x_g, y_{b0+bl}), ldu >= nb
  * iters    dev int32 [nb] (may be NULL): PCG iterations per sample
- * relres   dev fp64 [nb] (may be NULL): final recursive ||r||/||b||
+ * relres   dev fp64 [nb] (may be NULL): final recursive ||r||/||b|| (Jacobi path: or an upper bound)
  * n_noconv host int32 (may be NULL; syncs): samples that missed tol; > 0 -> USFFT_ENOCONV */
 usfft_status usfft_sample_pde(usfft_ctx *ctx, const usfft_pde_desc *pde,
                               const usfft_lattice_desc *lat, int64_t b0, int64_t nb,

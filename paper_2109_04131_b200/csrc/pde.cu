@@ -21,7 +21,7 @@
 namespace usfft {
 
 struct PdeParams {
-    int32_t n, d, theta, form, f_kind, maxit;
+    int32_t n, d, theta, form, f_kind, maxit, precond;
     double tol2;              // tol^2
     double amp[kMaxD];
 };
@@ -179,10 +179,29 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
 }  // namespace usfft
 
 #include "pcg_reg.cuh"
+#include "pcg_mg.cuh"
 
 using namespace usfft;
 
 namespace {
+template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
+usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
+                           const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
+                           int32_t *iters, double *relres, int32_t *noconv, const double *S) {
+    const size_t dyn = sizeof(double) * (size_t)MgLayout<NC>::doubles();
+    auto kern = k_pcg_mg<NC, BC, BR, LX, NWARP, MINB>;
+    USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+    int per_sm = 0;
+    USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWARP * 32, dyn));
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)per_sm * c->sm_count;
+    if (grid > nb) grid = nb;
+    kern<<<(unsigned)grid, NWARP * 32, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
+                                                         noconv, S);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                             const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
@@ -255,6 +274,7 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     USFFT_REQUIRE(c, pde->f_kind == 0, "f_kind %d not implemented", pde->f_kind);
     USFFT_REQUIRE(c, pde->amp != nullptr, "amp is NULL");
     USFFT_REQUIRE(c, pde->tol > 0.0 && pde->maxit >= 1, "tol/maxit");
+    USFFT_REQUIRE(c, pde->precond == 0 || pde->precond == 1, "precond %d", pde->precond);
     USFFT_REQUIRE(c, b0 >= 0 && nb >= 0 && b0 + nb <= (int64_t)P.L * P.M, "sample range");
     USFFT_REQUIRE(c, ldu >= nb && u != nullptr, "u is NULL or ldu < nb");
     if (nb == 0) {
@@ -267,6 +287,7 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     Q.form = pde->form;
     Q.f_kind = pde->f_kind;
     Q.maxit = pde->maxit;
+    Q.precond = pde->precond;
     Q.tol2 = pde->tol * pde->tol;
     for (int j = 0; j < pde->d; ++j) Q.amp[j] = pde->amp[j];
 
@@ -291,7 +312,13 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     // meshes of configs 1-2); otherwise the shared/global-memory PCG.  USFFT_PCG=smem forces the latter.
     const char *force = getenv("USFFT_PCG");
     const bool reg_ok = !(force && force[0] == 's');
-    if (reg_ok && n == 16)
+    if (pde->precond == 1 && n == 32)
+        s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else if (pde->precond == 1 && n == 16)
+        s = launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else if (pde->precond == 1)
+        return fail(c, USFFT_EUNIMPL, "multigrid preconditioner implemented for n = 16, 32");
+    else if (reg_ok && n == 16)
         s = launch_pcg_reg<16, 2, 4, 8, 1, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (reg_ok && n == 32)
     {

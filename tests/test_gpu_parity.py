@@ -380,19 +380,25 @@ def test_fft_variants_agree(B, ctx, monkeypatch):
 
 
 def test_pcg_variants_agree(B, ctx, monkeypatch):
-    """Register-resident PCG (default for n-1 <= 31) and the shared-memory PCG both meet the
-    oracle tolerance on the same samples."""
+    """Multigrid-preconditioned CG (default for n = 16, 32), the register-resident Jacobi PCG and
+    the shared-memory Jacobi PCG all meet the oracle tolerance on the same samples."""
     for cfgid in (1, 2):
         cfg = config(cfgid)
         p = B.usfft_plan_round(ctx, cfg["seed"], 2, 4, 2, cfg["d"], cfg["N"], cfg["s"], "A", 300)
         nb, G = 24, (cfg["n"] - 1) ** 2
         Y = olat.nodes(p.M, p.z, p.shift, 4)[:, 5:5 + nb]
         ref = ofe.sample_pde(cfg, Y)
-        for mode in ("reg", "smem"):
-            monkeypatch.setenv("USFFT_PCG", mode)
+        for precond, env in (("mg", "reg"), ("jacobi", "reg"), ("jacobi", "smem")):
+            monkeypatch.setenv("USFFT_PCG", env)
             u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
-            assert B.usfft_sample_pde(ctx, B.pde_desc(cfg), p, 5, nb, u, nb, check_conv=True) == 0
+            it = torch.empty(nb, dtype=torch.int32, device="cuda")
+            rel = torch.empty(nb, dtype=torch.float64, device="cuda")
+            assert B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond=precond), p, 5, nb, u, nb, None,
+                                      it, rel, check_conv=True) == 0
             assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
+            assert rel.max().item() <= 1e-12
+            if precond == "mg":
+                assert it.max().item() <= 30           # multigrid: iteration count ~ mesh independent
         monkeypatch.delenv("USFFT_PCG")
 
 
