@@ -25,7 +25,7 @@ constexpr double kMgOmega = 0.8;
 // per-level shared-memory arrays of a coarse grid with nl cells per side ((nl+1)^2 padded)
 struct MgLevel {
     int nl;
-    double *wh, *wv, *d, *di, *R, *Z, *T;
+    double *wh, *wv, *d, *di, *R, *Z, *S;   // R: rhs, Z: pre-smoothed, S: post-smoothed
 };
 
 template <int NC>
@@ -115,7 +115,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 L_.wv[e] = v;
                 L_.R[e] = 0.0;
                 L_.Z[e] = 0.0;
-                L_.T[e] = 0.0;
+                L_.S[e] = 0.0;
             }
         }
         __syncthreads();
@@ -193,23 +193,35 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     out[q][c] = fma(-cN[q][c], vd, a);
                 }
         };
-        // ---- the V(1,1) cycle: out = M^-1 rin ------------------------------------------------
+        // ---- the V(1,1) cycle: z = M^-1 rin (rin must be published in G0 before the call) ----
+        // Every phase reads only values published before the preceding barrier and recomputes
+        // the few derived neighbour values it needs (pre-smoothed iterates omega D^-1 R,
+        // residuals, prolongated corrections) instead of waiting for them: 8 barriers per cycle.
         auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
             double t[BR][BC];
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) z[q][c] = kMgOmega * DI0[ebase + q * np + c] * rin[q][c];
-            publish(G0, z);
-            __syncthreads();
-            apply_fine(G0, z, t);
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) t[q][c] = rin[q][c] - t[q][c];       // fine residual
+                for (int c = 0; c < BC; ++c) {       // fine residual t = r - A z, z = omega D^-1 r
+                    const int e = ebase + q * np + c;
+                    const double vl = c > 0 ? z[q][c - 1] : kMgOmega * DI0[e - 1] * G0[e - 1];
+                    const double vr = c + 1 < BC ? z[q][c + 1] : kMgOmega * DI0[e + 1] * G0[e + 1];
+                    const double vd = q > 0 ? z[q - 1][c] : kMgOmega * DI0[e - np] * G0[e - np];
+                    const double vu = q + 1 < BR ? z[q + 1][c] : kMgOmega * DI0[e + np] * G0[e + np];
+                    double a = D0[e] * z[q][c];
+                    a = fma(-cE[q][c + 1], vr, a);
+                    a = fma(-cE[q][c], vl, a);
+                    a = fma(-cN[q + 1][c], vu, a);
+                    a = fma(-cN[q][c], vd, a);
+                    t[q][c] = rin[q][c] - a;
+                }
             publish(G1, t);
             __syncthreads();
-            {   // restriction R = P^T to level 0 (n/2 cells)
+            {   // restriction R = P^T to level 1 (n/2 cells)
                 const MgLevel C = lev[0];
                 constexpr int m = NC / 2, mp = m + 1;
                 for (int e = tid; e < mp * mp; e += NT) {
@@ -221,79 +233,73 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
             }
             __syncthreads();
-            // coarse levels: down sweep
+            // down sweep: level l pre-smooths (Z = omega D^-1 R) and restricts its residual, which
+            // is recomputed from R at the 9 fine points; the coarsest level is solved exactly
 #pragma unroll
-            for (int l = 0; l < NLEV; ++l) {
-                const MgLevel C = lev[l];
+            for (int l = 0; l + 1 < NLEV; ++l) {
+                const MgLevel C = lev[l], Cn = lev[l + 1];
                 const int m = NC >> (l + 1), mp = m + 1;
-                if (l == NLEV - 1) {                 // coarsest (m == 2: one unknown): exact
-                    for (int e = tid; e < mp * mp; e += NT) C.Z[e] = C.di[e] * C.R[e];
-                    __syncthreads();
-                    break;
-                }
-                for (int e = tid; e < mp * mp; e += NT) C.Z[e] = kMgOmega * C.di[e] * C.R[e];
-                __syncthreads();
-                for (int e = tid; e < mp * mp; e += NT) {
-                    if (C.di[e] == 0.0) continue;
-                    const double az = C.d[e] * C.Z[e] - C.wh[e] * C.Z[e + 1] - C.wh[e - 1] * C.Z[e - 1] -
-                                      C.wv[e] * C.Z[e + mp] - C.wv[e - mp] * C.Z[e - mp];
-                    C.T[e] = C.R[e] - az;
-                }
-                __syncthreads();
-                const MgLevel Cn = lev[l + 1];
                 const int mn = NC >> (l + 2), mnp = mn + 1;
+                for (int e = tid; e < mp * mp; e += NT) C.Z[e] = kMgOmega * C.di[e] * C.R[e];
+                auto tres = [&](int f) -> double {  // residual of the pre-smoothed iterate at f
+                    if (C.di[f] == 0.0) return 0.0;
+                    const double zc = kMgOmega * C.di[f] * C.R[f];
+                    const double az = C.d[f] * zc - C.wh[f] * (kMgOmega * C.di[f + 1] * C.R[f + 1]) -
+                                      C.wh[f - 1] * (kMgOmega * C.di[f - 1] * C.R[f - 1]) -
+                                      C.wv[f] * (kMgOmega * C.di[f + mp] * C.R[f + mp]) -
+                                      C.wv[f - mp] * (kMgOmega * C.di[f - mp] * C.R[f - mp]);
+                    return C.R[f] - az;
+                };
                 for (int e = tid; e < mnp * mnp; e += NT) {
                     const int I = e % mnp, J = e / mnp;
                     if (I < 1 || I >= mn || J < 1 || J >= mn) continue;
                     const int f = (2 * J) * mp + 2 * I;
-                    Cn.R[e] = C.T[f] + 0.5 * (C.T[f - 1] + C.T[f + 1] + C.T[f - mp] + C.T[f + mp]) +
-                              0.25 * (C.T[f - mp - 1] + C.T[f - mp + 1] + C.T[f + mp - 1] + C.T[f + mp + 1]);
+                    const double rn = tres(f) + 0.5 * (tres(f - 1) + tres(f + 1) + tres(f - mp) + tres(f + mp)) +
+                                      0.25 * (tres(f - mp - 1) + tres(f - mp + 1) + tres(f + mp - 1) + tres(f + mp + 1));
+                    Cn.R[e] = rn;
+                    if (l + 2 == NLEV) Cn.Z[e] = Cn.di[e] * rn;      // coarsest: exact solve
                 }
                 __syncthreads();
             }
-            // up sweep: prolongate and post-smooth levels NLEV-2 .. 0
+            // up sweep: S_l = smooth(Z_l + P S_{l+1}); neighbours' corrected iterates recomputed
 #pragma unroll
             for (int l = NLEV - 2; l >= 0; --l) {
-                MgLevel &C = lev[l];
-                const MgLevel Cn = lev[l + 1];
+                const MgLevel C = lev[l], Cn = lev[l + 1];
                 const int m = NC >> (l + 1), mp = m + 1, mnp = (NC >> (l + 2)) + 1;
+                const double *Sn = (l + 2 == NLEV) ? Cn.Z : Cn.S;
+                auto zc = [&](int g) -> double {    // Z + bilinear prolongation of Sn at node g
+                    if (C.di[g] == 0.0) return 0.0;
+                    const int i = g % mp, j = g / mp;
+                    const double *z2 = Sn + (j >> 1) * mnp + (i >> 1);
+                    double v;
+                    if (!(i & 1) && !(j & 1)) v = z2[0];
+                    else if (!(j & 1)) v = 0.5 * (z2[0] + z2[1]);
+                    else if (!(i & 1)) v = 0.5 * (z2[0] + z2[mnp]);
+                    else v = 0.25 * (z2[0] + z2[1] + z2[mnp] + z2[mnp + 1]);
+                    return C.Z[g] + v;
+                };
                 for (int e = tid; e < mp * mp; e += NT) {
                     if (C.di[e] == 0.0) continue;
-                    const int i = e % mp, j = e / mp, I = i >> 1, J = j >> 1;
-                    const double *z2 = Cn.Z + J * mnp + I;
-                    double v = z2[0];
-                    if (i & 1) v = 0.5 * (z2[0] + z2[1]);
-                    if (j & 1) v = (i & 1) ? 0.25 * (z2[0] + z2[1] + z2[mnp] + z2[mnp + 1]) : 0.5 * (z2[0] + z2[mnp]);
-                    C.Z[e] += v;
+                    const double z0 = zc(e);
+                    const double az = C.d[e] * z0 - C.wh[e] * zc(e + 1) - C.wh[e - 1] * zc(e - 1) -
+                                      C.wv[e] * zc(e + mp) - C.wv[e - mp] * zc(e - mp);
+                    C.S[e] = fma(kMgOmega * C.di[e], C.R[e] - az, z0);
                 }
                 __syncthreads();
-                for (int e = tid; e < mp * mp; e += NT) {
-                    if (C.di[e] == 0.0) {
-                        C.T[e] = 0.0;
-                        continue;
-                    }
-                    const double az = C.d[e] * C.Z[e] - C.wh[e] * C.Z[e + 1] - C.wh[e - 1] * C.Z[e - 1] -
-                                      C.wv[e] * C.Z[e + mp] - C.wv[e - mp] * C.Z[e - mp];
-                    C.T[e] = fma(kMgOmega * C.di[e], C.R[e] - az, C.Z[e]);
-                }
-                __syncthreads();
-                double *tmp = C.Z;                   // smoothed iterate becomes Z (uniform swap)
-                C.Z = C.T;
-                C.T = tmp;
             }
-            // fine: prolongate the level-0 correction, then post-smooth.  Neighbours' corrected z
-            // = published z (G0) + prolongated correction, both readable without a barrier.
+            // fine up: z += P S_1 and post-smooth; neighbours' corrected z = omega D^-1 r + P S_1
             const MgLevel C0 = lev[0];
             constexpr int m0p = NC / 2 + 1;
-            auto prol = [&](int e) -> double {       // bilinear value of level-0 Z at fine node e
+            auto prol = [&](int e) -> double {       // bilinear value of level-1 S at fine node e
                 const int i = e % np, j = e / np, I = i >> 1, J = j >> 1;
                 if (i < 1 || i > nx || j < 1 || j > nx) return 0.0;
-                const double *z2 = C0.Z + J * m0p + I;
+                const double *z2 = C0.S + J * m0p + I;
                 if (!(i & 1) && !(j & 1)) return z2[0];
                 if (!(j & 1)) return 0.5 * (z2[0] + z2[1]);
                 if (!(i & 1)) return 0.5 * (z2[0] + z2[m0p]);
                 return 0.25 * (z2[0] + z2[1] + z2[m0p] + z2[m0p + 1]);
             };
+            auto zf = [&](int e) -> double { return kMgOmega * DI0[e] * G0[e] + prol(e); };
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
@@ -304,10 +310,10 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
                     const int e = ebase + q * np + c;
-                    const double vl = c > 0 ? z[q][c - 1] : G0[e - 1] + prol(e - 1);
-                    const double vr = c + 1 < BC ? z[q][c + 1] : G0[e + 1] + prol(e + 1);
-                    const double vd = q > 0 ? z[q - 1][c] : G0[e - np] + prol(e - np);
-                    const double vu = q + 1 < BR ? z[q + 1][c] : G0[e + np] + prol(e + np);
+                    const double vl = c > 0 ? z[q][c - 1] : zf(e - 1);
+                    const double vr = c + 1 < BC ? z[q][c + 1] : zf(e + 1);
+                    const double vd = q > 0 ? z[q - 1][c] : zf(e - np);
+                    const double vu = q + 1 < BR ? z[q + 1][c] : zf(e + np);
                     double a = D0[e] * z[q][c];
                     a = fma(-cE[q][c + 1], vr, a);
                     a = fma(-cE[q][c], vl, a);
@@ -336,6 +342,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         for (int k = 0;; ++k) {
             const int buf = k & 1;
             double uu[BR][BC], w[BR][BC];
+            publish(G0, r);
+            __syncthreads();
             vcycle(r, uu);
             publish(G2, uu);
             __syncthreads();
