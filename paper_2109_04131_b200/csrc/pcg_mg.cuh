@@ -1,48 +1,40 @@
-// pcg_mg.cuh — on-chip PCG with a geometric-multigrid V(1,1) preconditioner, one CTA per sample.
+// pcg_mg.cuh — on-chip CG with a three-level geometric-multigrid preconditioner, one CTA per sample.
 //
 // Same P1 discretisation as pde.cu (Z11/Z12); CG in the Chronopoulos-Gear single-reduction form
 //     u = M^-1 r;  w = A u;  gamma = (r,u), delta = (w,u), rho = (r,r)      [one reduction]
 //     beta = gamma/gamma_old;  alpha = gamma/(delta - beta gamma/alpha_old)
 //     p = u + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s,
-// stopping on rho = ||r||_2^2 <= tol^2 ||b||_2^2 (Z13).  M^-1 is one symmetric V(1,1) cycle:
-// damped Jacobi (omega = 0.8) pre/post smoothing, bilinear prolongation P, restriction P^T,
-// coarse operators by rediscretisation of the same P1 problem on the nested coarse "/" meshes
-// (n/2, n/4, ..., 2 cells; the centroid coefficient uses the same sin table because every
-// coarse centroid abscissa is a multiple of h/3), exact solve on the 1-node coarsest grid.  The
-// cycle is symmetric (same smoother before and after, R = P^T) and SPD, so CG stays CG.
+// stopping on rho = ||r||_2^2 <= tol^2 ||b||_2^2 (Z13).
+// M^-1 is one symmetric V(1,1) cycle over three nested "/" meshes (n, n/2, n/4 cells): damped
+// Jacobi (omega = 0.8) pre- and post-smoothing on levels 0 and 1, bilinear prolongation P,
+// restriction R = P^T, coarse operators by rediscretisation of the same P1 problem (every coarse
+// centroid abscissa is a multiple of h/3, so the fine sin table serves all levels), and an exact
+// solve on level 2 with its dense inverse (formed once per sample by Gauss-Jordan; (n/4-1)^2 = 49
+// unknowns at n = 32).  Same smoother before and after and R = P^T make the cycle symmetric
+// positive definite, so CG stays CG.
 //
-// Fine level: each thread owns a BC x BR block of nodes; the CG vectors x, r, p, s, the
-// preconditioned residual u and the coupling weights live in registers; every fine vector that a
-// stencil needs from other threads is published to one of three (n+1)^2 shared-memory grids with
-// a zero Dirichlet ring.  Coarse levels live in shared memory and are swept by all threads.
-// Reductions are fixed trees, so results do not depend on the CTA or launch split.
+// Level 0 (fine): each thread owns a BC x BR block of nodes with x, r, p, s, u and the coupling
+// weights in registers; values needed by other threads are published to shared-memory grids with
+// a zero Dirichlet ring.  Levels 1-2 live in shared memory; every size is a compile-time constant.
+// Reductions are fixed trees, so a sample's result does not depend on the CTA or launch split.
 #pragma once
 
 namespace usfft {
 
 constexpr double kMgOmega = 0.8;
 
-// per-level shared-memory arrays of a coarse grid with nl cells per side ((nl+1)^2 padded)
-struct MgLevel {
-    int nl;
-    double *wh, *wv, *d, *di, *R, *Z, *S;   // R: rhs, Z: pre-smoothed, S: post-smoothed
-};
-
 template <int NC>
-struct MgLayout {
-    __host__ __device__ static constexpr int levels() {   // coarse levels n/2 .. 2
-        int c = 0;
-        for (int m = NC / 2; m >= 2; m /= 2) ++c;
-        return c;
-    }
-    __host__ __device__ static constexpr int coarse_doubles() {
-        int s = 0;
-        for (int m = NC / 2; m >= 2; m /= 2) s += 7 * (m + 1) * (m + 1);
-        return s;
-    }
-    __host__ __device__ static constexpr int doubles() {  // fine d, dinv + 3 fine grids + coarse
-        return 5 * (NC + 1) * (NC + 1) + coarse_doubles();   // (aT aliases grids G1..G2)
-    }
+struct Mg3 {
+    static constexpr int n = NC, np = NC + 1, NP2 = np * np;
+    static constexpr int m1 = NC / 2, p1 = m1 + 1, N1 = p1 * p1;
+    static constexpr int m2 = NC / 4, p2 = m2 + 1, N2 = p2 * p2, U2 = (m2 - 1) * (m2 - 1);
+    // shared-memory layout (doubles)
+    static constexpr int oD0 = 0, oDI0 = NP2, oG0 = 2 * NP2, oG1 = 3 * NP2, oG2 = 4 * NP2;
+    static constexpr int oWH1 = 5 * NP2, oWV1 = oWH1 + N1, oD1 = oWV1 + N1, oDI1 = oD1 + N1;
+    static constexpr int oR1 = oDI1 + N1, oZ1 = oR1 + N1, oT1 = oZ1 + N1, oS1 = oT1 + N1;
+    static constexpr int oWH2 = oS1 + N1, oWV2 = oWH2 + N2, oR2 = oWV2 + N2, oE2 = oR2 + U2;
+    static constexpr int oAI = oE2 + U2;                 // dense inverse of the level-2 operator
+    __host__ __device__ static constexpr int doubles() { return oAI + U2 * U2; }
 };
 
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
@@ -50,49 +42,40 @@ __global__ void __launch_bounds__(NWARP * 32, MINB)
 k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
          int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S) {
+    using L = Mg3<NC>;
     constexpr int RGW = 32 / LX, NRG = NWARP * RGW, NT = NWARP * 32;
-    constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1, NP2 = np * np;
-    constexpr int NLEV = MgLayout<NC>::levels();
+    constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1, NP2 = L::NP2;
+    constexpr int m1 = L::m1, p1 = L::p1, N1 = L::N1, m2 = L::m2, p2 = L::p2, U2 = L::U2;
     static_assert(LX * BC >= nx && NRG * BR >= nx, "block mapping must cover the mesh");
+    static_assert(2 * NC * NC <= 2 * NP2, "aT must fit in G1..G2");
     extern __shared__ double sm[];
-    __shared__ double red[2][4][NWARP];
+    __shared__ double red[4][NWARP];
     __shared__ double th_amp[kMaxD];
+    double *D0 = sm + L::oD0, *DI0 = sm + L::oDI0, *G0 = sm + L::oG0, *G1 = sm + L::oG1;
+    double *G2 = sm + L::oG2, *aT = G1;                  // aT: setup only (aliases G1..G2)
+    double *WH1 = sm + L::oWH1, *WV1 = sm + L::oWV1, *D1 = sm + L::oD1, *DI1 = sm + L::oDI1;
+    double *R1 = sm + L::oR1, *Z1 = sm + L::oZ1, *T1 = sm + L::oT1, *S1 = sm + L::oS1;
+    double *WH2 = sm + L::oWH2, *WV2 = sm + L::oWV2, *R2 = sm + L::oR2, *E2 = sm + L::oE2;
+    double *AI = sm + L::oAI;
 
-    static_assert(2 * NC * NC <= 2 * (NC + 1) * (NC + 1), "aT must fit in G1..G2");
-    double *D0 = sm;                         // fine diagonal (0 outside the interior)
-    double *DI0 = D0 + NP2;                  // fine 1/diagonal (0 outside)
-    double *G0 = DI0 + NP2;                  // published fine vectors, zero ring
-    double *G1 = G0 + NP2;
-    double *G2 = G1 + NP2;
-    double *aT = G1;                         // [2n^2] setup only (aliases G1..G2)
-    MgLevel lev[NLEV];
-    {
-        double *c = G2 + NP2;
-#pragma unroll
-        for (int l = 0; l < NLEV; ++l) {
-            const int m = NC >> (l + 1), q = (m + 1) * (m + 1);
-            lev[l] = MgLevel{m, c, c + q, c + 2 * q, c + 3 * q, c + 4 * q, c + 5 * q, c + 6 * q};
-            c += 7 * q;
-        }
-    }
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int seg = lane / LX, lx = lane % LX;
     const int rg = warp * RGW + seg;
     const int col0 = lx * BC, row0 = rg * BR;
     const double inv_n3 = 1.0 / ((double)n * n * n);
 
-    // a at the centroid of T_lo / T_up of cell (ci, cj) of a grid with cell width 2^sh h
+    // a at the centroid of T_lo / T_up of cell (ci, cj) of the mesh with cell width 2^sh h
     auto coef = [&](int ci, int cj, int up, int sh) -> double {
-        const int m1 = (up ? 3 * ci + 1 : 3 * ci + 2) << sh;
-        const int m2 = (up ? 3 * cj + 2 : 3 * cj + 1) << sh;
+        const int ma = (up ? 3 * ci + 1 : 3 * ci + 2) << sh;
+        const int mb = (up ? 3 * cj + 2 : 3 * cj + 1) << sh;
         double s = 0.0;
-        for (int j = 0; j < Q.d; ++j) s += th_amp[j] * S[j * W + m1] * S[j * W + m2];
+        for (int j = 0; j < Q.d; ++j) s += th_amp[j] * __ldg(S + j * W + ma) * __ldg(S + j * W + mb);
         return Q.form == 0 ? 1.0 + s : exp(s);
     };
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
-        // ---- K3: coefficient field and all level operators ---------------------------------
+        // ---- K3: coefficients, fine/level-1/level-2 operators -------------------------------
         if (tid < Q.d) {
             const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
             th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
@@ -102,21 +85,16 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             const int cell = e >> 1;
             aT[e] = coef(cell % n, cell / n, e & 1, 0);
         }
-#pragma unroll
-        for (int l = 0; l < NLEV; ++l) {             // coarse operators by rediscretisation
-            const MgLevel L_ = lev[l];
-            const int m = NC >> (l + 1), mp = m + 1, sh = l + 1;
-            for (int e = tid; e < mp * mp; e += NT) {
-                const int i = e % mp, j = e / mp;
-                double h = 0.0, v = 0.0;
-                if (i < m && j >= 1 && j < m) h = 0.5 * (coef(i, j, 0, sh) + coef(i, j - 1, 1, sh));
-                if (j < m && i >= 1 && i < m) v = 0.5 * (coef(i, j, 1, sh) + coef(i - 1, j, 0, sh));
-                L_.wh[e] = h;
-                L_.wv[e] = v;
-                L_.R[e] = 0.0;
-                L_.Z[e] = 0.0;
-                L_.S[e] = 0.0;
-            }
+        for (int e = tid; e < N1; e += NT) {            // level 1 (cell width 2h)
+            const int i = e % p1, j = e / p1;
+            WH1[e] = (i < m1 && j >= 1 && j < m1) ? 0.5 * (coef(i, j, 0, 1) + coef(i, j - 1, 1, 1)) : 0.0;
+            WV1[e] = (j < m1 && i >= 1 && i < m1) ? 0.5 * (coef(i, j, 1, 1) + coef(i - 1, j, 0, 1)) : 0.0;
+            R1[e] = Z1[e] = T1[e] = S1[e] = 0.0;
+        }
+        for (int e = tid; e < L::N2; e += NT) {         // level 2 (cell width 4h)
+            const int i = e % p2, j = e / p2;
+            WH2[e] = (i < m2 && j >= 1 && j < m2) ? 0.5 * (coef(i, j, 0, 2) + coef(i, j - 1, 1, 2)) : 0.0;
+            WV2[e] = (j < m2 && i >= 1 && i < m2) ? 0.5 * (coef(i, j, 1, 2) + coef(i - 1, j, 0, 2)) : 0.0;
         }
         __syncthreads();
 #define WH(i, j) (0.5 * (aT[2 * ((j) * n + (i))] + aT[2 * (((j) - 1) * n + (i)) + 1]))
@@ -128,20 +106,27 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             D0[e] = dv;
             DI0[e] = in ? 1.0 / dv : 0.0;
         }
-#pragma unroll
-        for (int l = 0; l < NLEV; ++l) {
-            const MgLevel L_ = lev[l];
-            const int m = NC >> (l + 1), mp = m + 1;
-            for (int e = tid; e < mp * mp; e += NT) {
-                const int i = e % mp, j = e / mp;
-                const bool in = i >= 1 && i < m && j >= 1 && j < m;
-                const double dv = in ? L_.wh[e] + L_.wh[e - 1] + L_.wv[e] + L_.wv[e - mp] : 0.0;
-                L_.d[e] = dv;
-                L_.di[e] = in ? 1.0 / dv : 0.0;
-            }
+        for (int e = tid; e < N1; e += NT) {
+            const int i = e % p1, j = e / p1;
+            const bool in = i >= 1 && i < m1 && j >= 1 && j < m1;
+            const double dv = in ? WH1[e] + WH1[e - 1] + WV1[e] + WV1[e - p1] : 0.0;
+            D1[e] = dv;
+            DI1[e] = in ? 1.0 / dv : 0.0;
         }
-        // fine coupling weights in registers: zero on edges that touch the ring or padding
-        double cE[BR][BC + 1], cN[BR + 1][BC];
+        for (int e = tid; e < U2 * U2; e += NT) {        // dense level-2 operator, row-major
+            const int a = e / U2, c = e % U2;
+            const int ia = a % (m2 - 1) + 1, ja = a / (m2 - 1) + 1;
+            const int ic = c % (m2 - 1) + 1, jc = c / (m2 - 1) + 1;
+            const int g = ja * p2 + ia;
+            double v = 0.0;
+            if (a == c) v = WH2[g] + WH2[g - 1] + WV2[g] + WV2[g - p2];
+            else if (jc == ja && ic == ia + 1) v = -WH2[g];
+            else if (jc == ja && ic == ia - 1) v = -WH2[g - 1];
+            else if (ic == ia && jc == ja + 1) v = -WV2[g];
+            else if (ic == ia && jc == ja - 1) v = -WV2[g - p2];
+            AI[e] = v;
+        }
+        double cE[BR][BC + 1], cN[BR + 1][BC];          // fine couplings, zero at ring / padding
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
@@ -159,13 +144,29 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #undef WH
 #undef WV
         __syncthreads();
-        for (int e = tid; e < NP2; e += NT) {        // zero rings of the fine grids (aT is dead)
-            G0[e] = 0.0;
-            G1[e] = 0.0;
-            G2[e] = 0.0;
+        for (int e = tid; e < NP2; e += NT) G0[e] = G1[e] = G2[e] = 0.0;   // aT is dead now
+        // Gauss-Jordan inversion in place (SPD: no pivoting).  Step k copies row k and column k
+        // (old values) to scratch (R2 / E2 are free during setup), then updates every entry.
+        for (int k = 0; k < U2; ++k) {
+            __syncthreads();
+            for (int q = tid; q < U2; q += NT) {
+                R2[q] = AI[k * U2 + q];
+                E2[q] = AI[q * U2 + k];
+            }
+            __syncthreads();
+            const double piv = 1.0 / R2[k];
+            for (int e = tid; e < U2 * U2; e += NT) {
+                const int i = e / U2, j = e % U2;
+                double v;
+                if (i == k && j == k) v = piv;
+                else if (i == k) v = R2[j] * piv;
+                else if (j == k) v = -E2[i] * piv;
+                else v = fma(-E2[i] * piv, R2[j], AI[e]);
+                AI[e] = v;
+            }
         }
         __syncthreads();
-        // node (q, c) of this thread: fine grid index e = (row0+q+1)*np + col0+c+1 (may be padding)
+
         const int ebase = (row0 + 1) * np + col0 + 1;
         auto valid = [&](int q, int c) { return col0 + c + 1 <= nx && row0 + q + 1 <= nx; };
         auto publish = [&](double *Gd, const double (&v)[BR][BC]) {
@@ -175,7 +176,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < BC; ++c)
                     if (valid(q, c)) Gd[ebase + q * np + c] = v[q][c];
         };
-        // A v at this thread's nodes; neighbours inside the block from registers, others from Gs
         auto apply_fine = [&](const double *Gs, const double (&v)[BR][BC], double (&out)[BR][BC]) {
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -193,10 +193,11 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     out[q][c] = fma(-cN[q][c], vd, a);
                 }
         };
-        // ---- the V(1,1) cycle: z = M^-1 rin (rin must be published in G0 before the call) ----
-        // Every phase reads only values published before the preceding barrier and recomputes
-        // the few derived neighbour values it needs (pre-smoothed iterates omega D^-1 R,
-        // residuals, prolongated corrections) instead of waiting for them: 8 barriers per cycle.
+        auto A1 = [&](const double *Zs, int e) -> double {     // level-1 operator at node e
+            return D1[e] * Zs[e] - WH1[e] * Zs[e + 1] - WH1[e - 1] * Zs[e - 1] - WV1[e] * Zs[e + p1] -
+                   WV1[e - p1] * Zs[e - p1];
+        };
+        // ---- one V(1,1) cycle: z = M^-1 rin; rin is published in G0 by the caller -------------
         auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
             double t[BR][BC];
 #pragma unroll
@@ -206,7 +207,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) {       // fine residual t = r - A z, z = omega D^-1 r
+                for (int c = 0; c < BC; ++c) {       // residual of z = omega D^-1 r (neighbours from G0)
                     const int e = ebase + q * np + c;
                     const double vl = c > 0 ? z[q][c - 1] : kMgOmega * DI0[e - 1] * G0[e - 1];
                     const double vr = c + 1 < BC ? z[q][c + 1] : kMgOmega * DI0[e + 1] * G0[e + 1];
@@ -221,83 +222,76 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
             publish(G1, t);
             __syncthreads();
-            {   // restriction R = P^T to level 1 (n/2 cells)
-                const MgLevel C = lev[0];
-                constexpr int m = NC / 2, mp = m + 1;
-                for (int e = tid; e < mp * mp; e += NT) {
-                    const int I = e % mp, J = e / mp;
-                    if (I < 1 || I >= m || J < 1 || J >= m) continue;
-                    const int f = (2 * J) * np + 2 * I;
-                    C.R[e] = G1[f] + 0.5 * (G1[f - 1] + G1[f + 1] + G1[f - np] + G1[f + np]) +
-                             0.25 * (G1[f - np - 1] + G1[f - np + 1] + G1[f + np - 1] + G1[f + np + 1]);
-                }
+            for (int e = tid; e < N1; e += NT) {        // R1 = P^T t, Z1 = omega D1^-1 R1
+                const int I = e % p1, J = e / p1;
+                if (I < 1 || I >= m1 || J < 1 || J >= m1) continue;
+                const int f = (2 * J) * np + 2 * I;
+                const double rr = G1[f] + 0.5 * (G1[f - 1] + G1[f + 1] + G1[f - np] + G1[f + np]) +
+                                  0.25 * (G1[f - np - 1] + G1[f - np + 1] + G1[f + np - 1] + G1[f + np + 1]);
+                R1[e] = rr;
+                Z1[e] = kMgOmega * DI1[e] * rr;
             }
             __syncthreads();
-            // down sweep: level l pre-smooths (Z = omega D^-1 R) and restricts its residual, which
-            // is recomputed from R at the 9 fine points; the coarsest level is solved exactly
-#pragma unroll
-            for (int l = 0; l + 1 < NLEV; ++l) {
-                const MgLevel C = lev[l], Cn = lev[l + 1];
-                const int m = NC >> (l + 1), mp = m + 1;
-                const int mn = NC >> (l + 2), mnp = mn + 1;
-                for (int e = tid; e < mp * mp; e += NT) C.Z[e] = kMgOmega * C.di[e] * C.R[e];
-                auto tres = [&](int f) -> double {  // residual of the pre-smoothed iterate at f
-                    if (C.di[f] == 0.0) return 0.0;
-                    const double zc = kMgOmega * C.di[f] * C.R[f];
-                    const double az = C.d[f] * zc - C.wh[f] * (kMgOmega * C.di[f + 1] * C.R[f + 1]) -
-                                      C.wh[f - 1] * (kMgOmega * C.di[f - 1] * C.R[f - 1]) -
-                                      C.wv[f] * (kMgOmega * C.di[f + mp] * C.R[f + mp]) -
-                                      C.wv[f - mp] * (kMgOmega * C.di[f - mp] * C.R[f - mp]);
-                    return C.R[f] - az;
-                };
-                for (int e = tid; e < mnp * mnp; e += NT) {
-                    const int I = e % mnp, J = e / mnp;
-                    if (I < 1 || I >= mn || J < 1 || J >= mn) continue;
-                    const int f = (2 * J) * mp + 2 * I;
-                    const double rn = tres(f) + 0.5 * (tres(f - 1) + tres(f + 1) + tres(f - mp) + tres(f + mp)) +
-                                      0.25 * (tres(f - mp - 1) + tres(f - mp + 1) + tres(f + mp - 1) + tres(f + mp + 1));
-                    Cn.R[e] = rn;
-                    if (l + 2 == NLEV) Cn.Z[e] = Cn.di[e] * rn;      // coarsest: exact solve
-                }
-                __syncthreads();
+            for (int e = tid; e < N1; e += NT) {        // level-1 residual of the pre-smoothed Z1
+                if (DI1[e] == 0.0) continue;
+                T1[e] = R1[e] - A1(Z1, e);
             }
-            // up sweep: S_l = smooth(Z_l + P S_{l+1}); neighbours' corrected iterates recomputed
-#pragma unroll
-            for (int l = NLEV - 2; l >= 0; --l) {
-                const MgLevel C = lev[l], Cn = lev[l + 1];
-                const int m = NC >> (l + 1), mp = m + 1, mnp = (NC >> (l + 2)) + 1;
-                const double *Sn = (l + 2 == NLEV) ? Cn.Z : Cn.S;
-                auto zc = [&](int g) -> double {    // Z + bilinear prolongation of Sn at node g
-                    if (C.di[g] == 0.0) return 0.0;
-                    const int i = g % mp, j = g / mp;
-                    const double *z2 = Sn + (j >> 1) * mnp + (i >> 1);
-                    double v;
-                    if (!(i & 1) && !(j & 1)) v = z2[0];
-                    else if (!(j & 1)) v = 0.5 * (z2[0] + z2[1]);
-                    else if (!(i & 1)) v = 0.5 * (z2[0] + z2[mnp]);
-                    else v = 0.25 * (z2[0] + z2[1] + z2[mnp] + z2[mnp + 1]);
-                    return C.Z[g] + v;
-                };
-                for (int e = tid; e < mp * mp; e += NT) {
-                    if (C.di[e] == 0.0) continue;
-                    const double z0 = zc(e);
-                    const double az = C.d[e] * z0 - C.wh[e] * zc(e + 1) - C.wh[e - 1] * zc(e - 1) -
-                                      C.wv[e] * zc(e + mp) - C.wv[e - mp] * zc(e - mp);
-                    C.S[e] = fma(kMgOmega * C.di[e], C.R[e] - az, z0);
-                }
-                __syncthreads();
+            __syncthreads();
+            for (int a = tid; a < U2; a += NT) {         // R2 = P^T T1 on the level-2 unknowns
+                const int I = a % (m2 - 1) + 1, J = a / (m2 - 1) + 1;
+                const int f = (2 * J) * p1 + 2 * I;
+                R2[a] = T1[f] + 0.5 * (T1[f - 1] + T1[f + 1] + T1[f - p1] + T1[f + p1]) +
+                        0.25 * (T1[f - p1 - 1] + T1[f - p1 + 1] + T1[f + p1 - 1] + T1[f + p1 + 1]);
             }
-            // fine up: z += P S_1 and post-smooth; neighbours' corrected z = omega D^-1 r + P S_1
-            const MgLevel C0 = lev[0];
-            constexpr int m0p = NC / 2 + 1;
-            auto prol = [&](int e) -> double {       // bilinear value of level-1 S at fine node e
+            __syncthreads();
+            // E2 = A2^-1 R2: row a by the thread pair (2a, 2a+1), fixed split of the sum
+            for (int h = tid; h < 2 * ((U2 + 15) / 16) * 16; h += NT) {
+                const int a = h >> 1, half = h & 1;
+                double sum = 0.0;
+                if (a < U2) {
+                    const double *row = AI + a * U2;
+                    double s0 = 0.0, s1 = 0.0;
+                    for (int c = 2 * half; c < U2; c += 4) {
+                        s0 = fma(row[c], R2[c], s0);
+                        if (c + 1 < U2) s1 = fma(row[c + 1], R2[c + 1], s1);
+                    }
+                    sum = s0 + s1;
+                }
+                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
+                if (a < U2 && !half) E2[a] = sum;
+            }
+            __syncthreads();
+            // level 1: S1 = smooth(Z1 + P E2), neighbours' corrected values recomputed
+            auto e2at = [&](int I, int J) -> double {   // level-2 value at level-2 grid (I, J)
+                return (I >= 1 && I < m2 && J >= 1 && J < m2) ? E2[(J - 1) * (m2 - 1) + I - 1] : 0.0;
+            };
+            auto zc1 = [&](int g) -> double {
+                if (DI1[g] == 0.0) return 0.0;
+                const int i = g % p1, j = g / p1, I = i >> 1, J = j >> 1;
+                double v;
+                if (!(i & 1) && !(j & 1)) v = e2at(I, J);
+                else if (!(j & 1)) v = 0.5 * (e2at(I, J) + e2at(I + 1, J));
+                else if (!(i & 1)) v = 0.5 * (e2at(I, J) + e2at(I, J + 1));
+                else v = 0.25 * (e2at(I, J) + e2at(I + 1, J) + e2at(I, J + 1) + e2at(I + 1, J + 1));
+                return Z1[g] + v;
+            };
+            for (int e = tid; e < N1; e += NT) {
+                if (DI1[e] == 0.0) continue;
+                const double z0 = zc1(e);
+                const double az = D1[e] * z0 - WH1[e] * zc1(e + 1) - WH1[e - 1] * zc1(e - 1) -
+                                  WV1[e] * zc1(e + p1) - WV1[e - p1] * zc1(e - p1);
+                S1[e] = fma(kMgOmega * DI1[e], R1[e] - az, z0);
+            }
+            __syncthreads();
+            // level 0: z += P S1, post-smooth; neighbours' corrected z = omega D^-1 r + P S1
+            auto prol = [&](int e) -> double {
                 const int i = e % np, j = e / np, I = i >> 1, J = j >> 1;
                 if (i < 1 || i > nx || j < 1 || j > nx) return 0.0;
-                const double *z2 = C0.S + J * m0p + I;
+                const double *z2 = S1 + J * p1 + I;
                 if (!(i & 1) && !(j & 1)) return z2[0];
                 if (!(j & 1)) return 0.5 * (z2[0] + z2[1]);
-                if (!(i & 1)) return 0.5 * (z2[0] + z2[m0p]);
-                return 0.25 * (z2[0] + z2[1] + z2[m0p] + z2[m0p + 1]);
+                if (!(i & 1)) return 0.5 * (z2[0] + z2[p1]);
+                return 0.25 * (z2[0] + z2[1] + z2[p1] + z2[p1 + 1]);
             };
             auto zf = [&](int e) -> double { return kMgOmega * DI0[e] * G0[e] + prol(e); };
 #pragma unroll
@@ -340,7 +334,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         bool conv = false;
         int it = 0;
         for (int k = 0;; ++k) {
-            const int buf = k & 1;
             double uu[BR][BC], w[BR][BC];
             publish(G0, r);
             __syncthreads();
@@ -367,7 +360,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 v += __shfl_xor_sync(0xffffffffu, v, 4);
                 v += __shfl_xor_sync(0xffffffffu, v, 2);
                 v += __shfl_xor_sync(0xffffffffu, v, 1);
-                if ((lane & 7) == 0) red[buf][lane >> 3][warp] = v;
+                if ((lane & 7) == 0) red[lane >> 3][warp] = v;
             }
             __syncthreads();
             double gs[3];
@@ -375,7 +368,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int q = 0; q < 3; ++q) {
                 double tt[NWARP];
 #pragma unroll
-                for (int ww = 0; ww < NWARP; ++ww) tt[ww] = red[buf][q][ww];
+                for (int ww = 0; ww < NWARP; ++ww) tt[ww] = red[q][ww];
 #pragma unroll
                 for (int h = 1; h < NWARP; h <<= 1)
 #pragma unroll
