@@ -1,23 +1,24 @@
-// pcg_mg.cuh — on-chip CG with a three-level geometric-multigrid preconditioner, one CTA per sample.
+// pcg_mg.cuh — on-chip CG with a four-level geometric-multigrid preconditioner, one CTA per sample.
 //
 // Same P1 discretisation as pde.cu (Z11/Z12); CG in the Chronopoulos-Gear single-reduction form
 //     u = M^-1 r;  w = A u;  gamma = (r,u), delta = (w,u), rho = (r,r)      [one reduction]
 //     beta = gamma/gamma_old;  alpha = gamma/(delta - beta gamma/alpha_old)
 //     p = u + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s,
 // stopping on rho = ||r||_2^2 <= tol^2 ||b||_2^2 (Z13).
-// M^-1 is one symmetric V(1,1) cycle over three nested "/" meshes (n, n/2, n/4 cells): damped
-// Jacobi (omega = 0.8) pre- and post-smoothing on levels 0 and 1, bilinear prolongation P,
+// M^-1 is one symmetric V(1,1) cycle over four nested "/" meshes (n, n/2, n/4, n/8 cells): damped
+// Jacobi (omega = 0.8) pre- and post-smoothing on levels 0-2, bilinear prolongation P,
 // restriction R = P^T, coarse operators by rediscretisation of the same P1 problem (every coarse
 // centroid abscissa is a multiple of h/3, so the fine sin table serves all levels), and an exact
-// solve on level 2 with its dense inverse (formed once per sample by Gauss-Jordan; (n/4-1)^2 = 49
-// unknowns at n = 32).  Same smoother before and after and R = P^T make the cycle symmetric
-// positive definite, so CG stays CG.
+// solve on the coarsest level with its dense inverse (formed once per sample by Gauss-Jordan;
+// (n/8-1)^2 = 9 unknowns at n = 32).  Same smoother before and after and R = P^T make the cycle
+// symmetric positive definite, so CG stays CG.
 //
 // Level 0 (fine): each thread owns a BC x BR block of nodes with x, r, p, s, u and the coupling
 // weights in registers; values needed by other threads are published to shared-memory grids with
-// a zero Dirichlet ring.  Levels 1-2 live in shared memory; every size is a compile-time constant.
+// a zero Dirichlet ring.  Levels 1-3 live in shared memory; every size is a compile-time constant.
 // Reductions are fixed trees, so a sample's result does not depend on the CTA or launch split.
 #pragma once
+#include <type_traits>
 
 namespace usfft {
 
@@ -26,15 +27,21 @@ constexpr double kMgOmega = 0.8;
 template <int NC>
 struct Mg3 {
     static constexpr int n = NC, np = NC + 1, NP2 = np * np;
-    static constexpr int m1 = NC / 2, p1 = m1 + 1, N1 = p1 * p1;
-    static constexpr int m2 = NC / 4, p2 = m2 + 1, N2 = p2 * p2, U2 = (m2 - 1) * (m2 - 1);
+    static constexpr int m1 = NC / 2, p1 = m1 + 1, N1 = p1 * p1;      // smoothed level 1
+    static constexpr int m2 = NC / 4, p2 = m2 + 1, N2 = p2 * p2;      // smoothed level 2
+    static constexpr int m3 = NC / 8, p3 = m3 + 1, N3 = p3 * p3, U3 = (m3 - 1) * (m3 - 1);  // exact
     // shared-memory layout (doubles)
     static constexpr int oD0 = 0, oDI0 = NP2, oG0 = 2 * NP2, oG1 = 3 * NP2, oG2 = 4 * NP2;
-    static constexpr int oWH1 = 5 * NP2, oWV1 = oWH1 + N1, oD1 = oWV1 + N1, oDI1 = oD1 + N1;
-    static constexpr int oR1 = oDI1 + N1, oZ1 = oR1 + N1, oT1 = oZ1 + N1, oS1 = oT1 + N1;
-    static constexpr int oWH2 = oS1 + N1, oWV2 = oWH2 + N2, oR2 = oWV2 + N2, oE2 = oR2 + U2;
-    static constexpr int oAI = oE2 + U2;                 // dense inverse of the level-2 operator
-    __host__ __device__ static constexpr int doubles() { return oAI + U2 * U2; }
+    static constexpr int oL1 = 5 * NP2;                  // WH, WV, D, DI, R, Z, T, S of level 1
+    static constexpr int oL2 = oL1 + 8 * N1;             // same for level 2
+    static constexpr int oWH3 = oL2 + 8 * N2, oWV3 = oWH3 + N3, oR3 = oWV3 + N3, oE3 = oR3 + U3;
+    static constexpr int oAI = oE3 + U3;                 // dense inverse of the level-3 operator
+    __host__ __device__ static constexpr int doubles() { return oAI + U3 * U3; }
+};
+
+// one smoothed coarse level (arrays in shared memory, zero rings)
+struct MgLv {
+    double *WH, *WV, *D, *DI, *R, *Z, *T, *S;
 };
 
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
@@ -45,7 +52,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     using L = Mg3<NC>;
     constexpr int RGW = 32 / LX, NRG = NWARP * RGW, NT = NWARP * 32;
     constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1, NP2 = L::NP2;
-    constexpr int m1 = L::m1, p1 = L::p1, N1 = L::N1, m2 = L::m2, p2 = L::p2, U2 = L::U2;
+    constexpr int m3 = L::m3, p3 = L::p3, U3 = L::U3;
     static_assert(LX * BC >= nx && NRG * BR >= nx, "block mapping must cover the mesh");
     static_assert(2 * NC * NC <= 2 * NP2, "aT must fit in G1..G2");
     extern __shared__ double sm[];
@@ -53,9 +60,11 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     __shared__ double th_amp[kMaxD];
     double *D0 = sm + L::oD0, *DI0 = sm + L::oDI0, *G0 = sm + L::oG0, *G1 = sm + L::oG1;
     double *G2 = sm + L::oG2, *aT = G1;                  // aT: setup only (aliases G1..G2)
-    double *WH1 = sm + L::oWH1, *WV1 = sm + L::oWV1, *D1 = sm + L::oD1, *DI1 = sm + L::oDI1;
-    double *R1 = sm + L::oR1, *Z1 = sm + L::oZ1, *T1 = sm + L::oT1, *S1 = sm + L::oS1;
-    double *WH2 = sm + L::oWH2, *WV2 = sm + L::oWV2, *R2 = sm + L::oR2, *E2 = sm + L::oE2;
+    const MgLv V1{sm + L::oL1, sm + L::oL1 + L::N1, sm + L::oL1 + 2 * L::N1, sm + L::oL1 + 3 * L::N1,
+                  sm + L::oL1 + 4 * L::N1, sm + L::oL1 + 5 * L::N1, sm + L::oL1 + 6 * L::N1, sm + L::oL1 + 7 * L::N1};
+    const MgLv V2{sm + L::oL2, sm + L::oL2 + L::N2, sm + L::oL2 + 2 * L::N2, sm + L::oL2 + 3 * L::N2,
+                  sm + L::oL2 + 4 * L::N2, sm + L::oL2 + 5 * L::N2, sm + L::oL2 + 6 * L::N2, sm + L::oL2 + 7 * L::N2};
+    double *WH3 = sm + L::oWH3, *WV3 = sm + L::oWV3, *R3 = sm + L::oR3, *E3 = sm + L::oE3;
     double *AI = sm + L::oAI;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
@@ -72,10 +81,32 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         for (int j = 0; j < Q.d; ++j) s += th_amp[j] * __ldg(S + j * W + ma) * __ldg(S + j * W + mb);
         return Q.form == 0 ? 1.0 + s : exp(s);
     };
+    // rediscretised edge weights of a coarse level (cell width 2^SH h, M cells)
+    auto level_weights = [&](const MgLv &V, auto mconst, int sh) {
+        constexpr int M = decltype(mconst)::value, MP = M + 1;
+        for (int e = tid; e < MP * MP; e += NT) {
+            const int i = e % MP, j = e / MP;
+            V.WH[e] = (i < M && j >= 1 && j < M) ? 0.5 * (coef(i, j, 0, sh) + coef(i, j - 1, 1, sh)) : 0.0;
+            V.WV[e] = (j < M && i >= 1 && i < M) ? 0.5 * (coef(i, j, 1, sh) + coef(i - 1, j, 0, sh)) : 0.0;
+            V.R[e] = V.Z[e] = V.T[e] = V.S[e] = 0.0;
+        }
+    };
+    auto level_diag = [&](const MgLv &V, auto mconst) {
+        constexpr int M = decltype(mconst)::value, MP = M + 1;
+        for (int e = tid; e < MP * MP; e += NT) {
+            const int i = e % MP, j = e / MP;
+            const bool in = i >= 1 && i < M && j >= 1 && j < M;
+            const double dv = in ? V.WH[e] + V.WH[e - 1] + V.WV[e] + V.WV[e - MP] : 0.0;
+            V.D[e] = dv;
+            V.DI[e] = in ? 1.0 / dv : 0.0;
+        }
+    };
+    using C1 = std::integral_constant<int, L::m1>;
+    using C2 = std::integral_constant<int, L::m2>;
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
-        // ---- K3: coefficients, fine/level-1/level-2 operators -------------------------------
+        // ---- K3: coefficients and the operators of all levels --------------------------------
         if (tid < Q.d) {
             const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
             th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
@@ -85,16 +116,12 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             const int cell = e >> 1;
             aT[e] = coef(cell % n, cell / n, e & 1, 0);
         }
-        for (int e = tid; e < N1; e += NT) {            // level 1 (cell width 2h)
-            const int i = e % p1, j = e / p1;
-            WH1[e] = (i < m1 && j >= 1 && j < m1) ? 0.5 * (coef(i, j, 0, 1) + coef(i, j - 1, 1, 1)) : 0.0;
-            WV1[e] = (j < m1 && i >= 1 && i < m1) ? 0.5 * (coef(i, j, 1, 1) + coef(i - 1, j, 0, 1)) : 0.0;
-            R1[e] = Z1[e] = T1[e] = S1[e] = 0.0;
-        }
-        for (int e = tid; e < L::N2; e += NT) {         // level 2 (cell width 4h)
-            const int i = e % p2, j = e / p2;
-            WH2[e] = (i < m2 && j >= 1 && j < m2) ? 0.5 * (coef(i, j, 0, 2) + coef(i, j - 1, 1, 2)) : 0.0;
-            WV2[e] = (j < m2 && i >= 1 && i < m2) ? 0.5 * (coef(i, j, 1, 2) + coef(i - 1, j, 0, 2)) : 0.0;
+        level_weights(V1, C1{}, 1);
+        level_weights(V2, C2{}, 2);
+        for (int e = tid; e < L::N3; e += NT) {
+            const int i = e % p3, j = e / p3;
+            WH3[e] = (i < m3 && j >= 1 && j < m3) ? 0.5 * (coef(i, j, 0, 3) + coef(i, j - 1, 1, 3)) : 0.0;
+            WV3[e] = (j < m3 && i >= 1 && i < m3) ? 0.5 * (coef(i, j, 1, 3) + coef(i - 1, j, 0, 3)) : 0.0;
         }
         __syncthreads();
 #define WH(i, j) (0.5 * (aT[2 * ((j) * n + (i))] + aT[2 * (((j) - 1) * n + (i)) + 1]))
@@ -106,24 +133,19 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             D0[e] = dv;
             DI0[e] = in ? 1.0 / dv : 0.0;
         }
-        for (int e = tid; e < N1; e += NT) {
-            const int i = e % p1, j = e / p1;
-            const bool in = i >= 1 && i < m1 && j >= 1 && j < m1;
-            const double dv = in ? WH1[e] + WH1[e - 1] + WV1[e] + WV1[e - p1] : 0.0;
-            D1[e] = dv;
-            DI1[e] = in ? 1.0 / dv : 0.0;
-        }
-        for (int e = tid; e < U2 * U2; e += NT) {        // dense level-2 operator, row-major
-            const int a = e / U2, c = e % U2;
-            const int ia = a % (m2 - 1) + 1, ja = a / (m2 - 1) + 1;
-            const int ic = c % (m2 - 1) + 1, jc = c / (m2 - 1) + 1;
-            const int g = ja * p2 + ia;
+        level_diag(V1, C1{});
+        level_diag(V2, C2{});
+        for (int e = tid; e < U3 * U3; e += NT) {        // dense level-3 operator, row-major
+            const int a = e / U3, c = e % U3;
+            const int ia = a % (m3 - 1) + 1, ja = a / (m3 - 1) + 1;
+            const int ic = c % (m3 - 1) + 1, jc = c / (m3 - 1) + 1;
+            const int g = ja * p3 + ia;
             double v = 0.0;
-            if (a == c) v = WH2[g] + WH2[g - 1] + WV2[g] + WV2[g - p2];
-            else if (jc == ja && ic == ia + 1) v = -WH2[g];
-            else if (jc == ja && ic == ia - 1) v = -WH2[g - 1];
-            else if (ic == ia && jc == ja + 1) v = -WV2[g];
-            else if (ic == ia && jc == ja - 1) v = -WV2[g - p2];
+            if (a == c) v = WH3[g] + WH3[g - 1] + WV3[g] + WV3[g - p3];
+            else if (jc == ja && ic == ia + 1) v = -WH3[g];
+            else if (jc == ja && ic == ia - 1) v = -WH3[g - 1];
+            else if (ic == ia && jc == ja + 1) v = -WV3[g];
+            else if (ic == ia && jc == ja - 1) v = -WV3[g - p3];
             AI[e] = v;
         }
         double cE[BR][BC + 1], cN[BR + 1][BC];          // fine couplings, zero at ring / padding
@@ -145,23 +167,22 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #undef WV
         __syncthreads();
         for (int e = tid; e < NP2; e += NT) G0[e] = G1[e] = G2[e] = 0.0;   // aT is dead now
-        // Gauss-Jordan inversion in place (SPD: no pivoting).  Step k copies row k and column k
-        // (old values) to scratch (R2 / E2 are free during setup), then updates every entry.
-        for (int k = 0; k < U2; ++k) {
+        // in-place Gauss-Jordan inverse of the (m3-1)^2 x (m3-1)^2 coarsest operator (SPD, tiny)
+        for (int k = 0; k < U3; ++k) {
             __syncthreads();
-            for (int q = tid; q < U2; q += NT) {
-                R2[q] = AI[k * U2 + q];
-                E2[q] = AI[q * U2 + k];
+            for (int q = tid; q < U3; q += NT) {
+                R3[q] = AI[k * U3 + q];
+                E3[q] = AI[q * U3 + k];
             }
             __syncthreads();
-            const double piv = 1.0 / R2[k];
-            for (int e = tid; e < U2 * U2; e += NT) {
-                const int i = e / U2, j = e % U2;
+            const double piv = 1.0 / R3[k];
+            for (int e = tid; e < U3 * U3; e += NT) {
+                const int i = e / U3, j = e % U3;
                 double v;
                 if (i == k && j == k) v = piv;
-                else if (i == k) v = R2[j] * piv;
-                else if (j == k) v = -E2[i] * piv;
-                else v = fma(-E2[i] * piv, R2[j], AI[e]);
+                else if (i == k) v = R3[j] * piv;
+                else if (j == k) v = -E3[i] * piv;
+                else v = fma(-E3[i] * piv, R3[j], AI[e]);
                 AI[e] = v;
             }
         }
@@ -193,12 +214,27 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     out[q][c] = fma(-cN[q][c], vd, a);
                 }
         };
-        auto A1 = [&](const double *Zs, int e) -> double {     // level-1 operator at node e
-            return D1[e] * Zs[e] - WH1[e] * Zs[e + 1] - WH1[e - 1] * Zs[e - 1] - WV1[e] * Zs[e + p1] -
-                   WV1[e - p1] * Zs[e - p1];
+        // restriction R = P^T from a grid Xf (fine cells MF) to node (I, J) of the next level
+        auto restrict9 = [](const double *Xf, int f, int pf) -> double {
+            return Xf[f] + 0.5 * (Xf[f - 1] + Xf[f + 1] + Xf[f - pf] + Xf[f + pf]) +
+                   0.25 * (Xf[f - pf - 1] + Xf[f - pf + 1] + Xf[f + pf - 1] + Xf[f + pf + 1]);
+        };
+        // bilinear prolongation of a coarse grid Xc (row length pc) to fine node (i, j)
+        auto prol2 = [](const double *Xc, int pc, int i, int j) -> double {
+            const double *z2 = Xc + (j >> 1) * pc + (i >> 1);
+            if (!(i & 1) && !(j & 1)) return z2[0];
+            if (!(j & 1)) return 0.5 * (z2[0] + z2[1]);
+            if (!(i & 1)) return 0.5 * (z2[0] + z2[pc]);
+            return 0.25 * (z2[0] + z2[1] + z2[pc] + z2[pc + 1]);
+        };
+        // level operator A_V Z at node e of a level with row length MP
+        auto applyV = [](const MgLv &V, const double *Zs, int e, int MP) -> double {
+            return V.D[e] * Zs[e] - V.WH[e] * Zs[e + 1] - V.WH[e - 1] * Zs[e - 1] - V.WV[e] * Zs[e + MP] -
+                   V.WV[e - MP] * Zs[e - MP];
         };
         // ---- one V(1,1) cycle: z = M^-1 rin; rin is published in G0 by the caller -------------
         auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
+            constexpr int M1 = L::m1, P1 = L::p1, M2 = L::m2, P2 = L::p2;
             double t[BR][BC];
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -222,76 +258,79 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
             publish(G1, t);
             __syncthreads();
-            for (int e = tid; e < N1; e += NT) {        // R1 = P^T t, Z1 = omega D1^-1 R1
-                const int I = e % p1, J = e / p1;
-                if (I < 1 || I >= m1 || J < 1 || J >= m1) continue;
-                const int f = (2 * J) * np + 2 * I;
-                const double rr = G1[f] + 0.5 * (G1[f - 1] + G1[f + 1] + G1[f - np] + G1[f + np]) +
-                                  0.25 * (G1[f - np - 1] + G1[f - np + 1] + G1[f + np - 1] + G1[f + np + 1]);
-                R1[e] = rr;
-                Z1[e] = kMgOmega * DI1[e] * rr;
+            for (int e = tid; e < P1 * P1; e += NT) {   // level 1: R1 = P^T t, Z1 = omega D1^-1 R1
+                if (V1.DI[e] == 0.0) continue;
+                const int I = e % P1, J = e / P1;
+                const double rr = restrict9(G1, (2 * J) * np + 2 * I, np);
+                V1.R[e] = rr;
+                V1.Z[e] = kMgOmega * V1.DI[e] * rr;
             }
             __syncthreads();
-            for (int e = tid; e < N1; e += NT) {        // level-1 residual of the pre-smoothed Z1
-                if (DI1[e] == 0.0) continue;
-                T1[e] = R1[e] - A1(Z1, e);
+            for (int e = tid; e < P1 * P1; e += NT)
+                if (V1.DI[e] != 0.0) V1.T[e] = V1.R[e] - applyV(V1, V1.Z, e, P1);
+            __syncthreads();
+            for (int e = tid; e < P2 * P2; e += NT) {   // level 2: R2 = P^T T1, Z2 = omega D2^-1 R2
+                if (V2.DI[e] == 0.0) continue;
+                const int I = e % P2, J = e / P2;
+                const double rr = restrict9(V1.T, (2 * J) * P1 + 2 * I, P1);
+                V2.R[e] = rr;
+                V2.Z[e] = kMgOmega * V2.DI[e] * rr;
             }
             __syncthreads();
-            for (int a = tid; a < U2; a += NT) {         // R2 = P^T T1 on the level-2 unknowns
-                const int I = a % (m2 - 1) + 1, J = a / (m2 - 1) + 1;
-                const int f = (2 * J) * p1 + 2 * I;
-                R2[a] = T1[f] + 0.5 * (T1[f - 1] + T1[f + 1] + T1[f - p1] + T1[f + p1]) +
-                        0.25 * (T1[f - p1 - 1] + T1[f - p1 + 1] + T1[f + p1 - 1] + T1[f + p1 + 1]);
+            for (int e = tid; e < P2 * P2; e += NT)
+                if (V2.DI[e] != 0.0) V2.T[e] = V2.R[e] - applyV(V2, V2.Z, e, P2);
+            __syncthreads();
+            if (tid < U3) {                              // level 3: R3 = P^T T2 on its unknowns
+                const int I = tid % (m3 - 1) + 1, J = tid / (m3 - 1) + 1;
+                R3[tid] = restrict9(V2.T, (2 * J) * P2 + 2 * I, P2);
             }
             __syncthreads();
-            // E2 = A2^-1 R2: row a by the thread pair (2a, 2a+1), fixed split of the sum
-            for (int h = tid; h < 2 * ((U2 + 15) / 16) * 16; h += NT) {
-                const int a = h >> 1, half = h & 1;
-                double sum = 0.0;
-                if (a < U2) {
-                    const double *row = AI + a * U2;
-                    double s0 = 0.0, s1 = 0.0;
-                    for (int c = 2 * half; c < U2; c += 4) {
-                        s0 = fma(row[c], R2[c], s0);
-                        if (c + 1 < U2) s1 = fma(row[c + 1], R2[c + 1], s1);
-                    }
-                    sum = s0 + s1;
-                }
-                sum += __shfl_xor_sync(0xffffffffu, sum, 1);
-                if (a < U2 && !half) E2[a] = sum;
+            if (tid < U3) {                              // E3 = A3^-1 R3 (exact coarsest solve)
+                double sacc = 0.0;
+                for (int c = 0; c < U3; ++c) sacc = fma(AI[tid * U3 + c], R3[c], sacc);
+                E3[tid] = sacc;
             }
             __syncthreads();
-            // level 1: S1 = smooth(Z1 + P E2), neighbours' corrected values recomputed
-            auto e2at = [&](int I, int J) -> double {   // level-2 value at level-2 grid (I, J)
-                return (I >= 1 && I < m2 && J >= 1 && J < m2) ? E2[(J - 1) * (m2 - 1) + I - 1] : 0.0;
+            // level 2 up: S2 = smooth(Z2 + P E3); neighbours' corrected values recomputed
+            auto e3at = [&](int I, int J) -> double {
+                return (I >= 1 && I < m3 && J >= 1 && J < m3) ? E3[(J - 1) * (m3 - 1) + I - 1] : 0.0;
             };
-            auto zc1 = [&](int g) -> double {
-                if (DI1[g] == 0.0) return 0.0;
-                const int i = g % p1, j = g / p1, I = i >> 1, J = j >> 1;
+            auto zc2 = [&](int g) -> double {
+                if (V2.DI[g] == 0.0) return 0.0;
+                const int i = g % P2, j = g / P2, I = i >> 1, J = j >> 1;
                 double v;
-                if (!(i & 1) && !(j & 1)) v = e2at(I, J);
-                else if (!(j & 1)) v = 0.5 * (e2at(I, J) + e2at(I + 1, J));
-                else if (!(i & 1)) v = 0.5 * (e2at(I, J) + e2at(I, J + 1));
-                else v = 0.25 * (e2at(I, J) + e2at(I + 1, J) + e2at(I, J + 1) + e2at(I + 1, J + 1));
-                return Z1[g] + v;
+                if (!(i & 1) && !(j & 1)) v = e3at(I, J);
+                else if (!(j & 1)) v = 0.5 * (e3at(I, J) + e3at(I + 1, J));
+                else if (!(i & 1)) v = 0.5 * (e3at(I, J) + e3at(I, J + 1));
+                else v = 0.25 * (e3at(I, J) + e3at(I + 1, J) + e3at(I, J + 1) + e3at(I + 1, J + 1));
+                return V2.Z[g] + v;
             };
-            for (int e = tid; e < N1; e += NT) {
-                if (DI1[e] == 0.0) continue;
-                const double z0 = zc1(e);
-                const double az = D1[e] * z0 - WH1[e] * zc1(e + 1) - WH1[e - 1] * zc1(e - 1) -
-                                  WV1[e] * zc1(e + p1) - WV1[e - p1] * zc1(e - p1);
-                S1[e] = fma(kMgOmega * DI1[e], R1[e] - az, z0);
+            for (int e = tid; e < P2 * P2; e += NT) {
+                if (V2.DI[e] == 0.0) continue;
+                const double z0 = zc2(e);
+                const double az = V2.D[e] * z0 - V2.WH[e] * zc2(e + 1) - V2.WH[e - 1] * zc2(e - 1) -
+                                  V2.WV[e] * zc2(e + P2) - V2.WV[e - P2] * zc2(e - P2);
+                V2.S[e] = fma(kMgOmega * V2.DI[e], V2.R[e] - az, z0);
             }
             __syncthreads();
-            // level 0: z += P S1, post-smooth; neighbours' corrected z = omega D^-1 r + P S1
+            // level 1 up: S1 = smooth(Z1 + P S2)
+            auto zc1 = [&](int g) -> double {
+                if (V1.DI[g] == 0.0) return 0.0;
+                return V1.Z[g] + prol2(V2.S, P2, g % P1, g / P1);
+            };
+            for (int e = tid; e < P1 * P1; e += NT) {
+                if (V1.DI[e] == 0.0) continue;
+                const double z0 = zc1(e);
+                const double az = V1.D[e] * z0 - V1.WH[e] * zc1(e + 1) - V1.WH[e - 1] * zc1(e - 1) -
+                                  V1.WV[e] * zc1(e + P1) - V1.WV[e - P1] * zc1(e - P1);
+                V1.S[e] = fma(kMgOmega * V1.DI[e], V1.R[e] - az, z0);
+            }
+            __syncthreads();
+            // level 0 up: z += P S1, post-smooth; neighbours' corrected z = omega D^-1 r + P S1
             auto prol = [&](int e) -> double {
-                const int i = e % np, j = e / np, I = i >> 1, J = j >> 1;
+                const int i = e % np, j = e / np;
                 if (i < 1 || i > nx || j < 1 || j > nx) return 0.0;
-                const double *z2 = S1 + J * p1 + I;
-                if (!(i & 1) && !(j & 1)) return z2[0];
-                if (!(j & 1)) return 0.5 * (z2[0] + z2[1]);
-                if (!(i & 1)) return 0.5 * (z2[0] + z2[p1]);
-                return 0.25 * (z2[0] + z2[1] + z2[p1] + z2[p1 + 1]);
+                return prol2(V1.S, P1, i, j);
             };
             auto zf = [&](int e) -> double { return kMgOmega * DI0[e] * G0[e] + prol(e); };
 #pragma unroll
