@@ -124,12 +124,12 @@ def usfft_lattice(ctx: Context, plan: Plan, b0: int, nb: int, nodes=None, I_prev
 
 
 def pde_desc(cfg: dict, maxit: int = 20000, tol: float = 1e-12, precond: str | None = None):
-    """precond: "jacobi" or "mg" (default: cfg["precond"], else "mg" where implemented)."""
+    """precond: "jacobi" (default) or "mg" (multigrid-preconditioned CG, n = 16, 32)."""
     amp = np.ascontiguousarray(cfg["amp"][: cfg["d"]], dtype=np.float64)
     theta = {"sin": 0, "tent": 1, "probit": 2}[cfg["theta"]]
     form = {"affine": 0, "exp": 1}[cfg["form"]]
     f_kind = {"x2": 0}[cfg.get("f", "x2")]
-    pc = precond or cfg.get("precond") or ("mg" if cfg["n"] in (16, 32) else "jacobi")
+    pc = precond or cfg.get("precond") or "jacobi"
     dsc = N.PdeDesc(cfg["n"], cfg["d"], theta, form, f_kind, maxit,
                     amp.ctypes.data_as(C.POINTER(C.c_double)), tol, {"jacobi": 0, "mg": 1}[pc], 0)
     return dsc, amp
