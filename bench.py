@@ -231,14 +231,14 @@ def run_ours(args):
                        "nJ": nJ, "s_tilde": s_t, "cg_iters_mean": iters_all / max(samples, 1),
                        "l2": "flushed between timed steps (256 MB write)",
                        "parallelism": f"samples sharded over {world} GPU(s)"},
-            "roofline": {"kernel": "k_pcg (batched Jacobi PCG, on-chip)", "bound": "alu",
+            "roofline": {"kernel": "k_pcg_reg (batched Jacobi PCG, register-resident, 1 CTA/sample)", "bound": "alu",
                          "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": ach / fp64_peak if fp64_peak else None,
                          "traffic": (ncu_traffic("k_pcg_reg") or {}).get("bytes"),
                          "traffic_source": (ncu_traffic("k_pcg_reg") or {}).get("source"),
                          "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz",
                          "flops_per_node_iter": FLOPS_PER_NODE_ITER},
-            "fft": {"kernel": "k_dft_direct + k_kappa", "ms_per_step": fft_ms,
+            "fft": {"kernel": "k_fft_rader_t (Rader/Stockham) + k_kappa", "ms_per_step": fft_ms,
                     "achieved_gbs": fft_bytes / (fft_ms / 1e3) / 1e9 if fft_ms else None,
                     "hbm_peak_gbs": pk["hbm_gbs"],
                     "frac": (fft_bytes / (fft_ms / 1e3) / 1e9) / pk["hbm_gbs"] if fft_ms else None},

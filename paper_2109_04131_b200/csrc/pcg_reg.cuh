@@ -43,9 +43,12 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
     __shared__ double red[2][4][NWARP];          // [parity][gamma, delta, rho, pad][warp]
     __shared__ unsigned long long dminmax[2];    // bit patterns of min / max diagonal (d > 0)
     __shared__ double th_amp[kMaxD];
-    __shared__ double hr[2][2][NRG][NCOL];       // [parity][top, bottom row][row group][col]: r_k
-    __shared__ double hw[2][2][NRG][NCOL];       // w_k
-    __shared__ double hs[2][2][NRG][NCOL];       // s_{k-1}
+    // edge-row halo buffers in dynamic shared memory after aT and dg:
+    // [parity][top, bottom row][row group][col] of r_k, w_k, s_{k-1}
+    typedef double HaloArr[2][2][NRG][NCOL];
+    HaloArr &hr = *reinterpret_cast<HaloArr *>(sm + 2 * NC * NC + (NC + 1) * (NC + 1));
+    HaloArr &hw = *reinterpret_cast<HaloArr *>(sm + 2 * NC * NC + (NC + 1) * (NC + 1) + 4 * NRG * NCOL);
+    HaloArr &hs = *reinterpret_cast<HaloArr *>(sm + 2 * NC * NC + (NC + 1) * (NC + 1) + 8 * NRG * NCOL);
 
     constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1;   // NC = cells per side (== Q.n)
     double *aT = sm;                             // [2 n^2] coefficient at triangle centroids

@@ -207,7 +207,8 @@ usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q
                             const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
                             int32_t *iters, double *relres, int32_t *noconv, const double *S) {
     const int n = Q.n;
-    const size_t dyn = sizeof(double) * (size_t)(2 * n * n + (n + 1) * (n + 1));
+    constexpr int NRG = NWARP * (32 / LX), NCOL = LX * BC;
+    const size_t dyn = sizeof(double) * (size_t)(2 * n * n + (n + 1) * (n + 1) + 12 * NRG * NCOL);
     auto kern = k_pcg_reg<NC, BC, BR, LX, NWARP, MINB>;
     USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int per_sm = 0;
@@ -328,6 +329,8 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
         const char *lay = getenv("USFFT_PCG_LAYOUT");       // experiments: thread block of nodes
         if (lay && lay[0] == '1')
             s = launch_pcg_reg<32, 1, 4, 32, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        else if (lay && lay[0] == '4')                      // 4 columns x 2 rows per thread
+            s = launch_pcg_reg<32, 4, 2, 8, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
         else if (getenv("USFFT_PCG4"))
             s = launch_pcg_reg<32, 2, 4, 16, 4, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
         else
