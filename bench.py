@@ -131,6 +131,8 @@ def run_ours(args):
     if world > 1:
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     cfg = config(args.config)
+    if args.precond:
+        cfg["precond"] = args.precond
     t_b = args.t if args.t else min(5, cfg["d"])
     det, I_prev, kt = setup_detector(cfg, local, group, t_b)
     s_t = cfg["s_local"] if t_b < cfg["d"] else cfg["s"]
@@ -336,6 +338,7 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--precond", default="", choices=["", "jacobi", "mg"])
     args = ap.parse_args()
     if args.impl == "reference":
         run_reference(args)

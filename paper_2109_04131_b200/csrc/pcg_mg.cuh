@@ -34,8 +34,8 @@ struct Mg3 {
     static constexpr int oD0 = 0, oDI0 = NP2, oG0 = 2 * NP2, oG1 = 3 * NP2, oG2 = 4 * NP2;
     static constexpr int oL1 = 5 * NP2;                  // WH, WV, D, DI, R, Z, T, S of level 1
     static constexpr int oL2 = oL1 + 8 * N1;             // same for level 2
-    static constexpr int oWH3 = oL2 + 8 * N2, oWV3 = oWH3 + N3, oR3 = oWV3 + N3, oE3 = oR3 + U3;
-    static constexpr int oAI = oE3 + U3;                 // dense inverse of the level-3 operator
+    static constexpr int oWH3 = oL2 + 8 * N2, oWV3 = oWH3 + N3, oR3 = oWV3 + N3, oE3 = oR3 + N3;
+    static constexpr int oAI = oE3 + N3;                 // dense inverse of the level-3 operator
     __host__ __device__ static constexpr int doubles() { return oAI + U3 * U3; }
 };
 
@@ -187,6 +187,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
         }
         __syncthreads();
+        for (int e = tid; e < L::N3; e += NT) E3[e] = 0.0;      // padded grid with zero ring
+        __syncthreads();
 
         const int ebase = (row0 + 1) * np + col0 + 1;
         auto valid = [&](int q, int c) { return col0 + c + 1 <= nx && row0 + q + 1 <= nx; };
@@ -214,12 +216,12 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     out[q][c] = fma(-cN[q][c], vd, a);
                 }
         };
-        // restriction R = P^T from a grid Xf (fine cells MF) to node (I, J) of the next level
+        // restriction R = P^T from a grid Xf (row length pf) to the node whose fine centre is f
         auto restrict9 = [](const double *Xf, int f, int pf) -> double {
             return Xf[f] + 0.5 * (Xf[f - 1] + Xf[f + 1] + Xf[f - pf] + Xf[f + pf]) +
                    0.25 * (Xf[f - pf - 1] + Xf[f - pf + 1] + Xf[f + pf - 1] + Xf[f + pf + 1]);
         };
-        // bilinear prolongation of a coarse grid Xc (row length pc) to fine node (i, j)
+        // bilinear prolongation of a coarse grid Xc (row length pc, zero ring) to fine node (i, j)
         auto prol2 = [](const double *Xc, int pc, int i, int j) -> double {
             const double *z2 = Xc + (j >> 1) * pc + (i >> 1);
             if (!(i & 1) && !(j & 1)) return z2[0];
@@ -232,9 +234,25 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             return V.D[e] * Zs[e] - V.WH[e] * Zs[e + 1] - V.WH[e - 1] * Zs[e - 1] - V.WV[e] * Zs[e + MP] -
                    V.WV[e - MP] * Zs[e - MP];
         };
+        // loop over the interior nodes (I, J in [1, M-1]) of a coarse level: compile-time trip
+        // counts, e = J * (M + 1) + I
+        auto for_interior = [&](auto mconst, auto body) {
+            constexpr int M = decltype(mconst)::value, MI = M - 1, U = MI * MI;
+#pragma unroll
+            for (int k = 0; k < (U + NT - 1) / NT; ++k) {
+                const int q = tid + k * NT;
+                if (q < U) {
+                    const int I = q % MI + 1, J = q / MI + 1;
+                    body(J * (M + 1) + I, I, J);
+                }
+            }
+        };
         // ---- one V(1,1) cycle: z = M^-1 rin; rin is published in G0 by the caller -------------
+        // Short single-purpose phases (restrict / residual / prolongate / smooth), one barrier each.
         auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
-            constexpr int M1 = L::m1, P1 = L::p1, M2 = L::m2, P2 = L::p2;
+            constexpr int P1 = L::p1, P2 = L::p2;
+            using K1 = std::integral_constant<int, L::m1>;
+            using K2 = std::integral_constant<int, L::m2>;
             double t[BR][BC];
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -258,75 +276,54 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
             publish(G1, t);
             __syncthreads();
-            for (int e = tid; e < P1 * P1; e += NT) {   // level 1: R1 = P^T t, Z1 = omega D1^-1 R1
-                if (V1.DI[e] == 0.0) continue;
-                const int I = e % P1, J = e / P1;
+            for_interior(K1{}, [&](int e, int I, int J) {        // R1 = P^T t, Z1 = omega D1^-1 R1
                 const double rr = restrict9(G1, (2 * J) * np + 2 * I, np);
                 V1.R[e] = rr;
                 V1.Z[e] = kMgOmega * V1.DI[e] * rr;
-            }
+            });
             __syncthreads();
-            for (int e = tid; e < P1 * P1; e += NT)
-                if (V1.DI[e] != 0.0) V1.T[e] = V1.R[e] - applyV(V1, V1.Z, e, P1);
+            for_interior(K1{}, [&](int e, int, int) { V1.T[e] = V1.R[e] - applyV(V1, V1.Z, e, P1); });
             __syncthreads();
-            for (int e = tid; e < P2 * P2; e += NT) {   // level 2: R2 = P^T T1, Z2 = omega D2^-1 R2
-                if (V2.DI[e] == 0.0) continue;
-                const int I = e % P2, J = e / P2;
+            for_interior(K2{}, [&](int e, int I, int J) {        // R2 = P^T T1, Z2 = omega D2^-1 R2
                 const double rr = restrict9(V1.T, (2 * J) * P1 + 2 * I, P1);
                 V2.R[e] = rr;
                 V2.Z[e] = kMgOmega * V2.DI[e] * rr;
+            });
+            __syncthreads();
+            for_interior(K2{}, [&](int e, int, int) { V2.T[e] = V2.R[e] - applyV(V2, V2.Z, e, P2); });
+            __syncthreads();
+            if (warp == 0) {                                     // level 3: exact, one warp
+                if (lane < U3) {
+                    const int I = lane % (m3 - 1) + 1, J = lane / (m3 - 1) + 1;
+                    R3[lane] = restrict9(V2.T, (2 * J) * P2 + 2 * I, P2);
+                }
+                __syncwarp();
+                if (lane < U3) {
+                    double sacc = 0.0;
+#pragma unroll
+                    for (int c = 0; c < U3; ++c) sacc = fma(AI[lane * U3 + c], R3[c], sacc);
+                    const int I = lane % (m3 - 1) + 1, J = lane / (m3 - 1) + 1;
+                    E3[J * p3 + I] = sacc;                       // padded level-3 grid, zero ring
+                }
             }
             __syncthreads();
-            for (int e = tid; e < P2 * P2; e += NT)
-                if (V2.DI[e] != 0.0) V2.T[e] = V2.R[e] - applyV(V2, V2.Z, e, P2);
+            for_interior(K2{}, [&](int e, int I, int J) {        // Zc2 = Z2 + P E3 (into T2)
+                V2.T[e] = V2.Z[e] + prol2(E3, p3, I, J);
+            });
             __syncthreads();
-            if (tid < U3) {                              // level 3: R3 = P^T T2 on its unknowns
-                const int I = tid % (m3 - 1) + 1, J = tid / (m3 - 1) + 1;
-                R3[tid] = restrict9(V2.T, (2 * J) * P2 + 2 * I, P2);
-            }
+            for_interior(K2{}, [&](int e, int, int) {            // S2 = smooth(Zc2)
+                V2.S[e] = fma(kMgOmega * V2.DI[e], V2.R[e] - applyV(V2, V2.T, e, P2), V2.T[e]);
+            });
             __syncthreads();
-            if (tid < U3) {                              // E3 = A3^-1 R3 (exact coarsest solve)
-                double sacc = 0.0;
-                for (int c = 0; c < U3; ++c) sacc = fma(AI[tid * U3 + c], R3[c], sacc);
-                E3[tid] = sacc;
-            }
+            for_interior(K1{}, [&](int e, int I, int J) {        // Zc1 = Z1 + P S2 (into T1)
+                V1.T[e] = V1.Z[e] + prol2(V2.S, P2, I, J);
+            });
             __syncthreads();
-            // level 2 up: S2 = smooth(Z2 + P E3); neighbours' corrected values recomputed
-            auto e3at = [&](int I, int J) -> double {
-                return (I >= 1 && I < m3 && J >= 1 && J < m3) ? E3[(J - 1) * (m3 - 1) + I - 1] : 0.0;
-            };
-            auto zc2 = [&](int g) -> double {
-                if (V2.DI[g] == 0.0) return 0.0;
-                const int i = g % P2, j = g / P2, I = i >> 1, J = j >> 1;
-                double v;
-                if (!(i & 1) && !(j & 1)) v = e3at(I, J);
-                else if (!(j & 1)) v = 0.5 * (e3at(I, J) + e3at(I + 1, J));
-                else if (!(i & 1)) v = 0.5 * (e3at(I, J) + e3at(I, J + 1));
-                else v = 0.25 * (e3at(I, J) + e3at(I + 1, J) + e3at(I, J + 1) + e3at(I + 1, J + 1));
-                return V2.Z[g] + v;
-            };
-            for (int e = tid; e < P2 * P2; e += NT) {
-                if (V2.DI[e] == 0.0) continue;
-                const double z0 = zc2(e);
-                const double az = V2.D[e] * z0 - V2.WH[e] * zc2(e + 1) - V2.WH[e - 1] * zc2(e - 1) -
-                                  V2.WV[e] * zc2(e + P2) - V2.WV[e - P2] * zc2(e - P2);
-                V2.S[e] = fma(kMgOmega * V2.DI[e], V2.R[e] - az, z0);
-            }
+            for_interior(K1{}, [&](int e, int, int) {            // S1 = smooth(Zc1)
+                V1.S[e] = fma(kMgOmega * V1.DI[e], V1.R[e] - applyV(V1, V1.T, e, P1), V1.T[e]);
+            });
             __syncthreads();
-            // level 1 up: S1 = smooth(Z1 + P S2)
-            auto zc1 = [&](int g) -> double {
-                if (V1.DI[g] == 0.0) return 0.0;
-                return V1.Z[g] + prol2(V2.S, P2, g % P1, g / P1);
-            };
-            for (int e = tid; e < P1 * P1; e += NT) {
-                if (V1.DI[e] == 0.0) continue;
-                const double z0 = zc1(e);
-                const double az = V1.D[e] * z0 - V1.WH[e] * zc1(e + 1) - V1.WH[e - 1] * zc1(e - 1) -
-                                  V1.WV[e] * zc1(e + P1) - V1.WV[e - P1] * zc1(e - P1);
-                V1.S[e] = fma(kMgOmega * V1.DI[e], V1.R[e] - az, z0);
-            }
-            __syncthreads();
-            // level 0 up: z += P S1, post-smooth; neighbours' corrected z = omega D^-1 r + P S1
+            // level 0: z += P S1, post-smooth; neighbours' corrected z = omega D^-1 r + P S1
             auto prol = [&](int e) -> double {
                 const int i = e % np, j = e / np;
                 if (i < 1 || i > nx || j < 1 || j > nx) return 0.0;
@@ -337,7 +334,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c)
-                    if (valid(q, c)) z[q][c] += prol(ebase + q * np + c);
+                    if (valid(q, c)) z[q][c] += prol2(V1.S, P1, col0 + c + 1, row0 + q + 1);
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
