@@ -29,6 +29,16 @@ sys.path.insert(0, ROOT)
 METRIC = "usFFT step: PDE samples solved/s + lattice-FFT GB/s vs HBM peak, at 1/2/4/8 B200"
 UNIT = "samples/s"
 FLOPS_PER_NODE_ITER = 22      # Jacobi PCG, 5-point stencil: DESIGN.md §5 (algorithmic count)
+
+
+def mg_flops_per_iter(n: int) -> int:
+    """Algorithmic flops of one multigrid-preconditioned CG iteration on an n x n mesh (DESIGN.md
+    §5): 51 per fine node (smoothing, residual, restriction share, prolongation, A u, 3 dots,
+    4 vector updates), 38 per node of the two smoothed coarse levels, and the level-3 exact solve
+    (9-point restriction + dense (m3-1)^2 product)."""
+    u0, u1, u2 = (n - 1) ** 2, (n // 2 - 1) ** 2, (n // 4 - 1) ** 2
+    u3 = (n // 8 - 1) ** 2
+    return 51 * u0 + 38 * (u1 + u2) + 10 * u3 + 2 * u3 * u3
 FP64_FMA_PER_CLK_PER_SM = 64  # B200 fp64 datapath (DESIGN.md §5): 37 TF at 1.965 GHz x 148 SMs
 
 
@@ -217,8 +227,17 @@ def run_ours(args):
         G = det.G
         P = res.plan
         value = samples / (total_ms / 1e3)
-        # dominant kernel: the batched PCG (k_pcg) -> fp64 ALU roofline
-        flops = FLOPS_PER_NODE_ITER * G * iters_all
+        # dominant kernel: the batched PCG -> fp64 ALU roofline
+        from paper_2109_04131_b200.binding import effective_precond
+        mg = effective_precond(cfg) == "mg"
+        n_mesh = cfg["n"]
+        if mg:
+            kname, kdesc = "k_pcg_mg", "k_pcg_mg (batched multigrid-preconditioned CG, on-chip, 1 CTA/sample)"
+            fpi = mg_flops_per_iter(n_mesh)
+        else:
+            kname, kdesc = "k_pcg_reg", "k_pcg_reg (batched Jacobi PCG, register-resident, 1 CTA/sample)"
+            fpi = FLOPS_PER_NODE_ITER * G
+        flops = fpi * iters_all
         fp64_peak = 148 * FP64_FMA_PER_CLK_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
         ach = flops / (pde_ms / 1e3) / 1e12 / world if pde_ms > 0 else 0.0
         fft_ms = phase.get("fft", 0.0) / args.steps
@@ -233,13 +252,13 @@ def run_ours(args):
                        "nJ": nJ, "s_tilde": s_t, "cg_iters_mean": iters_all / max(samples, 1),
                        "l2": "flushed between timed steps (256 MB write)",
                        "parallelism": f"samples sharded over {world} GPU(s)"},
-            "roofline": {"kernel": "k_pcg_reg (batched Jacobi PCG, register-resident, 1 CTA/sample)", "bound": "alu",
+            "roofline": {"kernel": kdesc, "bound": "alu",
                          "achieved": ach, "peak": fp64_peak, "unit": "TFLOP/s",
                          "frac": ach / fp64_peak if fp64_peak else None,
-                         "traffic": (ncu_traffic("k_pcg_reg") or {}).get("bytes"),
-                         "traffic_source": (ncu_traffic("k_pcg_reg") or {}).get("source"),
+                         "traffic": (ncu_traffic(kname) or {}).get("bytes"),
+                         "traffic_source": (ncu_traffic(kname) or {}).get("source"),
                          "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz",
-                         "flops_per_node_iter": FLOPS_PER_NODE_ITER},
+                         "flops_per_sample_iter": fpi, "precond": "mg" if mg else "jacobi"},
             "fft": {"kernel": "k_fft_rader_t (Rader/Stockham) + k_kappa", "ms_per_step": fft_ms,
                     "achieved_gbs": fft_bytes / (fft_ms / 1e3) / 1e9 if fft_ms else None,
                     "hbm_peak_gbs": pk["hbm_gbs"],

@@ -123,13 +123,23 @@ def usfft_lattice(ctx: Context, plan: Plan, b0: int, nb: int, nodes=None, I_prev
     return [int(v) for v in inj] if injective else None
 
 
+MG_MESHES = (16, 32)      # meshes with a compiled multigrid-preconditioned CG kernel
+
+
+def effective_precond(cfg: dict, precond: str | None = None) -> str:
+    """The preconditioner a solve uses: the explicit choice, else cfg["precond"], else multigrid
+    where it is compiled (n = 16, 32: fastest measured) and Jacobi otherwise."""
+    return precond or cfg.get("precond") or ("mg" if cfg["n"] in MG_MESHES else "jacobi")
+
+
 def pde_desc(cfg: dict, maxit: int = 20000, tol: float = 1e-12, precond: str | None = None):
-    """precond: "jacobi" (default) or "mg" (multigrid-preconditioned CG, n = 16, 32)."""
+    """precond: "jacobi" or "mg" (multigrid-preconditioned CG, n = 16, 32); default see
+    effective_precond."""
     amp = np.ascontiguousarray(cfg["amp"][: cfg["d"]], dtype=np.float64)
     theta = {"sin": 0, "tent": 1, "probit": 2}[cfg["theta"]]
     form = {"affine": 0, "exp": 1}[cfg["form"]]
     f_kind = {"x2": 0}[cfg.get("f", "x2")]
-    pc = precond or cfg.get("precond") or "jacobi"
+    pc = effective_precond(cfg, precond)
     dsc = N.PdeDesc(cfg["n"], cfg["d"], theta, form, f_kind, maxit,
                     amp.ctypes.data_as(C.POINTER(C.c_double)), tol, {"jacobi": 0, "mg": 1}[pc], 0)
     return dsc, amp

@@ -314,8 +314,8 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     const char *force = getenv("USFFT_PCG");
     const bool reg_ok = !(force && force[0] == 's');
     const char *mgl = getenv("USFFT_MG_LAYOUT");
-    if (pde->precond == 1 && n == 32 && mgl && mgl[0] == 'w')        // 512 threads, 1x2 blocks
-        s = launch_pcg_mg<32, 1, 2, 32, 16, 1>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '2')        // 256 threads, 2x2 blocks
+        s = launch_pcg_mg<32, 2, 2, 16, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (pde->precond == 1 && n == 32)                          // 128 threads, 2x4 blocks
         s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (pde->precond == 1 && n == 16)
