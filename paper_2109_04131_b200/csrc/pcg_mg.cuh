@@ -17,15 +17,17 @@
 // lower/upper residue pattern), so the coarse coefficients are lookups into the fine per-triangle
 // table: the d-term coefficient sums are evaluated only for the 2 n^2 fine triangles.
 //
-// Level 0 (fine): each thread owns a BC x BR block of nodes with x, r, p, s, u and the coupling
-// weights in registers; values needed by other threads are published to shared-memory grids with
-// a zero Dirichlet ring.  Levels 1-3 live in shared memory; every size is a compile-time constant.
-// Level 1 runs on the whole CTA; levels 2 and 3 (49 + 9 unknowns at n = 32) run in warp 0 with
-// warp-level synchronisation.  The CG update of r is not published separately: the first V-cycle
-// phase recomputes a neighbour's r_{k+1} = r_k - alpha (w_k + beta s_{k-1}) from the (r, w, s)
-// grids published before the reduction barrier (the same fma sequence the owner runs, so the
-// values are bit-identical).  Eight CTA barriers per CG iteration.
-// Reductions are fixed trees, so a sample's result does not depend on the CTA or launch split.
+// The kernel is bound by shared-memory wavefronts (ncu: LSU data pipe ~85% busy in the previous
+// design), so this one minimises them:
+//  * level 0 (fine): each thread owns a 2 x BR block of nodes with x, r, p, s, u and the coupling
+//    weights in registers (the diagonal is summed from the couplings, not loaded); only the values
+//    neighbours need are published, one grid per exchange, with a zero Dirichlet ring;
+//  * grids of levels 0 and 1 store the even columns, then the odd columns of a row ("split"
+//    rows), so the stride-2 accesses of restriction, prolongation and the 2-column thread blocks
+//    are bank-conflict-free;
+//  * level 1 runs on the whole CTA; levels 2 and 3 (49 + 9 unknowns at n = 32) run in warp 0.
+// Nine CTA barriers per CG iteration.  Reductions are fixed trees, so a sample's result does not
+// depend on the CTA or launch split.
 #pragma once
 #include <type_traits>
 
@@ -35,24 +37,22 @@ constexpr double kMgOmega = 0.8;
 
 template <int NC>
 struct Mg3 {
-    static constexpr int n = NC, np = NC + 1, NP2 = np * np;
-    static constexpr int m1 = NC / 2, p1 = m1 + 1, N1 = p1 * p1;      // smoothed level 1
-    static constexpr int m2 = NC / 4, p2 = m2 + 1, N2 = p2 * p2;      // smoothed level 2
+    static constexpr int n = NC, np = NC + 1, NP2 = np * np, HE = NC / 2 + 1;   // HE even columns
+    static constexpr int m1 = NC / 2, p1 = m1 + 1, N1 = p1 * p1, H1 = m1 / 2 + 1;  // smoothed level 1
+    static constexpr int m2 = NC / 4, p2 = m2 + 1, N2 = p2 * p2;      // smoothed level 2 (natural)
     static constexpr int m3 = NC / 8, p3 = m3 + 1, N3 = p3 * p3, U3 = (m3 - 1) * (m3 - 1);  // exact
-    // shared-memory layout (doubles): fine grids D, D^-1, G0 (r), G1 (fine residual), G2 (u),
-    // Hr, Hw, Hs (CG vectors r, w, s for the neighbours' r update)
-    static constexpr int oD0 = 0, oDI0 = NP2, oG0 = 2 * NP2, oG1 = 3 * NP2, oG2 = 4 * NP2;
-    static constexpr int oHr = 5 * NP2, oHw = 6 * NP2, oHs = 7 * NP2;
-    static constexpr int oL1 = 8 * NP2;                  // WH, WV, D, DI, R, Z, T, S of level 1
-    static constexpr int oL2 = oL1 + 8 * N1;             // same for level 2
+    // shared-memory layout (doubles): fine grids omega D^-1, G0 (z0 = omega D^-1 r), G1 (fine
+    // residual, then u); level 1 WH, WV, omega D^-1, R, Z, T, S; level 2 WH, WV, D, omega D^-1,
+    // R, Z, T, S; level 3 WH, WV, R, E; the dense level-3 inverse.  The per-triangle coefficient
+    // table of the setup aliases G0..G1.
+    static constexpr int oDI0 = 0, oG0 = NP2, oG1 = 2 * NP2;
+    static constexpr int oL1 = 3 * NP2;
+    static constexpr int oL2 = oL1 + 7 * N1;
     static constexpr int oWH3 = oL2 + 8 * N2, oWV3 = oWH3 + N3, oR3 = oWV3 + N3, oE3 = oR3 + N3;
-    static constexpr int oAI = oE3 + N3;                 // dense inverse of the level-3 operator
+    static constexpr int oAI = oE3 + N3;
     __host__ __device__ static constexpr int doubles() { return oAI + U3 * U3; }
-};
-
-// one smoothed coarse level (arrays in shared memory, zero rings)
-struct MgLv {
-    double *WH, *WV, *D, *DI, *R, *Z, *T, *S;
+    // split-row slot of column i (even columns first)
+    __host__ __device__ static constexpr int col1s(int i) { return (i & 1) ? H1 + (i >> 1) : (i >> 1); }
 };
 
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
@@ -62,72 +62,55 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S) {
     using L = Mg3<NC>;
     constexpr int RGW = 32 / LX, NRG = NWARP * RGW, NT = NWARP * 32;
-    constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1, NP2 = L::NP2;
-    constexpr int m1 = L::m1, P1 = L::p1, m2 = L::m2, P2 = L::p2;
+    constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1, NP2 = L::NP2, HE = L::HE;
+    constexpr int m1 = L::m1, P1 = L::p1, N1 = L::N1, H1 = L::H1, m2 = L::m2, P2 = L::p2, N2 = L::N2;
     constexpr int m3 = L::m3, p3 = L::p3, U3 = L::U3;
+    static_assert(BC == 2 && BR % 2 == 0, "2 x BR node blocks (one odd and one even column)");
     static_assert(LX * BC >= nx && NRG * BR >= nx, "block mapping must cover the mesh");
-    static_assert(BC % 2 == 0 && BR % 2 == 0, "even node blocks: prolongation parity is compile-time");
     static_assert(NT % n == 0, "coefficient mapping: whole mesh rows per pass");
-    static_assert(2 * NC * NC <= 2 * NP2, "aT must fit in G1..G2");
+    static_assert(2 * n * n <= 2 * NP2, "coefficient table must fit in G0..G1");
     static_assert(U3 >= 1 && U3 <= 32, "level 3 is solved by one warp");
     extern __shared__ double sm[];
     __shared__ double red[4][NWARP];
     __shared__ double th_amp[kMaxD];
-    double *D0 = sm + L::oD0, *DI0 = sm + L::oDI0, *G0 = sm + L::oG0, *G1 = sm + L::oG1;
-    double *G2 = sm + L::oG2, *aT = G1;                  // aT: setup only (aliases G1..G2)
-    double *Hr = sm + L::oHr, *Hw = sm + L::oHw, *Hs = sm + L::oHs;
-    const MgLv V1{sm + L::oL1, sm + L::oL1 + L::N1, sm + L::oL1 + 2 * L::N1, sm + L::oL1 + 3 * L::N1,
-                  sm + L::oL1 + 4 * L::N1, sm + L::oL1 + 5 * L::N1, sm + L::oL1 + 6 * L::N1, sm + L::oL1 + 7 * L::N1};
-    const MgLv V2{sm + L::oL2, sm + L::oL2 + L::N2, sm + L::oL2 + 2 * L::N2, sm + L::oL2 + 3 * L::N2,
-                  sm + L::oL2 + 4 * L::N2, sm + L::oL2 + 5 * L::N2, sm + L::oL2 + 6 * L::N2, sm + L::oL2 + 7 * L::N2};
+    double *DI0 = sm + L::oDI0, *G0 = sm + L::oG0, *G1 = sm + L::oG1, *aT = G0;
+    double *WH1 = sm + L::oL1, *WV1 = WH1 + N1, *DI1 = WH1 + 2 * N1, *R1 = WH1 + 3 * N1;
+    double *Z1 = WH1 + 4 * N1, *T1 = WH1 + 5 * N1, *S1 = WH1 + 6 * N1;
+    double *WH2 = sm + L::oL2, *WV2 = WH2 + N2, *D2 = WH2 + 2 * N2, *DI2 = WH2 + 3 * N2;
+    double *R2 = WH2 + 4 * N2, *Z2 = WH2 + 5 * N2, *T2 = WH2 + 6 * N2, *S2 = WH2 + 7 * N2;
     double *WH3 = sm + L::oWH3, *WV3 = sm + L::oWV3, *R3 = sm + L::oR3, *E3 = sm + L::oE3;
     double *AI = sm + L::oAI;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int seg = lane / LX, lx = lane % LX;
     const int rg = warp * RGW + seg;
-    const int col0 = lx * BC, row0 = rg * BR;            // both even
+    const int col0 = lx * BC, row0 = rg * BR;            // block: columns 2lx+1 (odd), 2lx+2 (even)
     const double inv_n3 = 1.0 / ((double)n * n * n);
 
-    // a at the centroid of T_lo / T_up of cell (ci, cj) of the mesh with cell width 2^sh h: the
-    // fine triangle with the same centroid (abscissae ma, mb in units of h/3)
-    auto fcoef = [&](int ci, int cj, int up, int sh) -> double {
-        const int ma = (up ? 3 * ci + 1 : 3 * ci + 2) << sh;
-        const int mb = (up ? 3 * cj + 2 : 3 * cj + 1) << sh;
-        return aT[2 * ((mb / 3) * n + ma / 3) + (ma % 3 == 1 ? 1 : 0)];
-    };
-    // rediscretised edge weights of a coarse level (cell width 2^sh h, M cells)
-    auto level_weights = [&](const MgLv &V, auto mconst, int sh) {
-        constexpr int M = decltype(mconst)::value, MP = M + 1;
-        for (int e = tid; e < MP * MP; e += NT) {
-            const int i = e % MP, j = e / MP;
-            V.WH[e] = (i < M && j >= 1 && j < M) ? 0.5 * (fcoef(i, j, 0, sh) + fcoef(i, j - 1, 1, sh)) : 0.0;
-            V.WV[e] = (j < M && i >= 1 && i < M) ? 0.5 * (fcoef(i, j, 1, sh) + fcoef(i - 1, j, 0, sh)) : 0.0;
-            V.R[e] = V.Z[e] = V.T[e] = V.S[e] = 0.0;
-        }
-    };
-    auto level_diag = [&](const MgLv &V, auto mconst) {
-        constexpr int M = decltype(mconst)::value, MP = M + 1;
-        for (int e = tid; e < MP * MP; e += NT) {
-            const int i = e % MP, j = e / MP;
-            const bool in = i >= 1 && i < M && j >= 1 && j < M;
-            const double dv = in ? V.WH[e] + V.WH[e - 1] + V.WV[e] + V.WV[e - MP] : 0.0;
-            V.D[e] = dv;
-            V.DI[e] = in ? 1.0 / dv : 0.0;
+    // interior nodes of a coarse level (I, J in [1, M-1]), q = first + k * STRIDE
+    auto for_interior = [](auto mconst, auto sconst, int first, auto body) {
+        constexpr int M = decltype(mconst)::value, MI = M - 1, U = MI * MI;
+        constexpr int STRIDE = decltype(sconst)::value;
+#pragma unroll
+        for (int k = 0; k < (U + STRIDE - 1) / STRIDE; ++k) {
+            const int q = first + k * STRIDE;
+            if (q < U) body(q % MI + 1, q / MI + 1);
         }
     };
     using C1 = std::integral_constant<int, m1>;
     using C2 = std::integral_constant<int, m2>;
+    using SCTA = std::integral_constant<int, NT>;
+    using SW = std::integral_constant<int, 32>;
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
-        // ---- K3: coefficients and the operators of all levels --------------------------------
+        // ---- K3: coefficients ----------------------------------------------------------------
         if (tid < Q.d) {
             const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
             th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
         }
         __syncthreads();
-        {   // fine per-triangle coefficients a = 1 + sum_j amp_j theta_j S_j(ma) S_j(mb) (or exp):
+        {   // per-triangle a = 1 + sum_j amp_j theta_j S_j(ma) S_j(mb) (or exp) of the fine mesh:
             // thread (ci, cj0) keeps the ci-side factors of every j and sweeps KC rows cj
             constexpr int CJS = NT / n, KC = n / CJS;
             const int ci = tid % n, cj0 = tid / n;
@@ -153,42 +136,74 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
         }
         __syncthreads();
-        level_weights(V1, C1{}, 1);
-        level_weights(V2, C2{}, 2);
-        for (int e = tid; e < L::N3; e += NT) {
-            const int i = e % p3, j = e / p3;
-            WH3[e] = (i < m3 && j >= 1 && j < m3) ? 0.5 * (fcoef(i, j, 0, 3) + fcoef(i, j - 1, 1, 3)) : 0.0;
-            WV3[e] = (j < m3 && i >= 1 && i < m3) ? 0.5 * (fcoef(i, j, 1, 3) + fcoef(i - 1, j, 0, 3)) : 0.0;
-        }
-#define WH(i, j) (0.5 * (aT[2 * ((j) * n + (i))] + aT[2 * (((j) - 1) * n + (i)) + 1]))
-#define WV(i, j) (0.5 * (aT[2 * ((j) * n + (i)) + 1] + aT[2 * ((j) * n + (i) - 1)]))
-        for (int e = tid; e < NP2; e += NT) {
-            const int i = e % np, j = e / np;
-            const bool in = i >= 1 && i <= nx && j >= 1 && j <= nx;
-            const double dv = in ? WH(i, j) + WH(i - 1, j) + WV(i, j) + WV(i, j - 1) : 0.0;
-            D0[e] = dv;
-            DI0[e] = in ? 1.0 / dv : 0.0;
-        }
-        double cE[BR][BC + 1], cN[BR + 1][BC];          // fine couplings, zero at ring / padding
+        // a at the centroid of T_lo / T_up of cell (ci, cj) of the mesh with cell width 2^sh h: the
+        // fine triangle with the same centroid (abscissae ma, mb in units of h/3)
+        auto fcoef = [&](int ci, int cj, int up, int sh) -> double {
+            const int ma = (up ? 3 * ci + 1 : 3 * ci + 2) << sh;
+            const int mb = (up ? 3 * cj + 2 : 3 * cj + 1) << sh;
+            return aT[2 * ((mb / 3) * n + ma / 3) + (ma % 3 == 1 ? 1 : 0)];
+        };
+        // edge weights of node (i, j) of the mesh with M cells of width 2^sh h: to (i+1, j), (i, j+1)
+        auto wh = [&](int i, int j, int M, int sh) -> double {
+            return (i < M && j >= 1 && j < M) ? 0.5 * (fcoef(i, j, 0, sh) + fcoef(i, j - 1, 1, sh)) : 0.0;
+        };
+        auto wv = [&](int i, int j, int M, int sh) -> double {
+            return (j < M && i >= 1 && i < M) ? 0.5 * (fcoef(i, j, 1, sh) + fcoef(i - 1, j, 0, sh)) : 0.0;
+        };
+        double cE[BR][BC + 1], cN[BR + 1][BC];           // fine couplings (ring edges included)
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c <= BC; ++c) {
                 const int i = col0 + c, j = row0 + q + 1;
-                cE[q][c] = (i >= 1 && i + 1 <= nx && j <= nx) ? WH(i, j) : 0.0;
+                cE[q][c] = (i <= nx && j <= nx) ? wh(i, j, n, 0) : 0.0;
             }
 #pragma unroll
         for (int q = 0; q <= BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
                 const int i = col0 + c + 1, j = row0 + q;
-                cN[q][c] = (j >= 1 && j + 1 <= nx && i <= nx) ? WV(i, j) : 0.0;
+                cN[q][c] = (i <= nx && j <= nx) ? wv(i, j, n, 0) : 0.0;
             }
-#undef WH
-#undef WV
+        for (int e = tid; e < NP2; e += NT) {            // omega D^-1 (split rows), zero ring
+            const int j = e / np, s = e % np, i = s < HE ? 2 * s : 2 * (s - HE) + 1;
+            const bool in = i >= 1 && i <= nx && j >= 1 && j <= nx;
+            const double dv = in ? wh(i, j, n, 0) + wh(i - 1, j, n, 0) + wv(i, j, n, 0) + wv(i, j - 1, n, 0) : 1.0;
+            DI0[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+        }
+        for (int e = tid; e < N1; e += NT) {             // level 1 (split rows)
+            const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
+            WH1[e] = wh(I, J, m1, 1);
+            WV1[e] = wv(I, J, m1, 1);
+            R1[e] = Z1[e] = T1[e] = S1[e] = 0.0;
+        }
+        for (int e = tid; e < N2; e += NT) {             // level 2 (natural rows)
+            const int I = e % P2, J = e / P2;
+            WH2[e] = wh(I, J, m2, 2);
+            WV2[e] = wv(I, J, m2, 2);
+            R2[e] = Z2[e] = T2[e] = S2[e] = 0.0;
+        }
+        for (int e = tid; e < L::N3; e += NT) {
+            const int I = e % p3, J = e / p3;
+            WH3[e] = wh(I, J, m3, 3);
+            WV3[e] = wv(I, J, m3, 3);
+            E3[e] = 0.0;
+        }
         __syncthreads();                                 // aT is dead from here on
-        level_diag(V1, C1{});
-        level_diag(V2, C2{});
+        for (int e = tid; e < NP2; e += NT) G0[e] = G1[e] = 0.0;
+        for (int e = tid; e < N1; e += NT) {             // level-1 omega D^-1 (same sum as apply1)
+            const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
+            const bool in = I >= 1 && I < m1 && J >= 1 && J < m1;
+            const double dv = in ? WH1[e] + WH1[J * P1 + L::col1s(I - 1)] + WV1[e] + WV1[e - P1] : 1.0;
+            DI1[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+        }
+        for (int e = tid; e < N2; e += NT) {
+            const int I = e % P2, J = e / P2;
+            const bool in = I >= 1 && I < m2 && J >= 1 && J < m2;
+            const double dv = in ? WH2[e] + WH2[e - 1] + WV2[e] + WV2[e - P2] : 0.0;
+            D2[e] = dv;
+            DI2[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+        }
         for (int e = tid; e < U3 * U3; e += NT) {        // dense level-3 operator, row-major
             const int a = e / U3, c = e % U3;
             const int ia = a % (m3 - 1) + 1, ja = a / (m3 - 1) + 1;
@@ -201,12 +216,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             else if (ic == ia && jc == ja + 1) v = -WV3[g];
             else if (ic == ia && jc == ja - 1) v = -WV3[g - p3];
             AI[e] = v;
-        }
-        for (int e = tid; e < NP2; e += NT) {
-            const int i = e % np, j = e / np;
-            const bool in = i >= 1 && i <= nx && j >= 1 && j <= nx;
-            G0[e] = G1[e] = G2[e] = Hw[e] = Hs[e] = 0.0;
-            Hr[e] = in ? (double)j * inv_n3 : 0.0;       // r_0 = b = h^2 x2
         }
         __syncthreads();
         if (warp == 0) {   // in-place Gauss-Jordan inverse of the coarsest operator (SPD, tiny)
@@ -239,42 +248,59 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
                 __syncwarp();
             }
-            for (int e = lane; e < L::N3; e += 32) E3[e] = 0.0;   // padded grid with zero ring
-            __syncwarp();
         }
+        // (the first barriers of the CG loop order these writes before their uses)
 
-        const int ebase = (row0 + 1) * np + col0 + 1;
+        // ---- level-0 addressing: node (col0 + 1 + c, row0 + 1 + q), c in [-1, BC], q in [-1, BR];
+        // c even is an odd column (slot HE + lx + c/2), c odd an even column (slot lx + (c+1)/2)
+        auto fe = [&](int c, int q) -> int {
+            const int slot = (c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1);
+            return (row0 + 1 + q) * np + slot;
+        };
         auto valid = [&](int q, int c) { return col0 + c + 1 <= nx && row0 + q + 1 <= nx; };
         auto publish = [&](double *Gd, const double (&v)[BR][BC]) {
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c)
-                    if (valid(q, c)) Gd[ebase + q * np + c] = v[q][c];
+                    if (valid(q, c)) Gd[fe(c, q)] = v[q][c];
         };
+        auto diag = [&](int q, int c) -> double {        // same summation order as DI0
+            return cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c];
+        };
+        // A v at the own nodes, neighbour values from the published grid Gs; invalid nodes give 0
         auto apply_fine = [&](const double *Gs, const double (&v)[BR][BC], double (&out)[BR][BC]) {
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    const int e = ebase + q * np + c;
-                    const double vl = c > 0 ? v[q][c - 1] : Gs[e - 1];
-                    const double vr = c + 1 < BC ? v[q][c + 1] : Gs[e + 1];
-                    const double vd = q > 0 ? v[q - 1][c] : Gs[e - np];
-                    const double vu = q + 1 < BR ? v[q + 1][c] : Gs[e + np];
-                    double a = D0[e] * v[q][c];
+                    const double vl = c > 0 ? v[q][c - 1] : Gs[fe(c - 1, q)];
+                    const double vr = c + 1 < BC ? v[q][c + 1] : Gs[fe(c + 1, q)];
+                    const double vd = q > 0 ? v[q - 1][c] : Gs[fe(c, q - 1)];
+                    const double vu = q + 1 < BR ? v[q + 1][c] : Gs[fe(c, q + 1)];
+                    double a = diag(q, c) * v[q][c];
                     a = fma(-cE[q][c + 1], vr, a);
                     a = fma(-cE[q][c], vl, a);
                     a = fma(-cN[q + 1][c], vu, a);
-                    out[q][c] = fma(-cN[q][c], vd, a);
+                    a = fma(-cN[q][c], vd, a);
+                    out[q][c] = valid(q, c) ? a : 0.0;
                 }
         };
-        // restriction R = P^T from a grid Xf (row length pf) to the node whose fine centre is f
-        auto restrict9 = [](const double *Xf, int f, int pf) -> double {
-            return Xf[f] + 0.5 * (Xf[f - 1] + Xf[f + 1] + Xf[f - pf] + Xf[f + pf]) +
-                   0.25 * (Xf[f - pf - 1] + Xf[f - pf + 1] + Xf[f + pf - 1] + Xf[f + pf + 1]);
+        // level-1 node (I, J): split-row offset
+        auto e1 = [](int I, int J) -> int { return J * P1 + L::col1s(I); };
+        // level-1 operator at (I, J) (diagonal summed from the weights, same order as DI1)
+        auto apply1 = [&](const double *Zs, int I, int J) -> double {
+            const int e = e1(I, J), el = e1(I - 1, J), er = e1(I + 1, J);
+            const double whe = WH1[e], whl = WH1[el], wve = WV1[e], wvd = WV1[e - P1];
+            return (whe + whl + wve + wvd) * Zs[e] - whe * Zs[er] - whl * Zs[el] - wve * Zs[e + P1] -
+                   wvd * Zs[e - P1];
         };
-        // bilinear prolongation of a coarse grid Xc (row length pc, zero ring) to fine node (i, j)
+        // level-2 operator (natural layout)
+        auto apply2 = [&](const double *Zs, int e) -> double {
+            return D2[e] * Zs[e] - WH2[e] * Zs[e + 1] - WH2[e - 1] * Zs[e - 1] - WV2[e] * Zs[e + P2] -
+                   WV2[e - P2] * Zs[e - P2];
+        };
+        // bilinear prolongation of a coarse grid Xc (natural rows of length pc, zero ring) to node (i, j)
         auto prol2 = [](const double *Xc, int pc, int i, int j) -> double {
             const double *z2 = Xc + (j >> 1) * pc + (i >> 1);
             if (!(i & 1) && !(j & 1)) return z2[0];
@@ -282,80 +308,62 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             if (!(i & 1)) return 0.5 * (z2[0] + z2[pc]);
             return 0.25 * (z2[0] + z2[1] + z2[pc] + z2[pc + 1]);
         };
-        // level operator A_V Z at node e of a level with row length MP
-        auto applyV = [](const MgLv &V, const double *Zs, int e, int MP) -> double {
-            return V.D[e] * Zs[e] - V.WH[e] * Zs[e + 1] - V.WH[e - 1] * Zs[e - 1] - V.WV[e] * Zs[e + MP] -
-                   V.WV[e - MP] * Zs[e - MP];
-        };
-        // loop over the interior nodes (I, J in [1, M-1]) of a coarse level, e = J (M + 1) + I,
-        // with compile-time trip counts: over the CTA (stride NT) or over warp 0 (stride 32)
-        auto for_interior = [&](auto mconst, auto body) {
-            constexpr int M = decltype(mconst)::value, MI = M - 1, U = MI * MI;
-#pragma unroll
-            for (int k = 0; k < (U + NT - 1) / NT; ++k) {
-                const int q = tid + k * NT;
-                if (q < U) body(q / MI * (M + 1) + q % MI + M + 2, q % MI + 1, q / MI + 1);
-            }
-        };
-        auto for_interior_w = [&](auto mconst, auto body) {
-            constexpr int M = decltype(mconst)::value, MI = M - 1, U = MI * MI;
-#pragma unroll
-            for (int k = 0; k < (U + 31) / 32; ++k) {
-                const int q = lane + k * 32;
-                if (q < U) body(q / MI * (M + 1) + q % MI + M + 2, q % MI + 1, q / MI + 1);
-            }
+        // the same, branch-free: the weights are 0, 1/2, 1/4 or 1, so the result equals prol2 bit
+        // for bit.  Used on the 25-value level-3 grid, where the lanes' loads are broadcasts.
+        auto prol2w = [](const double *Xc, int pc, int i, int j) -> double {
+            const double *z2 = Xc + (j >> 1) * pc + (i >> 1);
+            const double wx1 = (i & 1) ? 0.5 : 0.0, wx0 = (i & 1) ? 0.5 : 1.0;
+            const double wy1 = (j & 1) ? 0.5 : 0.0, wy0 = (j & 1) ? 0.5 : 1.0;
+            return fma(wx1 * wy1, z2[pc + 1], fma(wx0 * wy1, z2[pc], fma(wx1 * wy0, z2[1], wx0 * wy0 * z2[0])));
         };
 
-        // ---- one V(1,1) cycle: z = M^-1 rin.  The neighbours' rin come from the (r, w, s) grids
-        // and the step (alpha, beta) of the previous CG iteration.
-        auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC], double alpha, double beta) {
+        // ---- one V(1,1) cycle: z = M^-1 rin ------------------------------------------------
+        auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
             double t[BR][BC];
-            auto zn = [&](int e) -> double {     // neighbour's omega D^-1 r_{k+1}
-                return kMgOmega * DI0[e] * fma(-alpha, fma(beta, Hs[e], Hw[e]), Hr[e]);
-            };
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) z[q][c] = kMgOmega * DI0[ebase + q * np + c] * rin[q][c];
+                for (int c = 0; c < BC; ++c) z[q][c] = DI0[fe(c, q)] * rin[q][c];   // z0 = omega D^-1 r
+            publish(G0, z);
+            __syncthreads();
+            apply_fine(G0, z, t);
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) {       // residual of z = omega D^-1 r
-                    const int e = ebase + q * np + c;
-                    const double vl = c > 0 ? z[q][c - 1] : zn(e - 1);
-                    const double vr = c + 1 < BC ? z[q][c + 1] : zn(e + 1);
-                    const double vd = q > 0 ? z[q - 1][c] : zn(e - np);
-                    const double vu = q + 1 < BR ? z[q + 1][c] : zn(e + np);
-                    double a = D0[e] * z[q][c];
-                    a = fma(-cE[q][c + 1], vr, a);
-                    a = fma(-cE[q][c], vl, a);
-                    a = fma(-cN[q + 1][c], vu, a);
-                    a = fma(-cN[q][c], vd, a);
-                    t[q][c] = rin[q][c] - a;
-                }
-            publish(G0, rin);
+                for (int c = 0; c < BC; ++c) t[q][c] = rin[q][c] - t[q][c];       // fine residual
             publish(G1, t);
             __syncthreads();
-            for_interior(C1{}, [&](int e, int I, int J) {        // R1 = P^T t, Z1 = omega D1^-1 R1
-                const double rr = restrict9(G1, (2 * J) * np + 2 * I, np);
-                V1.R[e] = rr;
-                V1.Z[e] = kMgOmega * V1.DI[e] * rr;
+            // R1 = P^T t (9-point, split rows of G1), Z1 = omega D1^-1 R1
+            for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {
+                const int f = 2 * J * np, c = I, l = HE + I - 1, r = HE + I;
+                const double rr = G1[f + c] + 0.5 * (G1[f + l] + G1[f + r] + G1[f - np + c] + G1[f + np + c]) +
+                                  0.25 * (G1[f - np + l] + G1[f - np + r] + G1[f + np + l] + G1[f + np + r]);
+                const int e = e1(I, J);
+                R1[e] = rr;
+                Z1[e] = DI1[e] * rr;
             });
             __syncthreads();
-            for_interior(C1{}, [&](int e, int, int) { V1.T[e] = V1.R[e] - applyV(V1, V1.Z, e, P1); });
+            for_interior(C1{}, SCTA{}, tid, [&](int I, int J) { T1[e1(I, J)] = R1[e1(I, J)] - apply1(Z1, I, J); });
             __syncthreads();
             if (warp == 0) {                                     // levels 2 and 3 in one warp
-                for_interior_w(C2{}, [&](int e, int I, int J) {  // R2 = P^T T1, Z2 = omega D2^-1 R2
-                    const double rr = restrict9(V1.T, (2 * J) * P1 + 2 * I, P1);
-                    V2.R[e] = rr;
-                    V2.Z[e] = kMgOmega * V2.DI[e] * rr;
+                for_interior(C2{}, SW{}, lane, [&](int I, int J) {   // R2 = P^T T1, Z2 = omega D2^-1 R2
+                    const int f = 2 * J * P1, c = I, l = H1 + I - 1, r = H1 + I;
+                    const double rr = T1[f + c] + 0.5 * (T1[f + l] + T1[f + r] + T1[f - P1 + c] + T1[f + P1 + c]) +
+                                      0.25 * (T1[f - P1 + l] + T1[f - P1 + r] + T1[f + P1 + l] + T1[f + P1 + r]);
+                    const int e = J * P2 + I;
+                    R2[e] = rr;
+                    Z2[e] = DI2[e] * rr;
                 });
                 __syncwarp();
-                for_interior_w(C2{}, [&](int e, int, int) { V2.T[e] = V2.R[e] - applyV(V2, V2.Z, e, P2); });
+                for_interior(C2{}, SW{}, lane, [&](int I, int J) {
+                    const int e = J * P2 + I;
+                    T2[e] = R2[e] - apply2(Z2, e);
+                });
                 __syncwarp();
                 if (lane < U3) {
-                    const int I = lane % (m3 - 1) + 1, J = lane / (m3 - 1) + 1;
-                    R3[lane] = restrict9(V2.T, (2 * J) * P2 + 2 * I, P2);
+                    const int I = lane % (m3 - 1) + 1, J = lane / (m3 - 1) + 1, f = 2 * J * P2 + 2 * I;
+                    R3[lane] = T2[f] + 0.5 * (T2[f - 1] + T2[f + 1] + T2[f - P2] + T2[f + P2]) +
+                               0.25 * (T2[f - P2 - 1] + T2[f - P2 + 1] + T2[f + P2 - 1] + T2[f + P2 + 1]);
                 }
                 __syncwarp();
                 if (lane < U3) {                                 // exact solve E3 = A3^-1 R3
@@ -366,25 +374,30 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     E3[J * p3 + I] = sacc;
                 }
                 __syncwarp();
-                for_interior_w(C2{}, [&](int e, int I, int J) {  // Zc2 = Z2 + P E3 (into T2)
-                    V2.T[e] = V2.Z[e] + prol2(E3, p3, I, J);
-                });
-                __syncwarp();
-                for_interior_w(C2{}, [&](int e, int, int) {      // S2 = smooth(Zc2)
-                    V2.S[e] = fma(kMgOmega * V2.DI[e], V2.R[e] - applyV(V2, V2.T, e, P2), V2.T[e]);
-                });
+                // S2 = smooth(Z2 + P E3) = Z2 + E + omega D2^-1 (T2 - A2 E), E = P E3 (the
+                // correction is evaluated at the 5 stencil nodes; E3 has 9 values)
+#pragma unroll 1
+                for (int q = lane; q < (m2 - 1) * (m2 - 1); q += 32) {
+                    const int I = q % (m2 - 1) + 1, J = q / (m2 - 1) + 1, e = J * P2 + I;
+                    const double ec = prol2w(E3, p3, I, J);
+                    const double ae = D2[e] * ec - WH2[e] * prol2w(E3, p3, I + 1, J) -
+                                      WH2[e - 1] * prol2w(E3, p3, I - 1, J) - WV2[e] * prol2w(E3, p3, I, J + 1) -
+                                      WV2[e - P2] * prol2w(E3, p3, I, J - 1);
+                    S2[e] = fma(DI2[e], T2[e] - ae, Z2[e] + ec);
+                }
             }
             __syncthreads();
-            for_interior(C1{}, [&](int e, int I, int J) {        // Zc1 = Z1 + P S2 (into T1)
-                V1.T[e] = V1.Z[e] + prol2(V2.S, P2, I, J);
+            for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {      // Zc1 = Z1 + P S2 (in place)
+                Z1[e1(I, J)] += prol2(S2, P2, I, J);
             });
             __syncthreads();
-            for_interior(C1{}, [&](int e, int, int) {            // S1 = smooth(Zc1)
-                V1.S[e] = fma(kMgOmega * V1.DI[e], V1.R[e] - applyV(V1, V1.T, e, P1), V1.T[e]);
+            for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {      // S1 = smooth(Zc1)
+                const int e = e1(I, J);
+                S1[e] = fma(DI1[e], R1[e] - apply1(Z1, I, J), Z1[e]);
             });
             __syncthreads();
-            // level 0: z += P S1, post-smooth.  The coarse values this block and its neighbours
-            // need form a (BR/2 + 2) x (BC/2 + 2) window of S1; the parity of every fine node
+            // level 0: z = z0 + P S1, post-smooth.  The coarse values this block and its
+            // neighbours need form a (BR/2 + 2) x 3 window of S1; the parity of every fine node
             // relative to (col0, row0) is a compile-time constant.
             constexpr int XW = BC / 2 + 2, YW = BR / 2 + 2;
             double cw[YW][XW];
@@ -392,19 +405,16 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int yy = 0; yy < YW; ++yy)
 #pragma unroll
                 for (int xx = 0; xx < XW; ++xx) {
-                    const int X = (col0 >> 1) + xx, Y = (row0 >> 1) + yy;
-                    cw[yy][xx] = (X <= m1 && Y <= m1) ? V1.S[Y * P1 + X] : 0.0;
+                    const int X = lx + xx, Y = (row0 >> 1) + yy;
+                    cw[yy][xx] = (X <= m1 && Y <= m1) ? S1[Y * P1 + L::col1s(X)] : 0.0;
                 }
-            // P S1 at the fine node (col0 + 1 + c, row0 + 1 + q), c in [-1, BC], q in [-1, BR]
-            auto pw = [&](int c, int q) -> double {
+            auto pw = [&](int c, int q) -> double {  // (P S1) at node (col0 + 1 + c, row0 + 1 + q)
                 const int fi = 1 + c, fj = 1 + q, x0 = fi >> 1, y0 = fj >> 1;
                 if (!(fi & 1) && !(fj & 1)) return cw[y0][x0];
                 if (!(fj & 1)) return 0.5 * (cw[y0][x0] + cw[y0][x0 + 1]);
                 if (!(fi & 1)) return 0.5 * (cw[y0][x0] + cw[y0 + 1][x0]);
                 return 0.25 * (cw[y0][x0] + cw[y0][x0 + 1] + cw[y0 + 1][x0] + cw[y0 + 1][x0 + 1]);
             };
-            // a neighbour's corrected z = omega D^-1 r + P S1
-            auto zf = [&](int e, int c, int q) -> double { return kMgOmega * DI0[e] * G0[e] + pw(c, q); };
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
@@ -413,18 +423,17 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) {
-                    const int e = ebase + q * np + c;
-                    const double vl = c > 0 ? z[q][c - 1] : zf(e - 1, c - 1, q);
-                    const double vr = c + 1 < BC ? z[q][c + 1] : zf(e + 1, c + 1, q);
-                    const double vd = q > 0 ? z[q - 1][c] : zf(e - np, c, q - 1);
-                    const double vu = q + 1 < BR ? z[q + 1][c] : zf(e + np, c, q + 1);
-                    double a = D0[e] * z[q][c];
+                for (int c = 0; c < BC; ++c) {                   // neighbours: z0 (G0) + P S1
+                    const double vl = c > 0 ? z[q][c - 1] : G0[fe(c - 1, q)] + pw(c - 1, q);
+                    const double vr = c + 1 < BC ? z[q][c + 1] : G0[fe(c + 1, q)] + pw(c + 1, q);
+                    const double vd = q > 0 ? z[q - 1][c] : G0[fe(c, q - 1)] + pw(c, q - 1);
+                    const double vu = q + 1 < BR ? z[q + 1][c] : G0[fe(c, q + 1)] + pw(c, q + 1);
+                    double a = diag(q, c) * z[q][c];
                     a = fma(-cE[q][c + 1], vr, a);
                     a = fma(-cE[q][c], vl, a);
                     a = fma(-cN[q + 1][c], vu, a);
                     a = fma(-cN[q][c], vd, a);
-                    t[q][c] = fma(kMgOmega * DI0[e], rin[q][c] - a, z[q][c]);
+                    t[q][c] = valid(q, c) ? fma(DI0[fe(c, q)], rin[q][c] - a, z[q][c]) : 0.0;
                 }
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -441,15 +450,15 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 x[q][c] = p[q][c] = s[q][c] = 0.0;
                 r[q][c] = valid(q, c) ? (double)(row0 + q + 1) * inv_n3 : 0.0;     // b = h^2 x2
             }
-        double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0, alpha = 0.0, beta = 0.0;
+        double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
         bool conv = false;
         int it = 0;
         for (int k = 0;; ++k) {
             double uu[BR][BC], w[BR][BC];
-            vcycle(r, uu, alpha, beta);
-            publish(G2, uu);
+            vcycle(r, uu);
+            publish(G1, uu);                                 // G1 (fine residual) is free again
             __syncthreads();
-            apply_fine(G2, uu, w);
+            apply_fine(G1, uu, w);
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -459,9 +468,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     acc[1] = fma(w[q][c], uu[q][c], acc[1]);
                     acc[2] = fma(r[q][c], r[q][c], acc[2]);
                 }
-            publish(Hr, r);                                  // read after the barrier below
-            publish(Hw, w);
-            publish(Hs, s);
             {   // warp reduction with value exchange (4 values, 6 double shuffles)
                 const bool hi16 = lane & 16, hi8 = lane & 8;
                 const double s0 = hi16 ? acc[0] : acc[2], s1 = hi16 ? acc[1] : acc[3];
@@ -492,8 +498,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             if (k == 0) bb = rho;
             conv = rho <= Q.tol2 * bb;
             if (conv || it >= Q.maxit) break;
-            beta = k == 0 ? 0.0 : gamma * g_inv;
-            alpha = gamma * rcp_pos(k == 0 ? delta : delta - gamma * gamma * ga_inv);
+            const double beta = k == 0 ? 0.0 : gamma * g_inv;
+            const double alpha = gamma * rcp_pos(k == 0 ? delta : delta - gamma * gamma * ga_inv);
             g_inv = rcp_pos(gamma);
             ga_inv = rcp_pos(gamma * alpha);
 #pragma unroll
