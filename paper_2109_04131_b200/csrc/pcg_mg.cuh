@@ -70,6 +70,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     static_assert(NT % n == 0, "coefficient mapping: whole mesh rows per pass");
     static_assert(2 * n * n <= 2 * NP2, "coefficient table must fit in G0..G1");
     static_assert(U3 >= 1 && U3 <= 32, "level 3 is solved by one warp");
+    constexpr bool XP_SMEM = MINB >= 3;
     extern __shared__ double sm[];
     __shared__ double red[4][NWARP];
     __shared__ double th_amp[kMaxD];
@@ -87,14 +88,16 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     const int col0 = lx * BC, row0 = rg * BR;            // block: columns 2lx+1 (odd), 2lx+2 (even)
     const double inv_n3 = 1.0 / ((double)n * n * n);
 
-    // interior nodes of a coarse level (I, J in [1, M-1]), q = first + k * STRIDE
+    // interior nodes of a coarse level (I, J in [1, M-1]), q = first + k * STRIDE.  Lanes walk
+    // rows of M slots (I = 1..M, the ring column I = M masked), so a warp's accesses cover whole
+    // 16-slot row segments of the split-row grids and stay bank-conflict-free.
     auto for_interior = [](auto mconst, auto sconst, int first, auto body) {
-        constexpr int M = decltype(mconst)::value, MI = M - 1, U = MI * MI;
+        constexpr int M = decltype(mconst)::value, U = M * (M - 1);
         constexpr int STRIDE = decltype(sconst)::value;
 #pragma unroll
         for (int k = 0; k < (U + STRIDE - 1) / STRIDE; ++k) {
-            const int q = first + k * STRIDE;
-            if (q < U) body(q % MI + 1, q / MI + 1);
+            const int q = first + k * STRIDE, I = q % M + 1, J = q / M + 1;
+            if (q < U && I < M) body(I, J);
         }
     };
     using C1 = std::integral_constant<int, m1>;
@@ -131,8 +134,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 const int cell = (cj0 + k * CJS) * n + ci;
-                aT[2 * cell] = Q.form == 0 ? 1.0 + slo[k] : exp(slo[k]);
-                aT[2 * cell + 1] = Q.form == 0 ? 1.0 + sup[k] : exp(sup[k]);
+                aT[cell] = Q.form == 0 ? 1.0 + slo[k] : exp(slo[k]);              // lower-triangle plane
+                aT[n * n + cell] = Q.form == 0 ? 1.0 + sup[k] : exp(sup[k]);      // upper-triangle plane
             }
         }
         __syncthreads();
@@ -141,7 +144,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         auto fcoef = [&](int ci, int cj, int up, int sh) -> double {
             const int ma = (up ? 3 * ci + 1 : 3 * ci + 2) << sh;
             const int mb = (up ? 3 * cj + 2 : 3 * cj + 1) << sh;
-            return aT[2 * ((mb / 3) * n + ma / 3) + (ma % 3 == 1 ? 1 : 0)];
+            return aT[(ma % 3 == 1 ? n * n : 0) + (mb / 3) * n + ma / 3];
         };
         // edge weights of node (i, j) of the mesh with M cells of width 2^sh h: to (i+1, j), (i, j+1)
         auto wh = [&](int i, int j, int M, int sh) -> double {
@@ -166,10 +169,10 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 cN[q][c] = (i <= nx && j <= nx) ? wv(i, j, n, 0) : 0.0;
             }
         for (int e = tid; e < NP2; e += NT) {            // omega D^-1 (split rows), zero ring
-            const int j = e / np, s = e % np, i = s < HE ? 2 * s : 2 * (s - HE) + 1;
+            const int j = e / np, i = e % np;
             const bool in = i >= 1 && i <= nx && j >= 1 && j <= nx;
             const double dv = in ? wh(i, j, n, 0) + wh(i - 1, j, n, 0) + wv(i, j, n, 0) + wv(i, j - 1, n, 0) : 1.0;
-            DI0[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+            DI0[j * np + ((i & 1) ? HE + (i >> 1) : (i >> 1))] = in ? kMgOmega * (1.0 / dv) : 0.0;
         }
         for (int e = tid; e < N1; e += NT) {             // level 1 (split rows)
             const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
@@ -442,12 +445,17 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         };
 
         // ---- Chronopoulos-Gear PCG ----------------------------------------------------------
-        double x[BR][BC], r[BR][BC], p[BR][BC], s[BR][BC];
+        // x and p are touched once per iteration: with XP_SMEM they live in thread-private shared
+        // slots (conflict-free [k][tid] layout) to free registers for a third CTA per SM
+        double xr[XP_SMEM ? 1 : BR][BC], pr[XP_SMEM ? 1 : BR][BC], r[BR][BC], s[BR][BC];
+        double *const xs = sm + L::doubles() + tid, *const ps = xs + BR * BC * NT;
+        auto xref = [&](int q, int c) -> double & { return XP_SMEM ? xs[(q * BC + c) * NT] : xr[XP_SMEM ? 0 : q][c]; };
+        auto pref = [&](int q, int c) -> double & { return XP_SMEM ? ps[(q * BC + c) * NT] : pr[XP_SMEM ? 0 : q][c]; };
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
-                x[q][c] = p[q][c] = s[q][c] = 0.0;
+                xref(q, c) = pref(q, c) = s[q][c] = 0.0;
                 r[q][c] = valid(q, c) ? (double)(row0 + q + 1) * inv_n3 : 0.0;     // b = h^2 x2
             }
         double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
@@ -506,9 +514,10 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    p[q][c] = fma(beta, p[q][c], uu[q][c]);
+                    const double pn = fma(beta, pref(q, c), uu[q][c]);
+                    pref(q, c) = pn;
                     s[q][c] = fma(beta, s[q][c], w[q][c]);
-                    x[q][c] = fma(alpha, p[q][c], x[q][c]);
+                    xref(q, c) = fma(alpha, pn, xref(q, c));
                     r[q][c] = fma(-alpha, s[q][c], r[q][c]);
                 }
             ++it;
@@ -517,7 +526,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c)
-                if (valid(q, c)) u[(int64_t)((row0 + q) * nx + col0 + c) * ldu + bl] = x[q][c];
+                if (valid(q, c)) u[(int64_t)((row0 + q) * nx + col0 + c) * ldu + bl] = xref(q, c);
         if (tid == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rho / bb);

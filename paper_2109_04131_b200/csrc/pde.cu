@@ -188,7 +188,7 @@ template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                            const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
                            int32_t *iters, double *relres, int32_t *noconv, const double *S) {
-    const size_t dyn = sizeof(double) * (size_t)Mg3<NC>::doubles();
+    const size_t dyn = sizeof(double) * ((size_t)Mg3<NC>::doubles() + (MINB >= 3 ? 2 * BC * BR * NWARP * 32 : 0));
     auto kern = k_pcg_mg<NC, BC, BR, LX, NWARP, MINB>;
     USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int per_sm = 0;
@@ -316,6 +316,8 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     const char *mgl = getenv("USFFT_MG_LAYOUT");
     if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '2')        // 256 threads, 2x2 blocks
         s = launch_pcg_mg<32, 2, 2, 16, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '3')   // 3 CTAs/SM, x and p in smem
+        s = launch_pcg_mg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (pde->precond == 1 && n == 32)                          // 128 threads, 2x4 blocks
         s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
     else if (pde->precond == 1 && n == 16)
