@@ -67,7 +67,10 @@ __global__ void k_dft_direct(const double *__restrict__ u, const SlabParams S, i
     }
 }
 
-// one CTA per owned node g; the node's L spectra rows are staged in shared memory when they fit
+// one CTA per owned node g; the node's L spectra rows are staged in shared memory when they fit.
+// Candidates go in tiles of 256: the tile's L bins rows are first staged in shared memory with
+// independent coalesced loads (the L2 latency is paid once per tile, not once per lattice),
+// then each thread gathers and reduces its candidate.
 __global__ void __launch_bounds__(256)
 k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t nJ, int64_t M,
         int32_t L, double *__restrict__ kmin, unsigned long long *__restrict__ kmax, int staged) {
@@ -75,26 +78,37 @@ k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t
     __shared__ unsigned long long wmax[32];
     const int64_t g = blockIdx.x;
     const int64_t Mh = M / 2 + 1;
+    const double inv_m = 1.0 / (double)M;
     const double2 *src = F + g * L * Mh;
+    int32_t *sb = reinterpret_cast<int32_t *>(fs + (staged ? (int64_t)L * Mh : 0));   // [L][256]
     if (staged) {
 #pragma unroll 8
         for (int64_t e = threadIdx.x; e < (int64_t)L * Mh; e += blockDim.x) fs[e] = __ldg(src + e);
-        __syncthreads();
         src = fs;
     }
     unsigned long long best = 0ull;
-    for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) {
-        double km = 0.0;
+    for (int64_t j0 = 0; j0 < nJ; j0 += 256) {
+        const int64_t j = j0 + threadIdx.x;
+        __syncthreads();                                  // previous tile's readers are done
+#pragma unroll 8
+        for (int l = 0; l < L; ++l) sb[l * 256 + threadIdx.x] = j < nJ ? __ldg(bins + (int64_t)l * nJ + j) : 0;
+        __syncthreads();
+        if (j < nJ) {
+            // v = F^[b] / M with F^[b] = conj(F[M - b]) above M/2 (the sign does not enter the
+            // key); the scaling is a multiplication by fl(1/M) here (Z5 reading)
+            double km = 0.0;
 #pragma unroll 4
-        for (int l = 0; l < L; ++l) {
-            const int64_t b = __ldg(bins + (int64_t)l * nJ + j);
-            const double2 v = spec_value(src + l * Mh, M, b);
-            const double k = __dadd_rn(__dmul_rn(v.x, v.x), __dmul_rn(v.y, v.y));
-            km = (l == 0) ? k : fmin(km, k);
+            for (int l = 0; l < L; ++l) {
+                const int b = sb[l * 256 + threadIdx.x];
+                const double2 f = src[(int)(l * Mh) + (b < (int)Mh ? b : (int)M - b)];
+                const double re = f.x * inv_m, im = f.y * inv_m;
+                const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+                km = (l == 0) ? k : fmin(km, k);
+            }
+            kmin[g * nJ + j] = km;
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
+            best = bits > best ? bits : best;
         }
-        kmin[g * nJ + j] = km;
-        const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
-        best = bits > best ? bits : best;
     }
     for (int o = 16; o > 0; o >>= 1) {
         unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
@@ -322,10 +336,12 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
         if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
         const size_t st_bytes = sizeof(double2) * (size_t)L * (size_t)(M / 2 + 1);
-        const int staged = st_bytes <= 96 * 1024 ? 1 : 0;
-        if (staged)
-            USFFT_CUDA(c, cudaFuncSetAttribute(k_kappa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)st_bytes));
-        k_kappa<<<(unsigned)G_loc, 256, staged ? st_bytes : 0, c->stream>>>(
+        const size_t tile_bytes = sizeof(int32_t) * 256 * (size_t)L;
+        const int staged = st_bytes + tile_bytes <= 112 * 1024 ? 1 : 0;
+        const size_t dyn = (staged ? st_bytes : 0) + tile_bytes;
+        USFFT_REQUIRE(c, dyn <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
+        USFFT_CUDA(c, cudaFuncSetAttribute(k_kappa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        k_kappa<<<(unsigned)G_loc, 256, dyn, c->stream>>>(
             reinterpret_cast<const double2 *>(spectra), bins, nJ, M, L, kappa_min, km, staged);
         USFFT_CHECK_LAUNCH(c);
     }

@@ -70,7 +70,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     static_assert(NT % n == 0, "coefficient mapping: whole mesh rows per pass");
     static_assert(2 * n * n <= 2 * NP2, "coefficient table must fit in G0..G1");
     static_assert(U3 >= 1 && U3 <= 32, "level 3 is solved by one warp");
-    constexpr bool XP_SMEM = MINB >= 3;
+    constexpr bool XP_SMEM = MINB * NWARP >= 12;       // >= 12 resident warps per SM: x, p in smem
     extern __shared__ double sm[];
     __shared__ double red[4][NWARP];
     __shared__ double th_amp[kMaxD];
