@@ -153,27 +153,23 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         auto wv = [&](int i, int j, int M, int sh) -> double {
             return (j < M && i >= 1 && i < M) ? 0.5 * (fcoef(i, j, 1, sh) + fcoef(i - 1, j, 0, sh)) : 0.0;
         };
-        double cE[BR][BC + 1], cN[BR + 1][BC];           // fine couplings (ring edges included)
+        // fine couplings (ring edges included), read straight from the lower / upper planes:
+        // edge (i, j)-(i+1, j) = (a_lo(i, j) + a_up(i, j-1)) / 2, (i, j)-(i, j+1) = (a_up(i, j) + a_lo(i-1, j)) / 2
+        double cE[BR][BC + 1], cN[BR + 1][BC];
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c <= BC; ++c) {
                 const int i = col0 + c, j = row0 + q + 1;
-                cE[q][c] = (i <= nx && j <= nx) ? wh(i, j, n, 0) : 0.0;
+                cE[q][c] = (i <= nx && j <= nx) ? 0.5 * (aT[j * n + i] + aT[n * n + (j - 1) * n + i]) : 0.0;
             }
 #pragma unroll
         for (int q = 0; q <= BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
                 const int i = col0 + c + 1, j = row0 + q;
-                cN[q][c] = (i <= nx && j <= nx) ? wv(i, j, n, 0) : 0.0;
+                cN[q][c] = (i <= nx && j <= nx) ? 0.5 * (aT[n * n + j * n + i] + aT[j * n + i - 1]) : 0.0;
             }
-        for (int e = tid; e < NP2; e += NT) {            // omega D^-1 (split rows), zero ring
-            const int j = e / np, i = e % np;
-            const bool in = i >= 1 && i <= nx && j >= 1 && j <= nx;
-            const double dv = in ? wh(i, j, n, 0) + wh(i - 1, j, n, 0) + wv(i, j, n, 0) + wv(i, j - 1, n, 0) : 1.0;
-            DI0[j * np + ((i & 1) ? HE + (i >> 1) : (i >> 1))] = in ? kMgOmega * (1.0 / dv) : 0.0;
-        }
         for (int e = tid; e < N1; e += NT) {             // level 1 (split rows)
             const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
             WH1[e] = wh(I, J, m1, 1);
@@ -194,6 +190,14 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         __syncthreads();                                 // aT is dead from here on
         for (int e = tid; e < NP2; e += NT) G0[e] = G1[e] = 0.0;
+#pragma unroll
+        for (int q = 0; q < BR; ++q)                     // omega D^-1 of the own nodes (0 off-mesh);
+#pragma unroll                                           // the diagonal in the order of diag() below
+            for (int c = 0; c < BC; ++c) {
+                const double dv = cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c];
+                DI0[(row0 + 1 + q) * np + ((c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1))] =
+                    (col0 + c + 1 <= nx && row0 + q + 1 <= nx) ? kMgOmega * (1.0 / dv) : 0.0;
+            }
         for (int e = tid; e < N1; e += NT) {             // level-1 omega D^-1 (same sum as apply1)
             const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
             const bool in = I >= 1 && I < m1 && J >= 1 && J < m1;
