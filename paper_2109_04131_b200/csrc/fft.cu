@@ -126,6 +126,7 @@ k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t
 
 #include "rader.cuh"
 #include "rader_t.cuh"
+#include "fft400.cuh"
 
 using namespace usfft;
 
@@ -144,6 +145,23 @@ usfft_status launch_rader_t(usfft_ctx *c, const double *u, const SlabParams &S, 
     const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
     if (grid > resident) grid = resident;                 // persistent: each group loops over rows
     kern<<<(unsigned)grid, WPR * 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
+usfft_status launch_fft400(usfft_ctx *c, const double *u, const SlabParams &S, int64_t G_loc,
+                           int32_t L, const RaderArgs &A, double2 *F) {
+    constexpr int RPC = 4;
+    const int64_t rows = G_loc * L;
+    const size_t smem = sizeof(double2) * (size_t)(101 + 20 * 21) * RPC;
+    auto kern = k_fft400<RPC>;
+    USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * RPC, smem));
+    int64_t grid = (rows + RPC - 1) / RPC;
+    const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
+    if (grid > resident) grid = resident;                 // persistent: each warp loops over rows
+    kern<<<(unsigned)grid, 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -315,6 +333,8 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         double2 *Fo = reinterpret_cast<double2 *>(spectra);
         const bool generic = force && force[0] == 'g';     // USFFT_DFT=generic: runtime-plan kernel
         if (!generic && R.N == 96) s = launch_rader_t<96, 1, 4>(c, u, S, G_loc, L, A, Fo);
+        else if (!generic && R.N == 400 && !(force && force[0] == 's'))   // USFFT_DFT=stockham
+            s = launch_fft400(c, u, S, G_loc, L, A, Fo);
         else if (!generic && R.N == 400) s = launch_rader_t<400, 1, 4>(c, u, S, G_loc, L, A, Fo);
         else if (!generic && R.N == 2016) s = launch_rader_t<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
         else if (!generic && R.N == 4000) s = launch_rader_t<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
