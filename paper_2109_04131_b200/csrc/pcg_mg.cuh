@@ -25,8 +25,9 @@
 //  * grids of levels 0 and 1 store the even columns, then the odd columns of a row ("split"
 //    rows), so the stride-2 accesses of restriction, prolongation and the 2-column thread blocks
 //    are bank-conflict-free;
-//  * level 1 runs on the whole CTA; levels 2 and 3 (49 + 9 unknowns at n = 32) run in warp 0.
-// Nine CTA barriers per CG iteration.  Reductions are fixed trees, so a sample's result does not
+//  * level 1 runs on the whole CTA; the level-2/3 part of the cycle (49 + 9 unknowns at n = 32)
+//    is a fixed linear map applied as one precomputed dense 49 x 49 product per iteration.
+// Ten CTA barriers per CG iteration.  Reductions are fixed trees, so a sample's result does not
 // depend on the CTA or launch split.
 #pragma once
 #include <type_traits>
@@ -35,22 +36,42 @@ namespace usfft {
 
 constexpr double kMgOmega = 0.8;
 
+// Phase-latency probe (tools/mg_probe.cu builds with -DUSFFT_MG_PROBE): clock64() of lane 0 of
+// every warp of CTA 0, first sample, CG iteration 6, after each synchronisation point.
+#ifdef USFFT_MG_PROBE
+__device__ long long g_mg_probe[16][32];
+#define USFFT_MG_MARK(id)                                                                           \
+    do {                                                                                           \
+        if (probe_on && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][id] = clock64();      \
+    } while (0)
+#define USFFT_MG_SMARK(id)                                                                          \
+    do {                                                                                           \
+        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][id] = clock64(); \
+    } while (0)
+#else
+#define USFFT_MG_MARK(id) ((void)0)
+#define USFFT_MG_SMARK(id) ((void)0)
+#endif
+
 template <int NC>
 struct Mg3 {
     static constexpr int n = NC, np = NC + 1, NP2 = np * np, HE = NC / 2 + 1;   // HE even columns
     static constexpr int m1 = NC / 2, p1 = m1 + 1, N1 = p1 * p1, H1 = m1 / 2 + 1;  // smoothed level 1
     static constexpr int m2 = NC / 4, p2 = m2 + 1, N2 = p2 * p2;      // smoothed level 2 (natural)
     static constexpr int m3 = NC / 8, p3 = m3 + 1, N3 = p3 * p3, U3 = (m3 - 1) * (m3 - 1);  // exact
+    static constexpr int U2 = (m2 - 1) * (m2 - 1), HK = (U2 + 1) / 2;
     // shared-memory layout (doubles): fine grids omega D^-1, G0 (z0 = omega D^-1 r), G1 (fine
-    // residual, then u); level 1 WH, WV, omega D^-1, R, Z, T, S; level 2 WH, WV, D, omega D^-1,
-    // R, Z, T, S; level 3 WH, WV, R, E; the dense level-3 inverse.  The per-triangle coefficient
-    // table of the setup aliases G0..G1.
+    // residual, then u); level 1 WH, WV, omega D^-1, R, Z, T, S (split rows); level 2 WH, WV, D,
+    // omega D^-1 (setup), S (natural rows, zero ring), R (compact); the level-2 cycle matrix K
+    // (U2 x U2, column-major); level 3 WH, WV and the dense inverse A3^-1 (setup); B, C (setup).
+    // The per-triangle coefficient table of the setup aliases G0..G1.
     static constexpr int oDI0 = 0, oG0 = NP2, oG1 = 2 * NP2;
     static constexpr int oL1 = 3 * NP2;
-    static constexpr int oL2 = oL1 + 7 * N1;
-    static constexpr int oWH3 = oL2 + 8 * N2, oWV3 = oWH3 + N3, oR3 = oWV3 + N3, oE3 = oR3 + N3;
-    static constexpr int oAI = oE3 + N3;
-    __host__ __device__ static constexpr int doubles() { return oAI + U3 * U3; }
+    static constexpr int oL2 = oL1 + 7 * N1;             // WH2, WV2, D2, DI2, S2 (N2 each), R2 (U2)
+    static constexpr int oK = oL2 + 5 * N2 + 2 * HK;     // R2 padded to 2 HK (zero tail)
+    static constexpr int oWH3 = oK + 2 * HK * U2, oWV3 = oWH3 + N3, oAI = oWV3 + N3;   // K: 2 HK columns
+    static constexpr int oB = oAI + U3 * U3, oC = oB + U3 * U2;
+    __host__ __device__ static constexpr int doubles() { return oC + U3 * U2; }
     // split-row slot of column i (even columns first)
     __host__ __device__ static constexpr int col1s(int i) { return (i & 1) ? H1 + (i >> 1) : (i >> 1); }
 };
@@ -64,12 +85,13 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr int RGW = 32 / LX, NRG = NWARP * RGW, NT = NWARP * 32;
     constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1, NP2 = L::NP2, HE = L::HE;
     constexpr int m1 = L::m1, P1 = L::p1, N1 = L::N1, H1 = L::H1, m2 = L::m2, P2 = L::p2, N2 = L::N2;
-    constexpr int m3 = L::m3, p3 = L::p3, U3 = L::U3;
+    constexpr int m3 = L::m3, p3 = L::p3, U3 = L::U3, U2 = L::U2, HK = L::HK;
     static_assert(BC == 2 && BR % 2 == 0, "2 x BR node blocks (one odd and one even column)");
     static_assert(LX * BC >= nx && NRG * BR >= nx, "block mapping must cover the mesh");
     static_assert(NT % n == 0, "coefficient mapping: whole mesh rows per pass");
     static_assert(2 * n * n <= 2 * NP2, "coefficient table must fit in G0..G1");
-    static_assert(U3 >= 1 && U3 <= 32, "level 3 is solved by one warp");
+    static_assert(U3 >= 1 && U3 <= 32, "level 3 is inverted by one warp");
+    static_assert(2 * U2 <= NT, "two threads per row of the level-2 cycle matrix");
     constexpr bool XP_SMEM = MINB * NWARP >= 12;       // >= 12 resident warps per SM: x, p in smem
     extern __shared__ double sm[];
     __shared__ double red[4][NWARP];
@@ -78,9 +100,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     double *WH1 = sm + L::oL1, *WV1 = WH1 + N1, *DI1 = WH1 + 2 * N1, *R1 = WH1 + 3 * N1;
     double *Z1 = WH1 + 4 * N1, *T1 = WH1 + 5 * N1, *S1 = WH1 + 6 * N1;
     double *WH2 = sm + L::oL2, *WV2 = WH2 + N2, *D2 = WH2 + 2 * N2, *DI2 = WH2 + 3 * N2;
-    double *R2 = WH2 + 4 * N2, *Z2 = WH2 + 5 * N2, *T2 = WH2 + 6 * N2, *S2 = WH2 + 7 * N2;
-    double *WH3 = sm + L::oWH3, *WV3 = sm + L::oWV3, *R3 = sm + L::oR3, *E3 = sm + L::oE3;
-    double *AI = sm + L::oAI;
+    double *S2 = WH2 + 4 * N2, *R2 = WH2 + 5 * N2, *Kt = sm + L::oK;
+    double *WH3 = sm + L::oWH3, *WV3 = sm + L::oWV3, *AI = sm + L::oAI, *Bm = sm + L::oB, *Cm = sm + L::oC;
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int seg = lane / LX, lx = lane % LX;
@@ -103,16 +124,19 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     using C1 = std::integral_constant<int, m1>;
     using C2 = std::integral_constant<int, m2>;
     using SCTA = std::integral_constant<int, NT>;
-    using SW = std::integral_constant<int, 32>;
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
+#ifdef USFFT_MG_PROBE
+        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][20] = clock64();
+#endif
         // ---- K3: coefficients ----------------------------------------------------------------
         if (tid < Q.d) {
             const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
             th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
         }
         __syncthreads();
+        USFFT_MG_SMARK(24);
         {   // per-triangle a = 1 + sum_j amp_j theta_j S_j(ma) S_j(mb) (or exp) of the fine mesh:
             // thread (ci, cj0) keeps the ci-side factors of every j and sweeps KC rows cj
             constexpr int CJS = NT / n, KC = n / CJS;
@@ -139,6 +163,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
         }
         __syncthreads();
+        USFFT_MG_SMARK(25);
         // a at the centroid of T_lo / T_up of cell (ci, cj) of the mesh with cell width 2^sh h: the
         // fine triangle with the same centroid (abscissae ma, mb in units of h/3)
         auto fcoef = [&](int ci, int cj, int up, int sh) -> double {
@@ -180,16 +205,34 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             const int I = e % P2, J = e / P2;
             WH2[e] = wh(I, J, m2, 2);
             WV2[e] = wv(I, J, m2, 2);
-            R2[e] = Z2[e] = T2[e] = S2[e] = 0.0;
+            S2[e] = 0.0;
         }
         for (int e = tid; e < L::N3; e += NT) {
             const int I = e % p3, J = e / p3;
             WH3[e] = wh(I, J, m3, 3);
             WV3[e] = wv(I, J, m3, 3);
-            E3[e] = 0.0;
         }
         __syncthreads();                                 // aT is dead from here on
-        for (int e = tid; e < NP2; e += NT) G0[e] = G1[e] = 0.0;
+        USFFT_MG_SMARK(26);
+        // warps >= 1 form the level-1/2 diagonals while warp 0 assembles and inverts A3
+        constexpr int HB = NWARP > 1 ? 32 : 0, HS = NT - HB;
+        if (tid >= HB) {
+            const int ht = tid - HB;
+            for (int e = ht; e < NP2; e += HS) G0[e] = G1[e] = 0.0;
+            for (int e = ht; e < N1; e += HS) {          // level-1 omega D^-1 (same sum as apply1)
+                const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
+                const bool in = I >= 1 && I < m1 && J >= 1 && J < m1;
+                const double dv = in ? WH1[e] + WH1[J * P1 + L::col1s(I - 1)] + WV1[e] + WV1[e - P1] : 1.0;
+                DI1[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+            }
+            for (int e = ht; e < N2; e += HS) {
+                const int I = e % P2, J = e / P2;
+                const bool in = I >= 1 && I < m2 && J >= 1 && J < m2;
+                const double dv = in ? WH2[e] + WH2[e - 1] + WV2[e] + WV2[e - P2] : 0.0;
+                D2[e] = dv;
+                DI2[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+            }
+        }
 #pragma unroll
         for (int q = 0; q < BR; ++q)                     // omega D^-1 of the own nodes (0 off-mesh);
 #pragma unroll                                           // the diagonal in the order of diag() below
@@ -198,20 +241,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 DI0[(row0 + 1 + q) * np + ((c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1))] =
                     (col0 + c + 1 <= nx && row0 + q + 1 <= nx) ? kMgOmega * (1.0 / dv) : 0.0;
             }
-        for (int e = tid; e < N1; e += NT) {             // level-1 omega D^-1 (same sum as apply1)
-            const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
-            const bool in = I >= 1 && I < m1 && J >= 1 && J < m1;
-            const double dv = in ? WH1[e] + WH1[J * P1 + L::col1s(I - 1)] + WV1[e] + WV1[e - P1] : 1.0;
-            DI1[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
-        }
-        for (int e = tid; e < N2; e += NT) {
-            const int I = e % P2, J = e / P2;
-            const bool in = I >= 1 && I < m2 && J >= 1 && J < m2;
-            const double dv = in ? WH2[e] + WH2[e - 1] + WV2[e] + WV2[e - P2] : 0.0;
-            D2[e] = dv;
-            DI2[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
-        }
-        for (int e = tid; e < U3 * U3; e += NT) {        // dense level-3 operator, row-major
+        if (warp == 0) {
+        for (int e = lane; e < U3 * U3; e += 32) {       // dense level-3 operator, row-major
             const int a = e / U3, c = e % U3;
             const int ia = a % (m3 - 1) + 1, ja = a / (m3 - 1) + 1;
             const int ic = c % (m3 - 1) + 1, jc = c / (m3 - 1) + 1;
@@ -224,7 +255,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             else if (ic == ia && jc == ja - 1) v = -WV3[g - p3];
             AI[e] = v;
         }
-        __syncthreads();
+        __syncwarp();
+        }
         if (warp == 0) {   // in-place Gauss-Jordan inverse of the coarsest operator (SPD, tiny)
             constexpr int GE = (U3 * U3 + 31) / 32;
             for (int k = 0; k < U3; ++k) {
@@ -254,6 +286,69 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     }
                 }
                 __syncwarp();
+            }
+            USFFT_MG_SMARK(30);
+        }
+        __syncthreads();
+        USFFT_MG_SMARK(27);
+        // The level-2 part of the cycle is a fixed linear map R2 -> S2 (damped-Jacobi pre-smoothing,
+        // exact level-3 correction, post-smoothing):  with Dw = omega D2^-1,
+        //   S2 = K R2,  K = 2 Dw - Dw A2 Dw + B^T A3^-1 B,  B = P3^T (I - A2 Dw)   (U3 x U2),
+        // formed once per sample so each CG iteration applies it as one dense product.
+        for (int e = tid; e < U3 * U2; e += NT) {        // B[r][k] = sum_m w(r, m) (I - A2 Dw)[m][k]
+            const int r = e / U2, k = e % U2;
+            const int Ir = r % (m3 - 1) + 1, Jr = r / (m3 - 1) + 1;
+            const int Ik = k % (m2 - 1) + 1, Jk = k / (m2 - 1) + 1, ek = Jk * P2 + Ik;
+            const double dwk = DI2[ek];
+            // restriction weight of level-2 node (Im, Jm) for level-3 node r (0 off the stencil)
+            auto wr = [&](int Im, int Jm) -> double {
+                const int ax = abs(Im - 2 * Ir), ay = abs(Jm - 2 * Jr);
+                return (ax > 1 || ay > 1) ? 0.0 : (ax ? 0.5 : 1.0) * (ay ? 0.5 : 1.0);
+            };
+            // the rows m of (I - A2 Dw) with a nonzero in column k: m = k and its 4 neighbours
+            double v = wr(Ik, Jk) * (1.0 - D2[ek] * dwk);
+            v = fma(wr(Ik + 1, Jk), WH2[ek] * dwk, v);
+            v = fma(wr(Ik - 1, Jk), WH2[ek - 1] * dwk, v);
+            v = fma(wr(Ik, Jk + 1), WV2[ek] * dwk, v);
+            v = fma(wr(Ik, Jk - 1), WV2[ek - P2] * dwk, v);
+            Bm[e] = v;
+        }
+        __syncthreads();
+        USFFT_MG_SMARK(28);
+        for (int e = tid; e < U3 * U2; e += NT) {        // C = A3^-1 B
+            const int r = e / U2, k = e % U2;
+            double v = 0.0;
+            for (int c = 0; c < U3; ++c) v = fma(AI[r * U3 + c], Bm[c * U2 + k], v);
+            Cm[e] = v;
+        }
+        __syncthreads();
+        USFFT_MG_SMARK(29);
+        for (int e = U2 * U2 + tid; e < 2 * HK * U2; e += NT) Kt[e] = 0.0;   // zero pad column(s)
+        if (tid < 2 * HK - U2) R2[U2 + tid] = 0.0;                           // and R2 tail
+        if (tid < 2 * U2) {      // K = B^T C + 2 Dw - Dw A2 Dw: thread (i, h) -> row i, columns [h HK, h HK + HK)
+            const int h = tid & 1, i = tid >> 1;
+            const int Ii = i % (m2 - 1) + 1, Ji = i / (m2 - 1) + 1, ei = Ji * P2 + Ii;
+            double bi[U3];
+#pragma unroll
+            for (int r = 0; r < U3; ++r) bi[r] = Bm[r * U2 + i];
+            const double dwi = DI2[ei];
+            // row i of 2 Dw - Dw A2 Dw (5-point): diagonal, right, left, up, down neighbours
+            const double s0 = fma(-dwi * D2[ei], dwi, 2.0 * dwi);
+            const double s1 = Ii < m2 - 1 ? dwi * WH2[ei] * DI2[ei + 1] : 0.0;
+            const double s2 = Ii > 1 ? dwi * WH2[ei - 1] * DI2[ei - 1] : 0.0;
+            const double s3 = Ji < m2 - 1 ? dwi * WV2[ei] * DI2[ei + P2] : 0.0;
+            const double s4 = Ji > 1 ? dwi * WV2[ei - P2] * DI2[ei - P2] : 0.0;
+#pragma unroll 5
+            for (int c = 0; c < HK; ++c) {
+                const int k = h * HK + c;
+                if (k < U2) {
+                    double v = 0.0;
+#pragma unroll
+                    for (int r = 0; r < U3; ++r) v = fma(bi[r], Cm[r * U2 + k], v);
+                    const double sp = k == i ? s0 : k == i + 1 ? s1 : k == i - 1 ? s2 : k == i + (m2 - 1) ? s3
+                                    : k == i - (m2 - 1) ? s4 : 0.0;
+                    Kt[k * U2 + i] = v + sp;
+                }
             }
         }
         // (the first barriers of the CG loop order these writes before their uses)
@@ -302,11 +397,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             return (whe + whl + wve + wvd) * Zs[e] - whe * Zs[er] - whl * Zs[el] - wve * Zs[e + P1] -
                    wvd * Zs[e - P1];
         };
-        // level-2 operator (natural layout)
-        auto apply2 = [&](const double *Zs, int e) -> double {
-            return D2[e] * Zs[e] - WH2[e] * Zs[e + 1] - WH2[e - 1] * Zs[e - 1] - WV2[e] * Zs[e + P2] -
-                   WV2[e - P2] * Zs[e - P2];
-        };
         // bilinear prolongation of a coarse grid Xc (natural rows of length pc, zero ring) to node (i, j)
         auto prol2 = [](const double *Xc, int pc, int i, int j) -> double {
             const double *z2 = Xc + (j >> 1) * pc + (i >> 1);
@@ -324,6 +414,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             return fma(wx1 * wy1, z2[pc + 1], fma(wx0 * wy1, z2[pc], fma(wx1 * wy0, z2[1], wx0 * wy0 * z2[0])));
         };
 
+        int probe_on = 0;
+        (void)probe_on;
         // ---- one V(1,1) cycle: z = M^-1 rin ------------------------------------------------
         auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
             double t[BR][BC];
@@ -333,6 +425,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < BC; ++c) z[q][c] = DI0[fe(c, q)] * rin[q][c];   // z0 = omega D^-1 r
             publish(G0, z);
             __syncthreads();
+            USFFT_MG_MARK(1);
             apply_fine(G0, z, t);
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -340,6 +433,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < BC; ++c) t[q][c] = rin[q][c] - t[q][c];       // fine residual
             publish(G1, t);
             __syncthreads();
+            USFFT_MG_MARK(2);
             // R1 = P^T t (9-point, split rows of G1), Z1 = omega D1^-1 R1
             for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {
                 const int f = 2 * J * np, c = I, l = HE + I - 1, r = HE + I;
@@ -350,59 +444,46 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 Z1[e] = DI1[e] * rr;
             });
             __syncthreads();
+            USFFT_MG_MARK(3);
             for_interior(C1{}, SCTA{}, tid, [&](int I, int J) { T1[e1(I, J)] = R1[e1(I, J)] - apply1(Z1, I, J); });
             __syncthreads();
-            if (warp == 0) {                                     // levels 2 and 3 in one warp
-                for_interior(C2{}, SW{}, lane, [&](int I, int J) {   // R2 = P^T T1, Z2 = omega D2^-1 R2
-                    const int f = 2 * J * P1, c = I, l = H1 + I - 1, r = H1 + I;
-                    const double rr = T1[f + c] + 0.5 * (T1[f + l] + T1[f + r] + T1[f - P1 + c] + T1[f + P1 + c]) +
-                                      0.25 * (T1[f - P1 + l] + T1[f - P1 + r] + T1[f + P1 + l] + T1[f + P1 + r]);
-                    const int e = J * P2 + I;
-                    R2[e] = rr;
-                    Z2[e] = DI2[e] * rr;
-                });
-                __syncwarp();
-                for_interior(C2{}, SW{}, lane, [&](int I, int J) {
-                    const int e = J * P2 + I;
-                    T2[e] = R2[e] - apply2(Z2, e);
-                });
-                __syncwarp();
-                if (lane < U3) {
-                    const int I = lane % (m3 - 1) + 1, J = lane / (m3 - 1) + 1, f = 2 * J * P2 + 2 * I;
-                    R3[lane] = T2[f] + 0.5 * (T2[f - 1] + T2[f + 1] + T2[f - P2] + T2[f + P2]) +
-                               0.25 * (T2[f - P2 - 1] + T2[f - P2 + 1] + T2[f + P2 - 1] + T2[f + P2 + 1]);
-                }
-                __syncwarp();
-                if (lane < U3) {                                 // exact solve E3 = A3^-1 R3
-                    double sacc = 0.0;
-#pragma unroll
-                    for (int c = 0; c < U3; ++c) sacc = fma(AI[lane * U3 + c], R3[c], sacc);
-                    const int I = lane % (m3 - 1) + 1, J = lane / (m3 - 1) + 1;
-                    E3[J * p3 + I] = sacc;
-                }
-                __syncwarp();
-                // S2 = smooth(Z2 + P E3) = Z2 + E + omega D2^-1 (T2 - A2 E), E = P E3 (the
-                // correction is evaluated at the 5 stencil nodes; E3 has 9 values)
-#pragma unroll 1
-                for (int q = lane; q < (m2 - 1) * (m2 - 1); q += 32) {
-                    const int I = q % (m2 - 1) + 1, J = q / (m2 - 1) + 1, e = J * P2 + I;
-                    const double ec = prol2w(E3, p3, I, J);
-                    const double ae = D2[e] * ec - WH2[e] * prol2w(E3, p3, I + 1, J) -
-                                      WH2[e - 1] * prol2w(E3, p3, I - 1, J) - WV2[e] * prol2w(E3, p3, I, J + 1) -
-                                      WV2[e - P2] * prol2w(E3, p3, I, J - 1);
-                    S2[e] = fma(DI2[e], T2[e] - ae, Z2[e] + ec);
-                }
-            }
-            __syncthreads();
-            for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {      // Zc1 = Z1 + P S2 (in place)
-                Z1[e1(I, J)] += prol2(S2, P2, I, J);
+            USFFT_MG_MARK(4);
+            for_interior(C2{}, SCTA{}, tid, [&](int I, int J) {      // R2 = P^T T1 (compact)
+                const int f = 2 * J * P1, c = I, l = H1 + I - 1, r = H1 + I;
+                R2[(J - 1) * (m2 - 1) + I - 1] =
+                    T1[f + c] + 0.5 * (T1[f + l] + T1[f + r] + T1[f - P1 + c] + T1[f + P1 + c]) +
+                    0.25 * (T1[f - P1 + l] + T1[f - P1 + r] + T1[f + P1 + l] + T1[f + P1 + r]);
             });
             __syncthreads();
+            USFFT_MG_MARK(5);
+            if (warp < (2 * U2 + 31) / 32) {                     // S2 = K R2 (levels 2 and 3)
+                // thread (i, h): half h of row i; K and R2 carry a zero column / entry past U2
+                const int h = tid & 1, i = min(tid >> 1, U2 - 1);
+                const bool own = tid < 2 * U2;
+                const double *kp = Kt + h * HK * U2 + i, *rp = R2 + h * HK;
+                double a0 = 0.0, a1 = 0.0;
+#pragma unroll
+                for (int c = 0; c < HK; c += 2) {
+                    a0 = fma(kp[c * U2], rp[c], a0);
+                    if (c + 1 < HK) a1 = fma(kp[(c + 1) * U2], rp[c + 1], a1);
+                }
+                double sv = a0 + a1;
+                sv += __shfl_xor_sync(0xffffffffu, sv, 1);       // whole warps take part
+                if (own && h == 0) S2[(i / (m2 - 1) + 1) * P2 + i % (m2 - 1) + 1] = sv;
+            }
+            __syncthreads();
+            USFFT_MG_MARK(9);
+            for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {      // Zc1 = Z1 + P S2 (in place)
+                Z1[e1(I, J)] += prol2w(S2, P2, I, J);
+            });
+            __syncthreads();
+            USFFT_MG_MARK(10);
             for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {      // S1 = smooth(Zc1)
                 const int e = e1(I, J);
                 S1[e] = fma(DI1[e], R1[e] - apply1(Z1, I, J), Z1[e]);
             });
             __syncthreads();
+            USFFT_MG_MARK(11);
             // level 0: z = z0 + P S1, post-smooth.  The coarse values this block and its
             // neighbours need form a (BR/2 + 2) x 3 window of S1; the parity of every fine node
             // relative to (col0, row0) is a compile-time constant.
@@ -448,6 +529,9 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < BC; ++c) z[q][c] = t[q][c];
         };
 
+#ifdef USFFT_MG_PROBE
+        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][21] = clock64();
+#endif
         // ---- Chronopoulos-Gear PCG ----------------------------------------------------------
         // x and p are touched once per iteration: with XP_SMEM they live in thread-private shared
         // slots (conflict-free [k][tid] layout) to free registers for a third CTA per SM
@@ -466,10 +550,13 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         bool conv = false;
         int it = 0;
         for (int k = 0;; ++k) {
+            probe_on = blockIdx.x == 0 && bl == gridDim.x && k == 6;
+            USFFT_MG_MARK(0);
             double uu[BR][BC], w[BR][BC];
             vcycle(r, uu);
             publish(G1, uu);                                 // G1 (fine residual) is free again
             __syncthreads();
+            USFFT_MG_MARK(12);
             apply_fine(G1, uu, w);
             double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
@@ -493,6 +580,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 if ((lane & 7) == 0) red[lane >> 3][warp] = v;
             }
             __syncthreads();
+            USFFT_MG_MARK(13);
             double gs[3];
 #pragma unroll
             for (int q = 0; q < 3; ++q) {
@@ -531,6 +619,12 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int c = 0; c < BC; ++c)
                 if (valid(q, c)) u[(int64_t)((row0 + q) * nx + col0 + c) * ldu + bl] = xref(q, c);
+#ifdef USFFT_MG_PROBE
+        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) {
+            g_mg_probe[threadIdx.x >> 5][22] = clock64();
+            g_mg_probe[threadIdx.x >> 5][23] = it;
+        }
+#endif
         if (tid == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rho / bb);

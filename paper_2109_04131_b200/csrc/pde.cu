@@ -354,3 +354,10 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
         return fail(c, USFFT_ENOCONV, "%d of %lld samples missed tol at maxit", host_nc, (long long)nb);
     return USFFT_OK;
 }
+
+#ifdef USFFT_MG_PROBE
+// probe build only (tools/mg_probe.cu): copy the phase clocks of k_pcg_mg out
+extern "C" int usfft_debug_mg_probe(long long *out) {
+    return (int)cudaMemcpyFromSymbol(out, usfft::g_mg_probe, sizeof(long long) * 16 * 32);
+}
+#endif
