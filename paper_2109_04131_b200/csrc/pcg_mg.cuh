@@ -257,35 +257,29 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         __syncwarp();
         }
-        if (warp == 0) {   // in-place Gauss-Jordan inverse of the coarsest operator (SPD, tiny)
-            constexpr int GE = (U3 * U3 + 31) / 32;
+        if (warp == 0) {   // in-place Gauss-Jordan inverse of the coarsest operator (SPD, tiny):
+            // lane i keeps row i in registers, the pivot row comes by shuffles
+            const int ri = lane < U3 ? lane : 0;
+            double a[U3];
+#pragma unroll
+            for (int c = 0; c < U3; ++c) a[c] = AI[ri * U3 + c];
+#pragma unroll
             for (int k = 0; k < U3; ++k) {
-                double rk[GE], ck[GE], old[GE];
-                const double piv = 1.0 / AI[k * U3 + k];
+                double prow[U3];
 #pragma unroll
-                for (int t = 0; t < GE; ++t) {
-                    const int e = lane + 32 * t;
-                    if (e < U3 * U3) {
-                        rk[t] = AI[k * U3 + e % U3];
-                        ck[t] = AI[(e / U3) * U3 + k];
-                        old[t] = AI[e];
-                    }
-                }
-                __syncwarp();
+                for (int c = 0; c < U3; ++c) prow[c] = __shfl_sync(0xffffffffu, a[c], k);
+                const double piv = 1.0 / prow[k];
+                const double f = -a[k] * piv;
 #pragma unroll
-                for (int t = 0; t < GE; ++t) {
-                    const int e = lane + 32 * t;
-                    if (e < U3 * U3) {
-                        const int i = e / U3, j = e % U3;
-                        double v;
-                        if (i == k && j == k) v = piv;
-                        else if (i == k) v = rk[t] * piv;
-                        else if (j == k) v = -ck[t] * piv;
-                        else v = fma(-ck[t] * piv, rk[t], old[t]);
-                        AI[e] = v;
-                    }
+                for (int c = 0; c < U3; ++c) {
+                    if (lane == k) a[c] = c == k ? piv : prow[c] * piv;
+                    else a[c] = c == k ? f : fma(f, prow[c], a[c]);
                 }
-                __syncwarp();
+            }
+            __syncwarp();
+            if (lane < U3) {
+#pragma unroll
+                for (int c = 0; c < U3; ++c) AI[lane * U3 + c] = a[c];
             }
             USFFT_MG_SMARK(30);
         }
@@ -325,31 +319,45 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         USFFT_MG_SMARK(29);
         for (int e = U2 * U2 + tid; e < 2 * HK * U2; e += NT) Kt[e] = 0.0;   // zero pad column(s)
         if (tid < 2 * HK - U2) R2[U2 + tid] = 0.0;                           // and R2 tail
-        if (tid < 2 * U2) {      // K = B^T C + 2 Dw - Dw A2 Dw: thread (i, h) -> row i, columns [h HK, h HK + HK)
-            const int h = tid & 1, i = tid >> 1;
-            const int Ii = i % (m2 - 1) + 1, Ji = i / (m2 - 1) + 1, ei = Ji * P2 + Ii;
-            double bi[U3];
+        {   // K = B^T C (rank-U3 product) in register tiles: thread (ti, tk) of a 16 x NT/16 grid
+            // owns rows ti + 16 m and columns tk + TK n
+            constexpr int TK = NT / 16, RI = (U2 + 15) / 16, CK = (U2 + TK - 1) / TK;
+            const int ti = tid % 16, tk = tid / 16;
+            double acc[RI][CK];
 #pragma unroll
-            for (int r = 0; r < U3; ++r) bi[r] = Bm[r * U2 + i];
-            const double dwi = DI2[ei];
-            // row i of 2 Dw - Dw A2 Dw (5-point): diagonal, right, left, up, down neighbours
-            const double s0 = fma(-dwi * D2[ei], dwi, 2.0 * dwi);
-            const double s1 = Ii < m2 - 1 ? dwi * WH2[ei] * DI2[ei + 1] : 0.0;
-            const double s2 = Ii > 1 ? dwi * WH2[ei - 1] * DI2[ei - 1] : 0.0;
-            const double s3 = Ji < m2 - 1 ? dwi * WV2[ei] * DI2[ei + P2] : 0.0;
-            const double s4 = Ji > 1 ? dwi * WV2[ei - P2] * DI2[ei - P2] : 0.0;
-#pragma unroll 5
-            for (int c = 0; c < HK; ++c) {
-                const int k = h * HK + c;
-                if (k < U2) {
-                    double v = 0.0;
+            for (int m = 0; m < RI; ++m)
 #pragma unroll
-                    for (int r = 0; r < U3; ++r) v = fma(bi[r], Cm[r * U2 + k], v);
-                    const double sp = k == i ? s0 : k == i + 1 ? s1 : k == i - 1 ? s2 : k == i + (m2 - 1) ? s3
-                                    : k == i - (m2 - 1) ? s4 : 0.0;
-                    Kt[k * U2 + i] = v + sp;
-                }
+                for (int q = 0; q < CK; ++q) acc[m][q] = 0.0;
+#pragma unroll 3
+            for (int r = 0; r < U3; ++r) {
+                double bv[RI], cv[CK];
+#pragma unroll
+                for (int m = 0; m < RI; ++m) bv[m] = Bm[r * U2 + min(ti + 16 * m, U2 - 1)];
+#pragma unroll
+                for (int q = 0; q < CK; ++q) cv[q] = Cm[r * U2 + min(tk + TK * q, U2 - 1)];
+#pragma unroll
+                for (int m = 0; m < RI; ++m)
+#pragma unroll
+                    for (int q = 0; q < CK; ++q) acc[m][q] = fma(bv[m], cv[q], acc[m][q]);
             }
+#pragma unroll
+            for (int m = 0; m < RI; ++m)
+#pragma unroll
+                for (int q = 0; q < CK; ++q) {
+                    const int i = ti + 16 * m, k = tk + TK * q;
+                    if (i < U2 && k < U2) Kt[k * U2 + i] = acc[m][q];
+                }
+        }
+        __syncthreads();
+        for (int e = tid; e < 5 * U2; e += NT) {         // + 2 Dw - Dw A2 Dw (5-point), row i
+            const int i = e % U2, d = e / U2;
+            const int Ii = i % (m2 - 1) + 1, Ji = i / (m2 - 1) + 1, ei = Ji * P2 + Ii;
+            const double dwi = DI2[ei];
+            if (d == 0) Kt[i * U2 + i] += fma(-dwi * D2[ei], dwi, 2.0 * dwi);
+            else if (d == 1 && Ii < m2 - 1) Kt[(i + 1) * U2 + i] += dwi * WH2[ei] * DI2[ei + 1];
+            else if (d == 2 && Ii > 1) Kt[(i - 1) * U2 + i] += dwi * WH2[ei - 1] * DI2[ei - 1];
+            else if (d == 3 && Ji < m2 - 1) Kt[(i + (m2 - 1)) * U2 + i] += dwi * WV2[ei] * DI2[ei + P2];
+            else if (d == 4 && Ji > 1) Kt[(i - (m2 - 1)) * U2 + i] += dwi * WV2[ei - P2] * DI2[ei - P2];
         }
         // (the first barriers of the CG loop order these writes before their uses)
 
