@@ -511,30 +511,20 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 if (!(fi & 1)) return 0.5 * (cw[y0][x0] + cw[y0 + 1][x0]);
                 return 0.25 * (cw[y0][x0] + cw[y0][x0 + 1] + cw[y0 + 1][x0] + cw[y0 + 1][x0 + 1]);
             };
+            // post-smoothing of z0 + E, E = P S1:  z0 + E + omega D^-1 (t - A E), with t = r - A z0
+            // the fine residual still in registers; the neighbours' E come from the window
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c)
-                    if (valid(q, c)) z[q][c] += pw(c, q);
-#pragma unroll
-            for (int q = 0; q < BR; ++q)
-#pragma unroll
-                for (int c = 0; c < BC; ++c) {                   // neighbours: z0 (G0) + P S1
-                    const double vl = c > 0 ? z[q][c - 1] : G0[fe(c - 1, q)] + pw(c - 1, q);
-                    const double vr = c + 1 < BC ? z[q][c + 1] : G0[fe(c + 1, q)] + pw(c + 1, q);
-                    const double vd = q > 0 ? z[q - 1][c] : G0[fe(c, q - 1)] + pw(c, q - 1);
-                    const double vu = q + 1 < BR ? z[q + 1][c] : G0[fe(c, q + 1)] + pw(c, q + 1);
-                    double a = diag(q, c) * z[q][c];
-                    a = fma(-cE[q][c + 1], vr, a);
-                    a = fma(-cE[q][c], vl, a);
-                    a = fma(-cN[q + 1][c], vu, a);
-                    a = fma(-cN[q][c], vd, a);
-                    t[q][c] = valid(q, c) ? fma(DI0[fe(c, q)], rin[q][c] - a, z[q][c]) : 0.0;
+                for (int c = 0; c < BC; ++c) {
+                    const double ec = pw(c, q);
+                    double a = diag(q, c) * ec;
+                    a = fma(-cE[q][c + 1], pw(c + 1, q), a);
+                    a = fma(-cE[q][c], pw(c - 1, q), a);
+                    a = fma(-cN[q + 1][c], pw(c, q + 1), a);
+                    a = fma(-cN[q][c], pw(c, q - 1), a);
+                    z[q][c] = valid(q, c) ? fma(DI0[fe(c, q)], t[q][c] - a, z[q][c] + ec) : 0.0;
                 }
-#pragma unroll
-            for (int q = 0; q < BR; ++q)
-#pragma unroll
-                for (int c = 0; c < BC; ++c) z[q][c] = t[q][c];
         };
 
 #ifdef USFFT_MG_PROBE
