@@ -72,6 +72,8 @@ struct Mg3 {
     static constexpr int oWH3 = oK + 2 * HK * U2, oWV3 = oWH3 + N3, oAI = oWV3 + N3;   // K: 2 HK columns
     static constexpr int oB = oAI + U3 * U3, oC = oB + U3 * U2;
     __host__ __device__ static constexpr int doubles() { return oC + U3 * U2; }
+    // the sin table S[j][m] (d x (3n+1)) is staged after these when it has at most SMAX doubles
+    static constexpr int SMAX = 2560;
     // split-row slot of column i (even columns first)
     __host__ __device__ static constexpr int col1s(int i) { return (i & 1) ? H1 + (i >> 1) : (i >> 1); }
 };
@@ -125,6 +127,14 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     using C2 = std::integral_constant<int, m2>;
     using SCTA = std::integral_constant<int, NT>;
 
+    // the sample-independent sin table, staged once per CTA (L1 reloads of it were ~500 cycles
+    // per coefficient term in the probe)
+    const bool s_staged = Q.d * W <= L::SMAX;
+    double *Ssm = sm + L::doubles() + (XP_SMEM ? 2 * BC * BR * NT : 0);
+    if (s_staged)
+        for (int e = tid; e < Q.d * W; e += NT) Ssm[e] = __ldg(S + e);
+    const double *Stab = s_staged ? Ssm : S;
+
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
 #ifdef USFFT_MG_PROBE
@@ -144,17 +154,19 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             double slo[KC], sup[KC];
 #pragma unroll
             for (int k = 0; k < KC; ++k) slo[k] = sup[k] = 0.0;
+#pragma unroll 2
             for (int j = 0; j < Q.d; ++j) {
-                const double *Sj = S + j * W;
-                const double tlo = th_amp[j] * __ldg(Sj + 3 * ci + 2);
-                const double tup = th_amp[j] * __ldg(Sj + 3 * ci + 1);
+                const double *Sj = Stab + j * W;
+                const double tlo = th_amp[j] * Sj[3 * ci + 2];
+                const double tup = th_amp[j] * Sj[3 * ci + 1];
 #pragma unroll
                 for (int k = 0; k < KC; ++k) {
                     const int cj = cj0 + k * CJS;
-                    slo[k] = fma(tlo, __ldg(Sj + 3 * cj + 1), slo[k]);
-                    sup[k] = fma(tup, __ldg(Sj + 3 * cj + 2), sup[k]);
+                    slo[k] = fma(tlo, Sj[3 * cj + 1], slo[k]);
+                    sup[k] = fma(tup, Sj[3 * cj + 2], sup[k]);
                 }
             }
+            USFFT_MG_SMARK(19);
 #pragma unroll
             for (int k = 0; k < KC; ++k) {
                 const int cell = (cj0 + k * CJS) * n + ci;
@@ -218,7 +230,13 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         constexpr int HB = NWARP > 1 ? 32 : 0, HS = NT - HB;
         if (tid >= HB) {
             const int ht = tid - HB;
-            for (int e = ht; e < NP2; e += HS) G0[e] = G1[e] = 0.0;
+            for (int e = ht; e < 4 * n; e += HS) {       // zero rings of G0, G1 (aT aliased them)
+                const int side = e / n, o = e % n;       // ring walk: bottom, right, top, left
+                const int i = side == 0 ? o : side == 1 ? n : side == 2 ? n - o : 0;
+                const int j = side == 0 ? 0 : side == 1 ? o : side == 2 ? n : n - o;
+                const int g = j * np + ((i & 1) ? HE + (i >> 1) : (i >> 1));
+                G0[g] = G1[g] = 0.0;
+            }
             for (int e = ht; e < N1; e += HS) {          // level-1 omega D^-1 (same sum as apply1)
                 const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
                 const bool in = I >= 1 && I < m1 && J >= 1 && J < m1;
@@ -232,6 +250,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 D2[e] = dv;
                 DI2[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
             }
+            USFFT_MG_SMARK(31);
         }
 #pragma unroll
         for (int q = 0; q < BR; ++q)                     // omega D^-1 of the own nodes (0 off-mesh);
@@ -239,36 +258,30 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int c = 0; c < BC; ++c) {
                 const double dv = cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c];
                 DI0[(row0 + 1 + q) * np + ((c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1))] =
-                    (col0 + c + 1 <= nx && row0 + q + 1 <= nx) ? kMgOmega * (1.0 / dv) : 0.0;
+                    (col0 + c + 1 <= nx && row0 + q + 1 <= nx) ? kMgOmega * rcp_pos(dv) : 0.0;
             }
-        if (warp == 0) {
-        for (int e = lane; e < U3 * U3; e += 32) {       // dense level-3 operator, row-major
-            const int a = e / U3, c = e % U3;
-            const int ia = a % (m3 - 1) + 1, ja = a / (m3 - 1) + 1;
-            const int ic = c % (m3 - 1) + 1, jc = c / (m3 - 1) + 1;
-            const int g = ja * p3 + ia;
-            double v = 0.0;
-            if (a == c) v = WH3[g] + WH3[g - 1] + WV3[g] + WV3[g - p3];
-            else if (jc == ja && ic == ia + 1) v = -WH3[g];
-            else if (jc == ja && ic == ia - 1) v = -WH3[g - 1];
-            else if (ic == ia && jc == ja + 1) v = -WV3[g];
-            else if (ic == ia && jc == ja - 1) v = -WV3[g - p3];
-            AI[e] = v;
-        }
-        __syncwarp();
-        }
+        USFFT_MG_SMARK(16);
         if (warp == 0) {   // in-place Gauss-Jordan inverse of the coarsest operator (SPD, tiny):
-            // lane i keeps row i in registers, the pivot row comes by shuffles
+            // lane i assembles row i of A3 (5-point, rediscretised) in registers; the pivot row of
+            // each step comes by shuffles
+            USFFT_MG_SMARK(17);
             const int ri = lane < U3 ? lane : 0;
+            const int ia = ri % (m3 - 1) + 1, ja = ri / (m3 - 1) + 1, g = ja * p3 + ia;
+            const double wr = WH3[g], wl = WH3[g - 1], wu = WV3[g], wd = WV3[g - p3];
             double a[U3];
 #pragma unroll
-            for (int c = 0; c < U3; ++c) a[c] = AI[ri * U3 + c];
+            for (int c = 0; c < U3; ++c)
+                a[c] = c == ri ? wr + wl + wu + wd
+                     : (c == ri + 1 && ia < m3 - 1) ? -wr
+                     : (c == ri - 1 && ia > 1) ? -wl
+                     : (c == ri + (m3 - 1) && ja < m3 - 1) ? -wu
+                     : (c == ri - (m3 - 1) && ja > 1) ? -wd : 0.0;
 #pragma unroll
             for (int k = 0; k < U3; ++k) {
                 double prow[U3];
 #pragma unroll
                 for (int c = 0; c < U3; ++c) prow[c] = __shfl_sync(0xffffffffu, a[c], k);
-                const double piv = 1.0 / prow[k];
+                const double piv = rcp_pos(prow[k]);             // SPD: positive pivots
                 const double f = -a[k] * piv;
 #pragma unroll
                 for (int c = 0; c < U3; ++c) {
@@ -276,6 +289,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     else a[c] = c == k ? f : fma(f, prow[c], a[c]);
                 }
             }
+            USFFT_MG_SMARK(18);
             __syncwarp();
             if (lane < U3) {
 #pragma unroll

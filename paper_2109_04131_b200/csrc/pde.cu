@@ -188,7 +188,9 @@ template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                            const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
                            int32_t *iters, double *relres, int32_t *noconv, const double *S) {
-    const size_t dyn = sizeof(double) * ((size_t)Mg3<NC>::doubles() + (MINB * NWARP >= 12 ? 2 * BC * BR * NWARP * 32 : 0));
+    const int sw = Q.d * (3 * NC + 1);                  // staged sin table (if small enough)
+    const size_t dyn = sizeof(double) * ((size_t)Mg3<NC>::doubles() + (MINB * NWARP >= 12 ? 2 * BC * BR * NWARP * 32 : 0) +
+                                         (sw <= Mg3<NC>::SMAX ? sw : 0));
     auto kern = k_pcg_mg<NC, BC, BR, LX, NWARP, MINB>;
     USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int per_sm = 0;

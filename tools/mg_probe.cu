@@ -69,7 +69,10 @@ int main() {
         const char *sn[] = {"theta", "a table", "weights", "diag/A3/K-prep", "B (+GJ)", "C", "K"};
         int ids[] = {20, 24, 25, 26, 27, 28, 29, 21};
         for (int q = 0; q < 7; ++q) printf("setup %-16s %7lld\n", sn[q], pr[0][ids[q + 1]] - pr[0][ids[q]]);
-        printf("setup GJ (warp 0)     %7lld\n", pr[0][30] - pr[0][27]);
+        printf("setup A3+GJ (warp 0)  %7lld  = DI0 %lld + A3 %lld + GJ %lld + store %lld\n", pr[0][30] - pr[0][26],
+               pr[0][16] - pr[0][26], pr[0][17] - pr[0][16], pr[0][18] - pr[0][17], pr[0][30] - pr[0][18]);
+        for (int w = 0; w < 4; ++w) printf("a-table loop (warp %d) %7lld\n", w, pr[w][19] - pr[w][24]);
+        for (int w = 1; w < 4; ++w) printf("setup diag (warp %d)   %7lld\n", w, pr[w][31] - pr[w][26]);
     }
     printf("sample 0 of CTA 0: setup %lld cycles, CG %lld cycles for %lld iterations\n",
            pr[0][21] - pr[0][20], pr[0][22] - pr[0][21], pr[0][23]);
