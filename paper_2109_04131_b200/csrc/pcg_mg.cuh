@@ -147,41 +147,59 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         __syncthreads();
         USFFT_MG_SMARK(24);
-        {   // per-triangle a = 1 + sum_j amp_j theta_j S_j(ma) S_j(mb) (or exp) of the fine mesh:
-            // thread (ci, cj0) keeps the ci-side factors of every j and sweeps KC rows cj
-            constexpr int CJS = NT / n, KC = n / CJS;
-            const int ci = tid % n, cj0 = tid / n;
-            double slo[KC], sup[KC];
+        {   // per-triangle a = 1 + sum_j amp_j theta_j S_j(ma) S_j(mb) (or exp) of the fine mesh,
+            // a rank-d product: thread (ci0, cj0) owns a KI x KJ tile of cells (ci0 + CIS a,
+            // cj0 + CJS b) in registers
+            constexpr int KI = NT >= 4 * n ? 4 : 2, CIS = n / KI, CJS = NT / CIS, KJ = n / CJS;
+            static_assert(NT % CIS == 0 && n % CJS == 0, "coefficient tile mapping");
+            const int ci0 = tid % CIS, cj0 = tid / CIS;
+            double slo[KI][KJ], sup[KI][KJ];
 #pragma unroll
-            for (int k = 0; k < KC; ++k) slo[k] = sup[k] = 0.0;
+            for (int a = 0; a < KI; ++a)
+#pragma unroll
+                for (int k = 0; k < KJ; ++k) slo[a][k] = sup[a][k] = 0.0;
 #pragma unroll 2
             for (int j = 0; j < Q.d; ++j) {
                 const double *Sj = Stab + j * W;
-                const double tlo = th_amp[j] * Sj[3 * ci + 2];
-                const double tup = th_amp[j] * Sj[3 * ci + 1];
+                const double am = th_amp[j];
+                double tlo[KI], tup[KI], vlo[KJ], vup[KJ];
 #pragma unroll
-                for (int k = 0; k < KC; ++k) {
-                    const int cj = cj0 + k * CJS;
-                    slo[k] = fma(tlo, Sj[3 * cj + 1], slo[k]);
-                    sup[k] = fma(tup, Sj[3 * cj + 2], sup[k]);
+                for (int a = 0; a < KI; ++a) {
+                    tlo[a] = am * Sj[3 * (ci0 + CIS * a) + 2];
+                    tup[a] = am * Sj[3 * (ci0 + CIS * a) + 1];
                 }
+#pragma unroll
+                for (int k = 0; k < KJ; ++k) {
+                    vlo[k] = Sj[3 * (cj0 + CJS * k) + 1];
+                    vup[k] = Sj[3 * (cj0 + CJS * k) + 2];
+                }
+#pragma unroll
+                for (int a = 0; a < KI; ++a)
+#pragma unroll
+                    for (int k = 0; k < KJ; ++k) {
+                        slo[a][k] = fma(tlo[a], vlo[k], slo[a][k]);
+                        sup[a][k] = fma(tup[a], vup[k], sup[a][k]);
+                    }
             }
             USFFT_MG_SMARK(19);
 #pragma unroll
-            for (int k = 0; k < KC; ++k) {
-                const int cell = (cj0 + k * CJS) * n + ci;
-                aT[cell] = Q.form == 0 ? 1.0 + slo[k] : exp(slo[k]);              // lower-triangle plane
-                aT[n * n + cell] = Q.form == 0 ? 1.0 + sup[k] : exp(sup[k]);      // upper-triangle plane
-            }
+            for (int a = 0; a < KI; ++a)
+#pragma unroll
+                for (int k = 0; k < KJ; ++k) {
+                    const int cell = (cj0 + CJS * k) * n + ci0 + CIS * a;
+                    aT[cell] = Q.form == 0 ? 1.0 + slo[a][k] : exp(slo[a][k]);          // lower plane
+                    aT[n * n + cell] = Q.form == 0 ? 1.0 + sup[a][k] : exp(sup[a][k]);  // upper plane
+                }
         }
         __syncthreads();
         USFFT_MG_SMARK(25);
         // a at the centroid of T_lo / T_up of cell (ci, cj) of the mesh with cell width 2^sh h: the
         // fine triangle with the same centroid (abscissae ma, mb in units of h/3)
+        // ma = 3 ci p + ra, mb = 3 cj p + rb with p = 2^sh and (ra, rb) = (2p, p) below / (p, 2p)
+        // above the diagonal, so ma / 3 = ci p + ra / 3 and ma % 3 = ra % 3: no run-time division
         auto fcoef = [&](int ci, int cj, int up, int sh) -> double {
-            const int ma = (up ? 3 * ci + 1 : 3 * ci + 2) << sh;
-            const int mb = (up ? 3 * cj + 2 : 3 * cj + 1) << sh;
-            return aT[(ma % 3 == 1 ? n * n : 0) + (mb / 3) * n + ma / 3];
+            const int p = 1 << sh, ra = up ? p : 2 * p, rb = up ? 2 * p : p;
+            return aT[(ra % 3 == 1 ? n * n : 0) + (cj * p + rb / 3) * n + ci * p + ra / 3];
         };
         // edge weights of node (i, j) of the mesh with M cells of width 2^sh h: to (i+1, j), (i, j+1)
         auto wh = [&](int i, int j, int M, int sh) -> double {
