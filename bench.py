@@ -34,11 +34,11 @@ FLOPS_PER_NODE_ITER = 22      # Jacobi PCG, 5-point stencil: DESIGN.md §5 (algo
 def mg_flops_per_iter(n: int) -> int:
     """Algorithmic flops of one multigrid-preconditioned CG iteration on an n x n mesh (DESIGN.md
     §5): 51 per fine node (smoothing, residual, restriction share, prolongation, A u, 3 dots,
-    4 vector updates), 38 per node of the two smoothed coarse levels, and the level-3 exact solve
-    (9-point restriction + dense (m3-1)^2 product)."""
+    4 vector updates), 38 per node of the smoothed level 1, and the level-2/3 part of the cycle
+    as applied: the 9-point restriction to level 2 (10 per node) and the dense level-2 map
+    K (2 U2^2).  The per-sample setup (coefficients, operators, K) is not counted."""
     u0, u1, u2 = (n - 1) ** 2, (n // 2 - 1) ** 2, (n // 4 - 1) ** 2
-    u3 = (n // 8 - 1) ** 2
-    return 51 * u0 + 38 * (u1 + u2) + 10 * u3 + 2 * u3 * u3
+    return 51 * u0 + 38 * u1 + 10 * u2 + 2 * u2 * u2
 FP64_FMA_PER_CLK_PER_SM = 64  # B200 fp64 datapath (DESIGN.md §5): 37 TF at 1.965 GHz x 148 SMs
 
 
@@ -268,7 +268,8 @@ def run_ours(args):
                          "traffic_source": (ncu_traffic(kname) or {}).get("source"),
                          "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz",
                          "flops_per_sample_iter": fpi, "precond": "mg" if mg else "jacobi"},
-            "fft": {"kernel": "k_fft_rader_t (Rader/Stockham) + k_kappa", "ms_per_step": fft_ms,
+            "fft": {"kernel": ("k_fft400 (Rader, register four-step 20 x 20)" if P.M == 401 else
+                               "k_fft_rader_t (Rader/Stockham)") + " + k_kappa", "ms_per_step": fft_ms,
                     "achieved_gbs": fft_bytes / (fft_ms / 1e3) / 1e9 if fft_ms else None,
                     "hbm_peak_gbs": pk["hbm_gbs"],
                     "frac": (fft_bytes / (fft_ms / 1e3) / 1e9) / pk["hbm_gbs"] if fft_ms else None},
