@@ -232,6 +232,48 @@ usfft_status usfft_gather_rows(usfft_ctx *ctx, const int32_t *idx, int64_t n,
 usfft_status usfft_eval(usfft_ctx *ctx, int32_t d, const int16_t *I, int64_t nI,
                         const double *C, int64_t G, const double *Y, int64_t n, double *U);
 
+/* ---- Step 3: multiple-R1L cover of the detected set (usfft_cover_plan / usfft_cover_gather)
+ * Alg. 1 Step 3: a sampling set X of the final I = I^(1..d) on which the Fourier
+ * matrix can be inverted efficiently, realised by multiple rank-1 lattices ([KaPoVo17, Alg. 1],
+ * P:349/P:362, Remark 4 P:1662) in reading Z26: every lattice has M = the smallest prime
+ * >= max(4 (|I| - 1), N + 1) with M - 1 7-smooth; lattice q (1-based) draws z in [1, M-1]^d
+ * (Z4 draw with tag 5, t = d, i = q, l = attempt) until some still unassigned k has a residue
+ * k.z mod M unique among the residues of ALL of I (<= 100 empty draws); those k are assigned to
+ * it (first lattice wins).  Its nodes are y_i = (i z mod M)/M in all d components (use
+ * usfft_lattice / usfft_sample_pde with t = d, L = 1, line_axis = -1, zero shift).
+ *   I      host int16 [nI][d] frequency rows
+ *   out    cover: nlat <= 64 lattices, shared M, z host int64 [nlat][d]
+ *   assign host int32 [nI]: the lattice of frequency a;  bin host int32 [nI]: its residue there
+ * Errors: EINVAL on bad sizes, ENOTRECON after 100 consecutive empty draws or > 64 lattices.
+ * Pure host computation (no device work, no sync). */
+typedef struct {
+    int32_t nlat;
+    int32_t d;
+    int64_t M;
+    int64_t z[64 * 64];
+} usfft_cover_desc;
+
+usfft_status usfft_cover_plan(usfft_ctx *ctx, int64_t seed, int32_t d, int32_t N, const int16_t *I,
+                              int64_t nI, usfft_cover_desc *out, int32_t *assign, int32_t *bin);
+
+/* Step 3 coefficients of one cover lattice: coef[g][idx[a]] = v(k, g) = F^[g][bin[a]] / M for
+ * a < n (each k read on its assigned lattice), where F^[m] = F[g][m] for m <= M/2
+ * and conj(F[g][M-m]) above (the half spectrum of usfft_lattice_fft with L = 1).
+ *   spectra dev fp64x2 [G][M/2+1]; idx, bin dev int32 [n]; coef dev fp64x2 [G][nI] */
+usfft_status usfft_cover_gather(usfft_ctx *ctx, int64_t M, int64_t G, const double *spectra,
+                                const int32_t *idx, const int32_t *bin, int64_t n, double *coef,
+                                int64_t nI);
+
+/* ---- accuracy metric (usfft_eval_err) ------------------------------------------------------
+ * per node g over the n test points y_q (Y dev fp64 [d][n]),
+ *   err[g][0] = (1/n) sum_q |Uref[g][q] - u(g, y_q)|,  err[g][1] = sqrt((1/n) sum_q |.|^2),
+ *   err[g][2] = max_q |.|,   u(g, y) = sum_{k in I} C[g][k] e^{2 pi i k . y} (complex modulus).
+ * I dev int16 [nI][d]; C dev fp64x2 [G][nI]; Uref dev fp64 [G][n] (the FE solutions at Y);
+ * err dev fp64 [G][3].  Fixed reduction order (deterministic).  Uses ctx workspace. */
+usfft_status usfft_eval_err(usfft_ctx *ctx, int32_t d, const int16_t *I, int64_t nI,
+                            const double *C, int64_t G, const double *Y, int64_t n,
+                            const double *Uref, double *err);
+
 #ifdef __cplusplus
 }
 #endif

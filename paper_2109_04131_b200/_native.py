@@ -38,6 +38,10 @@ class PlanOut(C.Structure):
                 ("z", i64 * 2048), ("shift", f64 * 64)]
 
 
+class CoverDesc(C.Structure):
+    _fields_ = [("nlat", i32), ("d", i32), ("M", i64), ("z", i64 * 4096)]
+
+
 # name -> (restype, argtypes)
 _SIGS = {
     "usfft_init": (i32, [C.POINTER(vp), C.c_int, vp]),
@@ -58,6 +62,9 @@ _SIGS = {
                             vp, vp]),
     "usfft_gather_rows": (i32, [vp, vp, i64, vp, i32, vp, i32, vp]),
     "usfft_eval": (i32, [vp, i32, vp, i64, vp, i64, vp, i64, vp]),
+    "usfft_cover_plan": (i32, [vp, i64, i32, i32, vp, i64, C.POINTER(CoverDesc), vp, vp]),
+    "usfft_cover_gather": (i32, [vp, i64, i64, vp, vp, vp, i64, vp, i64]),
+    "usfft_eval_err": (i32, [vp, i32, vp, i64, vp, i64, vp, i64, vp, vp]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -215,3 +215,48 @@ def usfft_eval(ctx: Context, I, C_, Y, U):
     st = ctx.lib.usfft_eval(ctx.h, d, _p(I, torch.int16), nI, _p(C_, torch.float64), G,
                             _p(Y, torch.float64), n, _p(U, torch.float64))
     _check(ctx, st, "usfft_eval")
+
+
+@dataclass
+class Cover:
+    """A Step-3 multiple-R1L cover (usfft_cover_desc) of a frequency set."""
+    d: int
+    M: int
+    z: np.ndarray          # int64 [nlat][d]
+    assign: np.ndarray     # int32 [nI]
+    bin: np.ndarray        # int32 [nI]
+
+    def lattice(self, q: int) -> Plan:
+        """Lattice q as a one-lattice plan (t = d, zero shift: X is a subset of T^d)."""
+        return Plan(self.d, self.M, 1, self.d, -1, self.z[q:q + 1].copy(), np.zeros(self.d))
+
+
+def usfft_cover_plan(ctx: Context, seed: int, N_: int, I_host: np.ndarray) -> Cover:
+    I = np.ascontiguousarray(I_host, dtype=np.int16)
+    nI, d = I.shape
+    out = N.CoverDesc()
+    assign = np.empty(nI, dtype=np.int32)
+    binv = np.empty(nI, dtype=np.int32)
+    _check(ctx, ctx.lib.usfft_cover_plan(ctx.h, seed, d, N_, I.ctypes.data, nI, C.byref(out),
+                                         assign.ctypes.data, binv.ctypes.data), "usfft_cover_plan")
+    z = np.ctypeslib.as_array(out.z)[: out.nlat * d].reshape(out.nlat, d).copy()
+    return Cover(d, int(out.M), z, assign, binv)
+
+
+def usfft_cover_gather(ctx: Context, M: int, G: int, spectra, idx, bins, coef):
+    """coef [G][nI][2] fp64 (device): the entries idx of the frequencies read on this lattice."""
+    nI = coef.shape[1]
+    st = ctx.lib.usfft_cover_gather(ctx.h, M, G, _p(spectra, torch.float64), _p(idx, torch.int32),
+                                    _p(bins, torch.int32), int(idx.numel()), _p(coef, torch.float64), nI)
+    _check(ctx, st, "usfft_cover_gather")
+
+
+def usfft_eval_err(ctx: Context, I, C_, Y, Uref, err):
+    """err [G][3] = (err_1, err_2, err_inf) of the approximant against Uref at the points Y."""
+    nI, d = I.shape
+    G = C_.shape[0]
+    n = Y.shape[1]
+    st = ctx.lib.usfft_eval_err(ctx.h, d, _p(I, torch.int16), nI, _p(C_, torch.float64), G,
+                                _p(Y, torch.float64), n, _p(Uref, torch.float64), _p(err, torch.float64))
+    _check(ctx, st, "usfft_eval_err")
+

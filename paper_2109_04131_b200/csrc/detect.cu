@@ -291,3 +291,31 @@ extern "C" usfft_status usfft_resolve(usfft_ctx *c, const usfft_lattice_desc *la
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
+
+// Step 3 (Z26): coefficients of the frequencies assigned to one cover lattice
+namespace usfft {
+__global__ void k_cover_gather(int64_t M, int64_t G, const double2 *__restrict__ F,
+                               const int32_t *__restrict__ idx, const int32_t *__restrict__ bin,
+                               int64_t n, double2 *__restrict__ coef, int64_t nI) {
+    const int64_t Mh = M / 2 + 1;
+    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < G * n;
+         e += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t g = e / n, a = e - g * n;
+        coef[g * nI + idx[a]] = spec_value(F + g * Mh, M, bin[a]);
+    }
+}
+}  // namespace usfft
+
+extern "C" usfft_status usfft_cover_gather(usfft_ctx *c, int64_t M, int64_t G, const double *spectra,
+                                           const int32_t *idx, const int32_t *bin, int64_t n,
+                                           double *coef, int64_t nI) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, M >= 2 && G >= 0 && n >= 0 && nI >= n, "bad sizes");
+    if (G == 0 || n == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, spectra && idx && bin && coef, "NULL argument");
+    k_cover_gather<<<grid1d(G * n, 256), 256, 0, c->stream>>>(
+        M, G, reinterpret_cast<const double2 *>(spectra), idx, bin, n, reinterpret_cast<double2 *>(coef), nI);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+

@@ -69,9 +69,130 @@ k_eval(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__re
     }
 }
 
+// usfft_eval_err: the same tiled sum with both the real and the imaginary part, the modulus of
+// the difference to the FE reference per (g, q), and per-tile partial sums (|.|, |.|^2, max)
+// reduced over the tile's 64 points by shuffles in a fixed order; k_eval_err_reduce then adds
+// the tiles of every node in tile order.
+__global__ void __launch_bounds__(256)
+k_eval_err(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
+           int64_t G, const double *__restrict__ Y, int64_t n, const double *__restrict__ Uref,
+           double *__restrict__ part) {
+    __shared__ double cre[EV_TK][EV_TG + 1], cim[EV_TK][EV_TG + 1];
+    __shared__ double cs[EV_TK][EV_TQ + 1], sn[EV_TK][EV_TQ + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t g0 = (int64_t)blockIdx.y * EV_TG, q0 = (int64_t)blockIdx.x * EV_TQ;
+    double are[4][4] = {}, aim[4][4] = {};
+    for (int64_t k0 = 0; k0 < nI; k0 += EV_TK) {
+        for (int e = threadIdx.x; e < EV_TK * EV_TG; e += blockDim.x) {
+            const int kk = e / EV_TG, gg = e % EV_TG;
+            double2 v = make_double2(0.0, 0.0);
+            if (k0 + kk < nI && g0 + gg < G) v = C[(g0 + gg) * nI + k0 + kk];
+            cre[kk][gg] = v.x;
+            cim[kk][gg] = v.y;
+        }
+        for (int e = threadIdx.x; e < EV_TK * EV_TQ; e += blockDim.x) {
+            const int kk = e / EV_TQ, qq = e % EV_TQ;
+            double c = 0.0, s = 0.0;
+            if (k0 + kk < nI && q0 + qq < n) {
+                double ph = 0.0;
+                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
+                sincospi(2.0 * (ph - rint(ph)), &s, &c);
+            }
+            cs[kk][qq] = c;
+            sn[kk][qq] = s;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int kk = 0; kk < EV_TK; ++kk) {
+            double a_re[4], a_im[4], b_c[4], b_s[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                a_re[r] = cre[kk][ty * 4 + r];
+                a_im[r] = cim[kk][ty * 4 + r];
+                b_c[r] = cs[kk][tx * 4 + r];
+                b_s[r] = sn[kk][tx * 4 + r];
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int s2 = 0; s2 < 4; ++s2) {
+                    are[r][s2] += a_re[r] * b_c[s2] - a_im[r] * b_s[s2];
+                    aim[r][s2] += a_re[r] * b_s[s2] + a_im[r] * b_c[s2];
+                }
+        }
+        __syncthreads();
+    }
+    const int64_t ntile = gridDim.x;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t g = g0 + ty * 4 + r;
+        double s1 = 0.0, s2s = 0.0, mx = 0.0;
+#pragma unroll
+        for (int s2 = 0; s2 < 4; ++s2) {
+            const int64_t q = q0 + tx * 4 + s2;
+            if (g < G && q < n) {
+                const double dr = Uref[g * n + q] - are[r][s2], di = -aim[r][s2];
+                const double m = hypot(dr, di);
+                s1 += m;
+                s2s = fma(m, m, s2s);
+                mx = fmax(mx, m);
+            }
+        }
+#pragma unroll
+        for (int o = 8; o > 0; o >>= 1) {           // the 16 threads of row group ty
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2s += __shfl_xor_sync(0xffffffffu, s2s, o);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if (tx == 0 && g < G) {
+            double *pp = part + (g * ntile + blockIdx.x) * 3;
+            pp[0] = s1;
+            pp[1] = s2s;
+            pp[2] = mx;
+        }
+    }
+}
+
+__global__ void k_eval_err_reduce(int64_t G, int64_t ntile, int64_t n, const double *__restrict__ part,
+                                  double *__restrict__ err) {
+    for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
+        double s1 = 0.0, s2 = 0.0, mx = 0.0;
+        for (int64_t t = 0; t < ntile; ++t) {
+            const double *pp = part + (g * ntile + t) * 3;
+            s1 += pp[0];
+            s2 += pp[1];
+            mx = fmax(mx, pp[2]);
+        }
+        err[g * 3 + 0] = s1 / (double)n;
+        err[g * 3 + 1] = sqrt(s2 / (double)n);
+        err[g * 3 + 2] = mx;
+    }
+}
+
 }  // namespace usfft
 
 using namespace usfft;
+
+extern "C" usfft_status usfft_eval_err(usfft_ctx *c, int32_t d, const int16_t *I, int64_t nI,
+                                       const double *C, int64_t G, const double *Y, int64_t n,
+                                       const double *Uref, double *err) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, d >= 1 && d <= kMaxD && nI >= 0 && G >= 0 && n >= 1, "bad sizes");
+    if (G == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, Y && Uref && err, "Y / Uref / err NULL");
+    USFFT_REQUIRE(c, nI == 0 || (I && C), "I / C NULL");
+    const int64_t ntile = (n + EV_TQ - 1) / EV_TQ;
+    USFFT_REQUIRE(c, ntile <= 0x7fffffff && (G + EV_TG - 1) / EV_TG <= 65535, "grid too large");
+    usfft_status s = ensure(c, &c->ws, &c->ws_size, sizeof(double) * 3 * (size_t)(G * ntile));
+    if (s) return s;
+    double *part = static_cast<double *>(c->ws);
+    dim3 grid((unsigned)ntile, (unsigned)((G + EV_TG - 1) / EV_TG));
+    k_eval_err<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref, part);
+    USFFT_CHECK_LAUNCH(c);
+    k_eval_err_reduce<<<grid1d(G, 128), 128, 0, c->stream>>>(G, ntile, n, part, err);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
 
 extern "C" usfft_status usfft_eval(usfft_ctx *c, int32_t d, const int16_t *I, int64_t nI,
                                    const double *C, int64_t G, const double *Y, int64_t n,

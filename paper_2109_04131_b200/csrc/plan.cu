@@ -129,3 +129,57 @@ extern "C" usfft_status usfft_plan_round(usfft_ctx *c, const usfft_plan_in *in,
     }
     return fail(c, USFFT_ENOTRECON, "no reconstructing lattice with M <= 2^26");
 }
+
+// Step 3: multiple-R1L cover of I, reading Z26 (include/usfft.h).  Host only.
+extern "C" usfft_status usfft_cover_plan(usfft_ctx *c, int64_t seed, int32_t d, int32_t N,
+                                         const int16_t *I, int64_t nI, usfft_cover_desc *out,
+                                         int32_t *assign, int32_t *bin) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, out && assign && bin && I, "NULL argument");
+    USFFT_REQUIRE(c, d >= 1 && d <= 64 && N >= 0 && nI >= 1 && nI <= (int64_t(1) << 24), "bad sizes");
+    const int64_t M = lattice_prime(std::max<int64_t>(4 * (nI - 1), (int64_t)N + 1));
+    USFFT_REQUIRE(c, M < (int64_t(1) << 31), "cover lattice too large");
+    out->nlat = 0;
+    out->d = d;
+    out->M = M;
+    std::vector<int64_t> res((size_t)nI);
+    std::vector<int32_t> cnt((size_t)M);
+    for (int64_t a = 0; a < nI; ++a) assign[a] = -1;
+    int64_t left = nI;
+    int empty = 0;
+    uint64_t attempt = 0;
+    int64_t z[64];
+    while (left > 0) {
+        USFFT_REQUIRE(c, out->nlat < 64, "cover needs more than 64 lattices");
+        const uint64_t q = (uint64_t)out->nlat + 1;
+        for (int j = 1; j <= d; ++j)
+            z[j - 1] = 1 + (int64_t)(draw((uint64_t)seed, 5, (uint64_t)d, q, attempt, (uint64_t)j) % (uint64_t)(M - 1));
+        ++attempt;
+        std::fill(cnt.begin(), cnt.end(), 0);
+        for (int64_t a = 0; a < nI; ++a) {               // residues of the FULL set
+            int64_t r = 0;
+            for (int j = 0; j < d; ++j) r = (r + (int64_t)I[a * d + j] * z[j]) % M;
+            if (r < 0) r += M;
+            res[(size_t)a] = r;
+            ++cnt[(size_t)r];
+        }
+        int64_t got = 0;
+        for (int64_t a = 0; a < nI; ++a)
+            if (assign[a] < 0 && cnt[(size_t)res[(size_t)a]] == 1) {
+                assign[a] = out->nlat;
+                bin[a] = (int32_t)res[(size_t)a];
+                ++got;
+            }
+        if (got == 0) {
+            if (++empty > 100) return fail(c, USFFT_ENOTRECON, "cover: 100 consecutive empty draws");
+            continue;
+        }
+        empty = 0;
+        attempt = 0;
+        for (int j = 0; j < d; ++j) out->z[(int64_t)out->nlat * d + j] = z[j];
+        ++out->nlat;
+        left -= got;
+    }
+    return USFFT_OK;
+}
+

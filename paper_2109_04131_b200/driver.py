@@ -190,6 +190,63 @@ class Detector:
         I1d = self.step1(log)
         return self.step2(I1d, log)
 
+    # ------------------------------------------------------------------------------------------
+    def step3(self, I_rows: torch.Tensor):
+        """Step 3: multiple-R1L cover of I (reading Z26, usfft_cover_plan), the samples
+        on every cover lattice (this rank's share, exchanged like a round) and the coefficient of
+        every k in I read on its lattice (usfft_cover_gather).  I_rows: int16 [nI][d] (device).
+        Returns (cover, coef fp64 [G_loc][nI][2])."""
+        cfg, ctx, dev = self.cfg, self.ctx, self.dev
+        I_host = I_rows.to("cpu").numpy()
+        cov = B.usfft_cover_plan(ctx, cfg["seed"], cfg["N"], I_host)
+        nI = I_host.shape[0]
+        M, Mh = cov.M, cov.M // 2 + 1
+        coef = torch.zeros((self.G_loc, nI, 2), dtype=torch.float64, device=dev)
+        assign = torch.from_numpy(cov.assign).to(dev)
+        bins = torch.from_numpy(cov.bin).to(dev)
+        for q in range(cov.z.shape[0]):
+            plan = cov.lattice(q)
+            b0, b1 = partition(M, self.P, self.rank)
+            nb = b1 - b0
+            u = torch.empty((self.G, nb), dtype=torch.float64, device=dev)
+            if nb and self.blackbox is not None:
+                u = self.blackbox(self, plan, b0, nb)
+            elif nb:
+                B.usfft_sample_pde(ctx, self.pde, plan, b0, nb, u, nb)
+            self.n_samples += M
+            slabs, sb = self.ex.transpose(u, self.G, M)
+            spectra = torch.empty((self.G_loc, 1, Mh, 2), dtype=torch.float64, device=dev)
+            B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, None, 0, spectra, None, None)
+            sel = torch.nonzero(assign == q).reshape(-1).to(torch.int32).contiguous()
+            B.usfft_cover_gather(ctx, M, self.G_loc, spectra, sel, bins[sel].contiguous(), coef)
+        return cov, coef
+
+    def errors(self, I_rows: torch.Tensor, coef: torch.Tensor, Y: torch.Tensor):
+        """Accuracy metric of the approximant at n test points Y (fp64 [d][n], device):
+        FE reference solves at Y (this rank's share, exchanged to node shards) and
+        usfft_eval_err on this rank's nodes.  Returns (err fp64 [G_loc][3], U_check [G_loc][n])."""
+        ctx, dev, d = self.ctx, self.dev, self.cfg["d"]
+        n = Y.shape[1]
+        plan = B.Plan(d, n, 1, d, -1, np.zeros((1, d), dtype=np.int64), np.zeros(d))
+        b0, b1 = partition(n, self.P, self.rank)
+        nb = b1 - b0
+        u = torch.empty((self.G, nb), dtype=torch.float64, device=dev)
+        if nb:
+            B.usfft_sample_pde(ctx, self.pde, plan, b0, nb, u, nb, Y[:, b0:b1].contiguous())
+        slabs, sb = self.ex.transpose(u, self.G, n)
+        if self.P == 1:
+            U = slabs.reshape(self.G_loc, n)
+        else:
+            parts, off = [], 0
+            for p in range(self.P):
+                w = sb[p + 1] - sb[p]
+                parts.append(slabs[off:off + self.G_loc * w].reshape(self.G_loc, w))
+                off += self.G_loc * w
+            U = torch.cat(parts, dim=1).contiguous()
+        err = torch.empty((self.G_loc, 3), dtype=torch.float64, device=dev)
+        B.usfft_eval_err(ctx, I_rows, coef, Y, U, err)
+        return err, U
+
 
 def to_numpy_rows(I: torch.Tensor) -> np.ndarray:
     return I.to("cpu").numpy().astype(np.int64)
