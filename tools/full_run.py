@@ -1,0 +1,64 @@
+"""Whole Alg. 1 on one workload: Steps 1-2 (detection), Step 3 (multiple-R1L coefficients) and
+the accuracy metric err_1 / err_2 / err_inf at n_test uniform test parameters.
+
+    python tools/full_run.py [--config 2] [--n-test 10000]
+
+Prints one JSON line: samples per step, times (CUDA events), |I| and q = |I| / s (Remark on
+P:1613-1619), and the errors (max and mean over the nodes chi_g).  Single GPU.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--n-test", type=int, default=10000)
+    args = ap.parse_args()
+    import numpy as np
+    import torch
+    from paper_2109_04131_b200.driver import Detector
+    from usfft_inputs import config, uniform_points
+
+    cfg = config(args.config)
+    det = Detector(cfg)
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
+    t0 = time.perf_counter()
+    ev[0].record()
+    log = []
+    I, _ = det.run(log)
+    ev[1].record()
+    n_detect = det.n_samples
+    cov, coef = det.step3(I)
+    ev[2].record()
+    n_step3 = det.n_samples - n_detect
+    Y = torch.as_tensor(uniform_points(1000 + args.config, cfg["d"], args.n_test), dtype=torch.float64,
+                        device="cuda")
+    err, _ = det.errors(I, coef, Y)
+    ev[3].record()
+    torch.cuda.synchronize()
+    wall = time.perf_counter() - t0
+    e = err.cpu().numpy()
+    out = {
+        "workload": f"config{args.config}:{cfg['name']}", "d": cfg["d"], "n": cfg["n"], "N": cfg["N"],
+        "s": cfg["s"], "rounds": len(log), "samples_detection": n_detect, "samples_step3": n_step3,
+        "step3_share": n_step3 / (n_detect + n_step3), "nI": int(I.shape[0]), "q": I.shape[0] / cfg["s"],
+        "cover_lattices": int(cov.z.shape[0]), "cover_M": int(cov.M),
+        "ms_detection": ev[0].elapsed_time(ev[1]), "ms_step3": ev[1].elapsed_time(ev[2]),
+        "ms_errors": ev[2].elapsed_time(ev[3]), "wall_s": wall, "n_test": args.n_test,
+        "err1_max": float(e[:, 0].max()), "err2_max": float(e[:, 1].max()), "errinf_max": float(e[:, 2].max()),
+        "err2_mean": float(e[:, 1].mean()),
+    }
+    print(json.dumps(out), flush=True)
+
+
+if __name__ == "__main__":
+    main()
