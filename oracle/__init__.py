@@ -14,7 +14,7 @@ against.  It is NOT part of the product:
 
 Citation convention: ``P:n`` = line n of the paper's PAPER.md (LaTeX source), with the
 section / equation / algorithm it falls in; ``S:n`` = line n of SPEC.md.  Readings of
-places where the paper is silent are labelled Z1..Z25 as in DESIGN.md §3.
+places where the paper is silent are labelled Z1..Z26 as in DESIGN.md §3.
 
 Pin status (what fixes each function besides itself; see tests/test_oracle_*.py):
 
@@ -33,6 +33,10 @@ detect.*               brute force on tiny inputs; Thm 1.1 exact recovery of spa
                        trig polynomials (SPEC acceptance 1); invariants
 usfft.run              exact support/coefficient recovery on sparse trig polynomials
 evaluate.evaluate      SPEC special cases; direct trig identities
+cover.build_cover      brute-force alias-freeness against the full set; Remark 4 lattice
+                       count / size bound; singleton
+cover.cover_coeffs     exact recovery of polynomials supported on I; zero samples
+cover.errors           closed forms (constant offset, single spike, complex modulus)
 mode-A detected sets   parity unpinned on PDE data (only trig-polynomial exactness pins
 on PDE samples         the algorithm; PDE-data sets are oracle-vs-GPU only, Z25)
 =====================  ==========================================================
