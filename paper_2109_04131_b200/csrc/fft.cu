@@ -150,15 +150,16 @@ usfft_status launch_rader_t(usfft_ctx *c, const double *u, const SlabParams &S, 
 }
 
 usfft_status launch_fft400(usfft_ctx *c, const double *u, const SlabParams &S, int64_t G_loc,
-                           int32_t L, const RaderArgs &A, double2 *F) {
+                           int32_t L, const RaderArgs &A, double2 *F, bool paired) {
     constexpr int RPC = 4;
     const int64_t rows = G_loc * L;
-    const size_t smem = sizeof(double2) * (size_t)(101 + 20 * 21) * RPC;
-    auto kern = k_fft400<RPC>;
+    const int64_t units = paired ? G_loc * ((L + 1) / 2) : rows;   // per-node lattice pairs or rows
+    const size_t smem = sizeof(double2) * (size_t)((paired ? 402 : 201) + 20 * 21) * RPC;
+    auto kern = paired ? k_fft400p<RPC> : k_fft400<RPC>;
     USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * RPC, smem));
-    int64_t grid = (rows + RPC - 1) / RPC;
+    int64_t grid = (units + RPC - 1) / RPC;
     const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
     if (grid > resident) grid = resident;                 // persistent: each warp loops over rows
     kern<<<(unsigned)grid, 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
@@ -334,7 +335,7 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         const bool generic = force && force[0] == 'g';     // USFFT_DFT=generic: runtime-plan kernel
         if (!generic && R.N == 96) s = launch_rader_t<96, 1, 4>(c, u, S, G_loc, L, A, Fo);
         else if (!generic && R.N == 400 && !(force && force[0] == 's'))   // USFFT_DFT=stockham
-            s = launch_fft400(c, u, S, G_loc, L, A, Fo);
+            s = launch_fft400(c, u, S, G_loc, L, A, Fo, force && force[0] == 'p');   // =paired
         else if (!generic && R.N == 400) s = launch_rader_t<400, 1, 4>(c, u, S, G_loc, L, A, Fo);
         else if (!generic && R.N == 2016) s = launch_rader_t<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
         else if (!generic && R.N == 4000) s = launch_rader_t<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);

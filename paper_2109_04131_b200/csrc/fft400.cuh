@@ -88,7 +88,7 @@ __global__ void __launch_bounds__(32 * RPC)
 k_fft400(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_t L,
          const RaderArgs A, double2 *__restrict__ F, int64_t rows) {
     constexpr int M = 401, MH = 201, PER = (M + 31) / 32;
-    constexpr int XS = 202;                               // staged real row (doubles, padded)
+    constexpr int XS = 402;                               // staged real row (doubles, padded)
     constexpr int WB = XS / 2 + 20 * 21;                  // double2 per warp: row + transpose / output
     extern __shared__ double2 sm4[];
     const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
@@ -154,6 +154,138 @@ k_fft400(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_
         double2 *dst = F + row * MH;
         for (int m = lane; m < MH; m += 32) dst[m] = m == 0 ? make_double2(part, 0.0) : T[m];
         __syncwarp();                                     // buffers are reused by the next row
+    }
+}
+
+// Option (USFFT_DFT=paired; measured no faster than one row per warp: the kernel is latency-
+// bound with 8 warps per SM, not fp64-throughput-bound).
+// Two real rows per complex transform: z = a0 + i a1, the Rader sequences of the lattices
+// 2j and 2j+1 of one node g (pairs never straddle nodes, so a row's result does not depend on
+// how the nodes are split across ranks or launches; an odd L leaves its last lattice paired
+// with a zero row).
+// FFT(z) = Z gives A0 = (Z + conj Z~) / 2 and A1 = (Z - conj Z~) / 2i with Z~[k] = Z[N - k] (a
+// shuffle from lane (20 - k1) mod 20); the products P_j = conj(A_j . FFT(b)/N) are packed as
+// P0 + i P1 for the second transform D, whose halves separate because each row's output
+// satisfies c[q + N/2] = conj(c[q]) (real input: X[M - m] = conj X[m] and g^{N/2} = -1 mod M):
+// c0 = (D[q] + conj D[q+200]) / 2, c1 = (D[q] - conj D[q+200]) / 2i, both lane-local.
+template <int RPC>
+__global__ void __launch_bounds__(32 * RPC)
+k_fft400p(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_t L,
+          const RaderArgs A, double2 *__restrict__ F, int64_t rows) {
+    constexpr int M = 401, MH = 201, PER = (M + 31) / 32;
+    constexpr int XS = 402;                               // one staged real row (doubles, padded)
+    constexpr int WB = XS + 20 * 21;                      // double2 per warp: two rows + transpose
+    extern __shared__ double2 sm4[];
+    const int w = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    double *xs0 = reinterpret_cast<double *>(sm4 + (size_t)w * WB), *xs1 = xs0 + XS;
+    double2 *T = sm4 + (size_t)w * WB + XS;               // transpose buffer, then output staging
+    const bool one_slab = S.nslab == 1;
+    const int64_t LP = (L + 1) / 2, pairs = (rows / L) * LP;     // rows = G_loc * L
+    const int64_t stride = (int64_t)gridDim.x * RPC;
+    int64_t pr = (int64_t)blockIdx.x * RPC + w;
+    double xv0[PER], xv1[PER];
+    auto fetch1 = [&](int64_t rw, double (&xv)[PER]) {
+        if (rw < 0) {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) xv[k] = 0.0;
+            return;
+        }
+        const int64_t g = rw / L, l = rw - g * L;
+        if (one_slab) {
+            const double *src = u + g * (int64_t)L * M + l * M;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int i = lane + 32 * k;
+                xv[k] = i < M ? __ldg(src + i) : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int i = lane + 32 * k;
+                xv[k] = i < M ? sample_at(u, S, G_loc, g, l * M + i) : 0.0;
+            }
+        }
+    };
+    // rows of pair q: (g, 2j) and (g, 2j+1) with g = q / LP, j = q % LP (-1: the zero row)
+    auto row0 = [&](int64_t q) { return (q / LP) * L + 2 * (q % LP); };
+    auto row1 = [&](int64_t q) { return 2 * (q % LP) + 1 < L ? row0(q) + 1 : int64_t(-1); };
+    if (pr < pairs) {
+        fetch1(row0(pr), xv0);
+        fetch1(row1(pr), xv1);
+    }
+    for (; pr < pairs; pr += stride) {
+        const int64_t r0 = row0(pr), r1 = row1(pr);
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = lane + 32 * k;
+            if (i < M) {
+                xs0[i] = xv0[k];
+                xs1[i] = xv1[k];
+            }
+            p0 += xv0[k];
+            p1 += xv1[k];
+        }
+        if (pr + stride < pairs) {                        // overlaps the transforms below
+            fetch1(row0(pr + stride), xv0);
+            fetch1(row1(pr + stride), xv1);
+        }
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {                // X[0] of both rows
+            p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+            p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+        }
+        __syncwarp();
+        const double x00 = xs0[0], x01 = xs1[0];
+        double2 v[20], a[20];
+        if (lane < 20) {
+#pragma unroll
+            for (int n1 = 0; n1 < 20; ++n1) {
+                const int pi = __ldg(A.perm + 20 * n1 + lane);
+                v[n1] = make_double2(xs0[pi], xs1[pi]);
+            }
+        }
+        fft400_core(v, a, T, A.tw, lane);                 // Z: lane k1, register k2
+        const int src = lane == 0 ? 0 : (lane < 20 ? 20 - lane : lane);
+#pragma unroll
+        for (int k2 = 0; k2 < 20; ++k2) {                 // separate, multiply, pack
+            const double2 zs = a[19 - k2];
+            double2 zm = make_double2(__shfl_sync(0xffffffffu, zs.x, src), __shfl_sync(0xffffffffu, zs.y, src));
+            if (lane == 0) zm = a[(20 - k2) % 20];
+            const double2 z = a[k2];
+            const double2 A0 = make_double2(0.5 * (z.x + zm.x), 0.5 * (z.y - zm.y));
+            const double2 A1 = make_double2(0.5 * (z.y + zm.y), -0.5 * (z.x - zm.x));
+            const double2 bf = __ldg(A.bf + (lane < 20 ? lane : 0) + 20 * k2);
+            const double2 c0 = cmul(A0, bf), c1 = cmul(A1, bf);
+            // P0 + i P1 with P_j = conj(c_j)
+            v[k2] = make_double2(c0.x + c1.y, -c0.y + c1.x);
+        }
+        fft400_core(v, a, T, A.tw, lane);                 // D = c0 + i c1 per (lane, register)
+        if (lane < 20) {
+#pragma unroll
+            for (int k2 = 0; k2 < 10; ++k2) {
+                const double2 dq = a[k2], dh = a[k2 + 10];
+                // c0 = (D[q] + conj D[q+200]) / 2,  c1 = (D[q] - conj D[q+200]) / 2i
+                const double2 c0 = make_double2(0.5 * (dq.x + dh.x), 0.5 * (dq.y - dh.y));
+                const double2 c1 = make_double2(0.5 * (dq.y + dh.y), -0.5 * (dq.x - dh.x));
+                const int m = __ldg(A.outidx + lane + 20 * k2);   // X[g^-q] = x0 + conj c[q]
+                if (m < MH) {
+                    T[m] = make_double2(x00 + c0.x, -c0.y);
+                    T[MH + m] = make_double2(x01 + c1.x, -c1.y);
+                } else {                                  // q + 200 maps to M - m <= M/2
+                    T[M - m] = make_double2(x00 + c0.x, c0.y);
+                    T[MH + M - m] = make_double2(x01 + c1.x, c1.y);
+                }
+            }
+        }
+        __syncwarp();
+        double2 *dst0 = F + r0 * MH;
+        for (int m = lane; m < MH; m += 32) dst0[m] = m == 0 ? make_double2(p0, 0.0) : T[m];
+        if (r1 >= 0) {
+            double2 *dst1 = F + r1 * MH;
+            for (int m = lane; m < MH; m += 32) dst1[m] = m == 0 ? make_double2(p1, 0.0) : T[MH + m];
+        }
+        __syncwarp();                                     // buffers are reused by the next pair
     }
 }
 

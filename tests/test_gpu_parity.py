@@ -359,16 +359,16 @@ def test_eval_parity(B, ctx):
 
 # ------------------------------------------------------------------------------ kernel variants
 def test_fft_variants_agree(B, ctx, monkeypatch):
-    """Rader FFT: compile-time kernels (four-step FFT-400 at M = 401, Stockham otherwise),
-    the compile-time Stockham kernel, the runtime-plan kernel and the direct DFT kernel all
-    match the oracle's direct DFT."""
+    """Rader FFT: compile-time kernels (four-step FFT-400 at M = 401, Stockham otherwise), the
+    four-step kernel on lattice pairs, the compile-time Stockham kernel, the runtime-plan kernel
+    and the direct DFT kernel all match the oracle's direct DFT (odd L: a half pair)."""
     from paper_2109_04131_b200.binding import Plan
     for G, M, L in ((5, 401, 3), (2, 4001, 2), (4, 97, 5)):
         U, z, J, bins = _round_inputs(M, G, M, L, 64)
         p = Plan(3, M, L, 3, -1, z, np.zeros(3))
         Mh = M // 2 + 1
         out = []
-        for mode in ("rader", "stockham", "generic", "direct"):
+        for mode in ("rader", "paired", "stockham", "generic", "direct"):
             monkeypatch.setenv("USFFT_DFT", mode)
             sp = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
             km = torch.empty((G, 64), dtype=torch.float64, device="cuda")
