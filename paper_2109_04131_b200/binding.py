@@ -89,19 +89,26 @@ class Plan:
     shift: np.ndarray    # float64 [d]
 
     def desc(self):
-        z = np.ascontiguousarray(self.z, dtype=np.int64)
-        s = np.ascontiguousarray(self.shift, dtype=np.float64)
-        dsc = N.LatticeDesc(self.d, self.t_z, self.line_axis, self.L, self.M,
-                            z.ctypes.data_as(C.POINTER(C.c_int64)),
-                            s.ctypes.data_as(C.POINTER(C.c_double)))
-        return dsc, (z, s)                              # keep the arrays alive
+        """The usfft_lattice_desc of this plan (built once; the arrays stay referenced)."""
+        cached = self.__dict__.get("_desc")
+        if cached is None:
+            z = np.ascontiguousarray(self.z, dtype=np.int64)
+            s = np.ascontiguousarray(self.shift, dtype=np.float64)
+            dsc = N.LatticeDesc(self.d, self.t_z, self.line_axis, self.L, self.M,
+                                z.ctypes.data_as(C.POINTER(C.c_int64)),
+                                s.ctypes.data_as(C.POINTER(C.c_double)))
+            cached = (dsc, (z, s))
+            self.__dict__["_desc"] = cached
+        return cached
 
 
 def usfft_plan_round(ctx: Context, seed: int, step: int, t: int, i: int, d: int, N_: int,
                      s_tilde: int, mode: str, nJ: int, I_prev=None, n_prev: int = 1,
                      kt=None) -> Plan:
     pin = N.PlanIn(seed, step, t, i, d, N_, s_tilde, 1 if mode == "R" else 0, 0, nJ)
-    out = N.PlanOut()
+    out = ctx.__dict__.get("_plan_out")                 # reused host struct (16 KB)
+    if out is None:
+        out = ctx.__dict__["_plan_out"] = N.PlanOut()
     n1 = 0 if kt is None else int(kt.numel())
     _check(ctx, ctx.lib.usfft_plan_round(ctx.h, C.byref(pin), _p(I_prev, torch.int16), n_prev,
                                          _p(kt, torch.int16), n1, C.byref(out)), "usfft_plan_round")

@@ -5,8 +5,8 @@ dist.Exchange; every step of a round (plan, nodes, bins, PDE solves, FFT, keys, 
 union, resolve, row gather) runs in libusfft.so.
 
 Round r = (step, t, i):
-  a1 plan (usfft_plan_round) -> a2/a3 bins (usfft_lattice) -> a4/a5 samples of this rank
-  (usfft_sample_pde, nodes generated in-kernel) -> a6 transpose (Exchange.transpose) ->
+  a1 plan (usfft_plan_round) -> a4/a5 samples of this rank (usfft_sample_pde, nodes a2
+  generated in-kernel) -> a3 bins (usfft_lattice) -> a6 transpose (Exchange.transpose) ->
   a7/a8 FFT + keys (usfft_lattice_fft) -> a9 kappa_max MAX -> a10 select + votes
   (usfft_detect_select) -> votes SUM -> a11 union (usfft_detect_union) -> a12 resolve
   (usfft_resolve, final round only).
@@ -78,9 +78,7 @@ class Detector:
                                   I_prev if t > 1 else None, n_prev, kt)
         L, M = plan.L, plan.M
         Btot = L * M
-        bins = torch.empty((L, nJ), dtype=torch.int32, device=dev)
-        B.usfft_lattice(ctx, plan, 0, 0, None, I_prev if plan.t_z > 1 else None, n_prev, kt, bins)
-        # this rank's samples
+        # this rank's samples (the solves go first: the index map is only needed by the keys)
         b0, b1 = partition(Btot, self.P, self.rank)
         nb = b1 - b0
         u = torch.empty((self.G, nb), dtype=torch.float64, device=dev)
@@ -91,6 +89,8 @@ class Detector:
         elif nb:
             B.usfft_sample_pde(ctx, self.pde, plan, b0, nb, u, nb, None, iters)
         self.n_samples += Btot
+        bins = torch.empty((L, nJ), dtype=torch.int32, device=dev)
+        B.usfft_lattice(ctx, plan, 0, 0, None, I_prev if plan.t_z > 1 else None, n_prev, kt, bins)
         mark("pde")
         slabs, sb = self.ex.transpose(u, self.G, Btot)
         mark("exchange")
