@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <map>
+#include <mutex>
 #include <string>
 #include <utility>
 
@@ -29,6 +30,8 @@ struct usfft_ctx {
     // cached tables
     std::map<int64_t, double2 *> twiddles;                  // M -> e^{-2 pi i m/M}, m < M
     std::map<std::pair<int, int>, double *> sintab;          // (n, d) -> sin(j pi m/(3n))
+    // resident blocks per SM per (kernel, threads, smem): the query costs ~10 us per call
+    std::map<std::pair<const void *, size_t>, int> occupancy;
 };
 
 namespace usfft {
@@ -102,6 +105,43 @@ inline usfft_status ensure(usfft_ctx *c, void **buf, size_t *size, size_t need) 
         return fail(c, USFFT_ENOMEM, "cudaMalloc(%zu) failed", want);
     }
     *size = want;
+    return USFFT_OK;
+}
+
+// Raise the kernel's dynamic shared-memory limit to smem (once per value) and return its
+// resident blocks per SM for (threads, smem), cached in the ctx.
+// The attribute is a per-(device, function) setting shared by every ctx of the process, so its
+// record is process-wide and only ever raised.
+inline std::mutex &smem_attr_mutex() {
+    static std::mutex m;
+    return m;
+}
+inline std::map<std::pair<int, const void *>, size_t> &smem_attr_table() {
+    static std::map<std::pair<int, const void *>, size_t> t;
+    return t;
+}
+
+template <class K>
+inline usfft_status kernel_fit(usfft_ctx *c, K kern, int threads, size_t smem, int *per_sm) {
+    const void *f = reinterpret_cast<const void *>(kern);
+    {
+        std::lock_guard<std::mutex> lock(smem_attr_mutex());
+        size_t &attr = smem_attr_table()[std::make_pair(c->device, f)];
+        if (smem > attr) {
+            USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+            attr = smem;
+        }
+    }
+    if (per_sm) {
+        const auto key = std::make_pair(f, smem * 2048 + (size_t)threads);
+        auto it = c->occupancy.find(key);
+        if (it == c->occupancy.end()) {
+            int ps = 0;
+            USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&ps, kern, threads, smem));
+            it = c->occupancy.emplace(key, ps).first;
+        }
+        *per_sm = it->second;
+    }
     return USFFT_OK;
 }
 

@@ -284,7 +284,7 @@ extern "C" usfft_status usfft_resolve(usfft_ctx *c, const usfft_lattice_desc *la
         if (s) return s;
         ls = static_cast<int32_t *>(c->ws);
     }
-    USFFT_CUDA(c, cudaFuncSetAttribute(k_resolve, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    if (usfft_status s = kernel_fit(c, k_resolve, 0, smem, nullptr)) return s;
     k_resolve<<<(unsigned)G_loc, 256, smem, c->stream>>>(
         reinterpret_cast<const double2 *>(spectra), bins, nJ, lat->M, lat->L, det_g, n_det_g,
         s_tilde, det_idx, n_det, reinterpret_cast<double2 *>(coef), ls);

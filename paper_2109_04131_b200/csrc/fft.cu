@@ -138,9 +138,8 @@ usfft_status launch_rader_t(usfft_ctx *c, const double *u, const SlabParams &S, 
     const int64_t rows = G_loc * L;
     const size_t smem = sizeof(double2) * 2 * (size_t)N * RPC;
     auto kern = k_fft_rader_t<N, WPR, RPC>;
-    USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, WPR * 32 * RPC, smem));
+    if (usfft_status s = kernel_fit(c, kern, WPR * 32 * RPC, smem, &per_sm)) return s;
     int64_t grid = (rows + RPC - 1) / RPC;
     const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
     if (grid > resident) grid = resident;                 // persistent: each group loops over rows
@@ -156,9 +155,8 @@ usfft_status launch_fft400(usfft_ctx *c, const double *u, const SlabParams &S, i
     const int64_t units = paired ? G_loc * ((L + 1) / 2) : rows;   // per-node lattice pairs or rows
     const size_t smem = sizeof(double2) * (size_t)((paired ? 402 : 201) + 20 * 21) * RPC;
     auto kern = paired ? k_fft400p<RPC> : k_fft400<RPC>;
-    USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * RPC, smem));
+    if (usfft_status s = kernel_fit(c, kern, 32 * RPC, smem, &per_sm)) return s;
     int64_t grid = (units + RPC - 1) / RPC;
     const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
     if (grid > resident) grid = resident;                 // persistent: each warp loops over rows
@@ -340,7 +338,7 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         else if (!generic && R.N == 2016) s = launch_rader_t<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
         else if (!generic && R.N == 4000) s = launch_rader_t<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
         else {
-            USFFT_CUDA(c, cudaFuncSetAttribute(k_fft_rader, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem_r));
+            if (usfft_status s2 = kernel_fit(c, k_fft_rader, 0, smem_r, nullptr)) return s2;
             const int threads = M <= 512 ? 128 : 256;
             k_fft_rader<<<(unsigned)rows, threads, smem_r, c->stream>>>(u, S, G_loc, L, A, Fo);
             USFFT_CHECK_LAUNCH(c);
@@ -348,7 +346,7 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         if (s) return s;
     } else {
         USFFT_REQUIRE(c, smem <= c->smem_optin, "M = %lld too large for the direct DFT", (long long)M);
-        USFFT_CUDA(c, cudaFuncSetAttribute(k_dft_direct, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+        if (usfft_status s2 = kernel_fit(c, k_dft_direct, 0, smem, nullptr)) return s2;
         k_dft_direct<<<(unsigned)rows, 256, smem, c->stream>>>(u, S, G_loc, M, L, tw,
                                                                 reinterpret_cast<double2 *>(spectra));
         USFFT_CHECK_LAUNCH(c);
@@ -361,7 +359,7 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         const int staged = st_bytes + tile_bytes <= 112 * 1024 ? 1 : 0;
         const size_t dyn = (staged ? st_bytes : 0) + tile_bytes;
         USFFT_REQUIRE(c, dyn <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
-        USFFT_CUDA(c, cudaFuncSetAttribute(k_kappa, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
+        if (usfft_status s2 = kernel_fit(c, k_kappa, 0, dyn, nullptr)) return s2;
         k_kappa<<<(unsigned)G_loc, 256, dyn, c->stream>>>(
             reinterpret_cast<const double2 *>(spectra), bins, nJ, M, L, kappa_min, km, staged);
         USFFT_CHECK_LAUNCH(c);

@@ -192,9 +192,8 @@ usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
     const size_t dyn = sizeof(double) * ((size_t)Mg3<NC>::doubles() + (MINB * NWARP >= 12 ? 2 * BC * BR * NWARP * 32 : 0) +
                                          (sw <= Mg3<NC>::SMAX ? sw : 0));
     auto kern = k_pcg_mg<NC, BC, BR, LX, NWARP, MINB>;
-    USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int per_sm = 0;
-    USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWARP * 32, dyn));
+    if (usfft_status s = kernel_fit(c, kern, NWARP * 32, dyn, &per_sm)) return s;
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)per_sm * c->sm_count;
     if (grid > nb) grid = nb;
@@ -212,9 +211,8 @@ usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q
     constexpr int NRG = NWARP * (32 / LX), NCOL = LX * BC;
     const size_t dyn = sizeof(double) * (size_t)(2 * n * n + (n + 1) * (n + 1) + 12 * NRG * NCOL);
     auto kern = k_pcg_reg<NC, BC, BR, LX, NWARP, MINB>;
-    USFFT_CUDA(c, cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
     int per_sm = 0;
-    USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, NWARP * 32, dyn));
+    if (usfft_status s = kernel_fit(c, kern, NWARP * 32, dyn, &per_sm)) return s;
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)per_sm * c->sm_count;
     if (grid > nb) grid = nb;
@@ -237,14 +235,13 @@ usfft_status launch_pcg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, co
     size_t dyn = 0;
     if (bytes + 1024 <= c->smem_optin) {
         dyn = bytes;
-        USFFT_CUDA(c, cudaFuncSetAttribute(k_pcg<NPT, THREADS>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)dyn));
         int per_sm = 0;
-        USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg<NPT, THREADS>, threads, dyn));
+        if (usfft_status s = kernel_fit(c, k_pcg<NPT, THREADS>, threads, dyn, &per_sm)) return s;
         if (per_sm < 1) per_sm = 1;
         grid = per_sm * c->sm_count;
     } else {
         int per_sm = 0;
-        USFFT_CUDA(c, cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_pcg<NPT, THREADS>, threads, 0));
+        if (usfft_status s = kernel_fit(c, k_pcg<NPT, THREADS>, threads, 0, &per_sm)) return s;
         if (per_sm < 1) per_sm = 1;
         grid = per_sm * c->sm_count;
         if ((int64_t)grid > nb) grid = (int)nb;
