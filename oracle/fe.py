@@ -33,8 +33,27 @@ import scipy.special
 # ---------------------------------------------------------------------------------------------
 # coefficient field
 # ---------------------------------------------------------------------------------------------
-def theta_map(kind: str, y: np.ndarray) -> np.ndarray:
-    """Theta_j(y_j) of the coefficient families (Z14, Z15)."""
+def tau2(y: np.ndarray, delta: float) -> np.ndarray:
+    """Shifted tent tau_{2,Delta}: T -> [-1/2, 1/2] (three branches)."""
+    y = np.asarray(y, dtype=np.float64)
+    return np.where(y < delta, -0.5 - 2.0 * (y - delta),
+                    np.where(y < 0.5 + delta, -0.5 + 2.0 * (y - delta), 1.5 - 2.0 * (y - delta)))
+
+
+def tau1(yb: np.ndarray) -> np.ndarray:
+    """tau_1(y) = sqrt(2) erf^-1(2 y) on (-1/2, 1/2), written as Phi^-1(y + 1/2) with
+    Phi(y) = (1 + erf(y / sqrt 2)) / 2."""
+    return scipy.special.ndtri(np.asarray(yb, dtype=np.float64) + 0.5)
+
+
+def global_delta(M0: int) -> float:
+    """The one global pole shift of a run (reading Z27): Delta_opt = 1/(4 M0) of the Lemma
+     for M0 = the Step-2 lattice size of the configuration (Z2)."""
+    return 1.0 / (4.0 * M0)
+
+
+def theta_map(kind: str, y: np.ndarray, delta: float | None = None) -> np.ndarray:
+    """Theta_j(y_j) of the coefficient families (Z14, Z15, Z27)."""
     y = np.asarray(y, dtype=np.float64)
     if kind == "sin":
         return np.sin(2.0 * np.pi * y)                               # P:91 (without 1/sqrt6)
@@ -42,13 +61,15 @@ def theta_map(kind: str, y: np.ndarray) -> np.ndarray:
         return 1.0 - np.abs(2.0 * (1.0 - 2.0 * y))                   # eq. tent, alpha=-1, beta=1
     if kind == "probit":
         return np.clip(scipy.special.ndtri(y), -6.0, 6.0)            # Phi^-1 clipped (Z15)
+    if kind == "phi_delta":                                          # phi_Delta = tau1 o tau2 (Z27)
+        return np.clip(tau1(tau2(y, delta)), -6.0, 6.0)              # eq. lognormal_transfo
     raise ValueError(f"unknown theta kind {kind!r}")
 
 
 def coefficient(model: dict, y: np.ndarray, x1: np.ndarray, x2: np.ndarray) -> np.ndarray:
     """a(x, y) at the points (x1, x2) for one parameter vector y (length d)."""
     d = model["d"]
-    th = theta_map(model["theta"], np.asarray(y, dtype=np.float64)[:d])
+    th = theta_map(model["theta"], np.asarray(y, dtype=np.float64)[:d], model.get("delta"))
     s = np.zeros_like(np.asarray(x1, dtype=np.float64))
     for j in range(1, d + 1):
         s = s + model["amp"][j - 1] * th[j - 1] * np.sin(j * np.pi * x1) * np.sin(j * np.pi * x2)

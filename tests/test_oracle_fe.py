@@ -147,3 +147,48 @@ def test_stencil_derivation_matches_element_assembly():
                 if q >= 0:
                     R[p, q] = -w
     assert np.abs(A - R).max() < 1e-13
+
+
+# ------------------------------------------------------------------ lognormal periodization (Z27)
+def test_phi_delta_spec_examples_and_poles():
+    """SPEC S:353-356 / P:500-515: with Delta = 0.1, phi^-1(0) = 0.35 (tau2^-1(0) = Delta + 1/4);
+    tau2 hits the poles -1/2 at Delta and +1/2 at 1/2 + Delta (clipped to -/+6); phi diverges
+    monotonically to -inf as y decreases to Delta."""
+    d = 0.1
+    assert abs(fe.tau2(np.array([0.35]), d)[0]) < 1e-15 and fe.tau1(np.array([0.0]))[0] == 0.0
+    assert fe.tau2(np.array([d]), d)[0] == -0.5 and fe.tau2(np.array([0.5 + d]), d)[0] == 0.5
+    assert fe.theta_map("phi_delta", np.array([d, 0.5 + d]), d).tolist() == [-6.0, 6.0]
+    eps = np.array([1e-2, 1e-4, 1e-6, 1e-9])
+    v = fe.tau1(fe.tau2(d + eps, d))
+    assert np.all(np.diff(v) < 0) and v[-1] < -5.8            # Phi^-1(2e-9) = -5.88
+
+
+def test_phi_delta_symmetry_and_inversion_method():
+    """tau2 is a tent with its maximum at 1/2 + Delta: tau2(1/2 + Delta - t) = tau2(1/2 + Delta + t);
+    the inversion method: uniform samples pushed through phi_Delta are N(0, 1)
+    (Kolmogorov-Smirnov statistic < 0.01 on 10^6 samples)."""
+    d = 1.0 / (4 * 2017)
+    t = np.linspace(0.0, 0.5, 101)
+    a = fe.tau2(np.mod(0.5 + d - t, 1.0), d)
+    b = fe.tau2(np.mod(0.5 + d + t, 1.0), d)
+    assert np.abs(a - b).max() < 1e-12
+    y = np.random.default_rng(0).random(1_000_000)
+    v = np.sort(fe.tau1(fe.tau2(y, d)))
+    import scipy.stats
+    ks = np.max(np.abs(scipy.stats.norm.cdf(v) - (np.arange(1, v.size + 1) / v.size)))
+    assert ks < 0.01
+
+
+def test_global_delta_is_the_lemma_optimum():
+    """Lemma P:847-870: for prime M and a rank-1 lattice with some z_j != 0 mod M, the smaller of the
+    distances of the nodes to Delta and to Delta + 1/2 is maximal at Delta = 1/(4M), where it
+    equals 1/(4M) (brute force over a Delta grid on (0, 1/(2M)))."""
+    from oracle import lattice
+    M, z = 97, [[5, 11, 0]]
+    Y = lattice.nodes(M, z, np.zeros(3), 3)
+    def score(dl):
+        return min(np.abs(Y - dl).min(), np.abs(Y - (dl + 0.5)).min())
+    grid = np.linspace(1e-6, 1.0 / (2 * M) - 1e-6, 2001)
+    best = grid[np.argmax([score(g) for g in grid])]
+    assert abs(best - fe.global_delta(M)) < 1.0 / (2 * M) / 1000
+    assert abs(score(fe.global_delta(M)) - 1.0 / (4 * M)) < 1e-15
