@@ -73,6 +73,8 @@ typedef struct {
  *   d          number of coefficient terms (<= 64)
  *   theta      0: sin(2 pi y) (periodic)  1: tent 1-|2(1-2y)| (eq. tent)
  *              2: clip(Phi^-1(y), -6, 6) (Z15)
+ *              3: clip(tau1(tau2_Delta(y)), -6, 6), the lognormal periodization phi_Delta
+ *                 (eq. lognormal_transfo, tau1 P:486, tau2 P:500-506; Z27)
  *   form       0: a = 1 + sum_j amp_j theta_j sin(j pi x1) sin(j pi x2)   1: a = exp(sum ...)
  *   f_kind     0: f(x) = x2 (all BASELINE configs)
  *   amp        host fp64 [d]
@@ -82,6 +84,8 @@ typedef struct {
  *              (damped-Jacobi smoothing, bilinear P, R = P^T, rediscretised coarse meshes;
  *              implemented for n = 16, 32 -> USFFT_EUNIMPL otherwise).  Any solver is admissible
  *              for the black box; both are CG with an SPD preconditioner (Z13).
+ *   delta      the pole shift Delta of theta = 3, in (0, 1/2): one global value per run
+ *              (Z27: 1/(4 M0), M0 the Step-2 lattice size, Lemma P:847-870); ignored otherwise
  */
 typedef struct {
     int32_t n;
@@ -94,6 +98,7 @@ typedef struct {
     double tol;
     int32_t precond;
     int32_t pad_;
+    double delta;
 } usfft_pde_desc;
 
 /* Round plan input/output (usfft_plan_round). */

@@ -25,7 +25,7 @@ class LatticeDesc(C.Structure):
 class PdeDesc(C.Structure):
     _fields_ = [("n", i32), ("d", i32), ("theta", i32), ("form", i32), ("f_kind", i32),
                 ("maxit", i32), ("amp", C.POINTER(f64)), ("tol", f64), ("precond", i32),
-                ("pad_", i32)]
+                ("pad_", i32), ("delta", f64)]
 
 
 class PlanIn(C.Structure):

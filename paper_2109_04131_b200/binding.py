@@ -139,16 +139,18 @@ def effective_precond(cfg: dict, precond: str | None = None) -> str:
     return precond or cfg.get("precond") or ("mg" if cfg["n"] in MG_MESHES else "jacobi")
 
 
-def pde_desc(cfg: dict, maxit: int = 20000, tol: float = 1e-12, precond: str | None = None):
+def pde_desc(cfg: dict, maxit: int = 20000, tol: float = 1e-12, precond: str | None = None,
+             delta: float = 0.0):
     """precond: "jacobi" or "mg" (multigrid-preconditioned CG, n = 16, 32); default see
-    effective_precond."""
+    effective_precond.  delta: the global pole shift of theta = "phi_delta" (Z27)."""
     amp = np.ascontiguousarray(cfg["amp"][: cfg["d"]], dtype=np.float64)
-    theta = {"sin": 0, "tent": 1, "probit": 2}[cfg["theta"]]
+    theta = {"sin": 0, "tent": 1, "probit": 2, "phi_delta": 3}[cfg["theta"]]
     form = {"affine": 0, "exp": 1}[cfg["form"]]
     f_kind = {"x2": 0}[cfg.get("f", "x2")]
     pc = effective_precond(cfg, precond)
     dsc = N.PdeDesc(cfg["n"], cfg["d"], theta, form, f_kind, maxit,
-                    amp.ctypes.data_as(C.POINTER(C.c_double)), tol, {"jacobi": 0, "mg": 1}[pc], 0)
+                    amp.ctypes.data_as(C.POINTER(C.c_double)), tol, {"jacobi": 0, "mg": 1}[pc], 0,
+                    float(delta))
     return dsc, amp
 
 

@@ -143,7 +143,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         // ---- K3: coefficients ----------------------------------------------------------------
         if (tid < Q.d) {
             const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
-            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
+            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
         USFFT_MG_SMARK(24);

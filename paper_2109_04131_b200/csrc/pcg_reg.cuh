@@ -64,7 +64,7 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         // ---- K3: coefficient at the 2n^2 centroids, then the diagonal ----------------------
         if (tid < Q.d) {
             const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
-            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
+            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
         for (int e = tid; e < 2 * n * n; e += NWARP * 32) {

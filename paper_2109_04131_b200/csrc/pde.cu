@@ -23,12 +23,18 @@ namespace usfft {
 struct PdeParams {
     int32_t n, d, theta, form, f_kind, maxit, precond;
     double tol2;              // tol^2
+    double delta;             // global pole shift of phi_Delta (Z27)
     double amp[kMaxD];
 };
 
-__device__ __forceinline__ double theta_of(int kind, double y) {
+__device__ __forceinline__ double theta_of(int kind, double y, double delta) {
     if (kind == 0) return sinpi(2.0 * y);                         // sin(2 pi y)
     if (kind == 1) return 1.0 - fabs(2.0 * (1.0 - 2.0 * y));      // tent, eq. tent
+    if (kind == 3) {                                               // phi_Delta = tau1 o tau2,Delta (Z27)
+        const double t2 = y < delta ? -0.5 - 2.0 * (y - delta)     // tau2,Delta
+                        : y < 0.5 + delta ? -0.5 + 2.0 * (y - delta) : 1.5 - 2.0 * (y - delta);
+        y = t2 + 0.5;                                              // tau1(t) = Phi^-1(t + 1/2)
+    }
     double v = normcdfinv(y);                                      // Phi^-1 (Z15)
     return fmin(fmax(v, -6.0), 6.0);                               // clip, NaN-free: -inf -> -6
 }
@@ -77,7 +83,7 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
         // ---- K3: theta_j(y_b) and the edge weights ----------------------------------------
         if (tid < Q.d) {
             const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
-            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y);
+            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
         for (int e = tid; e < np * np; e += T) {
@@ -269,7 +275,8 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     if (s) return s;
     USFFT_REQUIRE(c, pde->n >= 2 && pde->n <= 128, "n = %d out of [2, 128]", pde->n);
     USFFT_REQUIRE(c, pde->d >= 1 && pde->d <= P.d, "pde d = %d must be in [1, lattice d]", pde->d);
-    USFFT_REQUIRE(c, pde->theta >= 0 && pde->theta <= 2, "theta kind %d", pde->theta);
+    USFFT_REQUIRE(c, pde->theta >= 0 && pde->theta <= 3, "theta kind %d", pde->theta);
+    USFFT_REQUIRE(c, pde->theta != 3 || (pde->delta > 0.0 && pde->delta < 0.5), "delta out of (0, 1/2)");
     USFFT_REQUIRE(c, pde->form == 0 || pde->form == 1, "form %d", pde->form);
     USFFT_REQUIRE(c, pde->f_kind == 0, "f_kind %d not implemented", pde->f_kind);
     USFFT_REQUIRE(c, pde->amp != nullptr, "amp is NULL");
@@ -288,6 +295,7 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     Q.f_kind = pde->f_kind;
     Q.maxit = pde->maxit;
     Q.precond = pde->precond;
+    Q.delta = pde->delta;
     Q.tol2 = pde->tol * pde->tol;
     for (int j = 0; j < pde->d; ++j) Q.amp[j] = pde->amp[j];
 

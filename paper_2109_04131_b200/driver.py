@@ -48,7 +48,14 @@ class Detector:
         self.blackbox = blackbox
         self.dev = torch.device("cuda", device)
         self.ctx = B.Context(device)
-        self.pde = B.pde_desc(cfg, maxit=maxit, tol=cfg.get("cg_tol", 1e-12)) if blackbox is None else None
+        # phi_Delta map: one global pole shift Delta = 1/(4 M0), M0 the Step-2 lattice size (Z27)
+        self.delta = 0.0
+        if cfg.get("theta") == "phi_delta":
+            M0 = B.usfft_plan_round(self.ctx, cfg["seed"], 2, 2, 1, cfg["d"], cfg["N"], cfg["s_local"],
+                                    "A", 1).M
+            self.delta = 1.0 / (4.0 * M0)
+        self.pde = B.pde_desc(cfg, maxit=maxit, tol=cfg.get("cg_tol", 1e-12), delta=self.delta) \
+            if blackbox is None else None
         self.ex = Exchange(group)
         self.P, self.rank = self.ex.P, self.ex.rank
         self.G = cfg["G"] if blackbox is not None else (cfg["n"] - 1) ** 2

@@ -114,3 +114,26 @@ def test_eval_err_closed_form(B, ctx):
     A = np.abs(U)
     want = np.stack([A.mean(1), np.sqrt((A * A).mean(1)), A.max(1)], 1)
     assert np.abs(err.cpu().numpy() - want).max() <= 1e-13 * want.max()
+
+
+@pytest.mark.parametrize("cfgid", [1, 2])
+def test_phi_delta_samples(B, ctx, cfgid):
+    """NEXT #2 (Z27): the lognormal periodization phi_Delta as the coefficient map; the product's
+    global Delta (from its own plan) equals the oracle's, and the PDE samples match the oracle
+    (FE by banded Cholesky) at lattice nodes that include i = 0 and the node nearest the poles."""
+    from oracle import fe as ofe2
+    from oracle import lattice as olat
+    from oracle import plan as oplan
+    from paper_2109_04131_b200.driver import Detector
+    cfg = config(cfgid, theta="phi_delta", form="exp")
+    det = Detector(cfg)
+    M0 = oplan.lattice_size(cfg["s_local"], cfg["N"])
+    assert det.delta == ofe2.global_delta(M0)
+    ocfg = dict(cfg, delta=ofe2.global_delta(M0))
+    p = B.usfft_plan_round(ctx, cfg["seed"], 2, 3, 1, cfg["d"], cfg["N"], cfg["s"], "A", 300)
+    nb, G = 20, (cfg["n"] - 1) ** 2
+    u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
+    assert B.usfft_sample_pde(ctx, det.pde, p, 0, nb, u, nb, check_conv=True) == 0
+    Y = olat.nodes(p.M, p.z, p.shift, 3)[:, :nb]
+    ref = ofe.sample_pde(ocfg, Y)
+    assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()

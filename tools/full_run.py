@@ -22,6 +22,8 @@ def main():
     ap = argparse.ArgumentParser()
     ap.add_argument("--config", type=int, default=2)
     ap.add_argument("--n-test", type=int, default=10000)
+    ap.add_argument("--theta", default="", help="coefficient map override (sin, tent, probit, phi_delta)")
+    ap.add_argument("--form", default="", help="coefficient form override (affine, exp)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -29,6 +31,10 @@ def main():
     from usfft_inputs import config, uniform_points
 
     cfg = config(args.config)
+    if args.theta:
+        cfg["theta"] = args.theta
+    if args.form:
+        cfg["form"] = args.form
     det = Detector(cfg)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t0 = time.perf_counter()
@@ -48,7 +54,8 @@ def main():
     wall = time.perf_counter() - t0
     e = err.cpu().numpy()
     out = {
-        "workload": f"config{args.config}:{cfg['name']}", "d": cfg["d"], "n": cfg["n"], "N": cfg["N"],
+        "workload": f"config{args.config}:{cfg['name']}", "theta": cfg["theta"], "form": cfg["form"],
+        "delta": det.delta, "d": cfg["d"], "n": cfg["n"], "N": cfg["N"],
         "s": cfg["s"], "rounds": len(log), "samples_detection": n_detect, "samples_step3": n_step3,
         "step3_share": n_step3 / (n_detect + n_step3), "nI": int(I.shape[0]), "q": I.shape[0] / cfg["s"],
         "cover_lattices": int(cov.z.shape[0]), "cover_M": int(cov.M),
