@@ -269,6 +269,15 @@ usfft_status usfft_cover_gather(usfft_ctx *ctx, int64_t M, int64_t G, const doub
                                 const int32_t *idx, const int32_t *bin, int64_t n, double *coef,
                                 int64_t nI);
 
+/* Direct lattice DFT at the bins in use (Step 3 on cover lattices too large for the FFT
+ * kernels, Z26): coef[g][idx[a]] = (1/M) sum_{i<M} u[g][i] e^{-2 pi i (i bins[a] mod M)/M} with
+ * the exact integer phase index (the oracle's direct DFT, P:296 / S:158).  u is the exchanged
+ * sample slab buffer of one lattice as in usfft_lattice_fft (nslab, slab_b0 spanning [0, M]);
+ * bins, idx dev int32 [n]; coef dev fp64x2 [G_loc][nI]. */
+usfft_status usfft_lattice_dft_bins(usfft_ctx *ctx, int64_t M, int64_t G_loc, const double *u,
+                                    int32_t nslab, const int64_t *slab_b0, const int32_t *bins,
+                                    const int32_t *idx, int64_t n, double *coef, int64_t nI);
+
 /* ---- accuracy metric (usfft_eval_err) ------------------------------------------------------
  * per node g over the n test points y_q (Y dev fp64 [d][n]),
  *   err[g][0] = (1/n) sum_q |Uref[g][q] - u(g, y_q)|,  err[g][1] = sqrt((1/n) sum_q |.|^2),

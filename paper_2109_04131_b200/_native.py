@@ -65,6 +65,7 @@ _SIGS = {
     "usfft_cover_plan": (i32, [vp, i64, i32, i32, vp, i64, C.POINTER(CoverDesc), vp, vp]),
     "usfft_cover_gather": (i32, [vp, i64, i64, vp, vp, vp, i64, vp, i64]),
     "usfft_eval_err": (i32, [vp, i32, vp, i64, vp, i64, vp, i64, vp, vp]),
+    "usfft_lattice_dft_bins": (i32, [vp, i64, i64, vp, i32, C.POINTER(i64), vp, vp, i64, vp, i64]),
 }
 
 EXPORTED = tuple(_SIGS)

@@ -269,3 +269,13 @@ def usfft_eval_err(ctx: Context, I, C_, Y, Uref, err):
                                 _p(Y, torch.float64), n, _p(Uref, torch.float64), _p(err, torch.float64))
     _check(ctx, st, "usfft_eval_err")
 
+
+def usfft_lattice_dft_bins(ctx: Context, M: int, G_loc: int, u, slab_b0, bins, idx, coef):
+    """coef [G_loc][nI][2]: direct lattice DFT of one lattice's samples at the bins in use."""
+    sb = np.ascontiguousarray(slab_b0, dtype=np.int64)
+    st = ctx.lib.usfft_lattice_dft_bins(ctx.h, M, G_loc, _p(u, torch.float64), len(sb) - 1,
+                                        sb.ctypes.data_as(C.POINTER(C.c_int64)), _p(bins, torch.int32),
+                                        _p(idx, torch.int32), int(idx.numel()), _p(coef, torch.float64),
+                                        coef.shape[1])
+    _check(ctx, st, "usfft_lattice_dft_bins")
+

@@ -67,6 +67,65 @@ __global__ void k_dft_direct(const double *__restrict__ u, const SlabParams S, i
     }
 }
 
+// Direct lattice DFT at the bins in use (Step 3 with cover lattices beyond the FFT kernels):
+// coef[g][idx[a]] = (1/M) sum_i u[g][i] e^{-2 pi i (i b_a mod M)/M} -- a [G x M] . [M x n] complex
+// product with the right operand generated from the exact phase index; 64 x 64 output tiles,
+// 16-sample chunks staged in shared memory, 4 x 4 register tiles per thread.
+constexpr int DB_TG = 64, DB_TA = 64, DB_TI = 16;
+
+__global__ void __launch_bounds__(256)
+k_dft_bins(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int64_t M,
+           const double2 *__restrict__ tw, const int32_t *__restrict__ bins,
+           const int32_t *__restrict__ idx, int64_t n, double2 *__restrict__ coef, int64_t nI) {
+    __shared__ double us[DB_TI][DB_TG + 1];
+    __shared__ double2 ws[DB_TI][DB_TA + 1];
+    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
+    const int64_t g0 = (int64_t)blockIdx.y * DB_TG, a0 = (int64_t)blockIdx.x * DB_TA;
+    double are[4][4] = {}, aim[4][4] = {};
+    for (int64_t i0 = 0; i0 < M; i0 += DB_TI) {
+        for (int e = threadIdx.x; e < DB_TI * DB_TG; e += blockDim.x) {
+            const int ii = e % DB_TI, gg = e / DB_TI;
+            us[ii][gg] = (i0 + ii < M && g0 + gg < G_loc) ? sample_at(u, S, G_loc, g0 + gg, i0 + ii) : 0.0;
+        }
+        for (int e = threadIdx.x; e < DB_TI * DB_TA; e += blockDim.x) {
+            const int ii = e / DB_TA, aa = e % DB_TA;
+            double2 w = make_double2(0.0, 0.0);
+            if (i0 + ii < M && a0 + aa < n) w = tw[((i0 + ii) * (int64_t)bins[a0 + aa]) % M];
+            ws[ii][aa] = w;
+        }
+        __syncthreads();
+#pragma unroll 4
+        for (int ii = 0; ii < DB_TI; ++ii) {
+            double uv[4];
+            double2 wv[4];
+#pragma unroll
+            for (int r = 0; r < 4; ++r) {
+                uv[r] = us[ii][ty * 4 + r];
+                wv[r] = ws[ii][tx * 4 + r];
+            }
+#pragma unroll
+            for (int r = 0; r < 4; ++r)
+#pragma unroll
+                for (int q = 0; q < 4; ++q) {
+                    are[r][q] = fma(uv[r], wv[q].x, are[r][q]);
+                    aim[r][q] = fma(uv[r], wv[q].y, aim[r][q]);
+                }
+        }
+        __syncthreads();
+    }
+    const double Md = (double)M;
+#pragma unroll
+    for (int r = 0; r < 4; ++r) {
+        const int64_t g = g0 + ty * 4 + r;
+        if (g >= G_loc) continue;
+#pragma unroll
+        for (int q = 0; q < 4; ++q) {
+            const int64_t a = a0 + tx * 4 + q;
+            if (a < n) coef[g * nI + idx[a]] = make_double2(are[r][q] / Md, aim[r][q] / Md);
+        }
+    }
+}
+
 // one CTA per owned node g; the node's L spectra rows are staged in shared memory when they fit.
 // Candidates go in tiles of 256: the tile's L bins rows are first staged in shared memory with
 // independent coalesced loads (the L2 latency is paid once per tile, not once per lattice),
@@ -366,3 +425,26 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
     }
     return USFFT_OK;
 }
+
+extern "C" usfft_status usfft_lattice_dft_bins(usfft_ctx *c, int64_t M, int64_t G_loc, const double *u,
+                                               int32_t nslab, const int64_t *slab_b0,
+                                               const int32_t *bins, const int32_t *idx, int64_t n,
+                                               double *coef, int64_t nI) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, M >= 2 && M <= (int64_t(1) << 26) && G_loc >= 0 && n >= 0 && nI >= n, "bad sizes");
+    USFFT_REQUIRE(c, nslab >= 1 && nslab <= kMaxSlab && slab_b0 != nullptr, "nslab out of [1, %d]", kMaxSlab);
+    USFFT_REQUIRE(c, slab_b0[0] == 0 && slab_b0[nslab] == M, "slab_b0 must span [0, M]");
+    if (G_loc == 0 || n == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, u && bins && idx && coef, "NULL argument");
+    USFFT_REQUIRE(c, (n + DB_TA - 1) / DB_TA <= 0x7fffffff && (G_loc + DB_TG - 1) / DB_TG <= 65535, "grid too large");
+    SlabParams S;
+    S.nslab = nslab;
+    for (int p = 0; p <= nslab; ++p) S.b0[p] = slab_b0[p];
+    double2 *tw = nullptr;
+    if (usfft_status s = get_twiddles(c, M, &tw)) return s;
+    dim3 grid((unsigned)((n + DB_TA - 1) / DB_TA), (unsigned)((G_loc + DB_TG - 1) / DB_TG));
+    k_dft_bins<<<grid, 256, 0, c->stream>>>(u, S, G_loc, M, tw, bins, idx, n, reinterpret_cast<double2 *>(coef), nI);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+

@@ -198,6 +198,8 @@ class Detector:
         return self.step2(I1d, log)
 
     # ------------------------------------------------------------------------------------------
+    FFT_MAX_M = 4001           # largest lattice the Rader FFT kernels hold on chip (M-1 = 4000)
+
     def step3(self, I_rows: torch.Tensor):
         """Step 3: multiple-R1L cover of I (reading Z26, usfft_cover_plan), the samples
         on every cover lattice (this rank's share, exchanged like a round) and the coefficient of
@@ -222,10 +224,13 @@ class Detector:
                 B.usfft_sample_pde(ctx, self.pde, plan, b0, nb, u, nb)
             self.n_samples += M
             slabs, sb = self.ex.transpose(u, self.G, M)
-            spectra = torch.empty((self.G_loc, 1, Mh, 2), dtype=torch.float64, device=dev)
-            B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, None, 0, spectra, None, None)
             sel = torch.nonzero(assign == q).reshape(-1).to(torch.int32).contiguous()
-            B.usfft_cover_gather(ctx, M, self.G_loc, spectra, sel, bins[sel].contiguous(), coef)
+            if M <= self.FFT_MAX_M:                        # lattice FFT, then read the bins
+                spectra = torch.empty((self.G_loc, 1, Mh, 2), dtype=torch.float64, device=dev)
+                B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, None, 0, spectra, None, None)
+                B.usfft_cover_gather(ctx, M, self.G_loc, spectra, sel, bins[sel].contiguous(), coef)
+            else:                                          # direct DFT at the bins in use
+                B.usfft_lattice_dft_bins(ctx, M, self.G_loc, slabs, sb, bins[sel].contiguous(), sel, coef)
         return cov, coef
 
     def errors(self, I_rows: torch.Tensor, coef: torch.Tensor, Y: torch.Tensor):

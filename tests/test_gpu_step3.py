@@ -137,3 +137,41 @@ def test_phi_delta_samples(B, ctx, cfgid):
     Y = olat.nodes(p.M, p.z, p.shift, 3)[:, :nb]
     ref = ofe.sample_pde(ocfg, Y)
     assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+@pytest.mark.parametrize("G,M,n", [(70, 401, 130), (5, 17497, 300), (33, 97, 1)])
+def test_lattice_dft_bins_parity(B, ctx, G, M, n):
+    """Direct lattice DFT at the bins in use vs the oracle's direct DFT (exact phase index),
+    and bit-identical on an emulated 3-rank slab layout."""
+    from oracle import dft as odft
+    from paper_2109_04131_b200.dist import bounds
+    rng = np.random.default_rng(M + n)
+    U = rng.standard_normal((G, M))
+    b = rng.integers(0, M, size=n).astype(np.int32)
+    idx = rng.permutation(n + 3)[:n].astype(np.int32)
+    coef = torch.zeros((G, n + 3, 2), dtype=torch.float64, device="cuda")
+    Ud = torch.as_tensor(U, device="cuda")
+    B.usfft_lattice_dft_bins(ctx, M, G, Ud, [0, M], torch.as_tensor(b, device="cuda"),
+                             torch.as_tensor(idx, device="cuda"), coef)
+    ref = odft.lattice_dft(U, M, b)
+    got = coef.cpu().numpy()[:, idx]
+    assert np.abs(got[..., 0] + 1j * got[..., 1] - ref).max() <= 1e-12 * np.abs(ref).max()
+    gb, sb = bounds(G, 3), bounds(M, 3)
+    r = 1
+    slabs = torch.cat([Ud[gb[r]:gb[r + 1], sb[q]:sb[q + 1]].reshape(-1) for q in range(3)]).contiguous()
+    c2 = torch.zeros((gb[r + 1] - gb[r], n + 3, 2), dtype=torch.float64, device="cuda")
+    B.usfft_lattice_dft_bins(ctx, M, gb[r + 1] - gb[r], slabs, sb, torch.as_tensor(b, device="cuda"),
+                             torch.as_tensor(idx, device="cuda"), c2)
+    assert torch.equal(c2, coef[gb[r]:gb[r + 1]])
+
+
+def test_step3_direct_dft_path_exact(B):
+    """Step 3 with every cover lattice read by the direct DFT (the path of large covers)."""
+    from paper_2109_04131_b200.driver import Detector
+    d, N, G = 5, 12, 3
+    tp = trig_poly(32, d, N, G, 61, real=True, max_active=3)
+    det = Detector(dict(d=d, N=N, s=20, s_local=20, r=1, seed=32, G=G), blackbox=_tp_blackbox(tp))
+    det.FFT_MAX_M = 0
+    _, coef = det.step3(torch.as_tensor(tp.freqs, dtype=torch.int16, device="cuda"))
+    c = coef.cpu().numpy()
+    assert np.abs(c[..., 0] + 1j * c[..., 1] - tp.coefs).max() <= 1e-12
