@@ -6,6 +6,8 @@
 // sparse integer frequencies: each 64x64 output tile loops over k in chunks of 16, stages the
 // C chunk and the phase chunk (k.y reduced mod 1, then sincospi) in shared memory, and every
 // thread accumulates a 4x4 register tile in fp64.
+#include <cstdlib>
+
 #include "common.cuh"
 
 namespace usfft {
@@ -169,6 +171,74 @@ __global__ void k_eval_err_reduce(int64_t G, int64_t ntile, int64_t n, const dou
     }
 }
 
+// usfft_eval on the fp64 tensor pipe (DMMA, mma.sync m8n8k4 f64): the same product written as
+// U = [Cre | -Cim] . [cos ; sin] with K = 2 x 16 per chunk.  8 warps per 64 x 64 tile; warp
+// (wg, wq) owns rows 32 wg .. +32 and columns 16 wq .. +16 as 4 x 2 tiles of 8 x 8.
+// Fragments (PTX m8n8k4 .f64): A a0 = A[lane/4][lane%4], B b0 = B[lane%4][lane/4],
+// C/D {d0, d1} = C[lane/4][2 (lane%4) + {0, 1}].
+__device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
+}
+
+__global__ void __launch_bounds__(256)
+k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
+           int64_t G, const double *__restrict__ Y, int64_t n, double *__restrict__ U) {
+    constexpr int TK = EV_TK, K2 = 2 * TK;
+    __shared__ double As[EV_TG][K2 + 1];                  // [g][k]: Cre (k < TK), -Cim (k >= TK)
+    __shared__ double Bs[K2][EV_TQ + 1];                  // [k][q]: cos (k < TK), sin (k >= TK)
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wg = warp >> 2, wq = warp & 3;
+    const int64_t g0 = (int64_t)blockIdx.y * EV_TG, q0 = (int64_t)blockIdx.x * EV_TQ;
+    double acc[4][2][2] = {};
+    for (int64_t k0 = 0; k0 < nI; k0 += TK) {
+        for (int e = threadIdx.x; e < TK * EV_TG; e += blockDim.x) {
+            const int kk = e / EV_TG, gg = e % EV_TG;
+            double2 v = make_double2(0.0, 0.0);
+            if (k0 + kk < nI && g0 + gg < G) v = C[(g0 + gg) * nI + k0 + kk];
+            As[gg][kk] = v.x;
+            As[gg][TK + kk] = -v.y;
+        }
+        for (int e = threadIdx.x; e < TK * EV_TQ; e += blockDim.x) {
+            const int kk = e / EV_TQ, qq = e % EV_TQ;
+            double c = 0.0, sv = 0.0;
+            if (k0 + kk < nI && q0 + qq < n) {
+                double ph = 0.0;
+                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
+                sincospi(2.0 * (ph - rint(ph)), &sv, &c);
+            }
+            Bs[kk][qq] = c;
+            Bs[TK + kk][qq] = sv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < K2; k += 4) {
+            double a[4], b[2];
+#pragma unroll
+            for (int t = 0; t < 4; ++t) a[t] = As[32 * wg + 8 * t + (lane >> 2)][k + (lane & 3)];
+#pragma unroll
+            for (int u2 = 0; u2 < 2; ++u2) b[u2] = Bs[k + (lane & 3)][16 * wq + 8 * u2 + (lane >> 2)];
+#pragma unroll
+            for (int t = 0; t < 4; ++t)
+#pragma unroll
+                for (int u2 = 0; u2 < 2; ++u2) dmma_8x8x4(acc[t][u2][0], acc[t][u2][1], a[t], b[u2]);
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < 4; ++t) {
+        const int64_t g = g0 + 32 * wg + 8 * t + (lane >> 2);
+        if (g >= G) continue;
+#pragma unroll
+        for (int u2 = 0; u2 < 2; ++u2)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t q = q0 + 16 * wq + 8 * u2 + 2 * (lane & 3) + h;
+                if (q < n) U[g * n + q] = acc[t][u2][h];
+            }
+    }
+}
+
 }  // namespace usfft
 
 using namespace usfft;
@@ -204,7 +274,11 @@ extern "C" usfft_status usfft_eval(usfft_ctx *c, int32_t d, const int16_t *I, in
     USFFT_REQUIRE(c, nI == 0 || (I && C), "I / C NULL");
     USFFT_REQUIRE(c, (n + EV_TQ - 1) / EV_TQ <= 0x7fffffff && (G + EV_TG - 1) / EV_TG <= 65535, "grid too large");
     dim3 grid((unsigned)((n + EV_TQ - 1) / EV_TQ), (unsigned)((G + EV_TG - 1) / EV_TG));
-    k_eval<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
+    const char *force = getenv("USFFT_EVAL");                // =fma: CUDA-core variant
+    if (force && force[0] == 'f')
+        k_eval<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
+    else
+        k_eval_mma<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }

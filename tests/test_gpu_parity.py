@@ -478,3 +478,22 @@ def test_emulated_multirank_round_bitexact(B, ctx):
     a, b = one_round(1), one_round(3)
     for x, y in zip(a, b):
         assert torch.equal(x, y)
+
+
+def test_eval_tensor_and_fma_variants(B, ctx, monkeypatch):
+    """usfft_eval on the fp64 tensor pipe (DMMA, default) and on the CUDA cores (USFFT_EVAL=fma)
+    both match the oracle's direct double sum; odd sizes exercise every tile edge."""
+    rng = np.random.default_rng(8)
+    d, G, nI, n = 7, 37, 45, 301
+    I = rng.integers(-9, 10, size=(nI, d)) * (rng.random((nI, d)) < 0.4)
+    Cc = rng.standard_normal((G, nI)) + 1j * rng.standard_normal((G, nI))
+    Y = rng.random((d, n))
+    ref = oeval.evaluate(I, Cc, Y).real
+    Cd = dev(np.stack([Cc.real, Cc.imag], -1), torch.float64)
+    for mode in ("mma", "fma"):
+        if mode == "fma":
+            monkeypatch.setenv("USFFT_EVAL", "fma")
+        U = torch.empty((G, n), dtype=torch.float64, device="cuda")
+        B.usfft_eval(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), U)
+        assert np.abs(U.cpu().numpy() - ref).max() <= 1e-11 * np.abs(Cc).sum(1).max()
+    monkeypatch.delenv("USFFT_EVAL")
