@@ -172,8 +172,9 @@ __global__ void k_eval_err_reduce(int64_t G, int64_t ntile, int64_t n, const dou
 }
 
 // usfft_eval on the fp64 tensor pipe (DMMA, mma.sync m8n8k4 f64): the same product written as
-// U = [Cre | -Cim] . [cos ; sin] with K = 2 x 16 per chunk.  8 warps per 64 x 64 tile; warp
-// (wg, wq) owns rows 32 wg .. +32 and columns 16 wq .. +16 as 4 x 2 tiles of 8 x 8.
+// U = [Cre | -Cim] . [cos ; sin] with K = 2 x 12 per chunk.  8 warps per 128 x 64 tile (the
+// phases of a chunk, d FMAs and a sincospi each, serve 128 nodes); warp (wg, wq) owns rows
+// 64 wg .. +64 and columns 16 wq .. +16 as 8 x 2 tiles of 8 x 8.
 // Fragments (PTX m8n8k4 .f64): A a0 = A[lane/4][lane%4], B b0 = B[lane%4][lane/4],
 // C/D {d0, d1} = C[lane/4][2 (lane%4) + {0, 1}].
 __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, double b) {
@@ -184,16 +185,16 @@ __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, dou
 __global__ void __launch_bounds__(256)
 k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
            int64_t G, const double *__restrict__ Y, int64_t n, double *__restrict__ U) {
-    constexpr int TK = EV_TK, K2 = 2 * TK;
-    __shared__ double As[EV_TG][K2 + 1];                  // [g][k]: Cre (k < TK), -Cim (k >= TK)
+    constexpr int TK = 12, K2 = 2 * TK, TG = 128, WT = TG / 16;      // WT row tiles per warp
+    __shared__ double As[TG][K2 + 1];                     // [g][k]: Cre (k < TK), -Cim (k >= TK)
     __shared__ double Bs[K2][EV_TQ + 1];                  // [k][q]: cos (k < TK), sin (k >= TK)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wg = warp >> 2, wq = warp & 3;
-    const int64_t g0 = (int64_t)blockIdx.y * EV_TG, q0 = (int64_t)blockIdx.x * EV_TQ;
-    double acc[4][2][2] = {};
+    const int64_t g0 = (int64_t)blockIdx.y * TG, q0 = (int64_t)blockIdx.x * EV_TQ;
+    double acc[WT][2][2] = {};
     for (int64_t k0 = 0; k0 < nI; k0 += TK) {
-        for (int e = threadIdx.x; e < TK * EV_TG; e += blockDim.x) {
-            const int kk = e / EV_TG, gg = e % EV_TG;
+        for (int e = threadIdx.x; e < TK * TG; e += blockDim.x) {
+            const int kk = e / TG, gg = e % TG;
             double2 v = make_double2(0.0, 0.0);
             if (k0 + kk < nI && g0 + gg < G) v = C[(g0 + gg) * nI + k0 + kk];
             As[gg][kk] = v.x;
@@ -213,21 +214,21 @@ k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *
         __syncthreads();
 #pragma unroll
         for (int k = 0; k < K2; k += 4) {
-            double a[4], b[2];
+            double a[WT], b[2];
 #pragma unroll
-            for (int t = 0; t < 4; ++t) a[t] = As[32 * wg + 8 * t + (lane >> 2)][k + (lane & 3)];
+            for (int t = 0; t < WT; ++t) a[t] = As[8 * WT * wg + 8 * t + (lane >> 2)][k + (lane & 3)];
 #pragma unroll
             for (int u2 = 0; u2 < 2; ++u2) b[u2] = Bs[k + (lane & 3)][16 * wq + 8 * u2 + (lane >> 2)];
 #pragma unroll
-            for (int t = 0; t < 4; ++t)
+            for (int t = 0; t < WT; ++t)
 #pragma unroll
                 for (int u2 = 0; u2 < 2; ++u2) dmma_8x8x4(acc[t][u2][0], acc[t][u2][1], a[t], b[u2]);
         }
         __syncthreads();
     }
 #pragma unroll
-    for (int t = 0; t < 4; ++t) {
-        const int64_t g = g0 + 32 * wg + 8 * t + (lane >> 2);
+    for (int t = 0; t < WT; ++t) {
+        const int64_t g = g0 + 8 * WT * wg + 8 * t + (lane >> 2);
         if (g >= G) continue;
 #pragma unroll
         for (int u2 = 0; u2 < 2; ++u2)
@@ -277,8 +278,10 @@ extern "C" usfft_status usfft_eval(usfft_ctx *c, int32_t d, const int16_t *I, in
     const char *force = getenv("USFFT_EVAL");                // =fma: CUDA-core variant
     if (force && force[0] == 'f')
         k_eval<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
-    else
-        k_eval_mma<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
+    else {
+        dim3 gm((unsigned)((n + EV_TQ - 1) / EV_TQ), (unsigned)((G + 127) / 128));
+        k_eval_mma<<<gm, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
+    }
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
