@@ -6,6 +6,8 @@
 // > T and the first (by candidate index) keys == T up to s~ (Z6), and of those the ones with
 // kappa >= theta^2 and kappa > 0 (Z5).  All decisions are integer/ordered comparisons of the same
 // doubles, hence exact and independent of thread scheduling; votes are integer atomics.
+#include <algorithm>
+
 #include "common.cuh"
 
 namespace usfft {
@@ -165,31 +167,46 @@ __device__ __forceinline__ int member_sorted(const int32_t *__restrict__ a, int 
     return (lo < n && a[lo] == k) ? 1 : 0;
 }
 
-// one CTA per owned node g: l* = first lattice where k is alias-free w.r.t. D_g (Z1, a12)
+// one CTA per owned node g: l* = first lattice where k is alias-free w.r.t. D_g (Z1, a12).
+// The occupancy tables of LC lattices at a time live in shared memory ([LC][M] counts of D_g's
+// bins), so a chunk costs two barriers and every candidate walks its lattices in registers.
 __global__ void __launch_bounds__(256)
 k_resolve(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t nJ, int64_t M,
           int32_t L, const int32_t *__restrict__ det_g, const int32_t *__restrict__ n_det_g,
           int32_t s_tilde, const int32_t *__restrict__ det_idx, int64_t n_det,
-          double2 *__restrict__ coef, int32_t *__restrict__ lstar) {
-    extern __shared__ int cnt[];                       // [M]
+          double2 *__restrict__ coef, int32_t *__restrict__ lstar, int32_t LC) {
+    extern __shared__ int cnt[];                       // [LC][M], then D_g [s_tilde]
+    int32_t *Ds = cnt + (int64_t)LC * M;
     const int64_t g = blockIdx.x;
     const int32_t *Dg = det_g + g * (int64_t)s_tilde;
     const int nD = n_det_g[g];
     const int64_t Mh = M / 2 + 1;
     int32_t *ls = lstar + g * n_det;
+    for (int q = threadIdx.x; q < nD; q += blockDim.x) Ds[q] = Dg[q];
     for (int64_t q = threadIdx.x; q < n_det; q += blockDim.x) ls[q] = -1;
-    for (int l = 0; l < L; ++l) {
-        for (int64_t m = threadIdx.x; m < M; m += blockDim.x) cnt[m] = 0;
+    for (int l0 = 0; l0 < L; l0 += LC) {
+        const int lc = min(LC, L - l0);
+        for (int64_t m = threadIdx.x; m < (int64_t)lc * M; m += blockDim.x) cnt[m] = 0;
         __syncthreads();
-        for (int q = threadIdx.x; q < nD; q += blockDim.x) atomicAdd(&cnt[bins[(int64_t)l * nJ + Dg[q]]], 1);
+        for (int e = threadIdx.x; e < nD * lc; e += blockDim.x) {
+            const int q = e % nD, l = e / nD;
+            atomicAdd(&cnt[(int64_t)l * M + bins[(int64_t)(l0 + l) * nJ + Ds[q]]], 1);
+        }
         __syncthreads();
         for (int64_t q = threadIdx.x; q < n_det; q += blockDim.x) {
             if (ls[q] >= 0) continue;
             const int32_t k = det_idx[q];
-            const int64_t b = bins[(int64_t)l * nJ + k];
-            if (cnt[b] - member_sorted(Dg, nD, k) == 0) {
-                ls[q] = l;
-                coef[g * n_det + q] = spec_value(F + (g * L + l) * Mh, M, b);
+            int mem = -1;                              // k in D_g (looked up once, lazily)
+            for (int l = 0; l < lc; ++l) {
+                const int64_t b = bins[(int64_t)(l0 + l) * nJ + k];
+                const int c = cnt[(int64_t)l * M + b];
+                if (c == 1 && mem < 0) mem = member_sorted(Ds, nD, k);
+                // k's own entry (k in D_g) does not count as an alias
+                if (c == 0 || (c == 1 && mem == 1)) {
+                    ls[q] = l0 + l;
+                    coef[g * n_det + q] = spec_value(F + (g * L + l0 + l) * Mh, M, b);
+                    break;
+                }
             }
         }
         __syncthreads();
@@ -276,7 +293,10 @@ extern "C" usfft_status usfft_resolve(usfft_ctx *c, const usfft_lattice_desc *la
     USFFT_REQUIRE(c, G_loc >= 0 && n_det >= 0 && s_tilde >= 1, "bad sizes");
     if (G_loc == 0 || n_det == 0) return USFFT_OK;
     USFFT_REQUIRE(c, spectra && bins && det_g && n_det_g && det_idx && coef, "NULL pointer");
-    const size_t smem = sizeof(int) * (size_t)lat->M;
+    // as many lattices' occupancy tables as fit in ~96 KB (at least one)
+    const int64_t per_l = (int64_t)sizeof(int) * lat->M;
+    int32_t LC = (int32_t)std::max<int64_t>(1, std::min<int64_t>(lat->L, (96 * 1024 - 4 * (int64_t)s_tilde) / per_l));
+    const size_t smem = (size_t)per_l * LC + sizeof(int) * (size_t)s_tilde;
     USFFT_REQUIRE(c, smem <= c->smem_optin, "M too large for the resolve occupancy table");
     int32_t *ls = lstar;
     if (!ls) {
@@ -287,7 +307,7 @@ extern "C" usfft_status usfft_resolve(usfft_ctx *c, const usfft_lattice_desc *la
     if (usfft_status s = kernel_fit(c, k_resolve, 0, smem, nullptr)) return s;
     k_resolve<<<(unsigned)G_loc, 256, smem, c->stream>>>(
         reinterpret_cast<const double2 *>(spectra), bins, nJ, lat->M, lat->L, det_g, n_det_g,
-        s_tilde, det_idx, n_det, reinterpret_cast<double2 *>(coef), ls);
+        s_tilde, det_idx, n_det, reinterpret_cast<double2 *>(coef), ls, LC);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
