@@ -17,8 +17,11 @@ __device__ __forceinline__ double theta2_of(double theta_rel, double theta_abs, 
     return __dmul_rn(__dmul_rn(theta_rel, theta_rel), kmax[0]);
 }
 
-// one CTA per owned node g
-__global__ void __launch_bounds__(512)
+// one CTA per owned node g (128 threads: the radix passes are barrier-bound); the node's keys
+// are staged in shared memory when |J| <= KSTAGE
+constexpr int64_t KSTAGE = 6144;
+
+__global__ void __launch_bounds__(128)
 k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__ kmax,
          int32_t s_tilde, double theta_rel, double theta_abs, int32_t *__restrict__ votes,
          int32_t *__restrict__ det_g, int32_t *__restrict__ n_det_g, double *__restrict__ th2_out) {
@@ -27,9 +30,15 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     __shared__ long long s_need;
     __shared__ bool s_exact;
     __shared__ int scan_sh[33];
+    extern __shared__ unsigned long long kst[];
     const int64_t g = blockIdx.x;
     const unsigned long long *keys =
         reinterpret_cast<const unsigned long long *>(kmin + g * nJ);
+    if (nJ <= KSTAGE) {
+        for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) kst[j] = __ldg(keys + j);
+        keys = kst;
+        __syncthreads();
+    }
     const double th2 = theta2_of(theta_rel, theta_abs, kmax);
     if (g == 0 && threadIdx.x == 0 && th2_out) th2_out[0] = th2;
 
@@ -254,8 +263,10 @@ extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t
         if (G_loc > 0 && n_det_g) USFFT_CUDA(c, cudaMemsetAsync(n_det_g, 0, sizeof(int32_t) * G_loc, c->stream));
         return USFFT_OK;
     }
-    k_select<<<(unsigned)G_loc, 512, 0, c->stream>>>(kappa_min, nJ, kappa_max, s_tilde, theta_rel,
-                                                      theta_abs, votes, det_g, n_det_g, theta2);
+    const size_t kst = nJ <= KSTAGE ? sizeof(unsigned long long) * (size_t)nJ : 0;
+    if (usfft_status s = kernel_fit(c, k_select, 0, kst, nullptr)) return s;
+    k_select<<<(unsigned)G_loc, 128, kst, c->stream>>>(kappa_min, nJ, kappa_max, s_tilde, theta_rel,
+                                                        theta_abs, votes, det_g, n_det_g, theta2);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
