@@ -14,7 +14,7 @@ against.  It is NOT part of the product:
 
 Citation convention: ``P:n`` = line n of the paper's PAPER.md (LaTeX source), with the
 section / equation / algorithm it falls in; ``S:n`` = line n of SPEC.md.  Readings of
-places where the paper is silent are labelled Z1..Z26 as in DESIGN.md §3.
+places where the paper is silent are labelled Z1..Z28 as in DESIGN.md §3.
 
 Pin status (what fixes each function besides itself; see tests/test_oracle_*.py):
 
@@ -27,6 +27,10 @@ lattice.nodes/bins     SPEC worked examples; exact rational identity k.y_i = i.b
 lattice.injective      SPEC examples; brute-force pair check
 fe.assemble/solve      5-point Laplacian stencil for a=1; manufactured solutions O(h^2);
                        SPD + M-matrix (u >= 0); y=0 -> a=1; ellipticity bounds
+fe.psi / diag_index    Table 3 m1/m2/k (golden); affine a_min/a_max 0.1/1.9
+/ f_values (examples)  and c ~ 0.547 (P:1236); lognormal P(|b| <= 3) > 99% (P:1424);
+                       zero sets of psi_j; f = 1 load h^2; product-to-sum identity of f
+fe.tau1/tau2/phi_delta SPEC examples, poles, symmetry, inversion-method distribution
 dft.lattice_dft        orthogonality; exact recovery of trig polynomials on a
                        reconstructing lattice; brute-force tensor-grid FFT for t <= 3
 detect.*               brute force on tiny inputs; Thm 1.1 exact recovery of sparse

@@ -7,12 +7,17 @@ Problem (eq. pde; weak form P:155-158): find u(., y) in H^1_0(D), D = (
 G values u(x_g, y) of one solve are the G samples of one node y (Alg. 1 Step 2c P:313).
 
 Random coefficient (eq. random_coefficient_1; lognormal P:94-98), in the form the
-BASELINE configs instantiate (Z14/Z15):
-    affine form:     a(x,y) = 1 + sum_j amp_j * theta(y_j) * sin(j pi x1) sin(j pi x2)
-    lognormal form:  a(x,y) = exp( sum_j amp_j * theta(y_j) * sin(j pi x1) sin(j pi x2) )
+BASELINE configs and the paper's three examples instantiate (Z14/Z15/Z28):
+    affine form:     a(x,y) = 1 + sum_j amp_j * theta(y_j) * psi_j(x)
+    lognormal form:  a(x,y) = exp( sum_j amp_j * theta(y_j) * psi_j(x) )
+    psi_j = sin(j pi x1) sin(j pi x2)                  (BASELINE configs, periodic example P:1006)
+          | cos(2 pi m1(j) x1) cos(2 pi m2(j) x2)      (affine example P:1207, Table 3)
+          | sin(2 pi j x1) cos(2 pi (d+1-j) x2)        (lognormal example P:1418)
     theta = sin(2 pi y)              (periodic model Theta_j)
           | 1 - |2(1 - 2y)|          (tent, eq. tent P:473-479 with alpha=-1, beta=1)
           | clip(Phi^-1(y), -6, 6)   (lognormal config literal reading, Z15)
+          | clip(tau1(tau2_Delta(y)), -6, 6)  (lognormal periodization phi_Delta, Z27)
+    f = x2 | 1 | sin(1.3 pi x1 + 3.4 pi x2) cos(4.3 pi x1 - 3.1 pi x2)
 
 Discretisation (Z11, Z12): uniform n x n cells of width h = 1/n, each split
 by its SW->NE diagonal into T_lo = {(i,j),(i+1,j),(i+1,j+1)} and T_up = {(i,j),(i+1,j+1),(i,j+1)};
@@ -66,13 +71,41 @@ def theta_map(kind: str, y: np.ndarray, delta: float | None = None) -> np.ndarra
     raise ValueError(f"unknown theta kind {kind!r}")
 
 
+def diag_index(j: int):
+    """(m_1(j), m_2(j), k(j)) of the affine example (Table 3):
+    k(j) = floor(-1/2 + sqrt(1/4 + 2j)), m_1(j) = j - k(j)(k(j)+1)/2, m_2(j) = k(j) - m_1(j)."""
+    k = int(np.floor(-0.5 + np.sqrt(0.25 + 2.0 * j)))
+    m1 = j - k * (k + 1) // 2
+    return m1, k - m1, k
+
+
+def psi(model: dict, j: int, x1: np.ndarray, x2: np.ndarray) -> np.ndarray:
+    """psi_j(x) / amp_j, the spatial factor of term j (1-based) of the coefficient:
+    "sinsin"      sin(j pi x1) sin(j pi x2)                          (periodic example)
+    "cos_diag"    cos(2 pi m_1(j) x1) cos(2 pi m_2(j) x2)            (affine example)
+    "sin_cos_rev" sin(2 pi j x1) cos(2 pi (d + 1 - j) x2)            (lognormal example)
+    (the factor c j^-mu of the first two and 1/j of the third is amp_j)."""
+    kind = model.get("psi", "sinsin")
+    x1 = np.asarray(x1, dtype=np.float64)
+    x2 = np.asarray(x2, dtype=np.float64)
+    if kind == "sinsin":
+        return np.sin(j * np.pi * x1) * np.sin(j * np.pi * x2)
+    if kind == "cos_diag":
+        m1, m2, _ = diag_index(j)
+        return np.cos(2.0 * np.pi * m1 * x1) * np.cos(2.0 * np.pi * m2 * x2)
+    if kind == "sin_cos_rev":
+        return np.sin(2.0 * np.pi * j * x1) * np.cos(2.0 * np.pi * (model["d"] + 1 - j) * x2)
+    raise ValueError(f"unknown psi family {kind!r}")
+
+
 def coefficient(model: dict, y: np.ndarray, x1: np.ndarray, x2: np.ndarray) -> np.ndarray:
-    """a(x, y) at the points (x1, x2) for one parameter vector y (length d)."""
+    """a(x, y) at the points (x1, x2) for one parameter vector y (length d):
+    1 + sum_j amp_j theta(y_j) psi_j(x) (affine form) or exp(sum_j ...) (lognormal form)."""
     d = model["d"]
     th = theta_map(model["theta"], np.asarray(y, dtype=np.float64)[:d], model.get("delta"))
     s = np.zeros_like(np.asarray(x1, dtype=np.float64))
     for j in range(1, d + 1):
-        s = s + model["amp"][j - 1] * th[j - 1] * np.sin(j * np.pi * x1) * np.sin(j * np.pi * x2)
+        s = s + model["amp"][j - 1] * th[j - 1] * psi(model, j, x1, x2)
     if model["form"] == "affine":
         return 1.0 + s
     if model["form"] == "exp":
@@ -184,6 +217,12 @@ def f_values(model: dict, x1: np.ndarray, x2: np.ndarray) -> np.ndarray:
     kind = model.get("f", "x2")
     if kind == "x2":
         return np.asarray(x2, dtype=np.float64).copy()               # BASELINE configs: f = x2
+    if kind == "one":
+        return np.ones_like(np.asarray(x1, dtype=np.float64))        # affine example
+    if kind == "trig":                                               # lognormal example
+        x1 = np.asarray(x1, dtype=np.float64)
+        x2 = np.asarray(x2, dtype=np.float64)
+        return np.sin(1.3 * np.pi * x1 + 3.4 * np.pi * x2) * np.cos(4.3 * np.pi * x1 - 3.1 * np.pi * x2)
     if callable(kind):
         return np.asarray(kind(x1, x2), dtype=np.float64)
     raise ValueError(f"unknown right-hand side {kind!r}")

@@ -192,3 +192,107 @@ def test_global_delta_is_the_lemma_optimum():
     best = grid[np.argmax([score(g) for g in grid])]
     assert abs(best - fe.global_delta(M)) < 1.0 / (2 * M) / 1000
     assert abs(score(fe.global_delta(M)) - 1.0 / (4 * M)) < 1e-15
+
+
+# ---- the paper's example models (Sec. 4.2-4.4; Z28) --------------------------------
+EX = json.load(open(os.path.join(os.path.dirname(__file__), "golden", "paper_examples.json")))
+
+
+def test_affine_table3_indices():
+    """m1(j), m2(j), k(j) of the affine example equal Table 3, and psi_j of the
+    "cos_diag" family is cos(2 pi m1 x1) cos(2 pi m2 x2) with those integers: at x1 = 1/2 its
+    sign is (-1)^m1 and at x2 = 1/2 it is (-1)^m2 (at x = 0 it is 1)."""
+    t = EX["table3"]
+    got = [fe.diag_index(j) for j in t["j"]]
+    assert [g[0] for g in got] == t["m1"] and [g[1] for g in got] == t["m2"] and [g[2] for g in got] == t["k"]
+    m = dict(d=20, psi="cos_diag")
+    for j, m1, m2 in zip(t["j"], t["m1"], t["m2"]):
+        assert fe.psi(m, j, np.array([0.0]), np.array([0.0]))[0] == 1.0
+        assert abs(fe.psi(m, j, np.array([0.5]), np.array([0.0]))[0] - (-1.0) ** m1) < 1e-14
+        assert abs(fe.psi(m, j, np.array([0.0]), np.array([0.5]))[0] - (-1.0) ** m2) < 1e-14
+    # the diagonal enumeration covers every (m1, m2) with m1 + m2 = k exactly once per k
+    for k in range(1, 12):
+        js = [j for j in range(1, 200) if fe.diag_index(j)[2] == k]
+        assert sorted(fe.diag_index(j)[0] for j in js) == list(range(k + 1))
+
+
+def test_affine_example_bounds():
+    """Affine example: c = 0.9 / zeta(2) ~ 0.547 and a_min / a_max = 1 -/+ c zeta(2)
+    = 0.1 / 1.9; the preset's d = 20 coefficient stays inside them and reaches its own d-term
+    extremes 1 -/+ sum amp_j at x = 0 (all psi_j = 1) for y = 0 / y = 1/2 (tent: -1 / +1)."""
+    ex = EX["affine_bounds"]
+    m = config("affine_example")
+    c = m["amp"][0]
+    assert abs(c - ex["c_printed"]) <= ex["c_tol"]
+    z2 = scipy.special.zeta(ex["mu"])
+    assert abs(1 - c * z2 - ex["a_min"]) < 1e-12 and abs(1 + c * z2 - ex["a_max"]) < 1e-12
+    x0 = np.zeros(1)
+    assert abs(fe.coefficient(m, np.zeros(20), x0, x0)[0] - (1 - sum(m["amp"]))) < 1e-14
+    assert abs(fe.coefficient(m, np.full(20, 0.5), x0, x0)[0] - (1 + sum(m["amp"]))) < 1e-14
+    rng = np.random.default_rng(3)
+    for _ in range(30):
+        a = fe.coefficient(m, rng.random(20), *rng.random((2, 300)))
+        assert a.min() > ex["a_min"] and a.max() < ex["a_max"]
+
+
+def test_lognormal_example_b_range():
+    """Lognormal example: b(x, y) = sum_j (1/j) y_j psi_j(x) lies in [-3, 3] with
+    probability > 99% for each x (y ~ N(0, I), d = 10).  b is Gaussian with variance
+    sum_j (b_j(x))^2, b_j(x) = log a(x, y = e_j-probit) read through the oracle's own
+    coefficient (theta = probit, y_j = Phi(1), others 1/2 -> theta = e_j); the bound must hold at
+    the worst node of a fine grid, and fails if the amplitudes 1/j are dropped."""
+    ex = EX["lognormal_b_range"]
+    m = dict(config("lognormal_example"), theta="probit")
+    d = ex["d"]
+    g = np.linspace(0.0, 1.0, 401)
+    x1, x2 = (v.reshape(-1) for v in np.meshgrid(g, g))
+    var = np.zeros_like(x1)
+    for j in range(d):
+        y = np.full(d, 0.5)
+        y[j] = scipy.special.ndtr(1.0)
+        var += np.log(fe.coefficient(m, y, x1, x2)) ** 2
+    prob = 2 * scipy.special.ndtr(ex["bound"] / np.sqrt(var.max())) - 1
+    assert prob > ex["prob"]
+    m1 = dict(m, amp=[1.0] * d)
+    var1 = sum(np.log(fe.coefficient(m1, np.where(np.arange(d) == j, scipy.special.ndtr(1.0), 0.5),
+                                     x1, x2)) ** 2 for j in range(d))
+    assert 2 * scipy.special.ndtr(ex["bound"] / np.sqrt(var1.max())) - 1 < ex["prob"]
+
+
+def test_lognormal_example_psi_and_f():
+    """psi_j = sin(2 pi j x1) cos(2 pi (d+1-j) x2): zero on x1 = 0 and x1 = 1/2,
+    separable with its x1 factor vanishing exactly at multiples of 1/(2j), and at x1 = 1/(4j),
+    x2 = 0 equal to 1; f by the product-to-sum identity equals
+    (sin(5.6 pi x1 + 0.3 pi x2) + sin(-3 pi x1 + 6.5 pi x2)) / 2."""
+    m = config("lognormal_example")
+    d = m["d"]
+    for j in range(1, d + 1):
+        x2 = np.linspace(0, 1, 7)
+        assert np.abs(fe.psi(m, j, np.zeros(7), x2)).max() == 0.0
+        assert np.abs(fe.psi(m, j, np.full(7, 0.5), x2)).max() < 1e-14
+        assert abs(fe.psi(m, j, np.array([1 / (4 * j)]), np.array([0.0]))[0] - 1.0) < 1e-14
+        # x2 frequency d + 1 - j: psi vanishes at x2 = 1/(4 (d+1-j))
+        assert abs(fe.psi(m, j, np.array([1 / (4 * j)]), np.array([1 / (4 * (d + 1 - j))]))[0]) < 1e-14
+    x1, x2 = np.random.default_rng(9).random((2, 100))
+    want = 0.5 * (np.sin(5.6 * np.pi * x1 + 0.3 * np.pi * x2) + np.sin(-3.0 * np.pi * x1 + 6.5 * np.pi * x2))
+    assert np.abs(fe.f_values(m, x1, x2) - want).max() < 1e-14
+
+
+def test_constant_load_and_example_solves():
+    """f = 1 (affine example): the centroid load is h^2 at every interior node (the six
+    triangles around a node have total area 3 h^2, one third each); every example preset
+    assembles to an SPD system (Cholesky succeeds) and solves to round-off; f >= 0 gives u >= 0."""
+    for name in ("periodic_mu1.2", "periodic_mu3.6", "affine_example", "lognormal_example"):
+        m = dict(config(name), n=12)
+        if m["theta"] == "phi_delta":
+            m["delta"] = fe.global_delta(101)
+        cx, cy = fe.centroids(12)
+        _, b = fe.assemble(12, np.ones_like(cx), fe.f_values(m, cx, cy))
+        if m["f"] == "one":
+            assert np.allclose(b, 1.0 / 144, rtol=1e-14, atol=0)
+        rng = np.random.default_rng(5)
+        for _ in range(2):
+            u, rr = fe.solve(m, rng.random(m["d"]), return_residual=True)
+            assert rr < 1e-11
+            if m["f"] != "trig":
+                assert np.all(u >= 0.0)
