@@ -75,8 +75,15 @@ typedef struct {
  *              2: clip(Phi^-1(y), -6, 6) (Z15)
  *              3: clip(tau1(tau2_Delta(y)), -6, 6), the lognormal periodization phi_Delta
  *                 (eq. lognormal_transfo, tau1 P:486, tau2 P:500-506; Z27)
- *   form       0: a = 1 + sum_j amp_j theta_j sin(j pi x1) sin(j pi x2)   1: a = exp(sum ...)
- *   f_kind     0: f(x) = x2 (all BASELINE configs)
+ *   form       0: a = 1 + sum_j amp_j theta_j psi_j(x)   1: a = exp(sum_j amp_j theta_j psi_j(x))
+ *   psi        spatial factors psi_j (Z28):
+ *              0: sin(j pi x1) sin(j pi x2) (BASELINE configs; periodic example P:1006-1008)
+ *              1: cos(2 pi m1(j) x1) cos(2 pi m2(j) x2), m1/m2/k(j) of Table 3 (affine example
+ *                 P:1207-1216)
+ *              2: sin(2 pi j x1) cos(2 pi (d+1-j) x2) (lognormal example P:1418-1420)
+ *   f_kind     0: f(x) = x2 (BASELINE configs, periodic example P:1001)  1: f = 1 (affine
+ *              example P:1203)  2: f = sin(1.3 pi x1 + 3.4 pi x2) cos(4.3 pi x1 - 3.1 pi x2)
+ *              (lognormal example P:1414); loads by the centroid rule (Z12)
  *   amp        host fp64 [d]
  *   tol        relative residual target ||r_k||_2 <= tol ||b||_2 (Z13; BASELINE 1e-12)
  *   maxit      PCG iteration cap
@@ -97,7 +104,7 @@ typedef struct {
     const double *amp;
     double tol;
     int32_t precond;
-    int32_t pad_;
+    int32_t psi;
     double delta;
 } usfft_pde_desc;
 
@@ -201,6 +208,40 @@ usfft_status usfft_detect_select(usfft_ctx *ctx, int64_t G_loc, int64_t nJ,
                                  int32_t s_tilde, double theta_rel, double theta_abs,
                                  int32_t *votes, int32_t *det_g, int32_t *n_det_g,
                                  double *theta2);
+
+/* ---- a8 + a10 streamed over candidate chunks (large |J|; usfft_lattice_keys, usfft_detect_carry)
+ * kappa_min of a run is G_loc * nJ doubles (Step 2 of a slowly decaying function reaches
+ * |J| ~ 1e7, i.e. tens of GB).  The selection of a10 only needs each node's top s_tilde, so the
+ * keys can be produced chunk by chunk and merged into a per-node carry of at most s_tilde
+ * (key, j) pairs; the result is identical to the one-shot selection (Z29):
+ *   merged [G_loc][s_tilde + C]: carry keys (ascending j, 0-padded) then the chunk's keys;
+ *   usfft_detect_select on merged (theta_rel = theta_abs = 0: top s~ of the positive keys, with
+ *   positions ascending = j ascending because every carry j precedes every chunk j);
+ *   usfft_detect_carry (update mode) moves the selected pairs to the front (and to carry_k);
+ * after the last chunk (and the all-reduce of kappa_max), usfft_detect_select on carry_k with
+ * the real threshold and usfft_detect_carry (emit mode) give det_g (global j) and votes.
+ *
+ * usfft_lattice_keys: the keys of a8 from existing spectra for nJ candidates whose bins are
+ *   bins[l * ldb + j] (l < L, j < nJ); writes kappa_min[g * ldk + j] and max-accumulates
+ *   kappa_max (NOT reset: zero it before the first chunk). */
+usfft_status usfft_lattice_keys(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_t G_loc,
+                                const double *spectra, const int32_t *bins, int64_t ldb,
+                                int64_t nJ, double *kappa_min, int64_t ldk, double *kappa_max);
+
+/* usfft_detect_carry, for each owned g with the selection det_pos[g][0..n_det_g[g]) (positions
+ * into row g of merged, ascending, as written by usfft_detect_select on merged):
+ *   update mode (det_g == NULL): j of position p = carry_j[g][p] for p < s_tilde, else
+ *     j0 + p - s_tilde; the selected (key, j) pairs become merged[g][0..n) and carry_k[g][0..n),
+ *     carry_j[g][0..n); slots n..s_tilde-1 get key 0 and j = -1;
+ *   emit mode (det_g != NULL; merged = carry_k, width = s_tilde): det_g[g][r] =
+ *     carry_j[g][det_pos[g][r]] (-1 padded to s_tilde) and votes[that j] += 1 (votes zeroed by
+ *     the caller, int32 [nJ]).
+ * merged dev fp64 [G_loc][width]; carry_k dev fp64 [G_loc][s_tilde]; carry_j dev int32
+ * [G_loc][s_tilde]; det_pos dev int32 [G_loc][s_tilde]; n_det_g dev int32 [G_loc]. */
+usfft_status usfft_detect_carry(usfft_ctx *ctx, int64_t G_loc, int32_t s_tilde, int64_t width,
+                                double *merged, double *carry_k, int32_t *carry_j,
+                                const int32_t *det_pos, const int32_t *n_det_g, int64_t j0,
+                                int32_t *det_g, int32_t *votes);
 
 /* ---- a11: union (usfft_detect_union) ------------------------------------------------------
  * votes must be summed over all ranks (Step 2e P:318: union over g).  flags |= (votes > 0)

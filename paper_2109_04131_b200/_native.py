@@ -25,7 +25,7 @@ class LatticeDesc(C.Structure):
 class PdeDesc(C.Structure):
     _fields_ = [("n", i32), ("d", i32), ("theta", i32), ("form", i32), ("f_kind", i32),
                 ("maxit", i32), ("amp", C.POINTER(f64)), ("tol", f64), ("precond", i32),
-                ("pad_", i32), ("delta", f64)]
+                ("psi", i32), ("delta", f64)]
 
 
 class PlanIn(C.Structure):
@@ -57,6 +57,8 @@ _SIGS = {
     "usfft_lattice_fft": (i32, [vp, C.POINTER(LatticeDesc), i64, vp, i32, C.POINTER(i64), vp, i64,
                                 vp, vp, vp]),
     "usfft_detect_select": (i32, [vp, i64, i64, vp, vp, i32, f64, f64, vp, vp, vp, vp]),
+    "usfft_lattice_keys": (i32, [vp, C.POINTER(LatticeDesc), i64, vp, vp, i64, i64, vp, i64, vp]),
+    "usfft_detect_carry": (i32, [vp, i64, i32, i64, vp, vp, vp, vp, vp, i64, vp, vp]),
     "usfft_detect_union": (i32, [vp, i64, vp, vp, vp, C.POINTER(i64), vp, C.POINTER(i64)]),
     "usfft_resolve": (i32, [vp, C.POINTER(LatticeDesc), i64, vp, vp, i64, vp, vp, i32, vp, i64,
                             vp, vp]),

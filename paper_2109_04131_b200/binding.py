@@ -146,10 +146,11 @@ def pde_desc(cfg: dict, maxit: int = 20000, tol: float = 1e-12, precond: str | N
     amp = np.ascontiguousarray(cfg["amp"][: cfg["d"]], dtype=np.float64)
     theta = {"sin": 0, "tent": 1, "probit": 2, "phi_delta": 3}[cfg["theta"]]
     form = {"affine": 0, "exp": 1}[cfg["form"]]
-    f_kind = {"x2": 0}[cfg.get("f", "x2")]
+    f_kind = {"x2": 0, "one": 1, "trig": 2}[cfg.get("f", "x2")]
+    psi = {"sinsin": 0, "cos_diag": 1, "sin_cos_rev": 2}[cfg.get("psi", "sinsin")]
     pc = effective_precond(cfg, precond)
     dsc = N.PdeDesc(cfg["n"], cfg["d"], theta, form, f_kind, maxit,
-                    amp.ctypes.data_as(C.POINTER(C.c_double)), tol, {"jacobi": 0, "mg": 1}[pc], 0,
+                    amp.ctypes.data_as(C.POINTER(C.c_double)), tol, {"jacobi": 0, "mg": 1}[pc], psi,
                     float(delta))
     return dsc, amp
 
@@ -188,6 +189,28 @@ def usfft_detect_select(ctx: Context, G_loc: int, nJ: int, kappa_min, kappa_max,
                                      _p(votes, torch.int32), _p(det_g, torch.int32),
                                      _p(n_det_g, torch.int32), _p(theta2, torch.float64))
     _check(ctx, st, "usfft_detect_select")
+
+
+def usfft_lattice_keys(ctx: Context, plan: Plan, G_loc: int, spectra, bins, ldb: int, nJ: int, kappa_min,
+                       ldk: int, kappa_max, bins_off: int = 0, kmin_off: int = 0):
+    """a8 for a chunk of candidates: bins[l*ldb + bins_off + j] -> kappa_min[g*ldk + kmin_off + j]
+    (element offsets into the given tensors); kappa_max max-accumulates."""
+    dsc, keep = plan.desc()
+    _p(bins, torch.int32), _p(kappa_min, torch.float64)
+    st = ctx.lib.usfft_lattice_keys(ctx.h, C.byref(dsc), G_loc, _p(spectra, torch.float64),
+                                    bins.data_ptr() + 4 * bins_off, ldb, nJ,
+                                    kappa_min.data_ptr() + 8 * kmin_off, ldk, _p(kappa_max, torch.float64))
+    _check(ctx, st, "usfft_lattice_keys")
+
+
+def usfft_detect_carry(ctx: Context, G_loc: int, s_tilde: int, width: int, merged, carry_k, carry_j,
+                       det_pos, n_det_g, j0: int = 0, det_g=None, votes=None):
+    """Streamed selection step (Z29): update the per-node carry (det_g None) or emit det_g + votes."""
+    st = ctx.lib.usfft_detect_carry(ctx.h, G_loc, s_tilde, width, _p(merged, torch.float64),
+                                    _p(carry_k, torch.float64), _p(carry_j, torch.int32),
+                                    _p(det_pos, torch.int32), _p(n_det_g, torch.int32), j0,
+                                    _p(det_g, torch.int32), _p(votes, torch.int32))
+    _check(ctx, st, "usfft_detect_carry")
 
 
 def usfft_detect_union(ctx: Context, nJ: int, votes, flags, det_idx, union_idx=None):

@@ -8,6 +8,7 @@
 #include <cstdarg>
 #include <cstdio>
 #include <map>
+#include <tuple>
 #include <mutex>
 #include <string>
 #include <utility>
@@ -29,7 +30,8 @@ struct usfft_ctx {
     void *dscal = nullptr;
     // cached tables
     std::map<int64_t, double2 *> twiddles;                  // M -> e^{-2 pi i m/M}, m < M
-    std::map<std::pair<int, int>, double *> sintab;          // (n, d) -> sin(j pi m/(3n))
+    std::map<std::tuple<int, int, int>, double *> sintab;    // (n, d, psi) -> psi factor tables
+    std::map<std::pair<int, int>, double *> rhstab;          // (n, f_kind) -> centroid loads b
     // resident blocks per SM per (kernel, threads, smem): the query costs ~10 us per call
     std::map<std::pair<const void *, size_t>, int> occupancy;
 };

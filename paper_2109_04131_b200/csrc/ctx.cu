@@ -43,6 +43,7 @@ extern "C" usfft_status usfft_finalize(usfft_ctx *c) {
     cudaStreamSynchronize(c->stream);
     for (auto &kv : c->twiddles) cudaFree(kv.second);
     for (auto &kv : c->sintab) cudaFree(kv.second);
+    for (auto &kv : c->rhstab) cudaFree(kv.second);
     if (c->ws) cudaFree(c->ws);
     if (c->dscal) cudaFree(c->dscal);
     delete c;

@@ -137,6 +137,44 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     if (threadIdx.x == 0) n_det_g[g] = out_run;
 }
 
+// streamed selection (Z29): one CTA per owned node moves the selected (key, j) pairs of row g of
+// merged to the carry (update mode), or emits det_g and votes from the final selection on the
+// carry (emit mode, det_g != NULL).  The selection is read completely before anything is written,
+// so merged may alias carry_k.
+__global__ void __launch_bounds__(256)
+k_carry(int32_t s, int64_t width, double *merged, double *carry_k, int32_t *__restrict__ carry_j,
+        const int32_t *__restrict__ det_pos, const int32_t *__restrict__ n_det_g, int64_t j0,
+        int32_t *__restrict__ det_g, int32_t *__restrict__ votes) {
+    extern __shared__ double ck[];                               // [s] keys, then [s] j
+    int32_t *cj = reinterpret_cast<int32_t *>(ck + s);
+    const int64_t g = blockIdx.x;
+    const int n = n_det_g[g];
+    const int32_t *pos = det_pos + g * (int64_t)s;
+    double *row = merged + g * width;
+    int32_t *jrow = carry_j + g * (int64_t)s;
+    for (int r = threadIdx.x; r < n; r += blockDim.x) {
+        const int p = pos[r];
+        ck[r] = row[p];
+        cj[r] = p < s ? jrow[p] : (int32_t)(j0 + p - s);
+    }
+    __syncthreads();
+    if (det_g == nullptr) {
+        double *krow = carry_k + g * (int64_t)s;
+        for (int r = threadIdx.x; r < s; r += blockDim.x) {
+            const double k = r < n ? ck[r] : 0.0;
+            row[r] = k;
+            krow[r] = k;
+            jrow[r] = r < n ? cj[r] : -1;
+        }
+    } else {
+        int32_t *out = det_g + g * (int64_t)s;
+        for (int r = threadIdx.x; r < s; r += blockDim.x) {
+            out[r] = r < n ? cj[r] : -1;
+            if (r < n) atomicAdd(votes + cj[r], 1);
+        }
+    }
+}
+
 // single CTA: flags |= votes > 0; ordered compaction of this round's detections and of the union
 __global__ void __launch_bounds__(1024)
 k_union(const int32_t *__restrict__ votes, int64_t nJ, uint8_t *__restrict__ flags,
@@ -267,6 +305,25 @@ extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t
     if (usfft_status s = kernel_fit(c, k_select, 0, kst, nullptr)) return s;
     k_select<<<(unsigned)G_loc, 128, kst, c->stream>>>(kappa_min, nJ, kappa_max, s_tilde, theta_rel,
                                                         theta_abs, votes, det_g, n_det_g, theta2);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
+extern "C" usfft_status usfft_detect_carry(usfft_ctx *c, int64_t G_loc, int32_t s_tilde, int64_t width,
+                                           double *merged, double *carry_k, int32_t *carry_j,
+                                           const int32_t *det_pos, const int32_t *n_det_g, int64_t j0,
+                                           int32_t *det_g, int32_t *votes) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, G_loc >= 0 && s_tilde >= 1 && width >= s_tilde && j0 >= 0, "bad sizes");
+    USFFT_REQUIRE(c, j0 + width - s_tilde <= 0x7fffffff, "candidate index beyond int32");
+    if (G_loc == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, merged && carry_j && det_pos && n_det_g, "NULL argument");
+    USFFT_REQUIRE(c, det_g != nullptr || carry_k != nullptr, "update mode needs carry_k");
+    USFFT_REQUIRE(c, det_g == nullptr || (votes != nullptr && width == s_tilde), "emit mode: votes, width = s_tilde");
+    const size_t dyn = (sizeof(double) + sizeof(int32_t)) * (size_t)s_tilde;
+    if (usfft_status s = kernel_fit(c, k_carry, 0, dyn, nullptr)) return s;
+    k_carry<<<(unsigned)G_loc, 256, dyn, c->stream>>>(s_tilde, width, merged, carry_k, carry_j, det_pos, n_det_g,
+                                                       j0, det_g, votes);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }

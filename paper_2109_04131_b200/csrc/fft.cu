@@ -131,8 +131,9 @@ k_dft_bins(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int6
 // independent coalesced loads (the L2 latency is paid once per tile, not once per lattice),
 // then each thread gathers and reduces its candidate.
 __global__ void __launch_bounds__(256)
-k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t nJ, int64_t M,
-        int32_t L, double *__restrict__ kmin, unsigned long long *__restrict__ kmax, int staged) {
+k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t ldb, int64_t nJ,
+        int64_t M, int32_t L, double *__restrict__ kmin, int64_t ldk, unsigned long long *__restrict__ kmax,
+        int staged) {
     extern __shared__ double2 fs[];
     __shared__ unsigned long long wmax[32];
     const int64_t g = blockIdx.x;
@@ -150,7 +151,7 @@ k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t
         const int64_t j = j0 + threadIdx.x;
         __syncthreads();                                  // previous tile's readers are done
 #pragma unroll 8
-        for (int l = 0; l < L; ++l) sb[l * 256 + threadIdx.x] = j < nJ ? __ldg(bins + (int64_t)l * nJ + j) : 0;
+        for (int l = 0; l < L; ++l) sb[l * 256 + threadIdx.x] = j < nJ ? __ldg(bins + (int64_t)l * ldb + j) : 0;
         __syncthreads();
         if (j < nJ) {
             // v = F^[b] / M with F^[b] = conj(F[M - b]) above M/2 (the sign does not enter the
@@ -164,7 +165,7 @@ k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t
                 const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
                 km = (l == 0) ? k : fmin(km, k);
             }
-            kmin[g * nJ + j] = km;
+            kmin[g * ldk + j] = km;
             const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
             best = bits > best ? bits : best;
         }
@@ -345,6 +346,27 @@ static usfft_status get_twiddles(usfft_ctx *c, int64_t M, double2 **out) {
     return USFFT_OK;
 }
 
+namespace {
+// K7: keys of nJ candidates (bins[l * ldb + j]) into kmin[g * ldk + j], max into kappa_max
+// (NULL: a ctx scratch slot)
+usfft_status launch_keys(usfft_ctx *c, int64_t M, int32_t L, int64_t G_loc, const double *spectra,
+                         const int32_t *bins, int64_t ldb, int64_t nJ, double *kappa_min, int64_t ldk,
+                         double *kappa_max) {
+    unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
+    if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
+    const size_t st_bytes = sizeof(double2) * (size_t)L * (size_t)(M / 2 + 1);
+    const size_t tile_bytes = sizeof(int32_t) * 256 * (size_t)L;
+    const int staged = st_bytes + tile_bytes <= 112 * 1024 ? 1 : 0;
+    const size_t dyn = (staged ? st_bytes : 0) + tile_bytes;
+    USFFT_REQUIRE(c, dyn <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
+    if (usfft_status s2 = kernel_fit(c, k_kappa, 0, dyn, nullptr)) return s2;
+    k_kappa<<<(unsigned)G_loc, 256, dyn, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb,
+                                                       nJ, M, L, kappa_min, ldk, km, staged);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+}  // namespace
+
 extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc *lat,
                                           int64_t G_loc, const double *u, int32_t nslab,
                                           const int64_t *slab_b0, const int32_t *bins, int64_t nJ,
@@ -410,20 +432,20 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
                                                                 reinterpret_cast<double2 *>(spectra));
         USFFT_CHECK_LAUNCH(c);
     }
-    if (nJ > 0) {
-        unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
-        if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
-        const size_t st_bytes = sizeof(double2) * (size_t)L * (size_t)(M / 2 + 1);
-        const size_t tile_bytes = sizeof(int32_t) * 256 * (size_t)L;
-        const int staged = st_bytes + tile_bytes <= 112 * 1024 ? 1 : 0;
-        const size_t dyn = (staged ? st_bytes : 0) + tile_bytes;
-        USFFT_REQUIRE(c, dyn <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
-        if (usfft_status s2 = kernel_fit(c, k_kappa, 0, dyn, nullptr)) return s2;
-        k_kappa<<<(unsigned)G_loc, 256, dyn, c->stream>>>(
-            reinterpret_cast<const double2 *>(spectra), bins, nJ, M, L, kappa_min, km, staged);
-        USFFT_CHECK_LAUNCH(c);
-    }
+    if (nJ > 0) return launch_keys(c, M, L, G_loc, spectra, bins, nJ, nJ, kappa_min, nJ, kappa_max);
     return USFFT_OK;
+}
+
+extern "C" usfft_status usfft_lattice_keys(usfft_ctx *c, const usfft_lattice_desc *lat, int64_t G_loc,
+                                           const double *spectra, const int32_t *bins, int64_t ldb,
+                                           int64_t nJ, double *kappa_min, int64_t ldk, double *kappa_max) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, lat != nullptr, "lattice desc is NULL");
+    USFFT_REQUIRE(c, lat->M >= 2 && lat->M <= (int64_t(1) << 26) && lat->L >= 1, "bad M / L");
+    USFFT_REQUIRE(c, G_loc >= 0 && nJ >= 0 && ldb >= nJ && ldk >= nJ, "bad sizes / leading dimensions");
+    if (G_loc == 0 || nJ == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, spectra && bins && kappa_min && kappa_max, "NULL argument");
+    return launch_keys(c, lat->M, lat->L, G_loc, spectra, bins, ldb, nJ, kappa_min, ldk, kappa_max);
 }
 
 extern "C" usfft_status usfft_lattice_dft_bins(usfft_ctx *c, int64_t M, int64_t G_loc, const double *u,

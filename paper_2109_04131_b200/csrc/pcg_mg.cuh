@@ -72,8 +72,9 @@ struct Mg3 {
     static constexpr int oWH3 = oK + 2 * HK * U2, oWV3 = oWH3 + N3, oAI = oWV3 + N3;   // K: 2 HK columns
     static constexpr int oB = oAI + U3 * U3, oC = oB + U3 * U2;
     __host__ __device__ static constexpr int doubles() { return oC + U3 * U2; }
-    // the sin table S[j][m] (d x (3n+1)) is staged after these when it has at most SMAX doubles
-    static constexpr int SMAX = 2560;
+    // the psi tables S[plane][j][m] ((1 or 2) x d x (3n+1)) are staged after these when they
+    // have at most SMAX doubles (n = 32: 9208 + 4096 doubles, two CTAs still fit an SM)
+    static constexpr int SMAX = 4096;
     // split-row slot of column i (even columns first)
     __host__ __device__ static constexpr int col1s(int i) { return (i & 1) ? H1 + (i >> 1) : (i >> 1); }
 };
@@ -82,7 +83,8 @@ template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 __global__ void __launch_bounds__(NWARP * 32, MINB)
 k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
          int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
-         double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S) {
+         double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
+         const double *__restrict__ Bt) {
     using L = Mg3<NC>;
     constexpr int RGW = 32 / LX, NRG = NWARP * RGW, NT = NWARP * 32;
     constexpr int n = NC, nx = n - 1, np = n + 1, W = 3 * n + 1, NP2 = L::NP2, HE = L::HE;
@@ -129,11 +131,13 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 
     // the sample-independent sin table, staged once per CTA (L1 reloads of it were ~500 cycles
     // per coefficient term in the probe)
-    const bool s_staged = Q.d * W <= L::SMAX;
+    const int s_cnt = (Q.psi ? 2 : 1) * Q.d * W;         // X plane (+ Y plane unless psi = 0)
+    const bool s_staged = s_cnt <= L::SMAX;
     double *Ssm = sm + L::doubles() + (XP_SMEM ? 2 * BC * BR * NT : 0);
     if (s_staged)
-        for (int e = tid; e < Q.d * W; e += NT) Ssm[e] = __ldg(S + e);
+        for (int e = tid; e < s_cnt; e += NT) Ssm[e] = __ldg(S + e);
     const double *Stab = s_staged ? Ssm : S;
+    const double *StabY = Stab + (Q.psi ? Q.d * W : 0);
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
@@ -160,7 +164,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int k = 0; k < KJ; ++k) slo[a][k] = sup[a][k] = 0.0;
 #pragma unroll 2
             for (int j = 0; j < Q.d; ++j) {
-                const double *Sj = Stab + j * W;
+                const double *Sj = Stab + j * W, *Sy = StabY + j * W;
                 const double am = th_amp[j];
                 double tlo[KI], tup[KI], vlo[KJ], vup[KJ];
 #pragma unroll
@@ -170,8 +174,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
 #pragma unroll
                 for (int k = 0; k < KJ; ++k) {
-                    vlo[k] = Sj[3 * (cj0 + CJS * k) + 1];
-                    vup[k] = Sj[3 * (cj0 + CJS * k) + 2];
+                    vlo[k] = Sy[3 * (cj0 + CJS * k) + 1];
+                    vup[k] = Sy[3 * (cj0 + CJS * k) + 2];
                 }
 #pragma unroll
                 for (int a = 0; a < KI; ++a)
@@ -574,7 +578,9 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
                 xref(q, c) = pref(q, c) = s[q][c] = 0.0;
-                r[q][c] = valid(q, c) ? (double)(row0 + q + 1) * inv_n3 : 0.0;     // b = h^2 x2
+                r[q][c] = !valid(q, c) ? 0.0                                        // b = h^2 x2, or
+                        : Bt ? __ldg(Bt + (row0 + q) * nx + col0 + c)                // the load table
+                             : (double)(row0 + q + 1) * inv_n3;
             }
         double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
         bool conv = false;

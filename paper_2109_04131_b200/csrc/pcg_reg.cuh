@@ -35,7 +35,8 @@ template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 __global__ void __launch_bounds__(NWARP * 32, MINB)
 k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
           int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
-          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S) {
+          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
+          const double *__restrict__ Bt) {
     constexpr int RGW = 32 / LX;                 // row groups per warp
     constexpr int NRG = NWARP * RGW;             // row groups per CTA
     constexpr int NCOL = LX * BC;                // covered columns
@@ -58,6 +59,9 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
     const int rg = warp * RGW + seg;
     const int col0 = lx * BC, row0 = rg * BR;    // 0-based interior column/row of the block
     const double inv_n3 = 1.0 / ((double)n * n * n);
+    // load of interior node (i, j): h^2 x2 = j / n^3 for f = x2, else the centroid-rule table
+    auto bval = [&](int i, int j) -> double { return Bt ? __ldg(Bt + (j - 1) * nx + i - 1) : (double)j * inv_n3; };
+    const double *Sy = S + (Q.psi ? Q.d * W : 0);
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
@@ -72,7 +76,7 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             const int m1 = (e & 1) ? 3 * ci + 1 : 3 * ci + 2;     // T_up : T_lo
             const int m2 = (e & 1) ? 3 * cj + 2 : 3 * cj + 1;
             double s = 0.0;
-            for (int j = 0; j < Q.d; ++j) s += th_amp[j] * S[j * W + m1] * S[j * W + m2];
+            for (int j = 0; j < Q.d; ++j) s += th_amp[j] * S[j * W + m1] * Sy[j * W + m2];
             aT[e] = Q.form == 0 ? 1.0 + s : exp(s);
         }
         __syncthreads();
@@ -111,7 +115,7 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
                 x[k][c] = 0.0;
                 p[k][c] = 0.0;
                 s[k][c] = 0.0;
-                r[k][c] = ok ? ((double)j * inv_n3) / sqrt(dg[j * np + i]) : 0.0;      // b^ = D^-1/2 b
+                r[k][c] = ok ? bval(i, j) / sqrt(dg[j * np + i]) : 0.0;               // b^ = D^-1/2 b
             }
 #pragma unroll
         for (int k = 0; k < BR; ++k)
@@ -156,8 +160,8 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         for (int c = 0; c < BC; ++c) {           // r_0 of the neighbouring rows: b^ there
             const int i = col0 + c + 1;
             const int jb = row0, ja = row0 + BR + 1;
-            below[c] = (jb >= 1 && i <= nx && rg > 0) ? ((double)jb * inv_n3) / sqrt(dg[jb * np + i]) : 0.0;
-            above[c] = (ja <= nx && i <= nx && rg + 1 < NRG) ? ((double)ja * inv_n3) / sqrt(dg[ja * np + i]) : 0.0;
+            below[c] = (jb >= 1 && i <= nx && rg > 0) ? bval(i, jb) / sqrt(dg[jb * np + i]) : 0.0;
+            above[c] = (ja <= nx && i <= nx && rg + 1 < NRG) ? bval(i, ja) / sqrt(dg[ja * np + i]) : 0.0;
         }
         int it = 0;
         for (int k = 0;; ++k) {

@@ -6,7 +6,8 @@
 //     (A u)_p = sum_{edges e=(p,q)} w_e (u_p - u_q),
 //     w_h(i,j) = (a(T_lo(i,j)) + a(T_up(i,j-1)))/2,  w_v(i,j) = (a(T_up(i,j)) + a(T_lo(i-1,j)))/2,
 // T_lo(ci,cj) centroid ((ci+2/3)h, (cj+1/3)h), T_up(ci,cj) centroid ((ci+1/3)h, (cj+2/3)h);
-// the centroid load of f = x2 is b_p = h^2 x2_p.  (The oracle assembles element by element; a
+// the centroid load of f = x2 is b_p = h^2 x2_p (closed form); other f (Z28) come from a table
+// b_p = (h^2/6) sum of f over the centroids of the six triangles around p (k_rhs).  (The oracle assembles element by element; a
 // CPU test checks this stencil against that assembly.)
 //
 // One CTA solves one sample at a time (persistent loop over samples).  The padded node grid
@@ -21,7 +22,7 @@
 namespace usfft {
 
 struct PdeParams {
-    int32_t n, d, theta, form, f_kind, maxit, precond;
+    int32_t n, d, theta, form, f_kind, maxit, precond, psi;
     double tol2;              // tol^2
     double delta;             // global pole shift of phi_Delta (Z27)
     double amp[kMaxD];
@@ -39,20 +40,59 @@ __device__ __forceinline__ double theta_of(int kind, double y, double delta) {
     return fmin(fmax(v, -6.0), 6.0);                               // clip, NaN-free: -inf -> -6
 }
 
-// sin(j pi m / (3n)) for j = 1..d, m = 0..3n: the centroid abscissae are (3c+1)h/3, (3c+2)h/3.
-__global__ void k_sintab(int n, int d, double *__restrict__ S) {
-    const int W = 3 * n + 1;
-    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < d * W; e += gridDim.x * blockDim.x) {
-        const int j = e / W + 1, m = e % W;
-        S[e] = sinpi((double)(j * m) / (double)(3 * n));
+// The separable spatial factors psi_j(x) = X_j(x1) Y_j(x2) at the abscissae m h/3, m = 0..3n
+// (the centroid abscissae are (3c+1)h/3, (3c+2)h/3): S[0][j][m] = X_j, S[1][j][m] = Y_j, the
+// second plane only when Y differs from X (psi != 0).  Arguments are exact rationals
+// (integer numerator / 3n) through sinpi / cospi.
+//   psi 0: X_j = Y_j = sin(j pi t)
+//   psi 1: X_j = cos(2 pi m1(j) t), Y_j = cos(2 pi m2(j) t)          (Table 3)
+//   psi 2: X_j = sin(2 pi j t), Y_j = cos(2 pi (d+1-j) t)
+__global__ void k_psitab(int n, int d, int psi, double *__restrict__ S) {
+    const int W = 3 * n + 1, planes = psi == 0 ? 1 : 2;
+    for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < planes * d * W; e += gridDim.x * blockDim.x) {
+        const int pl = e / (d * W), j = (e / W) % d + 1, m = e % W;
+        const double t3n = (double)(3 * n);
+        double v;
+        if (psi == 0) {
+            v = sinpi((double)(j * m) / t3n);
+        } else if (psi == 1) {
+            int k = 1;                                       // k(j): largest k with k(k+1)/2 <= j
+            while ((k + 1) * (k + 2) / 2 <= j) ++k;
+            const int m1 = j - k * (k + 1) / 2, mm = pl == 0 ? m1 : k - m1;
+            v = cospi((double)(2 * mm * m) / t3n);
+        } else {
+            v = pl == 0 ? sinpi((double)(2 * j * m) / t3n) : cospi((double)(2 * (d + 1 - j) * m) / t3n);
+        }
+        S[e] = v;
     }
 }
 
-// a at a triangle centroid with sin-table columns m1 (x1) and m2 (x2)
+// f at the point (m1 h/3, m2 h/3) for f_kind 1, 2 (Z28)
+__device__ __forceinline__ double f_at(int kind, int n, int m1, int m2) {
+    if (kind == 1) return 1.0;                                   // affine example
+    const double x1 = (double)m1 / (3.0 * n), x2 = (double)m2 / (3.0 * n);
+    return sinpi(1.3 * x1 + 3.4 * x2) * cospi(4.3 * x1 - 3.1 * x2);   // lognormal example
+}
+
+// centroid-rule loads b_g = sum_{T containing g} f(c_T) |T| / 3 = (h^2 / 6) sum over the six
+// triangles T_lo(i,j), T_up(i,j), T_lo(i-1,j), T_lo(i-1,j-1), T_up(i-1,j-1), T_up(i,j-1)
+__global__ void k_rhs(int n, int kind, double *__restrict__ B) {
+    const int nx = n - 1;
+    for (int g = blockIdx.x * blockDim.x + threadIdx.x; g < nx * nx; g += gridDim.x * blockDim.x) {
+        const int i = g % nx + 1, j = g / nx + 1;
+        const double s = f_at(kind, n, 3 * i + 2, 3 * j + 1) + f_at(kind, n, 3 * i + 1, 3 * j + 2) +
+                         f_at(kind, n, 3 * i - 1, 3 * j + 1) + f_at(kind, n, 3 * i - 1, 3 * j - 2) +
+                         f_at(kind, n, 3 * i - 2, 3 * j - 1) + f_at(kind, n, 3 * i + 1, 3 * j - 1);
+        B[g] = s / (6.0 * n * n);
+    }
+}
+
+// a at a triangle centroid with table columns m1 (x1, plane X) and m2 (x2, plane Y)
 __device__ __forceinline__ double coef_at(const PdeParams &Q, const double *__restrict__ th_amp,
-                                          const double *__restrict__ S, int W, int m1, int m2) {
+                                          const double *__restrict__ X, const double *__restrict__ Y,
+                                          int W, int m1, int m2) {
     double s = 0.0;
-    for (int j = 0; j < Q.d; ++j) s += th_amp[j] * S[j * W + m1] * S[j * W + m2];
+    for (int j = 0; j < Q.d; ++j) s += th_amp[j] * X[j * W + m1] * Y[j * W + m2];
     return Q.form == 0 ? 1.0 + s : exp(s);
 }
 
@@ -61,7 +101,7 @@ __global__ void __launch_bounds__(THREADS)
 k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
       int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
       double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
-      double *__restrict__ gscratch, int64_t region) {
+      const double *__restrict__ Bt, double *__restrict__ gscratch, int64_t region) {
     extern __shared__ double smem[];
     __shared__ double red[64];
     __shared__ double th_amp[kMaxD];
@@ -76,7 +116,8 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
     double *dinv = r + G;                // [G]
     constexpr int T = THREADS;
     const int tid = threadIdx.x;
-    const double h2b = 1.0 / ((double)n * n * n);   // b_p = h^2 * x2_p = j / n^3
+    const double h2b = 1.0 / ((double)n * n * n);   // b_p = h^2 * x2_p = j / n^3 (f = x2)
+    const double *Sy = S + (Q.psi ? Q.d * W : 0);
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
@@ -91,11 +132,11 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
             p[e] = 0.0;
             double h = 0.0, v = 0.0;
             if (i < n && j >= 1 && j <= nx)                        // horizontal edge (i,j)-(i+1,j)
-                h = 0.5 * (coef_at(Q, th_amp, S, W, 3 * i + 2, 3 * j + 1) +        // T_lo(i,j)
-                           coef_at(Q, th_amp, S, W, 3 * i + 1, 3 * (j - 1) + 2));  // T_up(i,j-1)
+                h = 0.5 * (coef_at(Q, th_amp, S, Sy, W, 3 * i + 2, 3 * j + 1) +        // T_lo(i,j)
+                           coef_at(Q, th_amp, S, Sy, W, 3 * i + 1, 3 * (j - 1) + 2));  // T_up(i,j-1)
             if (j < n && i >= 1 && i <= nx)                        // vertical edge (i,j)-(i,j+1)
-                v = 0.5 * (coef_at(Q, th_amp, S, W, 3 * i + 1, 3 * j + 2) +        // T_up(i,j)
-                           coef_at(Q, th_amp, S, W, 3 * (i - 1) + 2, 3 * j + 1));  // T_lo(i-1,j)
+                v = 0.5 * (coef_at(Q, th_amp, S, Sy, W, 3 * i + 1, 3 * j + 2) +        // T_up(i,j)
+                           coef_at(Q, th_amp, S, Sy, W, 3 * (i - 1) + 2, 3 * j + 1));  // T_lo(i-1,j)
             wh[e] = h;
             wv[e] = v;
         }
@@ -108,7 +149,7 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
                 const int i = g % nx + 1, j = g / nx + 1, e = j * np + i;
                 const double dg = wh[e] + wh[e - 1] + wv[e] + wv[e - np];
                 const double di = 1.0 / dg;
-                const double bv = (double)j * h2b;
+                const double bv = Bt ? Bt[g] : (double)j * h2b;
                 dinv[g] = di;
                 x[g] = 0.0;
                 r[g] = bv;
@@ -193,8 +234,9 @@ namespace {
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                            const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
-                           int32_t *iters, double *relres, int32_t *noconv, const double *S) {
-    const int sw = Q.d * (3 * NC + 1);                  // staged sin table (if small enough)
+                           int32_t *iters, double *relres, int32_t *noconv, const double *S,
+                           const double *Bt) {
+    const int sw = (Q.psi ? 2 : 1) * Q.d * (3 * NC + 1);  // staged psi tables (if small enough)
     const size_t dyn = sizeof(double) * ((size_t)Mg3<NC>::doubles() + (MINB * NWARP >= 12 ? 2 * BC * BR * NWARP * 32 : 0) +
                                          (sw <= Mg3<NC>::SMAX ? sw : 0));
     auto kern = k_pcg_mg<NC, BC, BR, LX, NWARP, MINB>;
@@ -204,7 +246,7 @@ usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
     int64_t grid = (int64_t)per_sm * c->sm_count;
     if (grid > nb) grid = nb;
     kern<<<(unsigned)grid, NWARP * 32, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
-                                                         noconv, S);
+                                                         noconv, S, Bt);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -212,7 +254,8 @@ usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
 usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                             const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
-                            int32_t *iters, double *relres, int32_t *noconv, const double *S) {
+                            int32_t *iters, double *relres, int32_t *noconv, const double *S,
+                           const double *Bt) {
     const int n = Q.n;
     constexpr int NRG = NWARP * (32 / LX), NCOL = LX * BC;
     const size_t dyn = sizeof(double) * (size_t)(2 * n * n + (n + 1) * (n + 1) + 12 * NRG * NCOL);
@@ -223,7 +266,7 @@ usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q
     int64_t grid = (int64_t)per_sm * c->sm_count;
     if (grid > nb) grid = nb;
     kern<<<(unsigned)grid, NWARP * 32, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
-                                                         noconv, S);
+                                                         noconv, S, Bt);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -231,7 +274,7 @@ usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q
 template <int NPT, int THREADS>
 usfft_status launch_pcg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
                         int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters,
-                        double *relres, int32_t *noconv, const double *S) {
+                        double *relres, int32_t *noconv, const double *S, const double *Bt) {
     const int threads = THREADS;
     const int n = Q.n, G = (n - 1) * (n - 1), np = n + 1;
     const int64_t region = 3LL * np * np + 3LL * G;           // doubles per sample state
@@ -257,7 +300,7 @@ usfft_status launch_pcg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, co
     }
     if ((int64_t)grid > nb) grid = (int)nb;
     k_pcg<NPT, THREADS><<<grid, threads, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
-                                                   noconv, S, gscratch, region);
+                                                   noconv, S, Bt, gscratch, region);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -278,7 +321,8 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     USFFT_REQUIRE(c, pde->theta >= 0 && pde->theta <= 3, "theta kind %d", pde->theta);
     USFFT_REQUIRE(c, pde->theta != 3 || (pde->delta > 0.0 && pde->delta < 0.5), "delta out of (0, 1/2)");
     USFFT_REQUIRE(c, pde->form == 0 || pde->form == 1, "form %d", pde->form);
-    USFFT_REQUIRE(c, pde->f_kind == 0, "f_kind %d not implemented", pde->f_kind);
+    USFFT_REQUIRE(c, pde->f_kind >= 0 && pde->f_kind <= 2, "f_kind %d", pde->f_kind);
+    USFFT_REQUIRE(c, pde->psi >= 0 && pde->psi <= 2, "psi %d", pde->psi);
     USFFT_REQUIRE(c, pde->amp != nullptr, "amp is NULL");
     USFFT_REQUIRE(c, pde->tol > 0.0 && pde->maxit >= 1, "tol/maxit");
     USFFT_REQUIRE(c, pde->precond == 0 || pde->precond == 1, "precond %d", pde->precond);
@@ -296,21 +340,35 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     Q.maxit = pde->maxit;
     Q.precond = pde->precond;
     Q.delta = pde->delta;
+    Q.psi = pde->psi;
     Q.tol2 = pde->tol * pde->tol;
     for (int j = 0; j < pde->d; ++j) Q.amp[j] = pde->amp[j];
 
-    // sin table for (n, d): cached per ctx
-    auto key = std::make_pair(pde->n, pde->d);
-    double *S = nullptr;
+    // psi factor tables for (n, d, psi) and the load table for (n, f_kind != 0): cached per ctx
+    auto key = std::make_tuple(pde->n, pde->d, pde->psi);
+    double *S = nullptr, *Bt = nullptr;
     auto it = c->sintab.find(key);
     if (it == c->sintab.end()) {
-        const size_t cnt = (size_t)pde->d * (3 * pde->n + 1);
+        const size_t cnt = (size_t)(pde->psi ? 2 : 1) * pde->d * (3 * pde->n + 1);
         USFFT_CUDA(c, cudaMalloc(&S, cnt * sizeof(double)));
-        k_sintab<<<grid1d(cnt, 256), 256, 0, c->stream>>>(pde->n, pde->d, S);
+        k_psitab<<<grid1d(cnt, 256), 256, 0, c->stream>>>(pde->n, pde->d, pde->psi, S);
         USFFT_CHECK_LAUNCH(c);
         c->sintab[key] = S;
     } else {
         S = it->second;
+    }
+    if (pde->f_kind != 0) {
+        auto rk = std::make_pair(pde->n, pde->f_kind);
+        auto rt = c->rhstab.find(rk);
+        if (rt == c->rhstab.end()) {
+            const size_t cnt = (size_t)(pde->n - 1) * (pde->n - 1);
+            USFFT_CUDA(c, cudaMalloc(&Bt, cnt * sizeof(double)));
+            k_rhs<<<grid1d(cnt, 256), 256, 0, c->stream>>>(pde->n, pde->f_kind, Bt);
+            USFFT_CHECK_LAUNCH(c);
+            c->rhstab[rk] = Bt;
+        } else {
+            Bt = rt->second;
+        }
     }
     int32_t *noconv = reinterpret_cast<int32_t *>(c->dscal);      // device counter slot 0
     USFFT_CUDA(c, cudaMemsetAsync(noconv, 0, sizeof(int32_t), c->stream));
@@ -322,34 +380,34 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     const bool reg_ok = !(force && force[0] == 's');
     const char *mgl = getenv("USFFT_MG_LAYOUT");
     if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '2')        // 256 threads, 2x2 blocks
-        s = launch_pcg_mg<32, 2, 2, 16, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        s = launch_pcg_mg<32, 2, 2, 16, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '3')   // 3 CTAs/SM, x and p in smem
-        s = launch_pcg_mg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        s = launch_pcg_mg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 32)                          // 128 threads, 2x4 blocks
-        s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 16)
-        s = launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        s = launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1)
         return fail(c, USFFT_EUNIMPL, "multigrid preconditioner implemented for n = 16, 32");
     else if (reg_ok && n == 16)
-        s = launch_pcg_reg<16, 2, 4, 8, 1, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+        s = launch_pcg_reg<16, 2, 4, 8, 1, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (reg_ok && n == 32)
     {
         const char *lay = getenv("USFFT_PCG_LAYOUT");       // experiments: thread block of nodes
         if (lay && lay[0] == '1')
-            s = launch_pcg_reg<32, 1, 4, 32, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+            s = launch_pcg_reg<32, 1, 4, 32, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
         else if (lay && lay[0] == '4')                      // 4 columns x 2 rows per thread
-            s = launch_pcg_reg<32, 4, 2, 8, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+            s = launch_pcg_reg<32, 4, 2, 8, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
         else if (getenv("USFFT_PCG4"))
-            s = launch_pcg_reg<32, 2, 4, 16, 4, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+            s = launch_pcg_reg<32, 2, 4, 16, 4, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
         else
-            s = launch_pcg_reg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+            s = launch_pcg_reg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     }
     // threads x nodes-per-thread: 128x2 (G <= 256), 256x4 (G <= 1024), 512x8, 1024x16
-    else if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
-    else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
-    else if (G <= 4096) s = launch_pcg<8, 512>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
-    else s = launch_pcg<16, 1024>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S);
+    else if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (G <= 4096) s = launch_pcg<8, 512>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else s = launch_pcg<16, 1024>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     if (s) return s;
     int32_t host_nc = 0;
     if (n_noconv) {

@@ -103,17 +103,24 @@ class Detector:
         mark("exchange")
         Mh = M // 2 + 1
         spectra = torch.empty((self.G_loc, L, Mh, 2), dtype=torch.float64, device=dev)
-        kmin = torch.empty((self.G_loc, nJ), dtype=torch.float64, device=dev)
         kmax = torch.zeros(1, dtype=torch.float64, device=dev)
-        B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, nJ, spectra, kmin, kmax)
-        mark("fft")
-        self.ex.max_(kmax)
-        votes = torch.empty(nJ, dtype=torch.int32, device=dev)
         det_g = torch.empty((self.G_loc, s_tilde), dtype=torch.int32, device=dev)
         n_det_g = torch.empty(self.G_loc, dtype=torch.int32, device=dev)
         th2 = torch.empty(1, dtype=torch.float64, device=dev)
-        B.usfft_detect_select(ctx, self.G_loc, nJ, kmin, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
-                              cfg.get("theta_abs", 0.0), votes, det_g, n_det_g, th2)
+        chunk = self.key_chunk(nJ, s_tilde)
+        if chunk is None:
+            kmin = torch.empty((self.G_loc, nJ), dtype=torch.float64, device=dev)
+            B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, nJ, spectra, kmin, kmax)
+            mark("fft")
+            self.ex.max_(kmax)
+            votes = torch.empty(nJ, dtype=torch.int32, device=dev)
+            B.usfft_detect_select(ctx, self.G_loc, nJ, kmin, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
+                                  cfg.get("theta_abs", 0.0), votes, det_g, n_det_g, th2)
+        else:
+            kmin = None
+            B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, 0, spectra, None, kmax)
+            mark("fft")
+            votes = self._streamed_select(plan, nJ, s_tilde, chunk, spectra, bins, kmax, det_g, n_det_g, th2)
         self.ex.sum_(votes)
         det_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
         union_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
@@ -140,6 +147,44 @@ class Detector:
         return res
 
     # ------------------------------------------------------------------------------------------
+    KEY_BYTES = 4 << 30         # largest one-shot kappa_min [G_loc][|J|] before the keys are streamed
+
+    def key_chunk(self, nJ: int, s_tilde: int) -> int | None:
+        """Candidates per chunk of the streamed selection (Z29), or None for the one-shot path:
+        cfg["key_chunk"] forces a chunk size; otherwise stream when G_loc |J| 8 B > KEY_BYTES."""
+        forced = self.cfg.get("key_chunk")
+        if forced:
+            return int(forced) if nJ > int(forced) else None
+        if self.G_loc * nJ * 8 <= self.KEY_BYTES or self.G_loc == 0:
+            return None
+        return max(256, (self.KEY_BYTES // (8 * self.G_loc) - s_tilde) // 256 * 256)
+
+    def _streamed_select(self, plan, nJ, s_tilde, chunk, spectra, bins, kmax, det_g, n_det_g, th2):
+        """a8 + a9 + a10 over chunks of J with a per-node top-s~ carry (usfft.h, Z29): the same
+        D_g, votes and theta^2 as the one-shot selection, in O(G_loc (s~ + chunk)) memory."""
+        cfg, ctx, dev, G = self.cfg, self.ctx, self.dev, self.G_loc
+        W = s_tilde + chunk
+        merged = torch.zeros((G, W), dtype=torch.float64, device=dev)
+        carry_k = torch.zeros((G, s_tilde), dtype=torch.float64, device=dev)
+        carry_j = torch.full((G, s_tilde), -1, dtype=torch.int32, device=dev)
+        det_pos = torch.empty((G, s_tilde), dtype=torch.int32, device=dev)
+        scratch = torch.empty(W, dtype=torch.int32, device=dev)
+        for j0 in range(0, nJ, chunk):
+            c = min(chunk, nJ - j0)
+            if c < chunk:
+                merged[:, s_tilde + c:].zero_()                 # ragged last chunk: zero keys
+            B.usfft_lattice_keys(ctx, plan, G, spectra, bins, nJ, c, merged, W, kmax, bins_off=j0,
+                                 kmin_off=s_tilde)
+            B.usfft_detect_select(ctx, G, W, merged, kmax, s_tilde, 0.0, 0.0, scratch, det_pos, n_det_g)
+            B.usfft_detect_carry(ctx, G, s_tilde, W, merged, carry_k, carry_j, det_pos, n_det_g, j0)
+        self.ex.max_(kmax)
+        B.usfft_detect_select(ctx, G, s_tilde, carry_k, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
+                              cfg.get("theta_abs", 0.0), scratch, det_pos, n_det_g, th2)
+        votes = torch.zeros(nJ, dtype=torch.int32, device=dev)
+        B.usfft_detect_carry(ctx, G, s_tilde, s_tilde, carry_k, None, carry_j, det_pos, n_det_g, 0,
+                             det_g, votes)
+        return votes
+
     def step1(self, log: list | None = None) -> list[torch.Tensor]:
         """Step 1 & 2a: I^(t) for t = 1..d as device int16 vectors."""
         cfg, dev = self.cfg, self.dev
@@ -151,6 +196,7 @@ class Detector:
             flags = torch.zeros(kt.numel(), dtype=torch.uint8, device=dev)
             res = None
             for i in range(1, r + 1):
+                res = self.last_round = None                   # free the previous round first
                 res = self.round(1, t, i, empty, 1, kt, cfg["s_local"], flags)
                 if log is not None:
                     log.append(dict(step=1, t=t, i=i, M=res.plan.M, B=res.plan.M, nJ=res.nJ, n_det=res.n_det))
@@ -178,6 +224,7 @@ class Detector:
             flags = torch.zeros(nJ, dtype=torch.uint8, device=dev)
             res = None
             for i in range(1, r_t + 1):
+                res = self.last_round = None                   # free the previous round first
                 res = self.round(2, t, i, I_prev, n_prev, kt, s_t, flags, want_coef=(t == d))
                 if log is not None:
                     log.append(dict(step=2, t=t, i=i, M=res.plan.M, L=res.plan.L,

@@ -20,7 +20,7 @@ sys.path.insert(0, ROOT)
 
 def main():
     ap = argparse.ArgumentParser()
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", default="2", help="BASELINE config 1-5 or an example preset name")
     ap.add_argument("--n-test", type=int, default=10000)
     ap.add_argument("--theta", default="", help="coefficient map override (sin, tent, probit, phi_delta)")
     ap.add_argument("--form", default="", help="coefficient form override (affine, exp)")
@@ -30,7 +30,8 @@ def main():
     from paper_2109_04131_b200.driver import Detector
     from usfft_inputs import config, uniform_points
 
-    cfg = config(args.config)
+    key = int(args.config) if args.config.isdigit() else args.config
+    cfg = config(key)
     if args.theta:
         cfg["theta"] = args.theta
     if args.form:
@@ -46,7 +47,7 @@ def main():
     cov, coef = det.step3(I)
     ev[2].record()
     n_step3 = det.n_samples - n_detect
-    Y = torch.as_tensor(uniform_points(1000 + args.config, cfg["d"], args.n_test), dtype=torch.float64,
+    Y = torch.as_tensor(uniform_points(1000 + (key if isinstance(key, int) else cfg["seed"]), cfg["d"], args.n_test), dtype=torch.float64,
                         device="cuda")
     err, _ = det.errors(I, coef, Y)
     ev[3].record()
@@ -54,7 +55,7 @@ def main():
     wall = time.perf_counter() - t0
     e = err.cpu().numpy()
     out = {
-        "workload": f"config{args.config}:{cfg['name']}", "theta": cfg["theta"], "form": cfg["form"],
+        "workload": (f"config{key}" if isinstance(key, int) else "example") + f":{cfg['name']}", "theta": cfg["theta"], "form": cfg["form"],
         "delta": det.delta, "d": cfg["d"], "n": cfg["n"], "N": cfg["N"],
         "s": cfg["s"], "rounds": len(log), "samples_detection": n_detect, "samples_step3": n_step3,
         "step3_share": n_step3 / (n_detect + n_step3), "nI": int(I.shape[0]), "q": I.shape[0] / cfg["s"],
