@@ -14,7 +14,7 @@ against.  It is NOT part of the product:
 
 Citation convention: ``P:n`` = line n of the paper's PAPER.md (LaTeX source), with the
 section / equation / algorithm it falls in; ``S:n`` = line n of SPEC.md.  Readings of
-places where the paper is silent are labelled Z1..Z28 as in DESIGN.md §3.
+places where the paper is silent are labelled Z1..Z30 as in DESIGN.md §3.
 
 Pin status (what fixes each function besides itself; see tests/test_oracle_*.py):
 
@@ -41,6 +41,9 @@ cover.build_cover      brute-force alias-freeness against the full set; Remark 4
                        count / size bound; singleton
 cover.cover_coeffs     exact recovery of polynomials supported on I; zero samples
 cover.errors           closed forms (constant offset, single spike, complex modulus)
+moments.expectation    E[u(Y)] of known functions of uniform / normal Y through the tent /
+                       phi_Delta periodizations + FFT; half-period Gauss-Legendre integral
+moments.variance/gsi   Parseval; Sobol components by brute-force conditional means (d = 3)
 mode-A detected sets   parity unpinned on PDE data (only trig-polynomial exactness pins
 on PDE samples         the algorithm; PDE-data sets are oracle-vs-GPU only, Z25)
 =====================  ==========================================================
