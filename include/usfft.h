@@ -77,13 +77,13 @@ typedef struct {
  *                 (eq. lognormal_transfo, tau1 P:486, tau2 P:500-506; Z27)
  *   form       0: a = 1 + sum_j amp_j theta_j psi_j(x)   1: a = exp(sum_j amp_j theta_j psi_j(x))
  *   psi        spatial factors psi_j (Z28):
- *              0: sin(j pi x1) sin(j pi x2) (BASELINE configs; periodic example P:1006-1008)
+ *              0: sin(j pi x1) sin(j pi x2) (BASELINE configs; periodic example P:1008)
  *              1: cos(2 pi m1(j) x1) cos(2 pi m2(j) x2), m1/m2/k(j) of Table 3 (affine example
- *                 P:1207-1216)
- *              2: sin(2 pi j x1) cos(2 pi (d+1-j) x2) (lognormal example P:1418-1420)
- *   f_kind     0: f(x) = x2 (BASELINE configs, periodic example P:1001)  1: f = 1 (affine
- *              example P:1203)  2: f = sin(1.3 pi x1 + 3.4 pi x2) cos(4.3 pi x1 - 3.1 pi x2)
- *              (lognormal example P:1414); loads by the centroid rule (Z12)
+ *                 P:1210-1216)
+ *              2: sin(2 pi j x1) cos(2 pi (d+1-j) x2) (lognormal example P:1425)
+ *   f_kind     0: f(x) = x2 (BASELINE configs, periodic example P:1002)  1: f = 1 (affine
+ *              example P:1204)  2: f = sin(1.3 pi x1 + 3.4 pi x2) cos(4.3 pi x1 - 3.1 pi x2)
+ *              (lognormal example P:1419); loads by the centroid rule (Z12)
  *   amp        host fp64 [d]
  *   tol        relative residual target ||r_k||_2 <= tol ||b||_2 (Z13; BASELINE 1e-12)
  *   maxit      PCG iteration cap
@@ -328,6 +328,19 @@ usfft_status usfft_lattice_dft_bins(usfft_ctx *ctx, int64_t M, int64_t G_loc, co
 usfft_status usfft_eval_err(usfft_ctx *ctx, int32_t d, const int16_t *I, int64_t nI,
                             const double *C, int64_t G, const double *Y, int64_t n,
                             const double *Uref, double *err);
+
+/* ---- post-processing: expectation, variance, GSI (usfft_moments) ---------------------------
+ * Per node g (reading Z30), with I dev int16 [nI][d] and C dev fp64x2 [G][nI]:
+ *   E[g] (fp64x2) = sum_k C[g][k] D_k, D_k = prod_j D_{k_j}:
+ *     map 0 (periodic, theta = sin): D_k = 1 for k = 0, else 0 (E = c_0);
+ *     map 1 (tent; eq. affine_ew): D_{k_j} = 2i/(pi k_j) for odd k_j, 1 for 0, else 0;
+ *     map 3 (phi_Delta): the tent factors times e^{2 pi i k_j delta};
+ *   var[g] = sum_{k != 0} |C[g][k]|^2;
+ *   gsi[g][l-1] = sum_{||k||_0 = l} |C[g][k]|^2 / var[g] for l = 1..d (0 where var[g] = 0);
+ * gsi may be NULL.  Other maps (2: clipped Phi^-1) have no closed form: EINVAL.  Fixed-order
+ * reductions (deterministic).  Uses ctx workspace. */
+usfft_status usfft_moments(usfft_ctx *ctx, int32_t d, const int16_t *I, int64_t nI, const double *C,
+                           int64_t G, int32_t map, double delta, double *E, double *var, double *gsi);
 
 #ifdef __cplusplus
 }

@@ -28,7 +28,7 @@ lattice.injective      SPEC examples; brute-force pair check
 fe.assemble/solve      5-point Laplacian stencil for a=1; manufactured solutions O(h^2);
                        SPD + M-matrix (u >= 0); y=0 -> a=1; ellipticity bounds
 fe.psi / diag_index    Table 3 m1/m2/k (golden); affine a_min/a_max 0.1/1.9
-/ f_values (examples)  and c ~ 0.547 (P:1236); lognormal P(|b| <= 3) > 99% (P:1424);
+/ f_values (examples)  and c ~ 0.547 (P:1233); lognormal P(|b| <= 3) > 99% (P:1427);
                        zero sets of psi_j; f = 1 load h^2; product-to-sum identity of f
 fe.tau1/tau2/phi_delta SPEC examples, poles, symmetry, inversion-method distribution
 dft.lattice_dft        orthogonality; exact recovery of trig polynomials on a

@@ -17,7 +17,7 @@ BASELINE configs and the paper's three examples instantiate (Z14/
           | 1 - |2(1 - 2y)|          (tent, eq. tent P:473-479 with alpha=-1, beta=1)
           | clip(Phi^-1(y), -6, 6)   (lognormal config literal reading, Z15)
           | clip(tau1(tau2_Delta(y)), -6, 6)  (lognormal periodization phi_Delta, Z27)
-    f = x2 | 1 | sin(1.3 pi x1 + 3.4 pi x2) cos(4.3 pi x1 - 3.1 pi x2)   (P:1001, P:1203, P:1414)
+    f = x2 | 1 | sin(1.3 pi x1 + 3.4 pi x2) cos(4.3 pi x1 - 3.1 pi x2)   (P:1002, P:1204, P:1419)
 
 Discretisation (Z11, Z12): uniform n x n cells of width h = 1/n, each split
 by its SW->NE diagonal into T_lo = {(i,j),(i+1,j),(i+1,j+1)} and T_up = {(i,j),(i+1,j+1),(i,j+1)};
@@ -81,9 +81,9 @@ def diag_index(j: int):
 
 def psi(model: dict, j: int, x1: np.ndarray, x2: np.ndarray) -> np.ndarray:
     """psi_j(x) / amp_j, the spatial factor of term j (1-based) of the coefficient:
-    "sinsin"      sin(j pi x1) sin(j pi x2)                          (periodic example, P:1006-1008)
-    "cos_diag"    cos(2 pi m_1(j) x1) cos(2 pi m_2(j) x2)            (affine example, P:1207-1209)
-    "sin_cos_rev" sin(2 pi j x1) cos(2 pi (d + 1 - j) x2)            (lognormal example, P:1418-1420)
+    "sinsin"      sin(j pi x1) sin(j pi x2)                          (periodic example, P:1008)
+    "cos_diag"    cos(2 pi m_1(j) x1) cos(2 pi m_2(j) x2)            (affine example, P:1210)
+    "sin_cos_rev" sin(2 pi j x1) cos(2 pi (d + 1 - j) x2)            (lognormal example, P:1425)
     (the factor c j^-mu of the first two and 1/j of the third is amp_j)."""
     kind = model.get("psi", "sinsin")
     x1 = np.asarray(x1, dtype=np.float64)
@@ -218,8 +218,8 @@ def f_values(model: dict, x1: np.ndarray, x2: np.ndarray) -> np.ndarray:
     if kind == "x2":
         return np.asarray(x2, dtype=np.float64).copy()               # BASELINE configs: f = x2
     if kind == "one":
-        return np.ones_like(np.asarray(x1, dtype=np.float64))        # affine example, P:1203
-    if kind == "trig":                                               # lognormal example, P:1414
+        return np.ones_like(np.asarray(x1, dtype=np.float64))        # affine example, P:1204
+    if kind == "trig":                                               # lognormal example, P:1419
         x1 = np.asarray(x1, dtype=np.float64)
         x2 = np.asarray(x2, dtype=np.float64)
         return np.sin(1.3 * np.pi * x1 + 3.4 * np.pi * x2) * np.cos(4.3 * np.pi * x1 - 3.1 * np.pi * x2)

@@ -213,6 +213,19 @@ def usfft_detect_carry(ctx: Context, G_loc: int, s_tilde: int, width: int, merge
     _check(ctx, st, "usfft_detect_carry")
 
 
+MOMENT_MAPS = {"sin": 0, "tent": 1, "phi_delta": 3}
+
+
+def usfft_moments(ctx: Context, I, C, theta: str, delta: float, E, var, gsi=None):
+    """Expectation E [G][2], variance [G] and GSI [G][d] per node (Z30)."""
+    nI, d = (int(I.shape[0]), int(I.shape[1])) if I.dim() == 2 else (0, 1)
+    G = int(C.shape[0])
+    st = ctx.lib.usfft_moments(ctx.h, d, _p(I, torch.int16), nI, _p(C, torch.float64), G,
+                               MOMENT_MAPS[theta], float(delta), _p(E, torch.float64),
+                               _p(var, torch.float64), _p(gsi, torch.float64))
+    _check(ctx, st, "usfft_moments")
+
+
 def usfft_detect_union(ctx: Context, nJ: int, votes, flags, det_idx, union_idx=None):
     """a11; returns (n_det, n_union) (syncs)."""
     nd, nu = C.c_int64(0), C.c_int64(0)

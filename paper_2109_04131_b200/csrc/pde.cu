@@ -44,9 +44,9 @@ __device__ __forceinline__ double theta_of(int kind, double y, double delta) {
 // (the centroid abscissae are (3c+1)h/3, (3c+2)h/3): S[0][j][m] = X_j, S[1][j][m] = Y_j, the
 // second plane only when Y differs from X (psi != 0).  Arguments are exact rationals
 // (integer numerator / 3n) through sinpi / cospi.
-//   psi 0: X_j = Y_j = sin(j pi t)                                   (P:1006-1008)
-//   psi 1: X_j = cos(2 pi m1(j) t), Y_j = cos(2 pi m2(j) t)          (P:1207-1216, Table 3)
-//   psi 2: X_j = sin(2 pi j t), Y_j = cos(2 pi (d+1-j) t)            (P:1418-1420)
+//   psi 0: X_j = Y_j = sin(j pi t)                                   (P:1008)
+//   psi 1: X_j = cos(2 pi m1(j) t), Y_j = cos(2 pi m2(j) t)          (P:1210-1216, Table 3)
+//   psi 2: X_j = sin(2 pi j t), Y_j = cos(2 pi (d+1-j) t)            (P:1425)
 __global__ void k_psitab(int n, int d, int psi, double *__restrict__ S) {
     const int W = 3 * n + 1, planes = psi == 0 ? 1 : 2;
     for (int e = blockIdx.x * blockDim.x + threadIdx.x; e < planes * d * W; e += gridDim.x * blockDim.x) {
@@ -69,9 +69,9 @@ __global__ void k_psitab(int n, int d, int psi, double *__restrict__ S) {
 
 // f at the point (m1 h/3, m2 h/3) for f_kind 1, 2 (Z28)
 __device__ __forceinline__ double f_at(int kind, int n, int m1, int m2) {
-    if (kind == 1) return 1.0;                                   // affine example, P:1203
+    if (kind == 1) return 1.0;                                   // affine example, P:1204
     const double x1 = (double)m1 / (3.0 * n), x2 = (double)m2 / (3.0 * n);
-    return sinpi(1.3 * x1 + 3.4 * x2) * cospi(4.3 * x1 - 3.1 * x2);   // lognormal example, P:1414
+    return sinpi(1.3 * x1 + 3.4 * x2) * cospi(4.3 * x1 - 3.1 * x2);   // lognormal example, P:1419
 }
 
 // centroid-rule loads b_g = sum_{T containing g} f(c_T) |T| / 3 = (h^2 / 6) sum over the six

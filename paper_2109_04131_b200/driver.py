@@ -307,5 +307,17 @@ class Detector:
         return err, U
 
 
+    def moments(self, I_rows: torch.Tensor, coef: torch.Tensor):
+        """Expectation (complex, [G_loc][2]), variance [G_loc] and GSI [G_loc][d] of the
+        approximant on this rank's nodes (Z30) with the D_k weights of the
+        configuration's periodization (sin: none, tent, phi_Delta with this run's Delta)."""
+        G, d, dev = coef.shape[0], self.cfg["d"], self.dev
+        E = torch.empty((G, 2), dtype=torch.float64, device=dev)
+        var = torch.empty(G, dtype=torch.float64, device=dev)
+        gsi = torch.empty((G, d), dtype=torch.float64, device=dev)
+        B.usfft_moments(self.ctx, I_rows, coef, self.cfg["theta"], self.delta, E, var, gsi)
+        return E, var, gsi
+
+
 def to_numpy_rows(I: torch.Tensor) -> np.ndarray:
     return I.to("cpu").numpy().astype(np.int64)

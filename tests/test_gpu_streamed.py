@@ -95,7 +95,7 @@ def test_streamed_round_matches_one_shot(B):
 
 
 def test_example_lognormal_large_union_streams(B):
-    """The lognormal example (P:1412-1426) detects every 1-D frequency and unions to |J| ~ 1e5-1e7
+    """The lognormal example (P:1417-1427) detects every 1-D frequency and unions to |J| ~ 1e5-1e7
     candidates by t = 4 (tools/round_sizes.py); with a small key budget the rounds stream and the
     sets equal the one-shot run's up to t = 3."""
     from paper_2109_04131_b200.driver import Detector

@@ -236,7 +236,7 @@ def test_affine_example_bounds():
 
 
 def test_lognormal_example_b_range():
-    """Lognormal example (P:1424): b(x, y) = sum_j (1/j) y_j psi_j(x) lies in [-3, 3] with
+    """Lognormal example (P:1427): b(x, y) = sum_j (1/j) y_j psi_j(x) lies in [-3, 3] with
     probability > 99% for each x (y ~ N(0, I), d = 10).  b is Gaussian with variance
     sum_j (b_j(x))^2, b_j(x) = log a(x, y = e_j-probit) read through the oracle's own
     coefficient (theta = probit, y_j = Phi(1), others 1/2 -> theta = e_j); the bound must hold at
@@ -260,9 +260,9 @@ def test_lognormal_example_b_range():
 
 
 def test_lognormal_example_psi_and_f():
-    """psi_j = sin(2 pi j x1) cos(2 pi (d+1-j) x2) (P:1418-1420): zero on x1 = 0 and x1 = 1/2,
+    """psi_j = sin(2 pi j x1) cos(2 pi (d+1-j) x2) (P:1425): zero on x1 = 0 and x1 = 1/2,
     separable with its x1 factor vanishing exactly at multiples of 1/(2j), and at x1 = 1/(4j),
-    x2 = 0 equal to 1; f (P:1414) by the product-to-sum identity equals
+    x2 = 0 equal to 1; f (P:1419) by the product-to-sum identity equals
     (sin(5.6 pi x1 + 0.3 pi x2) + sin(-3 pi x1 + 6.5 pi x2)) / 2."""
     m = config("lognormal_example")
     d = m["d"]
@@ -279,7 +279,7 @@ def test_lognormal_example_psi_and_f():
 
 
 def test_constant_load_and_example_solves():
-    """f = 1 (affine example, P:1203): the centroid load is h^2 at every interior node (the six
+    """f = 1 (affine example, P:1204): the centroid load is h^2 at every interior node (the six
     triangles around a node have total area 3 h^2, one third each); every example preset
     assembles to an SPD system (Cholesky succeeds) and solves to round-off; f >= 0 gives u >= 0."""
     for name in ("periodic_mu1.2", "periodic_mu3.6", "affine_example", "lognormal_example"):

@@ -23,7 +23,7 @@ def _coeffs_1d(fun, kind, delta=0.0, npts=1 << 16):
 @pytest.mark.parametrize("fun,want", [(lambda y: y * y, 1.0 / 3.0), (lambda y: y, 0.0),
                                       (np.exp, math.sinh(1.0))])
 def test_tent_expectation_of_uniform(fun, want):
-    """Y uniform on [-1, 1] (affine example, P:1203): E[u(Y)] through the tent periodization and
+    """Y uniform on [-1, 1] (affine example, P:1204): E[u(Y)] through the tent periodization and
     the D_k weights of eq. affine_ew on the FFT coefficients of u o tent."""
     k, c = _coeffs_1d(fun, "tent")
     keep = np.abs(k) <= 4000
@@ -34,7 +34,7 @@ def test_tent_expectation_of_uniform(fun, want):
 @pytest.mark.parametrize("fun,want", [(lambda y: y * y, 1.0), (lambda y: y, 0.0),
                                       (lambda y: np.exp(0.5 * y), math.exp(0.125))])
 def test_phi_delta_expectation_of_normal(fun, want):
-    """Y ~ N(0, 1) (lognormal example, P:1422): E[u(Y)] through phi_Delta and D_{k,Delta}
+    """Y ~ N(0, 1) (lognormal example, P:1427): E[u(Y)] through phi_Delta and D_{k,Delta}
      on the FFT coefficients of u o phi_Delta, for Delta = 1/(4 * 401) (Z27)."""
     delta = fe.global_delta(401)
     k, c = _coeffs_1d(fun, "phi_delta", delta, npts=1 << 18)

@@ -51,6 +51,7 @@ def main():
                         device="cuda")
     err, _ = det.errors(I, coef, Y)
     ev[3].record()
+    Em, var, gsi = det.moments(I, coef) if cfg["theta"] in ("sin", "tent", "phi_delta") else (None, None, None)
     torch.cuda.synchronize()
     wall = time.perf_counter() - t0
     e = err.cpu().numpy()
@@ -65,6 +66,14 @@ def main():
         "err1_max": float(e[:, 0].max()), "err2_max": float(e[:, 1].max()), "errinf_max": float(e[:, 2].max()),
         "err2_mean": float(e[:, 1].mean()),
     }
+    if gsi is not None:                                  # post-processing (Z30)
+        gh = gsi.cpu().numpy()
+        Ih = I.cpu().numpy()
+        nnz = (Ih != 0).sum(1)
+        out.update({"J_l_sizes": [int((nnz == l).sum()) for l in range(1, 5)],
+                    "gsi_J1_min": float(gh[:, 0].min()), "gsi_J1_median": float(np.median(gh[:, 0])),
+                    "gsi_mean_l1_4": [float(v) for v in gh[:, :4].mean(0)],
+                    "E_max": float(Em[:, 0].max()), "E_imag_max": float(Em[:, 1].abs().max())})
     print(json.dumps(out), flush=True)
 
 

@@ -38,17 +38,17 @@ def _amp_mu(c: float, mu: float, d: int, scale: float = 1.0) -> list[float]:
 
 _ETA_I = dict(N=32, s=100, s_local=100, r=5, theta_rel=0.0, theta_abs=1e-12, mode="A")
 EXAMPLES = {
-    # periodic example (P:998-1016): a = 1 + (1/sqrt 6) sum_j sin(2 pi y_j) c j^-mu sin sin, f = x2
+    # periodic example (P:1000-1016): a = 1 + (1/sqrt 6) sum_j sin(2 pi y_j) c j^-mu sin sin, f = x2
     "periodic_mu1.2": dict(name="periodic_mu1.2", n=32, d=10, psi="sinsin", theta="sin", form="affine",
                            f="x2", amp=_amp_mu(0.4, 1.2, 10, 6 ** -0.5), seed=11, **_ETA_I),
     "periodic_mu3.6": dict(name="periodic_mu3.6", n=32, d=10, psi="sinsin", theta="sin", form="affine",
                            f="x2", amp=_amp_mu(1.5, 3.6, 10, 6 ** -0.5), seed=12, **_ETA_I),
-    # affine example (P:1201-1237): y uniform on [-1, 1] through the tent map, c = 0.9 / zeta(2),
+    # affine example (P:1202-1233): y uniform on [-1, 1] through the tent map, c = 0.9 / zeta(2),
     # mu = 2, psi_j = c j^-2 cos(2 pi m1(j) x1) cos(2 pi m2(j) x2), f = 1, d = 20
     "affine_example": dict(name="affine_example", n=32, d=20, psi="cos_diag", theta="tent", form="affine",
                            f="one", amp=_amp_mu(0.9 * 6.0 / 3.141592653589793 ** 2, 2.0, 20), seed=13,
                            **_ETA_I),
-    # lognormal example (P:1412-1426): a = exp(sum_j (1/j) y_j sin(2 pi j x1) cos(2 pi (d+1-j) x2)),
+    # lognormal example (P:1417-1427): a = exp(sum_j (1/j) y_j sin(2 pi j x1) cos(2 pi (d+1-j) x2)),
     # y ~ N(0, I) through phi_Delta (Z27), f = sin(1.3 pi x1 + 3.4 pi x2) cos(4.3 pi x1 - 3.1 pi x2)
     "lognormal_example": dict(name="lognormal_example", n=32, d=10, psi="sin_cos_rev", theta="phi_delta",
                               form="exp", f="trig", amp=_amp_mu(1.0, 1.0, 10), seed=14, **_ETA_I),
