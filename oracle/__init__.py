@@ -14,7 +14,7 @@ against.  It is NOT part of the product:
 
 Citation convention: ``P:n`` = line n of the paper's PAPER.md (LaTeX source), with the
 section / equation / algorithm it falls in; ``S:n`` = line n of SPEC.md.  Readings of
-places where the paper is silent are labelled Z1..Z30 as in DESIGN.md §3.
+places where the paper is silent are labelled Z1..Z31 as in DESIGN.md §3.
 
 Pin status (what fixes each function besides itself; see tests/test_oracle_*.py):
 
@@ -44,6 +44,8 @@ cover.errors           closed forms (constant offset, single spike, complex modu
 moments.expectation    E[u(Y)] of known functions of uniform / normal Y through the tent /
                        phi_Delta periodizations + FFT; half-period Gauss-Legendre integral
 moments.variance/gsi   Parseval; Sobol components by brute-force conditional means (d = 3)
+index_sets.brute_force the set definitions of P:1630-1638 as a filter of the box (itself
+                       the pin of the package's budgeted enumeration)
 mode-A detected sets   parity unpinned on PDE data (only trig-polynomial exactness pins
 on PDE samples         the algorithm; PDE-data sets are oracle-vs-GPU only, Z25)
 =====================  ==========================================================
