@@ -182,6 +182,55 @@ k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t
     }
 }
 
+// Keys with the bins tile shared by a group of nodes: CTA (candidate tile, node group) stages the
+// tile's L bins rows once (coalesced) and then, node by node, gathers the node's L spectrum values
+// per candidate straight from L1/L2 (L independent loads in flight per thread).  The bins are read
+// G/KG_NODES times instead of G times, and no per-node spectrum staging sits on the critical path.
+constexpr int KG_NODES = 8;
+
+__global__ void __launch_bounds__(256)
+k_kappa_grouped(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t ldb, int64_t nJ,
+                int64_t M, int32_t L, int64_t G, double *__restrict__ kmin, int64_t ldk,
+                unsigned long long *__restrict__ kmax) {
+    extern __shared__ int32_t sbins[];                 // [L][256]
+    __shared__ unsigned long long wmax[8];
+    const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
+    const int64_t g0 = (int64_t)blockIdx.y * KG_NODES;
+    const int64_t Mh = M / 2 + 1;
+    const double inv_m = 1.0 / (double)M;
+#pragma unroll 4
+    for (int l = 0; l < L; ++l) sbins[l * 256 + threadIdx.x] = j < nJ ? __ldg(bins + (int64_t)l * ldb + j) : 0;
+    __syncthreads();
+    unsigned long long best = 0ull;
+    if (j < nJ) {
+        for (int q = 0; q < KG_NODES && g0 + q < G; ++q) {
+            const double2 *src = F + (g0 + q) * L * Mh;
+            double km = 0.0;
+#pragma unroll 8
+            for (int l = 0; l < L; ++l) {
+                const int b = sbins[l * 256 + threadIdx.x];
+                const double2 f = __ldg(src + l * Mh + (b < (int)Mh ? b : (int)M - b));
+                const double re = f.x * inv_m, im = f.y * inv_m;
+                const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+                km = (l == 0) ? k : fmin(km, k);
+            }
+            kmin[(g0 + q) * ldk + j] = km;
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
+            best = bits > best ? bits : best;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other > best ? other : best;
+    }
+    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = best;
+    __syncthreads();
+    if (threadIdx.x == 0) {
+        for (int w = 1; w < 8; ++w) best = wmax[w] > best ? wmax[w] : best;
+        atomicMax(kmax, best);
+    }
+}
+
 }  // namespace usfft
 
 #include "rader.cuh"
@@ -356,6 +405,17 @@ usfft_status launch_keys(usfft_ctx *c, int64_t M, int32_t L, int64_t G_loc, cons
     if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
     const size_t st_bytes = sizeof(double2) * (size_t)L * (size_t)(M / 2 + 1);
     const size_t tile_bytes = sizeof(int32_t) * 256 * (size_t)L;
+    const char *kv = getenv("USFFT_KEYS");              // =staged: one CTA per node (previous kernel)
+    if (!(kv && kv[0] == 's')) {
+        USFFT_REQUIRE(c, tile_bytes <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
+        USFFT_REQUIRE(c, (G_loc + KG_NODES - 1) / KG_NODES <= 65535, "too many nodes for the key grid");
+        if (usfft_status s2 = kernel_fit(c, k_kappa_grouped, 0, tile_bytes, nullptr)) return s2;
+        dim3 grid((unsigned)((nJ + 255) / 256), (unsigned)((G_loc + KG_NODES - 1) / KG_NODES));
+        k_kappa_grouped<<<grid, 256, tile_bytes, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb,
+                                                              nJ, M, L, G_loc, kappa_min, ldk, km);
+        USFFT_CHECK_LAUNCH(c);
+        return USFFT_OK;
+    }
     const int staged = st_bytes + tile_bytes <= 112 * 1024 ? 1 : 0;
     const size_t dyn = (staged ? st_bytes : 0) + tile_bytes;
     USFFT_REQUIRE(c, dyn <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);

@@ -204,6 +204,28 @@ def test_lattice_fft_parity(B, ctx, G, M, L, nJ):
     assert torch.equal(sp2, spectra[gb[r]:gb[r + 1]]) and torch.equal(km2, kmin[gb[r]:gb[r + 1]])
 
 
+@pytest.mark.parametrize("G,M,L,nJ", [(19, 401, 17, 1000), (9, 97, 11, 300), (4, 2017, 3, 70)])
+def test_key_kernels_agree(B, ctx, monkeypatch, G, M, L, nJ):
+    """The grouped key kernel (bins tile shared by 8 nodes, default) and the per-node staged one
+    (USFFT_KEYS=staged) give bit-identical keys and kappa_max; G not a multiple of 8."""
+    from paper_2109_04131_b200.binding import Plan
+    U, z, J, bins = _round_inputs(G * M, G, M, L, nJ)
+    p = Plan(3, M, L, 3, -1, z, np.zeros(3))
+    Mh = M // 2 + 1
+    out = []
+    for mode in (None, "staged"):
+        if mode:
+            monkeypatch.setenv("USFFT_KEYS", mode)
+        spectra = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
+        kmin = torch.empty((G, nJ), dtype=torch.float64, device="cuda")
+        kmax = torch.empty(1, dtype=torch.float64, device="cuda")
+        B.usfft_lattice_fft(ctx, p, G, dev(U, torch.float64), [0, L * M], dev(bins, torch.int32), nJ, spectra,
+                            kmin, kmax)
+        out.append((kmin, kmax))
+    monkeypatch.delenv("USFFT_KEYS")
+    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+
+
 # ------------------------------------------------------------------------------ a9-a11 selection
 @pytest.mark.parametrize("G,nJ,s", [(5, 1000, 7), (17, 4097, 100), (3, 9, 20), (4, 600, 600), (2, 1, 1)])
 def test_select_union_bitexact(B, ctx, G, nJ, s):
