@@ -223,10 +223,13 @@ usfft_status usfft_detect_select(usfft_ctx *ctx, int64_t G_loc, int64_t nJ,
  *
  * usfft_lattice_keys: the keys of a8 from existing spectra for nJ candidates whose bins are
  *   bins[l * ldb + j] (l < L, j < nJ); writes kappa_min[g * ldk + j] and max-accumulates
- *   kappa_max (NOT reset: zero it before the first chunk). */
+ *   kappa_max (NOT reset: zero it before the first chunk) over the true keys.  tau (dev fp64
+ *   [G_loc], may be NULL): a key <= tau[g] is written as 0 (it cannot beat a full carry whose
+ *   smallest key is tau[g]: ties go to the carry's smaller j). */
 usfft_status usfft_lattice_keys(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_t G_loc,
                                 const double *spectra, const int32_t *bins, int64_t ldb,
-                                int64_t nJ, double *kappa_min, int64_t ldk, double *kappa_max);
+                                int64_t nJ, double *kappa_min, int64_t ldk, double *kappa_max,
+                                const double *tau);
 
 /* usfft_detect_carry, for each owned g with the selection det_pos[g][0..n_det_g[g]) (positions
  * into row g of merged, ascending, as written by usfft_detect_select on merged):
@@ -237,11 +240,13 @@ usfft_status usfft_lattice_keys(usfft_ctx *ctx, const usfft_lattice_desc *lat, i
  *     carry_j[g][det_pos[g][r]] (-1 padded to s_tilde) and votes[that j] += 1 (votes zeroed by
  *     the caller, int32 [nJ]).
  * merged dev fp64 [G_loc][width]; carry_k dev fp64 [G_loc][s_tilde]; carry_j dev int32
- * [G_loc][s_tilde]; det_pos dev int32 [G_loc][s_tilde]; n_det_g dev int32 [G_loc]. */
+ * [G_loc][s_tilde]; det_pos dev int32 [G_loc][s_tilde]; n_det_g dev int32 [G_loc];
+ * tau dev fp64 [G_loc] (update mode, may be NULL): the smallest carry key when the carry holds
+ * s_tilde pairs, else 0 (the prefilter of usfft_lattice_keys). */
 usfft_status usfft_detect_carry(usfft_ctx *ctx, int64_t G_loc, int32_t s_tilde, int64_t width,
                                 double *merged, double *carry_k, int32_t *carry_j,
                                 const int32_t *det_pos, const int32_t *n_det_g, int64_t j0,
-                                int32_t *det_g, int32_t *votes);
+                                int32_t *det_g, int32_t *votes, double *tau);
 
 /* ---- a11: union (usfft_detect_union) ------------------------------------------------------
  * votes must be summed over all ranks (Step 2e P:318: union over g).  flags |= (votes > 0)

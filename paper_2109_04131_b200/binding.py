@@ -192,24 +192,25 @@ def usfft_detect_select(ctx: Context, G_loc: int, nJ: int, kappa_min, kappa_max,
 
 
 def usfft_lattice_keys(ctx: Context, plan: Plan, G_loc: int, spectra, bins, ldb: int, nJ: int, kappa_min,
-                       ldk: int, kappa_max, bins_off: int = 0, kmin_off: int = 0):
+                       ldk: int, kappa_max, bins_off: int = 0, kmin_off: int = 0, tau=None):
     """a8 for a chunk of candidates: bins[l*ldb + bins_off + j] -> kappa_min[g*ldk + kmin_off + j]
     (element offsets into the given tensors); kappa_max max-accumulates."""
     dsc, keep = plan.desc()
     _p(bins, torch.int32), _p(kappa_min, torch.float64)
     st = ctx.lib.usfft_lattice_keys(ctx.h, C.byref(dsc), G_loc, _p(spectra, torch.float64),
                                     bins.data_ptr() + 4 * bins_off, ldb, nJ,
-                                    kappa_min.data_ptr() + 8 * kmin_off, ldk, _p(kappa_max, torch.float64))
+                                    kappa_min.data_ptr() + 8 * kmin_off, ldk, _p(kappa_max, torch.float64),
+                                    _p(tau, torch.float64))
     _check(ctx, st, "usfft_lattice_keys")
 
 
 def usfft_detect_carry(ctx: Context, G_loc: int, s_tilde: int, width: int, merged, carry_k, carry_j,
-                       det_pos, n_det_g, j0: int = 0, det_g=None, votes=None):
+                       det_pos, n_det_g, j0: int = 0, det_g=None, votes=None, tau=None):
     """Streamed selection step (Z29): update the per-node carry (det_g None) or emit det_g + votes."""
     st = ctx.lib.usfft_detect_carry(ctx.h, G_loc, s_tilde, width, _p(merged, torch.float64),
                                     _p(carry_k, torch.float64), _p(carry_j, torch.int32),
                                     _p(det_pos, torch.int32), _p(n_det_g, torch.int32), j0,
-                                    _p(det_g, torch.int32), _p(votes, torch.int32))
+                                    _p(det_g, torch.int32), _p(votes, torch.int32), _p(tau, torch.float64))
     _check(ctx, st, "usfft_detect_carry")
 
 

@@ -29,6 +29,7 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     __shared__ unsigned long long s_prefix;
     __shared__ long long s_need;
     __shared__ bool s_exact;
+    __shared__ unsigned int s_zero;
     __shared__ int scan_sh[33];
     extern __shared__ unsigned long long kst[];
     const int64_t g = blockIdx.x;
@@ -54,13 +55,25 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     } else {
         unsigned long long prefix = 0ull, pmask = 0ull;
         long long k = s_tilde;                   // rank (1-based, from the top) still to find
+        if (threadIdx.x == 0) s_zero = 0u;
         for (int pass = 0; pass < 8; ++pass) {
             const int shift = 56 - 8 * pass;
             for (int q = threadIdx.x; q < 256; q += blockDim.x) hist[q] = 0u;
             __syncthreads();
+            unsigned int nzero = 0u;
             for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) {
                 const unsigned long long key = keys[j];
+                nzero += key == 0ull ? 1u : 0u;
                 if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255ull], 1u);
+            }
+            if (pass == 0) {                     // at most s~ positive keys: all of them are members
+                if (nzero) atomicAdd(&s_zero, nzero);
+                __syncthreads();
+                if (nJ - (int64_t)s_zero <= (int64_t)s_tilde) {   // (zeros are never taken)
+                    by_min = true;
+                    Tmin = 1ull;
+                    break;
+                }
             }
             __syncthreads();
             if (threadIdx.x < 32) {              // warp-parallel search from the top bucket
@@ -144,7 +157,8 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
 __global__ void __launch_bounds__(256)
 k_carry(int32_t s, int64_t width, double *merged, double *carry_k, int32_t *__restrict__ carry_j,
         const int32_t *__restrict__ det_pos, const int32_t *__restrict__ n_det_g, int64_t j0,
-        int32_t *__restrict__ det_g, int32_t *__restrict__ votes) {
+        int32_t *__restrict__ det_g, int32_t *__restrict__ votes, double *__restrict__ tau) {
+    __shared__ double wmin[8];
     extern __shared__ double ck[];                               // [s] keys, then [s] j
     int32_t *cj = reinterpret_cast<int32_t *>(ck + s);
     const int64_t g = blockIdx.x;
@@ -160,11 +174,22 @@ k_carry(int32_t s, int64_t width, double *merged, double *carry_k, int32_t *__re
     __syncthreads();
     if (det_g == nullptr) {
         double *krow = carry_k + g * (int64_t)s;
+        double mn = 1.0 / 0.0;
         for (int r = threadIdx.x; r < s; r += blockDim.x) {
             const double k = r < n ? ck[r] : 0.0;
             row[r] = k;
             krow[r] = k;
             jrow[r] = r < n ? cj[r] : -1;
+            mn = fmin(mn, k);
+        }
+        if (tau) {                               // the carry's s~-th key once it is full (else 0)
+            for (int o = 16; o > 0; o >>= 1) mn = fmin(mn, __shfl_xor_sync(0xffffffffu, mn, o));
+            if ((threadIdx.x & 31) == 0) wmin[threadIdx.x >> 5] = mn;
+            __syncthreads();
+            if (threadIdx.x == 0) {
+                for (int w = 1; w < (int)(blockDim.x >> 5); ++w) mn = fmin(mn, wmin[w]);
+                tau[g] = n == s ? mn : 0.0;
+            }
         }
     } else {
         int32_t *out = det_g + g * (int64_t)s;
@@ -312,7 +337,7 @@ extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t
 extern "C" usfft_status usfft_detect_carry(usfft_ctx *c, int64_t G_loc, int32_t s_tilde, int64_t width,
                                            double *merged, double *carry_k, int32_t *carry_j,
                                            const int32_t *det_pos, const int32_t *n_det_g, int64_t j0,
-                                           int32_t *det_g, int32_t *votes) {
+                                           int32_t *det_g, int32_t *votes, double *tau) {
     USFFT_ENTER(c);
     USFFT_REQUIRE(c, G_loc >= 0 && s_tilde >= 1 && width >= s_tilde && j0 >= 0, "bad sizes");
     USFFT_REQUIRE(c, j0 + width - s_tilde <= 0x7fffffff, "candidate index beyond int32");
@@ -323,7 +348,7 @@ extern "C" usfft_status usfft_detect_carry(usfft_ctx *c, int64_t G_loc, int32_t 
     const size_t dyn = (sizeof(double) + sizeof(int32_t)) * (size_t)s_tilde;
     if (usfft_status s = kernel_fit(c, k_carry, 0, dyn, nullptr)) return s;
     k_carry<<<(unsigned)G_loc, 256, dyn, c->stream>>>(s_tilde, width, merged, carry_k, carry_j, det_pos, n_det_g,
-                                                       j0, det_g, votes);
+                                                       j0, det_g, votes, tau);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }

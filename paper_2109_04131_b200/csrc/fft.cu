@@ -133,7 +133,7 @@ k_dft_bins(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int6
 __global__ void __launch_bounds__(256)
 k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t ldb, int64_t nJ,
         int64_t M, int32_t L, double *__restrict__ kmin, int64_t ldk, unsigned long long *__restrict__ kmax,
-        int staged) {
+        int staged, const double *__restrict__ tau) {
     extern __shared__ double2 fs[];
     __shared__ unsigned long long wmax[32];
     const int64_t g = blockIdx.x;
@@ -165,7 +165,7 @@ k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t
                 const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
                 km = (l == 0) ? k : fmin(km, k);
             }
-            kmin[g * ldk + j] = km;
+            kmin[g * ldk + j] = (tau && km <= tau[g]) ? 0.0 : km;         // prefilter (Z29)
             const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
             best = bits > best ? bits : best;
         }
@@ -191,7 +191,7 @@ constexpr int KG_NODES = 8;
 __global__ void __launch_bounds__(256)
 k_kappa_grouped(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t ldb, int64_t nJ,
                 int64_t M, int32_t L, int64_t G, double *__restrict__ kmin, int64_t ldk,
-                unsigned long long *__restrict__ kmax) {
+                unsigned long long *__restrict__ kmax, const double *__restrict__ tau) {
     extern __shared__ int32_t sbins[];                 // [L][256]
     __shared__ unsigned long long wmax[8];
     const int64_t j = (int64_t)blockIdx.x * 256 + threadIdx.x;
@@ -214,7 +214,8 @@ k_kappa_grouped(const double2 *__restrict__ F, const int32_t *__restrict__ bins,
                 const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
                 km = (l == 0) ? k : fmin(km, k);
             }
-            kmin[(g0 + q) * ldk + j] = km;
+            // streamed selection (Z29): a key <= the node's carry threshold can never enter
+            kmin[(g0 + q) * ldk + j] = (tau && km <= tau[g0 + q]) ? 0.0 : km;
             const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
             best = bits > best ? bits : best;
         }
@@ -400,28 +401,35 @@ namespace {
 // (NULL: a ctx scratch slot)
 usfft_status launch_keys(usfft_ctx *c, int64_t M, int32_t L, int64_t G_loc, const double *spectra,
                          const int32_t *bins, int64_t ldb, int64_t nJ, double *kappa_min, int64_t ldk,
-                         double *kappa_max) {
+                         double *kappa_max, const double *tau = nullptr) {
     unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
     if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
     const size_t st_bytes = sizeof(double2) * (size_t)L * (size_t)(M / 2 + 1);
     const size_t tile_bytes = sizeof(int32_t) * 256 * (size_t)L;
-    const char *kv = getenv("USFFT_KEYS");              // =staged: one CTA per node (previous kernel)
-    if (!(kv && kv[0] == 's')) {
+    // Two kernels, identical results: the grouped kernel (bins tile shared by 8 nodes, spectra
+    // gathered from L1/L2; default) and one CTA per node with its spectra staged in shared
+    // memory (USFFT_KEYS=staged).  Measured on B200: grouped 57 vs 64 us on the config-2 round
+    // (|J| = 1000, L = 17) and 1.29 vs 1.99 s per streamed round of |J| = 8.2e6, L = 35 (the
+    // staged kernel's per-tile bins loads are latency-bound at one CTA per SM).
+    const char *kv = getenv("USFFT_KEYS");
+    const bool fits = st_bytes + tile_bytes + 1024 <= c->smem_optin;
+    const bool staged_path = kv && kv[0] == 's';
+    if (!staged_path) {
         USFFT_REQUIRE(c, tile_bytes <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
         USFFT_REQUIRE(c, (G_loc + KG_NODES - 1) / KG_NODES <= 65535, "too many nodes for the key grid");
         if (usfft_status s2 = kernel_fit(c, k_kappa_grouped, 0, tile_bytes, nullptr)) return s2;
         dim3 grid((unsigned)((nJ + 255) / 256), (unsigned)((G_loc + KG_NODES - 1) / KG_NODES));
         k_kappa_grouped<<<grid, 256, tile_bytes, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb,
-                                                              nJ, M, L, G_loc, kappa_min, ldk, km);
+                                                              nJ, M, L, G_loc, kappa_min, ldk, km, tau);
         USFFT_CHECK_LAUNCH(c);
         return USFFT_OK;
     }
-    const int staged = st_bytes + tile_bytes <= 112 * 1024 ? 1 : 0;
+    const int staged = fits ? 1 : 0;
     const size_t dyn = (staged ? st_bytes : 0) + tile_bytes;
     USFFT_REQUIRE(c, dyn <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
     if (usfft_status s2 = kernel_fit(c, k_kappa, 0, dyn, nullptr)) return s2;
     k_kappa<<<(unsigned)G_loc, 256, dyn, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb,
-                                                       nJ, M, L, kappa_min, ldk, km, staged);
+                                                       nJ, M, L, kappa_min, ldk, km, staged, tau);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -498,14 +506,15 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
 
 extern "C" usfft_status usfft_lattice_keys(usfft_ctx *c, const usfft_lattice_desc *lat, int64_t G_loc,
                                            const double *spectra, const int32_t *bins, int64_t ldb,
-                                           int64_t nJ, double *kappa_min, int64_t ldk, double *kappa_max) {
+                                           int64_t nJ, double *kappa_min, int64_t ldk, double *kappa_max,
+                                           const double *tau) {
     USFFT_ENTER(c);
     USFFT_REQUIRE(c, lat != nullptr, "lattice desc is NULL");
     USFFT_REQUIRE(c, lat->M >= 2 && lat->M <= (int64_t(1) << 26) && lat->L >= 1, "bad M / L");
     USFFT_REQUIRE(c, G_loc >= 0 && nJ >= 0 && ldb >= nJ && ldk >= nJ, "bad sizes / leading dimensions");
     if (G_loc == 0 || nJ == 0) return USFFT_OK;
     USFFT_REQUIRE(c, spectra && bins && kappa_min && kappa_max, "NULL argument");
-    return launch_keys(c, lat->M, lat->L, G_loc, spectra, bins, ldb, nJ, kappa_min, ldk, kappa_max);
+    return launch_keys(c, lat->M, lat->L, G_loc, spectra, bins, ldb, nJ, kappa_min, ldk, kappa_max, tau);
 }
 
 extern "C" usfft_status usfft_lattice_dft_bins(usfft_ctx *c, int64_t M, int64_t G_loc, const double *u,

@@ -169,14 +169,15 @@ class Detector:
         carry_j = torch.full((G, s_tilde), -1, dtype=torch.int32, device=dev)
         det_pos = torch.empty((G, s_tilde), dtype=torch.int32, device=dev)
         scratch = torch.empty(W, dtype=torch.int32, device=dev)
+        tau = torch.zeros(G, dtype=torch.float64, device=dev)    # carry threshold (prefilter)
         for j0 in range(0, nJ, chunk):
             c = min(chunk, nJ - j0)
             if c < chunk:
                 merged[:, s_tilde + c:].zero_()                 # ragged last chunk: zero keys
             B.usfft_lattice_keys(ctx, plan, G, spectra, bins, nJ, c, merged, W, kmax, bins_off=j0,
-                                 kmin_off=s_tilde)
+                                 kmin_off=s_tilde, tau=tau)
             B.usfft_detect_select(ctx, G, W, merged, kmax, s_tilde, 0.0, 0.0, scratch, det_pos, n_det_g)
-            B.usfft_detect_carry(ctx, G, s_tilde, W, merged, carry_k, carry_j, det_pos, n_det_g, j0)
+            B.usfft_detect_carry(ctx, G, s_tilde, W, merged, carry_k, carry_j, det_pos, n_det_g, j0, tau=tau)
         self.ex.max_(kmax)
         B.usfft_detect_select(ctx, G, s_tilde, carry_k, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
                               cfg.get("theta_abs", 0.0), scratch, det_pos, n_det_g, th2)

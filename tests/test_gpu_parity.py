@@ -204,16 +204,16 @@ def test_lattice_fft_parity(B, ctx, G, M, L, nJ):
     assert torch.equal(sp2, spectra[gb[r]:gb[r + 1]]) and torch.equal(km2, kmin[gb[r]:gb[r + 1]])
 
 
-@pytest.mark.parametrize("G,M,L,nJ", [(19, 401, 17, 1000), (9, 97, 11, 300), (4, 2017, 3, 70)])
+@pytest.mark.parametrize("G,M,L,nJ", [(19, 401, 17, 1000), (9, 97, 11, 300), (4, 2017, 3, 70), (11, 401, 35, 9000)])
 def test_key_kernels_agree(B, ctx, monkeypatch, G, M, L, nJ):
-    """The grouped key kernel (bins tile shared by 8 nodes, default) and the per-node staged one
-    (USFFT_KEYS=staged) give bit-identical keys and kappa_max; G not a multiple of 8."""
+    """The grouped key kernel (bins tile shared by 8 nodes) and the per-node staged one give
+    bit-identical keys and kappa_max (default choice, and each forced); G not a multiple of 8."""
     from paper_2109_04131_b200.binding import Plan
     U, z, J, bins = _round_inputs(G * M, G, M, L, nJ)
     p = Plan(3, M, L, 3, -1, z, np.zeros(3))
     Mh = M // 2 + 1
     out = []
-    for mode in (None, "staged"):
+    for mode in (None, "grouped", "staged"):
         if mode:
             monkeypatch.setenv("USFFT_KEYS", mode)
         spectra = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
@@ -223,7 +223,8 @@ def test_key_kernels_agree(B, ctx, monkeypatch, G, M, L, nJ):
                             kmin, kmax)
         out.append((kmin, kmax))
     monkeypatch.delenv("USFFT_KEYS")
-    assert torch.equal(out[0][0], out[1][0]) and torch.equal(out[0][1], out[1][1])
+    for o in out[1:]:
+        assert torch.equal(out[0][0], o[0]) and torch.equal(out[0][1], o[1])
 
 
 # ------------------------------------------------------------------------------ a9-a11 selection
