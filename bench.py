@@ -39,6 +39,21 @@ def mg_flops_per_iter(n: int) -> int:
     K (2 U2^2).  The per-sample setup (coefficients, operators, K) is not counted."""
     u0, u1, u2 = (n - 1) ** 2, (n // 2 - 1) ** 2, (n // 4 - 1) ** 2
     return 51 * u0 + 38 * u1 + 10 * u2 + 2 * u2 * u2
+
+
+def mgg_flops_per_iter(n: int) -> int:
+    """Algorithmic flops of one CG iteration of the scratch-slab multigrid kernel (k_pcg_mgg, n =
+    64, 128), phase by phase: per fine node 47 (p update 2, A p + p.q 11, x / r /
+    z0 updates + r.r 7, residual 10, prolongation 3, post-smoothing 12, r.u 2); per node of a
+    smoothed coarse level 37 (residual 10, restriction 12, prolongation 3, post-smoothing 12);
+    restriction to the 3 x 3 exact level 12 per node and its dense solve 2 * 81."""
+    L = 0
+    while (n >> L) > 4:
+        L += 1
+    u = [((n >> l) - 1) ** 2 for l in range(L + 1)]
+    return 47 * u[0] + sum(37 * u[l] for l in range(1, L)) + 12 * u[L] + 2 * 81
+
+
 FP64_FMA_PER_CLK_PER_SM = 64  # B200 fp64 datapath (DESIGN.md §5): 37 TF at 1.965 GHz x 148 SMs
 
 
@@ -201,9 +216,15 @@ def run_ours(args):
     # buffers, no per-phase event timing inside the round
     Ih = I_prev.cpu().pin_memory()
     kh = kt.cpu().pin_memory()
-    out_idx_h = torch.empty(nJ, dtype=torch.int32).pin_memory()
-    out_coef_h = torch.empty(det.G_loc * nJ * 2, dtype=torch.float64).pin_memory()
     det.timing = False
+    # output buffers sized by an untimed pass over the same rounds (|D| differs per round; a
+    # G_loc x |J| worst case does not fit pinned host memory at configs 4-5)
+    nd_max = 1
+    for k in range(args.steps):
+        flags = torch.zeros(nJ, dtype=torch.uint8, device="cuda")
+        nd_max = max(nd_max, det.round(2, t_b, 5000 + k, I_prev, n_prev, kt, s_t, flags, want_coef=True).n_det)
+    out_idx_h = torch.empty(nd_max, dtype=torch.int32).pin_memory()
+    out_coef_h = torch.empty(det.G_loc * nd_max * 2, dtype=torch.float64).pin_memory()
     e2e_ms, h2d, d2h = [], 0, 0
     for k in range(args.steps):
         flush.fill_(float(k))
@@ -240,9 +261,12 @@ def run_ours(args):
         from paper_2109_04131_b200.binding import effective_precond
         mg = effective_precond(cfg) == "mg"
         n_mesh = cfg["n"]
-        if mg:
+        if mg and n_mesh in (16, 32):
             kname, kdesc = "k_pcg_mg", "k_pcg_mg (batched multigrid-preconditioned CG, on-chip, 1 CTA/sample)"
             fpi = mg_flops_per_iter(n_mesh)
+        elif mg:
+            kname, kdesc = "k_pcg_mgg", "k_pcg_mgg (batched multigrid-preconditioned CG, scratch slab, 1 CTA/sample)"
+            fpi = mgg_flops_per_iter(n_mesh)
         else:
             kname, kdesc = "k_pcg_reg", "k_pcg_reg (batched Jacobi PCG, register-resident, 1 CTA/sample)"
             fpi = FLOPS_PER_NODE_ITER * G

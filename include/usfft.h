@@ -88,8 +88,8 @@ typedef struct {
  *   tol        relative residual target ||r_k||_2 <= tol ||b||_2 (Z13; BASELINE 1e-12)
  *   maxit      PCG iteration cap
  *   precond    0: Jacobi (diagonal) PCG;  1: geometric-multigrid V(1,1) preconditioned CG
- *              (damped-Jacobi smoothing, bilinear P, R = P^T, rediscretised coarse meshes;
- *              implemented for n = 16, 32 -> USFFT_EUNIMPL otherwise).  Any solver is admissible
+ *              (damped-Jacobi smoothing, bilinear P, R = P^T, rediscretised coarse meshes down
+ *              to 4 cells per side; n a power of two >= 8 -> USFFT_EUNIMPL otherwise).  Any solver is admissible
  *              for the black box; both are CG with an SPD preconditioner (Z13).
  *   delta      the pole shift Delta of theta = 3, in (0, 1/2): one global value per run
  *              (Z27: 1/(4 M0), M0 the Step-2 lattice size, Lemma P:847-870); ignored otherwise

@@ -130,13 +130,16 @@ def usfft_lattice(ctx: Context, plan: Plan, b0: int, nb: int, nodes=None, I_prev
     return [int(v) for v in inj] if injective else None
 
 
-MG_MESHES = (16, 32)      # meshes with a compiled multigrid-preconditioned CG kernel
+def mg_mesh(n: int) -> bool:
+    """Meshes with a multigrid-preconditioned CG kernel: n = 16, 32 (register-resident fine level)
+    and every other power of two >= 8 (scratch-slab kernel, n = 64, 128)."""
+    return n >= 8 and n & (n - 1) == 0
 
 
 def effective_precond(cfg: dict, precond: str | None = None) -> str:
     """The preconditioner a solve uses: the explicit choice, else cfg["precond"], else multigrid
-    where it is compiled (n = 16, 32: fastest measured) and Jacobi otherwise."""
-    return precond or cfg.get("precond") or ("mg" if cfg["n"] in MG_MESHES else "jacobi")
+    where it exists (fastest measured) and Jacobi otherwise."""
+    return precond or cfg.get("precond") or ("mg" if mg_mesh(cfg["n"]) else "jacobi")
 
 
 def pde_desc(cfg: dict, maxit: int = 20000, tol: float = 1e-12, precond: str | None = None,

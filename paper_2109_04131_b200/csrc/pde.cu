@@ -227,6 +227,7 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
 
 #include "pcg_reg.cuh"
 #include "pcg_mg.cuh"
+#include "pcg_mgg.cuh"
 
 using namespace usfft;
 
@@ -247,6 +248,25 @@ usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
     if (grid > nb) grid = nb;
     kern<<<(unsigned)grid, NWARP * 32, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
                                                          noconv, S, Bt);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
+usfft_status launch_pcg_mgg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
+                            int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
+                            int32_t *noconv, const double *S, const double *Bt) {
+    constexpr int T = 512;
+    const MggLayout Y = MggLayout::make(Q.n, 12288);           // coarse levels in <= 96 KB of smem
+    const size_t dyn = sizeof(double) * (size_t)Y.smem;
+    auto kern = k_pcg_mgg<T>;
+    int per_sm = 0;
+    if (usfft_status s = kernel_fit(c, kern, T, dyn, &per_sm)) return s;
+    if (per_sm < 1) per_sm = 1;
+    int64_t grid = (int64_t)per_sm * c->sm_count;
+    if (grid > nb) grid = nb;
+    if (usfft_status s = ensure(c, &c->ws, &c->ws_size, sizeof(double) * (size_t)grid * (size_t)Y.region)) return s;
+    kern<<<(unsigned)grid, T, dyn, c->stream>>>(P, Q, Y, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt,
+                                              static_cast<double *>(c->ws));
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -379,7 +399,10 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     const char *force = getenv("USFFT_PCG");
     const bool reg_ok = !(force && force[0] == 's');
     const char *mgl = getenv("USFFT_MG_LAYOUT");
-    if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '2')        // 256 threads, 2x2 blocks
+    const char *mgg = getenv("USFFT_MGG");              // =1: the scratch-slab multigrid kernel at any n
+    if (pde->precond == 1 && mgg && mgg[0] == '1' && n >= 8 && (n & (n - 1)) == 0)
+        s = launch_pcg_mgg(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '2')        // 256 threads, 2x2 blocks
         s = launch_pcg_mg<32, 2, 2, 16, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '3')   // 3 CTAs/SM, x and p in smem
         s = launch_pcg_mg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
@@ -387,8 +410,10 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
         s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 16)
         s = launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (pde->precond == 1 && n >= 8 && (n & (n - 1)) == 0)  // n = 64, 128 (and 8): scratch-slab multigrid
+        s = launch_pcg_mgg(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1)
-        return fail(c, USFFT_EUNIMPL, "multigrid preconditioner implemented for n = 16, 32");
+        return fail(c, USFFT_EUNIMPL, "multigrid preconditioner needs n a power of two >= 8");
     else if (reg_ok && n == 16)
         s = launch_pcg_reg<16, 2, 4, 8, 1, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (reg_ok && n == 32)
