@@ -61,8 +61,8 @@ struct MggLayout {
     }
 };
 
-template <int T>
-__global__ void __launch_bounds__(T, 2)
+template <int T, int MINB>
+__global__ void __launch_bounds__(T, MINB)
 k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double *__restrict__ nodes,
           int64_t b0, int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
           double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
