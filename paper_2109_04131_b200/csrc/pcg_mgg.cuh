@@ -6,14 +6,14 @@
 // R = P^T and rediscretised coarse operators whose coefficients are lookups into the fine
 // per-triangle table (every coarse centroid is a fine centroid), down to the mesh of 4 cells per
 // side whose 9 unknowns are solved exactly with a dense inverse (Gauss-Jordan once per sample).
-// Levels: n = 64 -> 64, 32, 16, 8 smoothed + 4 exact; n = 128 -> one more.  CG is the textbook
-// preconditioned CG (x0 = 0) stopping on ||r||_2 <= tol ||b||_2 (Z13).  13-14 iterations at
+// Levels: n = 64 -> 64, 32, 16, 8 smoothed + 4 exact; n = 128 -> one more.  CG in the
+// Chronopoulos-Gear single-reduction form (x0 = 0) stopping on ||r||_2 <= tol ||b||_2 (Z13).  13-14 iterations at
 // n = 64 and 128 against 280 and 560 with the Jacobi preconditioner (tools/mg_smoother_study.py).
 //
 // The n = 16, 32 kernel keeps the fine level in registers; at n = 64 (3969 unknowns) and 128
 // (16129) a sample no longer fits one SM's registers + shared memory, so here every grid is a
 // padded (m+1)^2 array with a zero Dirichlet ring in the CTA's scratch slab, every phase is a
-// CTA-wide loop over grid points and a barrier separates phases (25 per CG iteration at n = 64).
+// CTA-wide loop over grid points and a barrier separates phases (21 per CG iteration at n = 64).
 // Reductions are fixed trees: a sample's result does not depend on the CTA or the launch split.
 #pragma once
 
@@ -22,7 +22,7 @@ namespace usfft {
 constexpr int kMggMaxLev = 7;
 
 // Scratch layout per CTA (doubles).  Level l has m_l = n >> l cells, P_l = m_l + 1 points per
-// row.  Level 0: WH, WV, DI, B (= CG residual r), Z, T, X, P, Q (X, P, Q contiguous: the
+// row.  Level 0: WH, WV, DI, B (= CG residual r), Z, T, X, P, S, W (X, P, S contiguous: the
 // per-triangle coefficient table of the setup aliases them).  Levels 1..L-1: WH, WV, DI, B, Z, T.
 // Level L (m_L = 4): WH, WV, B, Z, then the dense inverse AI [U_L][U_L].
 struct MggLayout {
@@ -31,7 +31,7 @@ struct MggLayout {
     int64_t off[kMggMaxLev];         // start of level l (global slab or shared memory, doubles)
     int64_t region;                  // global doubles per CTA
     int64_t smem;                    // shared doubles per CTA
-    __host__ __device__ static int arrays(int l, int L) { return l == 0 ? 9 : (l < L ? 6 : 4); }
+    __host__ __device__ static int arrays(int l, int L) { return l == 0 ? 10 : (l < L ? 6 : 4); }
     __host__ static int64_t level_size(int n, int l, int L) {
         const int64_t P = (n >> l) + 1;
         return arrays(l, L) * P * P + (l == L ? 81 : 0);      // + AI: (4 - 1)^4 doubles
@@ -87,7 +87,7 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
             for (int j = 1 + tid / cw; j < m; j += rows) body(i, j, j * (m + 1) + i);
         }
     };
-    enum { WH = 0, WV = 1, DI = 2, BB = 3, ZZ = 4, TT = 5, XX = 6, PP = 7, QQ = 8 };
+    enum { WH = 0, WV = 1, DI = 2, BB = 3, ZZ = 4, TT = 5, XX = 6, PP = 7, QQ = 8, WW = 9 };
     double *aT = arr(0, XX);                               // setup only: [2][n][n]
     const double *Sy = S + (Q.psi ? Q.d * W : 0);
     const double inv_n3 = 1.0 / ((double)n * n * n);
@@ -185,14 +185,15 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
             }
             __syncthreads();
         }
-        // ---- CG init: x = 0, r = b, p = 0 (X, P, Q overwrite the coefficient table) ------------
+        // ---- CG init: x = 0, r = b, p = s = 0 (X, P, S overwrite the coefficient table) --------
         const int P0 = n + 1;
-        double *__restrict__ X = arr(0, XX), *__restrict__ Pv = arr(0, PP), *__restrict__ Qv = arr(0, QQ);
+        double *__restrict__ X = arr(0, XX), *__restrict__ Pv = arr(0, PP), *__restrict__ Sv = arr(0, QQ);
         double *__restrict__ R0 = arr(0, BB), *__restrict__ Z0 = arr(0, ZZ), *__restrict__ T0 = arr(0, TT);
+        double *__restrict__ Wv = arr(0, WW);
         const double *__restrict__ DI0 = arr(0, DI), *__restrict__ WH0 = arr(0, WH), *__restrict__ WV0 = arr(0, WV);
         double acc[3] = {0.0, 0.0, 0.0};
         for (int e = tid; e < P0 * P0; e += T) {
-            X[e] = Pv[e] = Qv[e] = 0.0;
+            X[e] = Pv[e] = Sv[e] = Wv[e] = 0.0;
             double bv = 0.0;
             if (interior(e, P0, n)) {
                 const int i = e % P0, j = e / P0;
@@ -263,41 +264,46 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
             }
         };
 
-        vcycle();
-        acc[0] = 0.0;
-        for_int(n, [&](int, int, int e) { acc[0] += R0[e] * T0[e]; });
-        block_sum<1>(*reinterpret_cast<double(*)[1]>(acc), red);
-        double rz = acc[0], rr = bb, beta = 0.0;
+        // ---- Chronopoulos-Gear PCG (as in pcg_mg.cuh): u = M^-1 r; w = A u; gamma = (r,u),
+        // delta = (w,u) in one reduction; p = u + beta p, s = w + beta s, x += alpha p,
+        // r -= alpha s fused with z0 = D r and (r,r)
+        auto precond_and_apply = [&](double &gamma, double &delta) {
+            vcycle();                                                 // T0 = M^-1 r
+            acc[0] = acc[1] = 0.0;
+            for_int(n, [&](int, int, int e) {
+                const double w = Az(WH0, WV0, T0, e, P0), uu = T0[e];
+                Wv[e] = w;
+                acc[0] += R0[e] * uu;
+                acc[1] += w * uu;
+            });
+            block_sum<2>(*reinterpret_cast<double(*)[2]>(acc), red);
+            gamma = acc[0];
+            delta = acc[1];
+        };
+        double gamma, delta, rr = bb, g_old = 0.0, a_old = 0.0;
+        precond_and_apply(gamma, delta);
         int it = 0;
         while (rr > Q.tol2 * bb && it < Q.maxit) {
-            for_int(n, [&](int, int, int e) { Pv[e] = T0[e] + beta * Pv[e]; });     // ring stays 0
-            __syncthreads();
+            const double beta = it == 0 ? 0.0 : gamma / g_old;
+            const double alpha = it == 0 ? gamma / delta : gamma / (delta - beta * gamma / a_old);
             acc[0] = 0.0;
             for_int(n, [&](int, int, int e) {
-                const double q = Az(WH0, WV0, Pv, e, P0);
-                Qv[e] = q;
-                acc[0] += Pv[e] * q;
-            });
-            block_sum<1>(*reinterpret_cast<double(*)[1]>(acc), red);
-            const double alpha = rz / acc[0];
-            acc[0] = 0.0;
-            for_int(n, [&](int, int, int e) {
-                X[e] += alpha * Pv[e];
-                const double r = R0[e] - alpha * Qv[e];
+                const double pv = T0[e] + beta * Pv[e], sv = Wv[e] + beta * Sv[e];
+                Pv[e] = pv;
+                Sv[e] = sv;
+                X[e] += alpha * pv;
+                const double r = R0[e] - alpha * sv;
                 R0[e] = r;
                 Z0[e] = DI0[e] * r;
                 acc[0] += r * r;
             });
             block_sum<1>(*reinterpret_cast<double(*)[1]>(acc), red);
             rr = acc[0];
+            g_old = gamma;
+            a_old = alpha;
             ++it;
             if (rr <= Q.tol2 * bb) break;
-            vcycle();
-            acc[0] = 0.0;
-            for_int(n, [&](int, int, int e) { acc[0] += R0[e] * T0[e]; });
-            block_sum<1>(*reinterpret_cast<double(*)[1]>(acc), red);
-            beta = acc[0] / rz;
-            rz = acc[0];
+            precond_and_apply(gamma, delta);
         }
         // ---- output u[g][bl] (interior nodes, x1 fastest) ---------------------------------------
         for (int g = tid; g < nx * nx; g += T) u[(int64_t)g * ldu + bl] = X[(g / nx + 1) * P0 + g % nx + 1];

@@ -17,6 +17,7 @@ def main():
     ap.add_argument("--nb", type=int, default=8192)
     ap.add_argument("--precond", default="")
     ap.add_argument("--reps", type=int, default=3)
+    ap.add_argument("--maxit", type=int, default=20000, help="cap (1: setup + one iteration)")
     args = ap.parse_args()
     import torch
     from paper_2109_04131_b200 import binding as B
@@ -28,7 +29,7 @@ def main():
     G = (cfg["n"] - 1) ** 2
     u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
     it = torch.empty(nb, dtype=torch.int32, device="cuda")
-    pde = B.pde_desc(cfg, precond=args.precond or None)
+    pde = B.pde_desc(cfg, precond=args.precond or None, maxit=args.maxit)
     B.usfft_sample_pde(ctx, pde, p, 0, nb, u, nb, None, it)
     torch.cuda.synchronize()
     ts = []
