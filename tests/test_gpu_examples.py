@@ -1,7 +1,8 @@
 """GPU parity of the paper's three example models (Sec. 4.2-4.4; DESIGN.md §3 Z28) as black boxes:
 the psi families (sin sin, Table 3 cos cos, sin cos reversed), the loads f = x2 / 1 / trig and
-the maps sin / tent / phi_Delta, through every PCG kernel (multigrid n = 16, 32; register Jacobi
-n = 16, 32; shared-memory Jacobi; the generic kernel at n = 20), against the oracle's element
+the maps sin / tent / phi_Delta, through every PCG kernel (multigrid n = 16, 32 and the scratch-slab
+multigrid at n = 64; register Jacobi n = 16, 32; shared-memory Jacobi; the generic kernel at n = 20),
+against the oracle's element
 assembly + banded Cholesky (oracle/fe.py) on the same lattice nodes.
 
 Tolerance: <= 1e-10 of max |u| (CG relres 1e-12 vs a direct solve).
@@ -44,7 +45,7 @@ def _solve(B, ctx, cfg, p, b0, nb, precond, delta):
 
 
 @pytest.mark.parametrize("name", sorted(EXAMPLES))
-@pytest.mark.parametrize("n", [32, 16, 20])
+@pytest.mark.parametrize("n", [32, 16, 20, 64])
 def test_example_samples_every_solver(B, ctx, monkeypatch, name, n):
     cfg = config(name, n=n)
     d, t = cfg["d"], 4
@@ -54,7 +55,8 @@ def test_example_samples_every_solver(B, ctx, monkeypatch, name, n):
     b0, nb = 7, 21                                    # includes a ragged tail of the CTA grid
     Y = olat.nodes(p.M, p.z, p.shift, t)[:, b0:b0 + nb]
     ref = ofe.sample_pde(ocfg, Y)
-    runs = [("jacobi", "smem")] + ([("mg", "reg"), ("jacobi", "reg")] if n in (16, 32) else [("jacobi", "reg")])
+    runs = [("jacobi", "smem")] + ([("mg", "reg"), ("jacobi", "reg")] if n in (16, 32) else
+                                   [("mg", "reg")] if n == 64 else [("jacobi", "reg")])
     for precond, env in runs:
         monkeypatch.setenv("USFFT_PCG", env)
         got, it = _solve(B, ctx, cfg, p, b0, nb, precond, delta)
