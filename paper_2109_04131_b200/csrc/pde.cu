@@ -255,8 +255,9 @@ usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
 usfft_status launch_pcg_mgg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
                             int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
                             int32_t *noconv, const double *S, const double *Bt) {
-    // 512 threads, two CTAs per SM (measured against 256 x 2, 256 x 3 and 1024 x 1 with the fine
-    // stencil arrays in shared memory: 2.66 vs 3.69, 3.93, 3.65 us per sample at n = 64)
+    // 512 threads, two CTAs per SM (measured against 256 x 2, 256 x 3, 512 x 1 and 1024 x 1 with
+    // the fine stencil arrays in shared memory: 2.66 vs 3.69, 3.93, 3.78, 3.65 us per sample at
+    // n = 64; the kernel is bound by L1/L2 latency, so resident warps matter more than L2 fit)
     constexpr int T = 512;
     const MggLayout Y = MggLayout::make(Q.n, 12288);           // coarse levels in <= 96 KB of smem
     const size_t dyn = sizeof(double) * (size_t)Y.smem;
