@@ -28,7 +28,9 @@ constexpr int kMggMaxLev = 7;
 struct MggLayout {
     int32_t n, nlev;                 // nlev = L + 1
     int32_t smem_from;               // levels >= smem_from live in shared memory
+    int32_t fine_mask;               // level-0 arrays (bit k = array k) in shared memory
     int64_t off[kMggMaxLev];         // start of level l (global slab or shared memory, doubles)
+    int64_t fine_off;                // shared offset of the level-0 arrays of fine_mask
     int64_t region;                  // global doubles per CTA
     int64_t smem;                    // shared doubles per CTA
     __host__ __device__ static int arrays(int l, int L) { return l == 0 ? 10 : (l < L ? 6 : 4); }
@@ -36,20 +38,31 @@ struct MggLayout {
         const int64_t P = (n >> l) + 1;
         return arrays(l, L) * P * P + (l == L ? 81 : 0);      // + AI: (4 - 1)^4 doubles
     }
-    __host__ static MggLayout make(int n, int64_t smem_budget_doubles) {
+    // The coarsest levels that fit `budget` shared doubles go to shared memory.  With
+    // fine_mask != 0 (the level-0 arrays Z = 4, T = 5: read at 5-9 stencil neighbours in every
+    // V-cycle pass), those arrays take shared memory first and the levels from 2 on follow.
+    __host__ static MggLayout make(int n, int64_t budget, int fine_mask = 0) {
         MggLayout Y{};
         Y.n = n;
         int L = 0;
         while ((n >> L) > 4) ++L;
         Y.nlev = L + 1;
-        Y.smem_from = L + 1;                                  // the coarsest levels that fit
+        const int64_t P0 = n + 1;
+        const int64_t fine = (int64_t)__builtin_popcount(fine_mask) * P0 * P0;
+        Y.fine_mask = fine_mask && fine < budget && L >= 2 ? fine_mask : 0;
+        const int64_t room = budget - (Y.fine_mask ? fine : 0);
+        Y.smem_from = L + 1;
         int64_t tail = 0;
-        for (int l = L; l >= 1; --l) {
+        for (int l = L; l >= (Y.fine_mask ? 2 : 1); --l) {
             tail += level_size(n, l, L);
-            if (tail > smem_budget_doubles) break;
+            if (tail > room) break;
             Y.smem_from = l;
         }
         int64_t og = 0, os = 0;
+        if (Y.fine_mask) {
+            Y.fine_off = 0;
+            os = fine;
+        }
         for (int l = 0; l <= L; ++l) {
             int64_t &o = l >= Y.smem_from ? os : og;
             Y.off[l] = o;
@@ -74,10 +87,17 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
     const int n = Y.n, L = Y.nlev - 1, W = 3 * n + 1, nx = n - 1;
     double *base = gscratch + (int64_t)blockIdx.x * Y.region;
     // level arrays (generic pointers into the global slab or shared memory)
-    auto arr = [&](int l, int k) -> double * {
+    // level array pointers, resolved once into a shared table (keeps the layout out of registers)
+    __shared__ double *ptab[kMggMaxLev * 10];
+    if (tid < Y.nlev * 10) {
+        const int l = tid / 10, k = tid % 10;
         const int64_t Pl = (n >> l) + 1;
-        return (l >= Y.smem_from ? smg : base) + Y.off[l] + (int64_t)k * Pl * Pl;
-    };
+        ptab[tid] = (l == 0 && ((Y.fine_mask >> k) & 1))
+                        ? smg + Y.fine_off + (int64_t)__popc(Y.fine_mask & ((1 << k) - 1)) * Pl * Pl
+                        : (l >= Y.smem_from ? smg : base) + Y.off[l] + (int64_t)k * Pl * Pl;
+    }
+    __syncthreads();
+    auto arr = [&](int l, int k) -> double * { return ptab[l * 10 + k]; };
     // body(i, j, e) for the interior points of an m-cell level (e = j (m+1) + i): thread tid owns
     // column 1 + tid % (m-1) of every (T / (m-1))-th row; one division per phase, none per point
     auto for_int = [&](int m, auto &&body) {

@@ -259,7 +259,8 @@ usfft_status launch_pcg_mgg(usfft_ctx *c, const LatParams &P, const PdeParams &Q
     // the fine stencil arrays in shared memory: 2.66 vs 3.69, 3.93, 3.78, 3.65 us per sample at
     // n = 64; the kernel is bound by L1/L2 latency, so resident warps matter more than L2 fit)
     constexpr int T = 512;
-    const MggLayout Y = MggLayout::make(Q.n, 12288);           // coarse levels in <= 96 KB of smem
+    const char *fm = getenv("USFFT_MGG_FINE");          // =0: no level-0 array in shared memory
+    const MggLayout Y = MggLayout::make(Q.n, 12288, fm && fm[0] == '0' ? 0 : (1 << 4) | (1 << 5));
     const size_t dyn = sizeof(double) * (size_t)Y.smem;
     auto kern = k_pcg_mgg<T, 2>;
     int per_sm = 0;
