@@ -61,7 +61,8 @@ def ncu_traffic(kernel_prefix: str):
     """dram read+write bytes per launch of a kernel from the newest committed ncu --set full
     summary (profiles/*_ncu.json), or None."""
     import glob
-    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json")))
+    files = sorted(glob.glob(os.path.join(ROOT, "profiles", "*_ncu.json")),
+                   key=lambda p: ("final" in os.path.basename(p), p))   # the round's final capture first
     scale = {"byte": 1.0, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}
     for path in reversed(files):
         for d in json.load(open(path)).get("full", []):
