@@ -7,6 +7,7 @@
 // kappa >= theta^2 and kappa > 0 (Z5).  All decisions are integer/ordered comparisons of the same
 // doubles, hence exact and independent of thread scheduling; votes are integer atomics.
 #include <algorithm>
+#include <cstdlib>
 
 #include "common.cuh"
 
@@ -148,6 +149,74 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     }
     for (int q = out_run + threadIdx.x; q < s_tilde; q += blockDim.x) out[q] = -1;
     if (threadIdx.x == 0) n_det_g[g] = out_run;
+}
+
+// Small candidate sets (|J| <= 32 KPL): one warp per node with the node's keys in registers
+// (candidate j = 32 k + lane in register k).  The s~-th largest key T is found by a bitwise binary
+// search (largest T with #{key >= T} >= s~, 63 counting passes, warp reductions only), then one
+// ordered pass takes every key > T and the first (by j) keys == T up to s~ - #{key > T}: the same
+// members as the radix select of k_select, with no CTA barrier.
+template <int KPL>
+__global__ void __launch_bounds__(128)
+k_select_warp(const double *__restrict__ kmin, int64_t nJ, int64_t G, const double *__restrict__ kmax,
+              int32_t s_tilde, double theta_rel, double theta_abs, int32_t *__restrict__ votes,
+              int32_t *__restrict__ det_g, int32_t *__restrict__ n_det_g, double *__restrict__ th2_out) {
+    const int lane = threadIdx.x & 31;
+    const int64_t g = (int64_t)blockIdx.x * 4 + (threadIdx.x >> 5);
+    const double th2 = theta2_of(theta_rel, theta_abs, kmax);
+    if (g == 0 && lane == 0 && th2_out) th2_out[0] = th2;
+    if (g >= G) return;
+    const unsigned long long *row = reinterpret_cast<const unsigned long long *>(kmin + g * nJ);
+    unsigned long long key[KPL];
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+        const int64_t j = 32 * k + lane;
+        key[k] = j < nJ ? __ldg(row + j) : 0ull;
+    }
+    auto count_ge = [&](unsigned long long t) -> int {
+        int c = 0;
+#pragma unroll
+        for (int k = 0; k < KPL; ++k) c += key[k] >= t ? 1 : 0;
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
+        return c;
+    };
+    unsigned long long T = 0ull;
+    if ((int64_t)s_tilde < nJ) {
+        for (int b = 62; b >= 0; --b) {                  // non-negative doubles: bit 63 is 0
+            const unsigned long long cand = T | (1ull << b);
+            if (count_ge(cand) >= s_tilde) T = cand;
+        }
+    }
+    // members: key > T, and the first need_eq keys == T by index (T = 0: every key qualifies)
+    int gt = 0;
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) gt += key[k] > T ? 1 : 0;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, o);
+    const int need_eq = (int64_t)s_tilde < nJ ? s_tilde - gt : KPL * 32;
+    const unsigned lt = (1u << lane) - 1u;
+    int eq_run = 0, out_run = 0;
+    int32_t *out = det_g + g * (int64_t)s_tilde;
+#pragma unroll
+    for (int k = 0; k < KPL; ++k) {
+        const int64_t j = 32 * k + lane;
+        const bool valid = j < nJ;
+        const bool is_eq = valid && key[k] == T;
+        const unsigned eqm = __ballot_sync(0xffffffffu, is_eq);
+        const bool member = valid && (key[k] > T || (is_eq && eq_run + __popc(eqm & lt) < need_eq));
+        const double kv = __longlong_as_double((long long)key[k]);
+        const bool take = member && kv >= th2 && kv > 0.0;
+        const unsigned tm = __ballot_sync(0xffffffffu, take);
+        if (take) {
+            out[out_run + __popc(tm & lt)] = (int32_t)j;
+            atomicAdd(votes + j, 1);
+        }
+        eq_run += __popc(eqm);
+        out_run += __popc(tm);
+    }
+    for (int q = out_run + lane; q < s_tilde; q += 32) out[q] = -1;
+    if (lane == 0) n_det_g[g] = out_run;
 }
 
 // streamed selection (Z29): one CTA per owned node moves the selected (key, j) pairs of row g of
@@ -324,6 +393,20 @@ extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t
     if (nJ > 0) USFFT_CUDA(c, cudaMemsetAsync(votes, 0, sizeof(int32_t) * nJ, c->stream));
     if (G_loc == 0 || nJ == 0) {
         if (G_loc > 0 && n_det_g) USFFT_CUDA(c, cudaMemsetAsync(n_det_g, 0, sizeof(int32_t) * G_loc, c->stream));
+        return USFFT_OK;
+    }
+    const char *sv = getenv("USFFT_SELECT");             // =radix: the CTA kernel at every size
+    if (!(sv && sv[0] == 'r') && nJ <= 32 * 64) {
+        const unsigned grid = (unsigned)((G_loc + 3) / 4);
+        auto launch = [&](auto kern) {
+            kern<<<grid, 128, 0, c->stream>>>(kappa_min, nJ, G_loc, kappa_max, s_tilde, theta_rel, theta_abs,
+                                              votes, det_g, n_det_g, theta2);
+        };
+        if (nJ <= 32 * 8) launch(k_select_warp<8>);
+        else if (nJ <= 32 * 16) launch(k_select_warp<16>);
+        else if (nJ <= 32 * 32) launch(k_select_warp<32>);
+        else launch(k_select_warp<64>);
+        USFFT_CHECK_LAUNCH(c);
         return USFFT_OK;
     }
     const size_t kst = nJ <= KSTAGE ? sizeof(unsigned long long) * (size_t)nJ : 0;

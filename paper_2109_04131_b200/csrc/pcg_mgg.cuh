@@ -150,14 +150,15 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
         for (int l = 0; l <= L; ++l) {
             const int m = n >> l, Pl = m + 1;
             double *wh = arr(l, WH), *wv = arr(l, WV);
-            double *bz = l < L ? arr(l, BB) : arr(l, 2);
+            double *bb_ = l < L ? arr(l, BB) : arr(l, 2), *zz = l < L ? arr(l, ZZ) : arr(l, 3);
+            double *tt = l < L ? arr(l, TT) : nullptr;                // (Z, T may live in shared memory)
             for (int e = tid; e < Pl * Pl; e += T) {
                 const int i = e % Pl, j = e / Pl;
                 wh[e] = (i < m && j >= 1 && j < m) ? 0.5 * (fcoef(i, j, 0, l) + fcoef(i, j - 1, 1, l)) : 0.0;
                 wv[e] = (j < m && i >= 1 && i < m) ? 0.5 * (fcoef(i, j, 1, l) + fcoef(i - 1, j, 0, l)) : 0.0;
-                bz[e] = 0.0;                                          // B (and Z, T below)
-                bz[Pl * Pl + e] = 0.0;
-                if (l < L) bz[2 * Pl * Pl + e] = 0.0;
+                bb_[e] = 0.0;                                         // B, Z, T with zero rings
+                zz[e] = 0.0;
+                if (tt) tt[e] = 0.0;
             }
         }
         __syncthreads();
