@@ -80,7 +80,10 @@ class Detector:
                 ev[name] = e
 
         mark("start")
-        plan = B.usfft_plan_round(ctx, cfg["seed"], step, t, i, cfg["d"], cfg["N"], s_tilde,
+        # cfg["lattice_factor"] f > 1 sizes the Step-2 lattices for f s~ (M >= 4 f s~, Z2) while
+        # the selection keeps s~: less aliasing per bin for non-sparse projections (§9)
+        s_plan = s_tilde * int(cfg.get("lattice_factor", 1)) if step == 2 else s_tilde
+        plan = B.usfft_plan_round(ctx, cfg["seed"], step, t, i, cfg["d"], cfg["N"], s_plan,
                                   cfg.get("mode", "A") if step == 2 else "A", nJ,
                                   I_prev if t > 1 else None, n_prev, kt)
         L, M = plan.L, plan.M

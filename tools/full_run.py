@@ -24,6 +24,7 @@ def main():
     ap.add_argument("--n-test", type=int, default=10000)
     ap.add_argument("--theta", default="", help="coefficient map override (sin, tent, probit, phi_delta)")
     ap.add_argument("--form", default="", help="coefficient form override (affine, exp)")
+    ap.add_argument("--lattice-factor", type=int, default=1, help="Step-2 lattices sized for f s~ (Z2 x f)")
     args = ap.parse_args()
     import numpy as np
     import torch
@@ -36,6 +37,8 @@ def main():
         cfg["theta"] = args.theta
     if args.form:
         cfg["form"] = args.form
+    if args.lattice_factor > 1:
+        cfg["lattice_factor"] = args.lattice_factor
     det = Detector(cfg)
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(4)]
     t0 = time.perf_counter()
@@ -57,7 +60,7 @@ def main():
     e = err.cpu().numpy()
     out = {
         "workload": (f"config{key}" if isinstance(key, int) else "example") + f":{cfg['name']}", "theta": cfg["theta"], "form": cfg["form"],
-        "delta": det.delta, "d": cfg["d"], "n": cfg["n"], "N": cfg["N"],
+        "delta": det.delta, "lattice_factor": args.lattice_factor, "d": cfg["d"], "n": cfg["n"], "N": cfg["N"],
         "s": cfg["s"], "rounds": len(log), "samples_detection": n_detect, "samples_step3": n_step3,
         "step3_share": n_step3 / (n_detect + n_step3), "nI": int(I.shape[0]), "q": I.shape[0] / cfg["s"],
         "cover_lattices": int(cov.z.shape[0]), "cover_M": int(cov.M),
