@@ -21,85 +21,73 @@ namespace usfft {
 
 constexpr int kMggMaxLev = 7;
 
-// Scratch layout per CTA (doubles).  Level l has m_l = n >> l cells, P_l = m_l + 1 points per
-// row.  Level 0: WH, WV, DI, B (= CG residual r), Z, T, X, P, S, W (X, P, S contiguous: the
-// per-triangle coefficient table of the setup aliases them).  Levels 1..L-1: WH, WV, DI, B, Z, T.
-// Level L (m_L = 4): WH, WV, B, Z, then the dense inverse AI [U_L][U_L].
-struct MggLayout {
-    int32_t n, nlev;                 // nlev = L + 1
-    int32_t smem_from;               // levels >= smem_from live in shared memory
-    int32_t fine_mask;               // level-0 arrays (bit k = array k) in shared memory
-    int64_t off[kMggMaxLev];         // start of level l (global slab or shared memory, doubles)
-    int64_t fine_off;                // shared offset of the level-0 arrays of fine_mask
-    int64_t region;                  // global doubles per CTA
-    int64_t smem;                    // shared doubles per CTA
-    __host__ __device__ static int arrays(int l, int L) { return l == 0 ? 10 : (l < L ? 6 : 4); }
-    __host__ static int64_t level_size(int n, int l, int L) {
-        const int64_t P = (n >> l) + 1;
-        return arrays(l, L) * P * P + (l == L ? 81 : 0);      // + AI: (4 - 1)^4 doubles
-    }
-    // The coarsest levels that fit `budget` shared doubles go to shared memory.  With
-    // fine_mask != 0 (the level-0 arrays Z = 4, T = 5: read at 5-9 stencil neighbours in every
-    // V-cycle pass), those arrays take shared memory first and the levels from 2 on follow.
-    __host__ static MggLayout make(int n, int64_t budget, int fine_mask = 0) {
-        MggLayout Y{};
-        Y.n = n;
-        int L = 0;
-        while ((n >> L) > 4) ++L;
-        Y.nlev = L + 1;
-        const int64_t P0 = n + 1;
-        const int64_t fine = (int64_t)__builtin_popcount(fine_mask) * P0 * P0;
-        Y.fine_mask = fine_mask && fine < budget && L >= 2 ? fine_mask : 0;
-        const int64_t room = budget - (Y.fine_mask ? fine : 0);
-        Y.smem_from = L + 1;
-        int64_t tail = 0;
-        for (int l = L; l >= (Y.fine_mask ? 2 : 1); --l) {
-            tail += level_size(n, l, L);
+// Scratch layout per CTA (doubles), fixed at compile time for each mesh NN so every level offset
+// and every per-level division below folds to a constant.  Level l has m_l = NN >> l cells and
+// P_l = m_l + 1 points per row.  Level 0: WH, WV, DI, B (= CG residual r), Z, T, X, P, S, W (X, P, S
+// contiguous: the per-triangle coefficient table of the setup aliases them).  Levels 1..L-1: WH,
+// WV, DI, B, Z, T.  Level L (m_L = 4): WH, WV, B, Z, then the dense inverse AI [9][9].  The
+// coarsest levels that fit BUDGET doubles live in shared memory; when the level-0 Z and T (read at
+// 5-9 stencil neighbours in every V-cycle pass) fit too, they come first and the levels from 2 on
+// follow.
+template <int NN>
+struct MggC {
+    static constexpr int L = NN == 8 ? 1 : NN == 16 ? 2 : NN == 32 ? 3 : NN == 64 ? 4 : NN == 128 ? 5 : -1;
+    static_assert(L >= 1, "mesh must be 8, 16, 32, 64 or 128 cells per side");
+    static constexpr int64_t BUDGET = 12288;                  // 96 KB: two CTAs per SM
+    __host__ __device__ static constexpr int64_t P(int l) { return (NN >> l) + 1; }
+    __host__ __device__ static constexpr int arrays(int l) { return l == 0 ? 10 : (l < L ? 6 : 4); }
+    __host__ __device__ static constexpr int64_t size(int l) { return arrays(l) * P(l) * P(l) + (l == L ? 81 : 0); }
+    static constexpr int64_t FINE = 2 * P(0) * P(0);
+    static constexpr bool FINE_SMEM = L >= 2 && FINE < BUDGET;
+    __host__ __device__ static constexpr int smem_from() {
+        int from = L + 1;
+        int64_t tail = 0, room = BUDGET - (FINE_SMEM ? FINE : 0);
+        for (int l = L; l >= (FINE_SMEM ? 2 : 1); --l) {
+            tail += size(l);
             if (tail > room) break;
-            Y.smem_from = l;
+            from = l;
         }
-        int64_t og = 0, os = 0;
-        if (Y.fine_mask) {
-            Y.fine_off = 0;
-            os = fine;
-        }
-        for (int l = 0; l <= L; ++l) {
-            int64_t &o = l >= Y.smem_from ? os : og;
-            Y.off[l] = o;
-            o += level_size(n, l, L);
-        }
-        Y.region = (og + 31) & ~int64_t(31);
-        Y.smem = os;
-        return Y;
+        return from;
+    }
+    static constexpr int SMEM_FROM = smem_from();
+    __host__ __device__ static constexpr int64_t off(int l) {   // in its space (global or shared)
+        int64_t og = 0, os = FINE_SMEM ? FINE : 0;
+        for (int q = 0; q < l; ++q) (q >= SMEM_FROM ? os : og) += size(q);
+        return l >= SMEM_FROM ? os : og;
+    }
+    __host__ __device__ static constexpr int64_t region() {
+        int64_t og = 0;
+        for (int q = 0; q < SMEM_FROM && q <= L; ++q) og += size(q);
+        return (og + 31) & ~int64_t(31);
+    }
+    __host__ __device__ static constexpr int64_t smem() {
+        int64_t os = FINE_SMEM ? FINE : 0;
+        for (int q = SMEM_FROM; q <= L; ++q) os += size(q);
+        return os;
     }
 };
 
-template <int T, int MINB>
+template <int NN, int T, int MINB>
 __global__ void __launch_bounds__(T, MINB)
-k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double *__restrict__ nodes,
+k_pcg_mgg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
           int64_t b0, int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
           double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
           const double *__restrict__ Bt, double *__restrict__ gscratch) {
+    using C = MggC<NN>;
     __shared__ double red[32 * 3];
     __shared__ double th_amp[kMaxD];
     extern __shared__ double smg[];
     const int tid = threadIdx.x;
-    const int n = Y.n, L = Y.nlev - 1, W = 3 * n + 1, nx = n - 1;
-    double *base = gscratch + (int64_t)blockIdx.x * Y.region;
-    // level arrays (generic pointers into the global slab or shared memory)
-    // level array pointers, resolved once into a shared table (keeps the layout out of registers)
-    __shared__ double *ptab[kMggMaxLev * 10];
-    if (tid < Y.nlev * 10) {
-        const int l = tid / 10, k = tid % 10;
-        const int64_t Pl = (n >> l) + 1;
-        ptab[tid] = (l == 0 && ((Y.fine_mask >> k) & 1))
-                        ? smg + Y.fine_off + (int64_t)__popc(Y.fine_mask & ((1 << k) - 1)) * Pl * Pl
-                        : (l >= Y.smem_from ? smg : base) + Y.off[l] + (int64_t)k * Pl * Pl;
-    }
-    __syncthreads();
-    auto arr = [&](int l, int k) -> double * { return ptab[l * 10 + k]; };
+    constexpr int n = NN, L = C::L, W = 3 * n + 1, nx = n - 1;
+    double *base = gscratch + (int64_t)blockIdx.x * C::region();
+    // array k of level l (constant offsets once the level loops are unrolled)
+    auto arr = [&](int l, int k) -> double * {
+        const int64_t Pl = C::P(l);
+        if (C::FINE_SMEM && l == 0 && (k == 4 || k == 5)) return smg + (k - 4) * Pl * Pl;
+        return (l >= C::SMEM_FROM ? smg : base) + C::off(l) + (int64_t)k * Pl * Pl;
+    };
     // body(i, j, e) for the interior points of an m-cell level (e = j (m+1) + i): thread tid owns
-    // column 1 + tid % (m-1) of every (T / (m-1))-th row; one division per phase, none per point
+    // column 1 + tid % (m-1) of every (T / (m-1))-th row
     auto for_int = [&](int m, auto &&body) {
         const int cw = m - 1, rows = T / cw;
         if (tid < rows * cw) {
@@ -147,6 +135,7 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
             return aT[(ra % 3 == 1 ? n * n : 0) + (cj * p + rb / 3) * n + ci * p + ra / 3];
         };
         // ---- edge weights of every level, zeroed vectors --------------------------------------
+#pragma unroll
         for (int l = 0; l <= L; ++l) {
             const int m = n >> l, Pl = m + 1;
             double *wh = arr(l, WH), *wv = arr(l, WV);
@@ -163,6 +152,7 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
         }
         __syncthreads();
         // ---- omega / diagonal on the smoothed levels; dense A_L --------------------------------
+#pragma unroll
         for (int l = 0; l < L; ++l) {
             const int m = n >> l, Pl = m + 1;
             const double *wh = arr(l, WH), *wv = arr(l, WV);
@@ -229,6 +219,7 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
 
         // ---- V(1,1) cycle: T0 = M^-1 R0, assuming Z0 = DI0 R0 already written -----------------
         auto vcycle = [&]() {
+#pragma unroll
             for (int l = 0; l < L; ++l) {                             // down
                 const int m = n >> l, Pl = m + 1;
                 const double *__restrict__ wh = arr(l, WH), *__restrict__ wv = arr(l, WV);
@@ -260,6 +251,7 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const MggLayout Y, const double 
                 }
                 __syncthreads();
             }
+#pragma unroll
             for (int l = L - 1; l >= 0; --l) {                        // up
                 const int m = n >> l, Pl = m + 1, Pc = (m >> 1) + 1;
                 const double *__restrict__ zc = (l + 1 < L) ? arr(l + 1, TT) : arr(L, 3);   // the coarse result

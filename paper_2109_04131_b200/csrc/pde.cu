@@ -252,27 +252,40 @@ usfft_status launch_pcg_mg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
     return USFFT_OK;
 }
 
-usfft_status launch_pcg_mgg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
-                            int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
-                            int32_t *noconv, const double *S, const double *Bt) {
+template <int NN>
+usfft_status launch_pcg_mgg_n(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
+                              int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
+                              int32_t *noconv, const double *S, const double *Bt) {
     // 512 threads, two CTAs per SM (measured against 256 x 2, 256 x 3, 512 x 1 and 1024 x 1 with
     // the fine stencil arrays in shared memory: 2.66 vs 3.69, 3.93, 3.78, 3.65 us per sample at
     // n = 64; the kernel is bound by L1/L2 latency, so resident warps matter more than L2 fit)
     constexpr int T = 512;
-    const char *fm = getenv("USFFT_MGG_FINE");          // =0: no level-0 array in shared memory
-    const MggLayout Y = MggLayout::make(Q.n, 12288, fm && fm[0] == '0' ? 0 : (1 << 4) | (1 << 5));
-    const size_t dyn = sizeof(double) * (size_t)Y.smem;
-    auto kern = k_pcg_mgg<T, 2>;
+    using C = MggC<NN>;
+    const size_t dyn = sizeof(double) * (size_t)C::smem();
+    auto kern = k_pcg_mgg<NN, T, 2>;
     int per_sm = 0;
     if (usfft_status s = kernel_fit(c, kern, T, dyn, &per_sm)) return s;
     if (per_sm < 1) per_sm = 1;
     int64_t grid = (int64_t)per_sm * c->sm_count;
     if (grid > nb) grid = nb;
-    if (usfft_status s = ensure(c, &c->ws, &c->ws_size, sizeof(double) * (size_t)grid * (size_t)Y.region)) return s;
-    kern<<<(unsigned)grid, T, dyn, c->stream>>>(P, Q, Y, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt,
+    if (usfft_status s = ensure(c, &c->ws, &c->ws_size, sizeof(double) * (size_t)grid * (size_t)C::region())) return s;
+    kern<<<(unsigned)grid, T, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt,
                                               static_cast<double *>(c->ws));
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
+}
+
+usfft_status launch_pcg_mgg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
+                            int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
+                            int32_t *noconv, const double *S, const double *Bt) {
+    switch (Q.n) {
+    case 8: return launch_pcg_mgg_n<8>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    case 16: return launch_pcg_mgg_n<16>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    case 32: return launch_pcg_mgg_n<32>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    case 64: return launch_pcg_mgg_n<64>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    case 128: return launch_pcg_mgg_n<128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    default: return fail(c, USFFT_EUNIMPL, "scratch-slab multigrid compiled for n = 8, 16, 32, 64, 128");
+    }
 }
 
 template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
