@@ -182,6 +182,7 @@ def run_ours(args):
     torch.cuda.cudart().cudaProfilerStart()          # ncu --profile-from-start off: timed steps only
     launches0 = det.ctx.launches()
     step_ms, phase, iters_sum, samples = [], {}, 0, 0
+    det.timing = False                               # no per-phase events / syncs inside timed steps
     for k in range(args.steps):
         flush.fill_(float(k))                         # evict L2 between timed iterations
         torch.cuda.synchronize()
@@ -194,15 +195,22 @@ def run_ours(args):
         torch.cuda.synchronize()
         step_ms.append(e0.elapsed_time(e1))
         if args.verbose:
-            print(f"step {k}: {step_ms[-1]:.3f} ms " + " ".join(f"{a}={b:.3f}" for a, b in res.times.items()),
-                  file=sys.stderr, flush=True)
-        for name, ms in res.times.items():
-            phase[name] = phase.get(name, 0.0) + ms
+            print(f"step {k}: {step_ms[-1]:.3f} ms", file=sys.stderr, flush=True)
         iters_sum += int(res.iters.sum().item()) if res.iters is not None and res.iters.numel() else 0
         samples += res.plan.L * res.plan.M
     launches = det.ctx.launches() - launches0
     torch.cuda.cudart().cudaProfilerStop()
     clk = clocks.stop()
+    # per-phase breakdown from the same rounds re-run untimed with per-phase CUDA events
+    det.timing = True
+    for k in range(args.steps):
+        flush.fill_(float(k))
+        res_p = one(k + 1)
+        if args.verbose:
+            print(f"phases {k}: " + " ".join(f"{a}={b:.3f}" for a, b in res_p.times.items()),
+                  file=sys.stderr, flush=True)
+        for name, ms in res_p.times.items():
+            phase[name] = phase.get(name, 0.0) + ms
     total_ms = float(np.sum(step_ms))
     t_tensor = torch.tensor([total_ms, phase.get("pde", 0.0)], dtype=torch.float64, device="cuda")
     it_tensor = torch.tensor([iters_sum], dtype=torch.int64, device="cuda")
