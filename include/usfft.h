@@ -169,11 +169,13 @@ usfft_status usfft_lattice(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_
  * One FE solve per node y_b, b = b0 .. b0+nb-1 (Alg. 1 Step 2c "Sample p ... for every chi_g",
  * P:313; one solve serves all G nodes).  The nodes are generated in-kernel from `lat`
  * (bit-identical to usfft_lattice) unless `nodes` (dev fp64 [d][nb]) is given.
- * Jacobi PCG from x0 = 0, stop on the recursive ||r||_2 <= tol ||b||_2 (Z13).
+ * Preconditioned CG (pde->precond: Jacobi or multigrid) from x0 = 0, stop on the recursive
+ * ||r||_2 <= tol ||b||_2 (Z13).
  * u        dev fp64 [G][ldu]: u[g*ldu + bl] = u(x_g, y_{b0+bl}), ldu >= nb
  * iters    dev int32 [nb] (may be NULL): PCG iterations per sample
  * relres   dev fp64 [nb] (may be NULL): final recursive ||r||/||b|| (Jacobi path: or an upper bound)
- * n_noconv host int32 (may be NULL; syncs): samples that missed tol; > 0 -> USFFT_ENOCONV */
+ * n_noconv host int32 (may be NULL: no count, no sync; else syncs): samples that missed tol;
+ *          > 0 -> USFFT_ENOCONV */
 usfft_status usfft_sample_pde(usfft_ctx *ctx, const usfft_pde_desc *pde,
                               const usfft_lattice_desc *lat, int64_t b0, int64_t nb,
                               const double *nodes, double *u, int64_t ldu, int32_t *iters,

@@ -323,7 +323,7 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         if (tid == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rr / bb);
-            if (rr > Q.tol2 * bb) atomicAdd(noconv, 1);
+            if (noconv && rr > Q.tol2 * bb) atomicAdd(noconv, 1);
         }
         __syncthreads();
     }

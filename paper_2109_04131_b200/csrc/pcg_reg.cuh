@@ -294,7 +294,7 @@ k_pcg_reg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
         if (tid == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rho / bb);       // exact or an upper bound
-            if (!conv) atomicAdd(noconv, 1);
+            if (noconv && !conv) atomicAdd(noconv, 1);
         }
         __syncthreads();
     }

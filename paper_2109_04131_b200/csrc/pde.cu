@@ -217,7 +217,7 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
         if (tid == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rr / bb);
-            if (rr > Q.tol2 * bb) atomicAdd(noconv, 1);
+            if (noconv && rr > Q.tol2 * bb) atomicAdd(noconv, 1);
         }
         __syncthreads();
     }
@@ -407,8 +407,9 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
             Bt = rt->second;
         }
     }
-    int32_t *noconv = reinterpret_cast<int32_t *>(c->dscal);      // device counter slot 0
-    USFFT_CUDA(c, cudaMemsetAsync(noconv, 0, sizeof(int32_t), c->stream));
+    // non-converged counter (device slot 0), only when the caller asks for it
+    int32_t *noconv = n_noconv ? reinterpret_cast<int32_t *>(c->dscal) : nullptr;
+    if (noconv) USFFT_CUDA(c, cudaMemsetAsync(noconv, 0, sizeof(int32_t), c->stream));
 
     const int n = pde->n, G = (n - 1) * (n - 1);
     // register-resident CTA-per-sample PCG (mesh size a template parameter: n = 16, 32, the

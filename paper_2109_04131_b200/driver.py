@@ -106,7 +106,7 @@ class Detector:
         mark("exchange")
         Mh = M // 2 + 1
         spectra = torch.empty((self.G_loc, L, Mh, 2), dtype=torch.float64, device=dev)
-        kmax = torch.zeros(1, dtype=torch.float64, device=dev)
+        kmax = torch.empty(1, dtype=torch.float64, device=dev)      # reset by usfft_lattice_fft
         det_g = torch.empty((self.G_loc, s_tilde), dtype=torch.int32, device=dev)
         n_det_g = torch.empty(self.G_loc, dtype=torch.int32, device=dev)
         th2 = torch.empty(1, dtype=torch.float64, device=dev)
