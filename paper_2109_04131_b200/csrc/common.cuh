@@ -47,7 +47,7 @@ constexpr int kMaxSlab = 64;     // exchange slabs (ranks)
 struct LatParams {
     int32_t d, t, line_axis, L;
     int64_t M;
-    int64_t z[kMaxZ];
+    int32_t z[kMaxZ];            // z < M <= 2^26: int32 halves the kernel-parameter copy per launch
     double shift[kMaxD];
 };
 

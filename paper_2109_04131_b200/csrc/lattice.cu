@@ -31,7 +31,7 @@ __global__ void k_bins(const LatParams P, const int16_t *__restrict__ I_prev, in
         const int64_t j = e - l * nJ;
         const int64_t a = j / n1;
         const int64_t cc = j - a * n1;
-        const int64_t *z = P.z + l * P.t;
+        const int32_t *z = P.z + l * P.t;
         int64_t s = (int64_t)kt[cc] * z[tp];
         for (int q = 0; q < tp; ++q) s += (int64_t)I_prev[a * tp + q] * z[q];
         int64_t b = s % P.M;

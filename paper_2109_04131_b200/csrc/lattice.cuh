@@ -14,10 +14,10 @@ __device__ __forceinline__ double lattice_node(const LatParams &P, int64_t b, in
     const int64_t l = b / P.M;
     const int64_t i = b - l * P.M;
     if (P.line_axis >= 0) {
-        if (j == P.line_axis) return (double)((i * P.z[l * P.t]) % P.M) / (double)P.M;
+        if (j == P.line_axis) return (double)((i * (int64_t)P.z[l * P.t]) % P.M) / (double)P.M;
         return P.shift[j];
     }
-    if (j < P.t) return (double)((i * P.z[l * P.t + j]) % P.M) / (double)P.M;
+    if (j < P.t) return (double)((i * (int64_t)P.z[l * P.t + j]) % P.M) / (double)P.M;
     return P.shift[j];
 }
 
@@ -40,7 +40,7 @@ inline usfft_status make_lat_params(usfft_ctx *c, const usfft_lattice_desc *L, L
     for (int k = 0; k < L->L * L->t; ++k) {
         USFFT_REQUIRE(c, L->z[k] >= 0 && L->z[k] < L->M, "z[%d] = %lld not in [0, M)", k,
                       (long long)L->z[k]);
-        P->z[k] = L->z[k];
+        P->z[k] = (int32_t)L->z[k];
     }
     for (int j = 0; j < L->d; ++j) {
         USFFT_REQUIRE(c, L->shift[j] >= 0.0 && L->shift[j] < 1.0, "shift[%d] not in [0,1)", j);
