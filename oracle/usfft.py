@@ -35,7 +35,8 @@ def round_plan(cfg: dict, t: int, i: int, nJ: int, s_tilde: int, J=None):
     if cfg.get("mode", "A") == "R":
         M, z = mode_r_lattice(J, cfg["seed"], t, i, cfg["N"])
         return M, 1, z
-    M = plan.lattice_size(s_tilde, cfg["N"])
+    # optional lattice factor f (Step-2 lattices sized for f s~, the Z2 rule at f s~)
+    M = plan.lattice_size(s_tilde * int(cfg.get("lattice_factor", 1)), cfg["N"])
     L = plan.num_lattices(nJ)
     return M, L, plan.z_vectors(cfg["seed"], t, i, M, L)
 

@@ -327,13 +327,14 @@ def _tp_blackbox(tp):
     return bb
 
 
-@pytest.mark.parametrize("mode", ["A", "R"])
-def test_full_run_trig_poly_matches_oracle(B, mode):
+@pytest.mark.parametrize("mode,factor", [("A", 1), ("R", 1), ("A", 3)])
+def test_full_run_trig_poly_matches_oracle(B, mode, factor):
     from paper_2109_04131_b200.driver import Detector
     d, N, G = 6, 16, 4
     for trial in range(3):
         tp = trig_poly(900 + trial, d, N, G, 16, real=True, max_active=3)
-        cfg = dict(d=d, N=N, s=20, s_local=20, r=5, seed=trial, theta_rel=1e-6, mode=mode, G=G)
+        cfg = dict(d=d, N=N, s=20, s_local=20, r=5, seed=trial, theta_rel=1e-6, mode=mode, G=G,
+                   lattice_factor=factor)
         det = Detector(cfg, blackbox=_tp_blackbox(tp))
         I, C = det.run()
         ref = ousfft.run(cfg, tp)
