@@ -217,7 +217,7 @@ def usfft_detect_carry(ctx: Context, G_loc: int, s_tilde: int, width: int, merge
     _check(ctx, st, "usfft_detect_carry")
 
 
-MOMENT_MAPS = {"sin": 0, "tent": 1, "phi_delta": 3}
+MOMENT_MAPS = {"sin": 0, "tent": 1, "probit": 2, "phi_delta": 3}   # the C side rejects 2
 
 
 def usfft_moments(ctx: Context, I, C, theta: str, delta: float, E, var, gsi=None):

@@ -145,9 +145,9 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][20] = clock64();
 #endif
         // ---- K3: coefficients ----------------------------------------------------------------
-        if (tid < Q.d) {
-            const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
-            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y, Q.delta);
+        for (int j = tid; j < Q.d; j += blockDim.x) {      // d may exceed the CTA (n = 16: 32 threads)
+            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
+            th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
         USFFT_MG_SMARK(24);

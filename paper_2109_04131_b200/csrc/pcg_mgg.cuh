@@ -114,9 +114,9 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
-        if (tid < Q.d) {
-            const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
-            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y, Q.delta);
+        for (int j = tid; j < Q.d; j += blockDim.x) {      // d may exceed the CTA (n = 16: 32 threads)
+            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
+            th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
         // ---- K3: a at the 2 n^2 fine triangle centroids (lower plane, then upper plane) -------

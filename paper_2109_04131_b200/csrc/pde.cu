@@ -122,9 +122,9 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
         // ---- K3: theta_j(y_b) and the edge weights ----------------------------------------
-        if (tid < Q.d) {
-            const double y = nodes ? nodes[(int64_t)tid * nb + bl] : lattice_node(P, b, tid);
-            th_amp[tid] = Q.amp[tid] * theta_of(Q.theta, y, Q.delta);
+        for (int j = tid; j < Q.d; j += blockDim.x) {      // d may exceed the CTA (n = 16: 32 threads)
+            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
+            th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
         for (int e = tid; e < np * np; e += T) {

@@ -104,3 +104,57 @@ def test_gather_rows_step1(B, ctx):
     rows2 = torch.empty((2, 3), dtype=torch.int16, device="cuda")
     B.usfft_gather_rows(ctx, idx2, 2, Ip, 3, kt2, rows2)
     assert rows2.tolist() == [[1, 2, 8], [3, 4, 9]]
+
+
+def test_new_entry_points_validate(B, ctx):
+    """EINVAL / EUNIMPL paths of the round's later entry points (nothing launched, ctx usable)."""
+    from paper_2109_04131_b200.binding import UsfftError
+    from usfft_inputs import config
+    I = torch.zeros((2, 3), dtype=torch.int16, device="cuda")
+    C = torch.zeros((4, 2, 2), dtype=torch.float64, device="cuda")
+    E = torch.full((4, 2), 7.0, dtype=torch.float64, device="cuda")
+    var = torch.empty(4, dtype=torch.float64, device="cuda")
+    with pytest.raises(UsfftError):                                   # clipped Phi^-1: no D_k
+        B.usfft_moments(ctx, I, C, "probit", 0.0, E, var)
+    assert torch.all(E == 7.0)
+    with pytest.raises(UsfftError):                                   # phi_Delta needs Delta
+        B.usfft_moments(ctx, I, C, "phi_delta", 0.0, E, var)
+    B.usfft_moments(ctx, I, C, "tent", 0.0, E, var)                  # C = 0 -> E = 0, var = 0
+    assert not E.any() and not var.any()
+    cfg = config(1, n=20)
+    p = B.usfft_plan_round(ctx, 0, 2, 2, 1, 4, 8, 20, "A", 30)
+    u = torch.empty((19 * 19, 2), dtype=torch.float64, device="cuda")
+    with pytest.raises(UsfftError) as e:                              # multigrid needs a power of two
+        B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond="mg"), p, 0, 2, u, 2)
+    assert e.value.status != 0
+    bad = B.pde_desc(config(1))
+    bad[0].psi = 7
+    with pytest.raises(UsfftError):
+        B.usfft_sample_pde(ctx, bad, p, 0, 2, torch.empty((225, 2), dtype=torch.float64, device="cuda"), 2)
+    km = torch.empty((3, 10), dtype=torch.float64, device="cuda")
+    sp = torch.zeros((3, p.L, p.M // 2 + 1, 2), dtype=torch.float64, device="cuda")
+    bins = torch.zeros((p.L, 10), dtype=torch.int32, device="cuda")
+    kx = torch.zeros(1, dtype=torch.float64, device="cuda")
+    with pytest.raises(UsfftError):                                   # ldk < nJ
+        B.usfft_lattice_keys(ctx, p, 3, sp, bins, 10, 10, km, 5, kx)
+    B.usfft_lattice_keys(ctx, p, 3, sp, bins, 10, 10, km, 10, kx)    # zero spectra -> zero keys
+    assert not km.any()
+    dp = torch.zeros((3, 4), dtype=torch.int32, device="cuda")
+    nd = torch.zeros(3, dtype=torch.int32, device="cuda")
+    cj = torch.full((3, 4), -1, dtype=torch.int32, device="cuda")
+    with pytest.raises(UsfftError):                                   # width < s~
+        B.usfft_detect_carry(ctx, 3, 4, 3, km, km, cj, dp, nd, 0)
+
+
+def test_maximum_parameter_dimension(B, ctx):
+    """d = 64 (kMaxD) coefficient terms on n = 16: samples match the oracle (the psi tables and
+    th_amp at their largest)."""
+    from oracle import fe as ofe
+    cfg = dict(n=16, d=64, amp=[0.3 / (j * j) for j in range(1, 65)], theta="sin", form="affine", f="x2")
+    p = B.usfft_plan_round(ctx, 3, 2, 2, 1, 64, 4, 10, "A", 30)
+    nb = 5
+    u = torch.empty((225, nb), dtype=torch.float64, device="cuda")
+    for precond in ("mg", "jacobi"):
+        assert B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond=precond), p, 0, nb, u, nb, check_conv=True) == 0
+        ref = ofe.sample_pde(cfg, olat.nodes(p.M, p.z, p.shift, 2)[:, :nb])
+        assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
