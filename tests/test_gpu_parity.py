@@ -549,3 +549,42 @@ def test_pcg_mg_large_meshes(B, ctx, monkeypatch, cfgid, n, nb):
     B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond="mg"), p, 3, h, a, h)
     if n != 16:
         assert torch.equal(a, u[:, :h])
+
+
+@pytest.mark.parametrize("d", [1, 2])
+def test_full_run_low_dimensions(B, d):
+    """Degenerate dimensions: d = 1 (Step 1 only, no Step-2 round) and d = 2 (one Step-2 round
+    with s~ = s): the detected set equals the oracle's and the polynomial's support."""
+    from paper_2109_04131_b200.driver import Detector
+    N, G = 12, 3
+    tp = trig_poly(950 + d, d, N, G, 7, real=True, max_active=d)
+    cfg = dict(d=d, N=N, s=12, s_local=12, r=3, seed=d, theta_rel=1e-6, mode="A", G=G)
+    det = Detector(cfg, blackbox=_tp_blackbox(tp))
+    I, C = det.run()
+    ref = ousfft.run(cfg, tp)
+    Ig = I.cpu().numpy().astype(np.int64).reshape(-1, d)
+    assert Ig.tolist() == np.asarray(ref["I"]).reshape(-1, d).tolist()
+    assert {tuple(k) for k in Ig.tolist()} == {tuple(k) for k in tp.freqs.tolist()}
+    cov, coef = det.step3(I.reshape(-1, d).contiguous())
+    c = coef.cpu().numpy()
+    order = {tuple(k): a for a, k in enumerate(tp.freqs.tolist())}
+    want = tp.coefs[:, [order[tuple(k)] for k in Ig.tolist()]]
+    assert np.abs(c[..., 0] + 1j * c[..., 1] - want).max() <= 1e-12
+
+
+@pytest.mark.parametrize("G,M,L,nJ", [(3, 4001, 2, 300)])
+def test_lattice_fft_largest_prime(B, ctx, G, M, L, nJ):
+    """M = 4001 (config 5's Step-2 lattices, the 4000-point Rader template): spectra and keys."""
+    from paper_2109_04131_b200.binding import Plan
+    U, z, J, bins = _round_inputs(G + M, G, M, L, nJ)
+    p = Plan(3, M, L, 3, -1, z, np.zeros(3))
+    Mh = M // 2 + 1
+    spectra = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
+    kmin = torch.empty((G, nJ), dtype=torch.float64, device="cuda")
+    kmax = torch.empty(1, dtype=torch.float64, device="cuda")
+    B.usfft_lattice_fft(ctx, p, G, dev(U, torch.float64), [0, L * M], dev(bins, torch.int32), nJ, spectra, kmin, kmax)
+    sp = spectra.cpu().numpy()
+    ref = np.stack([odft.lattice_dft(U[:, l * M:(l + 1) * M], M, np.arange(Mh)) for l in range(L)], 1)
+    assert np.abs((sp[..., 0] + 1j * sp[..., 1]) / M - ref).max() <= 1e-12 * np.abs(ref).max()
+    km_ref = odet.kappa_min(odft.round_values(U, M, L, bins))
+    assert np.abs(np.sqrt(kmin.cpu().numpy()) - np.sqrt(km_ref)).max() <= 1e-12 * np.sqrt(km_ref.max())
