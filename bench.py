@@ -151,11 +151,16 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
-    local = int(os.environ.get("LOCAL_RANK", "0"))
+    # one GPU per rank; with fewer visible GPUs than ranks (the --backend gloo check of the
+    # multi-rank flow on one GPU) ranks share devices round-robin
+    local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
     torch.cuda.set_device(local)
     group = None
     if world > 1:
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        if args.backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local))
+        else:
+            dist.init_process_group(args.backend)
     cfg = config(args.config)
     if args.precond:
         cfg["precond"] = args.precond
@@ -400,6 +405,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
     ap.add_argument("--verbose", action="store_true")
+    ap.add_argument("--backend", default="nccl", choices=["nccl", "gloo"],
+                    help="process-group backend for N > 1 (gloo: functional check with ranks sharing a GPU)")
     ap.add_argument("--precond", default="", choices=["", "jacobi", "mg"])
     args = ap.parse_args()
     if args.impl == "reference":

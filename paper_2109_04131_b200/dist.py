@@ -49,6 +49,13 @@ class Exchange:
         send = [(gb[q + 1] - gb[q]) * nb for q in range(self.P)]
         recv = [g_loc * (sb[p + 1] - sb[p]) for p in range(self.P)]
         out = torch.empty(sum(recv), dtype=u_local.dtype, device=u_local.device)
+        if u_local.is_cuda and dist.get_backend(self.group) == "gloo":
+            # gloo has no CUDA all-to-all: the multi-process GPU tests (several ranks sharing one
+            # GPU) stage through host memory; NCCL (the product) exchanges device buffers directly
+            host = torch.empty(sum(recv), dtype=u_local.dtype)
+            dist.all_to_all_single(host, u_local.reshape(-1).cpu(), recv, send, group=self.group)
+            out.copy_(host)
+            return out, sb
         dist.all_to_all_single(out, u_local.reshape(-1), recv, send, group=self.group)
         return out, sb
 
