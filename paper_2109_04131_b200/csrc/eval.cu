@@ -240,6 +240,105 @@ k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *
     }
 }
 
+// The accuracy metric on the fp64 tensor pipe: the same DMMA product as k_eval_mma for the real
+// part with A = [Cre | -Cim] and B = [cos; sin], and for the imaginary part with the same A and
+// B' = [sin; -cos] (read from the same staged phases), then |Uref - (re + i im)| per element and
+// per-row partial sums (mean, mean square, max) over the CTA's 64 columns in a fixed order, the
+// layout of k_eval_err's partials.
+__global__ void __launch_bounds__(256)
+k_eval_err_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
+               int64_t G, const double *__restrict__ Y, int64_t n, const double *__restrict__ Uref,
+               double *__restrict__ part) {
+    constexpr int TK = 12, K2 = 2 * TK, TG = 64, WT = TG / 16;
+    __shared__ double As[TG][K2 + 1];                     // [g][k]: Cre (k < TK), -Cim (k >= TK)
+    __shared__ double Bs[K2][EV_TQ + 1];                  // [k][q]: cos (k < TK), sin (k >= TK)
+    __shared__ double red[TG][4][3];
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int wg = warp >> 2, wq = warp & 3;
+    const int64_t g0 = (int64_t)blockIdx.y * TG, q0 = (int64_t)blockIdx.x * EV_TQ;
+    double are[WT][2][2] = {}, aim[WT][2][2] = {};
+    for (int64_t k0 = 0; k0 < nI; k0 += TK) {
+        for (int e = threadIdx.x; e < TK * TG; e += blockDim.x) {
+            const int kk = e / TG, gg = e % TG;
+            double2 v = make_double2(0.0, 0.0);
+            if (k0 + kk < nI && g0 + gg < G) v = C[(g0 + gg) * nI + k0 + kk];
+            As[gg][kk] = v.x;
+            As[gg][TK + kk] = -v.y;
+        }
+        for (int e = threadIdx.x; e < TK * EV_TQ; e += blockDim.x) {
+            const int kk = e / EV_TQ, qq = e % EV_TQ;
+            double c = 0.0, sv = 0.0;
+            if (k0 + kk < nI && q0 + qq < n) {
+                double ph = 0.0;
+                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
+                sincospi(2.0 * (ph - rint(ph)), &sv, &c);
+            }
+            Bs[kk][qq] = c;
+            Bs[TK + kk][qq] = sv;
+        }
+        __syncthreads();
+#pragma unroll
+        for (int k = 0; k < K2; k += 4) {
+            double a[WT], b[2], bi[2];
+#pragma unroll
+            for (int t = 0; t < WT; ++t) a[t] = As[8 * WT * wg + 8 * t + (lane >> 2)][k + (lane & 3)];
+#pragma unroll
+            for (int u2 = 0; u2 < 2; ++u2) {
+                const int col = 16 * wq + 8 * u2 + (lane >> 2);
+                b[u2] = Bs[k + (lane & 3)][col];
+                bi[u2] = k < TK ? Bs[TK + k + (lane & 3)][col] : -Bs[k - TK + (lane & 3)][col];
+            }
+#pragma unroll
+            for (int t = 0; t < WT; ++t)
+#pragma unroll
+                for (int u2 = 0; u2 < 2; ++u2) {
+                    dmma_8x8x4(are[t][u2][0], are[t][u2][1], a[t], b[u2]);
+                    dmma_8x8x4(aim[t][u2][0], aim[t][u2][1], a[t], bi[u2]);
+                }
+        }
+        __syncthreads();
+    }
+#pragma unroll
+    for (int t = 0; t < WT; ++t) {
+        const int r = 8 * WT * wg + 8 * t + (lane >> 2);
+        const int64_t g = g0 + r;
+        double s1 = 0.0, s2s = 0.0, mx = 0.0;
+#pragma unroll
+        for (int u2 = 0; u2 < 2; ++u2)
+#pragma unroll
+            for (int h = 0; h < 2; ++h) {
+                const int64_t q = q0 + 16 * wq + 8 * u2 + 2 * (lane & 3) + h;
+                if (g < G && q < n) {
+                    const double m = hypot(Uref[g * n + q] - are[t][u2][h], -aim[t][u2][h]);
+                    s1 += m;
+                    s2s = fma(m, m, s2s);
+                    mx = fmax(mx, m);
+                }
+            }
+#pragma unroll
+        for (int o = 1; o < 4; o <<= 1) {           // the 4 lanes of one row
+            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
+            s2s += __shfl_xor_sync(0xffffffffu, s2s, o);
+            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+        }
+        if ((lane & 3) == 0) {
+            red[r][wq][0] = s1;
+            red[r][wq][1] = s2s;
+            red[r][wq][2] = mx;
+        }
+    }
+    __syncthreads();
+    const int64_t ntile = gridDim.x;
+    for (int r = threadIdx.x; r < TG; r += blockDim.x) {             // the 4 column groups, in order
+        const int64_t g = g0 + r;
+        if (g >= G) continue;
+        double *pp = part + (g * ntile + blockIdx.x) * 3;
+        pp[0] = ((red[r][0][0] + red[r][1][0]) + red[r][2][0]) + red[r][3][0];
+        pp[1] = ((red[r][0][1] + red[r][1][1]) + red[r][2][1]) + red[r][3][1];
+        pp[2] = fmax(fmax(red[r][0][2], red[r][1][2]), fmax(red[r][2][2], red[r][3][2]));
+    }
+}
+
 }  // namespace usfft
 
 using namespace usfft;
@@ -258,7 +357,12 @@ extern "C" usfft_status usfft_eval_err(usfft_ctx *c, int32_t d, const int16_t *I
     if (s) return s;
     double *part = static_cast<double *>(c->ws);
     dim3 grid((unsigned)ntile, (unsigned)((G + EV_TG - 1) / EV_TG));
-    k_eval_err<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref, part);
+    const char *force = getenv("USFFT_EVAL");                // =fma: CUDA-core variant
+    if (force && force[0] == 'f')
+        k_eval_err<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref, part);
+    else
+        k_eval_err_mma<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref,
+                                                     part);
     USFFT_CHECK_LAUNCH(c);
     k_eval_err_reduce<<<grid1d(G, 128), 128, 0, c->stream>>>(G, ntile, n, part, err);
     USFFT_CHECK_LAUNCH(c);

@@ -520,6 +520,14 @@ def test_eval_tensor_and_fma_variants(B, ctx, monkeypatch):
         U = torch.empty((G, n), dtype=torch.float64, device="cuda")
         B.usfft_eval(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), U)
         assert np.abs(U.cpu().numpy() - ref).max() <= 1e-11 * np.abs(Cc).sum(1).max()
+        # the accuracy metric through the same variant: complex modulus errors
+        # against a reference with a known offset from the approximant
+        Uref = rng.standard_normal((G, n))
+        err = torch.empty((G, 3), dtype=torch.float64, device="cuda")
+        B.usfft_eval_err(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), dev(Uref, torch.float64), err)
+        D = np.abs(Uref - oeval.evaluate(I, Cc, Y))
+        want = np.stack([D.mean(1), np.sqrt((D * D).mean(1)), D.max(1)], 1)
+        assert np.abs(err.cpu().numpy() - want).max() <= 1e-11 * want.max()
     monkeypatch.delenv("USFFT_EVAL")
 
 

@@ -33,6 +33,17 @@ def main():
         ms = e0.elapsed_time(e1) / 5
         flops = 2.0 * G * n * 2 * nI
         print(f"{mode}: {ms:.3f} ms, {flops / ms / 1e9:.2f} TFLOP/s (G={G} n={n} |I|={nI})")
+        # the accuracy metric: real and imaginary parts (twice the products) + errors
+        err = torch.empty((G, 3), dtype=torch.float64, device="cuda")
+        B.usfft_eval_err(ctx, I, C, Y, U, err)
+        torch.cuda.synchronize()
+        e0.record()
+        for _ in range(5):
+            B.usfft_eval_err(ctx, I, C, Y, U, err)
+        e1.record()
+        torch.cuda.synchronize()
+        ms = e0.elapsed_time(e1) / 5
+        print(f"{mode} eval_err: {ms:.3f} ms, {2 * flops / ms / 1e9:.2f} TFLOP/s")
 
 
 if __name__ == "__main__":
