@@ -505,13 +505,15 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 const int h = tid & 1, i = min(tid >> 1, U2 - 1);
                 const bool own = tid < 2 * U2;
                 const double *kp = Kt + h * HK * U2 + i, *rp = R2 + h * HK;
-                double a0 = 0.0, a1 = 0.0;
+                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;    // four chains (DFMA latency)
 #pragma unroll
-                for (int c = 0; c < HK; c += 2) {
+                for (int c = 0; c < HK; c += 4) {
                     a0 = fma(kp[c * U2], rp[c], a0);
                     if (c + 1 < HK) a1 = fma(kp[(c + 1) * U2], rp[c + 1], a1);
+                    if (c + 2 < HK) a2 = fma(kp[(c + 2) * U2], rp[c + 2], a2);
+                    if (c + 3 < HK) a3 = fma(kp[(c + 3) * U2], rp[c + 3], a3);
                 }
-                double sv = a0 + a1;
+                double sv = (a0 + a1) + (a2 + a3);
                 sv += __shfl_xor_sync(0xffffffffu, sv, 1);       // whole warps take part
                 if (own && h == 0) S2[(i / (m2 - 1) + 1) * P2 + i % (m2 - 1) + 1] = sv;
             }
