@@ -26,6 +26,8 @@ struct usfft_ctx {
     // general device workspace — grows on demand
     void *ws = nullptr;
     size_t ws_size = 0;
+    void *ws2 = nullptr;                                          // second workspace (eval phases)
+    size_t ws2_size = 0;
     // small device scalar area (counters, maxima): 4 KB allocated at init
     void *dscal = nullptr;
     // cached tables

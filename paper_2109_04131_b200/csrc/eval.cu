@@ -182,15 +182,34 @@ __device__ __forceinline__ void dmma_8x8x4(double &d0, double &d1, double a, dou
                  : "+d"(d0), "+d"(d1) : "d"(a), "d"(b));
 }
 
+// The right operand once per call: E[0][k][q] = cos(2 pi k.y_q), E[1][k][q] = sin(2 pi k.y_q), with
+// k.y_q reduced mod 1 before sincospi exactly as in the tile kernels (bit-identical values).  The
+// DMMA kernels then stream E tiles instead of regenerating them for every row tile.
+__global__ void k_phases(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double *__restrict__ Y,
+                         int64_t n, double *__restrict__ E) {
+    const int64_t q = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
+    const int64_t k = blockIdx.y;
+    if (q >= n) return;
+    double ph = 0.0;
+    for (int j = 0; j < d; ++j) ph += (double)I[k * d + j] * Y[(int64_t)j * n + q];
+    double c, sv;
+    sincospi(2.0 * (ph - rint(ph)), &sv, &c);
+    E[k * n + q] = c;
+    E[(nI + k) * n + q] = sv;
+}
+
 __global__ void __launch_bounds__(256)
 k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
-           int64_t G, const double *__restrict__ Y, int64_t n, double *__restrict__ U) {
+           int64_t G, const double *__restrict__ Y, int64_t n, double *__restrict__ U,
+           const double *__restrict__ E) {
     constexpr int TK = 12, K2 = 2 * TK, TG = 128, WT = TG / 16;      // WT row tiles per warp
     __shared__ double As[TG][K2 + 1];                     // [g][k]: Cre (k < TK), -Cim (k >= TK)
     __shared__ double Bs[K2][EV_TQ + 1];                  // [k][q]: cos (k < TK), sin (k >= TK)
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wg = warp >> 2, wq = warp & 3;
-    const int64_t g0 = (int64_t)blockIdx.y * TG, q0 = (int64_t)blockIdx.x * EV_TQ;
+    // with precomputed phases the row tiles of one column tile are neighbours in the grid (x), so
+    // its E tile is read from L2 once for all of them
+    const int64_t g0 = (int64_t)(E ? blockIdx.x : blockIdx.y) * TG, q0 = (int64_t)(E ? blockIdx.y : blockIdx.x) * EV_TQ;
     double acc[WT][2][2] = {};
     for (int64_t k0 = 0; k0 < nI; k0 += TK) {
         for (int e = threadIdx.x; e < TK * TG; e += blockDim.x) {
@@ -204,9 +223,14 @@ k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *
             const int kk = e / EV_TQ, qq = e % EV_TQ;
             double c = 0.0, sv = 0.0;
             if (k0 + kk < nI && q0 + qq < n) {
-                double ph = 0.0;
-                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
-                sincospi(2.0 * (ph - rint(ph)), &sv, &c);
+                if (E) {
+                    c = __ldg(E + (k0 + kk) * n + q0 + qq);
+                    sv = __ldg(E + (nI + k0 + kk) * n + q0 + qq);
+                } else {
+                    double ph = 0.0;
+                    for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
+                    sincospi(2.0 * (ph - rint(ph)), &sv, &c);
+                }
             }
             Bs[kk][qq] = c;
             Bs[TK + kk][qq] = sv;
@@ -248,14 +272,15 @@ k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *
 __global__ void __launch_bounds__(256)
 k_eval_err_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
                int64_t G, const double *__restrict__ Y, int64_t n, const double *__restrict__ Uref,
-               double *__restrict__ part) {
+               double *__restrict__ part, const double *__restrict__ E) {
     constexpr int TK = 12, K2 = 2 * TK, TG = 64, WT = TG / 16;
     __shared__ double As[TG][K2 + 1];                     // [g][k]: Cre (k < TK), -Cim (k >= TK)
     __shared__ double Bs[K2][EV_TQ + 1];                  // [k][q]: cos (k < TK), sin (k >= TK)
     __shared__ double red[TG][4][3];
     const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
     const int wg = warp >> 2, wq = warp & 3;
-    const int64_t g0 = (int64_t)blockIdx.y * TG, q0 = (int64_t)blockIdx.x * EV_TQ;
+    const int64_t ti = E ? blockIdx.y : blockIdx.x, ntile = E ? gridDim.y : gridDim.x;   // column tile
+    const int64_t g0 = (int64_t)(E ? blockIdx.x : blockIdx.y) * TG, q0 = ti * EV_TQ;
     double are[WT][2][2] = {}, aim[WT][2][2] = {};
     for (int64_t k0 = 0; k0 < nI; k0 += TK) {
         for (int e = threadIdx.x; e < TK * TG; e += blockDim.x) {
@@ -269,9 +294,14 @@ k_eval_err_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const doubl
             const int kk = e / EV_TQ, qq = e % EV_TQ;
             double c = 0.0, sv = 0.0;
             if (k0 + kk < nI && q0 + qq < n) {
-                double ph = 0.0;
-                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
-                sincospi(2.0 * (ph - rint(ph)), &sv, &c);
+                if (E) {
+                    c = __ldg(E + (k0 + kk) * n + q0 + qq);
+                    sv = __ldg(E + (nI + k0 + kk) * n + q0 + qq);
+                } else {
+                    double ph = 0.0;
+                    for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
+                    sincospi(2.0 * (ph - rint(ph)), &sv, &c);
+                }
             }
             Bs[kk][qq] = c;
             Bs[TK + kk][qq] = sv;
@@ -328,11 +358,10 @@ k_eval_err_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const doubl
         }
     }
     __syncthreads();
-    const int64_t ntile = gridDim.x;
     for (int r = threadIdx.x; r < TG; r += blockDim.x) {             // the 4 column groups, in order
         const int64_t g = g0 + r;
         if (g >= G) continue;
-        double *pp = part + (g * ntile + blockIdx.x) * 3;
+        double *pp = part + (g * ntile + ti) * 3;
         pp[0] = ((red[r][0][0] + red[r][1][0]) + red[r][2][0]) + red[r][3][0];
         pp[1] = ((red[r][0][1] + red[r][1][1]) + red[r][2][1]) + red[r][3][1];
         pp[2] = fmax(fmax(red[r][0][2], red[r][1][2]), fmax(red[r][2][2], red[r][3][2]));
@@ -342,6 +371,29 @@ k_eval_err_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const doubl
 }  // namespace usfft
 
 using namespace usfft;
+
+namespace {
+// The phase matrix E [2][nI][n] in the second ctx workspace when it fits (<= 4 GiB) and the
+// column tiles fit the grid's y dimension; NULL: the kernels generate phases per tile.
+// USFFT_EVAL_PHASES=tile forces the per-tile generation.
+const double *phase_matrix(usfft_ctx *c, int32_t d, const int16_t *I, int64_t nI, const double *Y, int64_t n,
+                           usfft_status *st) {
+    *st = USFFT_OK;
+    const char *pv = getenv("USFFT_EVAL_PHASES");
+    if ((pv && pv[0] == 't') || nI == 0) return nullptr;
+    const size_t bytes = sizeof(double) * 2 * (size_t)nI * (size_t)n;
+    if (bytes > (size_t(4) << 30) || (n + EV_TQ - 1) / EV_TQ > 65535 || nI > 65535) return nullptr;
+    if ((*st = ensure(c, &c->ws2, &c->ws2_size, bytes))) return nullptr;
+    double *E = static_cast<double *>(c->ws2);
+    dim3 grid((unsigned)((n + 255) / 256), (unsigned)nI);
+    k_phases<<<grid, 256, 0, c->stream>>>(d, I, nI, Y, n, E);
+    if (cudaPeekAtLastError() != cudaSuccess) {
+        *st = fail(c, USFFT_ECUDA, "k_phases launch: %s", cudaGetErrorString(cudaGetLastError()));
+        return nullptr;
+    }
+    return E;
+}
+}  // namespace
 
 extern "C" usfft_status usfft_eval_err(usfft_ctx *c, int32_t d, const int16_t *I, int64_t nI,
                                        const double *C, int64_t G, const double *Y, int64_t n,
@@ -360,9 +412,14 @@ extern "C" usfft_status usfft_eval_err(usfft_ctx *c, int32_t d, const int16_t *I
     const char *force = getenv("USFFT_EVAL");                // =fma: CUDA-core variant
     if (force && force[0] == 'f')
         k_eval_err<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref, part);
-    else
-        k_eval_err_mma<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref,
-                                                     part);
+    else {
+        usfft_status st = USFFT_OK;
+        const double *E = phase_matrix(c, d, I, nI, Y, n, &st);
+        if (st) return st;
+        const dim3 gr = E ? dim3((unsigned)((G + EV_TG - 1) / EV_TG), (unsigned)ntile) : grid;
+        k_eval_err_mma<<<gr, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref,
+                                                   part, E);
+    }
     USFFT_CHECK_LAUNCH(c);
     k_eval_err_reduce<<<grid1d(G, 128), 128, 0, c->stream>>>(G, ntile, n, part, err);
     USFFT_CHECK_LAUNCH(c);
@@ -383,8 +440,12 @@ extern "C" usfft_status usfft_eval(usfft_ctx *c, int32_t d, const int16_t *I, in
     if (force && force[0] == 'f')
         k_eval<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
     else {
-        dim3 gm((unsigned)((n + EV_TQ - 1) / EV_TQ), (unsigned)((G + 127) / 128));
-        k_eval_mma<<<gm, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
+        usfft_status st = USFFT_OK;
+        const double *E = phase_matrix(c, d, I, nI, Y, n, &st);
+        if (st) return st;
+        const unsigned nq = (unsigned)((n + EV_TQ - 1) / EV_TQ), ng = (unsigned)((G + 127) / 128);
+        const dim3 gm = E ? dim3(ng, nq) : dim3(nq, ng);
+        k_eval_mma<<<gm, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U, E);
     }
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;

@@ -514,8 +514,11 @@ def test_eval_tensor_and_fma_variants(B, ctx, monkeypatch):
     Y = rng.random((d, n))
     ref = oeval.evaluate(I, Cc, Y).real
     Cd = dev(np.stack([Cc.real, Cc.imag], -1), torch.float64)
-    for mode in ("mma", "fma"):
+    for mode in ("mma", "mma-tile", "fma"):
+        if mode == "mma-tile":
+            monkeypatch.setenv("USFFT_EVAL_PHASES", "tile")
         if mode == "fma":
+            monkeypatch.delenv("USFFT_EVAL_PHASES")
             monkeypatch.setenv("USFFT_EVAL", "fma")
         U = torch.empty((G, n), dtype=torch.float64, device="cuda")
         B.usfft_eval(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), U)
