@@ -1,6 +1,6 @@
-"""Two ranks on one GPU (gloo, processes sharing cuda:0): the whole multi-rank driver path —
-sample sharding, the transpose into node slabs, kappa_max MAX, votes SUM, per-rank resolve and
-Step 3 — gives the single-process result bit for bit (all exchanges are data
+"""Two and three ranks on one GPU (gloo, processes sharing cuda:0): the whole multi-rank driver
+path — sample sharding, the transpose into node slabs, kappa_max MAX, votes SUM, per-rank resolve,
+Step 3, the accuracy metric and the moments — gives the single-process result bit for bit (all exchanges are data
 movement or order-free).  The product exchanges over NCCL; gloo stages the all-to-all through
 the host here because NCCL needs one GPU per rank."""
 import os
@@ -23,10 +23,15 @@ def _free_port():
 
 def _run(cfg):
     from paper_2109_04131_b200.driver import Detector
+    from usfft_inputs import uniform_points
     det = Detector(cfg)
     I, coef = det.run()
     cov, c3 = det.step3(I)
-    return I.cpu().numpy(), coef.cpu().numpy(), c3.cpu().numpy(), det.g0, det.g1
+    Y = torch.as_tensor(uniform_points(17, cfg["d"], 257), dtype=torch.float64, device="cuda")
+    err, _ = det.errors(I, c3, Y)                               # test solves sharded over ranks
+    E, var, gsi = det.moments(I, c3)
+    return (I.cpu().numpy(), coef.cpu().numpy(), c3.cpu().numpy(), err.cpu().numpy(),
+            torch.cat([E, var[:, None], gsi], 1).cpu().numpy(), det.g0, det.g1)
 
 
 def _worker(rank, world, port, cfg, q):
@@ -48,7 +53,7 @@ def test_multirank_detector_matches_single_process(world):
     import torch.multiprocessing as mp
     from usfft_inputs import config
     cfg = config(1)
-    ref_I, ref_coef, ref_c3, _, _ = _run(cfg)
+    ref_I, ref_coef, ref_c3, ref_err, ref_mom, _, _ = _run(cfg)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = _free_port()
@@ -60,7 +65,9 @@ def test_multirank_detector_matches_single_process(world):
         p.join(timeout=120)
         assert p.exitcode == 0
     for r in range(world):
-        I, coef, c3, g0, g1 = res[r]
+        I, coef, c3, err, mom, g0, g1 = res[r]
         assert np.array_equal(I, ref_I)                       # identical detected set on every rank
         assert np.array_equal(coef, ref_coef[g0:g1])          # this rank's nodes, bit for bit
         assert np.array_equal(c3, ref_c3[g0:g1])
+        assert np.array_equal(err, ref_err[g0:g1])            # accuracy metric of this rank's nodes
+        assert np.array_equal(mom, ref_mom[g0:g1])            # expectation, variance, GSI
