@@ -46,13 +46,16 @@ def _worker(rank, world, port, cfg, q):
         dist.destroy_process_group()
 
 
-@pytest.mark.parametrize("world", [2, 3])
-def test_multirank_detector_matches_single_process(world):
+@pytest.mark.parametrize("world,key_chunk", [(2, 0), (3, 0), (2, 64)])
+def test_multirank_detector_matches_single_process(world, key_chunk):
+    """key_chunk > 0: every Step-2 selection streamed over candidate chunks (Z29) on every rank."""
     if not torch.cuda.is_available():
         pytest.skip("no CUDA device")
     import torch.multiprocessing as mp
     from usfft_inputs import config
     cfg = config(1)
+    if key_chunk:
+        cfg["key_chunk"] = key_chunk
     ref_I, ref_coef, ref_c3, ref_err, ref_mom, _, _ = _run(cfg)
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
