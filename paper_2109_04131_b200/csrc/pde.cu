@@ -1,4 +1,4 @@
-// pde.cu — K3 coefficient field + K4 batched Jacobi-PCG: one P1 FE solve per lattice node.
+// pde.cu — K3 coefficient field + K4 batched preconditioned CG: one P1 FE solve per lattice node.
 // usfft_sample_pde (include/usfft.h; a4 + a5 of SURVEY §8(a)).
 //
 // Discretisation (DESIGN.md §3 Z11/Z12): on the uniform "/" triangulation the P1 stiffness of
@@ -7,14 +7,15 @@
 //     w_h(i,j) = (a(T_lo(i,j)) + a(T_up(i,j-1)))/2,  w_v(i,j) = (a(T_up(i,j)) + a(T_lo(i-1,j)))/2,
 // T_lo(ci,cj) centroid ((ci+2/3)h, (cj+1/3)h), T_up(ci,cj) centroid ((ci+1/3)h, (cj+2/3)h);
 // the centroid load of f = x2 is b_p = h^2 x2_p (closed form); other f (Z28) come from a table
-// b_p = (h^2/6) sum of f over the centroids of the six triangles around p (k_rhs).  (The oracle assembles element by element; a
-// CPU test checks this stencil against that assembly.)
+// b_p = (h^2/6) sum of f over the centroids of the six triangles around p (k_rhs).  (The oracle
+// assembles element by element; a CPU test checks this stencil against that assembly.)
 //
-// One CTA solves one sample at a time (persistent loop over samples).  The padded node grid
-// (n+1)^2 holds p with a zero Dirichlet ring, so the stencil needs no bounds checks.  Per-sample
-// state lives in shared memory when it fits (n <= 64) and in a per-CTA global scratch slab
-// otherwise; the per-thread q values stay in registers.  Block reductions are fixed trees, so a
-// sample's result does not depend on which CTA or rank solved it.
+// Kernels (one CTA per sample, persistent loop over samples, fixed-tree reductions so a sample's
+// result does not depend on which CTA or rank solved it):
+//   k_pcg_mg  (pcg_mg.cuh)   multigrid-preconditioned CG, fine level in registers, n = 16, 32
+//   k_pcg_mgg (pcg_mgg.cuh)  multigrid-preconditioned CG, per-CTA scratch slab, n = 8 .. 128
+//   k_pcg_reg (pcg_reg.cuh)  Jacobi PCG, register-resident, n = 16, 32
+//   k_pcg     (below)        Jacobi PCG, shared memory (n <= 64) or a global slab, any n
 #include <cstdlib>
 
 #include "lattice.cuh"
