@@ -69,7 +69,10 @@ struct Mg3 {
     static constexpr int oL1 = 3 * NP2;
     static constexpr int oL2 = oL1 + 7 * N1;             // WH2, WV2, D2, DI2, S2 (N2 each), R2 (U2)
     static constexpr int oK = oL2 + 5 * N2 + 2 * HK;     // R2 padded to 2 HK (zero tail)
-    static constexpr int oWH3 = oK + 2 * HK * U2, oWV3 = oWH3 + N3, oAI = oWV3 + N3;   // K: 2 HK columns
+    // K: 2 HK columns of U2; the second half starts KPAD doubles later so that the two halves a
+    // warp reads together (thread pairs (i, h)) fall into disjoint shared-memory banks
+    static constexpr int KPAD = (8 - (HK * U2) % 16 + 16) % 16;
+    static constexpr int oWH3 = oK + 2 * HK * U2 + KPAD, oWV3 = oWH3 + N3, oAI = oWV3 + N3;
     static constexpr int oB = oAI + U3 * U3, oC = oB + U3 * U2;
     __host__ __device__ static constexpr int doubles() { return oC + U3 * U2; }
     // the psi tables S[plane][j][m] ((1 or 2) x d x (3n+1)) are staged after these when they
@@ -353,7 +356,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         __syncthreads();
         USFFT_MG_SMARK(29);
-        for (int e = U2 * U2 + tid; e < 2 * HK * U2; e += NT) Kt[e] = 0.0;   // zero pad column(s)
+        auto kix = [](int col, int row) -> int { return col * U2 + row + (col >= HK ? L::KPAD : 0); };
+        for (int e = U2 * U2 + tid; e < 2 * HK * U2; e += NT) Kt[kix(e / U2, e % U2)] = 0.0;   // zero pad column(s)
         if (tid < 2 * HK - U2) R2[U2 + tid] = 0.0;                           // and R2 tail
         {   // K = B^T C (rank-U3 product) in register tiles: thread (ti, tk) of a 16 x NT/16 grid
             // owns rows ti + 16 m and columns tk + TK n
@@ -381,7 +385,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
                 for (int q = 0; q < CK; ++q) {
                     const int i = ti + 16 * m, k = tk + TK * q;
-                    if (i < U2 && k < U2) Kt[k * U2 + i] = acc[m][q];
+                    if (i < U2 && k < U2) Kt[kix(k, i)] = acc[m][q];
                 }
         }
         __syncthreads();
@@ -389,11 +393,11 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             const int i = e % U2, d = e / U2;
             const int Ii = i % (m2 - 1) + 1, Ji = i / (m2 - 1) + 1, ei = Ji * P2 + Ii;
             const double dwi = DI2[ei];
-            if (d == 0) Kt[i * U2 + i] += fma(-dwi * D2[ei], dwi, 2.0 * dwi);
-            else if (d == 1 && Ii < m2 - 1) Kt[(i + 1) * U2 + i] += dwi * WH2[ei] * DI2[ei + 1];
-            else if (d == 2 && Ii > 1) Kt[(i - 1) * U2 + i] += dwi * WH2[ei - 1] * DI2[ei - 1];
-            else if (d == 3 && Ji < m2 - 1) Kt[(i + (m2 - 1)) * U2 + i] += dwi * WV2[ei] * DI2[ei + P2];
-            else if (d == 4 && Ji > 1) Kt[(i - (m2 - 1)) * U2 + i] += dwi * WV2[ei - P2] * DI2[ei - P2];
+            if (d == 0) Kt[kix(i, i)] += fma(-dwi * D2[ei], dwi, 2.0 * dwi);
+            else if (d == 1 && Ii < m2 - 1) Kt[kix(i + 1, i)] += dwi * WH2[ei] * DI2[ei + 1];
+            else if (d == 2 && Ii > 1) Kt[kix(i - 1, i)] += dwi * WH2[ei - 1] * DI2[ei - 1];
+            else if (d == 3 && Ji < m2 - 1) Kt[kix(i + (m2 - 1), i)] += dwi * WV2[ei] * DI2[ei + P2];
+            else if (d == 4 && Ji > 1) Kt[kix(i - (m2 - 1), i)] += dwi * WV2[ei - P2] * DI2[ei - P2];
         }
         // (the first barriers of the CG loop order these writes before their uses)
 
@@ -504,7 +508,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 // thread (i, h): half h of row i; K and R2 carry a zero column / entry past U2
                 const int h = tid & 1, i = min(tid >> 1, U2 - 1);
                 const bool own = tid < 2 * U2;
-                const double *kp = Kt + h * HK * U2 + i, *rp = R2 + h * HK;
+                const double *kp = Kt + h * (HK * U2 + L::KPAD) + i, *rp = R2 + h * HK;
                 double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;    // four chains (DFMA latency)
 #pragma unroll
                 for (int c = 0; c < HK; c += 4) {
