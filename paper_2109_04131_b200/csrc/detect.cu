@@ -174,12 +174,10 @@ k_select_warp(const double *__restrict__ kmin, int64_t nJ, int64_t G, const doub
         key[k] = j < nJ ? __ldg(row + j) : 0ull;
     }
     auto count_ge = [&](unsigned long long t) -> int {
-        int c = 0;
+        unsigned c = 0;
 #pragma unroll
-        for (int k = 0; k < KPL; ++k) c += key[k] >= t ? 1 : 0;
-#pragma unroll
-        for (int o = 16; o > 0; o >>= 1) c += __shfl_xor_sync(0xffffffffu, c, o);
-        return c;
+        for (int k = 0; k < KPL; ++k) c += key[k] >= t ? 1u : 0u;
+        return (int)__reduce_add_sync(0xffffffffu, c);   // one warp-reduce instruction (sm_80+)
     };
     unsigned long long T = 0ull;
     if ((int64_t)s_tilde < nJ) {
@@ -189,11 +187,10 @@ k_select_warp(const double *__restrict__ kmin, int64_t nJ, int64_t G, const doub
         }
     }
     // members: key > T, and the first need_eq keys == T by index (T = 0: every key qualifies)
-    int gt = 0;
+    unsigned gtl = 0;
 #pragma unroll
-    for (int k = 0; k < KPL; ++k) gt += key[k] > T ? 1 : 0;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) gt += __shfl_xor_sync(0xffffffffu, gt, o);
+    for (int k = 0; k < KPL; ++k) gtl += key[k] > T ? 1u : 0u;
+    const int gt = (int)__reduce_add_sync(0xffffffffu, gtl);
     const int need_eq = (int64_t)s_tilde < nJ ? s_tilde - gt : KPL * 32;
     const unsigned lt = (1u << lane) - 1u;
     int eq_run = 0, out_run = 0;
