@@ -186,7 +186,7 @@ def run_ours(args):
     clocks.start()
     torch.cuda.cudart().cudaProfilerStart()          # ncu --profile-from-start off: timed steps only
     launches0 = det.ctx.launches()
-    step_ms, phase, iters_sum, samples = [], {}, 0, 0
+    step_ms, phase_runs, iters_sum, samples = [], {}, 0, 0
     det.timing = False                               # no per-phase events / syncs inside timed steps
     for k in range(args.steps):
         flush.fill_(float(k))                         # evict L2 between timed iterations
@@ -206,7 +206,9 @@ def run_ours(args):
     launches = det.ctx.launches() - launches0
     torch.cuda.cudart().cudaProfilerStop()
     clk = clocks.stop()
-    # per-phase breakdown from the same rounds re-run untimed with per-phase CUDA events
+    # per-phase breakdown from the same rounds re-run untimed with per-phase CUDA events; the
+    # events bracket host-side enqueue gaps too, so one slow re-run (allocator growth, a host
+    # hiccup) would skew a mean: each phase reports its median over the K re-runs
     det.timing = True
     for k in range(args.steps):
         flush.fill_(float(k))
@@ -215,9 +217,11 @@ def run_ours(args):
             print(f"phases {k}: " + " ".join(f"{a}={b:.3f}" for a, b in res_p.times.items()),
                   file=sys.stderr, flush=True)
         for name, ms in res_p.times.items():
-            phase[name] = phase.get(name, 0.0) + ms
+            phase_runs.setdefault(name, []).append(ms)
+    phase = {name: float(np.median(v)) for name, v in phase_runs.items()}      # ms per step
     total_ms = float(np.sum(step_ms))
-    t_tensor = torch.tensor([total_ms, phase.get("pde", 0.0)], dtype=torch.float64, device="cuda")
+    t_tensor = torch.tensor([total_ms, phase.get("pde", 0.0) * args.steps], dtype=torch.float64,
+                            device="cuda")
     it_tensor = torch.tensor([iters_sum], dtype=torch.int64, device="cuda")
     if world > 1:
         dist.all_reduce(t_tensor, op=dist.ReduceOp.MAX)
@@ -287,7 +291,7 @@ def run_ours(args):
         flops = fpi * iters_all
         fp64_peak = 148 * FP64_FMA_PER_CLK_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
         ach = flops / (pde_ms / 1e3) / 1e12 / world if pde_ms > 0 else 0.0
-        fft_ms = phase.get("fft", 0.0) / args.steps
+        fft_ms = phase.get("fft", 0.0)
         Mh = P.M // 2 + 1
         fft_bytes = G * P.L * P.M * 8 + G * P.L * Mh * 16
         line = {
@@ -311,7 +315,8 @@ def run_ours(args):
                     "achieved_gbs": fft_bytes / (fft_ms / 1e3) / 1e9 if fft_ms else None,
                     "hbm_peak_gbs": pk["hbm_gbs"],
                     "frac": (fft_bytes / (fft_ms / 1e3) / 1e9) / pk["hbm_gbs"] if fft_ms else None},
-            "phase_ms_per_step": {k: v / args.steps for k, v in phase.items()},
+            "phase_ms_per_step": phase,
+            "phase_stat": "median over the K untimed re-runs with per-phase events",
             "e2e": {"value": samples / (e2e_t.item() / 1e3) if e2e_t.item() else None, "unit": UNIT,
                     "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h},
             "gpu_launches": launches,
