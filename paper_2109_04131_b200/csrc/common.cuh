@@ -34,6 +34,7 @@ struct usfft_ctx {
     std::map<int64_t, double2 *> twiddles;                  // M -> e^{-2 pi i m/M}, m < M
     std::map<std::tuple<int, int, int>, double *> sintab;    // (n, d, psi) -> psi factor tables
     std::map<std::pair<int, int>, double *> rhstab;          // (n, f_kind) -> centroid loads b
+    std::map<std::tuple<int, int, int, int, int>, double *> x0tab;   // (n, d, psi, form, f_kind) -> k_pcg_mg initial-guess basis
     // resident blocks per SM per (kernel, threads, smem): the query costs ~10 us per call
     std::map<std::pair<const void *, size_t>, int> occupancy;
 };

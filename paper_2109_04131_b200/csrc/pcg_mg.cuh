@@ -147,10 +147,25 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #ifdef USFFT_MG_PROBE
         if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][20] = clock64();
 #endif
+        // initial guess (Z31): k_x0_guess left x0 in this sample's column of u; the loads are
+        // issued here so that their latency hides behind the setup
+        double x0[BR][BC];
+        if (Q.x0b) {
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+#pragma unroll
+                for (int c = 0; c < BC; ++c)
+                    x0[q][c] = (col0 + c + 1 <= nx && row0 + q + 1 <= nx)
+                                   ? u[(int64_t)((row0 + q) * nx + col0 + c) * ldu + bl] : 0.0;
+        }
         // ---- K3: coefficients ----------------------------------------------------------------
         for (int j = tid; j < Q.d; j += blockDim.x) {      // d may exceed the CTA (n = 16: 32 threads)
-            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
-            th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
+            if (Q.thov) {
+                th_amp[j] = Q.thov[bl * Q.d + j];
+            } else {
+                const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
+                th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
+            }
         }
         __syncthreads();
         USFFT_MG_SMARK(24);
@@ -588,6 +603,27 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                         : Bt ? __ldg(Bt + (row0 + q) * nx + col0 + c)                // the load table
                              : (double)(row0 + q + 1) * inv_n3;
             }
+        // ||b||^2 partial (reduced with the first iteration's dots), then r0 = b - A x0 for the
+        // initial guess loaded from u at the top of the sample (k_x0_guess, DESIGN Z31); without
+        // a basis x0 = 0 and r0 = b (Z13)
+        double bbp = 0.0;
+#pragma unroll
+        for (int q = 0; q < BR; ++q)
+#pragma unroll
+            for (int c = 0; c < BC; ++c) bbp = fma(r[q][c], r[q][c], bbp);
+        if (Q.x0b) {
+            double ax[BR][BC];
+            publish(G1, x0);
+            __syncthreads();
+            apply_fine(G1, x0, ax);
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+#pragma unroll
+                for (int c = 0; c < BC; ++c) {
+                    xref(q, c) = x0[q][c];
+                    r[q][c] = valid(q, c) ? r[q][c] - ax[q][c] : 0.0;
+                }
+        }
         double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
         bool conv = false;
         int it = 0;
@@ -600,7 +636,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             __syncthreads();
             USFFT_MG_MARK(12);
             apply_fine(G1, uu, w);
-            double acc[4] = {0.0, 0.0, 0.0, 0.0};
+            double acc[4] = {0.0, 0.0, 0.0, k == 0 ? bbp : 0.0};
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
@@ -623,9 +659,9 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
             __syncthreads();
             USFFT_MG_MARK(13);
-            double gs[3];
+            double gs[4];
 #pragma unroll
-            for (int q = 0; q < 3; ++q) {
+            for (int q = 0; q < 4; ++q) {
                 double tt[NWARP];
 #pragma unroll
                 for (int ww = 0; ww < NWARP; ++ww) tt[ww] = red[q][ww];
@@ -637,7 +673,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
             const double gamma = gs[0], delta = gs[1];
             rho = gs[2];
-            if (k == 0) bb = rho;
+            if (k == 0) bb = Q.x0b ? gs[3] : rho;
             conv = rho <= Q.tol2 * bb;
             if (conv || it >= Q.maxit) break;
             const double beta = k == 0 ? 0.0 : gamma * g_inv;

@@ -428,6 +428,31 @@ def test_pcg_variants_agree(B, ctx, monkeypatch):
         monkeypatch.delenv("USFFT_PCG")
 
 
+def test_pcg_mg_initial_guess(B, ctx, monkeypatch):
+    """USFFT_X0=1 (DESIGN Z31): k_pcg_mg started from the first-order guess x0 = u(0) + sum_j t_j
+    du/dt_j meets the same oracle tolerance and the same ||r|| <= 1e-12 ||b|| criterion, in no
+    more iterations than from x0 = 0 (n = 16 and 32)."""
+    for cfgid in (1, 2):
+        cfg = config(cfgid)
+        p = B.usfft_plan_round(ctx, cfg["seed"], 2, 4, 2, cfg["d"], cfg["N"], cfg["s"], "A", 300)
+        nb, G = 40, (cfg["n"] - 1) ** 2
+        Y = olat.nodes(p.M, p.z, p.shift, 4)[:, 7:7 + nb]
+        ref = ofe.sample_pde(cfg, Y)
+        its = {}
+        for x0 in ("0", "1"):
+            monkeypatch.setenv("USFFT_X0", x0)
+            u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
+            it = torch.empty(nb, dtype=torch.int32, device="cuda")
+            rel = torch.empty(nb, dtype=torch.float64, device="cuda")
+            assert B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond="mg"), p, 7, nb, u, nb, None,
+                                      it, rel, check_conv=True) == 0
+            assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
+            assert rel.max().item() <= 1e-12
+            its[x0] = it.cpu().numpy()
+        assert (its["1"] <= its["0"]).all() and its["1"].mean() < its["0"].mean()
+    monkeypatch.delenv("USFFT_X0")
+
+
 def test_pcg_all_samples_of_a_round_converge(B, ctx):
     """Every sample of a full config-2 round converges (guards against NaN/stagnation paths)."""
     cfg = config(2)
