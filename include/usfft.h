@@ -170,7 +170,10 @@ usfft_status usfft_lattice(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_
  * P:313; one solve serves all G nodes).  The nodes are generated in-kernel from `lat`
  * (bit-identical to usfft_lattice) unless `nodes` (dev fp64 [d][nb]) is given.
  * Preconditioned CG (pde->precond: Jacobi or multigrid) from x0 = 0, stop on the recursive
- * ||r||_2 <= tol ||b||_2 (Z13).
+ * ||r||_2 <= tol ||b||_2 (Z13).  Environment USFFT_X0=1 (multigrid, n = 16, 32 only): start from
+ * the first-order guess of DESIGN Z31 instead, written into u before the solve (same stopping
+ * rule; the first such call per (n, d, psi, form, f) builds and caches the basis with 2d + 1
+ * solves and one host sync).
  * u        dev fp64 [G][ldu]: u[g*ldu + bl] = u(x_g, y_{b0+bl}), ldu >= nb
  * iters    dev int32 [nb] (may be NULL): PCG iterations per sample
  * relres   dev fp64 [nb] (may be NULL): final recursive ||r||/||b|| (Jacobi path: or an upper bound)
