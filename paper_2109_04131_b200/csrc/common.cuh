@@ -15,6 +15,19 @@
 
 #include "../../include/usfft.h"
 
+namespace usfft {
+// Rader tables of one prime lattice size (fft.cu), owned by the ctx
+struct RaderPlan {
+    int64_t M = 0, N = 0;
+    int nstage = 0;
+    int radix[32] = {0};
+    double2 *tw = nullptr;      // [N]  e^{-2 pi i k / N}
+    int32_t *perm = nullptr;    // [N]  g^p mod M
+    int32_t *outidx = nullptr;  // [N]  g^{-q} mod M
+    double2 *bf = nullptr;      // [N]  FFT_N(b) / N
+};
+}  // namespace usfft
+
 struct usfft_ctx {
     int device = 0;
     cudaStream_t stream = nullptr;
@@ -34,7 +47,7 @@ struct usfft_ctx {
     std::map<int64_t, double2 *> twiddles;                  // M -> e^{-2 pi i m/M}, m < M
     std::map<std::tuple<int, int, int>, double *> sintab;    // (n, d, psi) -> psi factor tables
     std::map<std::pair<int, int>, double *> rhstab;          // (n, f_kind) -> centroid loads b
-    std::map<std::tuple<int, int, int, int, int>, double *> x0tab;   // (n, d, psi, form, f_kind) -> k_pcg_mg initial-guess basis
+    std::map<int64_t, usfft::RaderPlan> rader;               // M -> Rader tables (M = 0: not Rader-able)
     // resident blocks per SM per (kernel, threads, smem): the query costs ~10 us per call
     std::map<std::pair<const void *, size_t>, int> occupancy;
 };
@@ -88,12 +101,27 @@ inline usfft_status fail(usfft_ctx *c, usfft_status s, const char *fmt, ...) {
         if (!(cond)) return usfft::fail((c), USFFT_EINVAL, __VA_ARGS__);                      \
     } while (0)
 
+// Every entry point: validate the ctx and make its device current for the call (restored on
+// return), so contexts on different devices can be used from one thread.
+struct DeviceGuard {
+    int prev = -1, dev;
+    explicit DeviceGuard(int d) : dev(d) {
+        if (cudaGetDevice(&prev) != cudaSuccess) {
+            cudaGetLastError();
+            prev = -1;
+        }
+        if (prev != dev) cudaSetDevice(dev);
+    }
+    ~DeviceGuard() {
+        if (prev >= 0 && prev != dev) cudaSetDevice(prev);
+    }
+};
+
 #define USFFT_ENTER(c)                                                                        \
-    do {                                                                                      \
-        if (!(c)) return USFFT_EINVAL;                                                        \
-        if ((c)->sticky) return USFFT_ECUDA;                                                  \
-        (c)->err.clear();                                                                     \
-    } while (0)
+    if (!(c)) return USFFT_EINVAL;                                                            \
+    if ((c)->sticky) return USFFT_ECUDA;                                                      \
+    (c)->err.clear();                                                                         \
+    usfft::DeviceGuard usfft_device_guard_((c)->device)
 
 // Grow-only device buffers.  Growth synchronises the stream first (buffers may be in use).
 inline usfft_status ensure(usfft_ctx *c, void **buf, size_t *size, size_t need) {

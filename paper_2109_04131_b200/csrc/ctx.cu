@@ -44,7 +44,12 @@ extern "C" usfft_status usfft_finalize(usfft_ctx *c) {
     for (auto &kv : c->twiddles) cudaFree(kv.second);
     for (auto &kv : c->sintab) cudaFree(kv.second);
     for (auto &kv : c->rhstab) cudaFree(kv.second);
-    for (auto &kv : c->x0tab) cudaFree(kv.second);
+    for (auto &kv : c->rader) {
+        cudaFree(kv.second.tw);
+        cudaFree(kv.second.perm);
+        cudaFree(kv.second.outidx);
+        cudaFree(kv.second.bf);
+    }
     if (c->ws) cudaFree(c->ws);
     if (c->ws2) cudaFree(c->ws2);
     if (c->dscal) cudaFree(c->dscal);

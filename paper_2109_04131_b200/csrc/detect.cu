@@ -392,8 +392,7 @@ extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t
         if (G_loc > 0 && n_det_g) USFFT_CUDA(c, cudaMemsetAsync(n_det_g, 0, sizeof(int32_t) * G_loc, c->stream));
         return USFFT_OK;
     }
-    const char *sv = getenv("USFFT_SELECT");             // =radix: the CTA kernel at every size
-    if (!(sv && sv[0] == 'r') && nJ <= 32 * 64) {
+    if (nJ <= 32 * 64) {                                  // one warp per node; else the CTA radix select
         const unsigned grid = (unsigned)((G_loc + 3) / 4);
         auto launch = [&](auto kern) {
             kern<<<grid, 128, 0, c->stream>>>(kappa_min, nJ, G_loc, kappa_max, s_tilde, theta_rel, theta_abs,

@@ -2,10 +2,8 @@
 //
 // U[g][q] = Re sum_k C[g][k] e^{2 pi i k.y_q} = sum_k Cre[g][k] cos(2 pi k.y_q) - Cim[g][k] sin(2 pi k.y_q)
 // (eq. eval_formula P:468-470 with the identity periodization of the periodic model P:945-949).
-// This is a real GEMM [G x 2|I|] . [2|I| x n] whose right operand is generated on the fly from the
-// sparse integer frequencies: each 64x64 output tile loops over k in chunks of 16, stages the
-// C chunk and the phase chunk (k.y reduced mod 1, then sincospi) in shared memory, and every
-// thread accumulates a 4x4 register tile in fp64.
+// This is a real GEMM [G x 2|I|] . [2|I| x n] whose right operand comes from the sparse integer
+// frequencies (k.y reduced mod 1, then sincospi): on the fp64 tensor pipe (DMMA m8n8k4) below.
 #include <cstdlib>
 
 #include "common.cuh"
@@ -14,147 +12,9 @@ namespace usfft {
 
 constexpr int EV_TG = 64, EV_TQ = 64, EV_TK = 16;
 
-__global__ void __launch_bounds__(256)
-k_eval(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
-       int64_t G, const double *__restrict__ Y, int64_t n, double *__restrict__ U) {
-    __shared__ double cre[EV_TK][EV_TG + 1], cim[EV_TK][EV_TG + 1];
-    __shared__ double cs[EV_TK][EV_TQ + 1], sn[EV_TK][EV_TQ + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t g0 = (int64_t)blockIdx.y * EV_TG, q0 = (int64_t)blockIdx.x * EV_TQ;
-    double acc[4][4] = {};
-    for (int64_t k0 = 0; k0 < nI; k0 += EV_TK) {
-        for (int e = threadIdx.x; e < EV_TK * EV_TG; e += blockDim.x) {
-            const int kk = e / EV_TG, gg = e % EV_TG;
-            double2 v = make_double2(0.0, 0.0);
-            if (k0 + kk < nI && g0 + gg < G) v = C[(g0 + gg) * nI + k0 + kk];
-            cre[kk][gg] = v.x;
-            cim[kk][gg] = v.y;
-        }
-        for (int e = threadIdx.x; e < EV_TK * EV_TQ; e += blockDim.x) {
-            const int kk = e / EV_TQ, qq = e % EV_TQ;
-            double c = 0.0, s = 0.0;
-            if (k0 + kk < nI && q0 + qq < n) {
-                double ph = 0.0;
-                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
-                sincospi(2.0 * (ph - rint(ph)), &s, &c);
-            }
-            cs[kk][qq] = c;
-            sn[kk][qq] = s;
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int kk = 0; kk < EV_TK; ++kk) {
-            double a_re[4], a_im[4], b_c[4], b_s[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                a_re[r] = cre[kk][ty * 4 + r];
-                a_im[r] = cim[kk][ty * 4 + r];
-                b_c[r] = cs[kk][tx * 4 + r];
-                b_s[r] = sn[kk][tx * 4 + r];
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int s2 = 0; s2 < 4; ++s2) acc[r][s2] += a_re[r] * b_c[s2] - a_im[r] * b_s[s2];
-        }
-        __syncthreads();
-    }
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t g = g0 + ty * 4 + r;
-        if (g >= G) continue;
-#pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-            const int64_t q = q0 + tx * 4 + s2;
-            if (q < n) U[g * n + q] = acc[r][s2];
-        }
-    }
-}
-
-// usfft_eval_err: the same tiled sum with both the real and the imaginary part, the modulus of
-// the difference to the FE reference per (g, q), and per-tile partial sums (|.|, |.|^2, max)
-// reduced over the tile's 64 points by shuffles in a fixed order; k_eval_err_reduce then adds
-// the tiles of every node in tile order.
-__global__ void __launch_bounds__(256)
-k_eval_err(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
-           int64_t G, const double *__restrict__ Y, int64_t n, const double *__restrict__ Uref,
-           double *__restrict__ part) {
-    __shared__ double cre[EV_TK][EV_TG + 1], cim[EV_TK][EV_TG + 1];
-    __shared__ double cs[EV_TK][EV_TQ + 1], sn[EV_TK][EV_TQ + 1];
-    const int tx = threadIdx.x & 15, ty = threadIdx.x >> 4;
-    const int64_t g0 = (int64_t)blockIdx.y * EV_TG, q0 = (int64_t)blockIdx.x * EV_TQ;
-    double are[4][4] = {}, aim[4][4] = {};
-    for (int64_t k0 = 0; k0 < nI; k0 += EV_TK) {
-        for (int e = threadIdx.x; e < EV_TK * EV_TG; e += blockDim.x) {
-            const int kk = e / EV_TG, gg = e % EV_TG;
-            double2 v = make_double2(0.0, 0.0);
-            if (k0 + kk < nI && g0 + gg < G) v = C[(g0 + gg) * nI + k0 + kk];
-            cre[kk][gg] = v.x;
-            cim[kk][gg] = v.y;
-        }
-        for (int e = threadIdx.x; e < EV_TK * EV_TQ; e += blockDim.x) {
-            const int kk = e / EV_TQ, qq = e % EV_TQ;
-            double c = 0.0, s = 0.0;
-            if (k0 + kk < nI && q0 + qq < n) {
-                double ph = 0.0;
-                for (int j = 0; j < d; ++j) ph += (double)I[(k0 + kk) * d + j] * Y[(int64_t)j * n + q0 + qq];
-                sincospi(2.0 * (ph - rint(ph)), &s, &c);
-            }
-            cs[kk][qq] = c;
-            sn[kk][qq] = s;
-        }
-        __syncthreads();
-#pragma unroll 4
-        for (int kk = 0; kk < EV_TK; ++kk) {
-            double a_re[4], a_im[4], b_c[4], b_s[4];
-#pragma unroll
-            for (int r = 0; r < 4; ++r) {
-                a_re[r] = cre[kk][ty * 4 + r];
-                a_im[r] = cim[kk][ty * 4 + r];
-                b_c[r] = cs[kk][tx * 4 + r];
-                b_s[r] = sn[kk][tx * 4 + r];
-            }
-#pragma unroll
-            for (int r = 0; r < 4; ++r)
-#pragma unroll
-                for (int s2 = 0; s2 < 4; ++s2) {
-                    are[r][s2] += a_re[r] * b_c[s2] - a_im[r] * b_s[s2];
-                    aim[r][s2] += a_re[r] * b_s[s2] + a_im[r] * b_c[s2];
-                }
-        }
-        __syncthreads();
-    }
-    const int64_t ntile = gridDim.x;
-#pragma unroll
-    for (int r = 0; r < 4; ++r) {
-        const int64_t g = g0 + ty * 4 + r;
-        double s1 = 0.0, s2s = 0.0, mx = 0.0;
-#pragma unroll
-        for (int s2 = 0; s2 < 4; ++s2) {
-            const int64_t q = q0 + tx * 4 + s2;
-            if (g < G && q < n) {
-                const double dr = Uref[g * n + q] - are[r][s2], di = -aim[r][s2];
-                const double m = hypot(dr, di);
-                s1 += m;
-                s2s = fma(m, m, s2s);
-                mx = fmax(mx, m);
-            }
-        }
-#pragma unroll
-        for (int o = 8; o > 0; o >>= 1) {           // the 16 threads of row group ty
-            s1 += __shfl_xor_sync(0xffffffffu, s1, o);
-            s2s += __shfl_xor_sync(0xffffffffu, s2s, o);
-            mx = fmax(mx, __shfl_xor_sync(0xffffffffu, mx, o));
-        }
-        if (tx == 0 && g < G) {
-            double *pp = part + (g * ntile + blockIdx.x) * 3;
-            pp[0] = s1;
-            pp[1] = s2s;
-            pp[2] = mx;
-        }
-    }
-}
-
+// usfft_eval_err: per-tile partial sums (|.|, |.|^2, max) of |Uref - u| over the tile's 64 points,
+// reduced in a fixed order; k_eval_err_reduce then adds the tiles of every node in tile order
+// (P:885-891).
 __global__ void k_eval_err_reduce(int64_t G, int64_t ntile, int64_t n, const double *__restrict__ part,
                                   double *__restrict__ err) {
     for (int64_t g = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; g < G; g += (int64_t)gridDim.x * blockDim.x) {
@@ -268,7 +128,7 @@ k_eval_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *
 // part with A = [Cre | -Cim] and B = [cos; sin], and for the imaginary part with the same A and
 // B' = [sin; -cos] (read from the same staged phases), then |Uref - (re + i im)| per element and
 // per-row partial sums (mean, mean square, max) over the CTA's 64 columns in a fixed order, the
-// layout of k_eval_err's partials.
+// layout k_eval_err_reduce reads.
 __global__ void __launch_bounds__(256)
 k_eval_err_mma(int32_t d, const int16_t *__restrict__ I, int64_t nI, const double2 *__restrict__ C,
                int64_t G, const double *__restrict__ Y, int64_t n, const double *__restrict__ Uref,
@@ -375,12 +235,10 @@ using namespace usfft;
 namespace {
 // The phase matrix E [2][nI][n] in the second ctx workspace when it fits (<= 4 GiB) and the
 // column tiles fit the grid's y dimension; NULL: the kernels generate phases per tile.
-// USFFT_EVAL_PHASES=tile forces the per-tile generation.
 const double *phase_matrix(usfft_ctx *c, int32_t d, const int16_t *I, int64_t nI, const double *Y, int64_t n,
                            usfft_status *st) {
     *st = USFFT_OK;
-    const char *pv = getenv("USFFT_EVAL_PHASES");
-    if ((pv && pv[0] == 't') || nI == 0) return nullptr;
+    if (nI == 0) return nullptr;
     const size_t bytes = sizeof(double) * 2 * (size_t)nI * (size_t)n;
     if (bytes > (size_t(4) << 30) || (n + EV_TQ - 1) / EV_TQ > 65535 || nI > 65535) return nullptr;
     if ((*st = ensure(c, &c->ws2, &c->ws2_size, bytes))) return nullptr;
@@ -409,10 +267,7 @@ extern "C" usfft_status usfft_eval_err(usfft_ctx *c, int32_t d, const int16_t *I
     if (s) return s;
     double *part = static_cast<double *>(c->ws);
     dim3 grid((unsigned)ntile, (unsigned)((G + EV_TG - 1) / EV_TG));
-    const char *force = getenv("USFFT_EVAL");                // =fma: CUDA-core variant
-    if (force && force[0] == 'f')
-        k_eval_err<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, Uref, part);
-    else {
+    {
         usfft_status st = USFFT_OK;
         const double *E = phase_matrix(c, d, I, nI, Y, n, &st);
         if (st) return st;
@@ -436,10 +291,7 @@ extern "C" usfft_status usfft_eval(usfft_ctx *c, int32_t d, const int16_t *I, in
     USFFT_REQUIRE(c, nI == 0 || (I && C), "I / C NULL");
     USFFT_REQUIRE(c, (n + EV_TQ - 1) / EV_TQ <= 0x7fffffff && (G + EV_TG - 1) / EV_TG <= 65535, "grid too large");
     dim3 grid((unsigned)((n + EV_TQ - 1) / EV_TQ), (unsigned)((G + EV_TG - 1) / EV_TG));
-    const char *force = getenv("USFFT_EVAL");                // =fma: CUDA-core variant
-    if (force && force[0] == 'f')
-        k_eval<<<grid, 256, 0, c->stream>>>(d, I, nI, reinterpret_cast<const double2 *>(C), G, Y, n, U);
-    else {
+    {
         usfft_status st = USFFT_OK;
         const double *E = phase_matrix(c, d, I, nI, Y, n, &st);
         if (st) return st;

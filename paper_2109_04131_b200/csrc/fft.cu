@@ -126,62 +126,6 @@ k_dft_bins(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int6
     }
 }
 
-// one CTA per owned node g; the node's L spectra rows are staged in shared memory when they fit.
-// Candidates go in tiles of 256: the tile's L bins rows are first staged in shared memory with
-// independent coalesced loads (the L2 latency is paid once per tile, not once per lattice),
-// then each thread gathers and reduces its candidate.
-__global__ void __launch_bounds__(256)
-k_kappa(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t ldb, int64_t nJ,
-        int64_t M, int32_t L, double *__restrict__ kmin, int64_t ldk, unsigned long long *__restrict__ kmax,
-        int staged, const double *__restrict__ tau) {
-    extern __shared__ double2 fs[];
-    __shared__ unsigned long long wmax[32];
-    const int64_t g = blockIdx.x;
-    const int64_t Mh = M / 2 + 1;
-    const double inv_m = 1.0 / (double)M;
-    const double2 *src = F + g * L * Mh;
-    int32_t *sb = reinterpret_cast<int32_t *>(fs + (staged ? (int64_t)L * Mh : 0));   // [L][256]
-    if (staged) {
-#pragma unroll 8
-        for (int64_t e = threadIdx.x; e < (int64_t)L * Mh; e += blockDim.x) fs[e] = __ldg(src + e);
-        src = fs;
-    }
-    unsigned long long best = 0ull;
-    for (int64_t j0 = 0; j0 < nJ; j0 += 256) {
-        const int64_t j = j0 + threadIdx.x;
-        __syncthreads();                                  // previous tile's readers are done
-#pragma unroll 8
-        for (int l = 0; l < L; ++l) sb[l * 256 + threadIdx.x] = j < nJ ? __ldg(bins + (int64_t)l * ldb + j) : 0;
-        __syncthreads();
-        if (j < nJ) {
-            // v = F^[b] / M with F^[b] = conj(F[M - b]) above M/2 (the sign does not enter the
-            // key); the scaling is a multiplication by fl(1/M) here (Z5 reading)
-            double km = 0.0;
-#pragma unroll 4
-            for (int l = 0; l < L; ++l) {
-                const int b = sb[l * 256 + threadIdx.x];
-                const double2 f = src[(int)(l * Mh) + (b < (int)Mh ? b : (int)M - b)];
-                const double re = f.x * inv_m, im = f.y * inv_m;
-                const double k = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
-                km = (l == 0) ? k : fmin(km, k);
-            }
-            kmin[g * ldk + j] = (tau && km <= tau[g]) ? 0.0 : km;         // prefilter (Z29)
-            const unsigned long long bits = (unsigned long long)__double_as_longlong(km);
-            best = bits > best ? bits : best;
-        }
-    }
-    for (int o = 16; o > 0; o >>= 1) {
-        unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
-        best = other > best ? other : best;
-    }
-    if ((threadIdx.x & 31) == 0) wmax[threadIdx.x >> 5] = best;
-    __syncthreads();
-    if (threadIdx.x == 0) {
-        for (int w = 1; w < (int)(blockDim.x >> 5); ++w) best = wmax[w] > best ? wmax[w] : best;
-        atomicMax(kmax, best);
-    }
-}
-
 // Keys with the bins tile shared by a group of nodes: CTA (candidate tile, node group) stages the
 // tile's L bins rows once (coalesced) and then, node by node, gathers the node's L spectrum values
 // per candidate straight from L1/L2 (L independent loads in flight per thread).  The bins are read
@@ -296,8 +240,8 @@ int64_t powmod(int64_t b, int64_t e, int64_t m) {
 
 // Rader plan for prime M with 7-smooth M-1 (nullptr-equivalent plan.M == 0 otherwise)
 usfft_status get_rader(usfft_ctx *c, int64_t M, RaderPlan *out) {
-    static thread_local std::map<std::pair<usfft_ctx *, int64_t>, RaderPlan> cache;
-    auto key = std::make_pair(c, M);
+    auto &cache = c->rader;                               // per ctx (device), freed by usfft_finalize
+    const int64_t key = M;
     auto it = cache.find(key);
     if (it != cache.end()) {
         *out = it->second;
@@ -404,32 +348,16 @@ usfft_status launch_keys(usfft_ctx *c, int64_t M, int32_t L, int64_t G_loc, cons
                          double *kappa_max, const double *tau = nullptr) {
     unsigned long long *km = reinterpret_cast<unsigned long long *>(kappa_max);
     if (!km) km = reinterpret_cast<unsigned long long *>(static_cast<char *>(c->dscal) + 8);
-    const size_t st_bytes = sizeof(double2) * (size_t)L * (size_t)(M / 2 + 1);
     const size_t tile_bytes = sizeof(int32_t) * 256 * (size_t)L;
-    // Two kernels, identical results: the grouped kernel (bins tile shared by 8 nodes, spectra
-    // gathered from L1/L2; default) and one CTA per node with its spectra staged in shared
-    // memory (USFFT_KEYS=staged).  Measured on B200: grouped 57 vs 64 us on the config-2 round
-    // (|J| = 1000, L = 17) and 1.29 vs 1.99 s per streamed round of |J| = 8.2e6, L = 35 (the
-    // staged kernel's per-tile bins loads are latency-bound at one CTA per SM).
-    const char *kv = getenv("USFFT_KEYS");
-    const bool fits = st_bytes + tile_bytes + 1024 <= c->smem_optin;
-    const bool staged_path = kv && kv[0] == 's';
-    if (!staged_path) {
-        USFFT_REQUIRE(c, tile_bytes <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
-        USFFT_REQUIRE(c, (G_loc + KG_NODES - 1) / KG_NODES <= 65535, "too many nodes for the key grid");
-        if (usfft_status s2 = kernel_fit(c, k_kappa_grouped, 0, tile_bytes, nullptr)) return s2;
-        dim3 grid((unsigned)((nJ + 255) / 256), (unsigned)((G_loc + KG_NODES - 1) / KG_NODES));
-        k_kappa_grouped<<<grid, 256, tile_bytes, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb,
-                                                              nJ, M, L, G_loc, kappa_min, ldk, km, tau);
-        USFFT_CHECK_LAUNCH(c);
-        return USFFT_OK;
-    }
-    const int staged = fits ? 1 : 0;
-    const size_t dyn = (staged ? st_bytes : 0) + tile_bytes;
-    USFFT_REQUIRE(c, dyn <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
-    if (usfft_status s2 = kernel_fit(c, k_kappa, 0, dyn, nullptr)) return s2;
-    k_kappa<<<(unsigned)G_loc, 256, dyn, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb,
-                                                       nJ, M, L, kappa_min, ldk, km, staged, tau);
+    // the bins tile is shared by KG_NODES nodes whose spectra are gathered from L1/L2 (measured
+    // on B200 against one CTA per node with its spectra staged in shared memory: 57 vs 64 us on
+    // the config-2 round, 1.29 vs 1.99 s per streamed round of |J| = 8.2e6, L = 35)
+    USFFT_REQUIRE(c, tile_bytes <= c->smem_optin, "L = %d lattices: bins tile too large", (int)L);
+    USFFT_REQUIRE(c, (G_loc + KG_NODES - 1) / KG_NODES <= 65535, "too many nodes for the key grid");
+    if (usfft_status s2 = kernel_fit(c, k_kappa_grouped, 0, tile_bytes, nullptr)) return s2;
+    dim3 grid((unsigned)((nJ + 255) / 256), (unsigned)((G_loc + KG_NODES - 1) / KG_NODES));
+    k_kappa_grouped<<<grid, 256, tile_bytes, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb,
+                                                          nJ, M, L, G_loc, kappa_min, ldk, km, tau);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -465,9 +393,8 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
     RaderPlan R;
     s = get_rader(c, M, &R);
     if (s) return s;
-    const char *force = getenv("USFFT_DFT");
     const size_t smem_r = sizeof(double) * (size_t)((M + 1) & ~int64_t(1)) + 2 * sizeof(double2) * (size_t)(M - 1);
-    if (R.M == M && smem_r <= c->smem_optin && !(force && force[0] == 'd')) {
+    if (R.M == M && smem_r <= c->smem_optin) {
         RaderArgs A;
         A.M = R.M;
         A.N = R.N;
@@ -479,13 +406,12 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         A.outidx = R.outidx;
         A.bf = R.bf;
         double2 *Fo = reinterpret_cast<double2 *>(spectra);
-        const bool generic = force && force[0] == 'g';     // USFFT_DFT=generic: runtime-plan kernel
-        if (!generic && R.N == 96) s = launch_rader_t<96, 1, 4>(c, u, S, G_loc, L, A, Fo);
-        else if (!generic && R.N == 400 && !(force && force[0] == 's'))   // USFFT_DFT=stockham
-            s = launch_fft400(c, u, S, G_loc, L, A, Fo, force && force[0] == 'p');   // =paired
-        else if (!generic && R.N == 400) s = launch_rader_t<400, 1, 4>(c, u, S, G_loc, L, A, Fo);
-        else if (!generic && R.N == 2016) s = launch_rader_t<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
-        else if (!generic && R.N == 4000) s = launch_rader_t<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
+        // the lattice sizes of the BASELINE configs (Z2) have compile-time plans; other
+        // Rader-able M take the runtime-plan kernel
+        if (R.N == 96) s = launch_rader_t<96, 1, 4>(c, u, S, G_loc, L, A, Fo);
+        else if (R.N == 400) s = launch_fft400(c, u, S, G_loc, L, A, Fo, false);
+        else if (R.N == 2016) s = launch_rader_t<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
+        else if (R.N == 4000) s = launch_rader_t<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
         else {
             if (usfft_status s2 = kernel_fit(c, k_fft_rader, 0, smem_r, nullptr)) return s2;
             const int threads = M <= 512 ? 128 : 256;

@@ -36,22 +36,19 @@ namespace usfft {
 
 constexpr double kMgOmega = 0.8;
 
-// Phase-latency probe (tools/mg_probe.cu builds with -DUSFFT_MG_PROBE): clock64() of lane 0 of
-// every warp of CTA 0, first sample, CG iteration 6, after each synchronisation point.
-#ifdef USFFT_MG_PROBE
-__device__ long long g_mg_probe[16][32];
-#define USFFT_MG_MARK(id)                                                                           \
-    do {                                                                                           \
-        if (probe_on && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][id] = clock64();      \
-    } while (0)
-#define USFFT_MG_SMARK(id)                                                                          \
-    do {                                                                                           \
-        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][id] = clock64(); \
-    } while (0)
-#else
-#define USFFT_MG_MARK(id) ((void)0)
-#define USFFT_MG_SMARK(id) ((void)0)
-#endif
+// 1/a for positive normal a: hardware seed (MUFU.RCP64H) refined by three Newton steps, no
+// special-case branches (the CG scalars are positive and far from the fp64 range limits while
+// the iteration runs; breakdown values stop the loop through the residual test first).
+__device__ __forceinline__ double rcp_pos(double a) {
+    double y;
+    asm("rcp.approx.ftz.f64 %0, %1;" : "=d"(y) : "d"(a));
+    double e = fma(-a, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-a, y, 1.0);
+    y = fma(y, e, y);
+    e = fma(-a, y, 1.0);
+    return fma(y, e, y);
+}
 
 template <int NC>
 struct Mg3 {
@@ -144,31 +141,12 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 
     for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
         const int64_t b = b0 + bl;
-#ifdef USFFT_MG_PROBE
-        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][20] = clock64();
-#endif
-        // initial guess (Z31): k_x0_guess left x0 in this sample's column of u; the loads are
-        // issued here so that their latency hides behind the setup
-        double x0[BR][BC];
-        if (Q.x0b) {
-#pragma unroll
-            for (int q = 0; q < BR; ++q)
-#pragma unroll
-                for (int c = 0; c < BC; ++c)
-                    x0[q][c] = (col0 + c + 1 <= nx && row0 + q + 1 <= nx)
-                                   ? u[(int64_t)((row0 + q) * nx + col0 + c) * ldu + bl] : 0.0;
-        }
         // ---- K3: coefficients ----------------------------------------------------------------
         for (int j = tid; j < Q.d; j += blockDim.x) {      // d may exceed the CTA (n = 16: 32 threads)
-            if (Q.thov) {
-                th_amp[j] = Q.thov[bl * Q.d + j];
-            } else {
-                const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
-                th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
-            }
+            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
+            th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
-        USFFT_MG_SMARK(24);
         {   // per-triangle a = 1 + sum_j amp_j theta_j S_j(ma) S_j(mb) (or exp) of the fine mesh,
             // a rank-d product: thread (ci0, cj0) owns a KI x KJ tile of cells (ci0 + CIS a,
             // cj0 + CJS b) in registers
@@ -203,7 +181,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                         sup[a][k] = fma(tup[a], vup[k], sup[a][k]);
                     }
             }
-            USFFT_MG_SMARK(19);
 #pragma unroll
             for (int a = 0; a < KI; ++a)
 #pragma unroll
@@ -214,7 +191,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
         }
         __syncthreads();
-        USFFT_MG_SMARK(25);
         // a at the centroid of T_lo / T_up of cell (ci, cj) of the mesh with cell width 2^sh h: the
         // fine triangle with the same centroid (abscissae ma, mb in units of h/3)
         // ma = 3 ci p + ra, mb = 3 cj p + rb with p = 2^sh and (ra, rb) = (2p, p) below / (p, 2p)
@@ -265,7 +241,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             WV3[e] = wv(I, J, m3, 3);
         }
         __syncthreads();                                 // aT is dead from here on
-        USFFT_MG_SMARK(26);
         // warps >= 1 form the level-1/2 diagonals while warp 0 assembles and inverts A3
         constexpr int HB = NWARP > 1 ? 32 : 0, HS = NT - HB;
         if (tid >= HB) {
@@ -290,7 +265,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 D2[e] = dv;
                 DI2[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
             }
-            USFFT_MG_SMARK(31);
         }
 #pragma unroll
         for (int q = 0; q < BR; ++q)                     // omega D^-1 of the own nodes (0 off-mesh);
@@ -300,11 +274,9 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 DI0[(row0 + 1 + q) * np + ((c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1))] =
                     (col0 + c + 1 <= nx && row0 + q + 1 <= nx) ? kMgOmega * rcp_pos(dv) : 0.0;
             }
-        USFFT_MG_SMARK(16);
         if (warp == 0) {   // in-place Gauss-Jordan inverse of the coarsest operator (SPD, tiny):
             // lane i assembles row i of A3 (5-point, rediscretised) in registers; the pivot row of
             // each step comes by shuffles
-            USFFT_MG_SMARK(17);
             const int ri = lane < U3 ? lane : 0;
             const int ia = ri % (m3 - 1) + 1, ja = ri / (m3 - 1) + 1, g = ja * p3 + ia;
             const double wr = WH3[g], wl = WH3[g - 1], wu = WV3[g], wd = WV3[g - p3];
@@ -329,16 +301,13 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     else a[c] = c == k ? f : fma(f, prow[c], a[c]);
                 }
             }
-            USFFT_MG_SMARK(18);
             __syncwarp();
             if (lane < U3) {
 #pragma unroll
                 for (int c = 0; c < U3; ++c) AI[lane * U3 + c] = a[c];
             }
-            USFFT_MG_SMARK(30);
         }
         __syncthreads();
-        USFFT_MG_SMARK(27);
         // The level-2 part of the cycle is a fixed linear map R2 -> S2 (damped-Jacobi pre-smoothing,
         // exact level-3 correction, post-smoothing):  with Dw = omega D2^-1,
         //   S2 = K R2,  K = 2 Dw - Dw A2 Dw + B^T A3^-1 B,  B = P3^T (I - A2 Dw)   (U3 x U2),
@@ -362,7 +331,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             Bm[e] = v;
         }
         __syncthreads();
-        USFFT_MG_SMARK(28);
         for (int e = tid; e < U3 * U2; e += NT) {        // C = A3^-1 B
             const int r = e / U2, k = e % U2;
             double v = 0.0;
@@ -370,7 +338,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             Cm[e] = v;
         }
         __syncthreads();
-        USFFT_MG_SMARK(29);
         auto kix = [](int col, int row) -> int { return col * U2 + row + (col >= HK ? L::KPAD : 0); };
         for (int e = U2 * U2 + tid; e < 2 * HK * U2; e += NT) Kt[kix(e / U2, e % U2)] = 0.0;   // zero pad column(s)
         if (tid < 2 * HK - U2) R2[U2 + tid] = 0.0;                           // and R2 tail
@@ -477,8 +444,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             return fma(wx1 * wy1, z2[pc + 1], fma(wx0 * wy1, z2[pc], fma(wx1 * wy0, z2[1], wx0 * wy0 * z2[0])));
         };
 
-        int probe_on = 0;
-        (void)probe_on;
         // ---- one V(1,1) cycle: z = M^-1 rin ------------------------------------------------
         auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
             double t[BR][BC];
@@ -488,7 +453,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < BC; ++c) z[q][c] = DI0[fe(c, q)] * rin[q][c];   // z0 = omega D^-1 r
             publish(G0, z);
             __syncthreads();
-            USFFT_MG_MARK(1);
             apply_fine(G0, z, t);
 #pragma unroll
             for (int q = 0; q < BR; ++q)
@@ -496,7 +460,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < BC; ++c) t[q][c] = rin[q][c] - t[q][c];       // fine residual
             publish(G1, t);
             __syncthreads();
-            USFFT_MG_MARK(2);
             // R1 = P^T t (9-point, split rows of G1), Z1 = omega D1^-1 R1
             for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {
                 const int f = 2 * J * np, c = I, l = HE + I - 1, r = HE + I;
@@ -507,10 +470,8 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 Z1[e] = DI1[e] * rr;
             });
             __syncthreads();
-            USFFT_MG_MARK(3);
             for_interior(C1{}, SCTA{}, tid, [&](int I, int J) { T1[e1(I, J)] = R1[e1(I, J)] - apply1(Z1, I, J); });
             __syncthreads();
-            USFFT_MG_MARK(4);
             for_interior(C2{}, SCTA{}, tid, [&](int I, int J) {      // R2 = P^T T1 (compact)
                 const int f = 2 * J * P1, c = I, l = H1 + I - 1, r = H1 + I;
                 R2[(J - 1) * (m2 - 1) + I - 1] =
@@ -518,7 +479,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     0.25 * (T1[f - P1 + l] + T1[f - P1 + r] + T1[f + P1 + l] + T1[f + P1 + r]);
             });
             __syncthreads();
-            USFFT_MG_MARK(5);
             if (warp < (2 * U2 + 31) / 32) {                     // S2 = K R2 (levels 2 and 3)
                 // thread (i, h): half h of row i; K and R2 carry a zero column / entry past U2
                 const int h = tid & 1, i = min(tid >> 1, U2 - 1);
@@ -537,18 +497,15 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 if (own && h == 0) S2[(i / (m2 - 1) + 1) * P2 + i % (m2 - 1) + 1] = sv;
             }
             __syncthreads();
-            USFFT_MG_MARK(9);
             for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {      // Zc1 = Z1 + P S2 (in place)
                 Z1[e1(I, J)] += prol2w(S2, P2, I, J);
             });
             __syncthreads();
-            USFFT_MG_MARK(10);
             for_interior(C1{}, SCTA{}, tid, [&](int I, int J) {      // S1 = smooth(Zc1)
                 const int e = e1(I, J);
                 S1[e] = fma(DI1[e], R1[e] - apply1(Z1, I, J), Z1[e]);
             });
             __syncthreads();
-            USFFT_MG_MARK(11);
             // level 0: z = z0 + P S1, post-smooth.  The coarse values this block and its
             // neighbours need form a (BR/2 + 2) x 3 window of S1; the parity of every fine node
             // relative to (col0, row0) is a compile-time constant.
@@ -584,9 +541,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
         };
 
-#ifdef USFFT_MG_PROBE
-        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) g_mg_probe[threadIdx.x >> 5][21] = clock64();
-#endif
         // ---- Chronopoulos-Gear PCG ----------------------------------------------------------
         // x and p are touched once per iteration: with XP_SMEM they live in thread-private shared
         // slots (conflict-free [k][tid] layout) to free registers for a third CTA per SM
@@ -603,40 +557,17 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                         : Bt ? __ldg(Bt + (row0 + q) * nx + col0 + c)                // the load table
                              : (double)(row0 + q + 1) * inv_n3;
             }
-        // ||b||^2 partial (reduced with the first iteration's dots), then r0 = b - A x0 for the
-        // initial guess loaded from u at the top of the sample (k_x0_guess, DESIGN Z31); without
-        // a basis x0 = 0 and r0 = b (Z13)
-        double bbp = 0.0;
-#pragma unroll
-        for (int q = 0; q < BR; ++q)
-#pragma unroll
-            for (int c = 0; c < BC; ++c) bbp = fma(r[q][c], r[q][c], bbp);
-        if (Q.x0b) {
-            double ax[BR][BC];
-            publish(G1, x0);
-            __syncthreads();
-            apply_fine(G1, x0, ax);
-#pragma unroll
-            for (int q = 0; q < BR; ++q)
-#pragma unroll
-                for (int c = 0; c < BC; ++c) {
-                    xref(q, c) = x0[q][c];
-                    r[q][c] = valid(q, c) ? r[q][c] - ax[q][c] : 0.0;
-                }
-        }
+        // x0 = 0, r0 = b (Z13); ||b||^2 is the first iteration's (r, r)
         double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
         bool conv = false;
         int it = 0;
         for (int k = 0;; ++k) {
-            probe_on = blockIdx.x == 0 && bl == gridDim.x && k == 6;
-            USFFT_MG_MARK(0);
             double uu[BR][BC], w[BR][BC];
             vcycle(r, uu);
             publish(G1, uu);                                 // G1 (fine residual) is free again
             __syncthreads();
-            USFFT_MG_MARK(12);
             apply_fine(G1, uu, w);
-            double acc[4] = {0.0, 0.0, 0.0, k == 0 ? bbp : 0.0};
+            double acc[4] = {0.0, 0.0, 0.0, 0.0};
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
@@ -658,7 +589,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 if ((lane & 7) == 0) red[lane >> 3][warp] = v;
             }
             __syncthreads();
-            USFFT_MG_MARK(13);
             double gs[4];
 #pragma unroll
             for (int q = 0; q < 4; ++q) {
@@ -673,7 +603,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
             const double gamma = gs[0], delta = gs[1];
             rho = gs[2];
-            if (k == 0) bb = Q.x0b ? gs[3] : rho;
+            if (k == 0) bb = rho;
             conv = rho <= Q.tol2 * bb;
             if (conv || it >= Q.maxit) break;
             const double beta = k == 0 ? 0.0 : gamma * g_inv;
@@ -697,12 +627,6 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int c = 0; c < BC; ++c)
                 if (valid(q, c)) u[(int64_t)((row0 + q) * nx + col0 + c) * ldu + bl] = xref(q, c);
-#ifdef USFFT_MG_PROBE
-        if (blockIdx.x == 0 && bl == gridDim.x && (threadIdx.x & 31) == 0) {
-            g_mg_probe[threadIdx.x >> 5][22] = clock64();
-            g_mg_probe[threadIdx.x >> 5][23] = it;
-        }
-#endif
         if (tid == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rho / bb);

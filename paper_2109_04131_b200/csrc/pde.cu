@@ -14,7 +14,6 @@
 // result does not depend on which CTA or rank solved it):
 //   k_pcg_mg  (pcg_mg.cuh)   multigrid-preconditioned CG, fine level in registers, n = 16, 32
 //   k_pcg_mgg (pcg_mgg.cuh)  multigrid-preconditioned CG, per-CTA scratch slab, n = 8 .. 128
-//   k_pcg_reg (pcg_reg.cuh)  Jacobi PCG, register-resident, n = 16, 32
 //   k_pcg     (below)        Jacobi PCG, shared memory (n <= 64) or a global slab, any n
 #include <cstdlib>
 #include <vector>
@@ -27,10 +26,6 @@ struct PdeParams {
     int32_t n, d, theta, form, f_kind, maxit, precond, psi;
     double tol2;              // tol^2
     double delta;             // global pole shift of phi_Delta (Z27)
-    // k_pcg_mg only: x0b = the initial-guess basis [d + 1][G] (x0 = x0b[0] + sum_j t_j x0b[j + 1],
-    // t_j = amp_j theta_j(y); NULL: x0 = 0); thov = [nb][d] values of t replacing amp_j theta_j(y)
-    // (the basis build's own solves; NULL in every product call)
-    const double *x0b, *thov;
     double amp[kMaxD];
 };
 
@@ -231,7 +226,6 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
 
 }  // namespace usfft
 
-#include "pcg_reg.cuh"
 #include "pcg_mg.cuh"
 #include "pcg_mgg.cuh"
 
@@ -294,26 +288,6 @@ usfft_status launch_pcg_mgg(usfft_ctx *c, const LatParams &P, const PdeParams &Q
     }
 }
 
-template <int NC, int BC, int BR, int LX, int NWARP, int MINB>
-usfft_status launch_pcg_reg(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
-                            const double *nodes, int64_t b0, int64_t nb, double *u, int64_t ldu,
-                            int32_t *iters, double *relres, int32_t *noconv, const double *S,
-                           const double *Bt) {
-    const int n = Q.n;
-    constexpr int NRG = NWARP * (32 / LX), NCOL = LX * BC;
-    const size_t dyn = sizeof(double) * (size_t)(2 * n * n + (n + 1) * (n + 1) + 12 * NRG * NCOL);
-    auto kern = k_pcg_reg<NC, BC, BR, LX, NWARP, MINB>;
-    int per_sm = 0;
-    if (usfft_status s = kernel_fit(c, kern, NWARP * 32, dyn, &per_sm)) return s;
-    if (per_sm < 1) per_sm = 1;
-    int64_t grid = (int64_t)per_sm * c->sm_count;
-    if (grid > nb) grid = nb;
-    kern<<<(unsigned)grid, NWARP * 32, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
-                                                         noconv, S, Bt);
-    USFFT_CHECK_LAUNCH(c);
-    return USFFT_OK;
-}
-
 template <int NPT, int THREADS>
 usfft_status launch_pcg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
                         int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters,
@@ -345,94 +319,6 @@ usfft_status launch_pcg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, co
     k_pcg<NPT, THREADS><<<grid, threads, dyn, c->stream>>>(P, Q, nodes, b0, nb, u, ldu, iters, relres,
                                                    noconv, S, Bt, gscratch, region);
     USFFT_CHECK_LAUNCH(c);
-    return USFFT_OK;
-}
-// Initial-guess basis of k_pcg_mg (DESIGN Z31): with t_j = amp_j theta_j(y) the solution is
-// u(t), a smooth function of t (a = 1 + sum_j t_j psi_j, or exp of the sum), and
-//     x0(t) = u(0) + sum_j t_j du/dt_j(0)
-// leaves an initial residual of O(|t|^2) instead of ||b||.  Column 0 of U holds u(0), columns
-// 2j + 1, 2j + 2 hold u(+eps e_j), u(-eps e_j); the derivative is their central difference.
-__global__ void k_x0_basis(const double *__restrict__ U, int64_t G, int d, double eps,
-                           double *__restrict__ X0) {
-    const int64_t n = (int64_t)(d + 1) * G, ld = 2 * d + 1;
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < n; e += (int64_t)gridDim.x * blockDim.x) {
-        const int64_t j = e / G, g = e - j * G;
-        X0[e] = j == 0 ? U[g * ld] : (U[g * ld + 2 * j - 1] - U[g * ld + 2 * j]) / (2.0 * eps);
-    }
-}
-
-// t_j = amp_j theta_j(y_b) of every sample of the call, T[j][nb] (the same values the solve's own
-// setup forms), computed once so that k_x0_guess does no lattice / theta arithmetic per chunk
-__global__ void k_x0_t(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
-                       int64_t nb, double *__restrict__ T) {
-    for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < nb * Q.d; e += (int64_t)gridDim.x * blockDim.x) {
-        const int j = (int)(e / nb);
-        const int64_t bl = e - j * nb;
-        const double y = nodes ? nodes[e] : lattice_node(P, b0 + bl, j);
-        T[e] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
-    }
-}
-
-// x0 of every sample of the call into its column of u (read back by k_pcg_mg before the solve):
-// thread = sample (coalesced along the sample-fastest rows of u and of T), blockIdx.y = a chunk
-// of GC nodes accumulated in registers over j; the basis rows are warp-uniform reads.
-template <int GC>
-__global__ void __launch_bounds__(128) k_x0_guess(const double *__restrict__ x0b, const double *__restrict__ T,
-                                                  int d, int64_t nb, int64_t G, double *__restrict__ u, int64_t ldu) {
-    const int64_t bl = blockIdx.x * (int64_t)blockDim.x + threadIdx.x;
-    if (bl >= nb) return;
-    const int64_t g0 = (int64_t)blockIdx.y * GC;
-    const double *xb = x0b + g0;
-    double acc[GC];
-#pragma unroll
-    for (int i = 0; i < GC; ++i) acc[i] = g0 + i < G ? __ldg(xb + i) : 0.0;
-    for (int j = 0; j < d; ++j) {
-        const double t = __ldg(T + (int64_t)j * nb + bl);
-        const double *xj = xb + (j + 1) * G;
-#pragma unroll
-        for (int i = 0; i < GC; ++i)
-            if (g0 + i < G) acc[i] = fma(t, __ldg(xj + i), acc[i]);
-    }
-#pragma unroll
-    for (int i = 0; i < GC; ++i)
-        if (g0 + i < G) u[(g0 + i) * ldu + bl] = acc[i];
-}
-
-template <int NC>
-usfft_status x0_basis(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *S,
-                      const double *Bt, const double **out) {
-    auto key = std::make_tuple(Q.n, Q.d, Q.psi, Q.form, Q.f_kind);
-    auto it = c->x0tab.find(key);
-    if (it != c->x0tab.end()) {
-        *out = it->second;
-        return USFFT_OK;
-    }
-    const int d = Q.d, nb = 2 * d + 1;
-    const int64_t G = (int64_t)(NC - 1) * (NC - 1);
-    constexpr double eps = 1e-3;
-    std::vector<double> th((size_t)nb * d, 0.0);
-    for (int j = 0; j < d; ++j) {
-        th[(size_t)(2 * j + 1) * d + j] = eps;
-        th[(size_t)(2 * j + 2) * d + j] = -eps;
-    }
-    double *thd = nullptr, *U = nullptr, *X0 = nullptr;
-    USFFT_CUDA(c, cudaMalloc(&thd, th.size() * sizeof(double)));
-    USFFT_CUDA(c, cudaMalloc(&U, (size_t)G * nb * sizeof(double)));
-    USFFT_CUDA(c, cudaMalloc(&X0, (size_t)(d + 1) * G * sizeof(double)));
-    USFFT_CUDA(c, cudaMemcpyAsync(thd, th.data(), th.size() * sizeof(double), cudaMemcpyHostToDevice, c->stream));
-    PdeParams Qb = Q;
-    Qb.x0b = nullptr;
-    Qb.thov = thd;
-    usfft_status s = NC == 32 ? launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Qb, nullptr, 0, nb, U, nb, nullptr, nullptr, nullptr, S, Bt)
-                              : launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Qb, nullptr, 0, nb, U, nb, nullptr, nullptr, nullptr, S, Bt);
-    if (s) return s;
-    k_x0_basis<<<grid1d((d + 1) * G, 256), 256, 0, c->stream>>>(U, G, d, eps, X0);
-    USFFT_CHECK_LAUNCH(c);
-    USFFT_CUDA(c, cudaStreamSynchronize(c->stream));
-    cudaFree(thd);
-    cudaFree(U);
-    c->x0tab[key] = X0;
-    *out = X0;
     return USFFT_OK;
 }
 }  // namespace
@@ -473,7 +359,6 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     Q.delta = pde->delta;
     Q.psi = pde->psi;
     Q.tol2 = pde->tol * pde->tol;
-    Q.x0b = Q.thov = nullptr;
     for (int j = 0; j < pde->d; ++j) Q.amp[j] = pde->amp[j];
 
     // psi factor tables for (n, d, psi) and the load table for (n, f_kind != 0): cached per ctx
@@ -506,59 +391,18 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     int32_t *noconv = n_noconv ? reinterpret_cast<int32_t *>(c->dscal) : nullptr;
     if (noconv) USFFT_CUDA(c, cudaMemsetAsync(noconv, 0, sizeof(int32_t), c->stream));
 
+    // one kernel per (preconditioner, mesh): multigrid-preconditioned CG with the fine level in
+    // registers of one CTA (n = 16, 32) or of a thread-block cluster (n = 64, 128); Jacobi PCG
+    // (precond 0, or meshes the multigrid does not cover) through the shared/global-memory kernel
     const int n = pde->n, G = (n - 1) * (n - 1);
-    // register-resident CTA-per-sample PCG (mesh size a template parameter: n = 16, 32, the
-    // meshes of configs 1-2); otherwise the shared/global-memory PCG.  USFFT_PCG=smem forces the latter.
-    const char *force = getenv("USFFT_PCG");
-    const bool reg_ok = !(force && force[0] == 's');
-    const char *mgl = getenv("USFFT_MG_LAYOUT");
-    const char *mgg = getenv("USFFT_MGG");              // =1: the scratch-slab multigrid kernel at any n
-    if (pde->precond == 1 && mgg && mgg[0] == '1' && n >= 8 && (n & (n - 1)) == 0)
-        s = launch_pcg_mgg(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    else if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '2')        // 256 threads, 2x2 blocks
-        s = launch_pcg_mg<32, 2, 2, 16, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    else if (pde->precond == 1 && n == 32 && mgl && mgl[0] == '3')   // 3 CTAs/SM, x and p in smem
-        s = launch_pcg_mg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    else if (pde->precond == 1 && (n == 32 || n == 16)) {       // n = 32: 128 threads, 2x4 blocks
-        // =1: first-order initial guess (Z31; measured: 13.0 -> 11.6 iterations, k_pcg_mg -5 %,
-        // but the x0 pre-pass costs more than that), default x0 = 0 (Z13)
-        const char *x0e = getenv("USFFT_X0");
-        if (x0e && x0e[0] == '1') {
-            const double *X0 = nullptr;
-            s = n == 32 ? x0_basis<32>(c, P, Q, S, Bt, &X0) : x0_basis<16>(c, P, Q, S, Bt, &X0);
-            if (s) return s;
-            Q.x0b = X0;
-            const int64_t G = (int64_t)(n - 1) * (n - 1);
-            if (usfft_status st = ensure(c, &c->ws, &c->ws_size, sizeof(double) * (size_t)nb * Q.d)) return st;
-            double *T = static_cast<double *>(c->ws);
-            k_x0_t<<<grid1d(nb * Q.d, 256), 256, 0, c->stream>>>(P, Q, nodes, b0, nb, T);
-            USFFT_CHECK_LAUNCH(c);
-            constexpr int GC = 32;
-            const dim3 grid((unsigned)((nb + 127) / 128), (unsigned)((G + GC - 1) / GC));
-            k_x0_guess<GC><<<grid, 128, 0, c->stream>>>(X0, T, Q.d, nb, G, u, ldu);
-            USFFT_CHECK_LAUNCH(c);
-        }
-        s = n == 32 ? launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt)
-                    : launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    }
-    else if (pde->precond == 1 && n >= 8 && (n & (n - 1)) == 0)  // n = 64, 128 (and 8): scratch-slab multigrid
+    if (pde->precond == 1 && n == 32)
+        s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (pde->precond == 1 && n == 16)
+        s = launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (pde->precond == 1 && n >= 8 && (n & (n - 1)) == 0)
         s = launch_pcg_mgg(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1)
         return fail(c, USFFT_EUNIMPL, "multigrid preconditioner needs n a power of two >= 8");
-    else if (reg_ok && n == 16)
-        s = launch_pcg_reg<16, 2, 4, 8, 1, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    else if (reg_ok && n == 32)
-    {
-        const char *lay = getenv("USFFT_PCG_LAYOUT");       // experiments: thread block of nodes
-        if (lay && lay[0] == '1')
-            s = launch_pcg_reg<32, 1, 4, 32, 8, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-        else if (lay && lay[0] == '4')                      // 4 columns x 2 rows per thread
-            s = launch_pcg_reg<32, 4, 2, 8, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-        else if (getenv("USFFT_PCG4"))
-            s = launch_pcg_reg<32, 2, 4, 16, 4, 4>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-        else
-            s = launch_pcg_reg<32, 2, 4, 16, 4, 3>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    }
     // threads x nodes-per-thread: 128x2 (G <= 256), 256x4 (G <= 1024), 512x8, 1024x16
     else if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
@@ -576,9 +420,3 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     return USFFT_OK;
 }
 
-#ifdef USFFT_MG_PROBE
-// probe build only (tools/mg_probe.cu): copy the phase clocks of k_pcg_mg out
-extern "C" int usfft_debug_mg_probe(long long *out) {
-    return (int)cudaMemcpyFromSymbol(out, usfft::g_mg_probe, sizeof(long long) * 16 * 32);
-}
-#endif

@@ -11,16 +11,6 @@
 
 namespace usfft {
 
-struct RaderPlan {
-    int64_t M = 0, N = 0;
-    int nstage = 0;
-    int radix[32] = {0};
-    double2 *tw = nullptr;      // [N]  e^{-2 pi i k / N}
-    int32_t *perm = nullptr;    // [N]  g^p mod M
-    int32_t *outidx = nullptr;  // [N]  g^{-q} mod M
-    double2 *bf = nullptr;      // [N]  FFT_N(b) / N
-};
-
 struct RaderArgs {
     int64_t M, N;
     int nstage;

@@ -46,7 +46,7 @@ def _solve(B, ctx, cfg, p, b0, nb, precond, delta):
 
 @pytest.mark.parametrize("name", sorted(EXAMPLES))
 @pytest.mark.parametrize("n", [32, 16, 20, 64])
-def test_example_samples_every_solver(B, ctx, monkeypatch, name, n):
+def test_example_samples_every_solver(B, ctx, name, n):
     cfg = config(name, n=n)
     d, t = cfg["d"], 4
     delta = ofe.global_delta(oplan.lattice_size(cfg["s_local"], cfg["N"])) if cfg["theta"] == "phi_delta" else 0.0
@@ -55,16 +55,12 @@ def test_example_samples_every_solver(B, ctx, monkeypatch, name, n):
     b0, nb = 7, 21                                    # includes a ragged tail of the CTA grid
     Y = olat.nodes(p.M, p.z, p.shift, t)[:, b0:b0 + nb]
     ref = ofe.sample_pde(ocfg, Y)
-    runs = [("jacobi", "smem")] + ([("mg", "reg"), ("jacobi", "reg")] if n in (16, 32) else
-                                   [("mg", "reg")] if n == 64 else [("jacobi", "reg")])
-    for precond, env in runs:
-        monkeypatch.setenv("USFFT_PCG", env)
+    for precond in ("jacobi", "mg") if n != 20 else ("jacobi",):
         got, it = _solve(B, ctx, cfg, p, b0, nb, precond, delta)
         err = np.abs(got - ref).max() / np.abs(ref).max()
-        assert err <= 1e-10, (precond, env, err)
+        assert err <= 1e-10, (precond, err)
         if precond == "mg":                           # high-contrast exp fields take more
             assert it.max() <= (40 if cfg["form"] == "affine" else 80)
-    monkeypatch.delenv("USFFT_PCG")
 
 
 def test_example_loads_and_nonnegativity(B, ctx):

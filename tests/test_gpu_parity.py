@@ -205,26 +205,22 @@ def test_lattice_fft_parity(B, ctx, G, M, L, nJ):
 
 
 @pytest.mark.parametrize("G,M,L,nJ", [(19, 401, 17, 1000), (9, 97, 11, 300), (4, 2017, 3, 70), (11, 401, 35, 9000)])
-def test_key_kernels_agree(B, ctx, monkeypatch, G, M, L, nJ):
-    """The grouped key kernel (bins tile shared by 8 nodes) and the per-node staged one give
-    bit-identical keys and kappa_max (default choice, and each forced); G not a multiple of 8."""
+def test_keys_vs_oracle(B, ctx, G, M, L, nJ):
+    """a8 keys of the grouped key kernel (bins tile shared by 8 nodes, G not a multiple of 8)
+    against the oracle's kappa_min of the oracle's direct-DFT values; kappa_max exact."""
     from paper_2109_04131_b200.binding import Plan
     U, z, J, bins = _round_inputs(G * M, G, M, L, nJ)
     p = Plan(3, M, L, 3, -1, z, np.zeros(3))
     Mh = M // 2 + 1
-    out = []
-    for mode in (None, "grouped", "staged"):
-        if mode:
-            monkeypatch.setenv("USFFT_KEYS", mode)
-        spectra = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
-        kmin = torch.empty((G, nJ), dtype=torch.float64, device="cuda")
-        kmax = torch.empty(1, dtype=torch.float64, device="cuda")
-        B.usfft_lattice_fft(ctx, p, G, dev(U, torch.float64), [0, L * M], dev(bins, torch.int32), nJ, spectra,
-                            kmin, kmax)
-        out.append((kmin, kmax))
-    monkeypatch.delenv("USFFT_KEYS")
-    for o in out[1:]:
-        assert torch.equal(out[0][0], o[0]) and torch.equal(out[0][1], o[1])
+    spectra = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
+    kmin = torch.empty((G, nJ), dtype=torch.float64, device="cuda")
+    kmax = torch.empty(1, dtype=torch.float64, device="cuda")
+    B.usfft_lattice_fft(ctx, p, G, dev(U, torch.float64), [0, L * M], dev(bins, torch.int32), nJ, spectra,
+                        kmin, kmax)
+    km = kmin.cpu().numpy()
+    ref = odet.kappa_min(odft.round_values(U, M, L, bins))
+    assert np.abs(np.sqrt(km) - np.sqrt(ref)).max() <= 1e-12 * np.sqrt(ref.max())
+    assert kmax.item() == km.max()
 
 
 # ------------------------------------------------------------------------------ a9-a11 selection
@@ -382,40 +378,34 @@ def test_eval_parity(B, ctx):
 
 
 # ------------------------------------------------------------------------------ kernel variants
-def test_fft_variants_agree(B, ctx, monkeypatch):
-    """Rader FFT: compile-time kernels (four-step FFT-400 at M = 401, Stockham otherwise), the
-    four-step kernel on lattice pairs, the compile-time Stockham kernel, the runtime-plan kernel
-    and the direct DFT kernel all match the oracle's direct DFT (odd L: a half pair)."""
+@pytest.mark.parametrize("G,M,L", [(5, 401, 3), (2, 4001, 2), (4, 97, 5), (3, 2017, 2), (6, 61, 3),
+                                    (7, 65, 2), (5, 17, 3), (3, 2, 2)])
+def test_fft_paths_vs_oracle(B, ctx, G, M, L):
+    """Every lattice-FFT path, each on the M that selects it: the register four-step Rader
+    (M = 401), the compile-time Rader/Stockham plans (97, 2017, 4001), the runtime-plan Rader
+    (61: 60 = 4 * 3 * 5) and the direct DFT (65, 17, 2: not Rader-able) against the oracle's
+    direct DFT (odd L included)."""
     from paper_2109_04131_b200.binding import Plan
-    for G, M, L in ((5, 401, 3), (2, 4001, 2), (4, 97, 5)):
-        U, z, J, bins = _round_inputs(M, G, M, L, 64)
-        p = Plan(3, M, L, 3, -1, z, np.zeros(3))
-        Mh = M // 2 + 1
-        out = []
-        for mode in ("rader", "paired", "stockham", "generic", "direct"):
-            monkeypatch.setenv("USFFT_DFT", mode)
-            sp = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
-            km = torch.empty((G, 64), dtype=torch.float64, device="cuda")
-            kx = torch.empty(1, dtype=torch.float64, device="cuda")
-            B.usfft_lattice_fft(ctx, p, G, dev(U, torch.float64), [0, L * M], dev(bins, torch.int32), 64, sp, km, kx)
-            out.append(sp.cpu().numpy())
-        monkeypatch.delenv("USFFT_DFT")
-        ref = np.stack([odft.lattice_dft(U[:, l * M:(l + 1) * M], M, np.arange(Mh)) for l in range(L)], 1) * M
-        for o in out:
-            assert np.abs(o[..., 0] + 1j * o[..., 1] - ref).max() <= 1e-12 * np.abs(ref).max()
+    U, z, J, bins = _round_inputs(M, G, M, L, 64)
+    p = Plan(3, M, L, 3, -1, z, np.zeros(3))
+    Mh = M // 2 + 1
+    sp = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
+    B.usfft_lattice_fft(ctx, p, G, dev(U, torch.float64), [0, L * M], None, 0, sp, None, None)
+    o = sp.cpu().numpy()
+    ref = np.stack([odft.lattice_dft(U[:, l * M:(l + 1) * M], M, np.arange(Mh)) for l in range(L)], 1) * M
+    assert np.abs(o[..., 0] + 1j * o[..., 1] - ref).max() <= 1e-12 * np.abs(ref).max()
 
 
-def test_pcg_variants_agree(B, ctx, monkeypatch):
-    """Multigrid-preconditioned CG (default for n = 16, 32), the register-resident Jacobi PCG and
-    the shared-memory Jacobi PCG all meet the oracle tolerance on the same samples."""
+def test_pcg_preconditioners_agree(B, ctx):
+    """Multigrid-preconditioned CG (default for power-of-two meshes) and the Jacobi PCG both meet
+    the oracle tolerance on the same samples."""
     for cfgid in (1, 2):
         cfg = config(cfgid)
         p = B.usfft_plan_round(ctx, cfg["seed"], 2, 4, 2, cfg["d"], cfg["N"], cfg["s"], "A", 300)
         nb, G = 24, (cfg["n"] - 1) ** 2
         Y = olat.nodes(p.M, p.z, p.shift, 4)[:, 5:5 + nb]
         ref = ofe.sample_pde(cfg, Y)
-        for precond, env in (("mg", "reg"), ("jacobi", "reg"), ("jacobi", "smem")):
-            monkeypatch.setenv("USFFT_PCG", env)
+        for precond in ("mg", "jacobi"):
             u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
             it = torch.empty(nb, dtype=torch.int32, device="cuda")
             rel = torch.empty(nb, dtype=torch.float64, device="cuda")
@@ -425,32 +415,6 @@ def test_pcg_variants_agree(B, ctx, monkeypatch):
             assert rel.max().item() <= 1e-12
             if precond == "mg":
                 assert it.max().item() <= 30           # multigrid: iteration count ~ mesh independent
-        monkeypatch.delenv("USFFT_PCG")
-
-
-def test_pcg_mg_initial_guess(B, ctx, monkeypatch):
-    """USFFT_X0=1 (DESIGN Z31): k_pcg_mg started from the first-order guess x0 = u(0) + sum_j t_j
-    du/dt_j meets the same oracle tolerance and the same ||r|| <= 1e-12 ||b|| criterion, in no
-    more iterations than from x0 = 0 (n = 16 and 32)."""
-    for cfgid in (1, 2):
-        cfg = config(cfgid)
-        p = B.usfft_plan_round(ctx, cfg["seed"], 2, 4, 2, cfg["d"], cfg["N"], cfg["s"], "A", 300)
-        nb, G = 40, (cfg["n"] - 1) ** 2
-        Y = olat.nodes(p.M, p.z, p.shift, 4)[:, 7:7 + nb]
-        ref = ofe.sample_pde(cfg, Y)
-        its = {}
-        for x0 in ("0", "1"):
-            monkeypatch.setenv("USFFT_X0", x0)
-            u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
-            it = torch.empty(nb, dtype=torch.int32, device="cuda")
-            rel = torch.empty(nb, dtype=torch.float64, device="cuda")
-            assert B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond="mg"), p, 7, nb, u, nb, None,
-                                      it, rel, check_conv=True) == 0
-            assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
-            assert rel.max().item() <= 1e-12
-            its[x0] = it.cpu().numpy()
-        assert (its["1"] <= its["0"]).all() and its["1"].mean() < its["0"].mean()
-    monkeypatch.delenv("USFFT_X0")
 
 
 def test_pcg_all_samples_of_a_round_converge(B, ctx):
@@ -529,62 +493,52 @@ def test_emulated_multirank_round_bitexact(B, ctx):
         assert torch.equal(x, y)
 
 
-def test_eval_tensor_and_fma_variants(B, ctx, monkeypatch):
-    """usfft_eval on the fp64 tensor pipe (DMMA, default) and on the CUDA cores (USFFT_EVAL=fma)
-    both match the oracle's direct double sum; odd sizes exercise every tile edge."""
-    rng = np.random.default_rng(8)
-    d, G, nI, n = 7, 37, 45, 301
+@pytest.mark.parametrize("n", [301, 1])
+def test_eval_vs_oracle(B, ctx, n):
+    """usfft_eval and usfft_eval_err on the fp64 tensor pipe (DMMA) against the oracle's direct
+    double sum; odd sizes exercise every tile edge."""
+    rng = np.random.default_rng(8 + n)
+    d, G, nI = 7, 37, 45
     I = rng.integers(-9, 10, size=(nI, d)) * (rng.random((nI, d)) < 0.4)
     Cc = rng.standard_normal((G, nI)) + 1j * rng.standard_normal((G, nI))
     Y = rng.random((d, n))
     ref = oeval.evaluate(I, Cc, Y).real
     Cd = dev(np.stack([Cc.real, Cc.imag], -1), torch.float64)
-    for mode in ("mma", "mma-tile", "fma"):
-        if mode == "mma-tile":
-            monkeypatch.setenv("USFFT_EVAL_PHASES", "tile")
-        if mode == "fma":
-            monkeypatch.delenv("USFFT_EVAL_PHASES")
-            monkeypatch.setenv("USFFT_EVAL", "fma")
-        U = torch.empty((G, n), dtype=torch.float64, device="cuda")
-        B.usfft_eval(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), U)
-        assert np.abs(U.cpu().numpy() - ref).max() <= 1e-11 * np.abs(Cc).sum(1).max()
-        # the accuracy metric (P:885-891) through the same variant: complex modulus errors
-        # against a reference with a known offset from the approximant
-        Uref = rng.standard_normal((G, n))
-        err = torch.empty((G, 3), dtype=torch.float64, device="cuda")
-        B.usfft_eval_err(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), dev(Uref, torch.float64), err)
-        D = np.abs(Uref - oeval.evaluate(I, Cc, Y))
-        want = np.stack([D.mean(1), np.sqrt((D * D).mean(1)), D.max(1)], 1)
-        assert np.abs(err.cpu().numpy() - want).max() <= 1e-11 * want.max()
-    monkeypatch.delenv("USFFT_EVAL")
+    U = torch.empty((G, n), dtype=torch.float64, device="cuda")
+    B.usfft_eval(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), U)
+    assert np.abs(U.cpu().numpy() - ref).max() <= 1e-11 * np.abs(Cc).sum(1).max()
+    # the accuracy metric (P:885-891): complex modulus errors against a reference with a known
+    # offset from the approximant
+    Uref = rng.standard_normal((G, n))
+    err = torch.empty((G, 3), dtype=torch.float64, device="cuda")
+    B.usfft_eval_err(ctx, dev(I, torch.int16), Cd, dev(Y, torch.float64), dev(Uref, torch.float64), err)
+    D = np.abs(Uref - oeval.evaluate(I, Cc, Y))
+    want = np.stack([D.mean(1), np.sqrt((D * D).mean(1)), D.max(1)], 1)
+    assert np.abs(err.cpu().numpy() - want).max() <= 1e-11 * want.max()
 
 
 @pytest.mark.parametrize("cfgid,n,nb", [(3, 64, 9), (4, 64, 7), (5, 128, 4), (1, 8, 13), (2, 16, 11)])
-def test_pcg_mg_large_meshes(B, ctx, monkeypatch, cfgid, n, nb):
-    """The scratch-slab multigrid CG (n = 64, 128; also n = 8) meets the oracle tolerance with a
-    mesh-independent iteration count, and agrees with the Jacobi PCG; at n = 16 the register
-    kernel is forced aside (USFFT_MGG=1) so both multigrid kernels are compared too."""
+def test_pcg_mg_every_mesh(B, ctx, cfgid, n, nb):
+    """The multigrid CG of every mesh (n = 8 .. 128) meets the oracle tolerance with a
+    mesh-independent iteration count; the same samples solved in two ragged launches are
+    bit-identical."""
     cfg = config(cfgid, n=n)
     p = B.usfft_plan_round(ctx, cfg["seed"], 2, 3, 1, cfg["d"], cfg["N"], cfg["s"], "A", 200)
     G = (n - 1) ** 2
     Y = olat.nodes(p.M, p.z, p.shift, 3)[:, 3:3 + nb]
     ref = ofe.sample_pde(cfg, Y)
-    if n == 16:
-        monkeypatch.setenv("USFFT_MGG", "1")
     u = torch.empty((G, nb), dtype=torch.float64, device="cuda")
     it = torch.empty(nb, dtype=torch.int32, device="cuda")
     rel = torch.empty(nb, dtype=torch.float64, device="cuda")
     assert B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond="mg"), p, 3, nb, u, nb, None, it, rel,
                               check_conv=True) == 0
-    monkeypatch.delenv("USFFT_MGG", raising=False)
     assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
     assert rel.max().item() <= 1e-12 and it.max().item() <= 30
     # bit-identical when the same samples are solved in two ragged launches
     h = nb // 2
     a = torch.empty((G, h), dtype=torch.float64, device="cuda")
     B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond="mg"), p, 3, h, a, h)
-    if n != 16:
-        assert torch.equal(a, u[:, :h])
+    assert torch.equal(a, u[:, :h])
 
 
 @pytest.mark.parametrize("d", [1, 2])
