@@ -17,7 +17,8 @@ Readings:
       Exact zeros are never detected (kappa > 0, as with the paper's theta > 0).
   Z6  top-s~ order: kappa desc, candidate index asc.     Z7  fewer than s~ pass: keep all.
   Z24 "aggregated over all mesh nodes": votes_k = sum_g [k in D_g]; I_round = {votes >= 1}.
-  Z25 fragile decisions: |m - tau_g| <= 1e-10 max m, m = sqrt(kappa_min).
+  Z25 fragile decisions: a key within 1e-10 max m (m = sqrt(kappa_min)) of a different key on
+      the other side of the node's s~-cut, or of theta (two-sided; bit-equal keys never).
 """
 from __future__ import annotations
 
@@ -94,17 +95,39 @@ def resolve(V: np.ndarray, bins: np.ndarray, D: list, det: np.ndarray):
 
 
 def fragile(kmin: np.ndarray, s_tilde: int, theta2: float, band: float = 1e-10) -> np.ndarray:
-    """Boolean [G][|J|]: decisions within the Z25 band of their node's cut tau_g."""
+    """Boolean [G][|J|]: decisions a perturbation of the keys within the Z25 band could flip.
+
+    With m = sqrt(kappa_min), eps = band * max m and node g's candidates in the selection order
+    (m desc, index asc; Z6), the first s~ of that order are "in", the rest "out".
+    (k, g) is fragile when
+      * an "in" k has an "out" k' with m' != m and m' >= m - eps (the two could swap), or an
+        "out" k has an "in" k' with m' != m and m' <= m + eps;
+      * or k is "in" and |m - theta| <= eps (the threshold decision, Z5).
+    Bit-equal keys (e.g. two candidates in one bin of the minimising lattice) are ordered by
+    index on both sides, so they never make a decision fragile."""
     m = np.sqrt(kmin)
     G, nJ = kmin.shape
-    mmax = m.max() if m.size else 0.0
+    eps = band * (m.max() if m.size else 0.0)
     theta = np.sqrt(theta2)
+    s = min(s_tilde, nJ)
+    idx = np.arange(nJ)
     out = np.zeros_like(kmin, dtype=bool)
     for g in range(G):
-        srt = np.sort(m[g])[::-1]
-        cut = srt[s_tilde - 1] if s_tilde <= nJ else 0.0
-        tau = max(theta, cut)
-        out[g] = np.abs(m[g] - tau) <= band * mmax
+        order = np.lexsort((idx, -m[g]))
+        mv = m[g][order]
+        sel, rest = mv[:s], mv[s:]
+        fr = np.zeros(nJ, dtype=bool)
+        if rest.size and sel.size:
+            # in: the largest out-value strictly below m (rest is descending)
+            pos = np.searchsorted(-rest, -sel, side="right")
+            below = np.where(pos < rest.size, rest[np.minimum(pos, rest.size - 1)], -np.inf)
+            fr[:s] = below >= sel - eps
+            # out: the smallest in-value strictly above m (sel is descending)
+            q = np.searchsorted(-sel, -rest, side="left") - 1
+            above = np.where(q >= 0, sel[np.maximum(q, 0)], np.inf)
+            fr[s:] = above <= rest + eps
+        fr[:s] |= np.abs(sel - theta) <= eps
+        out[g, order] = fr
     return out
 
 

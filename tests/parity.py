@@ -13,12 +13,15 @@ def compare_round(det_g, n_det_g, det_idx, lstar, coef, ref, frag, val_tol):
     G = det_g.shape[0]
     same = np.zeros(G, dtype=bool)
     for g in range(G):
-        mine = set(det_g[g, :n_det_g[g]].tolist())
-        theirs = set(ref["D"][g].tolist())
-        diff = mine ^ theirs
+        mine = det_g[g, :n_det_g[g]].tolist()
+        theirs = ref["D"][g].tolist()
+        if not frag[g].any():                      # no fragile decision at g: D_g identical
+            assert mine == theirs, f"D_g differs at node {g} with no fragile decision"
+        diff = set(mine) ^ set(theirs)
         assert all(frag[g, k] for k in diff), f"non-fragile decision differs at node {g}: {sorted(diff)}"
         same[g] = not diff
-    out = {"nodes": G, "nodes_same_D": int(same.sum()), "fragile": int(frag.sum())}
+    out = {"nodes": G, "nodes_same_D": int(same.sum()), "fragile": int(frag.sum()),
+           "strict_set_check": not frag.any()}
     if not frag.any():
         assert det_idx.tolist() == ref["det"].tolist(), "round set differs with no fragile decision"
     if lstar is None:

@@ -205,3 +205,46 @@ def test_spec_evaluate(ex):
     U = evaluate.evaluate(np.array(ex["I"]), np.array([[complex(*c) for c in ex["C"]]]),
                           np.array(ex["y"]).reshape(-1, 1))
     assert abs(U[0, 0] - complex(*ex["value"])) < 1e-15
+
+
+# ---- Z25 fragile-decision rule (two-sided), pinned on hand-built key vectors ------------------
+# Keys are given as magnitudes m (kappa = m^2); max m = 1 so eps = 1e-10 throughout.
+def _frag(mags, s, theta=0.0):
+    m = np.asarray(mags, dtype=np.float64)[None, :]
+    return detect.fragile(m * m, s, theta * theta)[0].tolist()
+
+
+def test_fragile_separated_keys_none():
+    """Well separated keys and threshold: no decision is fragile, the cut element included (the
+    one-sided rule of round 1 flagged the s~-th key itself)."""
+    assert _frag([1.0, 0.5, 0.25, 0.125, 0.0625], 2, theta=0.01) == [False] * 5
+
+
+def test_fragile_cross_cut_pair():
+    """The 2nd (in) and 3rd (out) keys differ by 3e-11 < eps: exactly that pair is fragile."""
+    assert _frag([1.0, 0.5, 0.5 - 3e-11, 0.125], 2) == [False, True, True, False]
+
+
+def test_fragile_same_side_pair_not():
+    """A near tie inside the selection (both in) or outside it (both out) cannot change D_g."""
+    assert _frag([1.0, 1.0 - 3e-11, 0.5, 0.25, 0.25 - 3e-11], 2) == [False] * 5
+
+
+def test_fragile_bit_equal_across_cut_not():
+    """Bit-equal keys straddling the cut are ordered by index on both sides: not fragile; a
+    different key within eps of them across the cut is."""
+    assert _frag([1.0, 0.5, 0.5, 0.125], 2) == [False] * 4
+    assert _frag([1.0, 0.5, 0.5, 0.5 - 2e-11], 3) == [False, True, True, True]
+
+
+def test_fragile_threshold_band():
+    """An 'in' key within eps of theta is fragile (the threshold decision, Z5); an 'out' key
+    near theta is not (its rank already excludes it)."""
+    assert _frag([1.0, 0.3 + 5e-11, 0.2, 0.1], 2, theta=0.3) == [False, True, False, False]
+    assert _frag([1.0, 0.5, 0.3 + 5e-11, 0.1], 2, theta=0.3) == [False] * 4
+
+
+def test_fragile_band_edge():
+    """Differences just outside eps are not fragile; s~ >= |J| leaves no cut."""
+    assert _frag([1.0, 0.5, 0.5 - 2e-10], 2) == [False] * 3
+    assert _frag([1.0, 0.5 + 1e-12, 0.5], 5) == [False] * 3
