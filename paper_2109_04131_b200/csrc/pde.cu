@@ -13,7 +13,9 @@
 // Kernels (one CTA per sample, persistent loop over samples, fixed-tree reductions so a sample's
 // result does not depend on which CTA or rank solved it):
 //   k_pcg_mg  (pcg_mg.cuh)   multigrid-preconditioned CG, fine level in registers, n = 16, 32
-//   k_pcg_mgg (pcg_mgg.cuh)  multigrid-preconditioned CG, per-CTA scratch slab, n = 8 .. 128
+//   k_pcg_cl  (pcg_cl.cuh)   multigrid-preconditioned CG, one thread-block cluster per sample,
+//                            fine level in registers across the cluster, n = 64, 128
+//   k_pcg_mgg (pcg_mgg.cuh)  multigrid-preconditioned CG, per-CTA scratch slab, n = 8
 //   k_pcg     (below)        Jacobi PCG, shared memory (n <= 64) or a global slab, any n
 #include <cstdlib>
 #include <vector>
@@ -228,6 +230,7 @@ k_pcg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, in
 
 #include "pcg_mg.cuh"
 #include "pcg_mgg.cuh"
+#include "pcg_cl.cuh"
 
 using namespace usfft;
 
@@ -275,16 +278,50 @@ usfft_status launch_pcg_mgg_n(usfft_ctx *c, const LatParams &P, const PdeParams 
     return USFFT_OK;
 }
 
+// one thread-block cluster of CS CTAs per sample (pcg_cl.cuh), as many clusters as fit at once,
+// each looping over samples
+template <int NN, int CS, int MINB>
+usfft_status launch_pcg_cl(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
+                           int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
+                           int32_t *noconv, const double *S, const double *Bt) {
+    using C = ClC<NN, CS>;
+    const size_t dyn = sizeof(double) * (size_t)C::doubles();
+    auto kern = k_pcg_cl<NN, CS, MINB>;
+    if (usfft_status s = kernel_fit(c, kern, C::NT, dyn, nullptr)) return s;
+    cudaLaunchAttribute attr[1];
+    attr[0].id = cudaLaunchAttributeClusterDimension;
+    attr[0].val.clusterDim.x = CS;
+    attr[0].val.clusterDim.y = 1;
+    attr[0].val.clusterDim.z = 1;
+    cudaLaunchConfig_t cfg = {};
+    cfg.blockDim = dim3(C::NT);
+    cfg.dynamicSmemBytes = dyn;
+    cfg.stream = c->stream;
+    cfg.attrs = attr;
+    cfg.numAttrs = 1;
+    const auto key = std::make_pair(reinterpret_cast<const void *>(kern), dyn * 2048 + (size_t)C::NT + (size_t(1) << 62));
+    auto it = c->occupancy.find(key);
+    if (it == c->occupancy.end()) {
+        int ncl = 0;
+        cfg.gridDim = dim3(CS * c->sm_count);
+        USFFT_CUDA(c, cudaOccupancyMaxActiveClusters(&ncl, kern, &cfg));
+        if (ncl < 1) return fail(c, USFFT_ECUDA, "no cluster of %d CTAs (%zu B shared memory) fits", CS, dyn);
+        it = c->occupancy.emplace(key, ncl).first;
+    }
+    int64_t ncl = it->second;
+    if (ncl > nb) ncl = nb;
+    cfg.gridDim = dim3((unsigned)(ncl * CS));
+    USFFT_CUDA(c, cudaLaunchKernelEx(&cfg, kern, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt));
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
 usfft_status launch_pcg_mgg(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
                             int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
                             int32_t *noconv, const double *S, const double *Bt) {
     switch (Q.n) {
     case 8: return launch_pcg_mgg_n<8>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    case 16: return launch_pcg_mgg_n<16>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    case 32: return launch_pcg_mgg_n<32>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    case 64: return launch_pcg_mgg_n<64>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    case 128: return launch_pcg_mgg_n<128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    default: return fail(c, USFFT_EUNIMPL, "scratch-slab multigrid compiled for n = 8, 16, 32, 64, 128");
+    default: return fail(c, USFFT_EUNIMPL, "scratch-slab multigrid compiled for n = 8");
     }
 }
 
@@ -399,10 +436,14 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
         s = launch_pcg_mg<32, 2, 4, 16, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 16)
         s = launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
-    else if (pde->precond == 1 && n >= 8 && (n & (n - 1)) == 0)
+    else if (pde->precond == 1 && n == 128)
+        s = launch_pcg_cl<128, 8, 1>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (pde->precond == 1 && n == 64)
+        s = launch_pcg_cl<64, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+    else if (pde->precond == 1 && n == 8)
         s = launch_pcg_mgg(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1)
-        return fail(c, USFFT_EUNIMPL, "multigrid preconditioner needs n a power of two >= 8");
+        return fail(c, USFFT_EUNIMPL, "multigrid preconditioner needs n in {8, 16, 32, 64, 128}");
     // threads x nodes-per-thread: 128x2 (G <= 256), 256x4 (G <= 1024), 512x8, 1024x16
     else if (G <= 256) s = launch_pcg<2, 128>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (G <= 1024) s = launch_pcg<4, 256>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
