@@ -3,14 +3,16 @@
 One *step* = one whole Step-2 detection round of Alg. 1 (plan,
 lattice nodes + index maps, one batched PCG FE solve per lattice node, exchange, lattice FFT,
 keys, threshold, per-node selection, votes, union, resolve) at a fixed dimension t of the
-workload named by --config (default: BASELINE configs[1] = config 2, periodic d_y = 10).
+workload named by --config (default: BASELINE configs[4] = config 5, the scale workload whose
+samples BASELINE shards over 1/2/4/8 GPUs; --config 2 is the d_y = 10 periodic workload).
 The I^(1..t-1) and I^(t) sets the round works on come from running the real algorithm (Step 1
 and Step 2 up to t-1) during setup.  value = PDE samples solved per second over all ranks.
 
   python bench.py [--gpus N] [--steps K] [--warmup W] [--config C] [--impl ours|reference]
 
-Under torchrun (N > 1) the samples of each round are sharded across ranks (strong scaling);
-rank 0 prints one JSON line.
+--gpus N > 1 outside torchrun re-launches itself under torch.distributed.run with N ranks (one
+GPU each, NCCL); under torchrun WORLD_SIZE must equal N.  The samples of each round are sharded
+across ranks (strong scaling: the round's work is fixed); rank 0 prints one JSON line.
 """
 from __future__ import annotations
 
@@ -39,6 +41,25 @@ def mg_flops_per_iter(n: int) -> int:
     K (2 U2^2).  The per-sample setup (coefficients, operators, K) is not counted."""
     u0, u1, u2 = (n - 1) ** 2, (n // 2 - 1) ** 2, (n // 4 - 1) ** 2
     return 51 * u0 + 38 * u1 + 10 * u2 + 2 * u2 * u2
+
+
+def cl_flops_per_iter(n: int) -> int:
+    """Algorithmic flops of one CG iteration of the cluster multigrid kernel (k_pcg_cl, n = 64,
+    128), phase by phase: per fine node 47 (p update 2, A p + p.q 11, x / r / z0
+    updates + r.r 7, residual 10, prolongation 3, post-smoothing 12, r.u 2); per node of every
+    smoothed coarse level down to 16 cells per side 37 (residual 10, restriction 12,
+    prolongation 3, post-smoothing 12); the restriction to the 8-cell level (12 per node) and the
+    dense map K of the 8- and 4-cell levels (2 x 49^2).  Redundant work (the coarse levels are
+    replicated in every CTA of a cluster) and the per-sample setup are not counted."""
+    u = []
+    m = n
+    while m >= 8:
+        u.append((m - 1) ** 2)
+        m //= 2
+    return 47 * u[0] + sum(37 * v for v in u[1:-1]) + 12 * u[-1] + 2 * u[-1] * u[-1]
+
+
+SURVEY_FLOPS_PER_NODE_ITER = 20   # SURVEY §8(d): on-chip PCG unit, ~20 fp64 flops per node-iteration
 
 
 def mgg_flops_per_iter(n: int) -> int:
@@ -151,6 +172,8 @@ def run_ours(args):
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
+    if world != args.gpus:
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but WORLD_SIZE={world}")
     # one GPU per rank; with fewer visible GPUs than ranks (the --backend gloo check of the
     # multi-rank flow on one GPU) ranks share devices round-robin
     local = int(os.environ.get("LOCAL_RANK", "0")) % max(torch.cuda.device_count(), 1)
@@ -282,6 +305,10 @@ def run_ours(args):
         if mg and n_mesh in (16, 32):
             kname, kdesc = "k_pcg_mg", "k_pcg_mg (batched multigrid-preconditioned CG, on-chip, 1 CTA/sample)"
             fpi = mg_flops_per_iter(n_mesh)
+        elif mg and n_mesh in (64, 128):
+            kname, kdesc = "k_pcg_cl", ("k_pcg_cl (batched multigrid-preconditioned CG, on-chip, one "
+                                        "thread-block cluster of %d CTAs per sample)" % (8 if n_mesh == 128 else 4))
+            fpi = cl_flops_per_iter(n_mesh)
         elif mg:
             kname, kdesc = "k_pcg_mgg", "k_pcg_mgg (batched multigrid-preconditioned CG, scratch slab, 1 CTA/sample)"
             fpi = mgg_flops_per_iter(n_mesh)
@@ -309,9 +336,12 @@ def run_ours(args):
                          "traffic": (ncu_traffic(kname) or {}).get("bytes"),
                          "traffic_source": (ncu_traffic(kname) or {}).get("source"),
                          "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz",
-                         "flops_per_sample_iter": fpi, "precond": "mg" if mg else "jacobi"},
+                         "flops_per_sample_iter": fpi, "precond": "mg" if mg else "jacobi",
+                         "frac_survey_unit": (SURVEY_FLOPS_PER_NODE_ITER * G * iters_all / (pde_ms / 1e3) / 1e12
+                                              / world / fp64_peak) if pde_ms > 0 and fp64_peak else None,
+                         "survey_unit": "20 fp64 flops per fine node and CG iteration (SURVEY §8(d))"},
             "fft": {"kernel": ("k_fft400 (Rader, register four-step 20 x 20)" if P.M == 401 else
-                               "k_fft_rader_t (Rader/Stockham)") + " + k_kappa", "ms_per_step": fft_ms,
+                               "k_fft_rader_t (Rader/Stockham)") + " + k_kappa_grouped", "ms_per_step": fft_ms,
                     "achieved_gbs": fft_bytes / (fft_ms / 1e3) / 1e9 if fft_ms else None,
                     "hbm_peak_gbs": pk["hbm_gbs"],
                     "frac": (fft_bytes / (fft_ms / 1e3) / 1e9) / pk["hbm_gbs"] if fft_ms else None},
@@ -331,45 +361,84 @@ def run_ours(args):
         dist.destroy_process_group()
 
 
-def cpu_baseline(cfg, P, G, s_t, nJ, n_solve=None):
-    """The oracle as it stands, on a bounded sample of one round: n_solve banded-Cholesky FE
-    solves (scaled to the round's B samples) plus the oracle's DFT + detection of one full round
-    on seeded synthetic samples of the round's shape.  Single-threaded BLAS."""
+def _oracle_solves(job):
+    """Worker: the oracle's banded-Cholesky FE solves of a block of sample columns."""
+    cfg, Y = job
     from threadpoolctl import threadpool_limits
+    from oracle import fe as ofe
+    with threadpool_limits(1):
+        return ofe.sample_pde(cfg, Y)
+
+
+def cpu_cores() -> int:
+    try:
+        return len(os.sched_getaffinity(0))
+    except AttributeError:
+        return os.cpu_count() or 1
+
+
+def cpu_baseline(cfg, P, G, s_t, nJ, n_solve=None, pool=None):
+    """The oracle as it stands, on a bounded sample of one round, on all host cores: n_solve
+    banded-Cholesky FE solves spread over a process pool (one solve per core at a time; samples
+    are independent), and the oracle's lattice DFT + detection (numpy, multi-threaded
+    BLAS) of the round's L lattices of M samples for a subset of G_sub nodes and the round's |J|.
+    The round time is modelled from the two measured parts: B solves at the measured rate plus
+    the detection part scaled by G / G_sub."""
+    import multiprocessing as mp
     from oracle import detect as odet
     from oracle import dft as odft
-    from oracle import fe as ofe
+    cores = cpu_cores()
     Btot = P.L * P.M
     rng = np.random.default_rng(0)
-    with threadpool_limits(1):
-        n_solve = n_solve or max(16, min(2000, int(8.0 / (1e-6 * G * 15 + 1e-3))))
-        Y = rng.random((cfg["d"], n_solve))
-        t0 = time.perf_counter()
-        ofe.sample_pde(cfg, Y)
-        t_solve = (time.perf_counter() - t0) / n_solve
-        U = rng.standard_normal((G, Btot))
-        bins = rng.integers(0, P.M, size=(P.L, nJ))
-        t0 = time.perf_counter()
-        V = odft.round_values(U, P.M, P.L, bins)
-        odet.detect_round(V, bins, s_t, cfg["theta_rel"])
-        t_rest = time.perf_counter() - t0
+    if n_solve is None:
+        per = 1e-6 * G * 15 + 1e-3                          # ~ s per solve on one core
+        n_solve = max(cores, min(64 * cores, int(8.0 * cores / per)))
+    Y = rng.random((cfg["d"], n_solve))
+    blocks = [(cfg, Y[:, k::cores]) for k in range(cores) if Y[:, k::cores].shape[1]]
+    own = pool is None
+    if own:
+        pool = mp.get_context("fork").Pool(cores)
+    t0 = time.perf_counter()
+    pool.map(_oracle_solves, blocks)
+    t_solve = (time.perf_counter() - t0) / n_solve
+    if own:
+        pool.close()
+    nJ_s = min(nJ, 20000)
+    # ~2e9 complex multiply-adds of direct DFT (L lattices x M samples x <= min(|J|, M) bins)
+    G_sub = max(1, min(G, int(2e9 / (P.L * P.M * min(nJ_s, P.M)))))
+    U = rng.standard_normal((G_sub, Btot))
+    bins = rng.integers(0, P.M, size=(P.L, nJ_s))
+    t0 = time.perf_counter()
+    V = odft.round_values(U, P.M, P.L, bins)
+    odet.detect_round(V, bins, s_t, cfg["theta_rel"])
+    t_rest = (time.perf_counter() - t0) * (G / G_sub) * (nJ / nJ_s)
     t_round = Btot * t_solve + t_rest
-    return {"value": Btot / t_round, "unit": UNIT, "cores": 1, "kind": "oracle",
-            "sample": f"{n_solve} FE solves timed and scaled to B={Btot}, plus DFT+detect of one "
-                      f"full round ({G}x{Btot} samples, |J|={nJ}); round time {t_round:.1f} s"}
+    return {"value": Btot / t_round, "unit": UNIT, "cores": cores, "kind": "oracle",
+            "modelled": True, "t_round_s": t_round,
+            "sample": f"{n_solve} FE solves on {cores} processes (scaled to B={Btot}), plus the oracle's "
+                      f"DFT+detect of a full round for {G_sub} of {G} nodes and {nJ_s} of {nJ} candidates "
+                      f"(scaled to G and |J|); modelled round time {t_round:.1f} s"}
+
+
+# |J_t| of the Step-2 round the GPU arm times (t = 5; t = 3 for config 4), measured by the GPU
+# arm's own setup (profiles/r1_bench_configs.jsonl, BENCH_r01.json): the reference arm cannot run
+# the GPU setup, so it takes the round size from these measurements
+ROUND_NJ = {1: 205, 2: 1000, 3: 1755, 4: 2031105, 5: 1105}
 
 
 def run_reference(args):
-    """Reference arm = the oracle (CPU), rank 0 only; each step a bounded sample of the round."""
+    """Reference arm = the oracle (CPU, all host cores), rank 0 only; each step a bounded sample
+    of the round the GPU arm times, its round time modelled from the measured parts."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
+    import multiprocessing as mp
     from usfft_inputs import config
     from oracle import plan as oplan
     cfg = config(args.config)
     t_b = args.t if args.t else min(5, cfg["d"])
     s_t = cfg["s_local"] if t_b < cfg["d"] else cfg["s"]
-    nJ = 1000                                        # |J_t| of the config-2 t = 5 round the GPU arm times
+    nJ = ROUND_NJ.get(args.config, 1000)
     M = oplan.lattice_size(s_t, cfg["N"])
     L = oplan.num_lattices(nJ)
 
@@ -378,26 +447,51 @@ def run_reference(args):
     P = _P()
     P.M, P.L = M, L
     G = (cfg["n"] - 1) ** 2
-    vals = []
+    cores = cpu_cores()
+    pool = mp.get_context("fork").Pool(cores)
+    n_step = cores * (2 if G > 4000 else 8)
     for _ in range(args.warmup):
-        cpu_baseline(cfg, P, G, s_t, nJ, n_solve=16)
+        cpu_baseline(cfg, P, G, s_t, nJ, n_solve=cores, pool=pool)
     t0 = time.perf_counter()
+    vals, rounds = [], []
     for _ in range(args.steps):
-        vals.append(cpu_baseline(cfg, P, G, s_t, nJ, n_solve=64)["value"])
+        cb = cpu_baseline(cfg, P, G, s_t, nJ, n_solve=n_step, pool=pool)
+        vals.append(cb["value"])
+        rounds.append(cb["t_round_s"])
     wall = time.perf_counter() - t0
+    pool.close()
     v = float(np.mean(vals))
     line = {"impl": "reference", "metric": METRIC, "value": v, "unit": UNIT, "n_gpus": 1,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * (L * M) / v,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": 1e3 * float(np.mean(rounds)),
+            "ms_per_step_kind": "modelled from the measured bounded sample (see cpu_baseline.sample)",
+            "wall_ms_per_step": 1e3 * wall / max(args.steps, 1),
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "f64",
             "data": "synthetic",
             "config": {"workload": f"config{args.config}:{cfg['name']} Step-2 round t={t_b}",
                        "G": G, "M": M, "L": L, "nJ": nJ},
-            "cpu_baseline": {"value": v, "unit": UNIT, "cores": 1, "kind": "oracle",
-                             "sample": "per step: 64 FE solves scaled to B, plus one full-round "
-                                       "DFT+detect on synthetic samples"},
+            "cpu_baseline": {"value": v, "unit": UNIT, "cores": cores, "kind": "oracle", "modelled": True,
+                             "sample": f"per step: {n_step} FE solves on {cores} processes scaled to B = {L * M}, "
+                                       "plus the DFT+detect of a node subset of the round scaled to G"},
             "e2e": {"value": v, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
             "wall_s": wall}
     print(json.dumps(line), flush=True)
+
+
+def relaunch_distributed(args):
+    """--gpus N > 1 outside torchrun: re-run this script under torch.distributed.run, N ranks."""
+    import socket
+    import torch
+    n_vis = torch.cuda.device_count()
+    if args.gpus > n_vis and args.backend == "nccl":
+        raise SystemExit(f"bench.py: --gpus {args.gpus} but only {n_vis} GPU(s) visible")
+    with socket.socket() as sk:
+        sk.bind(("127.0.0.1", 0))
+        port = sk.getsockname()[1]
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")             # rank count and transport visible in stderr
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__)] + sys.argv[1:]
+    os.execvpe(sys.executable, cmd, env)
 
 
 def main():
@@ -405,7 +499,7 @@ def main():
     ap.add_argument("--gpus", type=int, default=1)
     ap.add_argument("--steps", type=int, default=10)
     ap.add_argument("--warmup", type=int, default=3)
-    ap.add_argument("--config", type=int, default=2)
+    ap.add_argument("--config", type=int, default=5)
     ap.add_argument("--t", type=int, default=0)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", dest="cpu_baseline", action="store_false")
@@ -414,6 +508,8 @@ def main():
                     help="process-group backend for N > 1 (gloo: functional check with ranks sharing a GPU)")
     ap.add_argument("--precond", default="", choices=["", "jacobi", "mg"])
     args = ap.parse_args()
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ and args.impl == "ours":
+        relaunch_distributed(args)
     if args.impl == "reference":
         run_reference(args)
     else:
