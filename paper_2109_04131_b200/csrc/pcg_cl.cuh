@@ -8,50 +8,62 @@
 // bottom two levels (8 and 4 cells per side) as the fixed dense map K of pcg_mg.cuh.
 //
 // A sample of n = 128 (16129 unknowns) needs ~0.5 MB of fp64 state, more than one SM holds, so a
-// cluster of CS CTAs (CS = 8 at n = 128, 4 at n = 64) shares it; CTA r of the cluster owns the
-// fine rows j0+1 .. j0+HR, j0 = r HR, HR = n / CS = 16:
-//  * level 0 (fine): each thread keeps a 2 x 4 block of nodes (x, r, p, s and the couplings) in
-//    registers, as in pcg_mg.cuh; the values the stencil needs are published in shared memory
-//    (split rows: even columns, then odd) and the strip's first / last row is also written into
-//    the neighbour CTA's halo row through distributed shared memory (st.shared::cluster);
-//  * level 1 (n/2 cells): distributed the same way (rows J0+1 .. J0+HR/2, one halo row per side);
+// cluster of CS CTAs (CS = 8 at n = 128, 4 at n = 64) shares it; CTA r owns the fine rows
+// j0+1 .. j0+HR, j0 = r HR, HR = n / CS = 16:
+//  * level 0 (fine): each thread keeps a 2 x BR block of nodes (x, r, p, s and the couplings) in
+//    registers, as in pcg_mg.cuh; the values a stencil needs are published in shared memory
+//    (split rows: even columns, then odd) with halo rows filled by the neighbour CTAs;
+//  * level 1 (n/2 cells): distributed the same way;
 //  * levels 2 .. (8 cells per side): replicated.  The restricted level-2 residual is gathered into
-//    every CTA of the cluster (each CTA writes its own rows into all CS copies) and every CTA runs
-//    the rest of the cycle locally with CTA barriers, so it needs no cluster synchronisation;
-//  * reductions: CTA partials are written into every CTA's slot table and summed in rank order,
-//    so all CTAs hold bit-identical scalars and take the same branch.
-// A phase that reads what another CTA wrote is separated from the write by one cluster barrier
-// (barrier.cluster.arrive.release / wait.acquire): eight per CG iteration.  The per-triangle
-// coefficient table of each CTA's strip is read by the other CTAs (DSMEM) for the replicated
-// levels' couplings during the setup.  Every quantity is computed in a fixed order independent of
-// the cluster's placement and of the launch, so a sample's result is deterministic.
+//    every CTA (each CTA sends its rows to all) and every CTA runs the rest of the cycle locally;
+//  * reductions: CTA partials are sent to every CTA and summed in rank order, so all CTAs hold
+//    bit-identical scalars and take the same branch.
+// Data moves between CTAs only as point-to-point DSMEM stores with transaction counts
+// (st.async ... mbarrier::complete_tx): the receiver waits on its own mbarrier for the expected
+// bytes, the sender never waits, and no cluster-wide barrier or release fence sits in the CG
+// loop.  Five exchanges per CG iteration:
+//   X1 z0 = omega D^-1 r (1 row below, 2 above) and r (1 row above): the fine residual t of the
+//      own rows and of the row above is then local;
+//   X2 level-1 Z1 (2 rows each side) and R1 (1 row each side): the level-1 residual of the own
+//      rows + the row above and the smoothed S1 of the own rows + one row each side are local;
+//   X3 the level-2 residual rows of every CTA to every CTA;
+//   X4 the preconditioned residual u (1 row each side) for w = A u;
+//   X5 the CTA partials of (r,u), (w,u), (r,r) to every CTA.
+// Every halo value is recomputed by exactly the arithmetic its owner uses, so halos equal the
+// owners' values bit for bit and the cycle is the same fixed linear map on every CTA.  A
+// transfer of exchange k for CG iteration i+1 cannot start before every CTA has sent its X5
+// partials of iteration i, which every CTA does only after its last read of iteration i's data:
+// the X5 all-to-all orders all buffer reuse (its own slots are double-buffered).  The per-sample
+// setup (coefficient tables, coarse operators, K) uses three cluster barriers.  Reductions and
+// the order of every sum are fixed, so a sample's result does not depend on the cluster that
+// solved it or on the launch split.
 #pragma once
 #include <cooperative_groups.h>
 
 namespace usfft {
 
-template <int NN, int CS>
+template <int NN, int CS, int BR_>
 struct ClC {
     static constexpr int n = NN, nx = n - 1, np = n + 1, HE = n / 2 + 1;
     static constexpr int HR = NN / CS;                       // fine rows per CTA
-    static constexpr int BC = 2, BR = 4, LX = n / 2, NRG = HR / BR, NT = LX * NRG, NWARP = NT / 32;
-    static constexpr int FR = (HR + 2) * np;                 // fine grid: local rows 0 .. HR+1
-    static constexpr int m1 = n / 2, P1 = m1 + 1, H1 = m1 / 2 + 1, R1ROWS = HR / 2 + 2, F1 = R1ROWS * P1;
-    static constexpr int HR1 = HR / 2, HR2 = HR / 4;        // own level-1 / level-2 rows
-    // replicated levels 2 .. LK-1 (natural rows, zero ring); level LK has 8 cells (the K map)
+    static constexpr int BC = 2, BR = BR_, LX = n / 2, NRG = HR / BR, NT = LX * NRG, NWARP = NT / 32;
+    static constexpr int FRW = HR + 3, FR = FRW * np;        // fine grid rows 0 .. HR+2 (local)
+    static constexpr int m1 = n / 2, P1 = m1 + 1, H1 = m1 / 2 + 1, HR1 = HR / 2, HR2 = HR / 4;
+    static constexpr int L1R = HR1 + 4, F1 = L1R * P1;       // level-1 rows jl = -1 .. HR1+2 (lr = jl+1)
     static constexpr int LK = NN == 64 ? 3 : NN == 128 ? 4 : -1;
     static_assert(LK > 0, "cluster multigrid compiled for n = 64, 128");
-    static_assert(HR % 8 == 0 && LX % 32 == 0, "strip geometry");
+    static_assert(HR % 8 == 0 && LX % 32 == 0 && BR % 2 == 0 && HR % BR == 0, "strip geometry");
     __host__ __device__ static constexpr int ml(int l) { return NN >> l; }
     __host__ __device__ static constexpr int Pl(int l) { return (NN >> l) + 1; }
     __host__ __device__ static constexpr int Nl(int l) { return ((NN >> l) + 1) * ((NN >> l) + 1); }
     static constexpr int mK = 8, PK = 9, NK = 81, UK = 49, HK = (UK + 1) / 2;
     static constexpr int mE = 4, PE = 5, NE = 25, UE = 9;
     static constexpr int KPAD = (8 - (HK * UK) % 16 + 16) % 16;
-    static constexpr int ATR = HR + 2;                       // coefficient-table rows j0 .. j0+HR+1
+    static constexpr int ATR = HR + 6;                       // coefficient-table cell rows j0-2 .. j0+HR+3
     // shared-memory layout (doubles)
-    static constexpr int oDI0 = 0, oG0 = FR, oG1 = 2 * FR;
-    static constexpr int oL1 = 3 * FR;                       // WH1, WV1, DI1, R1, Z1, T1 (= S1)
+    static constexpr int oDI0 = 0, oG0 = FR, oG1 = 2 * FR;   // fine omega D^-1, z0 grid, t / u grid
+    static constexpr int oRh = 3 * FR, oWHh = oRh + np, oWVh0 = oWHh + np, oWVh1 = oWVh0 + np;
+    static constexpr int oL1 = oWVh1 + np;                   // WH1, WV1, DI1, R1, Z1, T1 (= S1)
     __host__ __device__ static constexpr int oLev(int l) {   // replicated level l: WH, WV, DI, R, Z, T (= S)
         int o = oL1 + 6 * F1;
         for (int q = 2; q < l; ++q) o += 6 * Nl(q);
@@ -61,12 +73,19 @@ struct ClC {
     static constexpr int oKt = oKs + 5 * NK + 2 * HK;
     static constexpr int oWHE = oKt + 2 * HK * UK + KPAD, oWVE = oWHE + NE, oAI = oWVE + NE;
     static constexpr int oB = oAI + UE * UE, oC = oB + UE * UK;
-    static constexpr int oRed = oC + UE * UK;                // [CS][4] cluster reduction slots
-    static constexpr int oWred = oRed + 4 * CS;              // [4][NWARP] CTA reduction
+    static constexpr int oRed = oC + UE * UK;                // [2][CS][4] cluster partials (double-buffered)
+    static constexpr int oWred = oRed + 8 * CS;              // [4][NWARP] CTA partials
     __host__ __device__ static constexpr int doubles() { return oWred + 4 * NWARP; }
+    // setup: the coarse-level triangle coefficients (levels 2 .. LK+1, lower then upper plane)
+    __host__ __device__ static constexpr int ctoff(int l) {
+        int o = 0;
+        for (int q = 2; q < l; ++q) o += 2 * ml(q) * ml(q);
+        return o;
+    }
+    static constexpr int STAGE = oRed - oL1;                 // staging room for the psi factors
     static_assert(2 * ATR * n <= 3 * FR, "coefficient table must fit in DI0 .. G1");
-    static_assert(2 * UK <= NT, "two threads per row of K");
-    static_assert(3 * CS <= 32, "one warp writes the reduction slots");
+    static_assert(ctoff(LK + 2) <= oRed - oKt, "coarse coefficient table must fit in the K region");
+    static_assert(2 * UK <= NT && 3 * CS <= 32, "thread mapping");
 };
 
 __device__ __forceinline__ void cluster_barrier() {
@@ -82,38 +101,80 @@ __device__ __forceinline__ unsigned cluster_count_x() {
     asm("mov.u32 %0, %%nclusterid.x;" : "=r"(v));
     return v;
 }
+__device__ __forceinline__ unsigned cluster_rank() {
+    unsigned v;
+    asm("mov.u32 %0, %%cluster_ctarank;" : "=r"(v));
+    return v;
+}
+__device__ __forceinline__ uint32_t smem_addr(const void *p) { return (uint32_t)__cvta_generic_to_shared(p); }
+// shared::cluster address of the same variable in CTA `rank` of the cluster
+__device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
+    uint32_t o;
+    asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(rank));
+    return o;
+}
+// 8-byte DSMEM store completing 8 transaction bytes on the destination CTA's mbarrier
+__device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
+                 :: "r"(dst), "l"(__double_as_longlong(v)), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void mbar_init(uint32_t mb) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
+}
+__device__ __forceinline__ void mbar_expect(uint32_t mb, uint32_t bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
+    asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
+                 "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+                 "@!p bra WAIT_%=;\n\t}" :: "r"(mb), "r"(parity) : "memory");
+}
 
-template <int NN, int CS, int MINB>
-__global__ void __launch_bounds__(ClC<NN, CS>::NT, MINB)
+// Phase-latency probe (tools/cl_probe.py builds with -DUSFFT_CL_PROBE): clock64() of thread 0 of
+// every CTA of cluster 0 at each phase boundary of its first sample (setup) and CG iteration 6.
+#ifdef USFFT_CL_PROBE
+__device__ long long g_cl_probe[16][32];
+#define CL_MARK(on, id)                                                                             \
+    do {                                                                                           \
+        if ((on) && threadIdx.x == 0) g_cl_probe[rank][id] = clock64();                             \
+    } while (0)
+#else
+#define CL_MARK(on, id) ((void)0)
+#endif
+
+template <int NN, int CS, int BR_, int MINB>
+__global__ void __launch_bounds__(ClC<NN, CS, BR_>::NT, MINB)
 k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
          int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
          const double *__restrict__ Bt) {
-    using L = ClC<NN, CS>;
+    using L = ClC<NN, CS, BR_>;
     namespace cg = cooperative_groups;
     constexpr int n = NN, nx = L::nx, np = L::np, HE = L::HE, HR = L::HR, BC = L::BC, BR = L::BR;
     constexpr int LX = L::LX, NRG = L::NRG, NT = L::NT, NWARP = L::NWARP, W = 3 * n + 1;
     constexpr int m1 = L::m1, P1 = L::P1, H1 = L::H1, HR1 = L::HR1, HR2 = L::HR2, LK = L::LK;
     constexpr int mK = L::mK, PK = L::PK, NK = L::NK, UK = L::UK, HK = L::HK;
     constexpr int mE = L::mE, PE = L::PE, UE = L::UE, ATR = L::ATR;
+    constexpr int m2 = L::ml(2), P2 = L::Pl(2);
     extern __shared__ double sm[];
     __shared__ double th_amp[kMaxD];
+    __shared__ alignas(8) unsigned long long mbar[5];
     cg::cluster_group cluster = cg::this_cluster();
-    const int rank = (int)cluster.block_rank();
+    const int rank = (int)cluster_rank();
+    const bool has_lo = rank > 0, has_hi = rank < CS - 1;
     const int j0 = rank * HR, J0 = j0 / 2, J20 = j0 / 4;
 
     double *DI0 = sm + L::oDI0, *G0 = sm + L::oG0, *G1 = sm + L::oG1, *aT = sm;   // aT: setup only
+    double *Rh = sm + L::oRh, *WHh = sm + L::oWHh, *WVh0 = sm + L::oWVh0, *WVh1 = sm + L::oWVh1;
     double *WH1 = sm + L::oL1, *WV1 = WH1 + L::F1, *DI1 = WH1 + 2 * L::F1, *R1 = WH1 + 3 * L::F1;
     double *Z1 = WH1 + 4 * L::F1, *T1 = WH1 + 5 * L::F1, *S1 = T1;
     double *WHK = sm + L::oKs, *WVK = WHK + NK, *DK = WHK + 2 * NK, *DIK = WHK + 3 * NK, *SK = WHK + 4 * NK;
-    double *RK = WHK + 5 * NK, *Kt = sm + L::oKt;
+    double *RK = WHK + 5 * NK, *Kt = sm + L::oKt, *ctab = sm + L::oKt;
     double *WHE = sm + L::oWHE, *WVE = sm + L::oWVE, *AI = sm + L::oAI, *Bm = sm + L::oB, *Cm = sm + L::oC;
     double *cred = sm + L::oRed, *wred = sm + L::oWred;
-    // neighbours' grids (distributed shared memory); nullptr at the domain edges
-    double *G0lo = rank > 0 ? cluster.map_shared_rank(G0, rank - 1) : nullptr;
-    double *G0hi = rank < CS - 1 ? cluster.map_shared_rank(G0, rank + 1) : nullptr;
-    double *G1lo = rank > 0 ? cluster.map_shared_rank(G1, rank - 1) : nullptr;
-    double *G1hi = rank < CS - 1 ? cluster.map_shared_rank(G1, rank + 1) : nullptr;
+    auto lv = [&](int l, int k) -> double * { return sm + L::oLev(l) + k * L::Nl(l); };
+    enum { LWH = 0, LWV = 1, LDI = 2, LR = 3, LZ = 4, LT = 5 };
+    double *R2 = lv(2, LR);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lx = tid % LX, rg = tid / LX;
@@ -121,9 +182,32 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     const double inv_n3 = 1.0 / ((double)n * n * n);
     const double *Sy0 = S + (Q.psi ? Q.d * W : 0);
 
-    // replicated level l arrays (natural rows): WH, WV, DI, R, Z, T (= S)
-    auto lv = [&](int l, int k) -> double * { return sm + L::oLev(l) + k * L::Nl(l); };
-    enum { LWH = 0, LWV = 1, LDI = 2, LR = 3, LZ = 4, LT = 5 };
+    // ---- exchanges: mbarriers, expected bytes, peer addresses -----------------------------------
+    const uint32_t mb0 = smem_addr(&mbar[0]);
+    const uint32_t xb[5] = {(uint32_t)(8 * nx * ((has_hi ? 3 : 0) + (has_lo ? 1 : 0))),
+                            (uint32_t)(8 * (m1 - 1) * ((has_hi ? 3 : 0) + (has_lo ? 3 : 0))),
+                            (uint32_t)(8 * (m2 - 1) * (m2 - 1)),
+                            (uint32_t)(8 * nx * ((has_hi ? 1 : 0) + (has_lo ? 1 : 0))),
+                            (uint32_t)(8 * 3 * CS)};
+    if (tid == 0) {
+        for (int k = 0; k < 5; ++k) mbar_init(mb0 + 8 * k);
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        for (int k = 0; k < 5; ++k) mbar_expect(mb0 + 8 * k, xb[k]);
+    }
+    uint32_t ph = 0;                                     // bit k: parity of exchange k's next phase
+    auto xwait = [&](int k) {
+        mbar_wait(mb0 + 8 * k, (ph >> k) & 1u);
+        ph ^= 1u << k;
+        if (tid == 0) mbar_expect(mb0 + 8 * k, xb[k]);   // arm the next phase
+    };
+    const uint32_t lo_rank = has_lo ? rank - 1 : rank, hi_rank = has_hi ? rank + 1 : rank;
+    const uint32_t mb_lo = mapa(mb0, lo_rank), mb_hi = mapa(mb0, hi_rank);
+    const uint32_t G0_lo = mapa(smem_addr(G0), lo_rank), G0_hi = mapa(smem_addr(G0), hi_rank);
+    const uint32_t G1_lo = mapa(smem_addr(G1), lo_rank), G1_hi = mapa(smem_addr(G1), hi_rank);
+    const uint32_t Rh_lo = mapa(smem_addr(Rh), lo_rank);
+    const uint32_t R1_lo = mapa(smem_addr(R1), lo_rank), R1_hi = mapa(smem_addr(R1), hi_rank);
+    const uint32_t Z1_lo = mapa(smem_addr(Z1), lo_rank), Z1_hi = mapa(smem_addr(Z1), hi_rank);
+    cluster_barrier();                                   // mbarriers initialised everywhere
 
     // ---- addressing -------------------------------------------------------------------------
     // fine node (col0 + 1 + c, row0 + 1 + q) local; c even = odd column, c odd = even column
@@ -131,65 +215,85 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         const int slot = (c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1);
         return (row0 + 1 + q) * np + slot;
     };
+    auto slot0 = [](int i) -> int { return (i & 1) ? HE + (i >> 1) : (i >> 1); };   // fine column i
     auto valid = [&](int q, int c) { return col0 + c + 1 <= nx && j0 + row0 + q + 1 <= nx; };
     auto col1s = [](int i) -> int { return (i & 1) ? H1 + (i >> 1) : (i >> 1); };
-    auto e1 = [&](int I, int jl) -> int { return jl * P1 + col1s(I); };   // level-1 local row jl
+    auto e1 = [&](int I, int jl) -> int { return (jl + 1) * P1 + col1s(I); };      // level-1 row jl
 
     for (int64_t bl = cluster_id_x(); bl < nb; bl += cluster_count_x()) {
         const int64_t b = b0 + bl;
-        // ---- K3: coefficients of the strip's triangles ----------------------------------------
+        const bool pset = cluster_id_x() == 0 && bl == 0;
+        (void)pset;
+        CL_MARK(pset, 20);
+        // ---- K3: coefficients of the triangles of cell rows j0-2 .. j0+HR+3 --------------------
         for (int j = tid; j < Q.d; j += NT) {
             const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
             th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
-        {   // aT[plane][cj - j0][ci] for cell rows j0 .. j0+ATR-1 (< n): thread = (column, row set)
+        // stage the factors amp_j theta_j X_j at the 2n lower/upper abscissae and Y_j at the
+        // strip's 2 ATR ordinates (one bulk of independent L2 loads instead of a dependent one per term)
+        const bool staged = Q.d * (2 * n + 2 * ATR) <= L::STAGE;
+        double *Xs = sm + L::oL1, *Ys = Xs + 2 * n * Q.d;
+        if (staged) {
+            for (int e = tid; e < 2 * n * Q.d; e += NT) {
+                const int j = e / (2 * n), c = e - j * 2 * n, up = c >= n, ci = up ? c - n : c;
+                Xs[e] = th_amp[j] * __ldg(S + j * W + 3 * ci + (up ? 1 : 2));
+            }
+            for (int e = tid; e < 2 * ATR * Q.d; e += NT) {
+                const int j = e / (2 * ATR), c = e - j * 2 * ATR, up = c >= ATR, rl = up ? c - ATR : c;
+                const int cj = min(max(j0 - 2 + rl, 0), n - 1);
+                Ys[e] = __ldg(Sy0 + j * W + 3 * cj + (up ? 2 : 1));
+            }
+            __syncthreads();
+        }
+        {   // aT[plane][cj - (j0-2)][ci]: thread = (column, row set)
             constexpr int CPT = NT / n, KJ = (ATR + CPT - 1) / CPT;
             const int ci = tid % n, r0 = tid / n;
             double slo[KJ], sup[KJ];
 #pragma unroll
             for (int k = 0; k < KJ; ++k) slo[k] = sup[k] = 0.0;
+            if (staged) {
 #pragma unroll 2
-            for (int j = 0; j < Q.d; ++j) {
-                const double *Sj = S + j * W, *Sy = Sy0 + j * W;
-                const double am = th_amp[j];
-                const double tlo = am * __ldg(Sj + 3 * ci + 2), tup = am * __ldg(Sj + 3 * ci + 1);
+                for (int j = 0; j < Q.d; ++j) {
+                    const double tlo = Xs[j * 2 * n + ci], tup = Xs[j * 2 * n + n + ci];
+                    const double *yl = Ys + j * 2 * ATR, *yu = yl + ATR;
 #pragma unroll
-                for (int k = 0; k < KJ; ++k) {
-                    const int cj = min(j0 + r0 + CPT * k, n - 1);
-                    slo[k] = fma(tlo, __ldg(Sy + 3 * cj + 1), slo[k]);
-                    sup[k] = fma(tup, __ldg(Sy + 3 * cj + 2), sup[k]);
+                    for (int k = 0; k < KJ; ++k) {
+                        const int rl = min(r0 + CPT * k, ATR - 1);
+                        slo[k] = fma(tlo, yl[rl], slo[k]);
+                        sup[k] = fma(tup, yu[rl], sup[k]);
+                    }
+                }
+            } else {
+                for (int j = 0; j < Q.d; ++j) {
+                    const double am = th_amp[j];
+                    const double tlo = am * __ldg(S + j * W + 3 * ci + 2), tup = am * __ldg(S + j * W + 3 * ci + 1);
+#pragma unroll
+                    for (int k = 0; k < KJ; ++k) {
+                        const int cj = min(max(j0 - 2 + r0 + CPT * k, 0), n - 1);
+                        slo[k] = fma(tlo, __ldg(Sy0 + j * W + 3 * cj + 1), slo[k]);
+                        sup[k] = fma(tup, __ldg(Sy0 + j * W + 3 * cj + 2), sup[k]);
+                    }
                 }
             }
 #pragma unroll
             for (int k = 0; k < KJ; ++k) {
-                const int rl = r0 + CPT * k;
-                if (rl < ATR && j0 + rl < n) {
+                const int rl = r0 + CPT * k, cj = j0 - 2 + rl;
+                if (rl < ATR && cj >= 0 && cj < n) {
                     aT[rl * n + ci] = Q.form == 0 ? 1.0 + slo[k] : exp(slo[k]);              // lower
                     aT[(ATR + rl) * n + ci] = Q.form == 0 ? 1.0 + sup[k] : exp(sup[k]);      // upper
                 }
             }
         }
-        cluster_barrier();                               // every strip's table is complete
+        cluster_barrier();                               // A: nobody stages any more; own table complete
+        CL_MARK(pset, 21);
         // a of T_lo / T_up of cell (ci, cj) of the level with cells of width 2^sh h: the fine
-        // triangle with the same centroid (pcg_mg.cuh), read from the CTA whose strip holds it
-        auto fcoef = [&](int ci, int cj, int up, int sh) -> double {
+        // triangle with the same centroid (pcg_mg.cuh), from the local table
+        auto fcl = [&](int ci, int cj, int up, int sh) -> double {
             const int p = 1 << sh, ra = up ? p : 2 * p, rb = up ? 2 * p : p;
             const int fi = ci * p + ra / 3, fj = cj * p + rb / 3, pl = (ra % 3 == 1) ? 1 : 0;
-            const int own = min(fj / HR, CS - 1);
-            const double *src = own == rank ? aT : cluster.map_shared_rank(aT, own);
-            return src[(pl * ATR + fj - own * HR) * n + fi];
-        };
-        auto fcoef_loc = [&](int ci, int cj, int up, int sh) -> double {   // cell rows j0 .. j0+HR+1
-            const int p = 1 << sh, ra = up ? p : 2 * p, rb = up ? 2 * p : p;
-            const int fi = ci * p + ra / 3, fj = cj * p + rb / 3, pl = (ra % 3 == 1) ? 1 : 0;
-            return aT[(pl * ATR + fj - j0) * n + fi];
-        };
-        auto whg = [&](int i, int j, int M, int sh) -> double {
-            return (i < M && j >= 1 && j < M) ? 0.5 * (fcoef(i, j, 0, sh) + fcoef(i, j - 1, 1, sh)) : 0.0;
-        };
-        auto wvg = [&](int i, int j, int M, int sh) -> double {
-            return (j < M && i >= 1 && i < M) ? 0.5 * (fcoef(i, j, 1, sh) + fcoef(i - 1, j, 0, sh)) : 0.0;
+            return aT[(pl * ATR + fj - (j0 - 2)) * n + fi];
         };
         // fine couplings of the own block (ring edges included)
         double cE[BR][BC + 1], cN[BR + 1][BC];
@@ -198,54 +302,92 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int c = 0; c <= BC; ++c) {
                 const int i = col0 + c, j = j0 + row0 + q + 1;
-                cE[q][c] = (i <= nx && j <= nx) ? 0.5 * (aT[(j - j0) * n + i] + aT[(ATR + j - 1 - j0) * n + i]) : 0.0;
+                cE[q][c] = (i <= nx && j <= nx) ? 0.5 * (fcl(i, j, 0, 0) + fcl(i, j - 1, 1, 0)) : 0.0;
             }
 #pragma unroll
         for (int q = 0; q <= BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
                 const int i = col0 + c + 1, j = j0 + row0 + q;
-                cN[q][c] = (i <= nx && j <= nx) ? 0.5 * (aT[(ATR + j - j0) * n + i] + aT[(j - j0) * n + i - 1]) : 0.0;
+                cN[q][c] = (i <= nx && j <= nx) ? 0.5 * (fcl(i, j, 1, 0) + fcl(i - 1, j, 0, 0)) : 0.0;
             }
-        // level-1 couplings of the local rows 0 .. HR1 (J = J0 + jl)
-        for (int e = tid; e < (HR1 + 1) * P1; e += NT) {
-            const int jl = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, J = J0 + jl;
-            WH1[e] = (I < m1 && J >= 1 && J < m1 && jl >= 1)
-                         ? 0.5 * (fcoef_loc(I, J, 0, 1) + fcoef_loc(I, J - 1, 1, 1)) : 0.0;
-            WV1[e] = (J < m1 && I >= 1 && I < m1) ? 0.5 * (fcoef_loc(I, J, 1, 1) + fcoef_loc(I - 1, J, 0, 1)) : 0.0;
+        for (int i = tid; i <= n; i += NT) {             // couplings of the halo row above (HR+1)
+            const int jh = j0 + HR + 1;
+            WHh[i] = (i <= nx && jh <= nx) ? 0.5 * (fcl(i, jh, 0, 0) + fcl(i, jh - 1, 1, 0)) : 0.0;
+            WVh0[i] = (i >= 1 && i <= nx && jh - 1 <= nx) ? 0.5 * (fcl(i, jh - 1, 1, 0) + fcl(i - 1, jh - 1, 0, 0)) : 0.0;
+            WVh1[i] = (i >= 1 && i <= nx && jh <= nx) ? 0.5 * (fcl(i, jh, 1, 0) + fcl(i - 1, jh, 0, 0)) : 0.0;
         }
-        // replicated levels 2 .. LK-1, K level LK (8 cells), exact level (4 cells)
+        for (int e = tid; e < L::F1; e += NT) {           // level-1 couplings, rows jl = -1 .. HR1+1
+            const int lr = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lr - 1, J = J0 + jl;
+            WH1[e] = (jl >= 0 && jl <= HR1 + 1 && I < m1 && J >= 1 && J < m1)
+                         ? 0.5 * (fcl(I, J, 0, 1) + fcl(I, J - 1, 1, 1)) : 0.0;
+            WV1[e] = (jl <= HR1 + 1 && J >= 0 && J < m1 && I >= 1 && I < m1)
+                         ? 0.5 * (fcl(I, J, 1, 1) + fcl(I - 1, J, 0, 1)) : 0.0;
+        }
+        {   // coarse triangle coefficients (levels 2 .. LK+1) whose fine triangle is in the own rows,
+            // sent to every CTA's coarse table
+            constexpr int NC = L::ctoff(LK + 2) / 2;       // coarse cells of all levels
+            for (int e = tid; e < 2 * NC; e += NT) {
+                const int up = e >= NC, q = up ? e - NC : e;
+                int l = 2, base = 0;
+                while (q - base >= L::ml(l) * L::ml(l)) {
+                    base += L::ml(l) * L::ml(l);
+                    ++l;
+                }
+                const int m = L::ml(l), cell = q - base, ci = cell % m, cj = cell / m;
+                const int p = 1 << l, rb = up ? 2 * p : p, fj = cj * p + rb / 3;
+                if (fj / HR != rank) continue;
+                const double v = fcl(ci, cj, up, l);
+                const int dst = L::ctoff(l) + (up ? m * m : 0) + cell;
 #pragma unroll
-        for (int l = 2; l < LK; ++l) {
-            const int M = L::ml(l), Pq = L::Pl(l);
-            double *wh = lv(l, LWH), *wv = lv(l, LWV);
-            for (int e = tid; e < L::Nl(l); e += NT) {
-                const int I = e % Pq, J = e / Pq;
-                wh[e] = whg(I, J, M, l);
-                wv[e] = wvg(I, J, M, l);
+                for (int k = 0; k < CS; ++k) cluster.map_shared_rank(ctab, k)[dst] = v;
             }
         }
-        for (int e = tid; e < NK; e += NT) {
-            const int I = e % PK, J = e / PK;
-            WHK[e] = whg(I, J, mK, LK);
-            WVK[e] = wvg(I, J, mK, LK);
+        cluster_barrier();                               // B: every coarse table complete
+        CL_MARK(pset, 22);
+        {   // replicated couplings from the coarse table
+            auto ct = [&](int l, int ci, int cj, int up) -> double {
+                const int m = L::ml(l);
+                return ctab[L::ctoff(l) + (up ? m * m : 0) + cj * m + ci];
+            };
+            auto whc = [&](int l, int I, int J) -> double {
+                const int M = L::ml(l);
+                return (I < M && J >= 1 && J < M) ? 0.5 * (ct(l, I, J, 0) + ct(l, I, J - 1, 1)) : 0.0;
+            };
+            auto wvc = [&](int l, int I, int J) -> double {
+                const int M = L::ml(l);
+                return (J < M && I >= 1 && I < M) ? 0.5 * (ct(l, I, J, 1) + ct(l, I - 1, J, 0)) : 0.0;
+            };
+#pragma unroll
+            for (int l = 2; l < LK; ++l) {
+                const int Pq = L::Pl(l);
+                double *wh = lv(l, LWH), *wv = lv(l, LWV);
+                for (int e = tid; e < L::Nl(l); e += NT) {
+                    const int I = e % Pq, J = e / Pq;
+                    wh[e] = whc(l, I, J);
+                    wv[e] = wvc(l, I, J);
+                }
+            }
+            for (int e = tid; e < NK; e += NT) {
+                const int I = e % PK, J = e / PK;
+                WHK[e] = whc(LK, I, J);
+                WVK[e] = wvc(LK, I, J);
+            }
+            for (int e = tid; e < L::NE; e += NT) {
+                const int I = e % PE, J = e / PE;
+                WHE[e] = whc(LK + 1, I, J);
+                WVE[e] = wvc(LK + 1, I, J);
+            }
         }
-        for (int e = tid; e < L::NE; e += NT) {
-            const int I = e % PE, J = e / PE;
-            WHE[e] = whg(I, J, mE, LK + 1);
-            WVE[e] = wvg(I, J, mE, LK + 1);
-        }
-        cluster_barrier();                               // nobody reads a coefficient table any more
+        __syncthreads();                                 // the coarse table (K region) is dead
         // ---- diagonals, zeroed grids, the dense maps -------------------------------------------
-        for (int e = tid; e < 2 * L::FR; e += NT) G0[e] = 0.0;          // G0, G1 (rings, halos)
-        for (int e = tid; e < L::FR; e += NT) DI0[e] = 0.0;
-        for (int e = tid; e < 3 * L::F1; e += NT) R1[e] = 0.0;          // R1, Z1, T1
-        for (int e = tid; e < L::R1ROWS * P1; e += NT) {                // level-1 omega D^-1 (own rows)
-            const int jl = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, J = J0 + jl;
-            const bool in = I >= 1 && I < m1 && J >= 1 && J < m1 && jl >= 1 && jl <= HR1;
+        for (int e = tid; e < 3 * L::FR + L::np; e += NT) DI0[e] = 0.0;   // DI0, G0, G1, Rh
+        for (int e = tid; e < L::F1; e += NT) {           // level-1 omega D^-1 (rows 0 .. HR1+1)
+            const int lr = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lr - 1, J = J0 + jl;
+            const bool in = I >= 1 && I < m1 && J >= 1 && J < m1 && jl >= 0 && jl <= HR1 + 1;
             const double dv = in ? WH1[e] + WH1[e1(I - 1, jl)] + WV1[e] + WV1[e - P1] : 1.0;
-            DI1[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
-            if (jl > HR1) WH1[e] = WV1[e] = 0.0;                        // (unused halo row)
+            DI1[e] = in ? kMgOmega * rcp_pos(dv) : 0.0;
+            R1[e] = Z1[e] = T1[e] = 0.0;
         }
 #pragma unroll
         for (int l = 2; l < LK; ++l) {
@@ -255,7 +397,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int e = tid; e < L::Nl(l); e += NT) {
                 const int I = e % Pq, J = e / Pq;
                 const bool in = I >= 1 && I < M && J >= 1 && J < M;
-                di[e] = in ? kMgOmega * (1.0 / (wh[e] + wh[e - 1] + wv[e] + wv[e - Pq])) : 0.0;
+                di[e] = in ? kMgOmega * rcp_pos(wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) : 0.0;
                 lv(l, LR)[e] = lv(l, LZ)[e] = lv(l, LT)[e] = 0.0;
             }
         }
@@ -352,27 +494,10 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             else if (d == 3 && Ji < mK - 1) Kt[kix(i + (mK - 1), i)] += dwi * WVK[ei] * DIK[ei + PK];
             else if (d == 4 && Ji > 1) Kt[kix(i - (mK - 1), i)] += dwi * WVK[ei - PK] * DIK[ei - PK];
         }
-        cluster_barrier();   // setup complete in every CTA before any neighbour writes a halo
+        cluster_barrier();   // C: every CTA's grids are zeroed before any neighbour sends into them
+        CL_MARK(pset, 23);
 
         // ---- helpers of the iteration -----------------------------------------------------------
-        // publish own values into Gd and the strip's edge rows into the neighbours' halo rows
-        auto publish = [&](double *Gd, double *Glo, double *Ghi, const double (&v)[BR][BC]) {
-#pragma unroll
-            for (int q = 0; q < BR; ++q)
-#pragma unroll
-                for (int c = 0; c < BC; ++c)
-                    if (valid(q, c)) Gd[fe(c, q)] = v[q][c];
-            if (rg == 0 && Glo) {
-#pragma unroll
-                for (int c = 0; c < BC; ++c)
-                    if (valid(0, c)) Glo[fe(c, 0) + HR * np] = v[0][c];
-            }
-            if (rg == NRG - 1 && Ghi) {
-#pragma unroll
-                for (int c = 0; c < BC; ++c)
-                    if (valid(BR - 1, c)) Ghi[fe(c, BR - 1) - HR * np] = v[BR - 1][c];
-            }
-        };
         auto diag = [&](int q, int c) -> double { return cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c]; };
         auto apply_fine = [&](const double *Gs, const double (&v)[BR][BC], double (&out)[BR][BC]) {
 #pragma unroll
@@ -391,17 +516,29 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     out[q][c] = valid(q, c) ? a : 0.0;
                 }
         };
-        // level-1 operator at own (I, jl) (diagonal summed in the order of DI1)
-        auto apply1 = [&](const double *Zs, int I, int jl) -> double {
-            const int e = e1(I, jl), el = e1(I - 1, jl), er = e1(I + 1, jl);
-            const double whe = WH1[e], whl = WH1[el], wve = WV1[e], wvd = WV1[e - P1];
-            return (whe + whl + wve + wvd) * Zs[e] - whe * Zs[er] - whl * Zs[el] - wve * Zs[e + P1] -
-                   wvd * Zs[e - P1];
+        auto local_publish = [&](double *Gd, const double (&v)[BR][BC]) {
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+#pragma unroll
+                for (int c = 0; c < BC; ++c)
+                    if (valid(q, c)) Gd[fe(c, q)] = v[q][c];
         };
-        // the same on a replicated natural-row level
-        auto applyl = [](const double *wh, const double *wv, const double *z, int e, int Pq) -> double {
-            const double we = wh[e], ww = wh[e - 1], wn = wv[e], ws = wv[e - Pq];
-            return (we + ww + wn + ws) * z[e] - we * z[e + 1] - ww * z[e - 1] - wn * z[e + Pq] - ws * z[e - Pq];
+        // X1: z0 rows 1, 2 -> rows HR+1, HR+2 below; z0 row HR -> row 0 above; r row 1 -> Rh below
+        auto send_x1 = [&](const double (&z)[BR][BC], const double (&rv)[BR][BC]) {
+            if (rg == 0 && has_lo) {
+#pragma unroll
+                for (int c = 0; c < BC; ++c)
+                    if (col0 + c + 1 <= nx) {
+                        st_async(G0_lo + 8 * (fe(c, 0) + HR * np), z[0][c], mb_lo);
+                        st_async(G0_lo + 8 * (fe(c, 1) + HR * np), z[1][c], mb_lo);
+                        st_async(Rh_lo + 8 * (col0 + c + 1), rv[0][c], mb_lo);
+                    }
+            }
+            if (rg == NRG - 1 && has_hi) {
+#pragma unroll
+                for (int c = 0; c < BC; ++c)
+                    if (col0 + c + 1 <= nx) st_async(G0_hi + 8 * (fe(c, BR - 1) - HR * np), z[BR - 1][c], mb_hi);
+            }
         };
         auto prol2w = [](const double *Xc, int pc, int i, int j) -> double {   // bilinear, branch-free
             const double *z2 = Xc + (j >> 1) * pc + (i >> 1);
@@ -409,101 +546,162 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             const double wy1 = (j & 1) ? 0.5 : 0.0, wy0 = (j & 1) ? 0.5 : 1.0;
             return fma(wx1 * wy1, z2[pc + 1], fma(wx0 * wy1, z2[pc], fma(wx1 * wy0, z2[1], wx0 * wy0 * z2[0])));
         };
-        // own level-1 interior nodes: q -> (I, jl), lanes walk whole rows of m1 slots
-        auto for1 = [&](auto body) {
-            constexpr int U = m1 * HR1;
+        // level-1 nodes (I in 1 .. m1-1) of the local rows jl = JA .. JA+NR-1 inside the mesh
+        auto for1 = [&](auto ja, auto nr, auto body) {
+            constexpr int JA = decltype(ja)::value, NR = decltype(nr)::value, U = m1 * NR;
 #pragma unroll
             for (int k = 0; k < (U + NT - 1) / NT; ++k) {
-                const int q = tid + k * NT, I = q % m1 + 1, jl = q / m1 + 1;
-                if (q < U && I < m1 && J0 + jl < m1) body(I, jl);
+                const int q = tid + k * NT, I = q % m1 + 1, jl = q / m1 + JA, J = J0 + jl;
+                if (q < U && I < m1 && J >= 1 && J < m1) body(I, jl);
             }
         };
+        using C0 = std::integral_constant<int, 0>;
+        using C1 = std::integral_constant<int, 1>;
+        using CHR1 = std::integral_constant<int, HR1>;
+        using CHR1p1 = std::integral_constant<int, HR1 + 1>;
+        using CHR1p2 = std::integral_constant<int, HR1 + 2>;
         // interior of a replicated level with M cells
-        auto forl = [&](int M, auto body) {
-            const int U = (M - 1) * (M - 1);
-            for (int q = tid; q < U; q += NT) {
-                const int I = q % (M - 1) + 1, J = q / (M - 1) + 1;
-                body(I, J, J * (M + 1) + I);
+        auto forl = [&](auto mc, auto body) {
+            constexpr int M = decltype(mc)::value, U = (M - 1) * (M - 1);
+#pragma unroll 1
+            for (int k = 0; k < (U + NT - 1) / NT; ++k) {
+                const int q = tid + k * NT, I = q % (M - 1) + 1, J = q / (M - 1) + 1;
+                if (q < U) body(I, J, J * (M + 1) + I);
             }
         };
-        double *T1lo = rank > 0 ? cluster.map_shared_rank(T1, rank - 1) : nullptr;
-        double *T1hi = rank < CS - 1 ? cluster.map_shared_rank(T1, rank + 1) : nullptr;
-        double *Z1lo = rank > 0 ? cluster.map_shared_rank(Z1, rank - 1) : nullptr;
-        double *Z1hi = rank < CS - 1 ? cluster.map_shared_rank(Z1, rank + 1) : nullptr;
-        double *R2 = lv(2, LR);
+        // level-1 operator at (I, jl) (diagonal summed in the order of DI1)
+        auto apply1 = [&](const double *Zs, int I, int jl) -> double {
+            const int e = e1(I, jl), el = e1(I - 1, jl), er = e1(I + 1, jl);
+            const double whe = WH1[e], whl = WH1[el], wve = WV1[e], wvd = WV1[e - P1];
+            return (whe + whl + wve + wvd) * Zs[e] - whe * Zs[er] - whl * Zs[el] - wve * Zs[e + P1] -
+                   wvd * Zs[e - P1];
+        };
 
-        // ---- one V(1,1) cycle: z = M^-1 rin -------------------------------------------------------
-        auto vcycle = [&](const double (&rin)[BR][BC], double (&z)[BR][BC]) {
-            double t[BR][BC];
+        // ---- CG init: x = 0, r = b, z0 = omega D^-1 b -----------------------------------------------
+        double xr[BR][BC], pr[BR][BC], r[BR][BC], s[BR][BC];
+        {
+            double z0[BR][BC];
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) z[q][c] = DI0[fe(c, q)] * rin[q][c];   // z0 = omega D^-1 r
-            publish(G0, G0lo, G0hi, z);
-            cluster_barrier();
-            apply_fine(G0, z, t);
+                for (int c = 0; c < BC; ++c) {
+                    xr[q][c] = pr[q][c] = s[q][c] = 0.0;
+                    const int j = j0 + row0 + q + 1;
+                    r[q][c] = !valid(q, c) ? 0.0 : Bt ? __ldg(Bt + (j - 1) * nx + col0 + c) : (double)j * inv_n3;
+                    z0[q][c] = DI0[fe(c, q)] * r[q][c];
+                }
+            local_publish(G0, z0);
+            send_x1(z0, r);
+        }
+        double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
+        bool conv = false;
+        int it = 0;
+        bool pit = false;                                // probe this CG iteration
+        (void)pit;
+        for (int k = 0;; ++k) {
+            pit = cluster_id_x() == 0 && bl == 0 && k == 6;
+            CL_MARK(pit, 0);
+            // ======== V(1,1) cycle: uu = M^-1 r ========================================================
+            __syncthreads();
+            xwait(0);                                    // X1: z0 halos, r of the row above
+            CL_MARK(pit, 1);
+            {
+                double t[BR][BC], z0[BR][BC];
 #pragma unroll
-            for (int q = 0; q < BR; ++q)
+                for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) t[q][c] = rin[q][c] - t[q][c];       // fine residual
-            publish(G1, G1lo, G1hi, t);
-            cluster_barrier();
-            for1([&](int I, int jl) {                    // R1 = P^T t, Z1 = omega D1^-1 R1
-                const int f = 2 * jl * np, c = I, l = HE + I - 1, r = HE + I;
-                const double rr = G1[f + c] + 0.5 * (G1[f + l] + G1[f + r] + G1[f - np + c] + G1[f + np + c]) +
-                                  0.25 * (G1[f - np + l] + G1[f - np + r] + G1[f + np + l] + G1[f + np + r]);
+                    for (int c = 0; c < BC; ++c) z0[q][c] = valid(q, c) ? G0[fe(c, q)] : 0.0;
+                apply_fine(G0, z0, t);
+#pragma unroll
+                for (int q = 0; q < BR; ++q)
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) t[q][c] = r[q][c] - t[q][c];     // fine residual
+                local_publish(G1, t);
+            }
+            if (tid < nx) {                              // the residual of the row above (HR+1)
+                const int i = tid + 1, e = (HR + 1) * np + slot0(i);
+                const double east = WHh[i], west = WHh[i - 1], north = WVh1[i], south = WVh0[i];
+                double a = (east + west + north + south) * G0[e];
+                a = fma(-east, G0[(HR + 1) * np + slot0(i + 1)], a);
+                a = fma(-west, G0[(HR + 1) * np + slot0(i - 1)], a);
+                a = fma(-north, G0[e + np], a);
+                a = fma(-south, G0[e - np], a);
+                G1[e] = j0 + HR + 1 <= nx ? Rh[i] - a : 0.0;
+            }
+            __syncthreads();
+            CL_MARK(pit, 2);
+            for1(C1{}, CHR1{}, [&](int I, int jl) {      // R1 = P^T t, Z1 = omega D1^-1 R1 (own rows)
+                const int f = 2 * jl * np, c = I, l = HE + I - 1, rr = HE + I;
+                const double rv = G1[f + c] + 0.5 * (G1[f + l] + G1[f + rr] + G1[f - np + c] + G1[f + np + c]) +
+                                  0.25 * (G1[f - np + l] + G1[f - np + rr] + G1[f + np + l] + G1[f + np + rr]);
                 const int e = e1(I, jl);
-                const double zv = DI1[e] * rr;
-                R1[e] = rr;
+                const double zv = DI1[e] * rv;
+                R1[e] = rv;
                 Z1[e] = zv;
-                if (jl == 1 && Z1lo) Z1lo[e1(I, HR1 + 1)] = zv;
-                if (jl == HR1 && Z1hi) Z1hi[e1(I, 0)] = zv;
+                // X2: Z1 rows 1, 2 and R1 row 1 -> rows HR1+1, HR1+2 below; Z1 rows HR1-1, HR1 and R1
+                // row HR1 -> rows -1, 0 above
+                if (jl <= 2 && has_lo) {
+                    st_async(Z1_lo + 8 * e1(I, jl + HR1), zv, mb_lo + 8);
+                    if (jl == 1) st_async(R1_lo + 8 * e1(I, jl + HR1), rv, mb_lo + 8);
+                }
+                if (jl >= HR1 - 1 && has_hi) {
+                    st_async(Z1_hi + 8 * e1(I, jl - HR1), zv, mb_hi + 8);
+                    if (jl == HR1) st_async(R1_hi + 8 * e1(I, jl - HR1), rv, mb_hi + 8);
+                }
             });
-            cluster_barrier();
-            for1([&](int I, int jl) {                    // level-1 residual
-                const double tv = R1[e1(I, jl)] - apply1(Z1, I, jl);
-                T1[e1(I, jl)] = tv;
-                if (jl == 1 && T1lo) T1lo[e1(I, HR1 + 1)] = tv;
+            __syncthreads();
+            xwait(1);                                    // X2
+            CL_MARK(pit, 3);
+            for1(C1{}, CHR1p1{}, [&](int I, int jl) {   // level-1 residual, own rows + the row above
+                T1[e1(I, jl)] = R1[e1(I, jl)] - apply1(Z1, I, jl);
             });
-            cluster_barrier();
-            {   // R2 = P^T T1 on the own level-2 rows, into every CTA's replicated grid
-                constexpr int m2 = L::ml(2), P2 = L::Pl(2), U = (m2 - 1) * HR2;
-                for (int q = tid; q < U; q += NT) {
-                    const int I = q % (m2 - 1) + 1, jl2 = q / (m2 - 1) + 1, J = J20 + jl2;
-                    if (J >= m2) continue;
-                    const int f = 2 * jl2 * P1, c = I, l = H1 + I - 1, r = H1 + I;
-                    const double v = T1[f + c] + 0.5 * (T1[f + l] + T1[f + r] + T1[f - P1 + c] + T1[f + P1 + c]) +
-                                     0.25 * (T1[f - P1 + l] + T1[f - P1 + r] + T1[f + P1 + l] + T1[f + P1 + r]);
+            __syncthreads();
+            CL_MARK(pit, 4);
+            {   // X3: R2 = P^T T1 on the own level-2 rows, to every CTA's replicated grid
+                constexpr int U = (m2 - 1) * HR2;
+                const uint32_t R2a = smem_addr(R2);
 #pragma unroll
-                    for (int k = 0; k < CS; ++k) cluster.map_shared_rank(R2, k)[J * P2 + I] = v;
+                for (int kk = 0; kk < (U + NT - 1) / NT; ++kk) {
+                    const int q = tid + kk * NT, I = q % (m2 - 1) + 1, jl2 = q / (m2 - 1) + 1, J = J20 + jl2;
+                    if (q >= U || J >= m2) continue;
+                    const int f = (2 * jl2 + 1) * P1, c = I, l = H1 + I - 1, rr = H1 + I;
+                    const double v = T1[f + c] + 0.5 * (T1[f + l] + T1[f + rr] + T1[f - P1 + c] + T1[f + P1 + c]) +
+                                     0.25 * (T1[f - P1 + l] + T1[f - P1 + rr] + T1[f + P1 + l] + T1[f + P1 + rr]);
+#pragma unroll
+                    for (int kr = 0; kr < CS; ++kr) st_async(mapa(R2a + 8 * (J * P2 + I), kr), v, mapa(mb0 + 16, kr));
                 }
             }
-            cluster_barrier();
-            // ---- replicated levels 2 .. LK-1, then the K map (CTA-local) ----------------------
+            xwait(2);                                    // X3
+            CL_MARK(pit, 5);
+            // ---- replicated levels 2 .. LK-1, then the K map (CTA-local) --------------------------
 #pragma unroll
             for (int l = 2; l < LK; ++l) {               // down: Z = Dw R, T = R - A Z, restrict
-                const int M = L::ml(l), Pq = L::Pl(l);
+                const int Pq = L::Pl(l);
                 const double *wh = lv(l, LWH), *wv = lv(l, LWV), *di = lv(l, LDI), *rl = lv(l, LR);
                 double *zl = lv(l, LZ), *tl = lv(l, LT);
-                forl(M, [&](int, int, int e) {           // the pre-smoothing from zero in the same pass
+                auto down = [&](int, int, int e) {       // the pre-smoothing from zero in the same pass
                     const double zc = di[e] * rl[e];
                     const double az = (wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) * zc -
                                       wh[e] * (di[e + 1] * rl[e + 1]) - wh[e - 1] * (di[e - 1] * rl[e - 1]) -
                                       wv[e] * (di[e + Pq] * rl[e + Pq]) - wv[e - Pq] * (di[e - Pq] * rl[e - Pq]);
                     zl[e] = zc;
                     tl[e] = rl[e] - az;
-                });
-                __syncthreads();
-                const int Mc = M >> 1;
-                forl(Mc, [&](int I, int J, int ec) {
+                };
+                auto restr = [&](int I, int J, int ec) {
                     const int f = 2 * J * Pq + 2 * I;
                     const double v = tl[f] + 0.5 * (tl[f - 1] + tl[f + 1] + tl[f - Pq] + tl[f + Pq]) +
                                      0.25 * (tl[f - Pq - 1] + tl[f - Pq + 1] + tl[f + Pq - 1] + tl[f + Pq + 1]);
                     if (l + 1 < LK) lv(l + 1, LR)[ec] = v;
                     else RK[(J - 1) * (mK - 1) + I - 1] = v;
-                });
+                };
+                if (l == 2) forl(std::integral_constant<int, L::ml(2)>{}, down);
+                else forl(std::integral_constant<int, L::ml(LK - 1)>{}, down);
+                __syncthreads();
+                if (l == 2) forl(std::integral_constant<int, L::ml(3)>{}, restr);
+                else forl(std::integral_constant<int, L::ml(LK)>{}, restr);
                 __syncthreads();
             }
+            CL_MARK(pit, 6);
             if (warp < (2 * UK + 31) / 32) {             // SK = K RK (levels 8 and 4 cells)
                 const int h = tid & 1, i = min(tid >> 1, UK - 1);
                 const bool own = tid < 2 * UK;
@@ -521,84 +719,93 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 if (own && h == 0) SK[(i / (mK - 1) + 1) * PK + i % (mK - 1) + 1] = sv;
             }
             __syncthreads();
+            CL_MARK(pit, 7);
 #pragma unroll
-            for (int l = LK - 1; l >= 2; --l) {          // up: Z += P S_coarse, S = smooth(Z)
-                const int M = L::ml(l), Pq = L::Pl(l);
+            for (int l = LK - 1; l >= 2; --l) {          // up: S = smooth(Z + P S_coarse), fused
+                const int Pq = L::Pl(l);
                 const double *xc = l + 1 < LK ? lv(l + 1, LT) : SK;
                 const int pc = l + 1 < LK ? L::Pl(l + 1) : PK;
-                const double *wh = lv(l, LWH), *wv = lv(l, LWV), *di = lv(l, LDI), *rl = lv(l, LR);
-                double *zl = lv(l, LZ), *sl = lv(l, LT);
-                forl(M, [&](int I, int J, int e) { zl[e] += prol2w(xc, pc, I, J); });
-                __syncthreads();
-                forl(M, [&](int, int, int e) { sl[e] = fma(di[e], rl[e] - applyl(wh, wv, zl, e, Pq), zl[e]); });
+                const double *wh = lv(l, LWH), *wv = lv(l, LWV), *di = lv(l, LDI), *rl = lv(l, LR), *zl = lv(l, LZ);
+                double *sl = lv(l, LT);
+                auto up = [&](int I, int J, int e) {
+                    const double zc = zl[e] + prol2w(xc, pc, I, J), ze = zl[e + 1] + prol2w(xc, pc, I + 1, J);
+                    const double zw = zl[e - 1] + prol2w(xc, pc, I - 1, J), zn = zl[e + Pq] + prol2w(xc, pc, I, J + 1);
+                    const double zs = zl[e - Pq] + prol2w(xc, pc, I, J - 1);
+                    const double we = wh[e], ww = wh[e - 1], wn = wv[e], ws = wv[e - Pq];
+                    const double az = (we + ww + wn + ws) * zc - we * ze - ww * zw - wn * zn - ws * zs;
+                    sl[e] = fma(di[e], rl[e] - az, zc);
+                };
+                if (l == 2) forl(std::integral_constant<int, L::ml(2)>{}, up);
+                else forl(std::integral_constant<int, L::ml(LK - 1)>{}, up);
                 __syncthreads();
             }
-            {   // level 1: Z1 += P S2 on the own and halo rows, then S1 = smooth(Z1) on the own rows
+            CL_MARK(pit, 8);
+            {   // level 1: S1 = smooth(Z1 + P S2) on the rows 0 .. HR1+1 (own + one halo row each side)
                 const double *S2 = lv(2, LT);
-                constexpr int P2 = L::Pl(2), U = (m1 - 1) * (HR1 + 2);
-                for (int q = tid; q < U; q += NT) {
-                    const int I = q % (m1 - 1) + 1, jl = q / (m1 - 1), J = J0 + jl;
-                    if (J >= 1 && J < m1) Z1[e1(I, jl)] += prol2w(S2, P2, I, J);
-                }
-                __syncthreads();
-                for1([&](int I, int jl) {
-                    const int e = e1(I, jl);
-                    const double sv = fma(DI1[e], R1[e] - apply1(Z1, I, jl), Z1[e]);
-                    S1[e] = sv;
-                    if (jl == 1 && T1lo) T1lo[e1(I, HR1 + 1)] = sv;
-                    if (jl == HR1 && T1hi) T1hi[e1(I, 0)] = sv;
+                for1(C0{}, CHR1p2{}, [&](int I, int jl) {
+                    const int J = J0 + jl, e = e1(I, jl);
+                    const double zc = Z1[e] + prol2w(S2, P2, I, J);
+                    const double ze = Z1[e1(I + 1, jl)] + prol2w(S2, P2, I + 1, J);
+                    const double zw = Z1[e1(I - 1, jl)] + prol2w(S2, P2, I - 1, J);
+                    const double zn = Z1[e + P1] + prol2w(S2, P2, I, J + 1);
+                    const double zs = Z1[e - P1] + prol2w(S2, P2, I, J - 1);
+                    const double whe = WH1[e], whl = WH1[e1(I - 1, jl)], wve = WV1[e], wvd = WV1[e - P1];
+                    const double az = (whe + whl + wve + wvd) * zc - whe * ze - whl * zw - wve * zn - wvd * zs;
+                    S1[e] = fma(DI1[e], R1[e] - az, zc);
                 });
-                cluster_barrier();
+                __syncthreads();
             }
-            // level 0: z = z0 + P S1, post-smoothed (window of S1 as in pcg_mg.cuh)
-            constexpr int XW = BC / 2 + 2, YW = BR / 2 + 2;
-            double cw[YW][XW];
+            CL_MARK(pit, 9);
+            // level 0: uu = z0 + P S1, post-smoothed (window of S1 as in pcg_mg.cuh)
+            double uu[BR][BC];
+            {
+                constexpr int XW = BC / 2 + 2, YW = BR / 2 + 2;
+                double cw[YW][XW];
 #pragma unroll
-            for (int yy = 0; yy < YW; ++yy)
+                for (int yy = 0; yy < YW; ++yy)
 #pragma unroll
-                for (int xx = 0; xx < XW; ++xx) {
-                    const int X = lx + xx, Y = (row0 >> 1) + yy;
-                    cw[yy][xx] = (X <= m1 && J0 + Y <= m1) ? S1[Y * P1 + col1s(X)] : 0.0;
-                }
-            auto pw = [&](int c, int q) -> double {
-                const int fi = 1 + c, fj = 1 + q, x0 = fi >> 1, y0 = fj >> 1;
-                if (!(fi & 1) && !(fj & 1)) return cw[y0][x0];
-                if (!(fj & 1)) return 0.5 * (cw[y0][x0] + cw[y0][x0 + 1]);
-                if (!(fi & 1)) return 0.5 * (cw[y0][x0] + cw[y0 + 1][x0]);
-                return 0.25 * (cw[y0][x0] + cw[y0][x0 + 1] + cw[y0 + 1][x0] + cw[y0 + 1][x0 + 1]);
-            };
+                    for (int xx = 0; xx < XW; ++xx) {
+                        const int X = lx + xx, Y = (row0 >> 1) + yy;
+                        cw[yy][xx] = (X <= m1 && J0 + Y <= m1) ? S1[(Y + 1) * P1 + col1s(X)] : 0.0;
+                    }
+                auto pw = [&](int c, int q) -> double {
+                    const int fi = 1 + c, fj = 1 + q, xq = fi >> 1, yq = fj >> 1;
+                    if (!(fi & 1) && !(fj & 1)) return cw[yq][xq];
+                    if (!(fj & 1)) return 0.5 * (cw[yq][xq] + cw[yq][xq + 1]);
+                    if (!(fi & 1)) return 0.5 * (cw[yq][xq] + cw[yq + 1][xq]);
+                    return 0.25 * (cw[yq][xq] + cw[yq][xq + 1] + cw[yq + 1][xq] + cw[yq + 1][xq + 1]);
+                };
 #pragma unroll
-            for (int q = 0; q < BR; ++q)
+                for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) {
-                    const double ec = pw(c, q);
-                    double a = diag(q, c) * ec;
-                    a = fma(-cE[q][c + 1], pw(c + 1, q), a);
-                    a = fma(-cE[q][c], pw(c - 1, q), a);
-                    a = fma(-cN[q + 1][c], pw(c, q + 1), a);
-                    a = fma(-cN[q][c], pw(c, q - 1), a);
-                    z[q][c] = valid(q, c) ? fma(DI0[fe(c, q)], t[q][c] - a, z[q][c] + ec) : 0.0;
-                }
-        };
-
-        // ---- Chronopoulos-Gear PCG ----------------------------------------------------------------
-        double xr[BR][BC], pr[BR][BC], r[BR][BC], s[BR][BC];
-#pragma unroll
-        for (int q = 0; q < BR; ++q)
-#pragma unroll
-            for (int c = 0; c < BC; ++c) {
-                xr[q][c] = pr[q][c] = s[q][c] = 0.0;
-                const int j = j0 + row0 + q + 1;
-                r[q][c] = !valid(q, c) ? 0.0 : Bt ? __ldg(Bt + (j - 1) * nx + col0 + c) : (double)j * inv_n3;
+                    for (int c = 0; c < BC; ++c) {
+                        const double ec = pw(c, q);
+                        double a = diag(q, c) * ec;
+                        a = fma(-cE[q][c + 1], pw(c + 1, q), a);
+                        a = fma(-cE[q][c], pw(c - 1, q), a);
+                        a = fma(-cN[q + 1][c], pw(c, q + 1), a);
+                        a = fma(-cN[q][c], pw(c, q - 1), a);
+                        // t and z0 of the own nodes are still in G1 / G0
+                        uu[q][c] = valid(q, c) ? fma(DI0[fe(c, q)], G1[fe(c, q)] - a, G0[fe(c, q)] + ec) : 0.0;
+                    }
             }
-        double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
-        bool conv = false;
-        int it = 0;
-        for (int k = 0;; ++k) {
-            double uu[BR][BC], w[BR][BC];
-            vcycle(r, uu);
-            publish(G1, G1lo, G1hi, uu);
-            cluster_barrier();
+            CL_MARK(pit, 10);
+            // ======== w = A uu, dots, cluster reduction ================================================
+            local_publish(G1, uu);
+            if (rg == 0 && has_lo) {                     // X4: row 1 -> row HR+1 below
+#pragma unroll
+                for (int c = 0; c < BC; ++c)
+                    if (col0 + c + 1 <= nx) st_async(G1_lo + 8 * (fe(c, 0) + HR * np), uu[0][c], mb_lo + 24);
+            }
+            if (rg == NRG - 1 && has_hi) {               // row HR -> row 0 above
+#pragma unroll
+                for (int c = 0; c < BC; ++c)
+                    if (col0 + c + 1 <= nx) st_async(G1_hi + 8 * (fe(c, BR - 1) - HR * np), uu[BR - 1][c], mb_hi + 24);
+            }
+            __syncthreads();
+            xwait(3);                                    // X4
+            CL_MARK(pit, 11);
+            double w[BR][BC];
             apply_fine(G1, uu, w);
             double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
@@ -620,20 +827,22 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 wred[2 * NWARP + warp] = acc[2];
             }
             __syncthreads();
-            if (warp == 0 && lane < 3 * CS) {            // CTA sums (warp order) into every CTA's slots
+            const int buf = k & 1;
+            if (warp == 0 && lane < 3 * CS) {            // X5: CTA sums (warp order) to every CTA
                 const int v = lane % 3, dst = lane / 3;
                 double sv = 0.0;
 #pragma unroll
                 for (int ww = 0; ww < NWARP; ++ww) sv += wred[v * NWARP + ww];
-                cluster.map_shared_rank(cred, dst)[rank * 4 + v] = sv;
+                st_async(mapa(smem_addr(cred + (buf * CS + rank) * 4 + v), dst), sv, mapa(mb0 + 32, dst));
             }
-            cluster_barrier();
+            xwait(4);
+            CL_MARK(pit, 12);
             double gs[3];
 #pragma unroll
             for (int v = 0; v < 3; ++v) {
                 double sv = 0.0;
 #pragma unroll
-                for (int rr2 = 0; rr2 < CS; ++rr2) sv += cred[rr2 * 4 + v];
+                for (int rr2 = 0; rr2 < CS; ++rr2) sv += cred[(buf * CS + rr2) * 4 + v];
                 gs[v] = sv;
             }
             const double gamma = gs[0], delta = gs[1];
@@ -655,6 +864,16 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     xr[q][c] = fma(alpha, pn, xr[q][c]);
                     r[q][c] = fma(-alpha, s[q][c], r[q][c]);
                 }
+            {
+                double z0[BR][BC];
+#pragma unroll
+                for (int q = 0; q < BR; ++q)
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) z0[q][c] = DI0[fe(c, q)] * r[q][c];
+                local_publish(G0, z0);
+                send_x1(z0, r);
+            }
+            CL_MARK(pit, 13);
             ++it;
         }
 #pragma unroll
@@ -670,6 +889,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         // the next sample's coefficient table overwrites DI0 .. G1, which only this CTA reads now
         __syncthreads();
     }
+    cluster_barrier();                                   // no CTA leaves while others may address it
 }
 
 }  // namespace usfft
