@@ -17,9 +17,11 @@
  *    staged into ctx-owned device memory before the call returns).  Workspace (tables, per-CTA
  *    scratch) is owned by the ctx and grows on demand.
  *  - Calls are asynchronous on the ctx stream unless marked "syncs" (a host output needs it).
- *  - One ctx per (GPU, stream); not thread-safe.  Multi-GPU: every rank has its own ctx and the
- *    caller performs the exchange steps between calls; the calls take the
- *    node/sample ranges that rank owns.
+ *  - One ctx per (GPU, stream); not thread-safe.  Multi-GPU (one process per GPU):
+ *    every rank creates its ctx with (rank, nranks, id) and calls every collective function
+ *    (marked "collective") in the same order; the library moves the data itself over NCCL
+ *    (a6 usfft_transpose; C2 in usfft_detect_select; C3 in usfft_detect_union).  Samples and
+ *    nodes are partitioned in contiguous balanced ranges (the first n % P ranks get one more).
  *  - Layouts: sample index fastest.  Samples of a round are b = l*M + i (lattice l, node i).
  *    Candidates of a round are j = a*n1 + c for rows a of I_prev and entries c of kt (Z10).
  */
@@ -39,7 +41,7 @@ enum {
     USFFT_EINVAL = 1,     /* bad argument; nothing launched                                  */
     USFFT_ENOMEM = 2,     /* workspace allocation failed                                      */
     USFFT_ECUDA = 3,      /* CUDA error (sticky)                                              */
-    USFFT_ENCCL = 4,      /* reserved for an in-library collective                            */
+    USFFT_ENCCL = 4,      /* NCCL error or NCCL unavailable (sticky)                          */
     USFFT_ENOCONV = 5,    /* some PCG sample missed tol at maxit (outputs still written)      */
     USFFT_ENOTRECON = 6,  /* injectivity test failed (mode-R caller decides what to do)       */
     USFFT_EUNIMPL = 7     /* option not implemented                                           */
@@ -132,10 +134,34 @@ typedef struct {
     double shift[64];    /* x'_1..x'_d                                                        */
 } usfft_plan_out;
 
+/* Sizes of one detection round, for usfft_workspace_query. */
+typedef struct {
+    int32_t n;        /* cells per side of the FE mesh                                         */
+    int32_t d;        /* parameter dimension                                                   */
+    int64_t M;        /* lattice size                                                          */
+    int32_t L;        /* lattices                                                              */
+    int32_t s_tilde;  /* sparsity of the round                                                 */
+    int64_t nJ;       /* candidates                                                            */
+} usfft_round_desc;
+
 /* ---- context ------------------------------------------------------------------------------ */
 
-/* Create a ctx on `device` launching on `stream` (a cudaStream_t; NULL = legacy default). */
-usfft_status usfft_init(usfft_ctx **out, int device, void *stream);
+/* Create a ctx on `device` launching on `stream` (a cudaStream_t; NULL = legacy default) for rank
+ * `rank` of `nranks`.  nranks == 1: no communicator, comm_id may be NULL.
+ * nranks > 1: comm_id = 128 bytes; loopback == 0: an ncclUniqueId from usfft_comm_unique_id on
+ * one rank, broadcast by the caller (e.g. torch.distributed), and the communicator is created
+ * here (ncclCommInitRank, collective over the ranks, one GPU per rank); loopback == 1: nranks
+ * virtual ranks in ONE process on one GPU, each driven by its own host thread with its own ctx
+ * and stream, comm_id any 128 bytes shared by them (the rendezvous key).
+ * Errors: EINVAL (bad rank / device / id), ENCCL (NCCL unavailable or init failed). */
+usfft_status usfft_init(usfft_ctx **out, int device, void *stream, int rank, int nranks,
+                        const void *comm_id, int loopback);
+/* 128-byte ncclUniqueId (NCCL loaded at run time); ENCCL without NCCL. */
+usfft_status usfft_comm_unique_id(void *out);
+usfft_status usfft_comm_info(const usfft_ctx *ctx, int32_t *rank, int32_t *nranks, int32_t *loopback);
+/* Upper bound of the device bytes the calls of a round with these sizes allocate in the ctx
+ * (tables, workspace); caller-owned arrays not included.  No device work. */
+usfft_status usfft_workspace_query(usfft_ctx *ctx, const usfft_round_desc *round, size_t *bytes);
 usfft_status usfft_set_stream(usfft_ctx *ctx, void *stream);
 usfft_status usfft_finalize(usfft_ctx *ctx);
 const char *usfft_last_error(const usfft_ctx *ctx);
@@ -150,6 +176,12 @@ int64_t usfft_launch_count(const usfft_ctx *ctx);
  * I_prev / kt are only read in mode R (dev int16, layouts as in usfft_lattice). */
 usfft_status usfft_plan_round(usfft_ctx *ctx, const usfft_plan_in *in, const int16_t *I_prev,
                               int64_t n_prev, const int16_t *kt, int32_t n1, usfft_plan_out *out);
+
+/* The pole shift of the phi_Delta periodization (theta = 3), one global value per run (Z27):
+ * Delta = 1 / (4 M0), M0 the Step-2 lattice size of the run (Z2 rule for lattice_factor *
+ * s_local and N) -- the Lemma's optimum Delta_opt = 1/(4M) (Remark P:875-879). */
+usfft_status usfft_plan_delta(usfft_ctx *ctx, int32_t N, int32_t s_local, int32_t lattice_factor,
+                              double *delta);
 
 /* ---- a2 + a3: lattice nodes and candidate index maps (usfft_lattice) -----------------------
  * nodes    dev fp64 [d][nb] (may be NULL): component j of sample b0+bl, bl < nb, per the desc.
@@ -170,10 +202,7 @@ usfft_status usfft_lattice(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_
  * P:313; one solve serves all G nodes).  The nodes are generated in-kernel from `lat`
  * (bit-identical to usfft_lattice) unless `nodes` (dev fp64 [d][nb]) is given.
  * Preconditioned CG (pde->precond: Jacobi or multigrid) from x0 = 0, stop on the recursive
- * ||r||_2 <= tol ||b||_2 (Z13).  Environment USFFT_X0=1 (multigrid, n = 16, 32 only): start from
- * the first-order guess of DESIGN Z31 instead, written into u before the solve (same stopping
- * rule; the first such call per (n, d, psi, form, f) builds and caches the basis with 2d + 1
- * solves and one host sync).
+ * ||r||_2 <= tol ||b||_2 (Z13).
  * u        dev fp64 [G][ldu]: u[g*ldu + bl] = u(x_g, y_{b0+bl}), ldu >= nb
  * iters    dev int32 [nb] (may be NULL): PCG iterations per sample
  * relres   dev fp64 [nb] (may be NULL): final recursive ||r||/||b|| (Jacobi path: or an upper bound)
@@ -183,6 +212,16 @@ usfft_status usfft_sample_pde(usfft_ctx *ctx, const usfft_pde_desc *pde,
                               const usfft_lattice_desc *lat, int64_t b0, int64_t nb,
                               const double *nodes, double *u, int64_t ldu, int32_t *iters,
                               double *relres, int32_t *n_noconv);
+
+/* ---- a6: transpose (usfft_transpose, collective) ------------------------------------------
+ * The one exchange step of a round: this rank's samples of all nodes,
+ * u_local dev fp64 [G][nb] (nb = the rank's share of the B samples, ldu == nb), become the
+ * rank's nodes of all samples as P slabs back to back, slabs dev fp64 [G_loc][B] with slab p
+ * = [G_loc][nb_p] at offset G_loc * b0_p (the slab layout usfft_lattice_fft reads, slab_b0 =
+ * the sample partition).  nranks > 1: grouped ncclSend / ncclRecv (loopback: device copies);
+ * nranks == 1: a device copy (none if slabs == u_local).  Pure data movement (bit-exact). */
+usfft_status usfft_transpose(usfft_ctx *ctx, int64_t G, int64_t B, const double *u_local, int64_t ldu,
+                             double *slabs);
 
 /* ---- a7 + a8: lattice FFT and detection key (usfft_lattice_fft) ----------------------------
  * For each owned node g < G_loc and lattice l: the length-M DFT of the samples of lattice l
@@ -200,16 +239,17 @@ usfft_status usfft_lattice_fft(usfft_ctx *ctx, const usfft_lattice_desc *lat, in
                                const int32_t *bins, int64_t nJ, double *spectra,
                                double *kappa_min, double *kappa_max);
 
-/* ---- a9 + a10: threshold and per-node selection (usfft_detect_select) ----------------------
- * theta^2 = fl(theta_abs^2) if theta_abs > 0, else fl(fl(theta_rel^2) * kappa_max[0]) (Z5;
- * kappa_max must be the max over ALL nodes, i.e. all-reduced when nranks > 1).
+/* ---- a9 + a10: threshold and per-node selection (usfft_detect_select, collective) ----------
+ * theta^2 = fl(theta_abs^2) if theta_abs > 0, else fl(fl(theta_rel^2) * kappa_max[0]) (Z5);
+ * with nranks > 1 and the relative threshold (theta_abs <= 0 < theta_rel) the call first
+ * all-reduces kappa_max (MAX, in place: C2) so it is the max over ALL nodes.
  * For each owned g: D_g = the first s_tilde candidates in the order (kappa desc, j asc) (Z6)
  * that satisfy kappa >= theta^2 and kappa > 0 (Alg. 1, Step 2d P:316).
  * votes    dev int32 [nJ]: zeroed, then votes[j] = #{owned g : j in D_g} (Z24)
  * det_g    dev int32 [G_loc][s_tilde]: D_g ascending, -1 padded;  n_det_g dev int32 [G_loc]
  * theta2   dev fp64 [1] (may be NULL): the theta^2 used */
 usfft_status usfft_detect_select(usfft_ctx *ctx, int64_t G_loc, int64_t nJ,
-                                 const double *kappa_min, const double *kappa_max,
+                                 const double *kappa_min, double *kappa_max,
                                  int32_t s_tilde, double theta_rel, double theta_abs,
                                  int32_t *votes, int32_t *det_g, int32_t *n_det_g,
                                  double *theta2);
@@ -253,12 +293,13 @@ usfft_status usfft_detect_carry(usfft_ctx *ctx, int64_t G_loc, int32_t s_tilde, 
                                 const int32_t *det_pos, const int32_t *n_det_g, int64_t j0,
                                 int32_t *det_g, int32_t *votes, double *tau);
 
-/* ---- a11: union (usfft_detect_union) ------------------------------------------------------
- * votes must be summed over all ranks (Step 2e P:318: union over g).  flags |= (votes > 0)
+/* ---- a11: union (usfft_detect_union, collective) -------------------------------------------
+ * With nranks > 1 the call first all-reduces votes (SUM, in place: C3) so they count the nodes
+ * of every rank (Step 2e P:318: union over g).  flags |= (votes > 0)
  * (running union over the rounds i of one t).  Outputs, identical on every rank:
  * det_idx  dev int32 [nJ]: this round's detected j ascending; n_det host int64 (syncs)
  * union_idx dev int32 [nJ] (may be NULL): all j with flags set, ascending; n_union host int64 */
-usfft_status usfft_detect_union(usfft_ctx *ctx, int64_t nJ, const int32_t *votes,
+usfft_status usfft_detect_union(usfft_ctx *ctx, int64_t nJ, int32_t *votes,
                                 uint8_t *flags, int32_t *det_idx, int64_t *n_det,
                                 int32_t *union_idx, int64_t *n_union);
 

@@ -17,8 +17,9 @@ Readings:
       Exact zeros are never detected (kappa > 0, as with the paper's theta > 0).
   Z6  top-s~ order: kappa desc, candidate index asc.     Z7  fewer than s~ pass: keep all.
   Z24 "aggregated over all mesh nodes": votes_k = sum_g [k in D_g]; I_round = {votes >= 1}.
-  Z25 fragile decisions: a key within 1e-10 max m (m = sqrt(kappa_min)) of a different key on
-      the other side of the node's s~-cut, or of theta (two-sided; bit-equal keys never).
+  Z25 fragile decisions: a key >= theta - eps within eps = 1e-10 max m (m = sqrt(kappa_min)) of a
+      different key on the other side of the node's s~-cut, or an in-cut key within eps of theta
+      (two-sided; bit-equal keys and swaps below theta never).
 """
 from __future__ import annotations
 
@@ -100,11 +101,12 @@ def fragile(kmin: np.ndarray, s_tilde: int, theta2: float, band: float = 1e-10) 
     With m = sqrt(kappa_min), eps = band * max m and node g's candidates in the selection order
     (m desc, index asc; Z6), the first s~ of that order are "in", the rest "out".
     (k, g) is fragile when
-      * an "in" k has an "out" k' with m' != m and m' >= m - eps (the two could swap), or an
-        "out" k has an "in" k' with m' != m and m' <= m + eps;
+      * m >= theta - eps and an "in" k has an "out" k' with m' != m and m' >= m - eps (the two
+        could swap), or an "out" k has an "in" k' with m' != m and m' <= m + eps;
       * or k is "in" and |m - theta| <= eps (the threshold decision, Z5).
-    Bit-equal keys (e.g. two candidates in one bin of the minimising lattice) are ordered by
-    index on both sides, so they never make a decision fragile."""
+    A swap of two keys below theta - eps changes no D_g (neither is detected either way), and
+    bit-equal keys (e.g. two candidates in one bin of the minimising lattice) are ordered by
+    index on both sides, so neither makes a decision fragile."""
     m = np.sqrt(kmin)
     G, nJ = kmin.shape
     eps = band * (m.max() if m.size else 0.0)
@@ -113,20 +115,24 @@ def fragile(kmin: np.ndarray, s_tilde: int, theta2: float, band: float = 1e-10) 
     idx = np.arange(nJ)
     out = np.zeros_like(kmin, dtype=bool)
     for g in range(G):
-        order = np.lexsort((idx, -m[g]))
+        # order and equality on the key kappa itself (two keys 1 ulp apart can share one sqrt);
+        # distances on m
+        order = np.lexsort((idx, -kmin[g]))
+        kv = kmin[g][order]
         mv = m[g][order]
-        sel, rest = mv[:s], mv[s:]
+        ksel, krest, msel, mrest = kv[:s], kv[s:], mv[:s], mv[s:]
         fr = np.zeros(nJ, dtype=bool)
-        if rest.size and sel.size:
-            # in: the largest out-value strictly below m (rest is descending)
-            pos = np.searchsorted(-rest, -sel, side="right")
-            below = np.where(pos < rest.size, rest[np.minimum(pos, rest.size - 1)], -np.inf)
-            fr[:s] = below >= sel - eps
-            # out: the smallest in-value strictly above m (sel is descending)
-            q = np.searchsorted(-sel, -rest, side="left") - 1
-            above = np.where(q >= 0, sel[np.maximum(q, 0)], np.inf)
-            fr[s:] = above <= rest + eps
-        fr[:s] |= np.abs(sel - theta) <= eps
+        if krest.size and ksel.size:
+            # in: the largest out-key strictly below (rest is descending)
+            pos = np.searchsorted(-krest, -ksel, side="right")
+            below = np.where(pos < krest.size, mrest[np.minimum(pos, krest.size - 1)], -np.inf)
+            fr[:s] = below >= msel - eps
+            # out: the smallest in-key strictly above (sel is descending)
+            q = np.searchsorted(-ksel, -krest, side="left") - 1
+            above = np.where(q >= 0, msel[np.maximum(q, 0)], np.inf)
+            fr[s:] = above <= mrest + eps
+        fr &= mv >= theta - eps
+        fr[:s] |= np.abs(msel - theta) <= eps
         out[g, order] = fr
     return out
 

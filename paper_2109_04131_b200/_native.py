@@ -38,13 +38,22 @@ class PlanOut(C.Structure):
                 ("z", i64 * 2048), ("shift", f64 * 64)]
 
 
+class RoundDesc(C.Structure):
+    _fields_ = [("n", i32), ("d", i32), ("M", i64), ("L", i32), ("s_tilde", i32), ("nJ", i64)]
+
+
 class CoverDesc(C.Structure):
     _fields_ = [("nlat", i32), ("d", i32), ("M", i64), ("z", i64 * 4096)]
 
 
 # name -> (restype, argtypes)
 _SIGS = {
-    "usfft_init": (i32, [C.POINTER(vp), C.c_int, vp]),
+    "usfft_init": (i32, [C.POINTER(vp), C.c_int, vp, C.c_int, C.c_int, vp, C.c_int]),
+    "usfft_comm_unique_id": (i32, [vp]),
+    "usfft_comm_info": (i32, [vp, C.POINTER(i32), C.POINTER(i32), C.POINTER(i32)]),
+    "usfft_workspace_query": (i32, [vp, C.POINTER(RoundDesc), C.POINTER(C.c_size_t)]),
+    "usfft_plan_delta": (i32, [vp, i32, i32, i32, C.POINTER(f64)]),
+    "usfft_transpose": (i32, [vp, i64, i64, vp, i64, vp]),
     "usfft_set_stream": (i32, [vp, vp]),
     "usfft_finalize": (i32, [vp]),
     "usfft_last_error": (C.c_char_p, [vp]),

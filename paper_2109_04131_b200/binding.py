@@ -39,19 +39,36 @@ def _p(t, dtype=None):
     return t.data_ptr()
 
 
-class Context:
-    """usfft_ctx on one device, launching on a torch stream (default: the current stream)."""
+def usfft_comm_unique_id() -> bytes:
+    """A fresh 128-byte ncclUniqueId (to be broadcast to every rank by the caller)."""
+    lib = N.load()
+    buf = (C.c_char * 128)()
+    st = lib.usfft_comm_unique_id(buf)
+    if st != N.OK:
+        raise UsfftError(st, "usfft_comm_unique_id", "NCCL unavailable")
+    return bytes(buf)
 
-    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None):
+
+class Context:
+    """usfft_ctx on one device, launching on a torch stream (default: the current stream), for
+    rank `rank` of `nranks` (comm_id: the 128-byte id every rank shares; loopback: virtual ranks
+    of one process on one GPU, one host thread each)."""
+
+    def __init__(self, device: int = 0, stream: torch.cuda.Stream | None = None, rank: int = 0,
+                 nranks: int = 1, comm_id: bytes | None = None, loopback: bool = False):
         self.lib = N.load()
         if not torch.cuda.is_available():
             raise RuntimeError("usFFT needs a CUDA device; there is no CPU path")
         self.device = device
         self.stream = stream if stream is not None else torch.cuda.current_stream(device)
+        self.rank, self.nranks = rank, nranks
+        self._id = C.create_string_buffer(comm_id, 128) if comm_id is not None else None
         h = C.c_void_p()
-        st = self.lib.usfft_init(C.byref(h), device, C.c_void_p(self.stream.cuda_stream))
+        st = self.lib.usfft_init(C.byref(h), device, C.c_void_p(self.stream.cuda_stream), rank, nranks,
+                                 C.cast(self._id, C.c_void_p) if self._id is not None else None,
+                                 1 if loopback else 0)
         if st != N.OK:
-            raise UsfftError(st, "usfft_init", "device/context creation failed")
+            raise UsfftError(st, "usfft_init", "device/context/communicator creation failed")
         self.h = h
 
     def last_error(self) -> str:
@@ -171,6 +188,27 @@ def usfft_sample_pde(ctx: Context, pde, plan: Plan, b0: int, nb: int, u, ldu: in
                                   C.byref(nc) if check_conv else None)
     _check(ctx, st, "usfft_sample_pde", allow=(N.ENOCONV,))
     return int(nc.value) if check_conv else -1
+
+
+def usfft_transpose(ctx: Context, G: int, B_: int, u_local, slabs):
+    """a6 (collective): this rank's samples u_local [G][nb] -> slabs [G_loc * B] of its nodes."""
+    nb = int(u_local.shape[1]) if u_local.dim() == 2 else int(u_local.numel() // max(G, 1))
+    st = ctx.lib.usfft_transpose(ctx.h, G, B_, _p(u_local, torch.float64), nb, _p(slabs, torch.float64))
+    _check(ctx, st, "usfft_transpose")
+
+
+def usfft_plan_delta(ctx: Context, N_: int, s_local: int, lattice_factor: int = 1) -> float:
+    """The global pole shift Delta = 1/(4 M0) of the phi_Delta periodization (Z27)."""
+    out = C.c_double(0.0)
+    _check(ctx, ctx.lib.usfft_plan_delta(ctx.h, N_, s_local, lattice_factor, C.byref(out)), "usfft_plan_delta")
+    return float(out.value)
+
+
+def usfft_workspace_query(ctx: Context, n: int, d: int, M: int, L: int, s_tilde: int, nJ: int) -> int:
+    rd = N.RoundDesc(n, d, M, L, s_tilde, nJ)
+    out = C.c_size_t(0)
+    _check(ctx, ctx.lib.usfft_workspace_query(ctx.h, C.byref(rd), C.byref(out)), "usfft_workspace_query")
+    return int(out.value)
 
 
 def usfft_lattice_fft(ctx: Context, plan: Plan, G_loc: int, u, slab_b0, bins, nJ: int, spectra,

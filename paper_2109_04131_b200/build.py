@@ -10,8 +10,21 @@ HERE = os.path.dirname(os.path.abspath(__file__))
 SRC = os.path.join(HERE, "csrc")
 OUT = os.path.join(HERE, "libusfft.so")
 NVCC = os.environ.get("NVCC", "/usr/local/cuda/bin/nvcc")
+def nccl_include() -> str:
+    """Header of the NCCL torch loads (the library dlopens libnccl.so.2 at run time)."""
+    try:
+        import nvidia.nccl
+        for p in nvidia.nccl.__path__:
+            inc = os.path.join(p, "include")
+            if os.path.exists(os.path.join(inc, "nccl.h")):
+                return inc
+    except ImportError:
+        pass
+    return "/usr/include"
+
+
 FLAGS = ["-gencode", "arch=compute_100a,code=sm_100a", "-lineinfo", "-O3", "-std=c++17",
-         "-Xcompiler", "-fPIC", "-shared"]
+         "-Xcompiler", "-fPIC", "-shared", "-I" + nccl_include(), "-ldl"]
 
 
 def sources() -> list[str]:

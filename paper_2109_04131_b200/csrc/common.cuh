@@ -28,8 +28,11 @@ struct RaderPlan {
 };
 }  // namespace usfft
 
+struct usfft_comm;                                           // comm.cu: NCCL communicator / loopback hub
+
 struct usfft_ctx {
     int device = 0;
+    usfft_comm *comm = nullptr;                              // nranks > 1 only
     cudaStream_t stream = nullptr;
     int sm_count = 148;
     size_t smem_optin = 0;
@@ -177,6 +180,15 @@ inline usfft_status kernel_fit(usfft_ctx *c, K kern, int threads, size_t smem, i
     }
     return USFFT_OK;
 }
+
+// the in-library collectives (comm.cu); every rank calls them in the same order
+usfft_status comm_create(usfft_ctx *c, int rank, int nranks, const void *id, int loopback);
+void comm_destroy(usfft_ctx *c);
+int comm_size(const usfft_ctx *c);
+usfft_status comm_alltoallv(usfft_ctx *c, const double *send, const int64_t *scount, const int64_t *sdispl,
+                            double *recv, const int64_t *rcount, const int64_t *rdispl);
+usfft_status comm_max_f64(usfft_ctx *c, double *buf, int64_t count);
+usfft_status comm_sum_i32(usfft_ctx *c, int32_t *buf, int64_t count);
 
 inline unsigned grid1d(int64_t n, int block) {
     int64_t g = (n + block - 1) / block;

@@ -377,7 +377,7 @@ k_resolve(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64
 using namespace usfft;
 
 extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t nJ,
-                                            const double *kappa_min, const double *kappa_max,
+                                            const double *kappa_min, double *kappa_max,
                                             int32_t s_tilde, double theta_rel, double theta_abs,
                                             int32_t *votes, int32_t *det_g, int32_t *n_det_g,
                                             double *theta2) {
@@ -387,6 +387,11 @@ extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t
     USFFT_REQUIRE(c, theta_rel >= 0.0 && theta_abs >= 0.0, "negative theta");
     USFFT_REQUIRE(c, nJ == 0 || votes != nullptr, "votes NULL");
     USFFT_REQUIRE(c, G_loc == 0 || nJ == 0 || (kappa_min && kappa_max && det_g && n_det_g), "NULL pointer");
+    // C2: the relative threshold needs the max over ALL nodes (Z5): all-reduce MAX in place
+    if (comm_size(c) > 1 && theta_abs <= 0.0 && theta_rel > 0.0) {
+        USFFT_REQUIRE(c, kappa_max != nullptr, "kappa_max NULL");
+        if (usfft_status s = comm_max_f64(c, kappa_max, 1)) return s;
+    }
     if (nJ > 0) USFFT_CUDA(c, cudaMemsetAsync(votes, 0, sizeof(int32_t) * nJ, c->stream));
     if (G_loc == 0 || nJ == 0) {
         if (G_loc > 0 && n_det_g) USFFT_CUDA(c, cudaMemsetAsync(n_det_g, 0, sizeof(int32_t) * G_loc, c->stream));
@@ -432,7 +437,7 @@ extern "C" usfft_status usfft_detect_carry(usfft_ctx *c, int64_t G_loc, int32_t 
     return USFFT_OK;
 }
 
-extern "C" usfft_status usfft_detect_union(usfft_ctx *c, int64_t nJ, const int32_t *votes,
+extern "C" usfft_status usfft_detect_union(usfft_ctx *c, int64_t nJ, int32_t *votes,
                                            uint8_t *flags, int32_t *det_idx, int64_t *n_det,
                                            int32_t *union_idx, int64_t *n_union) {
     USFFT_ENTER(c);
@@ -440,6 +445,9 @@ extern "C" usfft_status usfft_detect_union(usfft_ctx *c, int64_t nJ, const int32
     USFFT_REQUIRE(c, nJ == 0 || (votes && flags && det_idx), "NULL pointer");
     USFFT_REQUIRE(c, n_det != nullptr, "n_det NULL");
     long long *counts = reinterpret_cast<long long *>(static_cast<char *>(c->dscal) + 64);
+    // C3: union over the nodes of every rank (Step 2e P:318): all-reduce SUM of the votes
+    if (comm_size(c) > 1 && nJ > 0)
+        if (usfft_status s = comm_sum_i32(c, votes, nJ)) return s;
     if (nJ == 0) {
         *n_det = 0;
         if (n_union) *n_union = 0;

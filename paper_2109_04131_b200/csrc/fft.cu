@@ -202,6 +202,22 @@ usfft_status launch_rader_t(usfft_ctx *c, const double *u, const SlabParams &S, 
     return USFFT_OK;
 }
 
+template <int N, int WPR, int RPC>
+usfft_status launch_rader_tp(usfft_ctx *c, const double *u, const SlabParams &S, int64_t G_loc,
+                             int32_t L, const RaderArgs &A, double2 *F) {
+    const int64_t rows = G_loc * L, pairs = G_loc * ((L + 1) / 2);
+    const size_t smem = sizeof(double2) * 2 * (size_t)(N + 2) * RPC;
+    auto kern = k_fft_rader_tp<N, WPR, RPC>;
+    int per_sm = 0;
+    if (usfft_status s = kernel_fit(c, kern, WPR * 32 * RPC, smem, &per_sm)) return s;
+    int64_t grid = (pairs + RPC - 1) / RPC;
+    const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
+    if (grid > resident) grid = resident;                 // persistent: each group loops over pairs
+    kern<<<(unsigned)grid, WPR * 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
 usfft_status launch_fft400(usfft_ctx *c, const double *u, const SlabParams &S, int64_t G_loc,
                            int32_t L, const RaderArgs &A, double2 *F, bool paired) {
     constexpr int RPC = 4;
@@ -409,9 +425,9 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         // the lattice sizes of the BASELINE configs (Z2) have compile-time plans; other
         // Rader-able M take the runtime-plan kernel
         if (R.N == 96) s = launch_rader_t<96, 1, 4>(c, u, S, G_loc, L, A, Fo);
-        else if (R.N == 400) s = launch_fft400(c, u, S, G_loc, L, A, Fo, false);
-        else if (R.N == 2016) s = launch_rader_t<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
-        else if (R.N == 4000) s = launch_rader_t<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
+        else if (R.N == 400) s = launch_fft400(c, u, S, G_loc, L, A, Fo, true);
+        else if (R.N == 2016) s = launch_rader_tp<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
+        else if (R.N == 4000) s = launch_rader_tp<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
         else {
             if (usfft_status s2 = kernel_fit(c, k_fft_rader, 0, smem_r, nullptr)) return s2;
             const int threads = M <= 512 ? 128 : 256;

@@ -157,17 +157,14 @@ k_fft400(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_
     }
 }
 
-// Option (USFFT_DFT=paired; measured no faster than one row per warp: the kernel is latency-
-// bound with 8 warps per SM, not fp64-throughput-bound).
 // Two real rows per complex transform: z = a0 + i a1, the Rader sequences of the lattices
 // 2j and 2j+1 of one node g (pairs never straddle nodes, so a row's result does not depend on
 // how the nodes are split across ranks or launches; an odd L leaves its last lattice paired
-// with a zero row).
-// FFT(z) = Z gives A0 = (Z + conj Z~) / 2 and A1 = (Z - conj Z~) / 2i with Z~[k] = Z[N - k] (a
-// shuffle from lane (20 - k1) mod 20); the products P_j = conj(A_j . FFT(b)/N) are packed as
-// P0 + i P1 for the second transform D, whose halves separate because each row's output
-// satisfies c[q + N/2] = conj(c[q]) (real input: X[M - m] = conj X[m] and g^{N/2} = -1 mod M):
-// c0 = (D[q] + conj D[q+200]) / 2, c1 = (D[q] - conj D[q+200]) / 2i, both lane-local.
+// with a zero row).  By linearity FFT(z) . FFT(b)/N = C0 + i C1 (C_j = FFT(a_j) . FFT(b)/N), so
+// the spectra need no separation; the second transform of conj(C0 + i C1) gives
+// D = conj(conv0) - i conj(conv1), whose halves separate because each row's convolution
+// satisfies conv[q + N/2] = conj(conv[q]) (k_fft_rader_tp in rader_t.cuh):
+// conj(conv0[q]) = (D[q] + conj D[q+200]) / 2, conj(conv1[q]) = (conj D[q+200] - D[q]) / 2i.
 template <int RPC>
 __global__ void __launch_bounds__(32 * RPC)
 k_fft400p(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_t L,
@@ -246,35 +243,27 @@ k_fft400p(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32
             }
         }
         fft400_core(v, a, T, A.tw, lane);                 // Z: lane k1, register k2
-        const int src = lane == 0 ? 0 : (lane < 20 ? 20 - lane : lane);
-#pragma unroll
-        for (int k2 = 0; k2 < 20; ++k2) {                 // separate, multiply, pack
-            const double2 zs = a[19 - k2];
-            double2 zm = make_double2(__shfl_sync(0xffffffffu, zs.x, src), __shfl_sync(0xffffffffu, zs.y, src));
-            if (lane == 0) zm = a[(20 - k2) % 20];
-            const double2 z = a[k2];
-            const double2 A0 = make_double2(0.5 * (z.x + zm.x), 0.5 * (z.y - zm.y));
-            const double2 A1 = make_double2(0.5 * (z.y + zm.y), -0.5 * (z.x - zm.x));
-            const double2 bf = __ldg(A.bf + (lane < 20 ? lane : 0) + 20 * k2);
-            const double2 c0 = cmul(A0, bf), c1 = cmul(A1, bf);
-            // P0 + i P1 with P_j = conj(c_j)
-            v[k2] = make_double2(c0.x + c1.y, -c0.y + c1.x);
-        }
-        fft400_core(v, a, T, A.tw, lane);                 // D = c0 + i c1 per (lane, register)
         if (lane < 20) {
 #pragma unroll
-            for (int k2 = 0; k2 < 10; ++k2) {
+            for (int k2 = 0; k2 < 20; ++k2) {             // conj(Z . FFT(b)/N)
+                const double2 c = cmul(a[k2], __ldg(A.bf + lane + 20 * k2));
+                v[k2] = make_double2(c.x, -c.y);
+            }
+        }
+        fft400_core(v, a, T, A.tw, lane);                 // D = conj(conv0) - i conj(conv1)
+        if (lane < 20) {
+#pragma unroll
+            for (int k2 = 0; k2 < 10; ++k2) {             // q = lane + 20 k2 < 200, q + 200 in register k2 + 10
                 const double2 dq = a[k2], dh = a[k2 + 10];
-                // c0 = (D[q] + conj D[q+200]) / 2,  c1 = (D[q] - conj D[q+200]) / 2i
-                const double2 c0 = make_double2(0.5 * (dq.x + dh.x), 0.5 * (dq.y - dh.y));
-                const double2 c1 = make_double2(0.5 * (dq.y + dh.y), -0.5 * (dq.x - dh.x));
-                const int m = __ldg(A.outidx + lane + 20 * k2);   // X[g^-q] = x0 + conj c[q]
-                if (m < MH) {
-                    T[m] = make_double2(x00 + c0.x, -c0.y);
-                    T[MH + m] = make_double2(x01 + c1.x, -c1.y);
+                const double2 s = make_double2(0.5 * (dq.x + dh.x), 0.5 * (dq.y - dh.y));      // conj(conv0)
+                const double2 tt = make_double2(0.5 * (dh.x - dq.x), 0.5 * (-dh.y - dq.y));    // conj(conv1) = -i tt
+                const int m = __ldg(A.outidx + lane + 20 * k2);
+                if (m < MH) {                             // X[g^-q] = x0 + conv[q]
+                    T[m] = make_double2(x00 + s.x, -s.y);
+                    T[MH + m] = make_double2(x01 + tt.y, tt.x);
                 } else {                                  // q + 200 maps to M - m <= M/2
-                    T[M - m] = make_double2(x00 + c0.x, c0.y);
-                    T[MH + M - m] = make_double2(x01 + c1.x, c1.y);
+                    T[M - m] = make_double2(x00 + s.x, s.y);
+                    T[MH + M - m] = make_double2(x01 + tt.y, -tt.x);
                 }
             }
         }

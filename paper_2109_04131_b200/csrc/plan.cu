@@ -183,3 +183,16 @@ extern "C" usfft_status usfft_cover_plan(usfft_ctx *c, int64_t seed, int32_t d, 
     return USFFT_OK;
 }
 
+
+// Z27: the global pole shift of the phi_Delta periodization, Delta = 1 / (4 M0) with M0 the
+// Step-2 lattice size of the run (Lemma P:847-870, "Delta_opt = 1/(4M)"; every Step-2 round
+// shares M0 = the Z2 lattice size for s_local).
+extern "C" usfft_status usfft_plan_delta(usfft_ctx *c, int32_t N, int32_t s_local, int32_t lattice_factor,
+                                         double *delta) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, N >= 0 && s_local >= 1 && lattice_factor >= 1 && delta, "bad arguments");
+    const int64_t K = 2 * (int64_t)N + 1;
+    const int64_t M0 = lattice_prime(std::max<int64_t>(4 * (int64_t)s_local * lattice_factor, K + 1));
+    *delta = 1.0 / (4.0 * (double)M0);
+    return USFFT_OK;
+}

@@ -157,3 +157,140 @@ k_fft_rader_t(const double *__restrict__ u, const SlabParams S, int64_t G_loc, i
 }
 
 }  // namespace usfft
+
+namespace usfft {
+
+// Two real rows per complex transform (lattices 2j and 2j+1 of one node g; an odd L pairs its
+// last lattice with a zero row, so a row's result never depends on how nodes are split).
+// With z = a0 + i a1 (the two Rader sequences) and C_j = FFT(a_j) . FFT(b)/N, linearity gives
+// FFT(z) . FFT(b)/N = C0 + i C1 without separating the two spectra, and the second transform of
+// P = conj(C0 + i C1) is D = conj(conv0) - i conj(conv1).  Each row's convolution satisfies
+// conv[q + N/2] = conj(conv[q]) (real input: X[M - m] = conj X[m], g^{N/2} = -1 mod M), so
+//   conj(conv0[q]) = (D[q] + conj D[q + N/2]) / 2,   conj(conv1[q]) = (conj D[q + N/2] - D[q]) / 2i,
+// and q < N/2 covers every pair {m, M - m} once: X_j[m] = x0_j + conv_j[q] for m = g^-q <= M/2,
+// else X_j[M - m] = conj(x0_j + conv_j[q]).  Half the transforms of k_fft_rader_t per row.
+template <int N, int WPR, int RPC>
+__global__ void __launch_bounds__(WPR * 32 * RPC)
+k_fft_rader_tp(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_t L,
+               const RaderArgs A, double2 *__restrict__ F, int64_t rows) {
+    constexpr int GROUP = WPR * 32;
+    constexpr int M = N + 1, MH = M / 2 + 1, NB = N + 2;  // buffer: N values (+2: staging room)
+    constexpr int PER = (M + GROUP - 1) / GROUP;
+    extern __shared__ double2 smt[];
+    __shared__ double wsum[2][32];
+    const int gid = threadIdx.x / GROUP, t = threadIdx.x % GROUP;
+    double2 *b0 = smt + (size_t)gid * 2 * NB;
+    double2 *b1 = b0 + NB;
+    double *xs0 = reinterpret_cast<double *>(b1), *xs1 = xs0 + M;   // both real rows in b1 (2M <= 2 NB)
+    const bool one_slab = S.nslab == 1;
+    const int64_t LP = (L + 1) / 2, pairs = (rows / L) * LP;         // rows = G_loc * L
+    const int64_t stride = (int64_t)gridDim.x * RPC;
+    int64_t pr = (int64_t)blockIdx.x * RPC + gid;
+    double xv0[PER], xv1[PER];
+    auto fetch = [&](int64_t rw, double (&xv)[PER]) {
+        if (rw < 0) {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) xv[k] = 0.0;
+            return;
+        }
+        const int64_t g = rw / L, l = rw - g * L;
+        if (one_slab) {
+            const double *src = u + g * (int64_t)L * M + l * M;
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int i = t + k * GROUP;
+                xv[k] = i < M ? __ldg(src + i) : 0.0;
+            }
+        } else {
+#pragma unroll
+            for (int k = 0; k < PER; ++k) {
+                const int i = t + k * GROUP;
+                xv[k] = i < M ? sample_at(u, S, G_loc, g, l * M + i) : 0.0;
+            }
+        }
+    };
+    auto row0 = [&](int64_t q) { return (q / LP) * L + 2 * (q % LP); };
+    auto row1 = [&](int64_t q) { return 2 * (q % LP) + 1 < L ? row0(q) + 1 : int64_t(-1); };
+    if (pr < pairs) {
+        fetch(row0(pr), xv0);
+        fetch(row1(pr), xv1);
+    }
+    for (; pr < pairs; pr += stride) {
+        const int64_t r0 = row0(pr), r1 = row1(pr);
+        double p0 = 0.0, p1 = 0.0;
+#pragma unroll
+        for (int k = 0; k < PER; ++k) {
+            const int i = t + k * GROUP;
+            if (i < M) {
+                xs0[i] = xv0[k];
+                xs1[i] = xv1[k];
+            }
+            p0 += xv0[k];
+            p1 += xv1[k];
+        }
+        if (pr + stride < pairs) {                          // overlaps the transforms below
+            fetch(row0(pr + stride), xv0);
+            fetch(row1(pr + stride), xv1);
+        }
+        // X[0] of both rows: fixed tree over the group (shuffles, then warp partials in order)
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1) {
+            p0 += __shfl_xor_sync(0xffffffffu, p0, o);
+            p1 += __shfl_xor_sync(0xffffffffu, p1, o);
+        }
+        if (WPR > 1 && (t & 31) == 0) {
+            wsum[0][gid * WPR + (t >> 5)] = p0;
+            wsum[1][gid * WPR + (t >> 5)] = p1;
+        }
+        group_sync<GROUP>(gid);
+        if (WPR > 1) {
+            double s0 = 0.0, s1 = 0.0;
+#pragma unroll
+            for (int w = 0; w < WPR; ++w) {
+                s0 += wsum[0][gid * WPR + w];
+                s1 += wsum[1][gid * WPR + w];
+            }
+            p0 = s0;
+            p1 = s1;
+        }
+        const double x00 = xs0[0], x01 = xs1[0];
+        for (int p = t; p < N; p += GROUP) {
+            const int pi = __ldg(A.perm + p);
+            b0[p] = make_double2(xs0[pi], xs1[pi]);
+        }
+        group_sync<GROUP>(gid);
+        double2 *Z = fft_t<N, 0, GROUP>(b0, b1, A.tw, t, gid);
+        double2 *other = Z == b0 ? b1 : b0;
+        for (int k = t; k < N; k += GROUP) {                // P = conj(Z . FFT(b)/N)
+            const double2 c = cmul(Z[k], __ldg(A.bf + k));
+            Z[k] = make_double2(c.x, -c.y);
+        }
+        group_sync<GROUP>(gid);
+        double2 *D = fft_t<N, 0, GROUP>(Z, other, A.tw, t, gid);
+        double2 *st = D == b0 ? b1 : b0;                    // staging: row 0 at [0, MH), row 1 at [MH, 2 MH)
+        for (int q = t; q < N / 2; q += GROUP) {
+            const double2 dq = D[q], dh = D[q + N / 2];
+            const double2 s = make_double2(0.5 * (dq.x + dh.x), 0.5 * (dq.y - dh.y));        // conj(conv0)
+            const double2 tt = make_double2(0.5 * (dh.x - dq.x), 0.5 * (-dh.y - dq.y));      // 2i conj(conv1) / 2
+            const int32_t m = __ldg(A.outidx + q);
+            // conv0 = (s.x, -s.y); conv1 = (tt.y, tt.x)
+            if (m < MH) {
+                st[m] = make_double2(x00 + s.x, -s.y);
+                st[MH + m] = make_double2(x01 + tt.y, tt.x);
+            } else {
+                st[M - m] = make_double2(x00 + s.x, s.y);
+                st[MH + M - m] = make_double2(x01 + tt.y, -tt.x);
+            }
+        }
+        group_sync<GROUP>(gid);
+        double2 *d0 = F + r0 * MH;
+        for (int m = t; m < MH; m += GROUP) d0[m] = m == 0 ? make_double2(p0, 0.0) : st[m];
+        if (r1 >= 0) {
+            double2 *d1 = F + r1 * MH;
+            for (int m = t; m < MH; m += GROUP) d1[m] = m == 0 ? make_double2(p1, 0.0) : st[MH + m];
+        }
+        group_sync<GROUP>(gid);                             // buffers are reused by the next pair
+    }
+}
+
+}  // namespace usfft

@@ -8,8 +8,13 @@ exchange steps are
   * an all-reduce MAX of the 8-byte kappa_max (threshold basis, Z5);
   * an all-reduce SUM of the int32 votes (union over all nodes, Alg. 1 Step 2e P:318).
 All three are pure data movement or order-free (MAX, integer SUM), so the results are
-bit-identical for every P.  torch.distributed provides the collectives (NCCL on GPUs; gloo in
-the CPU tests of this module's index math).
+bit-identical for every P.
+
+The product runs them inside libusfft (usfft_transpose, usfft_detect_select,
+usfft_detect_union over the library's own NCCL communicator): this module only bootstraps the
+communicator id over torch.distributed (bootstrap_id).  TorchExchange performs the same three
+steps with torch.distributed for process groups the library cannot use (gloo: ranks sharing one
+GPU in the multi-process tests, CPU-only index-math tests).
 """
 from __future__ import annotations
 
@@ -29,8 +34,22 @@ def bounds(n: int, P: int) -> list[int]:
     return [partition(n, P, p)[0] for p in range(P)] + [n]
 
 
-class Exchange:
-    """The collectives of a round for world size P (P = 1: no-ops)."""
+def bootstrap_id(group=None) -> bytes:
+    """The 128-byte ncclUniqueId of the library's communicator: made on rank 0 by libusfft and
+    broadcast over the (initialised) torch.distributed process group."""
+    from . import binding
+    rank = dist.get_rank(group)
+    dev = torch.device("cuda", torch.cuda.current_device()) if dist.get_backend(group) == "nccl" else "cpu"
+    buf = torch.zeros(128, dtype=torch.uint8, device=dev)
+    if rank == 0:
+        buf.copy_(torch.frombuffer(bytearray(binding.usfft_comm_unique_id()), dtype=torch.uint8))
+    dist.broadcast(buf, src=0, group=group)
+    return bytes(buf.cpu().numpy().tobytes())
+
+
+class TorchExchange:
+    """The collectives of a round through torch.distributed, for world size P (P = 1: no-ops).
+    Only for process groups the library's communicator cannot serve (gloo)."""
 
     def __init__(self, group=None):
         self.group = group

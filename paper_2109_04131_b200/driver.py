@@ -1,14 +1,15 @@
 """Alg. 1 "The usFFT on a set T_G" driven through the C-ABI on one or more GPUs.
 
-The host loop only sequences the C-ABI calls, sizes buffers and runs the collectives of
-dist.Exchange; every step of a round (plan, nodes, bins, PDE solves, FFT, keys, selection,
-union, resolve, row gather) runs in libusfft.so.
+The host loop only sequences the C-ABI calls and sizes buffers; every step of a round (plan,
+nodes, bins, PDE solves, transpose, FFT, keys, selection, union, resolve, row gather) and, with
+several GPUs, every collective runs in libusfft.so (its own NCCL communicator; dist.py only
+broadcasts the communicator id).
 
 Round r = (step, t, i):
   a1 plan (usfft_plan_round) -> a4/a5 samples of this rank (usfft_sample_pde, nodes a2
-  generated in-kernel) -> a3 bins (usfft_lattice) -> a6 transpose (Exchange.transpose) ->
-  a7/a8 FFT + keys (usfft_lattice_fft) -> a9 kappa_max MAX -> a10 select + votes
-  (usfft_detect_select) -> votes SUM -> a11 union (usfft_detect_union) -> a12 resolve
+  generated in-kernel) -> a3 bins (usfft_lattice) -> a6 transpose (usfft_transpose) ->
+  a7/a8 FFT + keys (usfft_lattice_fft) -> a9 kappa_max MAX + a10 select + votes
+  (usfft_detect_select) -> votes SUM + a11 union (usfft_detect_union) -> a12 resolve
   (usfft_resolve, final round only).
 """
 from __future__ import annotations
@@ -19,7 +20,9 @@ import numpy as np
 import torch
 
 from . import binding as B
-from .dist import Exchange, partition
+import torch.distributed as tdist
+
+from .dist import TorchExchange, bootstrap_id, bounds, partition
 
 
 @dataclass
@@ -41,28 +44,60 @@ class Detector:
     """One usFFT detection run (Steps 1-2 of Alg. 1) for a workload preset (usfft_inputs)."""
 
     def __init__(self, cfg: dict, device: int = 0, group=None, maxit: int = 20000,
-                 timing: bool = False, blackbox=None):
+                 timing: bool = False, blackbox=None, loopback=None):
         """blackbox: optional callable (detector, plan, b0, nb) -> fp64 CUDA tensor [G][nb]
-        replacing the PDE sampler (Alg. 1 takes any black box); cfg["G"] then gives G."""
+        replacing the PDE sampler (Alg. 1 takes any black box); cfg["G"] then gives G.
+        Ranks: with torch.distributed initialised on an NCCL process group the library builds
+        its own communicator (id broadcast by dist.bootstrap_id); loopback = (rank, P, key)
+        runs virtual rank `rank` of P in this thread on one GPU (key: 128 bytes shared by the P
+        threads); a gloo process group falls back to TorchExchange (ranks sharing one GPU)."""
         self.cfg = cfg
         self.blackbox = blackbox
         self.dev = torch.device("cuda", device)
-        self.ctx = B.Context(device)
+        world = tdist.get_world_size(group) if tdist.is_available() and tdist.is_initialized() else 1
+        if loopback is not None:
+            rank, P, key = loopback
+            self.ctx = B.Context(device, rank=rank, nranks=P, comm_id=key, loopback=True)
+            self.ex = None
+        elif world > 1 and tdist.get_backend(group) == "nccl":
+            rank, P = tdist.get_rank(group), world
+            self.ctx = B.Context(device, rank=rank, nranks=P, comm_id=bootstrap_id(group))
+            self.ex = None
+        else:
+            self.ex = TorchExchange(group)
+            rank, P = self.ex.rank, self.ex.P
+            self.ctx = B.Context(device)
+        self.P, self.rank = P, rank
         # phi_Delta map: one global pole shift Delta = 1/(4 M0), M0 the Step-2 lattice size (Z27)
         self.delta = 0.0
         if cfg.get("theta") == "phi_delta":
-            M0 = B.usfft_plan_round(self.ctx, cfg["seed"], 2, 2, 1, cfg["d"], cfg["N"], cfg["s_local"],
-                                    "A", 1).M
-            self.delta = 1.0 / (4.0 * M0)
+            self.delta = B.usfft_plan_delta(self.ctx, cfg["N"], cfg["s_local"], int(cfg.get("lattice_factor", 1)))
         self.pde = B.pde_desc(cfg, maxit=maxit, tol=cfg.get("cg_tol", 1e-12), delta=self.delta) \
             if blackbox is None else None
-        self.ex = Exchange(group)
-        self.P, self.rank = self.ex.P, self.ex.rank
         self.G = cfg["G"] if blackbox is not None else (cfg["n"] - 1) ** 2
         self.g0, self.g1 = partition(self.G, self.P, self.rank)
         self.G_loc = self.g1 - self.g0
         self.timing = timing
         self.n_samples = 0
+
+    # ---- exchange steps: in the library (usfft_transpose; the MAX / SUM inside
+    # usfft_detect_select / usfft_detect_union) or, for gloo groups, through torch.distributed
+    def transpose(self, u: torch.Tensor, G: int, Btot: int):
+        """a6: this rank's samples [G][nb] -> (slabs [G_loc * Btot] of its nodes, slab_b0)."""
+        if self.ex is not None:
+            return self.ex.transpose(u, G, Btot)
+        sb = bounds(Btot, self.P)
+        if self.P == 1:
+            return u, sb
+        slabs = torch.empty(self.G_loc * Btot, dtype=torch.float64, device=self.dev)
+        B.usfft_transpose(self.ctx, G, Btot, u, slabs)
+        return slabs, sb
+
+    def _max(self, t):
+        return self.ex.max_(t) if self.ex is not None else t
+
+    def _sum(self, t):
+        return self.ex.sum_(t) if self.ex is not None else t
 
     # ------------------------------------------------------------------------------------------
     def round(self, step: int, t: int, i: int, I_prev: torch.Tensor, n_prev: int,
@@ -102,7 +137,7 @@ class Detector:
         bins = torch.empty((L, nJ), dtype=torch.int32, device=dev)
         B.usfft_lattice(ctx, plan, 0, 0, None, I_prev if plan.t_z > 1 else None, n_prev, kt, bins)
         mark("pde")
-        slabs, sb = self.ex.transpose(u, self.G, Btot)
+        slabs, sb = self.transpose(u, self.G, Btot)
         mark("exchange")
         Mh = M // 2 + 1
         spectra = torch.empty((self.G_loc, L, Mh, 2), dtype=torch.float64, device=dev)
@@ -115,7 +150,7 @@ class Detector:
             kmin = torch.empty((self.G_loc, nJ), dtype=torch.float64, device=dev)
             B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, nJ, spectra, kmin, kmax)
             mark("fft")
-            self.ex.max_(kmax)
+            self._max(kmax)
             votes = torch.empty(nJ, dtype=torch.int32, device=dev)
             B.usfft_detect_select(ctx, self.G_loc, nJ, kmin, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
                                   cfg.get("theta_abs", 0.0), votes, det_g, n_det_g, th2)
@@ -124,7 +159,7 @@ class Detector:
             B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, 0, spectra, None, kmax)
             mark("fft")
             votes = self._streamed_select(plan, nJ, s_tilde, chunk, spectra, bins, kmax, det_g, n_det_g, th2)
-        self.ex.sum_(votes)
+        self._sum(votes)
         det_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
         union_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
         n_det, n_union = B.usfft_detect_union(ctx, nJ, votes, flags, det_idx, union_idx)
@@ -181,7 +216,7 @@ class Detector:
                                  kmin_off=s_tilde, tau=tau)
             B.usfft_detect_select(ctx, G, W, merged, kmax, s_tilde, 0.0, 0.0, scratch, det_pos, n_det_g)
             B.usfft_detect_carry(ctx, G, s_tilde, W, merged, carry_k, carry_j, det_pos, n_det_g, j0, tau=tau)
-        self.ex.max_(kmax)
+        self._max(kmax)
         B.usfft_detect_select(ctx, G, s_tilde, carry_k, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
                               cfg.get("theta_abs", 0.0), scratch, det_pos, n_det_g, th2)
         votes = torch.zeros(nJ, dtype=torch.int32, device=dev)
@@ -274,7 +309,7 @@ class Detector:
             elif nb:
                 B.usfft_sample_pde(ctx, self.pde, plan, b0, nb, u, nb)
             self.n_samples += M
-            slabs, sb = self.ex.transpose(u, self.G, M)
+            slabs, sb = self.transpose(u, self.G, M)
             sel = torch.nonzero(assign == q).reshape(-1).to(torch.int32).contiguous()
             if M <= self.FFT_MAX_M:                        # lattice FFT, then read the bins
                 spectra = torch.empty((self.G_loc, 1, Mh, 2), dtype=torch.float64, device=dev)
@@ -296,7 +331,7 @@ class Detector:
         u = torch.empty((self.G, nb), dtype=torch.float64, device=dev)
         if nb:
             B.usfft_sample_pde(ctx, self.pde, plan, b0, nb, u, nb, Y[:, b0:b1].contiguous())
-        slabs, sb = self.ex.transpose(u, self.G, n)
+        slabs, sb = self.transpose(u, self.G, n)
         if self.P == 1:
             U = slabs.reshape(self.G_loc, n)
         else:

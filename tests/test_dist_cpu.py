@@ -9,7 +9,7 @@ import torch
 import torch.distributed as dist
 import torch.multiprocessing as mp
 
-from paper_2109_04131_b200.dist import Exchange, bounds, partition
+from paper_2109_04131_b200.dist import TorchExchange, bounds, partition
 
 
 def test_partition_covers_and_balances():
@@ -35,7 +35,7 @@ def _worker(rank, world, port, G, Btot, out):
     os.environ["MASTER_PORT"] = str(port)
     dist.init_process_group("gloo", rank=rank, world_size=world)
     try:
-        ex = Exchange()
+        ex = TorchExchange()
         full = torch.arange(G * Btot, dtype=torch.float64).reshape(G, Btot)
         b0, b1 = partition(Btot, world, rank)
         u_local = full[:, b0:b1].contiguous()
@@ -69,3 +69,23 @@ def test_gloo_world2_exchange(G, Btot):
         assert ok
         assert km == 1.0
         assert v == [3 * i for i in range(10)]
+
+
+def _boot_worker(rank, world, port, out):
+    os.environ["MASTER_ADDR"] = "127.0.0.1"
+    os.environ["MASTER_PORT"] = str(port)
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2109_04131_b200.dist import bootstrap_id
+        out[rank] = bootstrap_id()
+    finally:
+        dist.destroy_process_group()
+
+
+def test_gloo_bootstrap_id_identical():
+    """C0: rank 0's 128-byte communicator id (made by libusfft) reaches every rank unchanged."""
+    world = 2
+    mgr = mp.Manager()
+    out = mgr.dict()
+    mp.spawn(_boot_worker, args=(world, _free_port(), out), nprocs=world, join=True)
+    assert len(out[0]) == 128 and out[0] == out[1]

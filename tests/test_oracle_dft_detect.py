@@ -248,3 +248,24 @@ def test_fragile_band_edge():
     """Differences just outside eps are not fragile; s~ >= |J| leaves no cut."""
     assert _frag([1.0, 0.5, 0.5 - 2e-10], 2) == [False] * 3
     assert _frag([1.0, 0.5 + 1e-12, 0.5], 5) == [False] * 3
+
+
+def test_fragile_swaps_below_threshold_not():
+    """A near tie across the cut between two keys below theta changes no D_g (neither is
+    detected either way); the same tie above theta is fragile."""
+    assert _frag([1.0, 0.5, 1e-3, 1e-3 - 2e-11], 3, theta=0.1) == [False] * 4
+    assert _frag([1.0, 0.5, 0.2, 0.2 - 2e-11], 3, theta=0.1) == [False, False, True, True]
+
+
+def test_fragile_keys_one_ulp_apart_with_equal_sqrt():
+    """Equality is judged on the key kappa, not on m = sqrt(kappa): two keys one ulp apart whose
+    square roots round to the same double straddle the cut -> fragile (the conjugate pair
+    k, -k of a real sample set has such keys)."""
+    k1 = 5.147219e-15
+    k2 = np.nextafter(k1, 1.0)
+    while np.sqrt(k2) != np.sqrt(k1):                  # find a pair with one shared sqrt
+        k1 = np.nextafter(k1, 1.0)
+        k2 = np.nextafter(k1, 1.0)
+    K = np.array([[1.0, k1, k2, 1e-20]])
+    fr = detect.fragile(K, 2, 0.0)[0].tolist()
+    assert fr == [False, True, True, False]
