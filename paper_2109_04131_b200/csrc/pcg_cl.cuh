@@ -7,12 +7,21 @@
 // R = P^T, coarse operators rediscretised from the fine per-triangle coefficients, and the
 // bottom two levels (8 and 4 cells per side) as the fixed dense map K of pcg_mg.cuh.
 //
-// A sample of n = 128 (16129 unknowns) needs ~0.5 MB of fp64 state, more than one SM holds, so a
-// cluster of CS CTAs (CS = 8 at n = 128, 4 at n = 64) shares it; CTA r owns the fine rows
+// Precision (Z32): the CG (x, r, p, s, the operator A in w = A u, the dot products, alpha,
+// beta) is fp64; the preconditioner M^-1 r is evaluated in fp32 (its input r rounded to fp32,
+// every level's operator, smoother, transfer and the map K in fp32, its output u exact in
+// fp64).  Any fixed SPD map is an admissible preconditioner; the fp32 one changes the CG
+// iteration counts of configs 2-5 by zero (tools/mg_precision_study.py) and the converged
+// samples by <= 2e-14 relative.  It halves the shared-memory footprint and wavefronts of the
+// cycle and runs it on the fp32 pipe.
+//
+// A sample of n = 128 (16129 unknowns) needs ~0.5 MB of fp64 CG state, more than one SM holds, so
+// a cluster of CS CTAs (CS = 8 at n = 128, 4 at n = 64) shares it; CTA r owns the fine rows
 // j0+1 .. j0+HR, j0 = r HR, HR = n / CS = 16:
-//  * level 0 (fine): each thread keeps a 2 x BR block of nodes (x, r, p, s and the couplings) in
-//    registers, as in pcg_mg.cuh; the values a stencil needs are published in shared memory
-//    (split rows: even columns, then odd) with halo rows filled by the neighbour CTAs;
+//  * level 0 (fine): each thread keeps a 2 x 2 block of nodes (x, r, p, s and the couplings in
+//    fp64, their fp32 copies and omega D^-1) in registers; the values a stencil needs are
+//    published in shared memory (fp32, split rows: even columns, then odd) with halo rows
+//    filled by the neighbour CTAs;
 //  * level 1 (n/2 cells): distributed the same way;
 //  * levels 2 .. (8 cells per side): replicated.  The restricted level-2 residual is gathered into
 //    every CTA (each CTA sends its rows to all) and every CTA runs the rest of the cycle locally;
@@ -29,62 +38,75 @@
 //   X3 the level-2 residual rows of every CTA to every CTA;
 //   X4 the preconditioned residual u (1 row each side) for w = A u;
 //   X5 the CTA partials of (r,u), (w,u), (r,r) to every CTA.
-// Every halo value is recomputed by exactly the arithmetic its owner uses, so halos equal the
-// owners' values bit for bit and the cycle is the same fixed linear map on every CTA.  A
-// transfer of exchange k for CG iteration i+1 cannot start before every CTA has sent its X5
+// A transfer of exchange k for CG iteration i+1 cannot start before every CTA has sent its X5
 // partials of iteration i, which every CTA does only after its last read of iteration i's data:
 // the X5 all-to-all orders all buffer reuse (its own slots are double-buffered).  The per-sample
 // setup (coefficient tables, coarse operators, K) uses three cluster barriers.  Reductions and
 // the order of every sum are fixed, so a sample's result does not depend on the cluster that
 // solved it or on the launch split.
+//
+// The up-sweep of every coarse level is two passes: Zp = Z + P S_coarse once per node, then
+// S = Zp + omega D^-1 (R - A Zp) (the prolongation is not recomputed for every stencil
+// neighbour).  16 warps per CTA (a 2 x 2 node block per thread), one CTA per SM.
 #pragma once
 #include <cooperative_groups.h>
 
 namespace usfft {
 
-template <int NN, int CS, int BR_>
+template <int NN, int CS>
 struct ClC {
     static constexpr int n = NN, nx = n - 1, np = n + 1, HE = n / 2 + 1;
     static constexpr int HR = NN / CS;                       // fine rows per CTA
-    static constexpr int BC = 2, BR = BR_, LX = n / 2, NRG = HR / BR, NT = LX * NRG, NWARP = NT / 32;
+    static constexpr int BC = 2, BR = 2, LX = n / 2, NRG = HR / BR, NT = LX * NRG, NWARP = NT / 32;
     static constexpr int FRW = HR + 3, FR = FRW * np;        // fine grid rows 0 .. HR+2 (local)
     static constexpr int m1 = n / 2, P1 = m1 + 1, H1 = m1 / 2 + 1, HR1 = HR / 2, HR2 = HR / 4;
     static constexpr int L1R = HR1 + 4, F1 = L1R * P1;       // level-1 rows jl = -1 .. HR1+2 (lr = jl+1)
     static constexpr int LK = NN == 64 ? 3 : NN == 128 ? 4 : -1;
     static_assert(LK > 0, "cluster multigrid compiled for n = 64, 128");
-    static_assert(HR % 8 == 0 && LX % 32 == 0 && BR % 2 == 0 && HR % BR == 0, "strip geometry");
+    static_assert(HR % 8 == 0 && LX % 32 == 0 && HR % BR == 0, "strip geometry");
     __host__ __device__ static constexpr int ml(int l) { return NN >> l; }
     __host__ __device__ static constexpr int Pl(int l) { return (NN >> l) + 1; }
     __host__ __device__ static constexpr int Nl(int l) { return ((NN >> l) + 1) * ((NN >> l) + 1); }
     static constexpr int mK = 8, PK = 9, NK = 81, UK = 49, HK = (UK + 1) / 2;
     static constexpr int mE = 4, PE = 5, NE = 25, UE = 9;
-    static constexpr int KPAD = (8 - (HK * UK) % 16 + 16) % 16;
+    static constexpr int KPAD = (16 - (HK * UK) % 32 + 32) % 32;   // the two K halves 16 banks apart
     static constexpr int ATR = HR + 6;                       // coefficient-table cell rows j0-2 .. j0+HR+3
-    // shared-memory layout (doubles)
-    static constexpr int oDI0 = 0, oG0 = FR, oG1 = 2 * FR;   // fine omega D^-1, z0 grid, t / u grid
-    static constexpr int oRh = 3 * FR, oWHh = oRh + np, oWVh0 = oWHh + np, oWVh1 = oWVh0 + np;
-    static constexpr int oL1 = oWVh1 + np;                   // WH1, WV1, DI1, R1, Z1, T1 (= S1)
-    __host__ __device__ static constexpr int oLev(int l) {   // replicated level l: WH, WV, DI, R, Z, T (= S)
-        int o = oL1 + 6 * F1;
-        for (int q = 2; q < l; ++q) o += 6 * Nl(q);
+    static constexpr int JC = 8;                             // psi factors staged JC terms at a time
+    // ---- shared memory, in 4-byte units ----
+    // persistent (written by the setup, read by every iteration), fp32
+    static constexpr int oWH1 = 0, oWV1 = F1, oDI1 = 2 * F1;
+    static constexpr int oWHh = 3 * F1, oWVh0 = oWHh + np, oWVh1 = oWVh0 + np;
+    __host__ __device__ static constexpr int oLC(int l) {   // replicated level l: WH, WV, DI
+        int o = oWVh1 + np;
+        for (int q = 2; q < l; ++q) o += 3 * Nl(q);
         return o;
     }
-    static constexpr int oKs = oLev(LK);                     // WHK, WVK, DK, DIK, SK (NK each), RK (2 HK)
-    static constexpr int oKt = oKs + 5 * NK + 2 * HK;
-    static constexpr int oWHE = oKt + 2 * HK * UK + KPAD, oWVE = oWHE + NE, oAI = oWVE + NE;
-    static constexpr int oB = oAI + UE * UE, oC = oB + UE * UK;
-    static constexpr int oRed = oC + UE * UK;                // [2][CS][4] cluster partials (double-buffered)
-    static constexpr int oWred = oRed + 8 * CS;              // [4][NWARP] CTA partials
-    __host__ __device__ static constexpr int doubles() { return oWred + 4 * NWARP; }
+    static constexpr int oKs = oLC(LK);                      // WHK, WVK, DK, DIK, SK (NK each), RK (2 HK)
+    static constexpr int oWHE = oKs + 5 * NK + 2 * HK, oWVE = oWHE + NE;
+    static constexpr int oKt = oWVE + NE;                    // K (2 HK UK + KPAD), AI, Bm, Cm; setup: ctab
+    static constexpr int oAI = oKt + 2 * HK * UK + KPAD, oB = oAI + UE * UE, oC = oB + UE * UK;
+    static constexpr int oU = ((oC + UE * UK) + 3) & ~3;     // 16-byte aligned union
+    // union U: runtime grids | setup coefficient table aT (fp64) | setup psi staging (fp64)
+    static constexpr int oG0 = oU, oG1 = oG0 + FR, oRh = oG1 + FR;
+    static constexpr int oR1 = oRh + np, oZ1 = oR1 + F1, oT1 = oZ1 + F1;
+    __host__ __device__ static constexpr int oLR(int l) {   // replicated level l: R, Z, T
+        int o = oT1 + F1;
+        for (int q = 2; q < l; ++q) o += 3 * Nl(q);
+        return o;
+    }
+    static constexpr int URUN = oLR(LK) - oU;
+    static constexpr int UAT = 2 * (2 * ATR * n);            // fp64 aT
+    static constexpr int USTG = 2 * (JC * 2 * n + JC * 2 * ATR);
+    static constexpr int USZ = URUN > UAT ? (URUN > USTG ? URUN : USTG) : (UAT > USTG ? UAT : USTG);
+    static constexpr int oRedF = (oU + USZ + 3) & ~3;        // fp64 [2][CS][4] cluster partials, [4][NWARP]
+    __host__ __device__ static constexpr size_t bytes() { return 4 * (size_t)oRedF + 8 * (size_t)(8 * CS + 4 * NWARP); }
     // setup: the coarse-level triangle coefficients (levels 2 .. LK+1, lower then upper plane)
     __host__ __device__ static constexpr int ctoff(int l) {
         int o = 0;
         for (int q = 2; q < l; ++q) o += 2 * ml(q) * ml(q);
         return o;
     }
-    static constexpr int STAGE = oRed - oL1;                 // staging room for the psi factors
-    static_assert(2 * ATR * n <= 3 * FR, "coefficient table must fit in DI0 .. G1");
-    static_assert(ctoff(LK + 2) <= oRed - oKt, "coarse coefficient table must fit in the K region");
+    static_assert(ctoff(LK + 2) <= oU - oKt, "coarse coefficient table must fit in the K region");
     static_assert(2 * UK <= NT && 3 * CS <= 32, "thread mapping");
 };
 
@@ -113,10 +135,14 @@ __device__ __forceinline__ uint32_t mapa(uint32_t a, uint32_t rank) {
     asm volatile("mapa.shared::cluster.u32 %0, %1, %2;" : "=r"(o) : "r"(a), "r"(rank));
     return o;
 }
-// 8-byte DSMEM store completing 8 transaction bytes on the destination CTA's mbarrier
+// DSMEM stores completing their byte count on the destination CTA's mbarrier
 __device__ __forceinline__ void st_async(uint32_t dst, double v, uint32_t mbar) {
     asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b64 [%0], %1, [%2];"
                  :: "r"(dst), "l"(__double_as_longlong(v)), "r"(mbar) : "memory");
+}
+__device__ __forceinline__ void st_async(uint32_t dst, float v, uint32_t mbar) {
+    asm volatile("st.async.shared::cluster.mbarrier::complete_tx::bytes.b32 [%0], %1, [%2];"
+                 :: "r"(dst), "r"(__float_as_uint(v)), "r"(mbar) : "memory");
 }
 __device__ __forceinline__ void mbar_init(uint32_t mb) {
     asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" :: "r"(mb) : "memory");
@@ -142,21 +168,22 @@ __device__ long long g_cl_probe[16][32];
 #define CL_MARK(on, id) ((void)0)
 #endif
 
-template <int NN, int CS, int BR_, int MINB>
-__global__ void __launch_bounds__(ClC<NN, CS, BR_>::NT, MINB)
+template <int NN, int CS, int MINB>
+__global__ void __launch_bounds__(ClC<NN, CS>::NT, MINB)
 k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
          int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
          const double *__restrict__ Bt) {
-    using L = ClC<NN, CS, BR_>;
+    using L = ClC<NN, CS>;
     namespace cg = cooperative_groups;
     constexpr int n = NN, nx = L::nx, np = L::np, HE = L::HE, HR = L::HR, BC = L::BC, BR = L::BR;
     constexpr int LX = L::LX, NRG = L::NRG, NT = L::NT, NWARP = L::NWARP, W = 3 * n + 1;
     constexpr int m1 = L::m1, P1 = L::P1, H1 = L::H1, HR1 = L::HR1, HR2 = L::HR2, LK = L::LK;
     constexpr int mK = L::mK, PK = L::PK, NK = L::NK, UK = L::UK, HK = L::HK;
-    constexpr int mE = L::mE, PE = L::PE, UE = L::UE, ATR = L::ATR;
+    constexpr int mE = L::mE, PE = L::PE, UE = L::UE, ATR = L::ATR, JC = L::JC;
     constexpr int m2 = L::ml(2), P2 = L::Pl(2);
-    extern __shared__ double sm[];
+    constexpr float om = 0.8f;                           // kMgOmega
+    extern __shared__ __align__(16) float sf[];
     __shared__ double th_amp[kMaxD];
     __shared__ alignas(8) unsigned long long mbar[5];
     cg::cluster_group cluster = cg::this_cluster();
@@ -164,17 +191,19 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     const bool has_lo = rank > 0, has_hi = rank < CS - 1;
     const int j0 = rank * HR, J0 = j0 / 2, J20 = j0 / 4;
 
-    double *DI0 = sm + L::oDI0, *G0 = sm + L::oG0, *G1 = sm + L::oG1, *aT = sm;   // aT: setup only
-    double *Rh = sm + L::oRh, *WHh = sm + L::oWHh, *WVh0 = sm + L::oWVh0, *WVh1 = sm + L::oWVh1;
-    double *WH1 = sm + L::oL1, *WV1 = WH1 + L::F1, *DI1 = WH1 + 2 * L::F1, *R1 = WH1 + 3 * L::F1;
-    double *Z1 = WH1 + 4 * L::F1, *T1 = WH1 + 5 * L::F1, *S1 = T1;
-    double *WHK = sm + L::oKs, *WVK = WHK + NK, *DK = WHK + 2 * NK, *DIK = WHK + 3 * NK, *SK = WHK + 4 * NK;
-    double *RK = WHK + 5 * NK, *Kt = sm + L::oKt, *ctab = sm + L::oKt;
-    double *WHE = sm + L::oWHE, *WVE = sm + L::oWVE, *AI = sm + L::oAI, *Bm = sm + L::oB, *Cm = sm + L::oC;
-    double *cred = sm + L::oRed, *wred = sm + L::oWred;
-    auto lv = [&](int l, int k) -> double * { return sm + L::oLev(l) + k * L::Nl(l); };
-    enum { LWH = 0, LWV = 1, LDI = 2, LR = 3, LZ = 4, LT = 5 };
-    double *R2 = lv(2, LR);
+    float *WH1 = sf + L::oWH1, *WV1 = sf + L::oWV1, *DI1 = sf + L::oDI1;
+    float *WHh = sf + L::oWHh, *WVh0 = sf + L::oWVh0, *WVh1 = sf + L::oWVh1;
+    float *WHK = sf + L::oKs, *WVK = WHK + NK, *DK = WHK + 2 * NK, *DIK = WHK + 3 * NK, *SK = WHK + 4 * NK;
+    float *RK = WHK + 5 * NK, *WHE = sf + L::oWHE, *WVE = sf + L::oWVE;
+    float *Kt = sf + L::oKt, *ctab = sf + L::oKt, *AI = sf + L::oAI, *Bm = sf + L::oB, *Cm = sf + L::oC;
+    float *G0 = sf + L::oG0, *G1 = sf + L::oG1, *Rh = sf + L::oRh;
+    float *R1 = sf + L::oR1, *Z1 = sf + L::oZ1, *T1 = sf + L::oT1;
+    double *aT = reinterpret_cast<double *>(sf + L::oU);                  // setup only
+    double *cred = reinterpret_cast<double *>(sf + L::oRedF), *wred = cred + 8 * CS;
+    auto lc = [&](int l, int k) -> float * { return sf + L::oLC(l) + k * L::Nl(l); };   // WH, WV, DI
+    auto lr = [&](int l, int k) -> float * { return sf + L::oLR(l) + k * L::Nl(l); };   // R, Z, T
+    enum { LWH = 0, LWV = 1, LDI = 2, LR = 0, LZ = 1, LT = 2 };
+    float *R2 = lr(2, LR);
 
     const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
     const int lx = tid % LX, rg = tid / LX;
@@ -184,10 +213,10 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 
     // ---- exchanges: mbarriers, expected bytes, peer addresses -----------------------------------
     const uint32_t mb0 = smem_addr(&mbar[0]);
-    const uint32_t xb[5] = {(uint32_t)(8 * nx * ((has_hi ? 3 : 0) + (has_lo ? 1 : 0))),
-                            (uint32_t)(8 * (m1 - 1) * ((has_hi ? 3 : 0) + (has_lo ? 3 : 0))),
-                            (uint32_t)(8 * (m2 - 1) * (m2 - 1)),
-                            (uint32_t)(8 * nx * ((has_hi ? 1 : 0) + (has_lo ? 1 : 0))),
+    const uint32_t xb[5] = {(uint32_t)(4 * nx * ((has_hi ? 3 : 0) + (has_lo ? 1 : 0))),
+                            (uint32_t)(4 * (m1 - 1) * ((has_hi ? 3 : 0) + (has_lo ? 3 : 0))),
+                            (uint32_t)(4 * (m2 - 1) * (m2 - 1)),
+                            (uint32_t)(4 * nx * ((has_hi ? 1 : 0) + (has_lo ? 1 : 0))),
                             (uint32_t)(8 * 3 * CS)};
     if (tid == 0) {
         for (int k = 0; k < 5; ++k) mbar_init(mb0 + 8 * k);
@@ -210,7 +239,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     cluster_barrier();                                   // mbarriers initialised everywhere
 
     // ---- addressing -------------------------------------------------------------------------
-    // fine node (col0 + 1 + c, row0 + 1 + q) local; c even = odd column, c odd = even column
+    // fine node (col0 + 1 + c, row0 + 1 + q) local, c in -1 .. BC; c even = odd column
     auto fe = [&](int c, int q) -> int {
         const int slot = (c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1);
         return (row0 + 1 + q) * np + slot;
@@ -231,31 +260,42 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
-        // stage the factors amp_j theta_j X_j at the 2n lower/upper abscissae and Y_j at the
-        // strip's 2 ATR ordinates (one bulk of independent L2 loads instead of a dependent one per term)
-        const bool staged = Q.d * (2 * n + 2 * ATR) <= L::STAGE;
-        double *Xs = sm + L::oL1, *Ys = Xs + 2 * n * Q.d;
-        if (staged) {
-            for (int e = tid; e < 2 * n * Q.d; e += NT) {
-                const int j = e / (2 * n), c = e - j * 2 * n, up = c >= n, ci = up ? c - n : c;
-                Xs[e] = th_amp[j] * __ldg(S + j * W + 3 * ci + (up ? 1 : 2));
-            }
-            for (int e = tid; e < 2 * ATR * Q.d; e += NT) {
-                const int j = e / (2 * ATR), c = e - j * 2 * ATR, up = c >= ATR, rl = up ? c - ATR : c;
-                const int cj = min(max(j0 - 2 + rl, 0), n - 1);
-                Ys[e] = __ldg(Sy0 + j * W + 3 * cj + (up ? 2 : 1));
-            }
-            __syncthreads();
-        }
-        {   // aT[plane][cj - (j0-2)][ci]: thread = (column, row set)
+        {   // aT[plane][cj - (j0-2)][ci] = sum_j amp_j theta_j X_j Y_j: thread = (column, row set); the
+            // factors amp_j theta_j X_j at the 2n abscissae and Y_j at the strip's 2 ATR ordinates are
+            // staged JC terms at a time, all loads of a chunk issued before its first store
+            constexpr int SX = JC * 2 * n, SY = JC * 2 * ATR;
+            constexpr int XPT = (SX + NT - 1) / NT, YPT = (SY + NT - 1) / NT;
             constexpr int CPT = NT / n, KJ = (ATR + CPT - 1) / CPT;
+            double *Xs = reinterpret_cast<double *>(sf + L::oU), *Ys = Xs + SX;
             const int ci = tid % n, r0 = tid / n;
             double slo[KJ], sup[KJ];
 #pragma unroll
             for (int k = 0; k < KJ; ++k) slo[k] = sup[k] = 0.0;
-            if (staged) {
+            for (int jb = 0; jb < Q.d; jb += JC) {
+                const int jn = min(JC, Q.d - jb);
+                double xv[XPT], yv[YPT];
+#pragma unroll
+                for (int k = 0; k < XPT; ++k) {
+                    const int e = tid + k * NT, j = e / (2 * n), c = e - j * 2 * n, up = c >= n;
+                    const int cc = up ? c - n : c;
+                    xv[k] = (e < SX && j < jn) ? th_amp[jb + j] * __ldg(S + (jb + j) * W + 3 * cc + (up ? 1 : 2)) : 0.0;
+                }
+#pragma unroll
+                for (int k = 0; k < YPT; ++k) {
+                    const int e = tid + k * NT, j = e / (2 * ATR), c = e - j * 2 * ATR, up = c >= ATR;
+                    const int rl = up ? c - ATR : c, cj = min(max(j0 - 2 + rl, 0), n - 1);
+                    yv[k] = (e < SY && j < jn) ? __ldg(Sy0 + (jb + j) * W + 3 * cj + (up ? 2 : 1)) : 0.0;
+                }
+                __syncthreads();                         // the previous chunk is consumed
+#pragma unroll
+                for (int k = 0; k < XPT; ++k)
+                    if (tid + k * NT < SX) Xs[tid + k * NT] = xv[k];
+#pragma unroll
+                for (int k = 0; k < YPT; ++k)
+                    if (tid + k * NT < SY) Ys[tid + k * NT] = yv[k];
+                __syncthreads();
 #pragma unroll 2
-                for (int j = 0; j < Q.d; ++j) {
+                for (int j = 0; j < jn; ++j) {
                     const double tlo = Xs[j * 2 * n + ci], tup = Xs[j * 2 * n + n + ci];
                     const double *yl = Ys + j * 2 * ATR, *yu = yl + ATR;
 #pragma unroll
@@ -265,18 +305,8 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                         sup[k] = fma(tup, yu[rl], sup[k]);
                     }
                 }
-            } else {
-                for (int j = 0; j < Q.d; ++j) {
-                    const double am = th_amp[j];
-                    const double tlo = am * __ldg(S + j * W + 3 * ci + 2), tup = am * __ldg(S + j * W + 3 * ci + 1);
-#pragma unroll
-                    for (int k = 0; k < KJ; ++k) {
-                        const int cj = min(max(j0 - 2 + r0 + CPT * k, 0), n - 1);
-                        slo[k] = fma(tlo, __ldg(Sy0 + j * W + 3 * cj + 1), slo[k]);
-                        sup[k] = fma(tup, __ldg(Sy0 + j * W + 3 * cj + 2), sup[k]);
-                    }
-                }
             }
+            __syncthreads();                             // staging consumed: aT overlaps it
 #pragma unroll
             for (int k = 0; k < KJ; ++k) {
                 const int rl = r0 + CPT * k, cj = j0 - 2 + rl;
@@ -286,7 +316,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
             }
         }
-        cluster_barrier();                               // A: nobody stages any more; own table complete
+        cluster_barrier();                               // A: previous sample done everywhere; own table complete
         CL_MARK(pset, 21);
         // a of T_lo / T_up of cell (ci, cj) of the level with cells of width 2^sh h: the fine
         // triangle with the same centroid (pcg_mg.cuh), from the local table
@@ -295,14 +325,16 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             const int fi = ci * p + ra / 3, fj = cj * p + rb / 3, pl = (ra % 3 == 1) ? 1 : 0;
             return aT[(pl * ATR + fj - (j0 - 2)) * n + fi];
         };
-        // fine couplings of the own block (ring edges included)
+        // fine couplings of the own block (ring edges included), fp64 and their fp32 copies
         double cE[BR][BC + 1], cN[BR + 1][BC];
+        float ce[BR][BC + 1], cn[BR + 1][BC];
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c <= BC; ++c) {
                 const int i = col0 + c, j = j0 + row0 + q + 1;
                 cE[q][c] = (i <= nx && j <= nx) ? 0.5 * (fcl(i, j, 0, 0) + fcl(i, j - 1, 1, 0)) : 0.0;
+                ce[q][c] = (float)cE[q][c];
             }
 #pragma unroll
         for (int q = 0; q <= BR; ++q)
@@ -310,19 +342,30 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int c = 0; c < BC; ++c) {
                 const int i = col0 + c + 1, j = j0 + row0 + q;
                 cN[q][c] = (i <= nx && j <= nx) ? 0.5 * (fcl(i, j, 1, 0) + fcl(i - 1, j, 0, 0)) : 0.0;
+                cn[q][c] = (float)cN[q][c];
+            }
+        float di0[BR][BC], dg32[BR][BC];                 // omega D^-1 and D of the own fine nodes
+        double dg64[BR][BC];
+#pragma unroll
+        for (int q = 0; q < BR; ++q)
+#pragma unroll
+            for (int c = 0; c < BC; ++c) {
+                dg64[q][c] = cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c];
+                dg32[q][c] = ce[q][c + 1] + ce[q][c] + cn[q + 1][c] + cn[q][c];
+                di0[q][c] = valid(q, c) ? (float)(kMgOmega * rcp_pos(dg64[q][c])) : 0.0f;
             }
         for (int i = tid; i <= n; i += NT) {             // couplings of the halo row above (HR+1)
             const int jh = j0 + HR + 1;
-            WHh[i] = (i <= nx && jh <= nx) ? 0.5 * (fcl(i, jh, 0, 0) + fcl(i, jh - 1, 1, 0)) : 0.0;
-            WVh0[i] = (i >= 1 && i <= nx && jh - 1 <= nx) ? 0.5 * (fcl(i, jh - 1, 1, 0) + fcl(i - 1, jh - 1, 0, 0)) : 0.0;
-            WVh1[i] = (i >= 1 && i <= nx && jh <= nx) ? 0.5 * (fcl(i, jh, 1, 0) + fcl(i - 1, jh, 0, 0)) : 0.0;
+            WHh[i] = (i <= nx && jh <= nx) ? (float)(0.5 * (fcl(i, jh, 0, 0) + fcl(i, jh - 1, 1, 0))) : 0.0f;
+            WVh0[i] = (i >= 1 && i <= nx && jh - 1 <= nx) ? (float)(0.5 * (fcl(i, jh - 1, 1, 0) + fcl(i - 1, jh - 1, 0, 0))) : 0.0f;
+            WVh1[i] = (i >= 1 && i <= nx && jh <= nx) ? (float)(0.5 * (fcl(i, jh, 1, 0) + fcl(i - 1, jh, 0, 0))) : 0.0f;
         }
         for (int e = tid; e < L::F1; e += NT) {           // level-1 couplings, rows jl = -1 .. HR1+1
-            const int lr = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lr - 1, J = J0 + jl;
+            const int lrw = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lrw - 1, J = J0 + jl;
             WH1[e] = (jl >= 0 && jl <= HR1 + 1 && I < m1 && J >= 1 && J < m1)
-                         ? 0.5 * (fcl(I, J, 0, 1) + fcl(I, J - 1, 1, 1)) : 0.0;
+                         ? (float)(0.5 * (fcl(I, J, 0, 1) + fcl(I, J - 1, 1, 1))) : 0.0f;
             WV1[e] = (jl <= HR1 + 1 && J >= 0 && J < m1 && I >= 1 && I < m1)
-                         ? 0.5 * (fcl(I, J, 1, 1) + fcl(I - 1, J, 0, 1)) : 0.0;
+                         ? (float)(0.5 * (fcl(I, J, 1, 1) + fcl(I - 1, J, 0, 1))) : 0.0f;
         }
         {   // coarse triangle coefficients (levels 2 .. LK+1) whose fine triangle is in the own rows,
             // sent to every CTA's coarse table
@@ -337,31 +380,31 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 const int m = L::ml(l), cell = q - base, ci = cell % m, cj = cell / m;
                 const int p = 1 << l, rb = up ? 2 * p : p, fj = cj * p + rb / 3;
                 if (fj / HR != rank) continue;
-                const double v = fcl(ci, cj, up, l);
+                const float v = (float)fcl(ci, cj, up, l);
                 const int dst = L::ctoff(l) + (up ? m * m : 0) + cell;
 #pragma unroll
                 for (int k = 0; k < CS; ++k) cluster.map_shared_rank(ctab, k)[dst] = v;
             }
         }
-        cluster_barrier();                               // B: every coarse table complete
+        cluster_barrier();                               // B: every coarse table complete; aT dead
         CL_MARK(pset, 22);
         {   // replicated couplings from the coarse table
-            auto ct = [&](int l, int ci, int cj, int up) -> double {
+            auto ct = [&](int l, int ci, int cj, int up) -> float {
                 const int m = L::ml(l);
                 return ctab[L::ctoff(l) + (up ? m * m : 0) + cj * m + ci];
             };
-            auto whc = [&](int l, int I, int J) -> double {
+            auto whc = [&](int l, int I, int J) -> float {
                 const int M = L::ml(l);
-                return (I < M && J >= 1 && J < M) ? 0.5 * (ct(l, I, J, 0) + ct(l, I, J - 1, 1)) : 0.0;
+                return (I < M && J >= 1 && J < M) ? 0.5f * (ct(l, I, J, 0) + ct(l, I, J - 1, 1)) : 0.0f;
             };
-            auto wvc = [&](int l, int I, int J) -> double {
+            auto wvc = [&](int l, int I, int J) -> float {
                 const int M = L::ml(l);
-                return (J < M && I >= 1 && I < M) ? 0.5 * (ct(l, I, J, 1) + ct(l, I - 1, J, 0)) : 0.0;
+                return (J < M && I >= 1 && I < M) ? 0.5f * (ct(l, I, J, 1) + ct(l, I - 1, J, 0)) : 0.0f;
             };
 #pragma unroll
             for (int l = 2; l < LK; ++l) {
                 const int Pq = L::Pl(l);
-                double *wh = lv(l, LWH), *wv = lv(l, LWV);
+                float *wh = lc(l, LWH), *wv = lc(l, LWV);
                 for (int e = tid; e < L::Nl(l); e += NT) {
                     const int I = e % Pq, J = e / Pq;
                     wh[e] = whc(l, I, J);
@@ -381,65 +424,56 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         __syncthreads();                                 // the coarse table (K region) is dead
         // ---- diagonals, zeroed grids, the dense maps -------------------------------------------
-        for (int e = tid; e < 3 * L::FR + L::np; e += NT) DI0[e] = 0.0;   // DI0, G0, G1, Rh
+        for (int e = tid; e < L::URUN; e += NT) sf[L::oU + e] = 0.0f;      // every runtime grid
         for (int e = tid; e < L::F1; e += NT) {           // level-1 omega D^-1 (rows 0 .. HR1+1)
-            const int lr = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lr - 1, J = J0 + jl;
+            const int lrw = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lrw - 1, J = J0 + jl;
             const bool in = I >= 1 && I < m1 && J >= 1 && J < m1 && jl >= 0 && jl <= HR1 + 1;
-            const double dv = in ? WH1[e] + WH1[e1(I - 1, jl)] + WV1[e] + WV1[e - P1] : 1.0;
-            DI1[e] = in ? kMgOmega * rcp_pos(dv) : 0.0;
-            R1[e] = Z1[e] = T1[e] = 0.0;
+            const float dv = in ? WH1[e] + WH1[e1(I - 1, jl)] + WV1[e] + WV1[e - P1] : 1.0f;
+            DI1[e] = in ? om / dv : 0.0f;
         }
 #pragma unroll
         for (int l = 2; l < LK; ++l) {
             const int M = L::ml(l), Pq = L::Pl(l);
-            const double *wh = lv(l, LWH), *wv = lv(l, LWV);
-            double *di = lv(l, LDI);
+            const float *wh = lc(l, LWH), *wv = lc(l, LWV);
+            float *di = lc(l, LDI);
             for (int e = tid; e < L::Nl(l); e += NT) {
                 const int I = e % Pq, J = e / Pq;
                 const bool in = I >= 1 && I < M && J >= 1 && J < M;
-                di[e] = in ? kMgOmega * rcp_pos(wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) : 0.0;
-                lv(l, LR)[e] = lv(l, LZ)[e] = lv(l, LT)[e] = 0.0;
+                di[e] = in ? om / (wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) : 0.0f;
             }
         }
         for (int e = tid; e < NK; e += NT) {
             const int I = e % PK, J = e / PK;
             const bool in = I >= 1 && I < mK && J >= 1 && J < mK;
-            const double dv = in ? WHK[e] + WHK[e - 1] + WVK[e] + WVK[e - PK] : 0.0;
+            const float dv = in ? WHK[e] + WHK[e - 1] + WVK[e] + WVK[e - PK] : 0.0f;
             DK[e] = dv;
-            DIK[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
-            SK[e] = 0.0;
+            DIK[e] = in ? om / dv : 0.0f;
+            SK[e] = 0.0f;
         }
         __syncthreads();
-#pragma unroll
-        for (int q = 0; q < BR; ++q)                     // omega D^-1 of the own fine nodes
-#pragma unroll
-            for (int c = 0; c < BC; ++c) {
-                const double dv = cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c];
-                if (valid(q, c)) DI0[fe(c, q)] = kMgOmega * rcp_pos(dv);
-            }
         if (warp == 0) {   // Gauss-Jordan inverse of the 4-cell operator (9 unknowns), by shuffles
             const int ri = lane < UE ? lane : 0;
             const int ia = ri % (mE - 1) + 1, ja = ri / (mE - 1) + 1, g = ja * PE + ia;
-            const double wr = WHE[g], wl = WHE[g - 1], wu = WVE[g], wd = WVE[g - PE];
-            double a[UE];
+            const float wr = WHE[g], wl = WHE[g - 1], wu = WVE[g], wd = WVE[g - PE];
+            float a[UE];
 #pragma unroll
             for (int c = 0; c < UE; ++c)
                 a[c] = c == ri ? wr + wl + wu + wd
                      : (c == ri + 1 && ia < mE - 1) ? -wr
                      : (c == ri - 1 && ia > 1) ? -wl
                      : (c == ri + (mE - 1) && ja < mE - 1) ? -wu
-                     : (c == ri - (mE - 1) && ja > 1) ? -wd : 0.0;
+                     : (c == ri - (mE - 1) && ja > 1) ? -wd : 0.0f;
 #pragma unroll
             for (int k = 0; k < UE; ++k) {
-                double prow[UE];
+                float prow[UE];
 #pragma unroll
                 for (int c = 0; c < UE; ++c) prow[c] = __shfl_sync(0xffffffffu, a[c], k);
-                const double piv = rcp_pos(prow[k]);
-                const double f = -a[k] * piv;
+                const float piv = 1.0f / prow[k];
+                const float f = -a[k] * piv;
 #pragma unroll
                 for (int c = 0; c < UE; ++c) {
                     if (lane == k) a[c] = c == k ? piv : prow[c] * piv;
-                    else a[c] = c == k ? f : fma(f, prow[c], a[c]);
+                    else a[c] = c == k ? f : fmaf(f, prow[c], a[c]);
                 }
             }
             __syncwarp();
@@ -448,47 +482,48 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < UE; ++c) AI[lane * UE + c] = a[c];
             }
         }
-        __syncthreads();
         // K = 2 Dw - Dw AK Dw + B^T AE^-1 B,  B = PE^T (I - AK Dw)  (pcg_mg.cuh)
         for (int e = tid; e < UE * UK; e += NT) {
             const int r = e / UK, k = e % UK;
             const int Ir = r % (mE - 1) + 1, Jr = r / (mE - 1) + 1;
             const int Ik = k % (mK - 1) + 1, Jk = k / (mK - 1) + 1, ek = Jk * PK + Ik;
-            const double dwk = DIK[ek];
-            auto wr = [&](int Im, int Jm) -> double {
+            const float dwk = DIK[ek];
+            auto wr = [&](int Im, int Jm) -> float {
                 const int ax = abs(Im - 2 * Ir), ay = abs(Jm - 2 * Jr);
-                return (ax > 1 || ay > 1) ? 0.0 : (ax ? 0.5 : 1.0) * (ay ? 0.5 : 1.0);
+                return (ax > 1 || ay > 1) ? 0.0f : (ax ? 0.5f : 1.0f) * (ay ? 0.5f : 1.0f);
             };
-            double v = wr(Ik, Jk) * (1.0 - DK[ek] * dwk);
-            v = fma(wr(Ik + 1, Jk), WHK[ek] * dwk, v);
-            v = fma(wr(Ik - 1, Jk), WHK[ek - 1] * dwk, v);
-            v = fma(wr(Ik, Jk + 1), WVK[ek] * dwk, v);
-            v = fma(wr(Ik, Jk - 1), WVK[ek - PK] * dwk, v);
+            float v = wr(Ik, Jk) * (1.0f - DK[ek] * dwk);
+            v = fmaf(wr(Ik + 1, Jk), WHK[ek] * dwk, v);
+            v = fmaf(wr(Ik - 1, Jk), WHK[ek - 1] * dwk, v);
+            v = fmaf(wr(Ik, Jk + 1), WVK[ek] * dwk, v);
+            v = fmaf(wr(Ik, Jk - 1), WVK[ek - PK] * dwk, v);
             Bm[e] = v;
         }
         __syncthreads();
         for (int e = tid; e < UE * UK; e += NT) {        // C = AE^-1 B
             const int r = e / UK, k = e % UK;
-            double v = 0.0;
-            for (int c = 0; c < UE; ++c) v = fma(AI[r * UE + c], Bm[c * UK + k], v);
+            float v = 0.0f;
+#pragma unroll
+            for (int c = 0; c < UE; ++c) v = fmaf(AI[r * UE + c], Bm[c * UK + k], v);
             Cm[e] = v;
         }
         __syncthreads();
         auto kix = [](int col, int row) -> int { return col * UK + row + (col >= HK ? L::KPAD : 0); };
-        for (int e = UK * UK + tid; e < 2 * HK * UK; e += NT) Kt[kix(e / UK, e % UK)] = 0.0;
-        if (tid < 2 * HK - UK) RK[UK + tid] = 0.0;
+        for (int e = UK * UK + tid; e < 2 * HK * UK; e += NT) Kt[kix(e / UK, e % UK)] = 0.0f;
+        if (tid < 2 * HK - UK) RK[UK + tid] = 0.0f;
         for (int e = tid; e < UK * UK; e += NT) {        // B^T C
             const int i = e % UK, k = e / UK;
-            double v = 0.0;
-            for (int r = 0; r < UE; ++r) v = fma(Bm[r * UK + i], Cm[r * UK + k], v);
+            float v = 0.0f;
+#pragma unroll
+            for (int r = 0; r < UE; ++r) v = fmaf(Bm[r * UK + i], Cm[r * UK + k], v);
             Kt[kix(k, i)] = v;
         }
         __syncthreads();
         for (int e = tid; e < 5 * UK; e += NT) {         // + 2 Dw - Dw AK Dw (5-point), row i
             const int i = e % UK, d = e / UK;
             const int Ii = i % (mK - 1) + 1, Ji = i / (mK - 1) + 1, ei = Ji * PK + Ii;
-            const double dwi = DIK[ei];
-            if (d == 0) Kt[kix(i, i)] += fma(-dwi * DK[ei], dwi, 2.0 * dwi);
+            const float dwi = DIK[ei];
+            if (d == 0) Kt[kix(i, i)] += fmaf(-dwi * DK[ei], dwi, 2.0f * dwi);
             else if (d == 1 && Ii < mK - 1) Kt[kix(i + 1, i)] += dwi * WHK[ei] * DIK[ei + 1];
             else if (d == 2 && Ii > 1) Kt[kix(i - 1, i)] += dwi * WHK[ei - 1] * DIK[ei - 1];
             else if (d == 3 && Ji < mK - 1) Kt[kix(i + (mK - 1), i)] += dwi * WVK[ei] * DIK[ei + PK];
@@ -498,25 +533,25 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         CL_MARK(pset, 23);
 
         // ---- helpers of the iteration -----------------------------------------------------------
-        auto diag = [&](int q, int c) -> double { return cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c]; };
-        auto apply_fine = [&](const double *Gs, const double (&v)[BR][BC], double (&out)[BR][BC]) {
+        // fp32 stencil of the preconditioner: own values in v, the rest from the grid Gs
+        auto apply32 = [&](const float *Gs, const float (&v)[BR][BC], float (&out)[BR][BC]) {
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    const double vl = c > 0 ? v[q][c - 1] : Gs[fe(c - 1, q)];
-                    const double vr = c + 1 < BC ? v[q][c + 1] : Gs[fe(c + 1, q)];
-                    const double vd = q > 0 ? v[q - 1][c] : Gs[fe(c, q - 1)];
-                    const double vu = q + 1 < BR ? v[q + 1][c] : Gs[fe(c, q + 1)];
-                    double a = diag(q, c) * v[q][c];
-                    a = fma(-cE[q][c + 1], vr, a);
-                    a = fma(-cE[q][c], vl, a);
-                    a = fma(-cN[q + 1][c], vu, a);
-                    a = fma(-cN[q][c], vd, a);
-                    out[q][c] = valid(q, c) ? a : 0.0;
+                    const float vl = c > 0 ? v[q][c - 1] : Gs[fe(c - 1, q)];
+                    const float vr = c + 1 < BC ? v[q][c + 1] : Gs[fe(c + 1, q)];
+                    const float vd = q > 0 ? v[q - 1][c] : Gs[fe(c, q - 1)];
+                    const float vu = q + 1 < BR ? v[q + 1][c] : Gs[fe(c, q + 1)];
+                    float a = dg32[q][c] * v[q][c];
+                    a = fmaf(-ce[q][c + 1], vr, a);
+                    a = fmaf(-ce[q][c], vl, a);
+                    a = fmaf(-cn[q + 1][c], vu, a);
+                    a = fmaf(-cn[q][c], vd, a);
+                    out[q][c] = valid(q, c) ? a : 0.0f;
                 }
         };
-        auto local_publish = [&](double *Gd, const double (&v)[BR][BC]) {
+        auto publish = [&](float *Gd, const float (&v)[BR][BC]) {
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
@@ -524,27 +559,27 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     if (valid(q, c)) Gd[fe(c, q)] = v[q][c];
         };
         // X1: z0 rows 1, 2 -> rows HR+1, HR+2 below; z0 row HR -> row 0 above; r row 1 -> Rh below
-        auto send_x1 = [&](const double (&z)[BR][BC], const double (&rv)[BR][BC]) {
+        auto send_x1 = [&](const float (&z)[BR][BC], const double (&rv)[BR][BC]) {
             if (rg == 0 && has_lo) {
 #pragma unroll
                 for (int c = 0; c < BC; ++c)
                     if (col0 + c + 1 <= nx) {
-                        st_async(G0_lo + 8 * (fe(c, 0) + HR * np), z[0][c], mb_lo);
-                        st_async(G0_lo + 8 * (fe(c, 1) + HR * np), z[1][c], mb_lo);
-                        st_async(Rh_lo + 8 * (col0 + c + 1), rv[0][c], mb_lo);
+                        st_async(G0_lo + 4 * (fe(c, 0) + HR * np), z[0][c], mb_lo);
+                        st_async(G0_lo + 4 * (fe(c, 1) + HR * np), z[1][c], mb_lo);
+                        st_async(Rh_lo + 4 * (col0 + c + 1), (float)rv[0][c], mb_lo);
                     }
             }
             if (rg == NRG - 1 && has_hi) {
 #pragma unroll
                 for (int c = 0; c < BC; ++c)
-                    if (col0 + c + 1 <= nx) st_async(G0_hi + 8 * (fe(c, BR - 1) - HR * np), z[BR - 1][c], mb_hi);
+                    if (col0 + c + 1 <= nx) st_async(G0_hi + 4 * (fe(c, BR - 1) - HR * np), z[BR - 1][c], mb_hi);
             }
         };
-        auto prol2w = [](const double *Xc, int pc, int i, int j) -> double {   // bilinear, branch-free
-            const double *z2 = Xc + (j >> 1) * pc + (i >> 1);
-            const double wx1 = (i & 1) ? 0.5 : 0.0, wx0 = (i & 1) ? 0.5 : 1.0;
-            const double wy1 = (j & 1) ? 0.5 : 0.0, wy0 = (j & 1) ? 0.5 : 1.0;
-            return fma(wx1 * wy1, z2[pc + 1], fma(wx0 * wy1, z2[pc], fma(wx1 * wy0, z2[1], wx0 * wy0 * z2[0])));
+        auto prol2w = [](const float *Xc, int pc, int i, int j) -> float {   // bilinear, branch-free
+            const float *z2 = Xc + (j >> 1) * pc + (i >> 1);
+            const float wx1 = (i & 1) ? 0.5f : 0.0f, wx0 = (i & 1) ? 0.5f : 1.0f;
+            const float wy1 = (j & 1) ? 0.5f : 0.0f, wy0 = (j & 1) ? 0.5f : 1.0f;
+            return fmaf(wx1 * wy1, z2[pc + 1], fmaf(wx0 * wy1, z2[pc], fmaf(wx1 * wy0, z2[1], wx0 * wy0 * z2[0])));
         };
         // level-1 nodes (I in 1 .. m1-1) of the local rows jl = JA .. JA+NR-1 inside the mesh
         auto for1 = [&](auto ja, auto nr, auto body) {
@@ -555,44 +590,44 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 if (q < U && I < m1 && J >= 1 && J < m1) body(I, jl);
             }
         };
-        using C0 = std::integral_constant<int, 0>;
         using C1 = std::integral_constant<int, 1>;
+        using CM1 = std::integral_constant<int, -1>;
+        using C0 = std::integral_constant<int, 0>;
         using CHR1 = std::integral_constant<int, HR1>;
         using CHR1p1 = std::integral_constant<int, HR1 + 1>;
         using CHR1p2 = std::integral_constant<int, HR1 + 2>;
+        using CHR1p4 = std::integral_constant<int, HR1 + 4>;
         // interior of a replicated level with M cells
         auto forl = [&](auto mc, auto body) {
             constexpr int M = decltype(mc)::value, U = (M - 1) * (M - 1);
-#pragma unroll 1
+#pragma unroll
             for (int k = 0; k < (U + NT - 1) / NT; ++k) {
                 const int q = tid + k * NT, I = q % (M - 1) + 1, J = q / (M - 1) + 1;
                 if (q < U) body(I, J, J * (M + 1) + I);
             }
         };
         // level-1 operator at (I, jl) (diagonal summed in the order of DI1)
-        auto apply1 = [&](const double *Zs, int I, int jl) -> double {
+        auto apply1 = [&](const float *Zs, int I, int jl) -> float {
             const int e = e1(I, jl), el = e1(I - 1, jl), er = e1(I + 1, jl);
-            const double whe = WH1[e], whl = WH1[el], wve = WV1[e], wvd = WV1[e - P1];
+            const float whe = WH1[e], whl = WH1[el], wve = WV1[e], wvd = WV1[e - P1];
             return (whe + whl + wve + wvd) * Zs[e] - whe * Zs[er] - whl * Zs[el] - wve * Zs[e + P1] -
                    wvd * Zs[e - P1];
         };
 
         // ---- CG init: x = 0, r = b, z0 = omega D^-1 b -----------------------------------------------
         double xr[BR][BC], pr[BR][BC], r[BR][BC], s[BR][BC];
-        {
-            double z0[BR][BC];
+        float z0[BR][BC];
 #pragma unroll
-            for (int q = 0; q < BR; ++q)
+        for (int q = 0; q < BR; ++q)
 #pragma unroll
-                for (int c = 0; c < BC; ++c) {
-                    xr[q][c] = pr[q][c] = s[q][c] = 0.0;
-                    const int j = j0 + row0 + q + 1;
-                    r[q][c] = !valid(q, c) ? 0.0 : Bt ? __ldg(Bt + (j - 1) * nx + col0 + c) : (double)j * inv_n3;
-                    z0[q][c] = DI0[fe(c, q)] * r[q][c];
-                }
-            local_publish(G0, z0);
-            send_x1(z0, r);
-        }
+            for (int c = 0; c < BC; ++c) {
+                xr[q][c] = pr[q][c] = s[q][c] = 0.0;
+                const int j = j0 + row0 + q + 1;
+                r[q][c] = !valid(q, c) ? 0.0 : Bt ? __ldg(Bt + (j - 1) * nx + col0 + c) : (double)j * inv_n3;
+                z0[q][c] = di0[q][c] * (float)r[q][c];
+            }
+        publish(G0, z0);
+        send_x1(z0, r);
         double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
         bool conv = false;
         int it = 0;
@@ -601,52 +636,49 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         for (int k = 0;; ++k) {
             pit = cluster_id_x() == 0 && bl == 0 && k == 6;
             CL_MARK(pit, 0);
-            // ======== V(1,1) cycle: uu = M^-1 r ========================================================
+            // ======== V(1,1) cycle in fp32: uu = M^-1 r ==================================================
             __syncthreads();
             xwait(0);                                    // X1: z0 halos, r of the row above
             CL_MARK(pit, 1);
+            float t[BR][BC];                             // fine residual r - A z0 of the own nodes
             {
-                double t[BR][BC], z0[BR][BC];
+                float az[BR][BC];
+                apply32(G0, z0, az);
 #pragma unroll
                 for (int q = 0; q < BR; ++q)
 #pragma unroll
-                    for (int c = 0; c < BC; ++c) z0[q][c] = valid(q, c) ? G0[fe(c, q)] : 0.0;
-                apply_fine(G0, z0, t);
-#pragma unroll
-                for (int q = 0; q < BR; ++q)
-#pragma unroll
-                    for (int c = 0; c < BC; ++c) t[q][c] = r[q][c] - t[q][c];     // fine residual
-                local_publish(G1, t);
+                    for (int c = 0; c < BC; ++c) t[q][c] = valid(q, c) ? (float)r[q][c] - az[q][c] : 0.0f;
+                publish(G1, t);
             }
             if (tid < nx) {                              // the residual of the row above (HR+1)
                 const int i = tid + 1, e = (HR + 1) * np + slot0(i);
-                const double east = WHh[i], west = WHh[i - 1], north = WVh1[i], south = WVh0[i];
-                double a = (east + west + north + south) * G0[e];
-                a = fma(-east, G0[(HR + 1) * np + slot0(i + 1)], a);
-                a = fma(-west, G0[(HR + 1) * np + slot0(i - 1)], a);
-                a = fma(-north, G0[e + np], a);
-                a = fma(-south, G0[e - np], a);
-                G1[e] = j0 + HR + 1 <= nx ? Rh[i] - a : 0.0;
+                const float east = WHh[i], west = WHh[i - 1], north = WVh1[i], south = WVh0[i];
+                float a = (east + west + north + south) * G0[e];
+                a = fmaf(-east, G0[(HR + 1) * np + slot0(i + 1)], a);
+                a = fmaf(-west, G0[(HR + 1) * np + slot0(i - 1)], a);
+                a = fmaf(-north, G0[e + np], a);
+                a = fmaf(-south, G0[e - np], a);
+                G1[e] = j0 + HR + 1 <= nx ? Rh[i] - a : 0.0f;
             }
             __syncthreads();
             CL_MARK(pit, 2);
             for1(C1{}, CHR1{}, [&](int I, int jl) {      // R1 = P^T t, Z1 = omega D1^-1 R1 (own rows)
                 const int f = 2 * jl * np, c = I, l = HE + I - 1, rr = HE + I;
-                const double rv = G1[f + c] + 0.5 * (G1[f + l] + G1[f + rr] + G1[f - np + c] + G1[f + np + c]) +
-                                  0.25 * (G1[f - np + l] + G1[f - np + rr] + G1[f + np + l] + G1[f + np + rr]);
+                const float rv = G1[f + c] + 0.5f * (G1[f + l] + G1[f + rr] + G1[f - np + c] + G1[f + np + c]) +
+                                 0.25f * (G1[f - np + l] + G1[f - np + rr] + G1[f + np + l] + G1[f + np + rr]);
                 const int e = e1(I, jl);
-                const double zv = DI1[e] * rv;
+                const float zv = DI1[e] * rv;
                 R1[e] = rv;
                 Z1[e] = zv;
                 // X2: Z1 rows 1, 2 and R1 row 1 -> rows HR1+1, HR1+2 below; Z1 rows HR1-1, HR1 and R1
                 // row HR1 -> rows -1, 0 above
                 if (jl <= 2 && has_lo) {
-                    st_async(Z1_lo + 8 * e1(I, jl + HR1), zv, mb_lo + 8);
-                    if (jl == 1) st_async(R1_lo + 8 * e1(I, jl + HR1), rv, mb_lo + 8);
+                    st_async(Z1_lo + 4 * e1(I, jl + HR1), zv, mb_lo + 8);
+                    if (jl == 1) st_async(R1_lo + 4 * e1(I, jl + HR1), rv, mb_lo + 8);
                 }
                 if (jl >= HR1 - 1 && has_hi) {
-                    st_async(Z1_hi + 8 * e1(I, jl - HR1), zv, mb_hi + 8);
-                    if (jl == HR1) st_async(R1_hi + 8 * e1(I, jl - HR1), rv, mb_hi + 8);
+                    st_async(Z1_hi + 4 * e1(I, jl - HR1), zv, mb_hi + 8);
+                    if (jl == HR1) st_async(R1_hi + 4 * e1(I, jl - HR1), rv, mb_hi + 8);
                 }
             });
             __syncthreads();
@@ -665,10 +697,10 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     const int q = tid + kk * NT, I = q % (m2 - 1) + 1, jl2 = q / (m2 - 1) + 1, J = J20 + jl2;
                     if (q >= U || J >= m2) continue;
                     const int f = (2 * jl2 + 1) * P1, c = I, l = H1 + I - 1, rr = H1 + I;
-                    const double v = T1[f + c] + 0.5 * (T1[f + l] + T1[f + rr] + T1[f - P1 + c] + T1[f + P1 + c]) +
-                                     0.25 * (T1[f - P1 + l] + T1[f - P1 + rr] + T1[f + P1 + l] + T1[f + P1 + rr]);
+                    const float v = T1[f + c] + 0.5f * (T1[f + l] + T1[f + rr] + T1[f - P1 + c] + T1[f + P1 + c]) +
+                                    0.25f * (T1[f - P1 + l] + T1[f - P1 + rr] + T1[f + P1 + l] + T1[f + P1 + rr]);
 #pragma unroll
-                    for (int kr = 0; kr < CS; ++kr) st_async(mapa(R2a + 8 * (J * P2 + I), kr), v, mapa(mb0 + 16, kr));
+                    for (int kr = 0; kr < CS; ++kr) st_async(mapa(R2a + 4 * (J * P2 + I), kr), v, mapa(mb0 + 16, kr));
                 }
             }
             xwait(2);                                    // X3
@@ -677,21 +709,21 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
             for (int l = 2; l < LK; ++l) {               // down: Z = Dw R, T = R - A Z, restrict
                 const int Pq = L::Pl(l);
-                const double *wh = lv(l, LWH), *wv = lv(l, LWV), *di = lv(l, LDI), *rl = lv(l, LR);
-                double *zl = lv(l, LZ), *tl = lv(l, LT);
+                const float *wh = lc(l, LWH), *wv = lc(l, LWV), *di = lc(l, LDI), *rl = lr(l, LR);
+                float *zl = lr(l, LZ), *tl = lr(l, LT);
                 auto down = [&](int, int, int e) {       // the pre-smoothing from zero in the same pass
-                    const double zc = di[e] * rl[e];
-                    const double az = (wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) * zc -
-                                      wh[e] * (di[e + 1] * rl[e + 1]) - wh[e - 1] * (di[e - 1] * rl[e - 1]) -
-                                      wv[e] * (di[e + Pq] * rl[e + Pq]) - wv[e - Pq] * (di[e - Pq] * rl[e - Pq]);
+                    const float zc = di[e] * rl[e];
+                    const float az = (wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) * zc -
+                                     wh[e] * (di[e + 1] * rl[e + 1]) - wh[e - 1] * (di[e - 1] * rl[e - 1]) -
+                                     wv[e] * (di[e + Pq] * rl[e + Pq]) - wv[e - Pq] * (di[e - Pq] * rl[e - Pq]);
                     zl[e] = zc;
                     tl[e] = rl[e] - az;
                 };
                 auto restr = [&](int I, int J, int ec) {
                     const int f = 2 * J * Pq + 2 * I;
-                    const double v = tl[f] + 0.5 * (tl[f - 1] + tl[f + 1] + tl[f - Pq] + tl[f + Pq]) +
-                                     0.25 * (tl[f - Pq - 1] + tl[f - Pq + 1] + tl[f + Pq - 1] + tl[f + Pq + 1]);
-                    if (l + 1 < LK) lv(l + 1, LR)[ec] = v;
+                    const float v = tl[f] + 0.5f * (tl[f - 1] + tl[f + 1] + tl[f - Pq] + tl[f + Pq]) +
+                                    0.25f * (tl[f - Pq - 1] + tl[f - Pq + 1] + tl[f + Pq - 1] + tl[f + Pq + 1]);
+                    if (l + 1 < LK) lr(l + 1, LR)[ec] = v;
                     else RK[(J - 1) * (mK - 1) + I - 1] = v;
                 };
                 if (l == 2) forl(std::integral_constant<int, L::ml(2)>{}, down);
@@ -705,115 +737,130 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             if (warp < (2 * UK + 31) / 32) {             // SK = K RK (levels 8 and 4 cells)
                 const int h = tid & 1, i = min(tid >> 1, UK - 1);
                 const bool own = tid < 2 * UK;
-                const double *kp = Kt + h * (HK * UK + L::KPAD) + i, *rp = RK + h * HK;
-                double a0 = 0.0, a1 = 0.0, a2 = 0.0, a3 = 0.0;
+                const float *kp = Kt + h * (HK * UK + L::KPAD) + i, *rp = RK + h * HK;
+                float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
 #pragma unroll
                 for (int c = 0; c < HK; c += 4) {
-                    a0 = fma(kp[c * UK], rp[c], a0);
-                    if (c + 1 < HK) a1 = fma(kp[(c + 1) * UK], rp[c + 1], a1);
-                    if (c + 2 < HK) a2 = fma(kp[(c + 2) * UK], rp[c + 2], a2);
-                    if (c + 3 < HK) a3 = fma(kp[(c + 3) * UK], rp[c + 3], a3);
+                    a0 = fmaf(kp[c * UK], rp[c], a0);
+                    if (c + 1 < HK) a1 = fmaf(kp[(c + 1) * UK], rp[c + 1], a1);
+                    if (c + 2 < HK) a2 = fmaf(kp[(c + 2) * UK], rp[c + 2], a2);
+                    if (c + 3 < HK) a3 = fmaf(kp[(c + 3) * UK], rp[c + 3], a3);
                 }
-                double sv = (a0 + a1) + (a2 + a3);
+                float sv = (a0 + a1) + (a2 + a3);
                 sv += __shfl_xor_sync(0xffffffffu, sv, 1);
                 if (own && h == 0) SK[(i / (mK - 1) + 1) * PK + i % (mK - 1) + 1] = sv;
             }
             __syncthreads();
             CL_MARK(pit, 7);
 #pragma unroll
-            for (int l = LK - 1; l >= 2; --l) {          // up: S = smooth(Z + P S_coarse), fused
+            for (int l = LK - 1; l >= 2; --l) {          // up: Zp = Z + P S_coarse; S = smooth(Zp) -> Z
                 const int Pq = L::Pl(l);
-                const double *xc = l + 1 < LK ? lv(l + 1, LT) : SK;
+                const float *xc = l + 1 < LK ? lr(l + 1, LZ) : SK;
                 const int pc = l + 1 < LK ? L::Pl(l + 1) : PK;
-                const double *wh = lv(l, LWH), *wv = lv(l, LWV), *di = lv(l, LDI), *rl = lv(l, LR), *zl = lv(l, LZ);
-                double *sl = lv(l, LT);
-                auto up = [&](int I, int J, int e) {
-                    const double zc = zl[e] + prol2w(xc, pc, I, J), ze = zl[e + 1] + prol2w(xc, pc, I + 1, J);
-                    const double zw = zl[e - 1] + prol2w(xc, pc, I - 1, J), zn = zl[e + Pq] + prol2w(xc, pc, I, J + 1);
-                    const double zs = zl[e - Pq] + prol2w(xc, pc, I, J - 1);
-                    const double we = wh[e], ww = wh[e - 1], wn = wv[e], ws = wv[e - Pq];
-                    const double az = (we + ww + wn + ws) * zc - we * ze - ww * zw - wn * zn - ws * zs;
-                    sl[e] = fma(di[e], rl[e] - az, zc);
+                const float *wh = lc(l, LWH), *wv = lc(l, LWV), *di = lc(l, LDI), *rl = lr(l, LR);
+                float *zl = lr(l, LZ), *zp = lr(l, LT);
+                auto upa = [&](int I, int J, int e) { zp[e] = zl[e] + prol2w(xc, pc, I, J); };
+                auto upb = [&](int, int, int e) {
+                    const float zc = zp[e], we = wh[e], ww = wh[e - 1], wn = wv[e], ws = wv[e - Pq];
+                    const float az = (we + ww + wn + ws) * zc - we * zp[e + 1] - ww * zp[e - 1] - wn * zp[e + Pq] -
+                                     ws * zp[e - Pq];
+                    zl[e] = fmaf(di[e], rl[e] - az, zc);
                 };
-                if (l == 2) forl(std::integral_constant<int, L::ml(2)>{}, up);
-                else forl(std::integral_constant<int, L::ml(LK - 1)>{}, up);
+                if (l == 2) forl(std::integral_constant<int, L::ml(2)>{}, upa);
+                else forl(std::integral_constant<int, L::ml(LK - 1)>{}, upa);
+                __syncthreads();
+                if (l == 2) forl(std::integral_constant<int, L::ml(2)>{}, upb);
+                else forl(std::integral_constant<int, L::ml(LK - 1)>{}, upb);
                 __syncthreads();
             }
             CL_MARK(pit, 8);
-            {   // level 1: S1 = smooth(Z1 + P S2) on the rows 0 .. HR1+1 (own + one halo row each side)
-                const double *S2 = lv(2, LT);
+            {   // level 1: Zp1 = Z1 + P S2 on rows -1 .. HR1+2 (-> T1), S1 = smooth(Zp1) on rows
+                // 0 .. HR1+1 (own + one halo row each side; -> Z1)
+                const float *S2 = lr(2, LZ);
+                for1(CM1{}, CHR1p4{}, [&](int I, int jl) { T1[e1(I, jl)] = Z1[e1(I, jl)] + prol2w(S2, P2, I, J0 + jl); });
+                __syncthreads();
                 for1(C0{}, CHR1p2{}, [&](int I, int jl) {
-                    const int J = J0 + jl, e = e1(I, jl);
-                    const double zc = Z1[e] + prol2w(S2, P2, I, J);
-                    const double ze = Z1[e1(I + 1, jl)] + prol2w(S2, P2, I + 1, J);
-                    const double zw = Z1[e1(I - 1, jl)] + prol2w(S2, P2, I - 1, J);
-                    const double zn = Z1[e + P1] + prol2w(S2, P2, I, J + 1);
-                    const double zs = Z1[e - P1] + prol2w(S2, P2, I, J - 1);
-                    const double whe = WH1[e], whl = WH1[e1(I - 1, jl)], wve = WV1[e], wvd = WV1[e - P1];
-                    const double az = (whe + whl + wve + wvd) * zc - whe * ze - whl * zw - wve * zn - wvd * zs;
-                    S1[e] = fma(DI1[e], R1[e] - az, zc);
+                    const int e = e1(I, jl);
+                    const float zc = T1[e];
+                    const float whe = WH1[e], whl = WH1[e1(I - 1, jl)], wve = WV1[e], wvd = WV1[e - P1];
+                    const float az = (whe + whl + wve + wvd) * zc - whe * T1[e1(I + 1, jl)] - whl * T1[e1(I - 1, jl)] -
+                                     wve * T1[e + P1] - wvd * T1[e - P1];
+                    Z1[e] = fmaf(DI1[e], R1[e] - az, zc);
                 });
                 __syncthreads();
             }
             CL_MARK(pit, 9);
             // level 0: uu = z0 + P S1, post-smoothed (window of S1 as in pcg_mg.cuh)
-            double uu[BR][BC];
+            float uu[BR][BC];
             {
                 constexpr int XW = BC / 2 + 2, YW = BR / 2 + 2;
-                double cw[YW][XW];
+                float cw[YW][XW];
 #pragma unroll
                 for (int yy = 0; yy < YW; ++yy)
 #pragma unroll
                     for (int xx = 0; xx < XW; ++xx) {
                         const int X = lx + xx, Y = (row0 >> 1) + yy;
-                        cw[yy][xx] = (X <= m1 && J0 + Y <= m1) ? S1[(Y + 1) * P1 + col1s(X)] : 0.0;
+                        cw[yy][xx] = (X <= m1 && J0 + Y <= m1) ? Z1[(Y + 1) * P1 + col1s(X)] : 0.0f;
                     }
-                auto pw = [&](int c, int q) -> double {
+                auto pw = [&](int c, int q) -> float {
                     const int fi = 1 + c, fj = 1 + q, xq = fi >> 1, yq = fj >> 1;
                     if (!(fi & 1) && !(fj & 1)) return cw[yq][xq];
-                    if (!(fj & 1)) return 0.5 * (cw[yq][xq] + cw[yq][xq + 1]);
-                    if (!(fi & 1)) return 0.5 * (cw[yq][xq] + cw[yq + 1][xq]);
-                    return 0.25 * (cw[yq][xq] + cw[yq][xq + 1] + cw[yq + 1][xq] + cw[yq + 1][xq + 1]);
+                    if (!(fj & 1)) return 0.5f * (cw[yq][xq] + cw[yq][xq + 1]);
+                    if (!(fi & 1)) return 0.5f * (cw[yq][xq] + cw[yq + 1][xq]);
+                    return 0.25f * (cw[yq][xq] + cw[yq][xq + 1] + cw[yq + 1][xq] + cw[yq + 1][xq + 1]);
                 };
 #pragma unroll
                 for (int q = 0; q < BR; ++q)
 #pragma unroll
                     for (int c = 0; c < BC; ++c) {
-                        const double ec = pw(c, q);
-                        double a = diag(q, c) * ec;
-                        a = fma(-cE[q][c + 1], pw(c + 1, q), a);
-                        a = fma(-cE[q][c], pw(c - 1, q), a);
-                        a = fma(-cN[q + 1][c], pw(c, q + 1), a);
-                        a = fma(-cN[q][c], pw(c, q - 1), a);
-                        // t and z0 of the own nodes are still in G1 / G0
-                        uu[q][c] = valid(q, c) ? fma(DI0[fe(c, q)], G1[fe(c, q)] - a, G0[fe(c, q)] + ec) : 0.0;
+                        const float ec = pw(c, q);
+                        float a = dg32[q][c] * ec;
+                        a = fmaf(-ce[q][c + 1], pw(c + 1, q), a);
+                        a = fmaf(-ce[q][c], pw(c - 1, q), a);
+                        a = fmaf(-cn[q + 1][c], pw(c, q + 1), a);
+                        a = fmaf(-cn[q][c], pw(c, q - 1), a);
+                        uu[q][c] = valid(q, c) ? fmaf(di0[q][c], t[q][c] - a, z0[q][c] + ec) : 0.0f;
                     }
             }
             CL_MARK(pit, 10);
-            // ======== w = A uu, dots, cluster reduction ================================================
-            local_publish(G1, uu);
+            // ======== w = A uu (fp64), dots, cluster reduction ===============================================
+            publish(G1, uu);
             if (rg == 0 && has_lo) {                     // X4: row 1 -> row HR+1 below
 #pragma unroll
                 for (int c = 0; c < BC; ++c)
-                    if (col0 + c + 1 <= nx) st_async(G1_lo + 8 * (fe(c, 0) + HR * np), uu[0][c], mb_lo + 24);
+                    if (col0 + c + 1 <= nx) st_async(G1_lo + 4 * (fe(c, 0) + HR * np), uu[0][c], mb_lo + 24);
             }
             if (rg == NRG - 1 && has_hi) {               // row HR -> row 0 above
 #pragma unroll
                 for (int c = 0; c < BC; ++c)
-                    if (col0 + c + 1 <= nx) st_async(G1_hi + 8 * (fe(c, BR - 1) - HR * np), uu[BR - 1][c], mb_hi + 24);
+                    if (col0 + c + 1 <= nx) st_async(G1_hi + 4 * (fe(c, BR - 1) - HR * np), uu[BR - 1][c], mb_hi + 24);
             }
             __syncthreads();
             xwait(3);                                    // X4
             CL_MARK(pit, 11);
             double w[BR][BC];
-            apply_fine(G1, uu, w);
+#pragma unroll
+            for (int q = 0; q < BR; ++q)
+#pragma unroll
+                for (int c = 0; c < BC; ++c) {
+                    const double vl = c > 0 ? (double)uu[q][c - 1] : (double)G1[fe(c - 1, q)];
+                    const double vr = c + 1 < BC ? (double)uu[q][c + 1] : (double)G1[fe(c + 1, q)];
+                    const double vd = q > 0 ? (double)uu[q - 1][c] : (double)G1[fe(c, q - 1)];
+                    const double vu = q + 1 < BR ? (double)uu[q + 1][c] : (double)G1[fe(c, q + 1)];
+                    double a = dg64[q][c] * (double)uu[q][c];
+                    a = fma(-cE[q][c + 1], vr, a);
+                    a = fma(-cE[q][c], vl, a);
+                    a = fma(-cN[q + 1][c], vu, a);
+                    a = fma(-cN[q][c], vd, a);
+                    w[q][c] = valid(q, c) ? a : 0.0;
+                }
             double acc[3] = {0.0, 0.0, 0.0};
 #pragma unroll
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    acc[0] = fma(r[q][c], uu[q][c], acc[0]);
-                    acc[1] = fma(w[q][c], uu[q][c], acc[1]);
+                    acc[0] = fma(r[q][c], (double)uu[q][c], acc[0]);
+                    acc[1] = fma(w[q][c], (double)uu[q][c], acc[1]);
                     acc[2] = fma(r[q][c], r[q][c], acc[2]);
                 }
 #pragma unroll
@@ -858,21 +905,15 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    const double pn = fma(beta, pr[q][c], uu[q][c]);
+                    const double pn = fma(beta, pr[q][c], (double)uu[q][c]);
                     pr[q][c] = pn;
                     s[q][c] = fma(beta, s[q][c], w[q][c]);
                     xr[q][c] = fma(alpha, pn, xr[q][c]);
                     r[q][c] = fma(-alpha, s[q][c], r[q][c]);
+                    z0[q][c] = di0[q][c] * (float)r[q][c];
                 }
-            {
-                double z0[BR][BC];
-#pragma unroll
-                for (int q = 0; q < BR; ++q)
-#pragma unroll
-                    for (int c = 0; c < BC; ++c) z0[q][c] = DI0[fe(c, q)] * r[q][c];
-                local_publish(G0, z0);
-                send_x1(z0, r);
-            }
+            publish(G0, z0);
+            send_x1(z0, r);
             CL_MARK(pit, 13);
             ++it;
         }
@@ -886,7 +927,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             if (relres) relres[bl] = sqrt(rho / bb);
             if (noconv && !conv) atomicAdd(noconv, 1);
         }
-        // the next sample's coefficient table overwrites DI0 .. G1, which only this CTA reads now
+        // the next sample's staging / coefficient table overwrite the union, which only this CTA reads now
         __syncthreads();
     }
     cluster_barrier();                                   // no CTA leaves while others may address it

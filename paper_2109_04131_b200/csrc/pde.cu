@@ -280,13 +280,13 @@ usfft_status launch_pcg_mgg_n(usfft_ctx *c, const LatParams &P, const PdeParams 
 
 // one thread-block cluster of CS CTAs per sample (pcg_cl.cuh), as many clusters as fit at once,
 // each looping over samples
-template <int NN, int CS, int BR, int MINB>
+template <int NN, int CS, int MINB>
 usfft_status launch_pcg_cl(usfft_ctx *c, const LatParams &P, const PdeParams &Q, const double *nodes,
                            int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
                            int32_t *noconv, const double *S, const double *Bt) {
-    using C = ClC<NN, CS, BR>;
-    const size_t dyn = sizeof(double) * (size_t)C::doubles();
-    auto kern = k_pcg_cl<NN, CS, BR, MINB>;
+    using C = ClC<NN, CS>;
+    const size_t dyn = C::bytes();
+    auto kern = k_pcg_cl<NN, CS, MINB>;
     if (usfft_status s = kernel_fit(c, kern, C::NT, dyn, nullptr)) return s;
     cudaLaunchAttribute attr[1];
     attr[0].id = cudaLaunchAttributeClusterDimension;
@@ -437,9 +437,9 @@ extern "C" usfft_status usfft_sample_pde(usfft_ctx *c, const usfft_pde_desc *pde
     else if (pde->precond == 1 && n == 16)
         s = launch_pcg_mg<16, 2, 4, 8, 1, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 128)
-        s = launch_pcg_cl<128, 8, 4, 1>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+        s = launch_pcg_cl<128, 8, 1>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 64)
-        s = launch_pcg_cl<64, 4, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
+        s = launch_pcg_cl<64, 4, 2>(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1 && n == 8)
         s = launch_pcg_mgg(c, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt);
     else if (pde->precond == 1)
