@@ -59,7 +59,10 @@ struct ClC {
     static constexpr int HR = NN / CS;                       // fine rows per CTA
     static constexpr int BC = 2, BR = 2, LX = n / 2, NRG = HR / BR, NT = LX * NRG, NWARP = NT / 32;
     static constexpr int FRW = HR + 3, FR = FRW * np;        // fine grid rows 0 .. HR+2 (local)
-    static constexpr int m1 = n / 2, P1 = m1 + 1, H1 = m1 / 2 + 1, HR1 = HR / 2, HR2 = HR / 4;
+    // level-1 split rows: even columns at slots 0 .. m1/2, odd columns from slot H1 = 48 (16 banks
+    // after the even run, so an instruction touching both parities is conflict-free in fp32)
+    static constexpr int m1 = n / 2, H1E = m1 / 2 + 1, H1 = 48, P1 = H1 + m1 / 2, HR1 = HR / 2, HR2 = HR / 4;
+    static_assert(H1 >= H1E && H1 % 32 == 16, "level-1 row layout");
     static constexpr int L1R = HR1 + 4, F1 = L1R * P1;       // level-1 rows jl = -1 .. HR1+2 (lr = jl+1)
     static constexpr int LK = NN == 64 ? 3 : NN == 128 ? 4 : -1;
     static_assert(LK > 0, "cluster multigrid compiled for n = 64, 128");
@@ -72,6 +75,9 @@ struct ClC {
     static constexpr int KPAD = (16 - (HK * UK) % 32 + 32) % 32;   // the two K halves 16 banks apart
     static constexpr int ATR = HR + 6;                       // coefficient-table cell rows j0-2 .. j0+HR+3
     static constexpr int JC = 8;                             // psi factors staged JC terms at a time
+    static constexpr int CPT = NT / n, KJ = (((ATR + CPT - 1) / CPT) + 1) & ~1, YP = CPT * KJ;
+    // resident psi slice (fp64, after the partials): X[j][2n] (lower, upper abscissae), Y[j][2][YP]
+    __host__ __device__ static constexpr size_t psi_bytes(int d) { return 8 * (size_t)d * (2 * n + 2 * YP); }
     // ---- shared memory, in 4-byte units ----
     // persistent (written by the setup, read by every iteration), fp32
     static constexpr int oWH1 = 0, oWV1 = F1, oDI1 = 2 * F1;
@@ -99,7 +105,9 @@ struct ClC {
     static constexpr int USTG = 2 * (JC * 2 * n + JC * 2 * ATR);
     static constexpr int USZ = URUN > UAT ? (URUN > USTG ? URUN : USTG) : (UAT > USTG ? UAT : USTG);
     static constexpr int oRedF = (oU + USZ + 3) & ~3;        // fp64 [2][CS][4] cluster partials, [4][NWARP]
-    __host__ __device__ static constexpr size_t bytes() { return 4 * (size_t)oRedF + 8 * (size_t)(8 * CS + 4 * NWARP); }
+    // then fp64: the cluster partials [2][CS][4] and CTA partials [4][NWARP], the CG iterate x
+    // and s = A p [BR*BC][NT] each (thread-major: touched once per iteration, so outside the registers)
+    __host__ __device__ static constexpr size_t bytes() { return 4 * (size_t)oRedF + 8 * (size_t)(8 * CS + 4 * NWARP + 2 * BR * BC * NT); }
     // setup: the coarse-level triangle coefficients (levels 2 .. LK+1, lower then upper plane)
     __host__ __device__ static constexpr int ctoff(int l) {
         int o = 0;
@@ -173,14 +181,14 @@ __global__ void __launch_bounds__(ClC<NN, CS>::NT, MINB)
 k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
          int64_t nb, double *__restrict__ u, int64_t ldu, int32_t *__restrict__ iters,
          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
-         const double *__restrict__ Bt) {
+         const double *__restrict__ Bt, int pd) {
     using L = ClC<NN, CS>;
     namespace cg = cooperative_groups;
     constexpr int n = NN, nx = L::nx, np = L::np, HE = L::HE, HR = L::HR, BC = L::BC, BR = L::BR;
     constexpr int LX = L::LX, NRG = L::NRG, NT = L::NT, NWARP = L::NWARP, W = 3 * n + 1;
     constexpr int m1 = L::m1, P1 = L::P1, H1 = L::H1, HR1 = L::HR1, HR2 = L::HR2, LK = L::LK;
     constexpr int mK = L::mK, PK = L::PK, NK = L::NK, UK = L::UK, HK = L::HK;
-    constexpr int mE = L::mE, PE = L::PE, UE = L::UE, ATR = L::ATR, JC = L::JC;
+    constexpr int mE = L::mE, PE = L::PE, UE = L::UE, ATR = L::ATR, JC = L::JC, H1E = L::H1E;
     constexpr int m2 = L::ml(2), P2 = L::Pl(2);
     constexpr float om = 0.8f;                           // kMgOmega
     extern __shared__ __align__(16) float sf[];
@@ -249,9 +257,25 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     auto col1s = [](int i) -> int { return (i & 1) ? H1 + (i >> 1) : (i >> 1); };
     auto e1 = [&](int I, int jl) -> int { return (jl + 1) * P1 + col1s(I); };      // level-1 row jl
 
+    // the psi factors of this CTA's strip do not depend on the sample: with pd = d they are loaded
+    // once per CTA (X at the 2n abscissae, Y at the strip's ATR ordinates, both planes)
+    constexpr int YP = L::YP, CPT = L::CPT, KJ = L::KJ;
+    double *Xg = cred + 8 * CS + 4 * NWARP;                                     // x, [BR*BC][NT]
+    double *Sg = Xg + BR * BC * NT;                                             // s, [BR*BC][NT]
+    double *XP = Sg + BR * BC * NT, *YPs = XP + (size_t)pd * 2 * n;
+    for (int e = tid; e < pd * 2 * n; e += NT) {
+        const int j = e / (2 * n), c = e - j * 2 * n, up = c >= n, cc = up ? c - n : c;
+        XP[e] = __ldg(S + j * W + 3 * cc + (up ? 1 : 2));
+    }
+    for (int e = tid; e < pd * 2 * YP; e += NT) {
+        const int j = e / (2 * YP), c = e - j * 2 * YP, up = c >= YP, rl = up ? c - YP : c;
+        const int cj = min(max(j0 - 2 + rl, 0), n - 1);
+        YPs[e] = rl < ATR ? __ldg(Sy0 + j * W + 3 * cj + (up ? 2 : 1)) : 0.0;
+    }
+
     for (int64_t bl = cluster_id_x(); bl < nb; bl += cluster_count_x()) {
         const int64_t b = b0 + bl;
-        const bool pset = cluster_id_x() == 0 && bl == 0;
+        const bool pset = cluster_id_x() == 0 && bl == cluster_count_x();   // probe: the 2nd sample (warm L2)
         (void)pset;
         CL_MARK(pset, 20);
         // ---- K3: coefficients of the triangles of cell rows j0-2 .. j0+HR+3 --------------------
@@ -260,12 +284,40 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
         __syncthreads();
-        {   // aT[plane][cj - (j0-2)][ci] = sum_j amp_j theta_j X_j Y_j: thread = (column, row set); the
+        if (pd) {   // aT from the resident slice: thread = (column, KJ consecutive rows), Y pairs as 16-byte loads
+            const int ci = tid % n, rs = tid / n;
+            double slo[KJ], sup[KJ];
+#pragma unroll
+            for (int k = 0; k < KJ; ++k) slo[k] = sup[k] = 0.0;
+#pragma unroll 2
+            for (int j = 0; j < pd; ++j) {
+                const double am = th_amp[j];
+                const double tlo = am * XP[j * 2 * n + ci], tup = am * XP[j * 2 * n + n + ci];
+                const double2 *yl = reinterpret_cast<const double2 *>(YPs + j * 2 * YP + rs * KJ);
+                const double2 *yu = reinterpret_cast<const double2 *>(YPs + j * 2 * YP + YP + rs * KJ);
+#pragma unroll
+                for (int k = 0; k < KJ / 2; ++k) {
+                    const double2 a = yl[k], b2 = yu[k];
+                    slo[2 * k] = fma(tlo, a.x, slo[2 * k]);
+                    slo[2 * k + 1] = fma(tlo, a.y, slo[2 * k + 1]);
+                    sup[2 * k] = fma(tup, b2.x, sup[2 * k]);
+                    sup[2 * k + 1] = fma(tup, b2.y, sup[2 * k + 1]);
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < KJ; ++k) {
+                const int rl = rs * KJ + k, cj = j0 - 2 + rl;
+                if (rl < ATR && cj >= 0 && cj < n) {
+                    aT[rl * n + ci] = Q.form == 0 ? 1.0 + slo[k] : exp(slo[k]);              // lower
+                    aT[(ATR + rl) * n + ci] = Q.form == 0 ? 1.0 + sup[k] : exp(sup[k]);      // upper
+                }
+            }
+        } else {   // aT[plane][cj - (j0-2)][ci] = sum_j amp_j theta_j X_j Y_j: thread = (column, row set); the
             // factors amp_j theta_j X_j at the 2n abscissae and Y_j at the strip's 2 ATR ordinates are
             // staged JC terms at a time, all loads of a chunk issued before its first store
             constexpr int SX = JC * 2 * n, SY = JC * 2 * ATR;
             constexpr int XPT = (SX + NT - 1) / NT, YPT = (SY + NT - 1) / NT;
-            constexpr int CPT = NT / n, KJ = (ATR + CPT - 1) / CPT;
+            constexpr int KJ = (ATR + CPT - 1) / CPT;
             double *Xs = reinterpret_cast<double *>(sf + L::oU), *Ys = Xs + SX;
             const int ci = tid % n, r0 = tid / n;
             double slo[KJ], sup[KJ];
@@ -345,14 +397,12 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 cn[q][c] = (float)cN[q][c];
             }
         float di0[BR][BC], dg32[BR][BC];                 // omega D^-1 and D of the own fine nodes
-        double dg64[BR][BC];
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
-                dg64[q][c] = cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c];
                 dg32[q][c] = ce[q][c + 1] + ce[q][c] + cn[q + 1][c] + cn[q][c];
-                di0[q][c] = valid(q, c) ? (float)(kMgOmega * rcp_pos(dg64[q][c])) : 0.0f;
+                di0[q][c] = valid(q, c) ? (float)(kMgOmega * rcp_pos(cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c])) : 0.0f;
             }
         for (int i = tid; i <= n; i += NT) {             // couplings of the halo row above (HR+1)
             const int jh = j0 + HR + 1;
@@ -361,7 +411,9 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             WVh1[i] = (i >= 1 && i <= nx && jh <= nx) ? (float)(0.5 * (fcl(i, jh, 1, 0) + fcl(i - 1, jh, 0, 0))) : 0.0f;
         }
         for (int e = tid; e < L::F1; e += NT) {           // level-1 couplings, rows jl = -1 .. HR1+1
-            const int lrw = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lrw - 1, J = J0 + jl;
+            const int lrw = e / P1, s = e % P1, I = s < H1E ? 2 * s : s >= H1 ? 2 * (s - H1) + 1 : -1;
+            const int jl = lrw - 1, J = J0 + jl;
+            if (I < 0) continue;                         // gap between the even and odd runs
             WH1[e] = (jl >= 0 && jl <= HR1 + 1 && I < m1 && J >= 1 && J < m1)
                          ? (float)(0.5 * (fcl(I, J, 0, 1) + fcl(I, J - 1, 1, 1))) : 0.0f;
             WV1[e] = (jl <= HR1 + 1 && J >= 0 && J < m1 && I >= 1 && I < m1)
@@ -426,7 +478,8 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         // ---- diagonals, zeroed grids, the dense maps -------------------------------------------
         for (int e = tid; e < L::URUN; e += NT) sf[L::oU + e] = 0.0f;      // every runtime grid
         for (int e = tid; e < L::F1; e += NT) {           // level-1 omega D^-1 (rows 0 .. HR1+1)
-            const int lrw = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1, jl = lrw - 1, J = J0 + jl;
+            const int lrw = e / P1, s = e % P1, I = s < H1E ? 2 * s : s >= H1 ? 2 * (s - H1) + 1 : -1;
+            const int jl = lrw - 1, J = J0 + jl;
             const bool in = I >= 1 && I < m1 && J >= 1 && J < m1 && jl >= 0 && jl <= HR1 + 1;
             const float dv = in ? WH1[e] + WH1[e1(I - 1, jl)] + WV1[e] + WV1[e - P1] : 1.0f;
             DI1[e] = in ? om / dv : 0.0f;
@@ -615,13 +668,13 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         };
 
         // ---- CG init: x = 0, r = b, z0 = omega D^-1 b -----------------------------------------------
-        double xr[BR][BC], pr[BR][BC], r[BR][BC], s[BR][BC];
+        double pr[BR][BC], r[BR][BC];
         float z0[BR][BC];
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
-                xr[q][c] = pr[q][c] = s[q][c] = 0.0;
+                Xg[(q * BC + c) * NT + tid] = Sg[(q * BC + c) * NT + tid] = pr[q][c] = 0.0;
                 const int j = j0 + row0 + q + 1;
                 r[q][c] = !valid(q, c) ? 0.0 : Bt ? __ldg(Bt + (j - 1) * nx + col0 + c) : (double)j * inv_n3;
                 z0[q][c] = di0[q][c] * (float)r[q][c];
@@ -634,7 +687,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         bool pit = false;                                // probe this CG iteration
         (void)pit;
         for (int k = 0;; ++k) {
-            pit = cluster_id_x() == 0 && bl == 0 && k == 6;
+            pit = pset && k == 6;
             CL_MARK(pit, 0);
             // ======== V(1,1) cycle in fp32: uu = M^-1 r ==================================================
             __syncthreads();
@@ -847,7 +900,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     const double vr = c + 1 < BC ? (double)uu[q][c + 1] : (double)G1[fe(c + 1, q)];
                     const double vd = q > 0 ? (double)uu[q - 1][c] : (double)G1[fe(c, q - 1)];
                     const double vu = q + 1 < BR ? (double)uu[q + 1][c] : (double)G1[fe(c, q + 1)];
-                    double a = dg64[q][c] * (double)uu[q][c];
+                    double a = (cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c]) * (double)uu[q][c];
                     a = fma(-cE[q][c + 1], vr, a);
                     a = fma(-cE[q][c], vl, a);
                     a = fma(-cN[q + 1][c], vu, a);
@@ -907,9 +960,10 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int c = 0; c < BC; ++c) {
                     const double pn = fma(beta, pr[q][c], (double)uu[q][c]);
                     pr[q][c] = pn;
-                    s[q][c] = fma(beta, s[q][c], w[q][c]);
-                    xr[q][c] = fma(alpha, pn, xr[q][c]);
-                    r[q][c] = fma(-alpha, s[q][c], r[q][c]);
+                    const double sn = fma(beta, Sg[(q * BC + c) * NT + tid], w[q][c]);
+                    Sg[(q * BC + c) * NT + tid] = sn;
+                    Xg[(q * BC + c) * NT + tid] = fma(alpha, pn, Xg[(q * BC + c) * NT + tid]);
+                    r[q][c] = fma(-alpha, sn, r[q][c]);
                     z0[q][c] = di0[q][c] * (float)r[q][c];
                 }
             publish(G0, z0);
@@ -921,7 +975,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c)
-                if (valid(q, c)) u[(int64_t)((j0 + row0 + q) * nx + col0 + c) * ldu + bl] = xr[q][c];
+                if (valid(q, c)) u[(int64_t)((j0 + row0 + q) * nx + col0 + c) * ldu + bl] = Xg[(q * BC + c) * NT + tid];
         if (tid == 0 && rank == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rho / bb);

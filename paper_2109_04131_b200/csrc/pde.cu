@@ -285,7 +285,9 @@ usfft_status launch_pcg_cl(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
                            int64_t b0, int64_t nb, double *u, int64_t ldu, int32_t *iters, double *relres,
                            int32_t *noconv, const double *S, const double *Bt) {
     using C = ClC<NN, CS>;
-    const size_t dyn = C::bytes();
+    // the psi factors of each CTA's strip resident in shared memory when they fit (pd = d)
+    const int pd = C::bytes() + C::psi_bytes(Q.d) + 1024 <= c->smem_optin ? Q.d : 0;
+    const size_t dyn = C::bytes() + (pd ? C::psi_bytes(pd) : 0);
     auto kern = k_pcg_cl<NN, CS, MINB>;
     if (usfft_status s = kernel_fit(c, kern, C::NT, dyn, nullptr)) return s;
     cudaLaunchAttribute attr[1];
@@ -311,7 +313,7 @@ usfft_status launch_pcg_cl(usfft_ctx *c, const LatParams &P, const PdeParams &Q,
     int64_t ncl = it->second;
     if (ncl > nb) ncl = nb;
     cfg.gridDim = dim3((unsigned)(ncl * CS));
-    USFFT_CUDA(c, cudaLaunchKernelEx(&cfg, kern, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt));
+    USFFT_CUDA(c, cudaLaunchKernelEx(&cfg, kern, P, Q, nodes, b0, nb, u, ldu, iters, relres, noconv, S, Bt, pd));
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
