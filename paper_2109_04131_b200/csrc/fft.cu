@@ -181,6 +181,7 @@ k_kappa_grouped(const double2 *__restrict__ F, const int32_t *__restrict__ bins,
 #include "rader.cuh"
 #include "rader_t.cuh"
 #include "fft400.cuh"
+#include "fft_r.cuh"
 
 using namespace usfft;
 
@@ -214,6 +215,23 @@ usfft_status launch_rader_tp(usfft_ctx *c, const double *u, const SlabParams &S,
     const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
     if (grid > resident) grid = resident;                 // persistent: each group loops over pairs
     kern<<<(unsigned)grid, WPR * 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
+}
+
+template <int N, int GROUP, int NPAIR, int MINB, int... Rs>
+usfft_status launch_rader_r(usfft_ctx *c, const double *u, const SlabParams &S, int64_t G_loc,
+                            int32_t L, const RaderArgs &A, double2 *F) {
+    const int64_t rows = G_loc * L, pairs = G_loc * ((L + 1) / 2);
+    constexpr int R0 = fr::First<Rs...>::value, MH = (N + 1) / 2 + 1, NB = 2 * MH > N + R0 ? 2 * MH : N + R0;
+    const size_t smem = sizeof(double2) * (size_t)NB * NPAIR;
+    auto kern = k_fft_rader_r<N, GROUP, NPAIR, MINB, Rs...>;
+    int per_sm = 0;
+    if (usfft_status s = kernel_fit(c, kern, GROUP * NPAIR, smem, &per_sm)) return s;
+    int64_t grid = (pairs + NPAIR - 1) / NPAIR;
+    const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
+    if (grid > resident) grid = resident;                 // persistent: each CTA loops over pairs
+    kern<<<(unsigned)grid, GROUP * NPAIR, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
     USFFT_CHECK_LAUNCH(c);
     return USFFT_OK;
 }
@@ -425,9 +443,9 @@ extern "C" usfft_status usfft_lattice_fft(usfft_ctx *c, const usfft_lattice_desc
         // the lattice sizes of the BASELINE configs (Z2) have compile-time plans; other
         // Rader-able M take the runtime-plan kernel
         if (R.N == 96) s = launch_rader_t<96, 1, 4>(c, u, S, G_loc, L, A, Fo);
-        else if (R.N == 400) s = launch_fft400(c, u, S, G_loc, L, A, Fo, true);
+        else if (R.N == 400) s = launch_rader_r<400, 20, 8, 3, 20, 20>(c, u, S, G_loc, L, A, Fo);
         else if (R.N == 2016) s = launch_rader_tp<2016, 4, 1>(c, u, S, G_loc, L, A, Fo);
-        else if (R.N == 4000) s = launch_rader_tp<4000, 8, 1>(c, u, S, G_loc, L, A, Fo);
+        else if (R.N == 4000) s = launch_rader_r<4000, 200, 1, 2, 20, 20, 10>(c, u, S, G_loc, L, A, Fo);
         else {
             if (usfft_status s2 = kernel_fit(c, k_fft_rader, 0, smem_r, nullptr)) return s2;
             const int threads = M <= 512 ? 128 : 256;

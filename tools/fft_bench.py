@@ -33,7 +33,7 @@ def main():
             ts.append(e0.elapsed_time(e1))
         ms = float(np.median(ts))
         byt = 8 * G * L * M + 16 * G * L * (M // 2 + 1)
-        out.append({"G": G, "M": M, "L": L, "ms": ms, "GBps": byt / ms / 1e6, "frac_hbm": byt / ms / 1e6 / 6540.8})
+        out.append({"G": G, "M": M, "L": L, "ms": ms, "GBps": byt / ms / 1e6, "frac_hbm": byt / ms / 1e6 / 6550.7})
         print(json.dumps(out[-1]), flush=True)
 
 
