@@ -43,20 +43,24 @@ def mg_flops_per_iter(n: int) -> int:
     return 51 * u0 + 38 * u1 + 10 * u2 + 2 * u2 * u2
 
 
-def cl_flops_per_iter(n: int) -> int:
+def cl_flops_per_iter(n: int, split: bool = False):
     """Algorithmic flops of one CG iteration of the cluster multigrid kernel (k_pcg_cl, n = 64,
-    128), phase by phase: per fine node 47 (p update 2, A p + p.q 11, x / r / z0
-    updates + r.r 7, residual 10, prolongation 3, post-smoothing 12, r.u 2); per node of every
+    128), phase by phase: per fine node 47, of them 22 in fp64 (the CG: p update 2,
+    w = A u + (w,u) 11, x / r / s updates + (r,r) 7, (r,u) 2) and 25 in fp32 (the fine part of the
+    V-cycle: z0 and the residual 10, prolongation 3, post-smoothing 12); per node of every
     smoothed coarse level down to 16 cells per side 37 (residual 10, restriction 12,
     prolongation 3, post-smoothing 12); the restriction to the 8-cell level (12 per node) and the
-    dense map K of the 8- and 4-cell levels (2 x 49^2).  Redundant work (the coarse levels are
-    replicated in every CTA of a cluster) and the per-sample setup are not counted."""
+    dense map K of the 8- and 4-cell levels (2 x 49^2), all fp32 (Z32).  Redundant work (the
+    coarse levels are replicated in every CTA of a cluster) and the per-sample setup are not
+    counted.  split=True returns (fp64 flops, fp32 flops)."""
     u = []
     m = n
     while m >= 8:
         u.append((m - 1) ** 2)
         m //= 2
-    return 47 * u[0] + sum(37 * v for v in u[1:-1]) + 12 * u[-1] + 2 * u[-1] * u[-1]
+    f64 = 22 * u[0]
+    f32 = 25 * u[0] + sum(37 * v for v in u[1:-1]) + 12 * u[-1] + 2 * u[-1] * u[-1]
+    return (f64, f32) if split else f64 + f32
 
 
 SURVEY_FLOPS_PER_NODE_ITER = 20   # SURVEY §8(d): on-chip PCG unit, ~20 fp64 flops per node-iteration
@@ -76,6 +80,7 @@ def mgg_flops_per_iter(n: int) -> int:
 
 
 FP64_FMA_PER_CLK_PER_SM = 64  # B200 fp64 datapath: 37 TF at 1.965 GHz x 148 SMs
+FP32_FMA_PER_CLK_PER_SM = 128  # B200 fp32 datapath: 74 TF at 1.965 GHz x 148 SMs
 
 
 def ncu_traffic(kernel_prefix: str):
@@ -317,7 +322,12 @@ def run_ours(args):
             fpi = FLOPS_PER_NODE_ITER * G
         flops = fpi * iters_all
         fp64_peak = 148 * FP64_FMA_PER_CLK_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
-        ach = flops / (pde_ms / 1e3) / 1e12 / world if pde_ms > 0 else 0.0
+        fp32_peak = 148 * FP32_FMA_PER_CLK_PER_SM * 2 * pk["sm_max_mhz"] * 1e6 / 1e12
+        # k_pcg_cl runs its V-cycle in fp32 (Z32): fp64-equivalent flops = F64 + F32 x (P64 / P32),
+        # so achieved / fp64 peak is the share of the kernel time the ALU roofline needs
+        f64, f32 = cl_flops_per_iter(n_mesh, split=True) if kname == "k_pcg_cl" else (fpi, 0)
+        flops_eq = (f64 + f32 * fp64_peak / fp32_peak) * iters_all
+        ach = flops_eq / (pde_ms / 1e3) / 1e12 / world if pde_ms > 0 else 0.0
         fft_ms = phase.get("fft", 0.0)
         Mh = P.M // 2 + 1
         fft_bytes = G * P.L * P.M * 8 + G * P.L * Mh * 16
@@ -337,11 +347,16 @@ def run_ours(args):
                          "traffic_source": (ncu_traffic(kname) or {}).get("source"),
                          "peak_source": "derived: 148 SM x 64 fp64 FMA/clk x 2 x sm_max_mhz",
                          "flops_per_sample_iter": fpi, "precond": "mg" if mg else "jacobi",
+                         "fp64_flops_per_sample_iter": f64, "fp32_flops_per_sample_iter": f32,
+                         "fp32_peak": fp32_peak,
+                         "achieved_def": "(F64 + F32 x P64/P32) / PDE time; frac = achieved / P64",
                          "frac_survey_unit": (SURVEY_FLOPS_PER_NODE_ITER * G * iters_all / (pde_ms / 1e3) / 1e12
                                               / world / fp64_peak) if pde_ms > 0 and fp64_peak else None,
                          "survey_unit": "20 fp64 flops per fine node and CG iteration (SURVEY §8(d))"},
-            "fft": {"kernel": ("k_fft400 (Rader, register four-step 20 x 20)" if P.M == 401 else
-                               "k_fft_rader_t (Rader/Stockham)") + " + k_kappa_grouped", "ms_per_step": fft_ms,
+            "fft": {"kernel": ("k_fft_rader_r (Rader on row pairs, register-radix in-place passes)"
+                               if P.M in (401, 4001) else "k_fft_rader_t (Rader/Stockham)") + " + k_kappa_grouped",
+                    "bytes_def": "8 G L M read + 16 G L (M/2+1) written (the FFT's algorithmic bytes) / fft phase time",
+                    "ms_per_step": fft_ms,
                     "achieved_gbs": fft_bytes / (fft_ms / 1e3) / 1e9 if fft_ms else None,
                     "hbm_peak_gbs": pk["hbm_gbs"],
                     "frac": (fft_bytes / (fft_ms / 1e3) / 1e9) / pk["hbm_gbs"] if fft_ms else None},

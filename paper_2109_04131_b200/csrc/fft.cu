@@ -236,23 +236,6 @@ usfft_status launch_rader_r(usfft_ctx *c, const double *u, const SlabParams &S, 
     return USFFT_OK;
 }
 
-usfft_status launch_fft400(usfft_ctx *c, const double *u, const SlabParams &S, int64_t G_loc,
-                           int32_t L, const RaderArgs &A, double2 *F, bool paired) {
-    constexpr int RPC = 4;
-    const int64_t rows = G_loc * L;
-    const int64_t units = paired ? G_loc * ((L + 1) / 2) : rows;   // per-node lattice pairs or rows
-    const size_t smem = sizeof(double2) * (size_t)((paired ? 402 : 201) + 20 * 21) * RPC;
-    auto kern = paired ? k_fft400p<RPC> : k_fft400<RPC>;
-    int per_sm = 0;
-    if (usfft_status s = kernel_fit(c, kern, 32 * RPC, smem, &per_sm)) return s;
-    int64_t grid = (units + RPC - 1) / RPC;
-    const int64_t resident = (int64_t)(per_sm > 0 ? per_sm : 1) * c->sm_count;
-    if (grid > resident) grid = resident;                 // persistent: each warp loops over rows
-    kern<<<(unsigned)grid, 32 * RPC, smem, c->stream>>>(u, S, G_loc, L, A, F, rows);
-    USFFT_CHECK_LAUNCH(c);
-    return USFFT_OK;
-}
-
 bool is_prime64(int64_t n) {
     if (n < 2) return false;
     if (n % 2 == 0) return n == 2;
