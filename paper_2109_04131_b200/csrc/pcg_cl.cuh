@@ -105,6 +105,7 @@ struct ClC {
     static constexpr int USTG = 2 * (JC * 2 * n + JC * 2 * ATR);
     static constexpr int USZ = URUN > UAT ? (URUN > USTG ? URUN : USTG) : (UAT > USTG ? UAT : USTG);
     static constexpr int oRedF = (oU + USZ + 3) & ~3;        // fp64 [2][CS][4] cluster partials, [4][NWARP]
+                                                             // (slot 3: the early (r,r) check, X6)
     // then fp64: the cluster partials [2][CS][4] and CTA partials [4][NWARP], the CG iterate x
     // and s = A p [BR*BC][NT] each (thread-major: touched once per iteration, so outside the registers)
     __host__ __device__ static constexpr size_t bytes() { return 4 * (size_t)oRedF + 8 * (size_t)(8 * CS + 4 * NWARP + 2 * BR * BC * NT); }
@@ -193,7 +194,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr float om = 0.8f;                           // kMgOmega
     extern __shared__ __align__(16) float sf[];
     __shared__ double th_amp[kMaxD];
-    __shared__ alignas(8) unsigned long long mbar[5];
+    __shared__ alignas(8) unsigned long long mbar[6];
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster_rank();
     const bool has_lo = rank > 0, has_hi = rank < CS - 1;
@@ -221,15 +222,15 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 
     // ---- exchanges: mbarriers, expected bytes, peer addresses -----------------------------------
     const uint32_t mb0 = smem_addr(&mbar[0]);
-    const uint32_t xb[5] = {(uint32_t)(4 * nx * ((has_hi ? 3 : 0) + (has_lo ? 1 : 0))),
+    const uint32_t xb[6] = {(uint32_t)(4 * nx * ((has_hi ? 3 : 0) + (has_lo ? 1 : 0))),
                             (uint32_t)(4 * (m1 - 1) * ((has_hi ? 3 : 0) + (has_lo ? 3 : 0))),
                             (uint32_t)(4 * (m2 - 1) * (m2 - 1)),
                             (uint32_t)(4 * nx * ((has_hi ? 1 : 0) + (has_lo ? 1 : 0))),
-                            (uint32_t)(8 * 3 * CS)};
+                            (uint32_t)(8 * 3 * CS), (uint32_t)(8 * CS)};
     if (tid == 0) {
-        for (int k = 0; k < 5; ++k) mbar_init(mb0 + 8 * k);
+        for (int k = 0; k < 6; ++k) mbar_init(mb0 + 8 * k);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < 5; ++k) mbar_expect(mb0 + 8 * k, xb[k]);
+        for (int k = 0; k < 6; ++k) mbar_expect(mb0 + 8 * k, xb[k]);
     }
     uint32_t ph = 0;                                     // bit k: parity of exchange k's next phase
     auto xwait = [&](int k) {
@@ -681,7 +682,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
         publish(G0, z0);
         send_x1(z0, r);
-        double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
+        double rho = 0.0, rho_prev = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
         bool conv = false;
         int it = 0;
         bool pit = false;                                // probe this CG iteration
@@ -946,6 +947,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 gs[v] = sv;
             }
             const double gamma = gs[0], delta = gs[1];
+            rho_prev = rho;
             rho = gs[2];
             if (k == 0) bb = rho;
             conv = rho <= Q.tol2 * bb;
@@ -966,6 +968,37 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     r[q][c] = fma(-alpha, sn, r[q][c]);
                     z0[q][c] = di0[q][c] * (float)r[q][c];
                 }
+            // Early stopping test: when the residual decay predicts (r,r) <= 4 tol^2 (b,b) for the new
+            // r (rho^2 / rho_prev), reduce (r,r) now (X6) instead of after one more V-cycle.  The
+            // partials follow exactly the tree of the X5 (r,r) (same fma order, shuffles, warp order,
+            // rank order), so the value, the decision and x are those of the next iteration's test.
+            if (k > 0 && rho * rho <= 4.0 * Q.tol2 * bb * rho_prev && it + 1 < Q.maxit) {
+                double a2 = 0.0;
+#pragma unroll
+                for (int q = 0; q < BR; ++q)
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) a2 = fma(r[q][c], r[q][c], a2);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+                if (lane == 0) wred[3 * NWARP + warp] = a2;
+                __syncthreads();
+                if (warp == 0 && lane < CS) {
+                    double sv = 0.0;
+#pragma unroll
+                    for (int ww = 0; ww < NWARP; ++ww) sv += wred[3 * NWARP + ww];
+                    st_async(mapa(smem_addr(cred + (buf * CS + rank) * 4 + 3), lane), sv, mapa(mb0 + 40, lane));
+                }
+                xwait(5);
+                double rn = 0.0;
+#pragma unroll
+                for (int rr2 = 0; rr2 < CS; ++rr2) rn += cred[(buf * CS + rr2) * 4 + 3];
+                if (rn <= Q.tol2 * bb) {                 // converged: x, r are the next test's
+                    rho = rn;
+                    conv = true;
+                    ++it;
+                    break;
+                }
+            }
             publish(G0, z0);
             send_x1(z0, r);
             CL_MARK(pit, 13);
