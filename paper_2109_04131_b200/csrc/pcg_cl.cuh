@@ -72,7 +72,7 @@ struct ClC {
     __host__ __device__ static constexpr int Nl(int l) { return ((NN >> l) + 1) * ((NN >> l) + 1); }
     static constexpr int mK = 8, PK = 9, NK = 81, UK = 49, HK = (UK + 1) / 2;
     static constexpr int mE = 4, PE = 5, NE = 25, UE = 9;
-    static constexpr int KPAD = (16 - (HK * UK) % 32 + 32) % 32;   // the two K halves 16 banks apart
+    static constexpr int KS = 56;                            // K row-major, row stride 56 (= 24 mod 32 banks)
     static constexpr int ATR = HR + 6;                       // coefficient-table cell rows j0-2 .. j0+HR+3
     static constexpr int JC = 8;                             // psi factors staged JC terms at a time
     static constexpr int CPT = NT / n, KJ = (((ATR + CPT - 1) / CPT) + 1) & ~1, YP = CPT * KJ;
@@ -89,8 +89,8 @@ struct ClC {
     }
     static constexpr int oKs = oLC(LK);                      // WHK, WVK, DK, DIK, SK (NK each), RK (2 HK)
     static constexpr int oWHE = oKs + 5 * NK + 2 * HK, oWVE = oWHE + NE;
-    static constexpr int oKt = oWVE + NE;                    // K (2 HK UK + KPAD), AI, Bm, Cm; setup: ctab
-    static constexpr int oAI = oKt + 2 * HK * UK + KPAD, oB = oAI + UE * UE, oC = oB + UE * UK;
+    static constexpr int oKt = oWVE + NE;                    // K (UK x KS), AI, Bm, Cm; setup: ctab
+    static constexpr int oAI = oKt + UK * KS, oB = oAI + UE * UE, oC = oB + UE * UK;
     static constexpr int oU = ((oC + UE * UK) + 3) & ~3;     // 16-byte aligned union
     // union U: runtime grids | setup coefficient table aT (fp64) | setup psi staging (fp64)
     static constexpr int oG0 = oU, oG1 = oG0 + FR, oRh = oG1 + FR;
@@ -477,7 +477,11 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         __syncthreads();                                 // the coarse table (K region) is dead
         // ---- diagonals, zeroed grids, the dense maps -------------------------------------------
-        for (int e = tid; e < L::URUN; e += NT) sf[L::oU + e] = 0.0f;      // every runtime grid
+        {   // every runtime grid (16-byte stores; oU is 16-byte aligned)
+            float4 *z4 = reinterpret_cast<float4 *>(sf + L::oU);
+            for (int e = tid; e < L::URUN / 4; e += NT) z4[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+            for (int e = 4 * (L::URUN / 4) + tid; e < L::URUN; e += NT) sf[L::oU + e] = 0.0f;
+        }
         for (int e = tid; e < L::F1; e += NT) {           // level-1 omega D^-1 (rows 0 .. HR1+1)
             const int lrw = e / P1, s = e % P1, I = s < H1E ? 2 * s : s >= H1 ? 2 * (s - H1) + 1 : -1;
             const int jl = lrw - 1, J = J0 + jl;
@@ -562,9 +566,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             Cm[e] = v;
         }
         __syncthreads();
-        auto kix = [](int col, int row) -> int { return col * UK + row + (col >= HK ? L::KPAD : 0); };
-        for (int e = UK * UK + tid; e < 2 * HK * UK; e += NT) Kt[kix(e / UK, e % UK)] = 0.0f;
-        if (tid < 2 * HK - UK) RK[UK + tid] = 0.0f;
+        auto kix = [](int col, int row) -> int { return row * L::KS + col; };     // K[row][col]
         for (int e = tid; e < UK * UK; e += NT) {        // B^T C
             const int i = e % UK, k = e / UK;
             float v = 0.0f;
@@ -788,21 +790,23 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 __syncthreads();
             }
             CL_MARK(pit, 6);
-            if (warp < (2 * UK + 31) / 32) {             // SK = K RK (levels 8 and 4 cells)
-                const int h = tid & 1, i = min(tid >> 1, UK - 1);
-                const bool own = tid < 2 * UK;
-                const float *kp = Kt + h * (HK * UK + L::KPAD) + i, *rp = RK + h * HK;
-                float a0 = 0.0f, a1 = 0.0f, a2 = 0.0f, a3 = 0.0f;
+            constexpr int KT = 8 * ((UK + 3) / 4 * 4);   // SK = K RK (levels 8 and 4 cells): row i, 8 lanes
 #pragma unroll
-                for (int c = 0; c < HK; c += 4) {
-                    a0 = fmaf(kp[c * UK], rp[c], a0);
-                    if (c + 1 < HK) a1 = fmaf(kp[(c + 1) * UK], rp[c + 1], a1);
-                    if (c + 2 < HK) a2 = fmaf(kp[(c + 2) * UK], rp[c + 2], a2);
-                    if (c + 3 < HK) a3 = fmaf(kp[(c + 3) * UK], rp[c + 3], a3);
+            for (int kb = 0; kb < (KT + NT - 1) / NT; ++kb) {
+                const int tk = tid + kb * NT;
+                if (tk - lane >= KT) break;              // whole warps only (shuffles below)
+                const int l8 = tk & 7, i = min(tk >> 3, UK - 1);
+                const float *kp = Kt + i * L::KS;
+                float a = 0.0f;
+#pragma unroll
+                for (int m = 0; m < (UK + 7) / 8; ++m) {
+                    const int c = l8 + 8 * m;
+                    if (c < UK) a = fmaf(kp[c], RK[c], a);
                 }
-                float sv = (a0 + a1) + (a2 + a3);
-                sv += __shfl_xor_sync(0xffffffffu, sv, 1);
-                if (own && h == 0) SK[(i / (mK - 1) + 1) * PK + i % (mK - 1) + 1] = sv;
+                a += __shfl_xor_sync(0xffffffffu, a, 4);
+                a += __shfl_xor_sync(0xffffffffu, a, 2);
+                a += __shfl_xor_sync(0xffffffffu, a, 1);
+                if (l8 == 0 && (tk >> 3) < UK) SK[(i / (mK - 1) + 1) * PK + i % (mK - 1) + 1] = a;
             }
             __syncthreads();
             CL_MARK(pit, 7);
