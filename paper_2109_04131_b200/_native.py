@@ -8,7 +8,8 @@ from __future__ import annotations
 import ctypes as C
 import os
 
-LIB_PATH = os.path.join(os.path.dirname(os.path.abspath(__file__)), "libusfft.so")
+# USFFT_LIB: load another build of the same sources instead (tools/bounds_check.sh, probe builds)
+LIB_PATH = os.environ.get("USFFT_LIB") or os.path.join(os.path.dirname(os.path.abspath(__file__)), "libusfft.so")
 
 i32, i64, f64, vp = C.c_int32, C.c_int64, C.c_double, C.c_void_p
 

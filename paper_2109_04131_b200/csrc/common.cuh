@@ -15,6 +15,16 @@
 
 #include "../../include/usfft.h"
 
+// Bounds-checked build (tools/bounds_check.sh: -DUSFFT_BOUNDS): every computed shared-memory and
+// DSMEM index of the on-chip kernels is asserted in range (compute-sanitizer is closed on this
+// pool).  The product build compiles the checks out.
+#ifdef USFFT_BOUNDS
+#include <cassert>
+#define UB_CHECK(cond) assert(cond)
+#else
+#define UB_CHECK(cond) ((void)0)
+#endif
+
 namespace usfft {
 // Rader tables of one prime lattice size (fft.cu), owned by the ctx
 struct RaderPlan {

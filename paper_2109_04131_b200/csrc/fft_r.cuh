@@ -125,9 +125,11 @@ __device__ __forceinline__ void pass(double2 *buf, const RaderArgs &A, int t, co
             for (int r = 0; r < R; ++r) {
                 const int idx = j + r * NBF;
                 if (MODE == GATHER) {
+                    UB_CHECK(gp >= 1 && gp < M);
                     v[b][r] = buf[gp];
                     gp = (gp * gstep) % M;
                 } else {
+                    UB_CHECK(idx < N && (!LOAD_T || tslot<N, R0>(idx) < N + R0));
                     v[b][r] = buf[LOAD_T ? tslot<N, R0>(idx) : idx];
                 }
             }
@@ -162,6 +164,7 @@ __device__ __forceinline__ void pass(double2 *buf, const RaderArgs &A, int t, co
                 const double2 c0 = make_double2(0.5 * (dq.x + dh.x), 0.5 * (dq.y - dh.y));       // conj(conv0)
                 const double2 c1 = make_double2(0.5 * (dh.x - dq.x), 0.5 * (-dh.y - dq.y));      // i conj(conv1)
                 (void)q;
+                UB_CHECK(m >= 1 && m < so.M && q < N / 2);
                 if (m < so.MH) {
                     so.st[m] = make_double2(so.x00 + c0.x, -c0.y);
                     so.st[so.MH + m] = make_double2(so.x01 + c1.y, c1.x);
@@ -181,6 +184,7 @@ __device__ __forceinline__ void pass(double2 *buf, const RaderArgs &A, int t, co
                     const double2 c = cmul(o, A.bf[k]);
                     o = make_double2(c.x, -c.y);
                 }
+                UB_CHECK(k < N && (!STORE_T || s * (NBF + 1) + j < N + R0));
                 buf[STORE_T ? s * (NBF + 1) + j : k] = o;
             }
         }

@@ -251,12 +251,16 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     // fine node (col0 + 1 + c, row0 + 1 + q) local, c in -1 .. BC; c even = odd column
     auto fe = [&](int c, int q) -> int {
         const int slot = (c & 1) == 0 ? HE + lx + (c >> 1) : lx + ((c + 1) >> 1);
+        UB_CHECK(slot >= 0 && slot < np && row0 + 1 + q >= 0 && row0 + 1 + q < L::FRW);
         return (row0 + 1 + q) * np + slot;
     };
     auto slot0 = [](int i) -> int { return (i & 1) ? HE + (i >> 1) : (i >> 1); };   // fine column i
     auto valid = [&](int q, int c) { return col0 + c + 1 <= nx && j0 + row0 + q + 1 <= nx; };
     auto col1s = [](int i) -> int { return (i & 1) ? H1 + (i >> 1) : (i >> 1); };
-    auto e1 = [&](int I, int jl) -> int { return (jl + 1) * P1 + col1s(I); };      // level-1 row jl
+    auto e1 = [&](int I, int jl) -> int {                                            // level-1 row jl
+        UB_CHECK(I >= 0 && I <= m1 && jl >= -1 && jl + 1 < L::L1R);
+        return (jl + 1) * P1 + col1s(I);
+    };
 
     // the psi factors of this CTA's strip do not depend on the sample: with pd = d they are loaded
     // once per CTA (X at the 2n abscissae, Y at the strip's ATR ordinates, both planes)
@@ -376,6 +380,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         auto fcl = [&](int ci, int cj, int up, int sh) -> double {
             const int p = 1 << sh, ra = up ? p : 2 * p, rb = up ? 2 * p : p;
             const int fi = ci * p + ra / 3, fj = cj * p + rb / 3, pl = (ra % 3 == 1) ? 1 : 0;
+            UB_CHECK(fi >= 0 && fi < n && fj - (j0 - 2) >= 0 && fj - (j0 - 2) < ATR);
             return aT[(pl * ATR + fj - (j0 - 2)) * n + fi];
         };
         // fine couplings of the own block (ring edges included), fp64 and their fp32 copies
@@ -435,6 +440,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 if (fj / HR != rank) continue;
                 const float v = (float)fcl(ci, cj, up, l);
                 const int dst = L::ctoff(l) + (up ? m * m : 0) + cell;
+                UB_CHECK(dst >= 0 && dst < L::ctoff(LK + 2));
 #pragma unroll
                 for (int k = 0; k < CS; ++k) cluster.map_shared_rank(ctab, k)[dst] = v;
             }
@@ -596,7 +602,9 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
                     const float vl = c > 0 ? v[q][c - 1] : Gs[fe(c - 1, q)];
-                    const float vr = c + 1 < BC ? v[q][c + 1] : Gs[fe(c + 1, q)];
+                    // the right neighbour of column n (the boundary node of the last column pair) is
+                    // outside the grid; that node's result is masked, so read nothing there
+                    const float vr = c + 1 < BC ? v[q][c + 1] : col0 + c + 2 <= n ? Gs[fe(c + 1, q)] : 0.0f;
                     const float vd = q > 0 ? v[q - 1][c] : Gs[fe(c, q - 1)];
                     const float vu = q + 1 < BR ? v[q + 1][c] : Gs[fe(c, q + 1)];
                     float a = dg32[q][c] * v[q][c];
@@ -752,6 +760,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 for (int kk = 0; kk < (U + NT - 1) / NT; ++kk) {
                     const int q = tid + kk * NT, I = q % (m2 - 1) + 1, jl2 = q / (m2 - 1) + 1, J = J20 + jl2;
                     if (q >= U || J >= m2) continue;
+                    UB_CHECK(J >= 1 && I >= 1 && I < m2 && (2 * jl2 + 2) * P1 + H1 + I < L::F1);
                     const int f = (2 * jl2 + 1) * P1, c = I, l = H1 + I - 1, rr = H1 + I;
                     const float v = T1[f + c] + 0.5f * (T1[f + l] + T1[f + rr] + T1[f - P1 + c] + T1[f + P1 + c]) +
                                     0.25f * (T1[f - P1 + l] + T1[f - P1 + rr] + T1[f + P1 + l] + T1[f + P1 + rr]);
@@ -858,6 +867,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
                     for (int xx = 0; xx < XW; ++xx) {
                         const int X = lx + xx, Y = (row0 >> 1) + yy;
+                        UB_CHECK(!(X <= m1 && J0 + Y <= m1) || (Y + 1) * P1 + col1s(X) < L::F1);
                         cw[yy][xx] = (X <= m1 && J0 + Y <= m1) ? Z1[(Y + 1) * P1 + col1s(X)] : 0.0f;
                     }
                 auto pw = [&](int c, int q) -> float {
@@ -902,7 +912,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
                     const double vl = c > 0 ? (double)uu[q][c - 1] : (double)G1[fe(c - 1, q)];
-                    const double vr = c + 1 < BC ? (double)uu[q][c + 1] : (double)G1[fe(c + 1, q)];
+                    const double vr = c + 1 < BC ? (double)uu[q][c + 1] : col0 + c + 2 <= n ? (double)G1[fe(c + 1, q)] : 0.0;
                     const double vd = q > 0 ? (double)uu[q - 1][c] : (double)G1[fe(c, q - 1)];
                     const double vu = q + 1 < BR ? (double)uu[q + 1][c] : (double)G1[fe(c, q + 1)];
                     double a = (cE[q][c + 1] + cE[q][c] + cN[q + 1][c] + cN[q][c]) * (double)uu[q][c];
