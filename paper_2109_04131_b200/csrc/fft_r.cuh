@@ -207,6 +207,13 @@ template <int R0, int... Rs>
 struct First { static constexpr int value = R0; };
 }  // namespace fr
 
+// streaming row loads that do not allocate in L1 (the FFT(b) and index tables should stay there)
+__device__ __forceinline__ double ld_stream(const double *p) {
+    double v;
+    asm volatile("ld.global.nc.L1::no_allocate.f64 %0, [%1];" : "=d"(v) : "l"(p));
+    return v;
+}
+
 template <int N, int GROUP, int NPAIR, int MINB, int... Rs>
 __global__ void __launch_bounds__(GROUP * NPAIR, MINB)
 k_fft_rader_r(const double *__restrict__ u, const SlabParams S, int64_t G_loc, int32_t L,
@@ -223,10 +230,13 @@ k_fft_rader_r(const double *__restrict__ u, const SlabParams S, int64_t G_loc, i
     auto row1 = [&](int64_t q) { return 2 * (q % LP) + 1 < L ? row0(q) + 1 : int64_t(-1); };
     auto at = [&](int64_t rw, const double *src, int i) -> double {
         if (rw < 0) return 0.0;
-        if (one_slab) return __ldcs(src + i);
+        if (one_slab) return ld_stream(src + i);
         const int64_t g = rw / L, l = rw - g * L;
         return sample_at(u, S, G_loc, g, l * M + i);
     };
+    // the FFT(b)/N table (16 N bytes, shared by every pair) into L1 once per CTA
+    for (int k = tid * 8; k < N; k += GROUP * NPAIR * 8)
+        asm volatile("prefetch.global.L1 [%0];" :: "l"(A.bf + k));
     // every pair of the CTA runs the same number of rounds (idle pairs transform zeros, not stored)
     const int64_t rounds = (pairs + (int64_t)gridDim.x * NPAIR - 1) / ((int64_t)gridDim.x * NPAIR);
     for (int64_t rd = 0; rd < rounds; ++rd) {
