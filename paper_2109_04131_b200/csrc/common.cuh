@@ -13,6 +13,8 @@
 #include <string>
 #include <utility>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/usfft.h"
 
 // Bounds-checked build (tools/bounds_check.sh: -DUSFFT_BOUNDS): every computed shared-memory and
@@ -130,7 +132,17 @@ struct DeviceGuard {
     }
 };
 
+// NVTX range per C-ABI call (header-only NVTX 3; a no-op unless a tool such as nsys / ncu
+// --nvtx is attached): the range is named after the entry point and spans its host side
+struct NvtxRange {
+    explicit NvtxRange(const char *name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange &) = delete;
+    NvtxRange &operator=(const NvtxRange &) = delete;
+};
+
 #define USFFT_ENTER(c)                                                                        \
+    usfft::NvtxRange usfft_nvtx_range_(__func__);                                             \
     if (!(c)) return USFFT_EINVAL;                                                            \
     if ((c)->sticky) return USFFT_ECUDA;                                                      \
     (c)->err.clear();                                                                         \

@@ -14,6 +14,8 @@ Round r = (step, t, i):
 """
 from __future__ import annotations
 
+import json
+import os
 from dataclasses import dataclass, field
 
 import numpy as np
@@ -224,6 +226,37 @@ class Detector:
                              det_g, votes)
         return votes
 
+    # ---- checkpoint / resume: after Step 1 and after every dimension t of Step 2 the
+    # run's state (the 1-D sets I^(t), t = 1..d, and I^(1..t)) goes to a small .npz file; all
+    # randomness is counter-based (Z4: seed, step, t, i), so a resumed run recomputes rounds
+    # t+1.. exactly as the uninterrupted run would.  Rank 0 writes (every rank holds the same
+    # sets); the file is replaced atomically.
+    def _ckpt_key(self) -> str:
+        c = self.cfg
+        return json.dumps({k: c.get(k) for k in ("name", "seed", "d", "N", "s", "s_local", "r", "mode", "n",
+                                                   "theta", "theta_rel")}, sort_keys=True)
+
+    def save_checkpoint(self, path: str, I1d: list[torch.Tensor], t: int, I_prev: torch.Tensor | None):
+        if self.rank != 0:
+            return
+        arrs = {f"I1d_{k}": v.cpu().numpy() for k, v in enumerate(I1d)}
+        if I_prev is not None:
+            arrs["I_prev"] = I_prev.cpu().numpy()
+        tmp = path + ".tmp.npz"
+        np.savez(tmp, key=np.array(self._ckpt_key()), t=np.array(t), **arrs)
+        os.replace(tmp, path)
+
+    def load_checkpoint(self, path: str):
+        """(I1d, t, I_prev) of a checkpoint of this configuration; t = 1 after Step 1 only."""
+        z = np.load(path)
+        if str(z["key"]) != self._ckpt_key():
+            raise ValueError(f"{path}: checkpoint of another configuration")
+        d = self.cfg["d"]
+        I1d = [torch.as_tensor(z[f"I1d_{k}"], device=self.dev) for k in range(d)]
+        t = int(z["t"])
+        I_prev = torch.as_tensor(z["I_prev"], device=self.dev).contiguous() if "I_prev" in z else None
+        return I1d, t, I_prev
+
     def step1(self, log: list | None = None) -> list[torch.Tensor]:
         """Step 1 & 2a: I^(t) for t = 1..d as device int16 vectors."""
         cfg, dev = self.cfg, self.dev
@@ -248,14 +281,21 @@ class Detector:
             out.append(rows.reshape(-1))
         return out
 
-    def step2(self, I1d: list[torch.Tensor], log: list | None = None, t_stop: int | None = None):
-        """Step 2: returns (I^(1..d) int16 [nI][d] device, coef [G_loc][nI][2])."""
+    def step2(self, I1d: list[torch.Tensor], log: list | None = None, t_stop: int | None = None,
+              checkpoint: str | None = None, start: tuple[int, torch.Tensor] | None = None):
+        """Step 2: returns (I^(1..d) int16 [nI][d] device, coef [G_loc][nI][2]).
+        checkpoint: write the state after every dimension; start = (t0, I^(1..t0)) continues a
+        checkpointed run at t0 + 1."""
         cfg, dev, ctx = self.cfg, self.dev, self.ctx
         d, r = cfg["d"], cfg["r"]
         I_prev = I1d[0].reshape(-1, 1).contiguous()
+        t_first = 2
+        if start is not None:
+            t_first = start[0] + 1
+            I_prev = start[1].contiguous()
         coef = None
         t_end = d if t_stop is None else t_stop
-        for t in range(2, t_end + 1):
+        for t in range(t_first, t_end + 1):
             r_t, s_t = (r, cfg["s_local"]) if t < d else (1, cfg["s"])          # P:305
             kt = I1d[t - 1]
             n_prev = I_prev.shape[0]
@@ -275,13 +315,24 @@ class Detector:
             I_prev = rows[:n_u].contiguous()
             if t == d:
                 coef = res.coef
+            if checkpoint is not None and t < d:
+                self.save_checkpoint(checkpoint, I1d, t, I_prev)
             if n_u == 0:
                 return I_prev, None
         return I_prev, coef
 
-    def run(self, log: list | None = None):
+    def run(self, log: list | None = None, checkpoint: str | None = None):
+        """Steps 1-2.  checkpoint: a path; an existing checkpoint of this configuration resumes
+        the run after its last completed dimension, and the state is written after Step 1 and
+        after every dimension of Step 2."""
+        if checkpoint is not None and os.path.exists(checkpoint):
+            I1d, t0, I_prev = self.load_checkpoint(checkpoint)
+            start = (t0, I_prev) if I_prev is not None else None
+            return self.step2(I1d, log, checkpoint=checkpoint, start=start)
         I1d = self.step1(log)
-        return self.step2(I1d, log)
+        if checkpoint is not None:
+            self.save_checkpoint(checkpoint, I1d, 1, None)
+        return self.step2(I1d, log, checkpoint=checkpoint)
 
     # ------------------------------------------------------------------------------------------
     FFT_MAX_M = 4001           # largest lattice the Rader FFT kernels hold on chip (M-1 = 4000)
