@@ -354,9 +354,9 @@ def run_ours(args):
                                               / world / fp64_peak) if pde_ms > 0 and fp64_peak else None,
                          "survey_unit": "20 fp64 flops per fine node and CG iteration (SURVEY §8(d))"},
             "fft": {"kernel": ("k_fft_rader_r (Rader on row pairs, register-radix in-place passes)"
-                               if P.M in (401, 4001) else "k_fft_rader_t (Rader/Stockham)") + " + k_kappa_grouped",
+                               if P.M in (401, 4001) else "k_fft_rader_t (Rader/Stockham)"),
                     "bytes_def": "8 G L M read + 16 G L (M/2+1) written (the FFT's algorithmic bytes) / fft phase time",
-                    "ms_per_step": fft_ms,
+                    "ms_per_step": fft_ms, "keys_ms_per_step": phase.get("keys"),
                     "achieved_gbs": fft_bytes / (fft_ms / 1e3) / 1e9 if fft_ms else None,
                     "hbm_peak_gbs": pk["hbm_gbs"],
                     "frac": (fft_bytes / (fft_ms / 1e3) / 1e9) / pk["hbm_gbs"] if fft_ms else None},

@@ -558,7 +558,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                              : (double)(row0 + q + 1) * inv_n3;
             }
         // x0 = 0, r0 = b (Z13); ||b||^2 is the first iteration's (r, r)
-        double rho = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
+        double rho = 0.0, rho_prev = 0.0, bb = 0.0, g_inv = 0.0, ga_inv = 0.0;
         bool conv = false;
         int it = 0;
         for (int k = 0;; ++k) {
@@ -602,6 +602,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 gs[q] = tt[0];
             }
             const double gamma = gs[0], delta = gs[1];
+            rho_prev = rho;
             rho = gs[2];
             if (k == 0) bb = rho;
             conv = rho <= Q.tol2 * bb;
@@ -620,6 +621,36 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                     xref(q, c) = fma(alpha, pn, xref(q, c));
                     r[q][c] = fma(-alpha, s[q][c], r[q][c]);
                 }
+            // Early stopping test (as in pcg_cl.cuh): when the residual decay predicts (r,r) <=
+            // 4 tol^2 (b,b) for the new r, reduce (r,r) now instead of after one more V-cycle.  The
+            // tree is the one (r,r) takes above (lane 16 of each warp: own + partner at offsets
+            // 16, 8, 4, 2, 1, then the fixed warp tree), so the value and the decision are those
+            // of the next iteration's test and x is the same.
+            if (k > 0 && rho * rho <= 4.0 * Q.tol2 * bb * rho_prev && it + 1 < Q.maxit) {
+                double a2 = 0.0;
+#pragma unroll
+                for (int q = 0; q < BR; ++q)
+#pragma unroll
+                    for (int c = 0; c < BC; ++c) a2 = fma(r[q][c], r[q][c], a2);
+#pragma unroll
+                for (int o = 16; o > 0; o >>= 1) a2 += __shfl_xor_sync(0xffffffffu, a2, o);
+                __syncthreads();                         // everyone has read red[] of this iteration
+                if (lane == 16) red[2][warp] = a2;
+                __syncthreads();
+                double tt[NWARP];
+#pragma unroll
+                for (int ww = 0; ww < NWARP; ++ww) tt[ww] = red[2][ww];
+#pragma unroll
+                for (int h = 1; h < NWARP; h <<= 1)
+#pragma unroll
+                    for (int ww = 0; ww + h < NWARP; ww += 2 * h) tt[ww] += tt[ww + h];
+                if (tt[0] <= Q.tol2 * bb) {
+                    rho = tt[0];
+                    conv = true;
+                    ++it;
+                    break;
+                }
+            }
             ++it;
         }
 #pragma unroll

@@ -150,8 +150,12 @@ class Detector:
         chunk = self.key_chunk(nJ, s_tilde)
         if chunk is None:
             kmin = torch.empty((self.G_loc, nJ), dtype=torch.float64, device=dev)
-            B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, nJ, spectra, kmin, kmax)
+            # a7 then a8 as two calls (the same kernels usfft_lattice_fft runs with nJ > 0), so the
+            # FFT and the keys are timed as separate phases
+            B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, 0, spectra, None, kmax)
             mark("fft")
+            B.usfft_lattice_keys(ctx, plan, self.G_loc, spectra, bins, nJ, nJ, kmin, nJ, kmax)
+            mark("keys")
             self._max(kmax)
             votes = torch.empty(nJ, dtype=torch.int32, device=dev)
             B.usfft_detect_select(ctx, self.G_loc, nJ, kmin, kmax, s_tilde, cfg.get("theta_rel", 1e-6),
