@@ -1022,7 +1022,12 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c)
-                if (valid(q, c)) u[(int64_t)((j0 + row0 + q) * nx + col0 + c) * ldu + bl] = Xg[(q * BC + c) * NT + tid];
+                if (valid(q, c))   // sample-fastest output: 8 bytes per node; keep the partially written
+                                   // sectors in L2 (evict_last) until the neighbouring samples' clusters fill them
+                    asm volatile("{\n\t.reg .b64 pol;\n\tcreatepolicy.fractional.L2::evict_last.b64 pol, 1.0;\n\t"
+                                 "st.global.L2::cache_hint.f64 [%0], %1, pol;\n\t}"
+                                 :: "l"(u + (int64_t)((j0 + row0 + q) * nx + col0 + c) * ldu + bl),
+                                    "d"(Xg[(q * BC + c) * NT + tid]) : "memory");
         if (tid == 0 && rank == 0) {
             if (iters) iters[bl] = it;
             if (relres) relres[bl] = sqrt(rho / bb);
