@@ -69,6 +69,8 @@ _SIGS = {
     "usfft_detect_select": (i32, [vp, i64, i64, vp, vp, i32, f64, f64, vp, vp, vp, vp]),
     "usfft_moments": (i32, [vp, i32, vp, i64, vp, i64, i32, f64, vp, vp, vp]),
     "usfft_lattice_keys": (i32, [vp, C.POINTER(LatticeDesc), i64, vp, vp, i64, i64, vp, i64, vp, vp]),
+    "usfft_lattice_keys_product": (i32, [vp, C.POINTER(LatticeDesc), i64, vp, vp, i64, i64, i64, i64, vp, i64, vp,
+                                         vp]),
     "usfft_detect_carry": (i32, [vp, i64, i32, i64, vp, vp, vp, vp, vp, i64, vp, vp, vp]),
     "usfft_detect_union": (i32, [vp, i64, vp, vp, vp, C.POINTER(i64), vp, C.POINTER(i64)]),
     "usfft_resolve": (i32, [vp, C.POINTER(LatticeDesc), i64, vp, vp, i64, vp, vp, i32, vp, i64,

@@ -245,6 +245,19 @@ def usfft_lattice_keys(ctx: Context, plan: Plan, G_loc: int, spectra, bins, ldb:
     _check(ctx, st, "usfft_lattice_keys")
 
 
+def usfft_lattice_keys_product(ctx: Context, plan: Plan, G_loc: int, spectra, bins, ldb: int, j0: int, nJ: int,
+                               n1: int, kappa_min, ldk: int, kappa_max, kmin_off: int = 0, tau=None):
+    """a8 for candidates j0 .. j0+nJ of the product set I_prev x kt (j = a n1 + c): bins is the
+    whole [L][ldb] map; keys into kappa_min[g*ldk + kmin_off + (j - j0)]."""
+    dsc, keep = plan.desc()
+    _p(bins, torch.int32), _p(kappa_min, torch.float64)
+    st = ctx.lib.usfft_lattice_keys_product(ctx.h, C.byref(dsc), G_loc, _p(spectra, torch.float64),
+                                            bins.data_ptr(), ldb, j0, nJ, n1,
+                                            kappa_min.data_ptr() + 8 * kmin_off, ldk,
+                                            _p(kappa_max, torch.float64), _p(tau, torch.float64))
+    _check(ctx, st, "usfft_lattice_keys_product")
+
+
 def usfft_detect_carry(ctx: Context, G_loc: int, s_tilde: int, width: int, merged, carry_k, carry_j,
                        det_pos, n_det_g, j0: int = 0, det_g=None, votes=None, tau=None):
     """Streamed selection step (Z29): update the per-node carry (det_g None) or emit det_g + votes."""

@@ -176,6 +176,117 @@ k_kappa_grouped(const double2 *__restrict__ F, const int32_t *__restrict__ bins,
     }
 }
 
+// K7 for |J| >> M (config 4's Step-2 rounds, |J| ~ 2e6 against M/2+1 ~ 1e3 bins): the candidates
+// are the product set J = I_prev x kt (Z10, j = a n1 + c), so
+//   bins[l][a n1 + c] = (bins[l][a n1] + bins[l][c] - bins[l][0]) mod M,
+// and a (node, lattice) spectrum has only M/2+1 distinct values for ~|J| / (M/2) candidates each.
+// One CTA per (node g, tile of KT = NT x KPT candidates): for every lattice the node's spectrum
+// slice (M/2+1 complex) and the tile's bin terms are staged in shared memory (the next lattice's
+// slice prefetched into registers meanwhile), each thread keeps the running min of its KPT
+// candidates in registers.  The arithmetic per (g, j, l) and the min order over l are those of
+// k_kappa_grouped, so the keys are bit-identical; the traffic is the spectra once per tile
+// (G |J| L (M/2+1) 16 B / KT) instead of one 32-byte sector per (g, j, l) gather.
+template <int NT, int KPT>
+__global__ void __launch_bounds__(NT, 1)
+k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t ldb, int64_t j0,
+              int64_t nJ, int32_t n1, int32_t M, int32_t L, double *__restrict__ kmin, int64_t ldk,
+              unsigned long long *__restrict__ kmax, const double *__restrict__ tau) {
+    constexpr int KT = NT * KPT;
+    const int Mh = M / 2 + 1;
+    extern __shared__ double2 ssp[];                     // [2][Mh] spectrum slices
+    const int AT = KT / n1 + 2;                          // a values a tile spans
+    int32_t *sA = reinterpret_cast<int32_t *>(ssp + 2 * Mh);   // [2][AT]: bins[l][a n1]
+    int32_t *sD = sA + 2 * AT;                                  // [2][n1]: bins[l][c] - bins[l][0] mod M
+    __shared__ unsigned long long wmax[NT / 32];
+    const int tid = threadIdx.x;
+    const int64_t g = blockIdx.y;
+    const int64_t t0 = j0 + (int64_t)blockIdx.x * KT, t1 = min(t0 + KT, j0 + nJ);
+    const int64_t a_lo = t0 / n1;
+    const int na = (int)((t1 - 1) / n1 - a_lo) + 1;
+    const double2 *src = F + g * (int64_t)L * Mh;
+    const double inv_m = 1.0 / (double)M;
+    // the first candidate of this thread and the per-step increments (j += NT)
+    const int64_t jt = t0 + tid;
+    int a_first = (int)(jt / n1 - a_lo), c_first = (int)(jt % n1);
+    const int qa = NT / n1, qc = NT % n1;
+    constexpr int PF = 2;                                // prefetch registers per thread (double2)
+    double2 pf[PF];
+    auto fetch = [&](int l) {
+#pragma unroll
+        for (int k = 0; k < PF; ++k) {
+            const int i = tid + k * NT;
+            pf[k] = i < Mh ? __ldg(src + (int64_t)l * Mh + i) : make_double2(0.0, 0.0);
+        }
+    };
+    auto stage = [&](int l, int buf) {                   // pf (lattice l) + bin terms -> buffer buf
+        double2 *S = ssp + buf * Mh;
+#pragma unroll
+        for (int k = 0; k < PF; ++k)
+            if (tid + k * NT < Mh) S[tid + k * NT] = pf[k];
+        for (int i = tid + PF * NT; i < Mh; i += NT) S[i] = __ldg(src + (int64_t)l * Mh + i);
+        const int32_t *bl = bins + (int64_t)l * ldb;
+        for (int i = tid; i < na; i += NT) sA[buf * AT + i] = __ldg(bl + (a_lo + i) * n1);
+        const int32_t b00 = __ldg(bl);
+        for (int i = tid; i < n1; i += NT) {
+            const int32_t v = __ldg(bl + i) - b00;
+            sD[buf * n1 + i] = v < 0 ? v + M : v;
+        }
+    };
+    double km[KPT];
+    fetch(0);
+    stage(0, 0);
+    __syncthreads();
+    for (int l = 0; l < L; ++l) {
+        const int buf = l & 1;
+        if (l + 1 < L) fetch(l + 1);                      // in flight during the gathers below
+        const double2 *S = ssp + buf * Mh;
+        const int32_t *A = sA + buf * AT, *D = sD + buf * n1;
+        int a = a_first, c = c_first;
+#pragma unroll
+        for (int k = 0; k < KPT; ++k) {
+            if (t0 + tid + (int64_t)k * NT >= t1) break;     // ragged tile end (a, c past the staged range)
+            UB_CHECK(a >= 0 && a < na && c >= 0 && c < n1);
+            int b = A[a] + D[c];
+            b = b >= M ? b - M : b;
+            UB_CHECK(b >= 0 && b < M);
+            const double2 f = S[b < Mh ? b : M - b];
+            const double re = f.x * inv_m, im = f.y * inv_m;
+            const double kk = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+            km[k] = (l == 0) ? kk : fmin(km[k], kk);
+            a += qa;
+            c += qc;
+            if (c >= n1) {
+                c -= n1;
+                ++a;
+            }
+        }
+        if (l + 1 < L) {
+            stage(l + 1, buf ^ 1);
+            __syncthreads();
+        }
+    }
+    unsigned long long best = 0ull;
+#pragma unroll
+    for (int k = 0; k < KPT; ++k) {
+        const int64_t j = t0 + tid + (int64_t)k * NT;
+        if (j < t1) {
+            kmin[g * ldk + (j - j0)] = (tau && km[k] <= tau[g]) ? 0.0 : km[k];
+            const unsigned long long bits = (unsigned long long)__double_as_longlong(km[k]);
+            best = bits > best ? bits : best;
+        }
+    }
+    for (int o = 16; o > 0; o >>= 1) {
+        const unsigned long long other = __shfl_xor_sync(0xffffffffu, best, o);
+        best = other > best ? other : best;
+    }
+    if ((tid & 31) == 0) wmax[tid >> 5] = best;
+    __syncthreads();
+    if (tid == 0) {
+        for (int w = 1; w < NT / 32; ++w) best = wmax[w] > best ? wmax[w] : best;
+        atomicMax(kmax, best);
+    }
+}
+
 }  // namespace usfft
 
 #include "rader.cuh"
@@ -458,6 +569,36 @@ extern "C" usfft_status usfft_lattice_keys(usfft_ctx *c, const usfft_lattice_des
     if (G_loc == 0 || nJ == 0) return USFFT_OK;
     USFFT_REQUIRE(c, spectra && bins && kappa_min && kappa_max, "NULL argument");
     return launch_keys(c, lat->M, lat->L, G_loc, spectra, bins, ldb, nJ, kappa_min, ldk, kappa_max, tau);
+}
+
+// a8 for the candidates j0 .. j0+nJ-1 of the product set J = I_prev x kt (j = a n1 + c, Z10):
+// bins is the whole [L][ldb] map; keys into kappa_min[g * ldk + (j - j0)].  |J| >= 4 (M/2+1):
+// k_kappa_tiled; otherwise the gather kernel on bins + j0 (both bit-identical).
+extern "C" usfft_status usfft_lattice_keys_product(usfft_ctx *c, const usfft_lattice_desc *lat, int64_t G_loc,
+                                                   const double *spectra, const int32_t *bins, int64_t ldb,
+                                                   int64_t j0, int64_t nJ, int64_t n1, double *kappa_min,
+                                                   int64_t ldk, double *kappa_max, const double *tau) {
+    USFFT_ENTER(c);
+    USFFT_REQUIRE(c, lat != nullptr, "lattice desc is NULL");
+    USFFT_REQUIRE(c, lat->M >= 2 && lat->M <= (int64_t(1) << 26) && lat->L >= 1, "bad M / L");
+    USFFT_REQUIRE(c, G_loc >= 0 && nJ >= 0 && j0 >= 0 && n1 >= 1 && ldb >= j0 + nJ && ldk >= nJ,
+                  "bad sizes / leading dimensions");
+    USFFT_REQUIRE(c, ldb % n1 == 0 && ldb < (int64_t(1) << 31), "ldb must be |J| = n_prev * n1 (< 2^31)");
+    if (G_loc == 0 || nJ == 0) return USFFT_OK;
+    USFFT_REQUIRE(c, spectra && bins && kappa_min && kappa_max, "NULL argument");
+    const int64_t M = lat->M, Mh = M / 2 + 1;
+    constexpr int NT = 512, KPT = 24, KT = NT * KPT;
+    const size_t smem = sizeof(double2) * 2 * (size_t)Mh + sizeof(int32_t) * 2 * (size_t)(KT / n1 + 2 + n1);
+    if (nJ < 4 * Mh || smem > c->smem_optin || G_loc > 65535)
+        return launch_keys(c, M, lat->L, G_loc, spectra, bins + j0, ldb, nJ, kappa_min, ldk, kappa_max, tau);
+    auto kern = k_kappa_tiled<NT, KPT>;
+    if (usfft_status s = kernel_fit(c, kern, NT, smem, nullptr)) return s;
+    dim3 grid((unsigned)((nJ + KT - 1) / KT), (unsigned)G_loc);
+    kern<<<grid, NT, smem, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb, j0, nJ, (int32_t)n1,
+                                        (int32_t)M, lat->L, kappa_min, ldk,
+                                        reinterpret_cast<unsigned long long *>(kappa_max), tau);
+    USFFT_CHECK_LAUNCH(c);
+    return USFFT_OK;
 }
 
 extern "C" usfft_status usfft_lattice_dft_bins(usfft_ctx *c, int64_t M, int64_t G_loc, const double *u,

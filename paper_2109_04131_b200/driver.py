@@ -154,7 +154,7 @@ class Detector:
             # FFT and the keys are timed as separate phases
             B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, 0, spectra, None, kmax)
             mark("fft")
-            B.usfft_lattice_keys(ctx, plan, self.G_loc, spectra, bins, nJ, nJ, kmin, nJ, kmax)
+            B.usfft_lattice_keys_product(ctx, plan, self.G_loc, spectra, bins, nJ, 0, nJ, n1, kmin, nJ, kmax)
             mark("keys")
             self._max(kmax)
             votes = torch.empty(nJ, dtype=torch.int32, device=dev)
@@ -164,7 +164,7 @@ class Detector:
             kmin = None
             B.usfft_lattice_fft(ctx, plan, self.G_loc, slabs, sb, bins, 0, spectra, None, kmax)
             mark("fft")
-            votes = self._streamed_select(plan, nJ, s_tilde, chunk, spectra, bins, kmax, det_g, n_det_g, th2)
+            votes = self._streamed_select(plan, nJ, n1, s_tilde, chunk, spectra, bins, kmax, det_g, n_det_g, th2)
         self._sum(votes)
         det_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
         union_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
@@ -203,7 +203,7 @@ class Detector:
             return None
         return max(256, (self.KEY_BYTES // (8 * self.G_loc) - s_tilde) // 256 * 256)
 
-    def _streamed_select(self, plan, nJ, s_tilde, chunk, spectra, bins, kmax, det_g, n_det_g, th2):
+    def _streamed_select(self, plan, nJ, n1, s_tilde, chunk, spectra, bins, kmax, det_g, n_det_g, th2):
         """a8 + a9 + a10 over chunks of J with a per-node top-s~ carry (usfft.h, Z29): the same
         D_g, votes and theta^2 as the one-shot selection, in O(G_loc (s~ + chunk)) memory."""
         cfg, ctx, dev, G = self.cfg, self.ctx, self.dev, self.G_loc
@@ -218,8 +218,8 @@ class Detector:
             c = min(chunk, nJ - j0)
             if c < chunk:
                 merged[:, s_tilde + c:].zero_()                 # ragged last chunk: zero keys
-            B.usfft_lattice_keys(ctx, plan, G, spectra, bins, nJ, c, merged, W, kmax, bins_off=j0,
-                                 kmin_off=s_tilde, tau=tau)
+            B.usfft_lattice_keys_product(ctx, plan, G, spectra, bins, nJ, j0, c, n1, merged, W, kmax,
+                                         kmin_off=s_tilde, tau=tau)
             B.usfft_detect_select(ctx, G, W, merged, kmax, s_tilde, 0.0, 0.0, scratch, det_pos, n_det_g)
             B.usfft_detect_carry(ctx, G, s_tilde, W, merged, carry_k, carry_j, det_pos, n_det_g, j0, tau=tau)
         self._max(kmax)

@@ -1,0 +1,72 @@
+"""a8 keys through the product-set path (usfft_lattice_keys_product, k_kappa_tiled for |J| >= 4
+(M/2+1)): bit-identical to the gather kernel (usfft_lattice_keys) on the same spectra, whole and
+in ragged chunks with the carry prefilter, and <= 1e-12 (sqrt) of the oracle's kappa_min of its
+direct-DFT values (Alg. 1 Step 2c P:313-315, Z1, Z5, Z10)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import detect as odet
+from oracle import dft as odft
+from oracle import lattice as olat
+
+pytestmark = pytest.mark.gpu
+
+
+@pytest.fixture(scope="module")
+def B():
+    from paper_2109_04131_b200 import binding
+    return binding
+
+
+@pytest.fixture(scope="module")
+def ctx(B):
+    return B.Context(0)
+
+
+def _inputs(G, M, L, n_prev, n1, t, seed):
+    rng = np.random.default_rng(seed)
+    I_prev = np.unique(rng.integers(-40, 41, size=(3 * n_prev, t - 1)), axis=0)[:n_prev]
+    kt = np.arange(-(n1 // 2), n1 - n1 // 2)
+    J = olat.candidates(I_prev, kt)
+    z = rng.integers(1, M, size=(L, t))
+    bins = olat.bins(J, z, M)
+    U = rng.standard_normal((G, L * M))
+    return U, z, J, bins
+
+
+@pytest.mark.parametrize("G,M,L,n_prev,n1,t", [(5, 97, 7, 300, 13, 3), (3, 401, 5, 1100, 17, 4),
+                                               (9, 2017, 3, 1400, 9, 3)])
+def test_product_keys_bitexact_and_vs_oracle(B, ctx, G, M, L, n_prev, n1, t):
+    from paper_2109_04131_b200.binding import Plan
+    U, z, J, bins = _inputs(G, M, L, n_prev, n1, t, seed=G + M)
+    nJ = J.shape[0]
+    Mh = M // 2 + 1
+    assert nJ >= 4 * Mh                                   # the tiled kernel runs
+    p = Plan(t, M, L, t, -1, z, np.zeros(t))
+    spectra = torch.empty((G, L, Mh, 2), dtype=torch.float64, device="cuda")
+    kmax0 = torch.zeros(1, dtype=torch.float64, device="cuda")
+    B.usfft_lattice_fft(ctx, p, G, torch.as_tensor(U, device="cuda"), [0, L * M], None, 0, spectra, None, kmax0)
+    bd = torch.as_tensor(bins, dtype=torch.int32, device="cuda").contiguous()
+    k_g = torch.empty((G, nJ), dtype=torch.float64, device="cuda")
+    k_p = torch.empty((G, nJ), dtype=torch.float64, device="cuda")
+    m_g = torch.zeros(1, dtype=torch.float64, device="cuda")
+    m_p = torch.zeros(1, dtype=torch.float64, device="cuda")
+    B.usfft_lattice_keys(ctx, p, G, spectra, bd, nJ, nJ, k_g, nJ, m_g)
+    B.usfft_lattice_keys_product(ctx, p, G, spectra, bd, nJ, 0, nJ, n1, k_p, nJ, m_p)
+    assert torch.equal(k_p, k_g) and m_p.item() == m_g.item()
+    ref = odet.kappa_min(odft.round_values(U, M, L, bins))
+    km = k_p.cpu().numpy()
+    assert np.abs(np.sqrt(km) - np.sqrt(ref)).max() <= 1e-12 * np.sqrt(ref.max())
+    # a ragged chunk at an offset, written behind a carry of width s (the streamed layout, Z29),
+    # with the carry prefilter tau
+    s, j0 = 11, nJ // 3 + 5
+    c = min(4 * Mh + 123, nJ - j0)
+    W = s + c
+    tau = torch.as_tensor(np.quantile(km[:, j0:j0 + c], 0.5, axis=1), device="cuda").contiguous()
+    out_g = torch.full((G, W), -1.0, dtype=torch.float64, device="cuda")
+    out_p = torch.full((G, W), -1.0, dtype=torch.float64, device="cuda")
+    B.usfft_lattice_keys(ctx, p, G, spectra, bd, nJ, c, out_g, W, m_g, bins_off=j0, kmin_off=s, tau=tau)
+    B.usfft_lattice_keys_product(ctx, p, G, spectra, bd, nJ, j0, c, n1, out_p, W, m_p, kmin_off=s, tau=tau)
+    assert torch.equal(out_p, out_g)
+    assert bool((out_p[:, :s] == -1.0).all())

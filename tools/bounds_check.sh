@@ -15,3 +15,4 @@ USFFT_LIB=/tmp/libusfft_bounds.so timeout 900 python tools/sanitize_run.py > gpu
 USFFT_LIB=/tmp/libusfft_bounds.so timeout 900 python tools/pde_bench.py --config 5 --nb 1184 --reps 1 > gpurun_out/bc_pde5.log 2>&1; echo "pde5 rc=$?"; tail -1 gpurun_out/bc_pde5.log
 USFFT_LIB=/tmp/libusfft_bounds.so timeout 900 python tools/pde_bench.py --config 3 --nb 2048 --reps 1 > gpurun_out/bc_pde3.log 2>&1; echo "pde3 rc=$?"; tail -1 gpurun_out/bc_pde3.log
 USFFT_LIB=/tmp/libusfft_bounds.so timeout 900 python tools/fft_bench.py > gpurun_out/bc_fft.log 2>&1; echo "fft rc=$?"; tail -3 gpurun_out/bc_fft.log
+USFFT_LIB=/tmp/libusfft_bounds.so timeout 900 python -m pytest tests/test_gpu_keys_product.py -q > gpurun_out/bc_keys.log 2>&1; echo "keys rc=$?"; tail -1 gpurun_out/bc_keys.log
