@@ -186,16 +186,16 @@ k_kappa_grouped(const double2 *__restrict__ F, const int32_t *__restrict__ bins,
 // candidates in registers.  The arithmetic per (g, j, l) and the min order over l are those of
 // k_kappa_grouped, so the keys are bit-identical; the traffic is the spectra once per tile
 // (G |J| L (M/2+1) 16 B / KT) instead of one 32-byte sector per (g, j, l) gather.
-template <int NT, int KPT>
-__global__ void __launch_bounds__(NT, 1)
+template <int NT, int KPT, int MINB>
+__global__ void __launch_bounds__(NT, MINB)
 k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, int64_t ldb, int64_t j0,
               int64_t nJ, int32_t n1, int32_t M, int32_t L, double *__restrict__ kmin, int64_t ldk,
               unsigned long long *__restrict__ kmax, const double *__restrict__ tau) {
     constexpr int KT = NT * KPT;
     const int Mh = M / 2 + 1;
-    extern __shared__ double2 ssp[];                     // [2][Mh] spectrum slices
+    extern __shared__ double ssk[];                      // [2][Mh] keys |F/M|^2 of a slice's bins
     const int AT = KT / n1 + 2;                          // a values a tile spans
-    int32_t *sA = reinterpret_cast<int32_t *>(ssp + 2 * Mh);   // [2][AT]: bins[l][a n1]
+    int32_t *sA = reinterpret_cast<int32_t *>(ssk + 2 * Mh);   // [2][AT]: bins[l][a n1]
     int32_t *sD = sA + 2 * AT;                                  // [2][n1]: bins[l][c] - bins[l][0] mod M
     __shared__ unsigned long long wmax[NT / 32];
     const int tid = threadIdx.x;
@@ -218,12 +218,17 @@ k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, i
             pf[k] = i < Mh ? __ldg(src + (int64_t)l * Mh + i) : make_double2(0.0, 0.0);
         }
     };
-    auto stage = [&](int l, int buf) {                   // pf (lattice l) + bin terms -> buffer buf
-        double2 *S = ssp + buf * Mh;
+    // the key of a bin, by exactly the arithmetic of k_kappa_grouped (it depends on the bin only)
+    auto key = [&](double2 f) -> double {
+        const double re = f.x * inv_m, im = f.y * inv_m;
+        return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+    };
+    auto stage = [&](int l, int buf) {                   // keys of lattice l's bins + bin terms -> buf
+        double *S = ssk + buf * Mh;
 #pragma unroll
         for (int k = 0; k < PF; ++k)
-            if (tid + k * NT < Mh) S[tid + k * NT] = pf[k];
-        for (int i = tid + PF * NT; i < Mh; i += NT) S[i] = __ldg(src + (int64_t)l * Mh + i);
+            if (tid + k * NT < Mh) S[tid + k * NT] = key(pf[k]);
+        for (int i = tid + PF * NT; i < Mh; i += NT) S[i] = key(__ldg(src + (int64_t)l * Mh + i));
         const int32_t *bl = bins + (int64_t)l * ldb;
         for (int i = tid; i < na; i += NT) sA[buf * AT + i] = __ldg(bl + (a_lo + i) * n1);
         const int32_t b00 = __ldg(bl);
@@ -239,7 +244,7 @@ k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, i
     for (int l = 0; l < L; ++l) {
         const int buf = l & 1;
         if (l + 1 < L) fetch(l + 1);                      // in flight during the gathers below
-        const double2 *S = ssp + buf * Mh;
+        const double *S = ssk + buf * Mh;
         const int32_t *A = sA + buf * AT, *D = sD + buf * n1;
         int a = a_first, c = c_first;
 #pragma unroll
@@ -249,9 +254,7 @@ k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, i
             int b = A[a] + D[c];
             b = b >= M ? b - M : b;
             UB_CHECK(b >= 0 && b < M);
-            const double2 f = S[b < Mh ? b : M - b];
-            const double re = f.x * inv_m, im = f.y * inv_m;
-            const double kk = __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
+            const double kk = S[b < Mh ? b : M - b];        // |F[M-b]| = |F[b]| (real input)
             km[k] = (l == 0) ? kk : fmin(km[k], kk);
             a += qa;
             c += qc;
@@ -587,11 +590,11 @@ extern "C" usfft_status usfft_lattice_keys_product(usfft_ctx *c, const usfft_lat
     if (G_loc == 0 || nJ == 0) return USFFT_OK;
     USFFT_REQUIRE(c, spectra && bins && kappa_min && kappa_max, "NULL argument");
     const int64_t M = lat->M, Mh = M / 2 + 1;
-    constexpr int NT = 512, KPT = 24, KT = NT * KPT;
-    const size_t smem = sizeof(double2) * 2 * (size_t)Mh + sizeof(int32_t) * 2 * (size_t)(KT / n1 + 2 + n1);
+    constexpr int NT = 512, KPT = 24, MINB = 1, KT = NT * KPT;
+    const size_t smem = sizeof(double) * 2 * (size_t)Mh + sizeof(int32_t) * 2 * (size_t)(KT / n1 + 2 + n1);
     if (nJ < 4 * Mh || smem > c->smem_optin || G_loc > 65535)
         return launch_keys(c, M, lat->L, G_loc, spectra, bins + j0, ldb, nJ, kappa_min, ldk, kappa_max, tau);
-    auto kern = k_kappa_tiled<NT, KPT>;
+    auto kern = k_kappa_tiled<NT, KPT, MINB>;
     if (usfft_status s = kernel_fit(c, kern, NT, smem, nullptr)) return s;
     dim3 grid((unsigned)((nJ + KT - 1) / KT), (unsigned)G_loc);
     kern<<<grid, NT, smem, c->stream>>>(reinterpret_cast<const double2 *>(spectra), bins, ldb, j0, nJ, (int32_t)n1,
