@@ -21,6 +21,9 @@ __device__ __forceinline__ double theta2_of(double theta_rel, double theta_abs, 
 // one CTA per owned node g (128 threads: the radix passes are barrier-bound); the node's keys
 // are staged in shared memory when |J| <= KSTAGE
 constexpr int64_t KSTAGE = 6144;
+// larger rows (the streamed chunks of Z29, mostly keys prefiltered to 0): the positive keys and
+// their indices are compacted in order into shared memory when there are at most KCOMP of them
+constexpr int KCOMP = 2048;
 
 __global__ void __launch_bounds__(128)
 k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__ kmax,
@@ -33,13 +36,52 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
     __shared__ unsigned int s_zero;
     __shared__ int scan_sh[33];
     extern __shared__ unsigned long long kst[];
+    __shared__ int warp_cnt[4];
     const int64_t g = blockIdx.x;
     const unsigned long long *keys =
         reinterpret_cast<const unsigned long long *>(kmin + g * nJ);
+    const int32_t *jmap = nullptr;                     // compacted row: entry q is candidate jmap[q]
     if (nJ <= KSTAGE) {
         for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) kst[j] = __ldg(keys + j);
         keys = kst;
         __syncthreads();
+    } else {
+        // order-preserving compaction of the positive keys: warp w owns the contiguous quarter
+        // [w seg, (w+1) seg); pass 1 counts (ballots), pass 2 writes at the warp's offset.  Zero
+        // keys are never taken, and with the zeros removed the radix select of the s~-th largest
+        // and the index order of ties are those of the full row.
+        const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+        const int64_t seg = (nJ + 3) / 4, lo = w * seg, hi = min(nJ, lo + seg);
+        int cnt = 0;
+        for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+            const int64_t j = j0 + lane;
+            const unsigned long long key = j < hi ? __ldg(keys + j) : 0ull;
+            cnt += __popc(__ballot_sync(0xffffffffu, key != 0ull));
+        }
+        if (lane == 0) warp_cnt[w] = cnt;
+        __syncthreads();
+        const int npos = warp_cnt[0] + warp_cnt[1] + warp_cnt[2] + warp_cnt[3];
+        if (npos <= KCOMP) {
+            unsigned long long *ck = kst;
+            int32_t *cj = reinterpret_cast<int32_t *>(kst + KCOMP);
+            int off = 0;
+            for (int q = 0; q < w; ++q) off += warp_cnt[q];
+            for (int64_t j0 = lo; j0 < hi; j0 += 32) {
+                const int64_t j = j0 + lane;
+                const unsigned long long key = j < hi ? __ldg(keys + j) : 0ull;
+                const unsigned int b = __ballot_sync(0xffffffffu, key != 0ull);
+                if (key != 0ull) {
+                    const int pos = off + __popc(b & ((1u << lane) - 1u));
+                    ck[pos] = key;
+                    cj[pos] = (int32_t)j;
+                }
+                off += __popc(b);
+            }
+            __syncthreads();
+            keys = ck;
+            jmap = cj;
+            nJ = npos;
+        }
     }
     const double th2 = theta2_of(theta_rel, theta_abs, kmax);
     if (g == 0 && threadIdx.x == 0 && th2_out) th2_out[0] = th2;
@@ -62,10 +104,15 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
             for (int q = threadIdx.x; q < 256; q += blockDim.x) hist[q] = 0u;
             __syncthreads();
             unsigned int nzero = 0u;
+#pragma unroll 8
             for (int64_t j = threadIdx.x; j < nJ; j += blockDim.x) {
                 const unsigned long long key = keys[j];
                 nzero += key == 0ull ? 1u : 0u;
-                if ((key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255ull], 1u);
+                // zero keys are never members (take needs kv > 0) and, once there are more than
+                // s~ positive keys, never hold rank s~: leaving them out of the histogram keeps
+                // the threshold and avoids serialising on bucket 0 (the streamed chunks, Z29,
+                // are mostly prefiltered zeros)
+                if (key != 0ull && (key & pmask) == prefix) atomicAdd(&hist[(key >> shift) & 255ull], 1u);
             }
             if (pass == 0) {                     // at most s~ positive keys: all of them are members
                 if (nzero) atomicAdd(&s_zero, nzero);
@@ -124,14 +171,29 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
         T = prefix;
         need_eq = k;                             // how many keys == T are taken (by index)
     }
-    // ordered pass: membership, threshold, output in ascending j, votes
+    // ordered pass: membership, threshold, output in ascending j, votes.  Keys are read OB blocks
+    // at a time (OB loads in flight per thread) and a group of blocks without any key that could
+    // be taken or counted (key >= the threshold) is skipped with one barrier
     int eq_run = 0, out_run = 0;
     int32_t *out = det_g + g * (int64_t)s_tilde;
-    for (int64_t base = 0; base < nJ; base += blockDim.x) {
+    constexpr int OB = 8;
+    for (int64_t base0 = 0; base0 < nJ; base0 += OB * (int64_t)blockDim.x) {
+        unsigned long long kb[OB];
+        bool any = false;
+#pragma unroll
+        for (int b = 0; b < OB; ++b) {
+            const int64_t j = base0 + (int64_t)b * blockDim.x + threadIdx.x;
+            kb[b] = j < nJ ? keys[j] : 0ull;
+            any |= kb[b] != 0ull && (by_min ? kb[b] >= Tmin : kb[b] >= T);
+        }
+        if (!__syncthreads_or(any)) continue;
+#pragma unroll 1
+        for (int b = 0; b < OB; ++b) {
+        const int64_t base = base0 + (int64_t)b * blockDim.x;
+        if (base >= nJ) break;
         const int64_t j = base + threadIdx.x;
-        unsigned long long key = 0ull;
-        bool valid = j < nJ;
-        if (valid) key = keys[j];
+        const bool valid = j < nJ;
+        const unsigned long long key = kb[b];
         const int is_eq = (!by_min && valid && key == T) ? 1 : 0;
         int eq_tot;
         const int eq_before = eq_run + block_exscan(is_eq, scan_sh, &eq_tot);
@@ -141,11 +203,13 @@ k_select(const double *__restrict__ kmin, int64_t nJ, const double *__restrict__
         int tot;
         const int pos = out_run + block_exscan(take, scan_sh, &tot);
         if (take) {
-            out[pos] = (int32_t)j;
-            atomicAdd(votes + j, 1);
+            const int32_t jj = jmap ? jmap[j] : (int32_t)j;
+            out[pos] = jj;
+            atomicAdd(votes + jj, 1);
         }
         eq_run += eq_tot;
         out_run += tot;
+        }
     }
     for (int q = out_run + threadIdx.x; q < s_tilde; q += blockDim.x) out[q] = -1;
     if (threadIdx.x == 0) n_det_g[g] = out_run;
@@ -410,7 +474,8 @@ extern "C" usfft_status usfft_detect_select(usfft_ctx *c, int64_t G_loc, int64_t
         USFFT_CHECK_LAUNCH(c);
         return USFFT_OK;
     }
-    const size_t kst = nJ <= KSTAGE ? sizeof(unsigned long long) * (size_t)nJ : 0;
+    const size_t kst = nJ <= KSTAGE ? sizeof(unsigned long long) * (size_t)nJ
+                                    : (sizeof(unsigned long long) + sizeof(int32_t)) * (size_t)KCOMP;
     if (usfft_status s = kernel_fit(c, k_select, 0, kst, nullptr)) return s;
     k_select<<<(unsigned)G_loc, 128, kst, c->stream>>>(kappa_min, nJ, kappa_max, s_tilde, theta_rel,
                                                         theta_abs, votes, det_g, n_det_g, theta2);

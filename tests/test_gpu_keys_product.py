@@ -70,3 +70,32 @@ def test_product_keys_bitexact_and_vs_oracle(B, ctx, G, M, L, n_prev, n1, t):
     B.usfft_lattice_keys_product(ctx, p, G, spectra, bd, nJ, j0, c, n1, out_p, W, m_p, kmin_off=s, tau=tau)
     assert torch.equal(out_p, out_g)
     assert bool((out_p[:, :s] == -1.0).all())
+
+
+@pytest.mark.parametrize("G,nJ,s,npos", [(4, 30000, 100, 1500), (3, 20000, 50, 5000), (2, 9000, 300, 250)])
+def test_select_sparse_rows_bitexact(B, ctx, G, nJ, s, npos):
+    """usfft_detect_select on rows longer than the staging limit whose keys are mostly 0 (the
+    streamed chunks after the carry prefilter, Z29): the compacted path (<= 2048 positive keys)
+    and the full-row path both give the oracle's D_g and votes exactly (ties by index, Z6)."""
+    rng = np.random.default_rng(nJ + npos)
+    km = np.zeros((G, nJ))
+    vals = np.r_[rng.random(40), 1e-13, 0.5, 0.5]            # repeated values: ties
+    for g in range(G):
+        idx = rng.choice(nJ, size=npos, replace=False)
+        km[g, idx] = rng.choice(vals, size=npos)
+    kmax_h = km.max()
+    th2_ref = odet.theta_squared(km, 1e-6)
+    D, votes_ref = odet.select(km, s, th2_ref)
+    kmd = torch.as_tensor(km, device="cuda")
+    votes = torch.empty(nJ, dtype=torch.int32, device="cuda")
+    det_g = torch.empty((G, s), dtype=torch.int32, device="cuda")
+    ndg = torch.empty(G, dtype=torch.int32, device="cuda")
+    th2 = torch.empty(1, dtype=torch.float64, device="cuda")
+    B.usfft_detect_select(ctx, G, nJ, kmd, torch.tensor([kmax_h], dtype=torch.float64, device="cuda"), s, 1e-6,
+                          0.0, votes, det_g, ndg, th2)
+    assert th2.item() == th2_ref
+    assert np.array_equal(votes.cpu().numpy(), votes_ref)
+    dg, nd = det_g.cpu().numpy(), ndg.cpu().numpy()
+    for g in range(G):
+        assert dg[g, :nd[g]].tolist() == D[g].tolist()
+        assert np.all(dg[g, nd[g]:] == -1)
