@@ -193,9 +193,11 @@ k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, i
               unsigned long long *__restrict__ kmax, const double *__restrict__ tau) {
     constexpr int KT = NT * KPT;
     const int Mh = M / 2 + 1;
-    extern __shared__ double ssk[];                      // [2][Mh] keys |F/M|^2 of a slice's bins
+    // [2][2M] keys |F/M|^2 of a slice: S[b] for every b = A + D in [0, 2M) (the bin b mod M,
+    // folded to M - b above M/2: |F[M-m]| = |F[m]| for real samples), so a candidate's key is one load
+    extern __shared__ double ssk[];
     const int AT = KT / n1 + 2;                          // a values a tile spans
-    int32_t *sA = reinterpret_cast<int32_t *>(ssk + 2 * Mh);   // [2][AT]: bins[l][a n1]
+    int32_t *sA = reinterpret_cast<int32_t *>(ssk + 4 * M);    // [2][AT]: bins[l][a n1]
     int32_t *sD = sA + 2 * AT;                                  // [2][n1]: bins[l][c] - bins[l][0] mod M
     __shared__ unsigned long long wmax[NT / 32];
     const int tid = threadIdx.x;
@@ -223,12 +225,20 @@ k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, i
         const double re = f.x * inv_m, im = f.y * inv_m;
         return __dadd_rn(__dmul_rn(re, re), __dmul_rn(im, im));
     };
+    auto put = [&](double *S, int i, double kk) {        // key of bin i (< Mh) at i, M-i, M+i, 2M-i
+        S[i] = kk;
+        S[M + i] = kk;
+        if (i > 0) {
+            S[M - i] = kk;
+            S[2 * M - i] = kk;
+        }
+    };
     auto stage = [&](int l, int buf) {                   // keys of lattice l's bins + bin terms -> buf
-        double *S = ssk + buf * Mh;
+        double *S = ssk + buf * 2 * M;
 #pragma unroll
         for (int k = 0; k < PF; ++k)
-            if (tid + k * NT < Mh) S[tid + k * NT] = key(pf[k]);
-        for (int i = tid + PF * NT; i < Mh; i += NT) S[i] = key(__ldg(src + (int64_t)l * Mh + i));
+            if (tid + k * NT < Mh) put(S, tid + k * NT, key(pf[k]));
+        for (int i = tid + PF * NT; i < Mh; i += NT) put(S, i, key(__ldg(src + (int64_t)l * Mh + i)));
         const int32_t *bl = bins + (int64_t)l * ldb;
         for (int i = tid; i < na; i += NT) sA[buf * AT + i] = __ldg(bl + (a_lo + i) * n1);
         const int32_t b00 = __ldg(bl);
@@ -244,17 +254,16 @@ k_kappa_tiled(const double2 *__restrict__ F, const int32_t *__restrict__ bins, i
     for (int l = 0; l < L; ++l) {
         const int buf = l & 1;
         if (l + 1 < L) fetch(l + 1);                      // in flight during the gathers below
-        const double *S = ssk + buf * Mh;
+        const double *S = ssk + buf * 2 * M;
         const int32_t *A = sA + buf * AT, *D = sD + buf * n1;
         int a = a_first, c = c_first;
 #pragma unroll
         for (int k = 0; k < KPT; ++k) {
             if (t0 + tid + (int64_t)k * NT >= t1) break;     // ragged tile end (a, c past the staged range)
             UB_CHECK(a >= 0 && a < na && c >= 0 && c < n1);
-            int b = A[a] + D[c];
-            b = b >= M ? b - M : b;
-            UB_CHECK(b >= 0 && b < M);
-            const double kk = S[b < Mh ? b : M - b];        // |F[M-b]| = |F[b]| (real input)
+            const int b = A[a] + D[c];
+            UB_CHECK(b >= 0 && b < 2 * M);
+            const double kk = S[b];
             km[k] = (l == 0) ? kk : fmin(km[k], kk);
             a += qa;
             c += qc;
@@ -591,7 +600,7 @@ extern "C" usfft_status usfft_lattice_keys_product(usfft_ctx *c, const usfft_lat
     USFFT_REQUIRE(c, spectra && bins && kappa_min && kappa_max, "NULL argument");
     const int64_t M = lat->M, Mh = M / 2 + 1;
     constexpr int NT = 512, KPT = 24, MINB = 1, KT = NT * KPT;
-    const size_t smem = sizeof(double) * 2 * (size_t)Mh + sizeof(int32_t) * 2 * (size_t)(KT / n1 + 2 + n1);
+    const size_t smem = sizeof(double) * 4 * (size_t)M + sizeof(int32_t) * 2 * (size_t)(KT / n1 + 2 + n1);
     if (nJ < 4 * Mh || smem > c->smem_optin || G_loc > 65535)
         return launch_keys(c, M, lat->L, G_loc, spectra, bins + j0, ldb, nJ, kappa_min, ldk, kappa_max, tau);
     auto kern = k_kappa_tiled<NT, KPT, MINB>;
