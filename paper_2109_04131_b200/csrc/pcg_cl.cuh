@@ -482,114 +482,130 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
         }
         __syncthreads();                                 // the coarse table (K region) is dead
+        CL_MARK(pset, 24);
         // ---- diagonals, zeroed grids, the dense maps -------------------------------------------
-        {   // every runtime grid (16-byte stores; oU is 16-byte aligned)
-            float4 *z4 = reinterpret_cast<float4 *>(sf + L::oU);
-            for (int e = tid; e < L::URUN / 4; e += NT) z4[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
-            for (int e = 4 * (L::URUN / 4) + tid; e < L::URUN; e += NT) sf[L::oU + e] = 0.0f;
-        }
-        for (int e = tid; e < L::F1; e += NT) {           // level-1 omega D^-1 (rows 0 .. HR1+1)
-            const int lrw = e / P1, s = e % P1, I = s < H1E ? 2 * s : s >= H1 ? 2 * (s - H1) + 1 : -1;
-            const int jl = lrw - 1, J = J0 + jl;
-            const bool in = I >= 1 && I < m1 && J >= 1 && J < m1 && jl >= 0 && jl <= HR1 + 1;
-            const float dv = in ? WH1[e] + WH1[e1(I - 1, jl)] + WV1[e] + WV1[e - P1] : 1.0f;
-            DI1[e] = in ? om / dv : 0.0f;
-        }
-#pragma unroll
-        for (int l = 2; l < LK; ++l) {
-            const int M = L::ml(l), Pq = L::Pl(l);
-            const float *wh = lc(l, LWH), *wv = lc(l, LWV);
-            float *di = lc(l, LDI);
-            for (int e = tid; e < L::Nl(l); e += NT) {
-                const int I = e % Pq, J = e / Pq;
-                const bool in = I >= 1 && I < M && J >= 1 && J < M;
-                di[e] = in ? om / (wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) : 0.0f;
+        // Two warp groups run concurrently: warps 0-3 build the dense map K (named barrier 1, 128
+        // threads), the other warps zero the runtime grids and form the level-1/2/3 diagonals.
+        // The groups touch disjoint shared memory; cluster barrier C joins them.
+        constexpr int KGT = 128;
+        auto kbar = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
+        if (tid < KGT) {
+            const int tk = tid;
+            for (int e = tk; e < NK; e += KGT) {
+                const int I = e % PK, J = e / PK;
+                const bool in = I >= 1 && I < mK && J >= 1 && J < mK;
+                const float dv = in ? WHK[e] + WHK[e - 1] + WVK[e] + WVK[e - PK] : 0.0f;
+                DK[e] = dv;
+                DIK[e] = in ? om / dv : 0.0f;
+                SK[e] = 0.0f;
             }
-        }
-        for (int e = tid; e < NK; e += NT) {
-            const int I = e % PK, J = e / PK;
-            const bool in = I >= 1 && I < mK && J >= 1 && J < mK;
-            const float dv = in ? WHK[e] + WHK[e - 1] + WVK[e] + WVK[e - PK] : 0.0f;
-            DK[e] = dv;
-            DIK[e] = in ? om / dv : 0.0f;
-            SK[e] = 0.0f;
-        }
-        __syncthreads();
-        if (warp == 0) {   // Gauss-Jordan inverse of the 4-cell operator (9 unknowns), by shuffles
-            const int ri = lane < UE ? lane : 0;
-            const int ia = ri % (mE - 1) + 1, ja = ri / (mE - 1) + 1, g = ja * PE + ia;
-            const float wr = WHE[g], wl = WHE[g - 1], wu = WVE[g], wd = WVE[g - PE];
-            float a[UE];
+            kbar();
+            CL_MARK(pset, 26);
+            if (warp == 0) {   // Gauss-Jordan inverse of the 4-cell operator (9 unknowns), by shuffles
+                const int ri = lane < UE ? lane : 0;
+                const int ia = ri % (mE - 1) + 1, ja = ri / (mE - 1) + 1, g = ja * PE + ia;
+                const float wr = WHE[g], wl = WHE[g - 1], wu = WVE[g], wd = WVE[g - PE];
+                float a[UE];
 #pragma unroll
-            for (int c = 0; c < UE; ++c)
-                a[c] = c == ri ? wr + wl + wu + wd
-                     : (c == ri + 1 && ia < mE - 1) ? -wr
-                     : (c == ri - 1 && ia > 1) ? -wl
-                     : (c == ri + (mE - 1) && ja < mE - 1) ? -wu
-                     : (c == ri - (mE - 1) && ja > 1) ? -wd : 0.0f;
+                for (int c = 0; c < UE; ++c)
+                    a[c] = c == ri ? wr + wl + wu + wd
+                         : (c == ri + 1 && ia < mE - 1) ? -wr
+                         : (c == ri - 1 && ia > 1) ? -wl
+                         : (c == ri + (mE - 1) && ja < mE - 1) ? -wu
+                         : (c == ri - (mE - 1) && ja > 1) ? -wd : 0.0f;
 #pragma unroll
-            for (int k = 0; k < UE; ++k) {
-                float prow[UE];
+                for (int k = 0; k < UE; ++k) {
+                    float prow[UE];
 #pragma unroll
-                for (int c = 0; c < UE; ++c) prow[c] = __shfl_sync(0xffffffffu, a[c], k);
-                const float piv = 1.0f / prow[k];
-                const float f = -a[k] * piv;
+                    for (int c = 0; c < UE; ++c) prow[c] = __shfl_sync(0xffffffffu, a[c], k);
+                    const float piv = 1.0f / prow[k];
+                    const float f = -a[k] * piv;
 #pragma unroll
-                for (int c = 0; c < UE; ++c) {
-                    if (lane == k) a[c] = c == k ? piv : prow[c] * piv;
-                    else a[c] = c == k ? f : fmaf(f, prow[c], a[c]);
+                    for (int c = 0; c < UE; ++c) {
+                        if (lane == k) a[c] = c == k ? piv : prow[c] * piv;
+                        else a[c] = c == k ? f : fmaf(f, prow[c], a[c]);
+                    }
+                }
+                __syncwarp();
+                if (lane < UE) {
+#pragma unroll
+                    for (int c = 0; c < UE; ++c) AI[lane * UE + c] = a[c];
                 }
             }
-            __syncwarp();
-            if (lane < UE) {
-#pragma unroll
-                for (int c = 0; c < UE; ++c) AI[lane * UE + c] = a[c];
+            // K = 2 Dw - Dw AK Dw + B^T AE^-1 B,  B = PE^T (I - AK Dw)  (pcg_mg.cuh)
+            for (int e = tk; e < UE * UK; e += KGT) {
+                const int r = e / UK, k = e % UK;
+                const int Ir = r % (mE - 1) + 1, Jr = r / (mE - 1) + 1;
+                const int Ik = k % (mK - 1) + 1, Jk = k / (mK - 1) + 1, ek = Jk * PK + Ik;
+                const float dwk = DIK[ek];
+                auto wr = [&](int Im, int Jm) -> float {
+                    const int ax = abs(Im - 2 * Ir), ay = abs(Jm - 2 * Jr);
+                    return (ax > 1 || ay > 1) ? 0.0f : (ax ? 0.5f : 1.0f) * (ay ? 0.5f : 1.0f);
+                };
+                float v = wr(Ik, Jk) * (1.0f - DK[ek] * dwk);
+                v = fmaf(wr(Ik + 1, Jk), WHK[ek] * dwk, v);
+                v = fmaf(wr(Ik - 1, Jk), WHK[ek - 1] * dwk, v);
+                v = fmaf(wr(Ik, Jk + 1), WVK[ek] * dwk, v);
+                v = fmaf(wr(Ik, Jk - 1), WVK[ek - PK] * dwk, v);
+                Bm[e] = v;
             }
-        }
-        // K = 2 Dw - Dw AK Dw + B^T AE^-1 B,  B = PE^T (I - AK Dw)  (pcg_mg.cuh)
-        for (int e = tid; e < UE * UK; e += NT) {
-            const int r = e / UK, k = e % UK;
-            const int Ir = r % (mE - 1) + 1, Jr = r / (mE - 1) + 1;
-            const int Ik = k % (mK - 1) + 1, Jk = k / (mK - 1) + 1, ek = Jk * PK + Ik;
-            const float dwk = DIK[ek];
-            auto wr = [&](int Im, int Jm) -> float {
-                const int ax = abs(Im - 2 * Ir), ay = abs(Jm - 2 * Jr);
-                return (ax > 1 || ay > 1) ? 0.0f : (ax ? 0.5f : 1.0f) * (ay ? 0.5f : 1.0f);
-            };
-            float v = wr(Ik, Jk) * (1.0f - DK[ek] * dwk);
-            v = fmaf(wr(Ik + 1, Jk), WHK[ek] * dwk, v);
-            v = fmaf(wr(Ik - 1, Jk), WHK[ek - 1] * dwk, v);
-            v = fmaf(wr(Ik, Jk + 1), WVK[ek] * dwk, v);
-            v = fmaf(wr(Ik, Jk - 1), WVK[ek - PK] * dwk, v);
-            Bm[e] = v;
-        }
-        __syncthreads();
-        for (int e = tid; e < UE * UK; e += NT) {        // C = AE^-1 B
-            const int r = e / UK, k = e % UK;
-            float v = 0.0f;
+            kbar();
+            CL_MARK(pset, 27);
+            for (int e = tk; e < UE * UK; e += KGT) {    // C = AE^-1 B
+                const int r = e / UK, k = e % UK;
+                float v = 0.0f;
 #pragma unroll
-            for (int c = 0; c < UE; ++c) v = fmaf(AI[r * UE + c], Bm[c * UK + k], v);
-            Cm[e] = v;
-        }
-        __syncthreads();
-        auto kix = [](int col, int row) -> int { return row * L::KS + col; };     // K[row][col]
-        for (int e = tid; e < UK * UK; e += NT) {        // B^T C
-            const int i = e % UK, k = e / UK;
-            float v = 0.0f;
+                for (int c = 0; c < UE; ++c) v = fmaf(AI[r * UE + c], Bm[c * UK + k], v);
+                Cm[e] = v;
+            }
+            kbar();
+            CL_MARK(pset, 28);
+            auto kix = [](int col, int row) -> int { return row * L::KS + col; };     // K[row][col]
+            for (int e = tk; e < UK * UK; e += KGT) {    // B^T C
+                const int i = e % UK, k = e / UK;
+                float v = 0.0f;
 #pragma unroll
-            for (int r = 0; r < UE; ++r) v = fmaf(Bm[r * UK + i], Cm[r * UK + k], v);
-            Kt[kix(k, i)] = v;
-        }
-        __syncthreads();
-        for (int e = tid; e < 5 * UK; e += NT) {         // + 2 Dw - Dw AK Dw (5-point), row i
-            const int i = e % UK, d = e / UK;
-            const int Ii = i % (mK - 1) + 1, Ji = i / (mK - 1) + 1, ei = Ji * PK + Ii;
-            const float dwi = DIK[ei];
-            if (d == 0) Kt[kix(i, i)] += fmaf(-dwi * DK[ei], dwi, 2.0f * dwi);
-            else if (d == 1 && Ii < mK - 1) Kt[kix(i + 1, i)] += dwi * WHK[ei] * DIK[ei + 1];
-            else if (d == 2 && Ii > 1) Kt[kix(i - 1, i)] += dwi * WHK[ei - 1] * DIK[ei - 1];
-            else if (d == 3 && Ji < mK - 1) Kt[kix(i + (mK - 1), i)] += dwi * WVK[ei] * DIK[ei + PK];
-            else if (d == 4 && Ji > 1) Kt[kix(i - (mK - 1), i)] += dwi * WVK[ei - PK] * DIK[ei - PK];
+                for (int r = 0; r < UE; ++r) v = fmaf(Bm[r * UK + i], Cm[r * UK + k], v);
+                Kt[kix(k, i)] = v;
+            }
+            kbar();
+            for (int e = tk; e < 5 * UK; e += KGT) {     // + 2 Dw - Dw AK Dw (5-point), row i
+                const int i = e % UK, d = e / UK;
+                const int Ii = i % (mK - 1) + 1, Ji = i / (mK - 1) + 1, ei = Ji * PK + Ii;
+                const float dwi = DIK[ei];
+                if (d == 0) Kt[kix(i, i)] += fmaf(-dwi * DK[ei], dwi, 2.0f * dwi);
+                else if (d == 1 && Ii < mK - 1) Kt[kix(i + 1, i)] += dwi * WHK[ei] * DIK[ei + 1];
+                else if (d == 2 && Ii > 1) Kt[kix(i - 1, i)] += dwi * WHK[ei - 1] * DIK[ei - 1];
+                else if (d == 3 && Ji < mK - 1) Kt[kix(i + (mK - 1), i)] += dwi * WVK[ei] * DIK[ei + PK];
+                else if (d == 4 && Ji > 1) Kt[kix(i - (mK - 1), i)] += dwi * WVK[ei - PK] * DIK[ei - PK];
+            }
+            CL_MARK(pset, 25);
+        } else {
+            const int tz = tid - KGT;
+            constexpr int NZ = NT - KGT;
+            {   // every runtime grid (16-byte stores; oU is 16-byte aligned)
+                float4 *z4 = reinterpret_cast<float4 *>(sf + L::oU);
+                for (int e = tz; e < L::URUN / 4; e += NZ) z4[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
+                for (int e = 4 * (L::URUN / 4) + tz; e < L::URUN; e += NZ) sf[L::oU + e] = 0.0f;
+            }
+            for (int e = tz; e < L::F1; e += NZ) {       // level-1 omega D^-1 (rows 0 .. HR1+1)
+                const int lrw = e / P1, s = e % P1, I = s < H1E ? 2 * s : s >= H1 ? 2 * (s - H1) + 1 : -1;
+                const int jl = lrw - 1, J = J0 + jl;
+                const bool in = I >= 1 && I < m1 && J >= 1 && J < m1 && jl >= 0 && jl <= HR1 + 1;
+                const float dv = in ? WH1[e] + WH1[e1(I - 1, jl)] + WV1[e] + WV1[e - P1] : 1.0f;
+                DI1[e] = in ? om / dv : 0.0f;
+            }
+#pragma unroll
+            for (int l = 2; l < LK; ++l) {
+                const int M = L::ml(l), Pq = L::Pl(l);
+                const float *wh = lc(l, LWH), *wv = lc(l, LWV);
+                float *di = lc(l, LDI);
+                for (int e = tz; e < L::Nl(l); e += NZ) {
+                    const int I = e % Pq, J = e / Pq;
+                    const bool in = I >= 1 && I < M && J >= 1 && J < M;
+                    di[e] = in ? om / (wh[e] + wh[e - 1] + wv[e] + wv[e - Pq]) : 0.0f;
+                }
+            }
         }
         cluster_barrier();   // C: every CTA's grids are zeroed before any neighbour sends into them
         CL_MARK(pset, 23);
