@@ -3,7 +3,7 @@
 //
 // Same discretisation (Z11/Z12), the same Chronopoulos-Gear CG (one reduction per iteration,
 // x0 = 0, stop on ||r||_2 <= tol ||b||_2, Z13) and the same preconditioner family as
-// pcg_mg.cuh: one symmetric V(1,1) cycle, damped Jacobi (omega = 0.8) smoothing, bilinear P,
+// pcg_mg.cuh: one symmetric V(1,1) cycle, damped Jacobi smoothing (omega = 0.8 on the fine level, 1 on the coarse levels), bilinear P,
 // R = P^T, coarse operators rediscretised from the fine per-triangle coefficients, and the
 // bottom two levels (8 and 4 cells per side) as the fixed dense map K of pcg_mg.cuh.
 //
@@ -191,7 +191,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr int mK = L::mK, PK = L::PK, NK = L::NK, UK = L::UK, HK = L::HK;
     constexpr int mE = L::mE, PE = L::PE, UE = L::UE, ATR = L::ATR, JC = L::JC, H1E = L::H1E;
     constexpr int m2 = L::ml(2), P2 = L::Pl(2);
-    constexpr float om = 0.8f;                           // kMgOmega
+    constexpr float om = (float)kMgOmegaCoarse;          // coarse-level Jacobi weight (the fine level: kMgOmega)
     extern __shared__ __align__(16) float sf[];
     __shared__ double th_amp[kMaxD];
     __shared__ alignas(8) unsigned long long mbar[6];

@@ -6,7 +6,7 @@
 //     p = u + beta p;  s = w + beta s;  x += alpha p;  r -= alpha s,
 // stopping on rho = ||r||_2^2 <= tol^2 ||b||_2^2 (Z13).
 // M^-1 is one symmetric V(1,1) cycle over four nested "/" meshes (n, n/2, n/4, n/8 cells): damped
-// Jacobi (omega = 0.8) pre- and post-smoothing on levels 0-2, bilinear prolongation P,
+// Jacobi (omega = 0.8 on level 0, 1 on levels 1-2) pre- and post-smoothing, bilinear prolongation P,
 // restriction R = P^T, coarse operators by rediscretisation of the same P1 problem, and an exact
 // solve on the coarsest level with its dense inverse (formed once per sample by Gauss-Jordan;
 // (n/8-1)^2 = 9 unknowns at n = 32).  Same smoother before and after and R = P^T make the cycle
@@ -34,7 +34,9 @@
 
 namespace usfft {
 
-constexpr double kMgOmega = 0.8;
+// damped-Jacobi weights of the V(1,1) cycle: 0.8 on the fine level, 1.0 on every coarse level
+// (tools/mg_omega_study.py: 14 -> 13 CG iterations at config 5, 13.6 -> 13 at config 3, never more)
+constexpr double kMgOmega = 0.8, kMgOmegaCoarse = 1.0;
 
 // 1/a for positive normal a: hardware seed (MUFU.RCP64H) refined by three Newton steps, no
 // special-case branches (the CG scalars are positive and far from the fp64 range limits while
@@ -256,14 +258,14 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 const int J = e / P1, s = e % P1, I = s < H1 ? 2 * s : 2 * (s - H1) + 1;
                 const bool in = I >= 1 && I < m1 && J >= 1 && J < m1;
                 const double dv = in ? WH1[e] + WH1[J * P1 + L::col1s(I - 1)] + WV1[e] + WV1[e - P1] : 1.0;
-                DI1[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+                DI1[e] = in ? kMgOmegaCoarse * (1.0 / dv) : 0.0;
             }
             for (int e = ht; e < N2; e += HS) {
                 const int I = e % P2, J = e / P2;
                 const bool in = I >= 1 && I < m2 && J >= 1 && J < m2;
                 const double dv = in ? WH2[e] + WH2[e - 1] + WV2[e] + WV2[e - P2] : 0.0;
                 D2[e] = dv;
-                DI2[e] = in ? kMgOmega * (1.0 / dv) : 0.0;
+                DI2[e] = in ? kMgOmegaCoarse * (1.0 / dv) : 0.0;
             }
         }
 #pragma unroll

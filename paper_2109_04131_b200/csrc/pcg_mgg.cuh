@@ -2,7 +2,7 @@
 // CTA per sample, grids in a per-CTA global scratch region (L1/L2 resident at n = 64).
 //
 // Same P1 discretisation (Z11/Z12) and the same preconditioner family as pcg_mg.cuh: a symmetric
-// V(1,1) cycle with damped Jacobi (omega = 0.8) smoothing, bilinear prolongation P, restriction
+// V(1,1) cycle with damped Jacobi smoothing (omega = 0.8 fine, 1 coarse), bilinear prolongation P, restriction
 // R = P^T and rediscretised coarse operators whose coefficients are lookups into the fine
 // per-triangle table (every coarse centroid is a fine centroid), down to the mesh of 4 cells per
 // side whose 9 unknowns are solved exactly with a dense inverse (Gauss-Jordan once per sample).
@@ -158,7 +158,7 @@ k_pcg_mgg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes
             const double *wh = arr(l, WH), *wv = arr(l, WV);
             double *di = arr(l, DI);
             for (int e = tid; e < Pl * Pl; e += T)
-                di[e] = interior(e, Pl, m) ? kMgOmega / (wh[e] + wh[e - 1] + wv[e] + wv[e - Pl]) : 0.0;
+                di[e] = interior(e, Pl, m) ? (l == 0 ? kMgOmega : kMgOmegaCoarse) / (wh[e] + wh[e - 1] + wv[e] + wv[e - Pl]) : 0.0;
         }
         if (tid < UL * UL) {                                          // 3 x 3 interior of the 5 x 5 grid
             const double *wh = arr(L, WH), *wv = arr(L, WV);
