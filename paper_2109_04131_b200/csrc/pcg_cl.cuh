@@ -18,8 +18,8 @@
 // A sample of n = 128 (16129 unknowns) needs ~0.5 MB of fp64 CG state, more than one SM holds, so
 // a cluster of CS CTAs (CS = 8 at n = 128, 4 at n = 64) shares it; CTA r owns the fine rows
 // j0+1 .. j0+HR, j0 = r HR, HR = n / CS = 16:
-//  * level 0 (fine): each thread keeps a 2 x 2 block of nodes (x, r, p, s and the couplings in
-//    fp64, their fp32 copies and omega D^-1) in registers; the values a stencil needs are
+//  * level 0 (fine): each thread keeps a 2 x 2 block of nodes: r and the couplings (fp64, with
+//    fp32 copies and omega D^-1) in registers, x, p, s in shared memory; stencil values are
 //    published in shared memory (fp32, split rows: even columns, then odd) with halo rows
 //    filled by the neighbour CTAs;
 //  * level 1 (n/2 cells): distributed the same way;
@@ -51,12 +51,22 @@
 #pragma once
 #include <cooperative_groups.h>
 
+// Per-mesh register choice (measured on the B200, tools/cl_variants.py): at n = 64 (two CTAs per SM)
+// t and z0 are re-read from the grids they were published to at the post-smoothing instead of
+// held in registers across the coarse levels (39.0 -> 37.6 ms at config 3; at n = 128 this costs
+// 2 %).  The CG direction p lives in shared memory next to x and s on both meshes (n = 128:
+// 533.5 -> 524.9 ms at config 5).
+#ifndef USFFT_CL_TZ
+#define USFFT_CL_TZ(nn) ((nn) == 64)
+#endif
+
 namespace usfft {
 
 template <int NN, int CS>
 struct ClC {
     static constexpr int n = NN, nx = n - 1, np = n + 1, HE = n / 2 + 1;
     static constexpr int HR = NN / CS;                       // fine rows per CTA
+    static constexpr bool TZ = USFFT_CL_TZ(NN);
     static constexpr int BC = 2, BR = 2, LX = n / 2, NRG = HR / BR, NT = LX * NRG, NWARP = NT / 32;
     static constexpr int FRW = HR + 3, FR = FRW * np;        // fine grid rows 0 .. HR+2 (local)
     // level-1 split rows: even columns at slots 0 .. m1/2, odd columns from slot H1 = 48 (16 banks
@@ -106,9 +116,10 @@ struct ClC {
     static constexpr int USZ = URUN > UAT ? (URUN > USTG ? URUN : USTG) : (UAT > USTG ? UAT : USTG);
     static constexpr int oRedF = (oU + USZ + 3) & ~3;        // fp64 [2][CS][4] cluster partials, [4][NWARP]
                                                              // (slot 3: the early (r,r) check, X6)
-    // then fp64: the cluster partials [2][CS][4] and CTA partials [4][NWARP], the CG iterate x
-    // and s = A p [BR*BC][NT] each (thread-major: touched once per iteration, so outside the registers)
-    __host__ __device__ static constexpr size_t bytes() { return 4 * (size_t)oRedF + 8 * (size_t)(8 * CS + 4 * NWARP + 2 * BR * BC * NT); }
+    // then fp64: the cluster partials [2][CS][4] and CTA partials [4][NWARP], the CG iterate x,
+    // s = A p and the direction p, [BR*BC][NT] each (thread-major: touched once per iteration, so
+    // outside the registers)
+    __host__ __device__ static constexpr size_t bytes() { return 4 * (size_t)oRedF + 8 * (size_t)(8 * CS + 4 * NWARP + 3 * BR * BC * NT); }
     // setup: the coarse-level triangle coefficients (levels 2 .. LK+1, lower then upper plane)
     __host__ __device__ static constexpr int ctoff(int l) {
         int o = 0;
@@ -191,6 +202,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr int mK = L::mK, PK = L::PK, NK = L::NK, UK = L::UK, HK = L::HK;
     constexpr int mE = L::mE, PE = L::PE, UE = L::UE, ATR = L::ATR, JC = L::JC, H1E = L::H1E;
     constexpr int m2 = L::ml(2), P2 = L::Pl(2);
+    constexpr bool TZ = L::TZ;
     constexpr float om = (float)kMgOmegaCoarse;          // coarse-level Jacobi weight (the fine level: kMgOmega)
     extern __shared__ __align__(16) float sf[];
     __shared__ double th_amp[kMaxD];
@@ -267,7 +279,8 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr int YP = L::YP, CPT = L::CPT, KJ = L::KJ;
     double *Xg = cred + 8 * CS + 4 * NWARP;                                     // x, [BR*BC][NT]
     double *Sg = Xg + BR * BC * NT;                                             // s, [BR*BC][NT]
-    double *XP = Sg + BR * BC * NT, *YPs = XP + (size_t)pd * 2 * n;
+    double *Pg = Sg + BR * BC * NT;                                             // p, [BR*BC][NT]
+    double *XP = Pg + BR * BC * NT, *YPs = XP + (size_t)pd * 2 * n;
     for (int e = tid; e < pd * 2 * n; e += NT) {
         const int j = e / (2 * n), c = e - j * 2 * n, up = c >= n, cc = up ? c - n : c;
         XP[e] = __ldg(S + j * W + 3 * cc + (up ? 1 : 2));
@@ -695,13 +708,13 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         };
 
         // ---- CG init: x = 0, r = b, z0 = omega D^-1 b -----------------------------------------------
-        double pr[BR][BC], r[BR][BC];
+        double r[BR][BC];
         float z0[BR][BC];
 #pragma unroll
         for (int q = 0; q < BR; ++q)
 #pragma unroll
             for (int c = 0; c < BC; ++c) {
-                Xg[(q * BC + c) * NT + tid] = Sg[(q * BC + c) * NT + tid] = pr[q][c] = 0.0;
+                Xg[(q * BC + c) * NT + tid] = Sg[(q * BC + c) * NT + tid] = Pg[(q * BC + c) * NT + tid] = 0.0;
                 const int j = j0 + row0 + q + 1;
                 r[q][c] = !valid(q, c) ? 0.0 : Bt ? __ldg(Bt + (j - 1) * nx + col0 + c) : (double)j * inv_n3;
                 z0[q][c] = di0[q][c] * (float)r[q][c];
@@ -720,7 +733,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             __syncthreads();
             xwait(0);                                    // X1: z0 halos, r of the row above
             CL_MARK(pit, 1);
-            float t[BR][BC];                             // fine residual r - A z0 of the own nodes
+            float t[BR][BC];                             // fine residual t = r - A z0 of the own nodes -> G1
             {
                 float az[BR][BC];
                 apply32(G0, z0, az);
@@ -903,7 +916,9 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                         a = fmaf(-ce[q][c], pw(c - 1, q), a);
                         a = fmaf(-cn[q + 1][c], pw(c, q + 1), a);
                         a = fmaf(-cn[q][c], pw(c, q - 1), a);
-                        uu[q][c] = valid(q, c) ? fmaf(di0[q][c], t[q][c] - a, z0[q][c] + ec) : 0.0f;
+                        // TZ: t and z0 of the own node from the grids they were published to
+                        uu[q][c] = !valid(q, c) ? 0.0f : TZ ? fmaf(di0[q][c], G1[fe(c, q)] - a, G0[fe(c, q)] + ec)
+                                                            : fmaf(di0[q][c], t[q][c] - a, z0[q][c] + ec);
                     }
             }
             CL_MARK(pit, 10);
@@ -990,8 +1005,8 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             for (int q = 0; q < BR; ++q)
 #pragma unroll
                 for (int c = 0; c < BC; ++c) {
-                    const double pn = fma(beta, pr[q][c], (double)uu[q][c]);
-                    pr[q][c] = pn;
+                    const double pn = fma(beta, Pg[(q * BC + c) * NT + tid], (double)uu[q][c]);
+                    Pg[(q * BC + c) * NT + tid] = pn;
                     const double sn = fma(beta, Sg[(q * BC + c) * NT + tid], w[q][c]);
                     Sg[(q * BC + c) * NT + tid] = sn;
                     Xg[(q * BC + c) * NT + tid] = fma(alpha, pn, Xg[(q * BC + c) * NT + tid]);
