@@ -253,6 +253,16 @@ k_fft_rader_r(const double *__restrict__ u, const SlabParams S, int64_t G_loc, i
                 xa[k] = i < M ? at(r0, src0, i) : 0.0;
                 xb[k] = i < M ? at(r1, src1, i) : 0.0;
             }
+            // the next round's rows towards L2 while this pair is transformed (one 128-byte line per
+            // thread and step; the rows of a pair are contiguous within a slab)
+            const int64_t pn = ((rd + 1) * gridDim.x + blockIdx.x) * NPAIR + pi;
+            if (one_slab && pn < pairs) {
+                const int64_t rn = row0(pn);
+                const char *nx = reinterpret_cast<const char *>(u + rn * (int64_t)M);
+                const int nbytes = (row1(pn) >= 0 ? 2 : 1) * M * 8;
+                for (int o = t * 128; o < nbytes; o += GROUP * 128)
+                    asm volatile("prefetch.global.L2 [%0];" :: "l"(nx + o));
+            }
 #pragma unroll
             for (int k = 0; k < PER; ++k)
                 if (t + k * GROUP < M) buf[t + k * GROUP] = make_double2(xa[k], xb[k]);
