@@ -41,7 +41,8 @@
 // A transfer of exchange k for CG iteration i+1 cannot start before every CTA has sent its X5
 // partials of iteration i, which every CTA does only after its last read of iteration i's data:
 // the X5 all-to-all orders all buffer reuse (its own slots are double-buffered).  The per-sample
-// setup (coefficient tables, coarse operators, K) uses three cluster barriers.  Reductions and
+// setup (coefficient tables, coarse operators, K) uses three cluster barriers, each split into an
+// early arrive and a late wait.  Reductions and
 // the order of every sum are fixed, so a sample's result does not depend on the cluster that
 // solved it or on the launch split.
 //
@@ -86,8 +87,12 @@ struct ClC {
     static constexpr int ATR = HR + 6;                       // coefficient-table cell rows j0-2 .. j0+HR+3
     static constexpr int JC = 8;                             // psi factors staged JC terms at a time
     static constexpr int CPT = NT / n, KJ = (((ATR + CPT - 1) / CPT) + 1) & ~1, YP = CPT * KJ;
-    // resident psi slice (fp64, after the partials): X[j][2n] (lower, upper abscissae), Y[j][2][YP]
-    __host__ __device__ static constexpr size_t psi_bytes(int d) { return 8 * (size_t)d * (2 * n + 2 * YP); }
+    // resident psi slice (fp64, after the partials): X[j][2n] (lower, upper abscissae), Y[j][2][YP];
+    // term strides XS, YS = 4 mod 16 doubles, so the DMMA fragment loads of the coefficient
+    // table (4 consecutive terms x 8 consecutive columns / rows per warp) are conflict-free
+    static constexpr int XS = 2 * n + 4, YS = 2 * YP + 4;
+    static_assert(YP % 8 == 0 && YP >= ATR && XS % 16 == 4 && YS % 16 == 4 && NWARP % 2 == 0 && n / 8 == NWARP, "coefficient-table tiling");
+    __host__ __device__ static constexpr size_t psi_bytes(int d) { return 8 * (size_t)d * (XS + YS); }
     // ---- shared memory, in 4-byte units ----
     // persistent (written by the setup, read by every iteration), fp32
     static constexpr int oWH1 = 0, oWV1 = F1, oDI1 = 2 * F1;
@@ -132,6 +137,13 @@ struct ClC {
 
 __device__ __forceinline__ void cluster_barrier() {
     asm volatile("barrier.cluster.arrive.release.aligned;\n\tbarrier.cluster.wait.acquire.aligned;" ::: "memory");
+}
+// split form: every thread arrives (releasing its writes), works on, and waits later
+__device__ __forceinline__ void cluster_arrive() {
+    asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
+}
+__device__ __forceinline__ void cluster_wait() {
+    asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
 __device__ __forceinline__ unsigned cluster_id_x() {
     unsigned v;
@@ -205,7 +217,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr bool TZ = L::TZ;
     constexpr float om = (float)kMgOmegaCoarse;          // coarse-level Jacobi weight (the fine level: kMgOmega)
     extern __shared__ __align__(16) float sf[];
-    __shared__ double th_amp[kMaxD];
+    __shared__ double th_amp2[2][kMaxD];                 // amp_j theta_j(y_j) of the current / the next sample
     __shared__ alignas(8) unsigned long long mbar[6];
     cg::cluster_group cluster = cg::this_cluster();
     const int rank = (int)cluster_rank();
@@ -280,16 +292,25 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     double *Xg = cred + 8 * CS + 4 * NWARP;                                     // x, [BR*BC][NT]
     double *Sg = Xg + BR * BC * NT;                                             // s, [BR*BC][NT]
     double *Pg = Sg + BR * BC * NT;                                             // p, [BR*BC][NT]
-    double *XP = Pg + BR * BC * NT, *YPs = XP + (size_t)pd * 2 * n;
+    constexpr int XS = L::XS, YS = L::YS;
+    double *XP = Pg + BR * BC * NT, *YPs = XP + (size_t)pd * XS;
     for (int e = tid; e < pd * 2 * n; e += NT) {
         const int j = e / (2 * n), c = e - j * 2 * n, up = c >= n, cc = up ? c - n : c;
-        XP[e] = __ldg(S + j * W + 3 * cc + (up ? 1 : 2));
+        XP[j * XS + c] = __ldg(S + j * W + 3 * cc + (up ? 1 : 2));
     }
     for (int e = tid; e < pd * 2 * YP; e += NT) {
         const int j = e / (2 * YP), c = e - j * 2 * YP, up = c >= YP, rl = up ? c - YP : c;
         const int cj = min(max(j0 - 2 + rl, 0), n - 1);
-        YPs[e] = rl < ATR ? __ldg(Sy0 + j * W + 3 * cj + (up ? 2 : 1)) : 0.0;
+        YPs[j * YS + c] = rl < ATR ? __ldg(Sy0 + j * W + 3 * cj + (up ? 2 : 1)) : 0.0;
     }
+    // amp_j theta_j(y_j) of sample bl of this launch; the first sample's here, every later one
+    // during the previous sample's setup (by warps that wait for the K map there)
+    auto theta_amp = [&](int64_t bl, int j, double *dst) {
+        const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b0 + bl, j);
+        dst[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
+    };
+    if (tid < Q.d && (int64_t)cluster_id_x() < nb) theta_amp(cluster_id_x(), tid, th_amp2[0]);
+    int tbuf = 0;
 
     for (int64_t bl = cluster_id_x(); bl < nb; bl += cluster_count_x()) {
         const int64_t b = b0 + bl;
@@ -297,37 +318,47 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         (void)pset;
         CL_MARK(pset, 20);
         // ---- K3: coefficients of the triangles of cell rows j0-2 .. j0+HR+3 --------------------
-        for (int j = tid; j < Q.d; j += NT) {
-            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
-            th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
-        }
+        const double *th_amp = th_amp2[tbuf];
+        double *th_next = th_amp2[tbuf ^ 1];
+        tbuf ^= 1;
+        cluster_arrive();                                // A: this CTA is done with the previous sample
         __syncthreads();
-        if (pd) {   // aT from the resident slice: thread = (column, KJ consecutive rows), Y pairs as 16-byte loads
-            const int ci = tid % n, rs = tid / n;
-            double slo[KJ], sup[KJ];
+        CL_MARK(pset, 29);
+        if (pd) {   // aT[plane] = Y_plane^T . (amp theta X_plane) from the resident slice: two [YP x d] . [d x n]
+            // products on the fp64 tensor pipe (DMMA m8n8k4: A a = A[lane/4][lane%4], B b =
+            // B[lane%4][lane/4], C {c0, c1} = C[lane/4][2 (lane%4) + {0, 1}]); warp = (plane, two
+            // column tiles) x all YP / 8 row tiles, terms four at a time (zero beyond d)
+            constexpr int MT = YP / 8, NW2 = NWARP / 2;
+            const int pl = warp / NW2, nt0 = 2 * (warp % NW2), fr = lane >> 2, fk = lane & 3;
+            double acc[MT][2][2];
 #pragma unroll
-            for (int k = 0; k < KJ; ++k) slo[k] = sup[k] = 0.0;
+            for (int m = 0; m < MT; ++m) acc[m][0][0] = acc[m][0][1] = acc[m][1][0] = acc[m][1][1] = 0.0;
+            const double *xb = XP + pl * n + nt0 * 8 + fr, *yb = YPs + pl * YP + fr;
 #pragma unroll 2
-            for (int j = 0; j < pd; ++j) {
-                const double am = th_amp[j];
-                const double tlo = am * XP[j * 2 * n + ci], tup = am * XP[j * 2 * n + n + ci];
-                const double2 *yl = reinterpret_cast<const double2 *>(YPs + j * 2 * YP + rs * KJ);
-                const double2 *yu = reinterpret_cast<const double2 *>(YPs + j * 2 * YP + YP + rs * KJ);
+            for (int jk = 0; jk < pd; jk += 4) {
+                const int j = jk + fk;
+                const bool in = j < pd;
+                const double am = in ? th_amp[j] : 0.0;
+                const double bq0 = in ? am * xb[j * XS] : 0.0, bq1 = in ? am * xb[j * XS + 8] : 0.0;
 #pragma unroll
-                for (int k = 0; k < KJ / 2; ++k) {
-                    const double2 a = yl[k], b2 = yu[k];
-                    slo[2 * k] = fma(tlo, a.x, slo[2 * k]);
-                    slo[2 * k + 1] = fma(tlo, a.y, slo[2 * k + 1]);
-                    sup[2 * k] = fma(tup, b2.x, sup[2 * k]);
-                    sup[2 * k + 1] = fma(tup, b2.y, sup[2 * k + 1]);
+                for (int m = 0; m < MT; ++m) {
+                    const double a = in ? yb[j * YS + m * 8] : 0.0;
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(acc[m][0][0]), "+d"(acc[m][0][1]) : "d"(a), "d"(bq0));
+                    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                                 : "+d"(acc[m][1][0]), "+d"(acc[m][1][1]) : "d"(a), "d"(bq1));
                 }
             }
 #pragma unroll
-            for (int k = 0; k < KJ; ++k) {
-                const int rl = rs * KJ + k, cj = j0 - 2 + rl;
+            for (int m = 0; m < MT; ++m) {
+                const int rl = m * 8 + fr, cj = j0 - 2 + rl;
                 if (rl < ATR && cj >= 0 && cj < n) {
-                    aT[rl * n + ci] = Q.form == 0 ? 1.0 + slo[k] : exp(slo[k]);              // lower
-                    aT[(ATR + rl) * n + ci] = Q.form == 0 ? 1.0 + sup[k] : exp(sup[k]);      // upper
+#pragma unroll
+                    for (int t2 = 0; t2 < 2; ++t2) {
+                        const double v0 = Q.form == 0 ? 1.0 + acc[m][t2][0] : exp(acc[m][t2][0]);
+                        const double v1 = Q.form == 0 ? 1.0 + acc[m][t2][1] : exp(acc[m][t2][1]);
+                        *reinterpret_cast<double2 *>(aT + (pl * ATR + rl) * n + (nt0 + t2) * 8 + 2 * fk) = make_double2(v0, v1);
+                    }
                 }
             }
         } else {   // aT[plane][cj - (j0-2)][ci] = sum_j amp_j theta_j X_j Y_j: thread = (column, row set); the
@@ -386,7 +417,9 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
             }
         }
-        cluster_barrier();                               // A: previous sample done everywhere; own table complete
+        CL_MARK(pset, 30);
+        __syncthreads();                                 // own table complete
+        cluster_wait();                                  // A: previous sample done everywhere
         CL_MARK(pset, 21);
         // a of T_lo / T_up of cell (ci, cj) of the level with cells of width 2^sh h: the fine
         // triangle with the same centroid (pcg_mg.cuh), from the local table
@@ -396,6 +429,27 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             UB_CHECK(fi >= 0 && fi < n && fj - (j0 - 2) >= 0 && fj - (j0 - 2) < ATR);
             return aT[(pl * ATR + fj - (j0 - 2)) * n + fi];
         };
+        {   // coarse triangle coefficients (levels 2 .. LK+1) whose fine triangle is in the own rows,
+            // sent to every CTA's coarse table
+            constexpr int NC = L::ctoff(LK + 2) / 2;       // coarse cells of all levels
+            for (int e = tid; e < 2 * NC; e += NT) {
+                const int up = e >= NC, q = up ? e - NC : e;
+                int l = 2, base = 0;
+                while (q - base >= L::ml(l) * L::ml(l)) {
+                    base += L::ml(l) * L::ml(l);
+                    ++l;
+                }
+                const int m = L::ml(l), cell = q - base, ci = cell % m, cj = cell / m;
+                const int p = 1 << l, rb = up ? 2 * p : p, fj = cj * p + rb / 3;
+                if (fj / HR != rank) continue;
+                const float v = (float)fcl(ci, cj, up, l);
+                const int dst = L::ctoff(l) + (up ? m * m : 0) + cell;
+                UB_CHECK(dst >= 0 && dst < L::ctoff(LK + 2));
+#pragma unroll
+                for (int k = 0; k < CS; ++k) cluster.map_shared_rank(ctab, k)[dst] = v;
+            }
+        }
+        cluster_arrive();                                // B: own coarse coefficients pushed
         // fine couplings of the own block (ring edges included), fp64 and their fp32 copies
         double cE[BR][BC + 1], cN[BR + 1][BC];
         float ce[BR][BC + 1], cn[BR + 1][BC];
@@ -438,27 +492,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             WV1[e] = (jl <= HR1 + 1 && J >= 0 && J < m1 && I >= 1 && I < m1)
                          ? (float)(0.5 * (fcl(I, J, 1, 1) + fcl(I - 1, J, 0, 1))) : 0.0f;
         }
-        {   // coarse triangle coefficients (levels 2 .. LK+1) whose fine triangle is in the own rows,
-            // sent to every CTA's coarse table
-            constexpr int NC = L::ctoff(LK + 2) / 2;       // coarse cells of all levels
-            for (int e = tid; e < 2 * NC; e += NT) {
-                const int up = e >= NC, q = up ? e - NC : e;
-                int l = 2, base = 0;
-                while (q - base >= L::ml(l) * L::ml(l)) {
-                    base += L::ml(l) * L::ml(l);
-                    ++l;
-                }
-                const int m = L::ml(l), cell = q - base, ci = cell % m, cj = cell / m;
-                const int p = 1 << l, rb = up ? 2 * p : p, fj = cj * p + rb / 3;
-                if (fj / HR != rank) continue;
-                const float v = (float)fcl(ci, cj, up, l);
-                const int dst = L::ctoff(l) + (up ? m * m : 0) + cell;
-                UB_CHECK(dst >= 0 && dst < L::ctoff(LK + 2));
-#pragma unroll
-                for (int k = 0; k < CS; ++k) cluster.map_shared_rank(ctab, k)[dst] = v;
-            }
-        }
-        cluster_barrier();                               // B: every coarse table complete; aT dead
+        cluster_wait();                                  // B: every coarse table complete; aT dead
         CL_MARK(pset, 22);
         {   // replicated couplings from the coarse table
             auto ct = [&](int l, int ci, int cj, int up) -> float {
@@ -504,6 +538,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         auto kbar = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
         if (tid < KGT) {
             const int tk = tid;
+            cluster_arrive();                            // C (this group zeroes nothing)
             for (int e = tk; e < NK; e += KGT) {
                 const int I = e % PK, J = e / PK;
                 const bool in = I >= 1 && I < mK && J >= 1 && J < mK;
@@ -573,34 +608,16 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             }
             kbar();
             CL_MARK(pset, 28);
-            auto kix = [](int col, int row) -> int { return row * L::KS + col; };     // K[row][col]
-            for (int e = tk; e < UK * UK; e += KGT) {    // B^T C
-                const int i = e % UK, k = e / UK;
-                float v = 0.0f;
-#pragma unroll
-                for (int r = 0; r < UE; ++r) v = fmaf(Bm[r * UK + i], Cm[r * UK + k], v);
-                Kt[kix(k, i)] = v;
-            }
-            kbar();
-            for (int e = tk; e < 5 * UK; e += KGT) {     // + 2 Dw - Dw AK Dw (5-point), row i
-                const int i = e % UK, d = e / UK;
-                const int Ii = i % (mK - 1) + 1, Ji = i / (mK - 1) + 1, ei = Ji * PK + Ii;
-                const float dwi = DIK[ei];
-                if (d == 0) Kt[kix(i, i)] += fmaf(-dwi * DK[ei], dwi, 2.0f * dwi);
-                else if (d == 1 && Ii < mK - 1) Kt[kix(i + 1, i)] += dwi * WHK[ei] * DIK[ei + 1];
-                else if (d == 2 && Ii > 1) Kt[kix(i - 1, i)] += dwi * WHK[ei - 1] * DIK[ei - 1];
-                else if (d == 3 && Ji < mK - 1) Kt[kix(i + (mK - 1), i)] += dwi * WVK[ei] * DIK[ei + PK];
-                else if (d == 4 && Ji > 1) Kt[kix(i - (mK - 1), i)] += dwi * WVK[ei - PK] * DIK[ei - PK];
-            }
-            CL_MARK(pset, 25);
         } else {
             const int tz = tid - KGT;
             constexpr int NZ = NT - KGT;
+            if (tz < Q.d && bl + cluster_count_x() < nb) theta_amp(bl + cluster_count_x(), tz, th_next);
             {   // every runtime grid (16-byte stores; oU is 16-byte aligned)
                 float4 *z4 = reinterpret_cast<float4 *>(sf + L::oU);
                 for (int e = tz; e < L::URUN / 4; e += NZ) z4[e] = make_float4(0.0f, 0.0f, 0.0f, 0.0f);
                 for (int e = 4 * (L::URUN / 4) + tz; e < L::URUN; e += NZ) sf[L::oU + e] = 0.0f;
             }
+            cluster_arrive();                            // C: own share of the grids zeroed
             for (int e = tz; e < L::F1; e += NZ) {       // level-1 omega D^-1 (rows 0 .. HR1+1)
                 const int lrw = e / P1, s = e % P1, I = s < H1E ? 2 * s : s >= H1 ? 2 * (s - H1) + 1 : -1;
                 const int jl = lrw - 1, J = J0 + jl;
@@ -620,7 +637,29 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 }
             }
         }
-        cluster_barrier();   // C: every CTA's grids are zeroed before any neighbour sends into them
+        __syncthreads();                                 // the two groups join: B, C complete, grids zeroed
+        CL_MARK(pset, 25);
+        {   // K = B^T C + (2 Dw - Dw AK Dw), all warps
+            auto kix = [](int col, int row) -> int { return row * L::KS + col; };     // K[row][col]
+            for (int e = tid; e < UK * UK; e += NT) {    // B^T C + the 5-point part of row i
+                const int i = e % UK, k = e / UK;
+                float v = 0.0f;
+#pragma unroll
+                for (int r = 0; r < UE; ++r) v = fmaf(Bm[r * UK + i], Cm[r * UK + k], v);
+                const int Ii = i % (mK - 1) + 1, Ji = i / (mK - 1) + 1, ei = Ji * PK + Ii;
+                const float dwi = DIK[ei];
+                const int dk = k - i;
+                float add = 0.0f;
+                if (dk == 0) add = fmaf(-dwi * DK[ei], dwi, 2.0f * dwi);
+                else if (dk == 1 && Ii < mK - 1) add = dwi * WHK[ei] * DIK[ei + 1];
+                else if (dk == -1 && Ii > 1) add = dwi * WHK[ei - 1] * DIK[ei - 1];
+                else if (dk == mK - 1 && Ji < mK - 1) add = dwi * WVK[ei] * DIK[ei + PK];
+                else if (dk == -(mK - 1) && Ji > 1) add = dwi * WVK[ei - PK] * DIK[ei - PK];
+                Kt[kix(k, i)] = v + add;
+            }
+        }
+        CL_MARK(pset, 31);
+        cluster_wait();      // C: every CTA's grids are zeroed before any neighbour sends into them
         CL_MARK(pset, 23);
 
         // ---- helpers of the iteration -----------------------------------------------------------
