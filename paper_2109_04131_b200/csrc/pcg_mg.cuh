@@ -101,7 +101,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr bool XP_SMEM = MINB * NWARP >= 12;       // >= 12 resident warps per SM: x, p in smem
     extern __shared__ double sm[];
     __shared__ double red[4][NWARP];
-    __shared__ double th_amp[kMaxD];
+    __shared__ double th_amp2[2][kMaxD];                 // amp_j theta_j(y_j): the current / the next sample
     double *DI0 = sm + L::oDI0, *G0 = sm + L::oG0, *G1 = sm + L::oG1, *aT = G0;
     double *WH1 = sm + L::oL1, *WV1 = WH1 + N1, *DI1 = WH1 + 2 * N1, *R1 = WH1 + 3 * N1;
     double *Z1 = WH1 + 4 * N1, *T1 = WH1 + 5 * N1, *S1 = WH1 + 6 * N1;
@@ -141,13 +141,22 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     const double *Stab = s_staged ? Ssm : S;
     const double *StabY = Stab + (Q.psi ? Q.d * W : 0);
 
-    for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
-        const int64_t b = b0 + bl;
-        // ---- K3: coefficients ----------------------------------------------------------------
-        for (int j = tid; j < Q.d; j += blockDim.x) {      // d may exceed the CTA (n = 16: 32 threads)
-            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b, j);
-            th_amp[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
+    // amp_j theta_j(y_j) of sample bl of this launch: the first sample's here, every later one during
+    // the previous sample's setup (by the warps that wait for the A3 inverse), off the critical path
+    auto theta_amp = [&](int64_t bl, int first, int stride, double *dst) {
+        for (int j = first; j < Q.d; j += stride) {      // d may exceed the CTA (n = 16: 32 threads)
+            const double y = nodes ? nodes[(int64_t)j * nb + bl] : lattice_node(P, b0 + bl, j);
+            dst[j] = Q.amp[j] * theta_of(Q.theta, y, Q.delta);
         }
+    };
+    if ((int64_t)blockIdx.x < nb) theta_amp(blockIdx.x, tid, NT, th_amp2[0]);
+    int tbuf = 0;
+
+    for (int64_t bl = blockIdx.x; bl < nb; bl += gridDim.x) {
+        // ---- K3: coefficients ----------------------------------------------------------------
+        const double *th_amp = th_amp2[tbuf];
+        double *th_next = th_amp2[tbuf ^ 1];
+        tbuf ^= 1;
         __syncthreads();
         {   // per-triangle a = 1 + sum_j amp_j theta_j S_j(ma) S_j(mb) (or exp) of the fine mesh,
             // a rank-d product: thread (ci0, cj0) owns a KI x KJ tile of cells (ci0 + CIS a,
@@ -247,6 +256,7 @@ k_pcg_mg(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         constexpr int HB = NWARP > 1 ? 32 : 0, HS = NT - HB;
         if (tid >= HB) {
             const int ht = tid - HB;
+            if (bl + gridDim.x < nb) theta_amp(bl + gridDim.x, ht, HS, th_next);
             for (int e = ht; e < 4 * n; e += HS) {       // zero rings of G0, G1 (aT aliased them)
                 const int side = e / n, o = e % n;       // ring walk: bottom, right, top, left
                 const int i = side == 0 ? o : side == 1 ? n : side == 2 ? n - o : 0;
