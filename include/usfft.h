@@ -311,7 +311,10 @@ usfft_status usfft_detect_carry(usfft_ctx *ctx, int64_t G_loc, int32_t s_tilde, 
  * of every rank (Step 2e P:318: union over g).  flags |= (votes > 0)
  * (running union over the rounds i of one t).  Outputs, identical on every rank:
  * det_idx  dev int32 [nJ]: this round's detected j ascending; n_det host int64 (syncs)
- * union_idx dev int32 [nJ] (may be NULL): all j with flags set, ascending; n_union host int64 */
+ * union_idx dev int32 [nJ] (may be NULL): all j with flags set, ascending; n_union host int64
+ * n_det == NULL (then n_union must be NULL too): the call does not synchronise; the rounds
+ * i < r of one dimension t only feed the running flags, so a driver enqueues them back to back
+ * and reads the counts of the last round alone. */
 usfft_status usfft_detect_union(usfft_ctx *ctx, int64_t nJ, int32_t *votes,
                                 uint8_t *flags, int32_t *det_idx, int64_t *n_det,
                                 int32_t *union_idx, int64_t *n_union);

@@ -281,8 +281,13 @@ def usfft_moments(ctx: Context, I, C, theta: str, delta: float, E, var, gsi=None
     _check(ctx, st, "usfft_moments")
 
 
-def usfft_detect_union(ctx: Context, nJ: int, votes, flags, det_idx, union_idx=None):
-    """a11; returns (n_det, n_union) (syncs)."""
+def usfft_detect_union(ctx: Context, nJ: int, votes, flags, det_idx, union_idx=None, counts: bool = True):
+    """a11; returns (n_det, n_union) (syncs), or (None, None) without synchronising (counts=False)."""
+    if not counts:
+        st = ctx.lib.usfft_detect_union(ctx.h, nJ, _p(votes, torch.int32), _p(flags, torch.uint8),
+                                        _p(det_idx, torch.int32), None, _p(union_idx, torch.int32), None)
+        _check(ctx, st, "usfft_detect_union")
+        return None, None
     nd, nu = C.c_int64(0), C.c_int64(0)
     st = ctx.lib.usfft_detect_union(ctx.h, nJ, _p(votes, torch.int32), _p(flags, torch.uint8),
                                     _p(det_idx, torch.int32), C.byref(nd),

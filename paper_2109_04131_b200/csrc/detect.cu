@@ -508,18 +508,19 @@ extern "C" usfft_status usfft_detect_union(usfft_ctx *c, int64_t nJ, int32_t *vo
     USFFT_ENTER(c);
     USFFT_REQUIRE(c, nJ >= 0 && nJ <= 0x7fffffff, "bad |J|");
     USFFT_REQUIRE(c, nJ == 0 || (votes && flags && det_idx), "NULL pointer");
-    USFFT_REQUIRE(c, n_det != nullptr, "n_det NULL");
+    USFFT_REQUIRE(c, n_det != nullptr || n_union == nullptr, "n_union without n_det");
     long long *counts = reinterpret_cast<long long *>(static_cast<char *>(c->dscal) + 64);
     // C3: union over the nodes of every rank (Step 2e P:318): all-reduce SUM of the votes
     if (comm_size(c) > 1 && nJ > 0)
         if (usfft_status s = comm_sum_i32(c, votes, nJ)) return s;
     if (nJ == 0) {
-        *n_det = 0;
+        if (n_det) *n_det = 0;
         if (n_union) *n_union = 0;
         return USFFT_OK;
     }
     k_union<<<1, 1024, 0, c->stream>>>(votes, nJ, flags, det_idx, union_idx, counts);
     USFFT_CHECK_LAUNCH(c);
+    if (!n_det) return USFFT_OK;                          // asynchronous: the running flags are the output
     long long h[2];
     USFFT_CUDA(c, cudaMemcpyAsync(h, counts, sizeof h, cudaMemcpyDeviceToHost, c->stream));
     USFFT_CUDA(c, cudaStreamSynchronize(c->stream));

@@ -104,7 +104,9 @@ class Detector:
     # ------------------------------------------------------------------------------------------
     def round(self, step: int, t: int, i: int, I_prev: torch.Tensor, n_prev: int,
               kt: torch.Tensor, s_tilde: int, flags: torch.Tensor, want_coef: bool = False,
-              keep_iters: bool = False) -> RoundResult:
+              keep_iters: bool = False, counts: bool = True) -> RoundResult:
+        """One detection round.  counts=False: the round only feeds the running union `flags` and
+        returns without synchronising (n_det, n_union = None): the rounds i < r of a dimension."""
         cfg, ctx, dev = self.cfg, self.ctx, self.dev
         n1 = int(kt.numel())
         nJ = n_prev * n1
@@ -168,11 +170,13 @@ class Detector:
         self._sum(votes)
         det_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
         union_idx = torch.empty(nJ, dtype=torch.int32, device=dev)
-        n_det, n_union = B.usfft_detect_union(ctx, nJ, votes, flags, det_idx, union_idx)
+        n_det, n_union = B.usfft_detect_union(ctx, nJ, votes, flags, det_idx, union_idx,
+                                              counts=counts or want_coef)
         mark("detect")
-        res = RoundResult(plan, nJ, n_det, n_union, det_idx[:n_det], union_idx[:n_union])
+        res = RoundResult(plan, nJ, n_det, n_union, det_idx[:n_det] if n_det is not None else None,
+                          union_idx[:n_union] if n_union is not None else None)
         res.iters = iters
-        if want_coef and n_det > 0:
+        if want_coef and n_det:
             coef = torch.empty((self.G_loc, n_det, 2), dtype=torch.float64, device=dev)
             lstar = torch.empty((self.G_loc, n_det), dtype=torch.int32, device=dev)
             B.usfft_resolve(ctx, plan, self.G_loc, spectra, bins, nJ, det_g, n_det_g, s_tilde,
@@ -308,7 +312,10 @@ class Detector:
             res = None
             for i in range(1, r_t + 1):
                 res = self.last_round = None                   # free the previous round first
-                res = self.round(2, t, i, I_prev, n_prev, kt, s_t, flags, want_coef=(t == d))
+                # only the last round of a dimension needs the counts on the host; the others are
+                # enqueued without a synchronisation (the log wants n_det of every round)
+                res = self.round(2, t, i, I_prev, n_prev, kt, s_t, flags, want_coef=(t == d),
+                                 counts=(i == r_t or log is not None))
                 if log is not None:
                     log.append(dict(step=2, t=t, i=i, M=res.plan.M, L=res.plan.L,
                                     B=res.plan.M * res.plan.L, nJ=nJ, n_det=res.n_det))

@@ -37,3 +37,17 @@ def test_checkpoint_of_another_config_is_refused(tmp_path):
     other = dict(cfg, seed=cfg["seed"] + 1)
     with pytest.raises(ValueError):
         Detector(other).load_checkpoint(path)
+
+
+def test_unsynchronised_rounds_match_synchronised_rounds():
+    """The rounds i < r of a Step-2 dimension are enqueued without a host synchronisation
+    (usfft_detect_union with n_det == NULL); a run that synchronises after every round (log
+    requested) must give the same frequency set and coefficients bit for bit."""
+    from paper_2109_04131_b200.driver import Detector
+    cfg = config(1, mode="A")
+    log = []
+    I_sync, C_sync = Detector(cfg).run(log=log)
+    I_async, C_async = Detector(cfg).run()
+    assert any(e["step"] == 2 and e["i"] > 1 for e in log)          # the workload has r > 1 rounds
+    assert torch.equal(I_sync, I_async)
+    assert np.array_equal(C_sync.cpu().numpy(), C_async.cpu().numpy())
