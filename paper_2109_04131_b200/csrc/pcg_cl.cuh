@@ -200,6 +200,42 @@ __device__ long long g_cl_probe[16][32];
 #define CL_MARK(on, id) ((void)0)
 #endif
 
+// K = B^T C + (2 Dw - Dw AK Dw) of the 8-/4-cell levels from B, C and the 8-cell operator in
+// shared memory, all warps of the CTA; the 5-point part is its own short pass (folded into the
+// product loop its five branches diverge in every warp: ~1000 instead of ~230 cycles per loop
+// iteration).  Not inlined: its registers are allocated apart from the solver's (inlined, its
+// pressure moved spills into the CG loop: config 3 37.2 -> 38.5 ms for the same code; as a
+// function 36.1 ms).  Measured and rejected: the whole K build (inverse, B, C, diagonals) in this
+// function as CTA-wide passes (config 5 496.4 -> 502.1 ms).
+template <int NN, int CS>
+__device__ __noinline__ void cl_build_k(float *sf) {
+    using L = ClC<NN, CS>;
+    constexpr int NT = L::NT, mK = L::mK, PK = L::PK, NK = L::NK, UK = L::UK, UE = L::UE;
+    const float *WHK = sf + L::oKs, *WVK = WHK + NK, *DK = WHK + 2 * NK, *DIK = WHK + 3 * NK;
+    const float *Bm = sf + L::oB, *Cm = sf + L::oC;
+    float *Kt = sf + L::oKt;
+    const int tid = threadIdx.x;
+    auto kix = [](int col, int row) -> int { return row * L::KS + col; };     // K[row][col]
+    for (int e = tid; e < UK * UK; e += NT) {
+        const int i = e % UK, k = e / UK;
+        float v = 0.0f;
+#pragma unroll
+        for (int r = 0; r < UE; ++r) v = fmaf(Bm[r * UK + i], Cm[r * UK + k], v);
+        Kt[kix(k, i)] = v;
+    }
+    __syncthreads();
+    for (int e = tid; e < 5 * UK; e += NT) {             // row i
+        const int i = e % UK, d = e / UK;
+        const int Ii = i % (mK - 1) + 1, Ji = i / (mK - 1) + 1, ei = Ji * PK + Ii;
+        const float dwi = DIK[ei];
+        if (d == 0) Kt[kix(i, i)] += fmaf(-dwi * DK[ei], dwi, 2.0f * dwi);
+        else if (d == 1 && Ii < mK - 1) Kt[kix(i + 1, i)] += dwi * WHK[ei] * DIK[ei + 1];
+        else if (d == 2 && Ii > 1) Kt[kix(i - 1, i)] += dwi * WHK[ei - 1] * DIK[ei - 1];
+        else if (d == 3 && Ji < mK - 1) Kt[kix(i + (mK - 1), i)] += dwi * WVK[ei] * DIK[ei + PK];
+        else if (d == 4 && Ji > 1) Kt[kix(i - (mK - 1), i)] += dwi * WVK[ei - PK] * DIK[ei - PK];
+    }
+}
+
 template <int NN, int CS, int MINB>
 __global__ void __launch_bounds__(ClC<NN, CS>::NT, MINB)
 k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes, int64_t b0,
@@ -639,25 +675,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         __syncthreads();                                 // the two groups join: B, C complete, grids zeroed
         CL_MARK(pset, 25);
-        {   // K = B^T C + (2 Dw - Dw AK Dw), all warps
-            auto kix = [](int col, int row) -> int { return row * L::KS + col; };     // K[row][col]
-            for (int e = tid; e < UK * UK; e += NT) {    // B^T C + the 5-point part of row i
-                const int i = e % UK, k = e / UK;
-                float v = 0.0f;
-#pragma unroll
-                for (int r = 0; r < UE; ++r) v = fmaf(Bm[r * UK + i], Cm[r * UK + k], v);
-                const int Ii = i % (mK - 1) + 1, Ji = i / (mK - 1) + 1, ei = Ji * PK + Ii;
-                const float dwi = DIK[ei];
-                const int dk = k - i;
-                float add = 0.0f;
-                if (dk == 0) add = fmaf(-dwi * DK[ei], dwi, 2.0f * dwi);
-                else if (dk == 1 && Ii < mK - 1) add = dwi * WHK[ei] * DIK[ei + 1];
-                else if (dk == -1 && Ii > 1) add = dwi * WHK[ei - 1] * DIK[ei - 1];
-                else if (dk == mK - 1 && Ji < mK - 1) add = dwi * WVK[ei] * DIK[ei + PK];
-                else if (dk == -(mK - 1) && Ji > 1) add = dwi * WVK[ei - PK] * DIK[ei - PK];
-                Kt[kix(k, i)] = v + add;
-            }
-        }
+        cl_build_k<NN, CS>(sf);                          // K = B^T C + (2 Dw - Dw AK Dw), all warps
         CL_MARK(pset, 31);
         cluster_wait();      // C: every CTA's grids are zeroed before any neighbour sends into them
         CL_MARK(pset, 23);
