@@ -72,7 +72,7 @@ def oracle_solves(pool, cfg, Y):
 def test_sample_pde_whole_round(B, ctx, pool, cfgid):
     """All L*M samples of a bench-sized round in one call (>= 20 samples per CTA / cluster on
     the persistent loop); 64 random samples against the oracle's banded Cholesky (<= 1e-10
-    max-norm relative), every sample at relres <= 1e-12, and a ragged re-solve of a sub-range
+    max-norm relative), every sample at relres <= 1e-12 within 14 CG iterations, and a ragged re-solve of a sub-range
     bit-identical (a sample's result does not depend on its CTA, cluster or launch)."""
     cfg = config(cfgid)
     t, nJ = ROUND[cfgid]
@@ -83,7 +83,9 @@ def test_sample_pde_whole_round(B, ctx, pool, cfgid):
     rel = torch.empty(nb, dtype=torch.float64, device="cuda")
     assert B.usfft_sample_pde(ctx, B.pde_desc(cfg), p, 0, nb, u, nb, None, it, rel, check_conv=True) == 0
     assert rel.max().item() <= 1e-12 and torch.isfinite(u).all()
-    assert it.max().item() <= 40
+    # multigrid-preconditioned CG with the per-level smoother weights: 13 iterations
+    # on configs 2, 3, 5 and 13-14 on config 4; a regression of the cycle shows up here first
+    assert it.max().item() <= 14 and it.float().mean().item() <= 13.2
     rng = np.random.default_rng(100 + cfgid)
     pick = np.sort(rng.choice(nb, size=64, replace=False))
     Y = olat.nodes(p.M, p.z, p.shift, t)[:, pick]
