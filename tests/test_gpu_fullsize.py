@@ -186,7 +186,8 @@ def test_full_run_pde_config2_lockstep(B, pool):
     stats = dict(rounds=0, strict=0, fragile=0)
 
     class Lockstep(Detector):
-        def round(self, step, t, i, I_prev, n_prev, kt, s_tilde, flags, want_coef=False, keep_iters=False):
+        def round(self, step, t, i, I_prev, n_prev, kt, s_tilde, flags, want_coef=False, keep_iters=False,
+                  counts=True):
             res = super().round(step, t, i, I_prev, n_prev, kt, s_tilde, flags, want_coef, keep_iters)
             p = res.plan
             shift = oplan.shift(cfg["seed"], step, t, i, cfg["d"])

@@ -29,7 +29,8 @@ def main():
     done = [False]
 
     class D(Detector):
-        def round(self, step, t, i, I_prev, n_prev, kt, s_tilde, flags, want_coef=False, keep_iters=False):
+        def round(self, step, t, i, I_prev, n_prev, kt, s_tilde, flags, want_coef=False, keep_iters=False,
+                  counts=True):
             res = super().round(step, t, i, I_prev, n_prev, kt, s_tilde, flags, want_coef, keep_iters)
             if done[0] or step == 1:
                 return res
