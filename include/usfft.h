@@ -280,8 +280,8 @@ usfft_status usfft_lattice_keys(usfft_ctx *ctx, const usfft_lattice_desc *lat, i
  *   J = I_prev x kt with j = a n1 + c (Z10; n1 = |kt|, ldb = |J| = n_prev n1, < 2^31), whose bin
  *   map bins[l * ldb + j] is given whole (the candidate offset is j0, not folded into bins).
  *   kappa_min[g * ldk + (j - j0)]; kappa_max and tau as above.  The product structure gives
- *   bins[l][a n1 + c] = (bins[l][a n1] + bins[l][c] - bins[l][0]) mod M, so for |J| >= 4 (M/2+1)
- *   the library stages each (node, lattice) spectrum once per tile of candidates in shared memory
+ *   bins[l][a n1 + c] = (bins[l][a n1] + bins[l][c] - bins[l][0]) mod M, so when the spectra
+ *   of the call exceed the L2 cache and |J| >= 4 (M/2+1) the library stages each (node, lattice) spectrum once per tile of candidates in shared memory
  *   instead of gathering one sector per (node, candidate, lattice) (Alg. 1 Step 2c P:313-315; the
  *   keys are bit-identical to usfft_lattice_keys).  Errors: EINVAL on sizes (ldb % n1 != 0). */
 usfft_status usfft_lattice_keys_product(usfft_ctx *ctx, const usfft_lattice_desc *lat, int64_t G_loc,

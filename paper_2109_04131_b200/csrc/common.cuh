@@ -48,6 +48,7 @@ struct usfft_ctx {
     cudaStream_t stream = nullptr;
     int sm_count = 148;
     size_t smem_optin = 0;
+    size_t l2_bytes = 0;                                     // L2 cache size of the device
     bool sticky = false;
     std::string err;
     int64_t launches = 0;

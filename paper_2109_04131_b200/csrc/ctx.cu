@@ -25,6 +25,8 @@ extern "C" usfft_status usfft_init(usfft_ctx **out, int device, void *stream, in
     c->sm_count = v > 0 ? v : 148;
     cudaDeviceGetAttribute(&v, cudaDevAttrMaxSharedMemoryPerBlockOptin, device);
     c->smem_optin = v > 0 ? (size_t)v : 48 * 1024;
+    cudaDeviceGetAttribute(&v, cudaDevAttrL2CacheSize, device);
+    c->l2_bytes = v > 0 ? (size_t)v : (size_t)64 << 20;
     if (cudaMalloc(&c->dscal, 4096) != cudaSuccess) {
         cudaGetLastError();
         delete c;

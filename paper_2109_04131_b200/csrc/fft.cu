@@ -14,6 +14,10 @@
 
 #include "common.cuh"
 
+#ifndef USFFT_KEYS_TILED_ALWAYS
+#define USFFT_KEYS_TILED_ALWAYS 0                           // tools/keys_crossover.py builds with 1
+#endif
+
 namespace usfft {
 
 struct SlabParams {
@@ -584,7 +588,7 @@ extern "C" usfft_status usfft_lattice_keys(usfft_ctx *c, const usfft_lattice_des
 }
 
 // a8 for the candidates j0 .. j0+nJ-1 of the product set J = I_prev x kt (j = a n1 + c, Z10):
-// bins is the whole [L][ldb] map; keys into kappa_min[g * ldk + (j - j0)].  |J| >= 4 (M/2+1):
+// bins is the whole [L][ldb] map; keys into kappa_min[g * ldk + (j - j0)].  spectra larger than L2 and |J| >= 4 (M/2+1):
 // k_kappa_tiled; otherwise the gather kernel on bins + j0 (both bit-identical).
 extern "C" usfft_status usfft_lattice_keys_product(usfft_ctx *c, const usfft_lattice_desc *lat, int64_t G_loc,
                                                    const double *spectra, const int32_t *bins, int64_t ldb,
@@ -601,7 +605,16 @@ extern "C" usfft_status usfft_lattice_keys_product(usfft_ctx *c, const usfft_lat
     const int64_t M = lat->M, Mh = M / 2 + 1;
     constexpr int NT = 512, KPT = 24, MINB = 1, KT = NT * KPT;
     const size_t smem = sizeof(double) * 4 * (size_t)M + sizeof(int32_t) * 2 * (size_t)(KT / n1 + 2 + n1);
-    if (nJ < 4 * Mh || smem > c->smem_optin || G_loc > 65535)
+    // The gathers of k_kappa_grouped hit L2 while the spectra fit there (config 2: 52 MB): it is
+    // then 1.1-3.6x faster than the tiled kernel for every |J|.  With spectra beyond L2 every
+    // gather is a DRAM access and the tiled kernel, which streams each spectrum once per tile but
+    // builds 2M keys per (node, lattice), wins from |J| ~ 2-4 (M/2+1) on: 1.8 vs 4.1 ms at
+    // |J| = 4 (M/2+1) and 15.7 vs 50.1 ms at 64 (M/2+1) on config 4's shape, while at |J| <= 2
+    // (M/2+1) the gathers are faster (configs 3, 5: 0.52 vs 0.78 ms, 3.5 vs 5.1 ms)
+    // (tools/keys_crossover.py and bench.py, measured on the B200).
+    const size_t spectra_bytes = sizeof(double2) * (size_t)G_loc * lat->L * Mh;
+    const bool tiled = USFFT_KEYS_TILED_ALWAYS || (4 * spectra_bytes > 3 * c->l2_bytes && nJ >= 4 * Mh);
+    if (!tiled || smem > c->smem_optin || G_loc > 65535)
         return launch_keys(c, M, lat->L, G_loc, spectra, bins + j0, ldb, nJ, kappa_min, ldk, kappa_max, tau);
     auto kern = k_kappa_tiled<NT, KPT, MINB>;
     if (usfft_status s = kernel_fit(c, kern, NT, smem, nullptr)) return s;
