@@ -142,6 +142,11 @@ __device__ __forceinline__ void cluster_barrier() {
 __device__ __forceinline__ void cluster_arrive() {
     asm volatile("barrier.cluster.arrive.release.aligned;" ::: "memory");
 }
+// arrive without release semantics: for threads that have no writes to publish to the cluster
+// (a release arrive first waits until the thread's earlier global stores are performed)
+__device__ __forceinline__ void cluster_arrive_relaxed() {
+    asm volatile("barrier.cluster.arrive.relaxed.aligned;" ::: "memory");
+}
 __device__ __forceinline__ void cluster_wait() {
     asm volatile("barrier.cluster.wait.acquire.aligned;" ::: "memory");
 }
@@ -357,7 +362,9 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         const double *th_amp = th_amp2[tbuf];
         double *th_next = th_amp2[tbuf ^ 1];
         tbuf ^= 1;
-        cluster_arrive();                                // A: this CTA is done with the previous sample
+        // A: this CTA is done with the previous sample (its reads of K; nothing to publish: relaxed, so
+        // the arrive does not wait for the sample's output stores)
+        cluster_arrive_relaxed();
         __syncthreads();
         CL_MARK(pset, 29);
         if (pd) {   // aT[plane] = Y_plane^T . (amp theta X_plane) from the resident slice: two [YP x d] . [d x n]
@@ -574,7 +581,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         auto kbar = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
         if (tid < KGT) {
             const int tk = tid;
-            cluster_arrive();                            // C (this group zeroes nothing)
+            cluster_arrive_relaxed();                    // C (this group zeroes nothing)
             for (int e = tk; e < NK; e += KGT) {
                 const int I = e % PK, J = e / PK;
                 const bool in = I >= 1 && I < mK && J >= 1 && J < mK;
