@@ -41,8 +41,9 @@
 // A transfer of exchange k for CG iteration i+1 cannot start before every CTA has sent its X5
 // partials of iteration i, which every CTA does only after its last read of iteration i's data:
 // the X5 all-to-all orders all buffer reuse (its own slots are double-buffered).  The per-sample
-// setup (coefficient tables, coarse operators, K) uses three cluster barriers, each split into an
-// early arrive and a late wait.  Reductions and
+// setup (coefficient tables, coarse operators, K) uses two cluster barriers (A: the previous sample
+// is done everywhere, C: every CTA's grids are zeroed), each split into an early arrive and a late
+// wait, and one more counted exchange (XB: the coarse coefficients).  Reductions and
 // the order of every sum are fixed, so a sample's result does not depend on the cluster that
 // solved it or on the launch split.
 //
@@ -248,7 +249,6 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
          double *__restrict__ relres, int32_t *__restrict__ noconv, const double *__restrict__ S,
          const double *__restrict__ Bt, int pd) {
     using L = ClC<NN, CS>;
-    namespace cg = cooperative_groups;
     constexpr int n = NN, nx = L::nx, np = L::np, HE = L::HE, HR = L::HR, BC = L::BC, BR = L::BR;
     constexpr int LX = L::LX, NRG = L::NRG, NT = L::NT, NWARP = L::NWARP, W = 3 * n + 1;
     constexpr int m1 = L::m1, P1 = L::P1, H1 = L::H1, HR1 = L::HR1, HR2 = L::HR2, LK = L::LK;
@@ -259,8 +259,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
     constexpr float om = (float)kMgOmegaCoarse;          // coarse-level Jacobi weight (the fine level: kMgOmega)
     extern __shared__ __align__(16) float sf[];
     __shared__ double th_amp2[2][kMaxD];                 // amp_j theta_j(y_j) of the current / the next sample
-    __shared__ alignas(8) unsigned long long mbar[6];
-    cg::cluster_group cluster = cg::this_cluster();
+    __shared__ alignas(8) unsigned long long mbar[7];
     const int rank = (int)cluster_rank();
     const bool has_lo = rank > 0, has_hi = rank < CS - 1;
     const int j0 = rank * HR, J0 = j0 / 2, J20 = j0 / 4;
@@ -287,15 +286,16 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
 
     // ---- exchanges: mbarriers, expected bytes, peer addresses -----------------------------------
     const uint32_t mb0 = smem_addr(&mbar[0]);
-    const uint32_t xb[6] = {(uint32_t)(4 * nx * ((has_hi ? 3 : 0) + (has_lo ? 1 : 0))),
+    const uint32_t xb[7] = {(uint32_t)(4 * nx * ((has_hi ? 3 : 0) + (has_lo ? 1 : 0))),
                             (uint32_t)(4 * (m1 - 1) * ((has_hi ? 3 : 0) + (has_lo ? 3 : 0))),
                             (uint32_t)(4 * (m2 - 1) * (m2 - 1)),
                             (uint32_t)(4 * nx * ((has_hi ? 1 : 0) + (has_lo ? 1 : 0))),
-                            (uint32_t)(8 * 3 * CS), (uint32_t)(8 * CS)};
+                            (uint32_t)(8 * 3 * CS), (uint32_t)(8 * CS),
+                            (uint32_t)(4 * L::ctoff(LK + 2))};   // XB: the whole coarse coefficient table
     if (tid == 0) {
-        for (int k = 0; k < 6; ++k) mbar_init(mb0 + 8 * k);
+        for (int k = 0; k < 7; ++k) mbar_init(mb0 + 8 * k);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
-        for (int k = 0; k < 6; ++k) mbar_expect(mb0 + 8 * k, xb[k]);
+        for (int k = 0; k < 7; ++k) mbar_expect(mb0 + 8 * k, xb[k]);
     }
     uint32_t ph = 0;                                     // bit k: parity of exchange k's next phase
     auto xwait = [&](int k) {
@@ -473,8 +473,10 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             return aT[(pl * ATR + fj - (j0 - 2)) * n + fi];
         };
         {   // coarse triangle coefficients (levels 2 .. LK+1) whose fine triangle is in the own rows,
-            // sent to every CTA's coarse table
+            // sent to every CTA's coarse table (XB: st.async with byte counts on the receivers' mbarrier;
+            // every CTA receives the whole table once per sample, its own share included)
             constexpr int NC = L::ctoff(LK + 2) / 2;       // coarse cells of all levels
+            const uint32_t ctab_a = smem_addr(ctab);
             for (int e = tid; e < 2 * NC; e += NT) {
                 const int up = e >= NC, q = up ? e - NC : e;
                 int l = 2, base = 0;
@@ -489,10 +491,9 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 const int dst = L::ctoff(l) + (up ? m * m : 0) + cell;
                 UB_CHECK(dst >= 0 && dst < L::ctoff(LK + 2));
 #pragma unroll
-                for (int k = 0; k < CS; ++k) cluster.map_shared_rank(ctab, k)[dst] = v;
+                for (int k = 0; k < CS; ++k) st_async(mapa(ctab_a + 4 * dst, k), v, mapa(mb0 + 48, k));
             }
         }
-        cluster_arrive();                                // B: own coarse coefficients pushed
         // fine couplings of the own block (ring edges included), fp64 and their fp32 copies
         double cE[BR][BC + 1], cN[BR + 1][BC];
         float ce[BR][BC + 1], cn[BR + 1][BC];
@@ -535,7 +536,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
             WV1[e] = (jl <= HR1 + 1 && J >= 0 && J < m1 && I >= 1 && I < m1)
                          ? (float)(0.5 * (fcl(I, J, 1, 1) + fcl(I - 1, J, 0, 1))) : 0.0f;
         }
-        cluster_wait();                                  // B: every coarse table complete; aT dead
+        xwait(6);                                        // XB: the coarse table complete (every CTA's share)
         CL_MARK(pset, 22);
         {   // replicated couplings from the coarse table
             auto ct = [&](int l, int ci, int cj, int up) -> float {
