@@ -132,7 +132,7 @@ struct ClC {
         for (int q = 2; q < l; ++q) o += 2 * ml(q) * ml(q);
         return o;
     }
-    static_assert(ctoff(LK + 2) <= oU - oKt, "coarse coefficient table must fit in the K region");
+    static_assert(ctoff(LK + 2) <= UK * KS, "the coarse coefficient table overlays K only (AE^-1, B, C are built while it is read)");
     static_assert(2 * UK <= NT && 3 * CS <= 32, "thread mapping");
 };
 
@@ -538,51 +538,41 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         }
         xwait(6);                                        // XB: the coarse table complete (every CTA's share)
         CL_MARK(pset, 22);
-        {   // replicated couplings from the coarse table
-            auto ct = [&](int l, int ci, int cj, int up) -> float {
-                const int m = L::ml(l);
-                return ctab[L::ctoff(l) + (up ? m * m : 0) + cj * m + ci];
-            };
-            auto whc = [&](int l, int I, int J) -> float {
-                const int M = L::ml(l);
-                return (I < M && J >= 1 && J < M) ? 0.5f * (ct(l, I, J, 0) + ct(l, I, J - 1, 1)) : 0.0f;
-            };
-            auto wvc = [&](int l, int I, int J) -> float {
-                const int M = L::ml(l);
-                return (J < M && I >= 1 && I < M) ? 0.5f * (ct(l, I, J, 1) + ct(l, I - 1, J, 0)) : 0.0f;
-            };
-#pragma unroll
-            for (int l = 2; l < LK; ++l) {
-                const int Pq = L::Pl(l);
-                float *wh = lc(l, LWH), *wv = lc(l, LWV);
-                for (int e = tid; e < L::Nl(l); e += NT) {
-                    const int I = e % Pq, J = e / Pq;
-                    wh[e] = whc(l, I, J);
-                    wv[e] = wvc(l, I, J);
-                }
-            }
-            for (int e = tid; e < NK; e += NT) {
-                const int I = e % PK, J = e / PK;
-                WHK[e] = whc(LK, I, J);
-                WVK[e] = wvc(LK, I, J);
-            }
-            for (int e = tid; e < L::NE; e += NT) {
-                const int I = e % PE, J = e / PE;
-                WHE[e] = whc(LK + 1, I, J);
-                WVE[e] = wvc(LK + 1, I, J);
-            }
-        }
-        __syncthreads();                                 // the coarse table (K region) is dead
-        CL_MARK(pset, 24);
-        // ---- diagonals, zeroed grids, the dense maps -------------------------------------------
-        // Two warp groups run concurrently: warps 0-3 build the dense map K (named barrier 1, 128
-        // threads), the other warps zero the runtime grids and form the level-1/2/3 diagonals.
-        // The groups touch disjoint shared memory; cluster barrier C joins them.
+        __syncthreads();                                 // every thread is done with aT (zeroed below)
+        // ---- replicated couplings, diagonals, zeroed grids, the dense maps -----------------------
+        // Two warp groups run concurrently.  Warps 0-3 (named barrier 1) form the couplings of the 8-
+        // and 4-cell levels from the coarse table and build AE^-1, B and C of the dense map K (none
+        // of which overlays the table; K itself does and waits for the join).  The other warps
+        // (named barrier 2) form the couplings of the replicated smoothed levels from the table, zero
+        // the runtime grids, compute the next sample's amp theta and every diagonal.
+        auto ct = [&](int l, int ci, int cj, int up) -> float {
+            const int m = L::ml(l);
+            return ctab[L::ctoff(l) + (up ? m * m : 0) + cj * m + ci];
+        };
+        auto whc = [&](int l, int I, int J) -> float {
+            const int M = L::ml(l);
+            return (I < M && J >= 1 && J < M) ? 0.5f * (ct(l, I, J, 0) + ct(l, I, J - 1, 1)) : 0.0f;
+        };
+        auto wvc = [&](int l, int I, int J) -> float {
+            const int M = L::ml(l);
+            return (J < M && I >= 1 && I < M) ? 0.5f * (ct(l, I, J, 1) + ct(l, I - 1, J, 0)) : 0.0f;
+        };
         constexpr int KGT = 128;
         auto kbar = []() { asm volatile("bar.sync 1, 128;" ::: "memory"); };
         if (tid < KGT) {
             const int tk = tid;
             cluster_arrive_relaxed();                    // C (this group zeroes nothing)
+            for (int e = tk; e < NK; e += KGT) {
+                const int I = e % PK, J = e / PK;
+                WHK[e] = whc(LK, I, J);
+                WVK[e] = wvc(LK, I, J);
+            }
+            for (int e = tk; e < L::NE; e += KGT) {
+                const int I = e % PE, J = e / PE;
+                WHE[e] = whc(LK + 1, I, J);
+                WVE[e] = wvc(LK + 1, I, J);
+            }
+            kbar();
             for (int e = tk; e < NK; e += KGT) {
                 const int I = e % PK, J = e / PK;
                 const bool in = I >= 1 && I < mK && J >= 1 && J < mK;
@@ -655,6 +645,16 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
         } else {
             const int tz = tid - KGT;
             constexpr int NZ = NT - KGT;
+#pragma unroll
+            for (int l = 2; l < LK; ++l) {
+                const int Pq = L::Pl(l);
+                float *wh = lc(l, LWH), *wv = lc(l, LWV);
+                for (int e = tz; e < L::Nl(l); e += NZ) {
+                    const int I = e % Pq, J = e / Pq;
+                    wh[e] = whc(l, I, J);
+                    wv[e] = wvc(l, I, J);
+                }
+            }
             if (tz < Q.d && bl + cluster_count_x() < nb) theta_amp(bl + cluster_count_x(), tz, th_next);
             {   // every runtime grid (16-byte stores; oU is 16-byte aligned)
                 float4 *z4 = reinterpret_cast<float4 *>(sf + L::oU);
@@ -669,6 +669,7 @@ k_pcg_cl(const LatParams P, const PdeParams Q, const double *__restrict__ nodes,
                 const float dv = in ? WH1[e] + WH1[e1(I - 1, jl)] + WV1[e] + WV1[e - P1] : 1.0f;
                 DI1[e] = in ? om / dv : 0.0f;
             }
+            asm volatile("bar.sync 2, %0;" :: "n"(NZ) : "memory");   // the group's level-2.. couplings
 #pragma unroll
             for (int l = 2; l < LK; ++l) {
                 const int M = L::ml(l), Pq = L::Pl(l);

@@ -16,7 +16,7 @@ NAMES = {0: "iteration start", 1: "X1 wait", 2: "fine residual", 3: "R1, Z1 + X2
          5: "R2 + X3", 6: "replicated down", 7: "K map", 8: "replicated up", 9: "S1",
          10: "fine post-smooth", 11: "u + X4", 12: "A u, dots + X5", 13: "update + X1 send",
          20: "setup start", 29: "theta, amp", 30: "coef table", 21: "barrier A", 22: "couplings + coarse push", 24: "replicated couplings",
-         26: "DK, DIK", 27: "GJ + B", 28: "C", 25: "join", 31: "BtC + 5-point", 23: "barrier C"}
+         26: "K-level couplings, DK, DIK", 27: "GJ + B", 28: "C", 25: "join", 31: "BtC + 5-point", 23: "barrier C"}
 
 
 def main():
@@ -44,7 +44,7 @@ def main():
     ctx.lib.usfft_debug_cl_probe(buf)
     v = [[buf[r * 32 + k] for k in range(32)] for r in range(16)]
     CS = 8 if cfg["n"] == 128 else 4
-    for seq in ([20, 29, 30, 21, 22, 24, 26, 27, 28, 25, 31, 23], list(range(14))):
+    for seq in ([20, 29, 30, 21, 22, 26, 27, 28, 25, 31, 23], list(range(14))):
         print("phase".ljust(20) + "".join(f"  cta{r:<5d}" for r in range(CS)))
         for a, b in zip(seq[:-1], seq[1:]):
             print(NAMES[b].ljust(20) + "".join(f"{v[r][b] - v[r][a]:9d}" for r in range(CS)))
