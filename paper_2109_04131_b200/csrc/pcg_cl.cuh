@@ -188,9 +188,13 @@ __device__ __forceinline__ void mbar_init(uint32_t mb) {
 __device__ __forceinline__ void mbar_expect(uint32_t mb, uint32_t bytes) {
     asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" :: "r"(mb), "r"(bytes) : "memory");
 }
+// Default semantics (acquire at CTA scope), as in the usual transaction-barrier wait: the st.async
+// data lands in this CTA's own shared memory before its bytes complete on the mbarrier.  With
+// .acquire.cluster every successful wait was followed by CCTL.IVALL, an invalidation of the whole
+// L1 (six per CG iteration), after which the loop's spill reloads missed to L2.
 __device__ __forceinline__ void mbar_wait(uint32_t mb, uint32_t parity) {
     asm volatile("{\n\t.reg .pred p;\n\tWAIT_%=:\n\t"
-                 "mbarrier.try_wait.parity.acquire.cluster.shared::cta.b64 p, [%0], %1;\n\t"
+                 "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
                  "@!p bra WAIT_%=;\n\t}" :: "r"(mb), "r"(parity) : "memory");
 }
 
