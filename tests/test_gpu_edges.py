@@ -158,3 +158,35 @@ def test_maximum_parameter_dimension(B, ctx):
         assert B.usfft_sample_pde(ctx, B.pde_desc(cfg, precond=precond), p, 0, nb, u, nb, check_conv=True) == 0
         ref = ofe.sample_pde(cfg, olat.nodes(p.M, p.z, p.shift, 2)[:, :nb])
         assert np.abs(u.cpu().numpy() - ref).max() <= 1e-10 * np.abs(ref).max()
+
+
+def test_union_without_counts(B, ctx):
+    """usfft_detect_union with n_det == NULL: no host outputs, same device outputs as the
+    synchronising call; n_union without n_det is refused (include/usfft.h, a11)."""
+    import ctypes as C
+    rng = np.random.default_rng(5)
+    nJ = 5000
+    votes_h = (rng.random(nJ) < 0.1).astype(np.int32) * rng.integers(1, 9, nJ).astype(np.int32)
+    outs = []
+    for counts in (True, False):
+        votes = dev(votes_h, torch.int32)
+        flags = torch.zeros(nJ, dtype=torch.uint8, device="cuda")
+        flags[::7] = 1                                       # a running union from earlier rounds
+        det_idx = torch.full((nJ,), -1, dtype=torch.int32, device="cuda")
+        union_idx = torch.full((nJ,), -1, dtype=torch.int32, device="cuda")
+        nd, nu = B.usfft_detect_union(ctx, nJ, votes, flags, det_idx, union_idx, counts=counts)
+        torch.cuda.synchronize()
+        outs.append((nd, nu, flags.cpu().numpy(), det_idx.cpu().numpy(), union_idx.cpu().numpy()))
+    (nd, nu, f0, d0, u0), (nd1, nu1, f1, d1, u1) = outs
+    assert (nd1, nu1) == (None, None)
+    expect = (votes_h > 0) | (np.arange(nJ) % 7 == 0)
+    assert nd == int((votes_h > 0).sum()) and nu == int(expect.sum())
+    assert np.array_equal(f0, expect.astype(np.uint8)) and np.array_equal(f1, f0)
+    assert np.array_equal(d1[:nd], d0[:nd]) and np.array_equal(u1[:nu], u0[:nu])
+    assert np.array_equal(d0[:nd], np.flatnonzero(votes_h > 0)) and np.array_equal(u0[:nu], np.flatnonzero(expect))
+    votes = dev(votes_h, torch.int32)
+    flags = torch.zeros(nJ, dtype=torch.uint8, device="cuda")
+    nu_c = C.c_int64(0)
+    st = ctx.lib.usfft_detect_union(ctx.h, nJ, votes.data_ptr(), flags.data_ptr(), det_idx.data_ptr(), None,
+                                    union_idx.data_ptr(), C.byref(nu_c))
+    assert st != 0 and "n_union without n_det" in ctx.last_error()
