@@ -13,7 +13,6 @@ subprocess.run([build.NVCC, *build.FLAGS, "-DUSFFT_KEYS_TILED_ALWAYS=1", "-o", o
 _native.LIB_PATH = out
 import torch
 from paper_2109_04131_b200 import binding as B
-from oracle import lattice as olat
 
 ctx = B.Context(0)
 rng = np.random.default_rng(0)
@@ -25,11 +24,11 @@ for G, M, L, n1 in ((961, 401, 17, 65), (3969, 2017, 31, 129), (16129, 4001, 17,
         t = 3
         I_prev = np.unique(rng.integers(-64, 65, size=(4 * n_prev, t - 1)), axis=0)[:n_prev]
         kt = np.arange(-(n1 // 2), n1 - n1 // 2)
-        J = olat.candidates(I_prev, kt)
+        J = np.concatenate([np.repeat(I_prev, n1, axis=0), np.tile(kt, len(I_prev))[:, None]], axis=1)   # j = a n1 + c
         nJ = J.shape[0]
         z = rng.integers(1, M, size=(L, t))
         p = B.Plan(t, M, L, t, -1, z, np.zeros(t))
-        bd = torch.as_tensor(olat.bins(J, z, M), dtype=torch.int32, device="cuda").contiguous()
+        bd = torch.as_tensor((J @ z.T % M).T, dtype=torch.int32, device="cuda").contiguous()   # [L][|J|]
         k = torch.empty((G, nJ), dtype=torch.float64, device="cuda")
         m = torch.zeros(1, dtype=torch.float64, device="cuda")
         res = {}
